@@ -1,0 +1,153 @@
+/* octgpu — B200-native evaluation of direct-transcription OCP NLPs.
+ *
+ * C ABI of the drop-in for the reference's evaluation layer:
+ *   octrans::ipm::detail::EvalContext     /root/reference/proj/src/ipm/ipm_internal.hpp:40-95
+ *   octrans::ipm::detail::Reduction       /root/reference/proj/src/ipm/ipm_internal.hpp:102-111
+ *   octrans::ipm::detail::KktAssembler    /root/reference/proj/src/ipm/ipm_internal.hpp:119-146
+ * fed by a StructuredNlp built from the same model text
+ *   octrans::dsl::parse_ocp + octrans::transcribe::transcribe
+ *                                         /root/reference/proj/include/octrans/dsl/parser.hpp:33
+ *                                         /root/reference/proj/include/octrans/transcribe/transcribe.hpp:56-59
+ *
+ * Conventions: integer status returns (OCG_OK = 0,
+ * OCG_EVAL_DOMAIN = 1 when an evaluation met a non-finite value or a domain
+ * error — the reference's `false` — and negative codes for API/CUDA errors);
+ * no C++ exceptions cross the ABI; library-owned device buffers; an explicit
+ * CUDA stream argument (cudaStream_t passed as void*; NULL = legacy default
+ * stream). Evaluation calls are asynchronous: they enqueue kernels and set a
+ * device-side failure flag; ocg_eval_status() synchronises the stream and
+ * reports (and clears) the flag, which is how the blocking bool semantics of
+ * the reference are recovered. Index arrays are int64 like the reference's
+ * `Index`. There is no CPU fallback: without a usable sm_100 device every
+ * call that needs one returns OCG_ERR_CUDA.
+ */
+#ifndef OCTGPU_H_
+#define OCTGPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCG_OK 0
+#define OCG_EVAL_DOMAIN 1
+#define OCG_ERR_ARG (-1)
+#define OCG_ERR_CUDA (-2)
+#define OCG_ERR_PARSE (-3)
+#define OCG_ERR_JIT (-4)
+#define OCG_ERR_STATE (-5)
+
+typedef struct ocg_model ocg_model; /* StructuredNlp */
+typedef struct ocg_eval ocg_eval;   /* EvalContext on one device */
+typedef struct ocg_kkt ocg_kkt;     /* Reduction + KktAssembler */
+typedef void* ocg_stream;           /* cudaStream_t */
+
+/* Thread-local message for the last failed call. */
+const char* ocg_last_error(void);
+void ocg_free(void* p);
+const char* ocg_version(void);
+
+/* ---- model: parse + transcribe (reference transcribe.hpp:56-59) ---------- */
+/* scheme: 0 = euler, 1 = trapezoid (transcribe::Scheme) */
+int ocg_model_create(const char* source, int scheme, int64_t N, int boxes_as_bounds, ocg_model** out);
+void ocg_model_destroy(ocg_model* m);
+int64_t ocg_model_nvar(const ocg_model* m);
+int64_t ocg_model_mcon(const ocg_model* m);
+int64_t ocg_model_grid(const ocg_model* m);
+/* Host copies of StructuredNlp's lvar/uvar/x_start/clip_lo/clip_hi (nvar)
+ * and lcon/ucon (m_con); any pointer may be NULL. */
+int ocg_model_arrays(const ocg_model* m, double* lvar, double* uvar, double* x_start, double* clip_lo,
+                     double* clip_hi, double* lcon, double* ucon);
+/* Graphs, patterns, ranges, layout as JSON (caller frees with ocg_free). */
+char* ocg_model_structure_json(const ocg_model* m);
+/* Synthetic inputs with libstdc++'s mt19937 (reference recipes):
+ * acceptance_main.cpp:179-193 (x in the shrunk clip box, then lambda~U(-1,1))
+ * and ipm_test.cpp:398-403 (U(lo,hi) per slot). Host arrays. */
+int ocg_model_synth_acceptance(const ocg_model* m, uint32_t seed, double* x, double* lambda);
+int ocg_synth_uniform(uint32_t seed, double lo, double hi, int64_t n, double* out);
+
+/* ---- EvalContext (eval.cpp:40-286) ---------------------------------------- */
+typedef struct {
+  int device;       /* CUDA ordinal */
+  int fma;          /* 0: no FMA contraction (bit-compatible with the x86 reference); 1: allow */
+  int block;        /* threads per block, a multiple of 32; each warp owns 32-index tiles (0 = 128) */
+  int64_t idx_lo;   /* shard: first main grid index (0 with idx_hi = -1: whole grid) */
+  int64_t idx_hi;   /* shard: one past the last main grid index, -1 = all */
+  int specials;     /* evaluate the endpoint-pair instances on this shard (1 = yes) */
+} ocg_eval_options;
+
+void ocg_eval_default_options(ocg_eval_options* o);
+int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval** out);
+void ocg_eval_destroy(ocg_eval* e);
+
+/* jac_row/jac_col, hess_row/hess_col (row >= col), grad_col sizes */
+int ocg_eval_sizes(const ocg_eval* e, int64_t* jac_nnz, int64_t* hess_nnz, int64_t* grad_nnz);
+/* host copies of the global COO structure, bit-identical to EvalContext's */
+int ocg_eval_structure(const ocg_eval* e, int64_t* jac_row, int64_t* jac_col, int64_t* hess_row,
+                       int64_t* hess_col, int64_t* grad_col);
+
+#define OCG_BUF_JAC 0       /* jac_val  [jac_nnz]   */
+#define OCG_BUF_HESS 1      /* hess_val [hess_nnz]  */
+#define OCG_BUF_GRAD 2      /* grad_val [grad_nnz]  */
+#define OCG_BUF_ROWSCALE 3  /* row_scale [m_con]    */
+#define OCG_BUF_OBJV 4      /* per-instance objective values */
+/* library-owned device buffers */
+double* ocg_eval_buffer(ocg_eval* e, int which);
+/* Replace one of those buffers by caller-owned device memory of the same
+ * length (e.g. a framework tensor); the caller keeps it alive. */
+int ocg_eval_bind_buffer(ocg_eval* e, int which, double* dev_ptr);
+
+/* obj_scale and row_scale (host array of m_con, NULL = ones) */
+int ocg_eval_set_scaling(ocg_eval* e, double obj_scale, const double* row_scale);
+int ocg_eval_get_scaling(ocg_eval* e, double* obj_scale, double* row_scale);
+/* EvalContext::compute_scaling (eval.cpp:266-286) at device x0; synchronous */
+int ocg_eval_compute_scaling(ocg_eval* e, const double* x0, int enabled, ocg_stream s);
+
+/* Device pointers in, device pointers out; asynchronous. */
+int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s);
+int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_stream s);
+int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s); /* f: device scalar */
+int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stream s);
+int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_stream s);
+/* fused eval_constraints_jacobian + eval_hessian at one x (one forward pass) */
+int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double* c, ocg_stream s);
+int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s); /* out: device scalar */
+/* Synchronise s; OCG_OK if every evaluation since the last call was finite,
+ * else OCG_EVAL_DOMAIN. Clears the flag. */
+int ocg_eval_status(ocg_eval* e, ocg_stream s);
+/* number of kernels this context has launched (all entry points) */
+int64_t ocg_eval_launch_count(const ocg_eval* e);
+
+/* Diagnostics: the CUDA source generated for a model (ocg_free it; a final
+ * "// ocg-meta {...}" line gives gridDim.y, tail threads and shared memory per
+ * kernel and the parameter-block values), and an NVRTC compile of it for
+ * sm_100a without loading (works without a GPU).
+ */
+char* ocg_debug_generated_source(const ocg_model* m, int fma, int block);
+int ocg_debug_compile(const ocg_model* m, int fma, int block);
+
+/* ---- Reduction + KktAssembler (eval.cpp:290-440) -------------------------- */
+int ocg_kkt_create(const ocg_model* m, ocg_eval* e, ocg_kkt** out);
+void ocg_kkt_destroy(ocg_kkt* k);
+/* out[7] = n_free, n_slack, ntot, m, dim, nnz, contradictory */
+int ocg_kkt_dims(const ocg_kkt* k, int64_t* out);
+/* lower-CSC pattern of K (colp[dim+1], rowi[nnz]), bit-identical to KktAssembler::K */
+int ocg_kkt_pattern(const ocg_kkt* k, int64_t* colp, int64_t* rowi);
+/* prim_index/xlo/xhi [nvar]; slack_index/dual_index/row_slot [m_con] */
+int ocg_kkt_maps(const ocg_kkt* k, int64_t* prim_index, int64_t* slack_index, int64_t* dual_index,
+                 int64_t* row_slot, double* xlo, double* xhi);
+double* ocg_kkt_values(ocg_kkt* k); /* device K.val [nnz] */
+/* K.val from the eval context's current jac/hess buffers + sigma[ntot] (device) */
+int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s);
+/* y = K x with the symmetric mirror (sparse::matvec_sym, sparse.cpp:51-61) */
+int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s);
+/* out[ntot] = J^T lambda over kept rows, minus lambda on slacks
+ * (Solver::compute_jt_lambda, solver.cpp:244-257); lambda indexed by dual ordinal */
+int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OCTGPU_H_ */

@@ -1,0 +1,10 @@
+"""octgpu: B200-native (sm_100a) evaluation hot path of the arXiv 2510.03932
+reference (`octrans`): per-node fp64 objective / constraint / gradient /
+Jacobian / Lagrangian-Hessian evaluation into the reference's COO slots, the
+atomic-free KKT assembly and the interior-point vector kernels, behind the
+reference's EvalContext / KktAssembler interface (include/octgpu.h).
+"""
+from .evaluation import EvalContext, KktAssembler, Model, synth_uniform  # noqa: F401
+from .models import MODELS  # noqa: F401
+
+__all__ = ["EvalContext", "KktAssembler", "Model", "MODELS", "synth_uniform"]

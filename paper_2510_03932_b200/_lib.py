@@ -1,0 +1,113 @@
+"""ctypes binding of include/octgpu.h (libocgpu.so, built in-tree).
+
+The product path has no fallback: if the shared library is missing this
+module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libocgpu.so"
+
+OCG_OK = 0
+OCG_EVAL_DOMAIN = 1
+OCG_BUF_JAC, OCG_BUF_HESS, OCG_BUF_GRAD, OCG_BUF_ROWSCALE, OCG_BUF_OBJV = range(5)
+
+# every symbol include/octgpu.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "ocg_last_error", "ocg_free", "ocg_version",
+    "ocg_model_create", "ocg_model_destroy", "ocg_model_nvar", "ocg_model_mcon", "ocg_model_grid",
+    "ocg_model_arrays", "ocg_model_structure_json", "ocg_model_synth_acceptance", "ocg_synth_uniform",
+    "ocg_eval_default_options", "ocg_eval_create", "ocg_eval_destroy", "ocg_eval_sizes", "ocg_eval_structure",
+    "ocg_eval_buffer", "ocg_eval_bind_buffer", "ocg_eval_set_scaling", "ocg_eval_get_scaling", "ocg_eval_compute_scaling",
+    "ocg_eval_constraints", "ocg_eval_constraints_jacobian", "ocg_eval_objective", "ocg_eval_gradient",
+    "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_max_abs_hessian", "ocg_eval_status",
+    "ocg_eval_launch_count",
+    "ocg_debug_generated_source", "ocg_debug_compile",
+    "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
+    "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
+]
+
+
+class EvalOptions(C.Structure):
+    _fields_ = [("device", C.c_int), ("fma", C.c_int), ("block", C.c_int), ("idx_lo", C.c_int64),
+                ("idx_hi", C.c_int64), ("specials", C.c_int)]
+
+
+class OcgError(RuntimeError):
+    pass
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                          "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = C.CDLL(str(LIB_PATH))
+    vp, i64, i32, dp, ip = C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_int64)
+    sig = {
+        "ocg_last_error": (C.c_char_p, []),
+        "ocg_free": (None, [vp]),
+        "ocg_version": (C.c_char_p, []),
+        "ocg_model_create": (i32, [C.c_char_p, i32, i64, i32, C.POINTER(vp)]),
+        "ocg_model_destroy": (None, [vp]),
+        "ocg_model_nvar": (i64, [vp]),
+        "ocg_model_mcon": (i64, [vp]),
+        "ocg_model_grid": (i64, [vp]),
+        "ocg_model_arrays": (i32, [vp] + [dp] * 7),
+        "ocg_model_structure_json": (vp, [vp]),
+        "ocg_model_synth_acceptance": (i32, [vp, C.c_uint32, dp, dp]),
+        "ocg_synth_uniform": (i32, [C.c_uint32, C.c_double, C.c_double, i64, dp]),
+        "ocg_eval_default_options": (None, [C.POINTER(EvalOptions)]),
+        "ocg_eval_create": (i32, [vp, C.POINTER(EvalOptions), C.POINTER(vp)]),
+        "ocg_eval_destroy": (None, [vp]),
+        "ocg_eval_sizes": (i32, [vp, ip, ip, ip]),
+        "ocg_eval_structure": (i32, [vp] + [dp] * 5),
+        "ocg_eval_buffer": (vp, [vp, i32]),
+        "ocg_eval_bind_buffer": (i32, [vp, i32, dp]),
+        "ocg_eval_set_scaling": (i32, [vp, C.c_double, dp]),
+        "ocg_eval_get_scaling": (i32, [vp, C.POINTER(C.c_double), dp]),
+        "ocg_eval_compute_scaling": (i32, [vp, dp, i32, vp]),
+        "ocg_eval_constraints": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_constraints_jacobian": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_objective": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_gradient": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_hessian": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_jac_hess": (i32, [vp, dp, dp, dp, vp]),
+        "ocg_eval_max_abs_hessian": (i32, [vp, dp, vp]),
+        "ocg_eval_status": (i32, [vp, vp]),
+        "ocg_eval_launch_count": (i64, [vp]),
+        "ocg_debug_generated_source": (vp, [vp, i32, i32]),
+        "ocg_debug_compile": (i32, [vp, i32, i32]),
+        "ocg_kkt_create": (i32, [vp, vp, C.POINTER(vp)]),
+        "ocg_kkt_destroy": (None, [vp]),
+        "ocg_kkt_dims": (i32, [vp, dp]),
+        "ocg_kkt_pattern": (i32, [vp, dp, dp]),
+        "ocg_kkt_maps": (i32, [vp] + [dp] * 6),
+        "ocg_kkt_values": (vp, [vp]),
+        "ocg_kkt_assemble": (i32, [vp, dp, vp]),
+        "ocg_kkt_matvec": (i32, [vp, dp, dp, vp]),
+        "ocg_kkt_jt_lambda": (i32, [vp, dp, dp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = _load()
+
+
+def check(rc: int, what: str = "") -> int:
+    """Raise on negative (API/CUDA) codes; pass OCG_OK / OCG_EVAL_DOMAIN through."""
+    if rc < 0:
+        msg = LIB.ocg_last_error().decode(errors="replace")
+        raise OcgError(f"{what}: {msg} (code {rc})")
+    return rc
+
+
+def take_string(ptr: int) -> str:
+    s = C.cast(ptr, C.c_char_p).value.decode()
+    LIB.ocg_free(ptr)
+    return s

@@ -1,0 +1,923 @@
+// extern "C" boundary (include/octgpu.h): model, EvalContext and KKT objects.
+//
+// ocg_eval mirrors octrans::ipm::detail::EvalContext (ipm_internal.hpp:40-95):
+// identical COO structure, identical scaled outputs, bool results recovered
+// from a device-side failure flag. ocg_kkt mirrors Reduction + KktAssembler
+// (ipm_internal.hpp:102-146, eval.cpp:290-440): identical lower-CSC pattern,
+// assembly as a precomputed segmented gather (no atomics) that adds the
+// sources of every slot in the reference's order.
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/octgpu.h"
+#include "jit.hpp"
+#include "kernels.hpp"
+#include "model.hpp"
+#include "plan.hpp"
+
+using ocg::Index;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  bool owned = true;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p && owned) cudaFree(p);
+  }
+  // caller-owned device memory of the same size replaces the library buffer
+  void bind(T* ext) {
+    if (p && owned) cudaFree(p);
+    p = ext;
+    owned = false;
+  }
+  void alloc(size_t count) {
+    if (p && owned) cudaFree(p);
+    owned = true;
+    p = nullptr;
+    n = count;
+    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  }
+};
+
+cudaStream_t st(ocg_stream s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct ocg_model {
+  ocg::Problem prob;
+  ocg::Nlp nlp;
+};
+
+struct ocg_eval {
+  const ocg_model* model = nullptr;
+  int device = 0;
+  ocg::Layout lay;
+  ocg::JitModule mod;
+  cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,
+               k_grad = nullptr;
+  int block = 128;
+  bool specials = true;
+  std::map<std::string, int> slices, tail, smem;
+  std::vector<long long> prm;  // by-value parameter block of the generated kernels
+  std::map<std::string, int> resident;  // resident blocks per SM per kernel
+  int sm_count = 148;
+  Index i0 = 0, n_main = 0;
+
+  DBuf<double> jac, hess, grad, row_scale, objv, objw, partials, scratch;
+  DBuf<int> flag;
+  double obj_scale = 1.0;
+  std::vector<double> obj_weight;  // group weights (host)
+
+  // objective reduction plan
+  DBuf<int64_t> og_off, og_count, og_cbase;
+  Index n_chunks = 0;
+  DBuf<double> og_weight;
+
+  // dense gradient gather (slot -> grad COO entries)
+  DBuf<int64_t> gg_ptr;
+  DBuf<int32_t> gg_idx;
+
+  int64_t launches = 0;
+
+  // tail instances this shard runs for kernel `name`
+  Index n_spec(const char* name) const { return specials ? tail.at(name) : 0; }
+
+  // persistent grid: min(tiles, SMs x resident blocks per SM)
+  void launch(cudaKernel_t k, const char* name, void** args, cudaStream_t s) {
+    const Index ns = n_spec(name);
+    const Index tiles = (n_main + block - 1) / block;
+    if (tiles <= 0 && ns <= 0) return;
+    const Index cap = static_cast<Index>(sm_count) * std::max(1, resident.at(name));
+    const unsigned grid = static_cast<unsigned>(std::max<Index>(1, std::min(tiles, cap)));
+    ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(static_cast<unsigned>(block)), args,
+                        static_cast<size_t>(smem.at(name)), s),
+       "launch generated kernel");
+    ++launches;
+  }
+
+  void refresh_objw(cudaStream_t s) {
+    std::vector<double> w(obj_weight.size());
+    for (size_t g = 0; g < w.size(); ++g) w[g] = obj_scale * obj_weight[g];  // eval.cpp:206,246
+    if (!w.empty()) ck(cudaMemcpyAsync(objw.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, s), "objw");
+    ck(cudaStreamSynchronize(s), "sync");
+  }
+};
+
+struct ocg_kkt {
+  ocg_eval* ev = nullptr;
+  Index nvar = 0, m_con = 0;
+  Index n_free = 0, n_slack = 0, ntot = 0, m = 0, dim = 0, nnz = 0;
+  bool contradictory = false;
+  std::vector<Index> prim_index, free_slot, slack_index, slack_of, dual_index, dual_row, row_slot;
+  std::vector<double> xlo, xhi;
+  std::vector<Index> colp, rowi;
+  DBuf<double> val;
+  DBuf<int64_t> src_ptr, src_code;
+  Index H = 0, J = 0;
+  // matvec (full symmetric CSR in increasing column order)
+  DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
+  // J^T lambda
+  DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
+};
+
+namespace {
+
+// host COO structure, exactly as EvalContext's constructor materialises it
+// (eval.cpp:83-119)
+void host_structure(const ocg::Nlp& nlp, std::vector<Index>* jr, std::vector<Index>* jc, std::vector<Index>* hr,
+                    std::vector<Index>* hc, std::vector<Index>* gc) {
+  for (const auto& g : nlp.cons) {
+    const auto& ins = g.kernel.graph.inputs();
+    for (Index k = 0; k < g.range.count(); ++k) {
+      const Index idx = g.range.at(k);
+      if (jr)
+        for (const auto& [r, j] : g.pattern.jac) {
+          jr->push_back(g.row_base + k * g.out_dim() + r);
+          jc->push_back(ins[static_cast<size_t>(j)].slot(idx));
+        }
+      if (hr)
+        for (const auto& [a, b] : g.pattern.hess) {
+          const Index sa = ins[static_cast<size_t>(a)].slot(idx), sb = ins[static_cast<size_t>(b)].slot(idx);
+          hr->push_back(std::max(sa, sb));
+          hc->push_back(std::min(sa, sb));
+        }
+    }
+  }
+  for (const auto& g : nlp.objs) {
+    const auto& ins = g.kernel.graph.inputs();
+    for (Index k = 0; k < g.range.count(); ++k) {
+      const Index idx = g.range.at(k);
+      if (gc)
+        for (const auto& e : g.pattern.jac) gc->push_back(ins[static_cast<size_t>(e.second)].slot(idx));
+      if (hr)
+        for (const auto& [a, b] : g.pattern.hess) {
+          const Index sa = ins[static_cast<size_t>(a)].slot(idx), sb = ins[static_cast<size_t>(b)].slot(idx);
+          hr->push_back(std::max(sa, sb));
+          hc->push_back(std::min(sa, sb));
+        }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ocg_last_error(void) { return g_err.c_str(); }
+void ocg_free(void* p) { std::free(p); }
+const char* ocg_version(void) { return "octgpu 0.1 (sm_100a)"; }
+
+// ---- model --------------------------------------------------------------------
+
+int ocg_model_create(const char* source, int scheme, int64_t N, int boxes_as_bounds, ocg_model** out) {
+  if (!source || !out) return fail(OCG_ERR_ARG, "null argument");
+  try {
+    auto m = std::make_unique<ocg_model>();
+    m->prob = ocg::parse_problem(source);
+    m->nlp = ocg::transcribe(m->prob, scheme == 0 ? ocg::Scheme::euler : ocg::Scheme::trapezoid, N,
+                             boxes_as_bounds != 0);
+    *out = m.release();
+    return OCG_OK;
+  } catch (const ocg::ParseError& e) {
+    return fail(OCG_ERR_PARSE, e.what());
+  } catch (const std::exception& e) {
+    return fail(OCG_ERR_ARG, e.what());
+  }
+}
+
+void ocg_model_destroy(ocg_model* m) { delete m; }
+int64_t ocg_model_nvar(const ocg_model* m) { return m ? m->nlp.nvar : -1; }
+int64_t ocg_model_mcon(const ocg_model* m) { return m ? m->nlp.m_con : -1; }
+int64_t ocg_model_grid(const ocg_model* m) { return m ? m->nlp.N : -1; }
+
+int ocg_model_arrays(const ocg_model* m, double* lvar, double* uvar, double* x_start, double* clip_lo, double* clip_hi,
+                     double* lcon, double* ucon) {
+  if (!m) return fail(OCG_ERR_ARG, "null model");
+  auto cp = [](double* d, const std::vector<double>& v) {
+    if (d && !v.empty()) std::memcpy(d, v.data(), v.size() * sizeof(double));
+  };
+  const auto& n = m->nlp;
+  cp(lvar, n.lvar);
+  cp(uvar, n.uvar);
+  cp(x_start, n.x_start);
+  cp(clip_lo, n.clip_lo);
+  cp(clip_hi, n.clip_hi);
+  cp(lcon, n.lcon);
+  cp(ucon, n.ucon);
+  return OCG_OK;
+}
+
+char* ocg_model_structure_json(const ocg_model* m) {
+  if (!m) return nullptr;
+  const std::string s = m->nlp.structure_json();
+  char* out = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+
+int ocg_model_synth_acceptance(const ocg_model* m, uint32_t seed, double* x, double* lambda) {
+  if (!m || !x) return fail(OCG_ERR_ARG, "null argument");
+  const auto& n = m->nlp;
+  std::mt19937 rng(seed);
+  for (Index i = 0; i < n.nvar; ++i) {
+    double lo = n.clip_lo[static_cast<size_t>(i)], hi = n.clip_hi[static_cast<size_t>(i)];
+    if (!std::isfinite(lo) || !std::isfinite(hi)) {
+      lo = std::isfinite(lo) ? lo + 0.05 : 0.4;
+      hi = std::isfinite(hi) ? hi - 0.05 : 1.2;
+      if (lo >= hi) {
+        lo = 0.4;
+        hi = 1.2;
+      }
+    } else {
+      const double w = hi - lo;
+      lo += 0.05 * w;
+      hi -= 0.05 * w;
+    }
+    std::uniform_real_distribution<double> d(lo, hi);
+    x[i] = d(rng);
+  }
+  if (lambda) {
+    std::uniform_real_distribution<double> d(-1.0, 1.0);
+    for (Index r = 0; r < n.m_con; ++r) lambda[r] = d(rng);
+  }
+  return OCG_OK;
+}
+
+int ocg_synth_uniform(uint32_t seed, double lo, double hi, int64_t n, double* out) {
+  if (!out) return fail(OCG_ERR_ARG, "null argument");
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> d(lo, hi);
+  for (int64_t i = 0; i < n; ++i) out[i] = d(rng);
+  return OCG_OK;
+}
+
+// ---- eval ---------------------------------------------------------------------
+
+void ocg_eval_default_options(ocg_eval_options* o) {
+  o->device = 0;
+  o->fma = 0;
+  o->block = 128;
+  o->idx_lo = 0;
+  o->idx_hi = -1;
+  o->specials = 1;
+}
+
+int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval** out) {
+  if (!m || !out) return fail(OCG_ERR_ARG, "null argument");
+  ocg_eval_options o;
+  ocg_eval_default_options(&o);
+  if (opts) o = *opts;
+  try {
+    auto e = std::make_unique<ocg_eval>();
+    e->model = m;
+    e->device = o.device;
+    e->block = o.block > 0 ? o.block : 128;
+    ck(cudaSetDevice(o.device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
+    if (prop.major != 10) return fail(OCG_ERR_CUDA, "octgpu kernels target sm_100a; device is sm_" +
+                                                        std::to_string(prop.major) + std::to_string(prop.minor));
+    const ocg::Nlp& nlp = m->nlp;
+    e->lay = ocg::make_layout(nlp);
+    const Index lo = std::max(e->lay.idx_lo, o.idx_lo);
+    const Index hi = o.idx_hi < 0 ? e->lay.idx_hi : std::min(e->lay.idx_hi, o.idx_hi);
+    e->i0 = lo;
+    e->n_main = std::max<Index>(0, hi - lo);
+    e->specials = o.specials != 0;
+
+    ocg::GenOptions go;
+    go.fma = o.fma != 0;
+    go.block = e->block;
+    ocg::Generated gen = ocg::generate(nlp, e->lay, go);
+    // shared memory per block scales with warps per block: halve the block
+    // until every kernel fits the 227 KB per-block limit
+    auto max_smem = [](const ocg::Generated& g) {
+      int mx = 0;
+      for (const auto& kv : g.smem) mx = std::max(mx, kv.second);
+      return mx;
+    };
+    while (max_smem(gen) > prop.sharedMemPerBlockOptin && go.block > 32) {
+      go.block /= 2;
+      gen = ocg::generate(nlp, e->lay, go);
+    }
+    if (max_smem(gen) > static_cast<int>(prop.sharedMemPerBlockOptin))
+      return fail(OCG_ERR_JIT, "model needs more shared memory per warp than one block provides");
+    e->block = go.block;
+    e->slices = gen.slices;
+    e->tail = gen.tail;
+    e->smem = gen.smem;
+    e->prm = gen.params;
+    ocg::jit_compile(gen.source, go.fma, e->mod);
+    e->k_c = e->mod.kernel("ocg_c");
+    e->k_cjac = e->mod.kernel("ocg_cjac");
+    e->k_hess = e->mod.kernel("ocg_hess");
+    e->k_cjh = e->mod.kernel("ocg_cjh");
+    e->k_objv = e->mod.kernel("ocg_objv");
+    e->k_grad = e->mod.kernel("ocg_grad");
+    for (auto [k, name] : {std::pair{e->k_c, "ocg_c"}, {e->k_cjac, "ocg_cjac"}, {e->k_hess, "ocg_hess"},
+                           {e->k_cjh, "ocg_cjh"}, {e->k_objv, "ocg_objv"}, {e->k_grad, "ocg_grad"}}) {
+      const int bytes = e->smem.at(name);
+      if (bytes > 48 * 1024)
+        ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+           "dynamic shared memory attribute");
+      int nb = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(k), e->block, bytes),
+         "occupancy");
+      e->resident[name] = nb;
+    }
+    e->sm_count = prop.multiProcessorCount;
+
+    e->jac.alloc(static_cast<size_t>(e->lay.jac_nnz));
+    e->hess.alloc(static_cast<size_t>(e->lay.hess_nnz));
+    e->grad.alloc(static_cast<size_t>(e->lay.grad_nnz));
+    e->objv.alloc(static_cast<size_t>(e->lay.objv_n));
+    e->row_scale.upload(std::vector<double>(static_cast<size_t>(nlp.m_con), 1.0));
+    e->flag.upload(std::vector<int>{0});
+    e->scratch.alloc(4);
+    for (const auto& g : nlp.objs) e->obj_weight.push_back(g.weight);
+    e->objw.alloc(std::max<size_t>(1, nlp.objs.size()));
+    e->refresh_objw(nullptr);
+
+    // objective reduction plan: chunks of 512 per group
+    std::vector<int64_t> off, cnt, cbase{0};
+    for (size_t g = 0; g < nlp.objs.size(); ++g) {
+      off.push_back(e->lay.objv_off[g]);
+      cnt.push_back(nlp.objs[g].range.count());
+      cbase.push_back(cbase.back() + (cnt.back() + 511) / 512);
+    }
+    e->n_chunks = cbase.back();
+    e->og_off.upload(off);
+    e->og_count.upload(cnt);
+    e->og_cbase.upload(cbase);
+    e->og_weight.upload(e->obj_weight);
+    e->partials.alloc(static_cast<size_t>(std::max<Index>(1, e->n_chunks)));
+
+    // dense gradient: per slot, grad COO entries in increasing order
+    std::vector<Index> gc;
+    host_structure(nlp, nullptr, nullptr, nullptr, nullptr, &gc);
+    std::vector<int64_t> ptr(static_cast<size_t>(nlp.nvar) + 1, 0);
+    for (Index c : gc) ptr[static_cast<size_t>(c) + 1]++;
+    for (Index i = 0; i < nlp.nvar; ++i) ptr[static_cast<size_t>(i) + 1] += ptr[static_cast<size_t>(i)];
+    std::vector<int32_t> idx(gc.size());
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t q = 0; q < gc.size(); ++q) idx[static_cast<size_t>(fill[static_cast<size_t>(gc[q])]++)] = static_cast<int32_t>(q);
+    e->gg_ptr.upload(ptr);
+    e->gg_idx.upload(idx);
+    ck(cudaDeviceSynchronize(), "sync");
+    *out = e.release();
+    return OCG_OK;
+  } catch (const CudaError& ex) {
+    return fail(OCG_ERR_CUDA, ex.what());
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_JIT, ex.what());
+  }
+}
+
+void ocg_eval_destroy(ocg_eval* e) { delete e; }
+
+int ocg_eval_sizes(const ocg_eval* e, int64_t* jn, int64_t* hn, int64_t* gn) {
+  if (!e) return fail(OCG_ERR_ARG, "null eval");
+  if (jn) *jn = e->lay.jac_nnz;
+  if (hn) *hn = e->lay.hess_nnz;
+  if (gn) *gn = e->lay.grad_nnz;
+  return OCG_OK;
+}
+
+int ocg_eval_structure(const ocg_eval* e, int64_t* jr, int64_t* jc, int64_t* hr, int64_t* hc, int64_t* gc) {
+  if (!e) return fail(OCG_ERR_ARG, "null eval");
+  std::vector<Index> a, b, c, d, g;
+  host_structure(e->model->nlp, &a, &b, &c, &d, &g);
+  auto cp = [](int64_t* dst, const std::vector<Index>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(Index));
+  };
+  cp(jr, a);
+  cp(jc, b);
+  cp(hr, c);
+  cp(hc, d);
+  cp(gc, g);
+  return OCG_OK;
+}
+
+double* ocg_eval_buffer(ocg_eval* e, int which) {
+  if (!e) return nullptr;
+  switch (which) {
+    case OCG_BUF_JAC: return e->jac.p;
+    case OCG_BUF_HESS: return e->hess.p;
+    case OCG_BUF_GRAD: return e->grad.p;
+    case OCG_BUF_ROWSCALE: return e->row_scale.p;
+    case OCG_BUF_OBJV: return e->objv.p;
+  }
+  return nullptr;
+}
+
+int ocg_eval_bind_buffer(ocg_eval* e, int which, double* dev_ptr) {
+  if (!e || !dev_ptr) return fail(OCG_ERR_ARG, "null argument");
+  try {
+    switch (which) {
+      case OCG_BUF_JAC: e->jac.bind(dev_ptr); break;
+      case OCG_BUF_HESS: e->hess.bind(dev_ptr); break;
+      case OCG_BUF_GRAD: e->grad.bind(dev_ptr); break;
+      case OCG_BUF_ROWSCALE: {
+        const size_t m = static_cast<size_t>(e->model->nlp.m_con);
+        if (m) ck(cudaMemcpy(dev_ptr, e->row_scale.p, m * sizeof(double), cudaMemcpyDeviceToDevice), "rs copy");
+        e->row_scale.bind(dev_ptr);
+        break;
+      }
+      case OCG_BUF_OBJV: e->objv.bind(dev_ptr); break;
+      default: return fail(OCG_ERR_ARG, "unknown buffer");
+    }
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_CUDA, ex.what());
+  }
+}
+
+int ocg_eval_set_scaling(ocg_eval* e, double obj_scale, const double* row_scale) {
+  if (!e) return fail(OCG_ERR_ARG, "null eval");
+  try {
+    const size_t m = static_cast<size_t>(e->model->nlp.m_con);
+    std::vector<double> rs(m, 1.0);
+    if (row_scale) std::copy(row_scale, row_scale + m, rs.begin());
+    if (m) ck(cudaMemcpy(e->row_scale.p, rs.data(), m * sizeof(double), cudaMemcpyHostToDevice), "row_scale");
+    e->obj_scale = obj_scale;
+    e->refresh_objw(nullptr);
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_CUDA, ex.what());
+  }
+}
+
+int ocg_eval_get_scaling(ocg_eval* e, double* obj_scale, double* row_scale) {
+  if (!e) return fail(OCG_ERR_ARG, "null eval");
+  try {
+    if (obj_scale) *obj_scale = e->obj_scale;
+    const size_t m = static_cast<size_t>(e->model->nlp.m_con);
+    if (row_scale && m) ck(cudaMemcpy(row_scale, e->row_scale.p, m * sizeof(double), cudaMemcpyDeviceToHost), "rs");
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_CUDA, ex.what());
+  }
+}
+
+#define OCG_GUARD_BEGIN try {
+#define OCG_GUARD_END                          \
+  }                                            \
+  catch (const std::exception& ex) {           \
+    return fail(OCG_ERR_CUDA, ex.what());      \
+  }
+
+int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s) {
+  if (!e || !x || !c) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const double* rs = e->row_scale.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_c");
+  void* args[] = {e->prm.data(), &x, &rs, &c, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_c, "ocg_c", args, st(s));
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_stream s) {
+  if (!e || !x || !c) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const double* rs = e->row_scale.p;
+  double* jac = e->jac.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_cjac");
+  void* args[] = {e->prm.data(), &x, &rs, &c, &jac, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_cjac, "ocg_cjac", args, st(s));
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_stream s) {
+  if (!e || !x || !lambda) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const double* rs = e->row_scale.p;
+  const double* ow = e->objw.p;
+  double* hess = e->hess.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_hess");
+  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &hess, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_hess, "ocg_hess", args, st(s));
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double* c, ocg_stream s) {
+  if (!e || !x || !lambda || !c) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const double* rs = e->row_scale.p;
+  const double* ow = e->objw.p;
+  double* jac = e->jac.p;
+  double* hess = e->hess.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_cjh");
+  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &c, &jac, &hess, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_cjh, "ocg_cjh", args, st(s));
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
+  if (!e || !x || !f) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  double* ov = e->objv.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_objv");
+  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_objv, "ocg_objv", args, st(s));
+  ocg::dev::objective_reduce(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks, e->og_weight.p,
+                             static_cast<int>(e->obj_weight.size()), e->obj_scale, e->partials.p, f, e->flag.p, st(s));
+  e->launches += 2;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stream s) {
+  if (!e || !x || !grad_dense) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const double* ow = e->objw.p;
+  double* g = e->grad.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_grad");
+  void* args[] = {e->prm.data(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_grad, "ocg_grad", args, st(s));
+  ocg::dev::gather_sum(e->grad.p, e->gg_ptr.p, e->gg_idx.p, e->model->nlp.nvar, grad_dense, st(s));
+  e->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s) {
+  if (!e || !out) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::max_abs(e->hess.p, e->lay.hess_nnz, out, st(s));
+  e->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_status(ocg_eval* e, ocg_stream s) {
+  if (!e) return fail(OCG_ERR_ARG, "null eval");
+  OCG_GUARD_BEGIN
+  int h = 0;
+  ck(cudaMemcpyAsync(&h, e->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st(s)), "flag d2h");
+  ck(cudaStreamSynchronize(st(s)), "sync");
+  if (h) {
+    ck(cudaMemsetAsync(e->flag.p, 0, sizeof(int), st(s)), "flag reset");
+    ck(cudaStreamSynchronize(st(s)), "sync");
+    return OCG_EVAL_DOMAIN;
+  }
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int64_t ocg_eval_launch_count(const ocg_eval* e) { return e ? e->launches : -1; }
+
+// EvalContext::compute_scaling (eval.cpp:266-286): gradient and Jacobian at x0
+// with unit scales on the device, the max-abs rules on the host.
+int ocg_eval_compute_scaling(ocg_eval* e, const double* x0, int enabled, ocg_stream s) {
+  if (!e || !x0) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const auto& nlp = e->model->nlp;
+  const size_t m = static_cast<size_t>(nlp.m_con), nv = static_cast<size_t>(nlp.nvar);
+  int rc = ocg_eval_set_scaling(e, 1.0, nullptr);
+  if (rc != OCG_OK || !enabled) return rc;
+  DBuf<double> gd, cd;
+  gd.alloc(nv);
+  cd.alloc(m);
+  ocg_eval_gradient(e, x0, gd.p, s);
+  if (ocg_eval_status(e, s) != OCG_OK) return OCG_OK;  // keep unit scales
+  ocg_eval_constraints_jacobian(e, x0, cd.p, s);
+  if (ocg_eval_status(e, s) != OCG_OK) return OCG_OK;
+  std::vector<double> g(nv), jv(static_cast<size_t>(e->lay.jac_nnz));
+  ck(cudaMemcpy(g.data(), gd.p, nv * sizeof(double), cudaMemcpyDeviceToHost), "grad d2h");
+  if (!jv.empty()) ck(cudaMemcpy(jv.data(), e->jac.p, jv.size() * sizeof(double), cudaMemcpyDeviceToHost), "jac d2h");
+  double gmax = 0.0;
+  for (double v : g) gmax = std::max(gmax, std::abs(v));
+  double os = 1.0;
+  if (gmax > 0.0) os = std::min(1.0, 100.0 / gmax);
+  std::vector<Index> jr, jc;
+  host_structure(nlp, &jr, &jc, nullptr, nullptr, nullptr);
+  std::vector<double> jmax(m, 0.0), rs(m, 1.0);
+  for (size_t q = 0; q < jv.size(); ++q) {
+    const auto r = static_cast<size_t>(jr[q]);
+    jmax[r] = std::max(jmax[r], std::abs(jv[q]));
+  }
+  for (size_t r = 0; r < m; ++r) rs[r] = jmax[r] > 0.0 ? std::min(1.0, 100.0 / jmax[r]) : 1.0;
+  return ocg_eval_set_scaling(e, os, rs.data());
+  OCG_GUARD_END
+}
+
+// ---- KKT ----------------------------------------------------------------------
+
+int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
+  if (!mdl || !e || !out) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const ocg::Nlp& nlp = mdl->nlp;
+  auto K = std::make_unique<ocg_kkt>();
+  K->ev = e;
+  K->nvar = nlp.nvar;
+  K->m_con = nlp.m_con;
+  const auto nv = static_cast<size_t>(nlp.nvar), mc = static_cast<size_t>(nlp.m_con);
+
+  // Reduction (eval.cpp:290-316): fold rows whose root is a bare input
+  K->xlo = nlp.lvar;
+  K->xhi = nlp.uvar;
+  K->row_slot.assign(mc, -1);
+  for (const auto& g : nlp.cons) {
+    const auto& gr = g.kernel.graph;
+    for (int r = 0; r < g.out_dim(); ++r) {
+      const ocg::Node& root = gr.at(g.kernel.roots[static_cast<size_t>(r)]);
+      if (root.op != ocg::Op::input) continue;
+      const ocg::Addr a = gr.inputs()[static_cast<size_t>(root.a)];
+      for (Index k = 0; k < g.range.count(); ++k) {
+        const auto row = static_cast<size_t>(g.row_base + k * g.out_dim() + r);
+        const auto slot = static_cast<size_t>(a.slot(g.range.at(k)));
+        K->row_slot[row] = static_cast<Index>(slot);
+        K->xlo[slot] = std::max(K->xlo[slot], nlp.lcon[row]);
+        K->xhi[slot] = std::min(K->xhi[slot], nlp.ucon[row]);
+        if (K->xlo[slot] > K->xhi[slot]) K->contradictory = true;
+      }
+    }
+  }
+  K->dual_index.assign(mc, -1);
+  for (size_t r = 0; r < mc; ++r) {
+    if (K->row_slot[r] >= 0) continue;
+    K->dual_index[r] = K->m++;
+    K->dual_row.push_back(static_cast<Index>(r));
+  }
+  // KktAssembler (eval.cpp:318-403)
+  K->prim_index.assign(nv, -1);
+  for (size_t s = 0; s < nv; ++s) {
+    if (K->xlo[s] == K->xhi[s]) continue;
+    K->prim_index[s] = K->n_free++;
+    K->free_slot.push_back(static_cast<Index>(s));
+  }
+  K->slack_index.assign(mc, -1);
+  for (size_t r = 0; r < mc; ++r) {
+    if (K->dual_index[r] < 0 || nlp.lcon[r] == nlp.ucon[r]) continue;
+    K->slack_index[r] = K->n_slack++;
+    K->slack_of.push_back(static_cast<Index>(r));
+  }
+  K->ntot = K->n_free + K->n_slack;
+  K->dim = K->ntot + K->m;
+
+  std::vector<Index> jr, jc, hr, hc;
+  host_structure(nlp, &jr, &jc, &hr, &hc, nullptr);
+  K->H = static_cast<Index>(hr.size());
+  K->J = static_cast<Index>(jr.size());
+  // structural entries as (key=(col,row), source code); code order == the
+  // reference's accumulation order
+  struct Src {
+    Index col, row, code;
+  };
+  std::vector<Src> srcs;
+  srcs.reserve(hr.size() + jr.size() + static_cast<size_t>(K->ntot + K->m));
+  for (size_t q = 0; q < hr.size(); ++q) {
+    const Index pi = K->prim_index[static_cast<size_t>(hr[q])], pj = K->prim_index[static_cast<size_t>(hc[q])];
+    if (pi < 0 || pj < 0) continue;
+    srcs.push_back({std::min(pi, pj), std::max(pi, pj), static_cast<Index>(q)});
+  }
+  for (size_t q = 0; q < jr.size(); ++q) {
+    const Index d = K->dual_index[static_cast<size_t>(jr[q])];
+    if (d < 0) continue;
+    const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
+    if (pj < 0) continue;
+    srcs.push_back({pj, K->ntot + d, K->H + static_cast<Index>(q)});
+  }
+  const Index S = K->n_slack;
+  for (Index k = 0; k < S; ++k) {
+    const Index d = K->dual_index[static_cast<size_t>(K->slack_of[static_cast<size_t>(k)])];
+    srcs.push_back({K->n_free + k, K->ntot + d, K->H + K->J + k});
+  }
+  for (Index i = 0; i < K->ntot; ++i) srcs.push_back({i, i, K->H + K->J + S + i});
+  for (Index r = 0; r < K->m; ++r) srcs.push_back({K->ntot + r, K->ntot + r, -1});  // dual diagonal: no source
+  std::sort(srcs.begin(), srcs.end(), [](const Src& a, const Src& b) {
+    if (a.col != b.col) return a.col < b.col;
+    if (a.row != b.row) return a.row < b.row;
+    return a.code < b.code;
+  });
+  K->colp.assign(static_cast<size_t>(K->dim) + 1, 0);
+  std::vector<int64_t> sptr{0}, scode;
+  for (size_t q = 0; q < srcs.size(); ++q) {
+    const bool fresh = q == 0 || srcs[q].col != srcs[q - 1].col || srcs[q].row != srcs[q - 1].row;
+    if (fresh) {
+      if (q) sptr.push_back(static_cast<int64_t>(scode.size()));
+      K->rowi.push_back(srcs[q].row);
+      K->colp[static_cast<size_t>(srcs[q].col) + 1]++;
+    }
+    if (srcs[q].code >= 0) scode.push_back(srcs[q].code);
+  }
+  sptr.push_back(static_cast<int64_t>(scode.size()));
+  for (Index j = 0; j < K->dim; ++j) K->colp[static_cast<size_t>(j) + 1] += K->colp[static_cast<size_t>(j)];
+  K->nnz = static_cast<Index>(K->rowi.size());
+  K->src_ptr.upload(sptr);
+  K->src_code.upload(scode);
+  K->val.alloc(static_cast<size_t>(K->nnz));
+  ck(cudaMemset(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double)), "memset");
+
+  // full symmetric CSR for matvec, rows in increasing column order
+  {
+    const auto n = static_cast<size_t>(K->dim);
+    std::vector<int64_t> cnt(n + 1, 0);
+    for (size_t j = 0; j < n; ++j)
+      for (Index p = K->colp[j]; p < K->colp[j + 1]; ++p) {
+        const auto i = static_cast<size_t>(K->rowi[static_cast<size_t>(p)]);
+        cnt[i + 1]++;
+        if (i != j) cnt[j + 1]++;
+      }
+    for (size_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int64_t> col(static_cast<size_t>(cnt[n])), vidx(static_cast<size_t>(cnt[n]));
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (size_t j = 0; j < n; ++j)
+      for (Index p = K->colp[j]; p < K->colp[j + 1]; ++p) {
+        const auto i = static_cast<size_t>(K->rowi[static_cast<size_t>(p)]);
+        col[static_cast<size_t>(fill[i])] = static_cast<int64_t>(j);
+        vidx[static_cast<size_t>(fill[i]++)] = p;
+        if (i != j) {
+          col[static_cast<size_t>(fill[j])] = static_cast<int64_t>(i);
+          vidx[static_cast<size_t>(fill[j]++)] = p;
+        }
+      }
+    K->mv_ptr.upload(cnt);
+    K->mv_col.upload(col);
+    K->mv_vidx.upload(vidx);
+  }
+  // J^T lambda gather: per primal column, jac entries in increasing order
+  {
+    const auto nf = static_cast<size_t>(K->n_free);
+    const auto nt = static_cast<size_t>(K->ntot);
+    std::vector<int64_t> ptr(nt + 1, 0);
+    for (size_t q = 0; q < jr.size(); ++q) {
+      const Index d = K->dual_index[static_cast<size_t>(jr[q])];
+      const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
+      if (d < 0 || pj < 0) continue;
+      ptr[static_cast<size_t>(pj) + 1]++;
+    }
+    for (size_t i = 0; i < nt; ++i) ptr[i + 1] += ptr[i];
+    std::vector<int64_t> ei(static_cast<size_t>(ptr[nt])), di(static_cast<size_t>(ptr[nt]));
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t q = 0; q < jr.size(); ++q) {
+      const Index d = K->dual_index[static_cast<size_t>(jr[q])];
+      const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
+      if (d < 0 || pj < 0) continue;
+      ei[static_cast<size_t>(fill[static_cast<size_t>(pj)])] = static_cast<int64_t>(q);
+      di[static_cast<size_t>(fill[static_cast<size_t>(pj)]++)] = d;
+    }
+    std::vector<int64_t> sd(static_cast<size_t>(K->n_slack));
+    for (Index k = 0; k < K->n_slack; ++k)
+      sd[static_cast<size_t>(k)] = K->dual_index[static_cast<size_t>(K->slack_of[static_cast<size_t>(k)])];
+    (void)nf;
+    K->jt_ptr.upload(ptr);
+    K->jt_e.upload(ei);
+    K->jt_dual.upload(di);
+    K->jt_slack_dual.upload(sd);
+  }
+  *out = K.release();
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+void ocg_kkt_destroy(ocg_kkt* k) { delete k; }
+
+int ocg_kkt_dims(const ocg_kkt* k, int64_t* out) {
+  if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
+  out[0] = k->n_free;
+  out[1] = k->n_slack;
+  out[2] = k->ntot;
+  out[3] = k->m;
+  out[4] = k->dim;
+  out[5] = k->nnz;
+  out[6] = k->contradictory ? 1 : 0;
+  return OCG_OK;
+}
+
+int ocg_kkt_pattern(const ocg_kkt* k, int64_t* colp, int64_t* rowi) {
+  if (!k) return fail(OCG_ERR_ARG, "null kkt");
+  if (colp) std::memcpy(colp, k->colp.data(), k->colp.size() * sizeof(Index));
+  if (rowi && !k->rowi.empty()) std::memcpy(rowi, k->rowi.data(), k->rowi.size() * sizeof(Index));
+  return OCG_OK;
+}
+
+int ocg_kkt_maps(const ocg_kkt* k, int64_t* prim_index, int64_t* slack_index, int64_t* dual_index, int64_t* row_slot,
+                 double* xlo, double* xhi) {
+  if (!k) return fail(OCG_ERR_ARG, "null kkt");
+  auto cpi = [](int64_t* d, const std::vector<Index>& v) {
+    if (d && !v.empty()) std::memcpy(d, v.data(), v.size() * sizeof(Index));
+  };
+  auto cpd = [](double* d, const std::vector<double>& v) {
+    if (d && !v.empty()) std::memcpy(d, v.data(), v.size() * sizeof(double));
+  };
+  cpi(prim_index, k->prim_index);
+  cpi(slack_index, k->slack_index);
+  cpi(dual_index, k->dual_index);
+  cpi(row_slot, k->row_slot);
+  cpd(xlo, k->xlo);
+  cpd(xhi, k->xhi);
+  return OCG_OK;
+}
+
+double* ocg_kkt_values(ocg_kkt* k) { return k ? k->val.p : nullptr; }
+
+int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
+  if (!k || !sigma) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
+                         k->n_slack, k->val.p, st(s));
+  k->ev->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
+  if (!k || !x || !y) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y, st(s));
+  k->ev->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s) {
+  if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
+                      k->n_slack, out, st(s));
+  k->ev->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+}  // extern "C"
+
+extern "C" char* ocg_debug_generated_source(const ocg_model* m, int fma, int block) {
+  if (!m) return nullptr;
+  ocg::GenOptions go;
+  go.fma = fma != 0;
+  go.block = block > 0 ? block : 128;
+  const ocg::Generated gen = ocg::generate(m->nlp, ocg::make_layout(m->nlp), go);
+  std::string s = gen.source + "// ocg-meta {";
+  bool first = true;
+  for (const auto& [name, y] : gen.slices) {
+    s += std::string(first ? "" : ", ") + "\"" + name + "\": [" + std::to_string(y) + ", " +
+         std::to_string(gen.tail.at(name)) + ", " + std::to_string(gen.smem.at(name)) + "]";
+    first = false;
+  }
+  s += ", \"params\": [";
+  for (size_t i = 0; i < gen.params.size(); ++i) s += (i ? ", " : "") + std::to_string(gen.params[i]);
+  s += "]}\n";
+  char* out = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+
+extern "C" int ocg_debug_compile(const ocg_model* m, int fma, int block) {
+  if (!m) return fail(OCG_ERR_ARG, "null model");
+  try {
+    ocg::GenOptions go;
+    go.fma = fma != 0;
+    go.block = block > 0 ? block : 128;
+    std::string cubin;
+    ocg::jit_compile_only(ocg::generate_source(m->nlp, ocg::make_layout(m->nlp), go), go.fma, cubin);
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_JIT, ex.what());
+  }
+}

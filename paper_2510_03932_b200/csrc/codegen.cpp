@@ -1,0 +1,936 @@
+// Graph -> straight-line fp64 CUDA for the per-node evaluation kernels.
+//
+// The generated code performs, operation for operation, what the reference's
+// tape interpreter does (/root/reference/proj/src/kernel/evaluator.cpp):
+//   forward values + local partials            evaluator.cpp:47-87
+//   one reverse sweep per Jacobian row          evaluator.cpp:96-130
+//   forward dual + reverse adjoint/adjoint-dual
+//     sweep per Hessian direction j             evaluator.cpp:145-233
+// but at code-generation time, so the interpreter, the zero-adjoint skips and
+// every structurally-zero seed disappear. Only folds that are exact in IEEE
+// arithmetic are applied (x*1, x*(-1), x+0, 0*x for finite x, constant
+// arithmetic done in the same double precision on the host), so with FMA
+// contraction off the device performs the same roundings in the same order as
+// the x86 reference; only the libm/libdevice transcendentals differ (<=2 ulp).
+//
+// Thread mapping: blockIdx.x % slices selects a grid-indexed group, one thread per grid
+// index of it, with shared-memory staging of the node slabs and of the COO
+// outputs (see Generator::kernel). Endpoint-pair and single-index instances
+// run on a short tail of threads. All grid-size-dependent integers are kernel
+// parameters, so one compiled module serves every N of a model.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+#include <functional>
+#include <sstream>
+
+#include "plan.hpp"
+
+namespace ocg {
+
+Layout make_layout(const Nlp& nlp) {
+  Layout L;
+  Index jac = 0, hess = 0, grad = 0, objv = 0;
+  bool any_main = false;
+  Index lo = 0, hi = 0;
+  auto cover = [&](const Range& r) {
+    if (r.endpoints) return;
+    if (!any_main) {
+      lo = r.lo;
+      hi = r.hi;
+      any_main = true;
+    } else {
+      lo = std::min(lo, r.lo);
+      hi = std::max(hi, r.hi);
+    }
+  };
+  for (size_t g = 0; g < nlp.cons.size(); ++g) {
+    const Group& grp = nlp.cons[g];
+    L.jac_off.push_back(jac);
+    L.hess_off_con.push_back(hess);
+    jac += static_cast<Index>(grp.pattern.jac.size()) * grp.range.count();
+    hess += static_cast<Index>(grp.pattern.hess.size()) * grp.range.count();
+    cover(grp.range);
+    if (grp.range.endpoints)
+      for (Index k = 0; k < grp.range.count(); ++k) L.specials.push_back({false, static_cast<int>(g), k});
+  }
+  for (size_t g = 0; g < nlp.objs.size(); ++g) {
+    const Group& grp = nlp.objs[g];
+    L.grad_off.push_back(grad);
+    L.hess_off_obj.push_back(hess);
+    L.objv_off.push_back(objv);
+    grad += static_cast<Index>(grp.pattern.jac.size()) * grp.range.count();
+    hess += static_cast<Index>(grp.pattern.hess.size()) * grp.range.count();
+    objv += grp.range.count();
+    cover(grp.range);
+    if (grp.range.endpoints)
+      for (Index k = 0; k < grp.range.count(); ++k) L.specials.push_back({true, static_cast<int>(g), k});
+  }
+  L.jac_nnz = jac;
+  L.hess_nnz = hess;
+  L.grad_nnz = grad;
+  L.objv_n = objv;
+  L.idx_lo = lo;
+  L.idx_hi = hi;
+  return L;
+}
+
+namespace {
+
+struct V {
+  bool is_c = true;
+  double c = 0.0;
+  int id = -1;
+  bool zero() const { return is_c && c == 0.0; }
+  bool one() const { return is_c && c == 1.0; }
+  bool minus_one() const { return is_c && c == -1.0; }
+};
+V K(double c) { return V{true, c, -1}; }
+
+std::string lit(double c) {
+  if (std::isnan(c)) return "__longlong_as_double(0x7ff8000000000000LL)";
+  if (std::isinf(c)) return c > 0 ? "__longlong_as_double(0x7ff0000000000000LL)"
+                                   : "__longlong_as_double(0xfff0000000000000LL)";
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%a", c);
+  return std::string("(") + buf + ")";
+}
+
+class Emitter {
+ public:
+  std::string out;
+  int depth = 1;
+
+  Emitter() { scopes_.emplace_back(); }
+
+  void line(const std::string& s) {
+    out.append(static_cast<size_t>(depth) * 2, ' ');
+    out += s;
+    out += '\n';
+  }
+  void open(const std::string& head) {
+    line(head + " {");
+    ++depth;
+    scopes_.emplace_back();
+  }
+  void close(const std::string& tail = "") {
+    --depth;
+    line("}" + tail);
+    scopes_.pop_back();
+  }
+
+  std::string s(V v) const { return v.is_c ? lit(v.c) : "t" + std::to_string(v.id); }
+
+  // SSA temp for an expression, reused if the same key is visible in scope
+  V emit(const std::string& key, const std::string& expr) {
+    for (auto it = scopes_.rbegin(); it != scopes_.rend(); ++it) {
+      auto f = it->find(key);
+      if (f != it->end()) return f->second;
+    }
+    V v{false, 0.0, next_++};
+    line("const double t" + std::to_string(v.id) + " = " + expr + ";");
+    scopes_.back().emplace(key, v);
+    return v;
+  }
+  // named temp without CSE (e.g. sincos outputs)
+  V fresh() { return V{false, 0.0, next_++}; }
+  void bind(const std::string& key, V v) { scopes_.back().emplace(key, v); }
+  bool lookup(const std::string& key, V& v) const {
+    for (auto it = scopes_.rbegin(); it != scopes_.rend(); ++it) {
+      auto f = it->find(key);
+      if (f != it->end()) {
+        v = f->second;
+        return true;
+      }
+    }
+    return false;
+  }
+
+  V add(V a, V b) {
+    if (a.zero()) return b;
+    if (b.zero()) return a;
+    if (a.is_c && b.is_c) return K(a.c + b.c);
+    return emit("+" + s(a) + "," + s(b), s(a) + " + " + s(b));
+  }
+  V sub(V a, V b) {
+    if (b.zero()) return a;
+    if (a.zero()) return neg(b);
+    if (a.is_c && b.is_c) return K(a.c - b.c);
+    return emit("-" + s(a) + "," + s(b), s(a) + " - " + s(b));
+  }
+  V mul(V a, V b) {
+    if (a.zero() || b.zero()) return K(0.0);
+    if (a.one()) return b;
+    if (b.one()) return a;
+    if (a.minus_one()) return neg(b);
+    if (b.minus_one()) return neg(a);
+    if (a.is_c && b.is_c) return K(a.c * b.c);
+    return emit("*" + s(a) + "," + s(b), s(a) + " * " + s(b));
+  }
+  V div(V a, V b) {
+    if (b.one()) return a;
+    if (a.is_c && b.is_c) return K(a.c / b.c);
+    return emit("/" + s(a) + "," + s(b), s(a) + " / " + s(b));
+  }
+  V neg(V a) {
+    if (a.is_c) return K(-a.c);
+    return emit("n" + s(a), "-" + s(a));
+  }
+  V call(const char* fn, V a) {
+    if (a.is_c) {  // only reachable for literal arguments; fold with host libm
+      const std::string f(fn);
+      if (f == "exp") return K(std::exp(a.c));
+      if (f == "log") return K(std::log(a.c));
+      if (f == "sqrt") return K(std::sqrt(a.c));
+      if (f == "tan") return K(std::tan(a.c));
+      if (f == "sin") return K(std::sin(a.c));
+      if (f == "cos") return K(std::cos(a.c));
+    }
+    return emit(std::string(fn) + s(a), std::string(fn) + "(" + s(a) + ")");
+  }
+  // sin and cos of the same argument from one sincos call
+  V trig(bool want_sin, V a) {
+    if (a.is_c) return K(want_sin ? std::sin(a.c) : std::cos(a.c));
+    V sv, cv;
+    const std::string ks = "sin" + s(a), kc = "cos" + s(a);
+    if (lookup(want_sin ? ks : kc, sv)) return sv;
+    sv = fresh();
+    cv = fresh();
+    line("double " + s(sv) + ", " + s(cv) + ";");
+    line("sincos(" + s(a) + ", &" + s(sv) + ", &" + s(cv) + ");");
+    bind(ks, sv);
+    bind(kc, cv);
+    return want_sin ? sv : cv;
+  }
+  // pow with a constant exponent; exponents where glibc's pow is provably
+  // identical to direct arithmetic are strength-reduced
+  V powc(V a, double c) {
+    if (c == 0.0) return K(1.0);
+    if (c == 1.0) return a;
+    if (a.is_c) return K(std::pow(a.c, c));
+    // correctly rounded forms of pow for these exponents (device helpers in
+    // the module prelude; the host checker maps them back to libm pow)
+    if (c == 2.0) return call("ocg_pow2", a);
+    if (c == -1.0) return call("ocg_powm1", a);
+    if (c == 0.5) return call("ocg_pow05", a);
+    return emit("pow" + s(a) + "," + lit(c), "pow(" + s(a) + ", " + lit(c) + ")");
+  }
+
+ private:
+  int next_ = 0;
+  std::vector<std::map<std::string, V>> scopes_;
+};
+
+enum class Mode { c, cjac, hess, cjh, objv, grad };
+
+bool mode_values_only(Mode m) { return m == Mode::c || m == Mode::objv; }
+
+// Per-node forward results of one group instance.
+struct Fwd {
+  std::vector<V> v, p1, p2;
+};
+
+struct Check {
+  std::vector<int> owners;  // group ordinals (cons: g, objs: 1000+g) that need the value finite
+  V v;
+};
+
+class Generator {
+ public:
+  Generator(const Nlp& nlp, const Layout& lay, const GenOptions& opt) : nlp_(nlp), lay_(lay), opt_(opt) {}
+
+  Generated module() {
+    Generated out;
+    struct KSpec {
+      Mode m;
+      const char* name;
+      const char* params;
+    };
+    const KSpec ks[] = {
+        {Mode::c, "ocg_c",
+         "const double* __restrict__ x, const double* __restrict__ rs, double* __restrict__ cout, "
+         "int* __restrict__ flag"},
+        {Mode::cjac, "ocg_cjac",
+         "const double* __restrict__ x, const double* __restrict__ rs, double* __restrict__ cout, "
+         "double* __restrict__ jac, int* __restrict__ flag"},
+        {Mode::hess, "ocg_hess",
+         "const double* __restrict__ x, const double* __restrict__ lam, const double* __restrict__ rs, "
+         "const double* __restrict__ objw, double* __restrict__ hess, int* __restrict__ flag"},
+        {Mode::cjh, "ocg_cjh",
+         "const double* __restrict__ x, const double* __restrict__ lam, const double* __restrict__ rs, "
+         "const double* __restrict__ objw, double* __restrict__ cout, double* __restrict__ jac, "
+         "double* __restrict__ hess, int* __restrict__ flag"},
+        {Mode::objv, "ocg_objv", "const double* __restrict__ x, double* __restrict__ objv, int* __restrict__ flag"},
+        {Mode::grad, "ocg_grad",
+         "const double* __restrict__ x, const double* __restrict__ objw, double* __restrict__ gout, "
+         "int* __restrict__ flag"},
+    };
+    std::string kernels;
+    for (const KSpec& k : ks) {
+      int slices = 1, tail = 0;
+      smem_out_ = 0;
+      kernels += kernel(k.m, k.name, k.params, slices, tail);
+      out.slices[k.name] = slices;
+      out.tail[k.name] = tail;
+      out.smem[k.name] = static_cast<int>(smem_out_);
+    }
+    std::ostringstream os;
+    os << "// generated by ocgpu codegen: do not edit\n";
+    os << "#define OCG_BLOCK " << opt_.block << "\n";
+    os << "// grid-size-dependent integers (offsets, ranges, slab bases) arrive by value:\n";
+    for (size_t i = 0; i < pkeys_.size(); ++i) os << "//   prm.v[" << i << "] = " << pkeys_[i] << "\n";
+    os << "struct OcgParams { long long v[" << std::max<size_t>(1, pkeys_.size()) << "]; };\n";
+    os << "__device__ __forceinline__ bool fin(double v) { return fabs(v) <= 1.7976931348623157e308; }\n";
+    os << "#ifndef OCG_HOST_POW\n";
+    os << "__device__ __forceinline__ double ocg_pow2(double a) { return a * a; }\n";
+    os << "__device__ __forceinline__ double ocg_powm1(double a) { return 1.0 / a; }\n";
+    os << "__device__ __forceinline__ double ocg_pow05(double a) { return sqrt(a); }\n";
+    os << "#endif\n\n";
+    os << kernels;
+    out.source = os.str();
+    out.params.assign(pvals_.begin(), pvals_.end());
+    if (out.params.empty()) out.params.push_back(0);
+    return out;
+  }
+
+ private:
+  const Nlp& nlp_;
+  const Layout& lay_;
+  const GenOptions& opt_;
+  // staging hooks: shared-memory source of a strided input, and shared-memory
+  // target of an output (kind 0 c, 1 jac, 2 grad, 3 objv, 4 hess; e = row /
+  // entry); empty string = global memory
+  std::function<std::string(const Addr&)> load_from_;
+  std::function<std::string(int, Index)> store_to_;
+  Index smem_out_ = 0;  // dynamic shared memory (bytes) of the last kernel
+
+  // Grid-size-dependent integers live in a by-value parameter block keyed by
+  // their meaning, so the generated source — and its cached cubin — depends
+  // only on the model structure, not on N.
+  std::vector<std::string> pkeys_;
+  std::vector<Index> pvals_;
+  std::map<std::string, size_t> pidx_;
+  std::string P(const std::string& key, Index v) {
+    auto it = pidx_.find(key);
+    if (it == pidx_.end()) {
+      it = pidx_.emplace(key, pkeys_.size()).first;
+      pkeys_.push_back(key);
+      pvals_.push_back(v);
+    }
+    return "prm.v[" + std::to_string(it->second) + "]";
+  }
+  std::string G(bool objective, int gi, const char* what, Index v) {
+    return P(std::string(objective ? "obj" : "con") + std::to_string(gi) + "." + what, v);
+  }
+
+  // which parts of a group a mode evaluates
+  struct Parts {
+    bool values = false, jac = false, hess = false, partials = false, grad = false, objv = false;
+    bool any() const { return values || jac || hess || grad || objv; }
+  };
+  Parts parts(Mode m, bool objective, const Group& g) const {
+    Parts p;
+    const bool has_h = !g.pattern.hess.empty();
+    if (!objective) {
+      p.values = m == Mode::c || m == Mode::cjac || m == Mode::cjh;
+      p.jac = m == Mode::cjac || m == Mode::cjh;
+      p.hess = (m == Mode::hess || m == Mode::cjh) && has_h;
+    } else {
+      p.hess = (m == Mode::hess || m == Mode::cjh) && has_h;
+      p.grad = m == Mode::grad;
+      p.objv = m == Mode::objv;
+    }
+    p.partials = p.jac || p.hess || p.grad;
+    return p;
+  }
+
+  // Forward values whose finiteness must be tested explicitly. The reference
+  // tests every node value (evaluator.cpp:79). A non-finite v always makes a
+  // consumer u non-finite when v enters u through +, -, *, the numerator of /,
+  // neg, sin, cos, tan, log, sqrt or pow with a positive exponent; so v needs
+  // no test of its own when such a consumer is itself tested or covered.
+  // (exp, a denominator and negative powers can absorb inf, e.g. 1/inf = 0.)
+  static std::vector<char> value_checks(const Graph& gr) {
+    const auto& nodes = gr.nodes();
+    std::vector<char> covered(nodes.size(), 0), check(nodes.size(), 0);
+    std::vector<std::vector<int>> feeds(nodes.size());  // v -> propagating consumers
+    for (size_t u = 0; u < nodes.size(); ++u) {
+      const Node& nd = nodes[u];
+      switch (nd.op) {
+        case Op::add:
+        case Op::sub:
+        case Op::mul:
+          feeds[static_cast<size_t>(nd.a)].push_back(static_cast<int>(u));
+          feeds[static_cast<size_t>(nd.b)].push_back(static_cast<int>(u));
+          break;
+        case Op::div:
+        case Op::neg:
+        case Op::sin:
+        case Op::cos:
+        case Op::tan:
+        case Op::log:
+        case Op::sqrt: feeds[static_cast<size_t>(nd.a)].push_back(static_cast<int>(u)); break;
+        case Op::pow:
+          if (nd.c > 0.0) feeds[static_cast<size_t>(nd.a)].push_back(static_cast<int>(u));
+          break;
+        default: break;
+      }
+    }
+    for (size_t v = nodes.size(); v-- > 0;) {
+      bool by_consumer = false;
+      for (int u : feeds[v]) by_consumer |= covered[static_cast<size_t>(u)] != 0;
+      covered[v] = 1;
+      check[v] = by_consumer ? 0 : 1;
+    }
+    return check;
+  }
+
+  // slab holding an address: node offset and component; -1 if none
+  long slab_of(const Addr& a, Index& node, Index& comp) const {
+    for (size_t s = 0; s < nlp_.slabs.size(); ++s) {
+      const Slab& sl = nlp_.slabs[s];
+      if (a.base < sl.base || a.base >= sl.base + sl.dim * sl.nodes) continue;
+      if (a.stride != 0 && a.stride != sl.dim) continue;
+      node = (a.base - sl.base) / sl.dim;
+      comp = (a.base - sl.base) % sl.dim;
+      return static_cast<long>(s);
+    }
+    return -1;
+  }
+
+  // slot expression of an input at grid index `idx`
+  std::string idx_slot(const Addr& a, const std::string& idx, bool /*clamp*/) {
+    Index node = 0, comp = 0;
+    const long s = slab_of(a, node, comp);
+    if (s < 0) return a.stride == 0 ? i64(a.base) : "(" + i64(a.base) + " + " + i64(a.stride) + " * " + idx + ")";
+    const Slab& sl = nlp_.slabs[static_cast<size_t>(s)];
+    const std::string base = P("slab" + std::to_string(s) + ".base", sl.base);
+    if (a.stride == 0) {
+      // absolute slot: first node, last node (grid-dependent) or a free variable
+      const bool last = sl.nodes > 1 && node == sl.nodes - 1;
+      const std::string nd = last ? P("N", nlp_.N) : i64(node);
+      return "(" + base + " + " + nd + " * " + i64(sl.dim) + " + " + i64(comp) + ")";
+    }
+    return "(" + base + " + " + i64(node * sl.dim + comp) + " + " + i64(sl.dim) + " * " + idx + ")";
+  }
+  Fwd forward(Emitter& E, const Group& g, const std::string& idx, bool clamp, bool partials, int owner,
+              std::vector<Check>& checks) {
+    const auto& nodes = g.kernel.graph.nodes();
+    const auto& ins = g.kernel.graph.inputs();
+    Fwd f;
+    const std::vector<char> need = value_checks(g.kernel.graph);
+    f.v.resize(nodes.size());
+    f.p1.assign(nodes.size(), K(0.0));
+    f.p2.assign(nodes.size(), K(0.0));
+    for (size_t k = 0; k < nodes.size(); ++k) {
+      const Node& nd = nodes[k];
+      V r, q1 = K(0.0), q2 = K(0.0);
+      bool check_q = false;
+      auto va = [&] { return f.v[static_cast<size_t>(nd.a)]; };
+      auto vb = [&] { return f.v[static_cast<size_t>(nd.b)]; };
+      switch (nd.op) {
+        case Op::cnst: r = K(nd.c); break;
+        case Op::input: {
+          const Addr& ad = ins[static_cast<size_t>(nd.a)];
+          const std::string staged = load_from_ ? load_from_(ad) : std::string();
+          if (!staged.empty()) {
+            r = E.emit("ld" + staged, staged);
+          } else {
+            const std::string slot = idx_slot(ad, idx, clamp);
+            r = E.emit("ld" + slot, "__ldg(x + " + slot + ")");
+          }
+          break;
+        }
+        case Op::index: r = E.emit("ix" + idx + lit(nd.c), "(double)(" + idx + ") + " + lit(nd.c)); break;
+        case Op::add:
+          r = E.add(va(), vb());
+          q1 = K(1.0);
+          q2 = K(1.0);
+          break;
+        case Op::sub:
+          r = E.sub(va(), vb());
+          q1 = K(1.0);
+          q2 = K(-1.0);
+          break;
+        case Op::mul:
+          r = E.mul(va(), vb());
+          q1 = vb();
+          q2 = va();
+          break;
+        case Op::div:
+          r = E.div(va(), vb());
+          if (partials) {
+            q1 = E.div(K(1.0), vb());
+            q2 = E.div(E.neg(r), vb());
+            check_q = true;
+          }
+          break;
+        case Op::neg:
+          r = E.neg(va());
+          q1 = K(-1.0);
+          break;
+        case Op::sin:
+          r = E.trig(true, va());
+          if (partials) q1 = E.trig(false, va());
+          break;
+        case Op::cos:
+          r = E.trig(false, va());
+          if (partials) q1 = E.neg(E.trig(true, va()));
+          break;
+        case Op::tan:
+          r = E.call("tan", va());
+          if (partials) {
+            q1 = E.add(K(1.0), E.mul(r, r));
+            check_q = true;
+          }
+          break;
+        case Op::exp:
+          r = E.call("exp", va());
+          q1 = r;
+          break;
+        case Op::log:
+          r = E.call("log", va());
+          if (partials) {
+            q1 = E.div(K(1.0), va());
+            check_q = true;
+          }
+          break;
+        case Op::sqrt:
+          r = E.call("sqrt", va());
+          if (partials) {
+            q1 = E.div(K(0.5), r);
+            check_q = true;
+          }
+          break;
+        case Op::pow:
+          r = E.powc(va(), nd.c);
+          if (partials) {
+            q1 = E.mul(K(nd.c), E.powc(va(), nd.c - 1.0));
+            check_q = true;
+          }
+          break;
+      }
+      f.v[k] = r;
+      f.p1[k] = q1;
+      f.p2[k] = q2;
+      if (!r.is_c && need[k]) checks.push_back({{owner}, r});
+      if (partials && check_q) {
+        if (!q1.is_c) checks.push_back({{owner}, q1});
+        if (!q2.is_c) checks.push_back({{owner}, q2});
+      }
+    }
+    return f;
+  }
+
+  // reverse sweep for one output row (evaluator.cpp:96-112); returns the dense
+  // stencil gradient over input ordinals
+  std::vector<V> reverse_row(Emitter& E, const Group& g, const Fwd& f, int root) {
+    const auto& nodes = g.kernel.graph.nodes();
+    std::vector<V> adj(nodes.size(), K(0.0));
+    std::vector<V> grad(static_cast<size_t>(g.kernel.graph.n_inputs()), K(0.0));
+    adj[static_cast<size_t>(root)] = K(1.0);
+    for (size_t k = nodes.size(); k-- > 0;) {
+      const V ak = adj[k];
+      if (ak.zero()) continue;
+      const Node& nd = nodes[k];
+      if (nd.op == Op::input) {
+        grad[static_cast<size_t>(nd.a)] = E.add(grad[static_cast<size_t>(nd.a)], ak);
+      } else if (nd.a >= 0) {
+        adj[static_cast<size_t>(nd.a)] = E.add(adj[static_cast<size_t>(nd.a)], E.mul(ak, f.p1[k]));
+        if (nd.b >= 0) adj[static_cast<size_t>(nd.b)] = E.add(adj[static_cast<size_t>(nd.b)], E.mul(ak, f.p2[k]));
+      }
+    }
+    return grad;
+  }
+
+  // Jacobian entries of all rows in pattern order (evaluator.cpp:114-130)
+  std::vector<V> jacobian(Emitter& E, const Group& g, const Fwd& f) {
+    std::vector<V> out(g.pattern.jac.size());
+    size_t e = 0;
+    for (int r = 0; r < g.out_dim(); ++r) {
+      const size_t lo = e;
+      while (e < g.pattern.jac.size() && g.pattern.jac[e].first == r) ++e;
+      if (lo == e) continue;
+      std::vector<V> grad = reverse_row(E, g, f, g.kernel.roots[static_cast<size_t>(r)]);
+      for (size_t q = lo; q < e; ++q) out[q] = grad[static_cast<size_t>(g.pattern.jac[q].second)];
+    }
+    return out;
+  }
+
+  // weighted Hessian stencil (evaluator.cpp:145-233)
+  std::vector<V> hessian(Emitter& E, const Group& g, const Fwd& f, const std::vector<V>& w) {
+    const auto& nodes = g.kernel.graph.nodes();
+    const int ni = g.kernel.graph.n_inputs();
+    std::vector<int> input_node(static_cast<size_t>(ni), -1);
+    for (size_t k = 0; k < nodes.size(); ++k)
+      if (nodes[k].op == Op::input) input_node[static_cast<size_t>(nodes[k].a)] = static_cast<int>(k);
+    std::vector<V> seeds(nodes.size(), K(0.0));
+    for (int r = 0; r < g.out_dim(); ++r) {
+      auto& s = seeds[static_cast<size_t>(g.kernel.roots[static_cast<size_t>(r)])];
+      s = E.add(s, w[static_cast<size_t>(r)]);
+    }
+    std::vector<V> out(g.pattern.hess.size(), K(0.0));
+    for (int j = 0; j < ni; ++j) {
+      const int lo = g.pattern.dir_ptr[static_cast<size_t>(j)], hi = g.pattern.dir_ptr[static_cast<size_t>(j) + 1];
+      if (lo == hi) continue;
+      // forward dual sweep seeded on input j
+      std::vector<V> dv(nodes.size(), K(0.0));
+      for (size_t k = 0; k < nodes.size(); ++k) {
+        const Node& nd = nodes[k];
+        switch (nd.op) {
+          case Op::cnst:
+          case Op::index: dv[k] = K(0.0); break;
+          case Op::input: dv[k] = K(nd.a == j ? 1.0 : 0.0); break;
+          default: {
+            const V t1 = E.mul(f.p1[k], dv[static_cast<size_t>(nd.a)]);
+            const V t2 = nd.b >= 0 ? E.mul(f.p2[k], dv[static_cast<size_t>(nd.b)]) : K(0.0);
+            dv[k] = E.add(t1, t2);
+          }
+        }
+      }
+      // reverse sweep of adjoints and adjoint duals
+      std::vector<V> a = seeds, ad(nodes.size(), K(0.0));
+      for (size_t k = nodes.size(); k-- > 0;) {
+        const V ak = a[k], adk = ad[k];
+        if (ak.zero() && adk.zero()) continue;
+        const Node& nd = nodes[k];
+        if (nd.a < 0 || nd.op == Op::input) continue;
+        const size_t ia = static_cast<size_t>(nd.a);
+        V p1d = K(0.0), p2d = K(0.0);
+        switch (nd.op) {
+          case Op::mul:
+            p1d = dv[static_cast<size_t>(nd.b)];
+            p2d = dv[ia];
+            break;
+          case Op::div:
+            p1d = E.mul(E.mul(E.neg(f.p1[k]), f.p1[k]), dv[static_cast<size_t>(nd.b)]);
+            p2d = E.neg(E.add(E.mul(dv[k], f.p1[k]), E.mul(f.v[k], p1d)));
+            break;
+          case Op::sin:
+          case Op::cos: p1d = E.mul(E.neg(f.v[k]), dv[ia]); break;
+          case Op::tan: p1d = E.mul(E.mul(K(2.0), f.v[k]), dv[k]); break;
+          case Op::exp: p1d = dv[k]; break;
+          case Op::log: p1d = E.mul(E.mul(E.neg(f.p1[k]), f.p1[k]), dv[ia]); break;
+          case Op::sqrt:
+            if (!dv[k].zero()) {
+              const V num = E.mul(E.neg(f.p1[k]), dv[k]);
+              const V vk = f.v[k];
+              p1d = E.emit("sq" + E.s(num) + E.s(vk),
+                           "(" + E.s(vk) + " != 0.0) ? " + E.s(num) + " / " + E.s(vk) + " : 0.0");
+            }
+            break;
+          case Op::pow: {
+            const V s = E.mul(K(nd.c * (nd.c - 1.0)), E.powc(f.v[ia], nd.c - 2.0));
+            p1d = E.mul(s, dv[ia]);
+            if (!ak.zero() && !s.is_c) E.line("ok = ok & (fin(" + E.s(s) + ") | (" + E.s(ak) + " == 0.0));");
+            break;
+          }
+          default: break;
+        }
+        a[ia] = E.add(a[ia], E.mul(ak, f.p1[k]));
+        ad[ia] = E.add(ad[ia], E.add(E.mul(adk, f.p1[k]), E.mul(ak, p1d)));
+        if (nd.b >= 0) {
+          const size_t ib = static_cast<size_t>(nd.b);
+          a[ib] = E.add(a[ib], E.mul(ak, f.p2[k]));
+          ad[ib] = E.add(ad[ib], E.add(E.mul(adk, f.p2[k]), E.mul(ak, p2d)));
+        }
+      }
+      for (int e = lo; e < hi; ++e) {
+        const int node = input_node[static_cast<size_t>(g.pattern.hess[static_cast<size_t>(e)].first)];
+        out[static_cast<size_t>(e)] = node >= 0 ? ad[static_cast<size_t>(node)] : K(0.0);
+      }
+    }
+    return out;
+  }
+
+  // finiteness: one DFMA per checked value (v*0 is NaN iff v is not finite)
+  void check_inline(Emitter& E, V v) {
+    if (!v.is_c) E.line("okacc = __fma_rn(" + E.s(v) + ", 0.0, okacc);");
+  }
+
+  static std::string i64(Index v) { return std::to_string(v) + "LL"; }
+
+  // AD + stores for one group instance; k is the range ordinal expression.
+  void group_body(Emitter& E, Mode m, bool objective, int gi, const Fwd& f, const std::string& k) {
+    const Group& g = objective ? nlp_.objs[static_cast<size_t>(gi)] : nlp_.cons[static_cast<size_t>(gi)];
+    const size_t gs = static_cast<size_t>(gi);
+    const Parts p = parts(m, objective, g);
+    const int od = g.out_dim();
+    const std::string rb = objective ? std::string() : G(false, gi, "row_base", g.row_base);
+    auto row_expr = [&](int r) { return "(" + rb + " + " + k + " * " + i64(od) + " + " + i64(r) + ")"; };
+    std::vector<V> rsv(static_cast<size_t>(od));
+    auto rowscale = [&](int r) {
+      V& v = rsv[static_cast<size_t>(r)];
+      if (v.id < 0) v = E.emit("rs" + row_expr(r), "__ldg(rs + " + row_expr(r) + ")");
+      return v;
+    };
+    // store target: staged shared memory when the kernel stages, else global
+    auto lv = [&](int kind, Index e, const std::string& global) {
+      const std::string s = store_to_ ? store_to_(kind, e) : std::string();
+      return s.empty() ? global : s;
+    };
+    if (p.values) {
+      for (int r = 0; r < od; ++r) {
+        const V c = E.mul(rowscale(r), f.v[static_cast<size_t>(g.kernel.roots[static_cast<size_t>(r)])]);
+        E.line(lv(0, r, "cout[" + row_expr(r) + "]") + " = " + E.s(c) + ";");
+      }
+    }
+    if (p.jac) {
+      const std::vector<V> jv = jacobian(E, g, f);
+      const Index nnz = static_cast<Index>(g.pattern.jac.size());
+      const std::string base = G(false, gi, "jac_off", lay_.jac_off[gs]) + " + " + k + " * " + i64(nnz);
+      for (size_t e = 0; e < jv.size(); ++e) {
+        check_inline(E, jv[e]);
+        const V sv = E.mul(jv[e], rowscale(g.pattern.jac[e].first));
+        E.line(lv(1, static_cast<Index>(e), "jac[" + base + " + " + i64(static_cast<Index>(e)) + "]") + " = " +
+               E.s(sv) + ";");
+      }
+    }
+    if (p.grad) {
+      const std::vector<V> jv = jacobian(E, g, f);
+      const V w = E.emit("ow" + std::to_string(gi), "__ldg(objw + " + std::to_string(gi) + ")");
+      const Index nnz = static_cast<Index>(g.pattern.jac.size());
+      const std::string base = G(true, gi, "grad_off", lay_.grad_off[gs]) + " + " + k + " * " + i64(nnz);
+      for (size_t e = 0; e < jv.size(); ++e) {
+        check_inline(E, jv[e]);
+        E.line(lv(2, static_cast<Index>(e), "gout[" + base + " + " + i64(static_cast<Index>(e)) + "]") + " = " +
+               E.s(E.mul(jv[e], w)) + ";");
+      }
+    }
+    if (p.objv) {
+      const V v = f.v[static_cast<size_t>(g.kernel.roots[0])];
+      E.line(lv(3, 0, "objv[" + G(true, gi, "objv_off", lay_.objv_off[gs]) + " + " + k + "]") + " = " + E.s(v) + ";");
+    }
+    if (p.hess) {
+      std::vector<V> w(static_cast<size_t>(od));
+      if (objective) {
+        w[0] = E.emit("ow" + std::to_string(gi), "__ldg(objw + " + std::to_string(gi) + ")");
+      } else {
+        for (int r = 0; r < od; ++r) {
+          const V lam = E.emit("lam" + row_expr(r), "__ldg(lam + " + row_expr(r) + ")");
+          w[static_cast<size_t>(r)] = E.mul(lam, rowscale(r));
+        }
+      }
+      const std::vector<V> hv = hessian(E, g, f, w);
+      const Index nnz = static_cast<Index>(g.pattern.hess.size());
+      const std::string off = objective ? G(true, gi, "hess_off", lay_.hess_off_obj[gs])
+                                        : G(false, gi, "hess_off", lay_.hess_off_con[gs]);
+      const std::string base = off + " + " + k + " * " + i64(nnz);
+      for (size_t e = 0; e < hv.size(); ++e) {
+        check_inline(E, hv[e]);
+        E.line(lv(4, static_cast<Index>(e), "hess[" + base + " + " + i64(static_cast<Index>(e)) + "]") + " = " +
+               E.s(hv[e]) + ";");
+      }
+    }
+  }
+
+  // One kernel of a mode: persistent, warp-synchronous. Every warp walks its
+  // own tiles of 32 grid indices (one per lane) with no block barriers:
+  //   (1) the node slabs the grid-indexed groups read are staged into the
+  //       warp's shared-memory rows with coalesced loads (x read once);
+  //   (2) the groups run one after another — the whole warp executes one
+  //       group's straight-line code at a time, keeping the instruction working
+  //       set to one group — each lane writing its COO entries into its
+  //       shared-memory row;
+  //   (3) after __syncwarp the warp writes the group's contiguous COO segment
+  //       (32 x nnz doubles) back with fully coalesced stores.
+  // Endpoint and single-index (boundary/Mayer) instances run after the loop on
+  // the last block, one thread each, straight to global memory.
+  std::string kernel(Mode m, const char* name, const char* params, int& slices, int& tail) {
+    struct Inst {
+      bool objective;
+      int gi;
+      Index k;
+    };
+    std::vector<Inst> members, tails;
+    auto scan = [&](bool objective, const std::vector<Group>& gs) {
+      for (size_t g = 0; g < gs.size(); ++g) {
+        if (!parts(m, objective, gs[g]).any()) continue;
+        const Range& r = gs[g].range;
+        if (!r.endpoints && gs[g].kind != Group::Kind::boundary)
+          members.push_back({objective, static_cast<int>(g), 0});
+        else
+          for (Index k = 0; k < r.count(); ++k) tails.push_back({objective, static_cast<int>(g), k});
+      }
+    };
+    scan(false, nlp_.cons);
+    scan(true, nlp_.objs);
+    constexpr Index W = 32;  // grid indices per warp tile
+
+    // node slabs read by any member group: nodes [ib, ib + W + max_off)
+    struct Use {
+      Index soff = 0, max_off = 0;
+    };
+    std::map<size_t, Use> uses;
+    for (const Inst& mb : members) {
+      const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+      for (const Addr& a : g.kernel.graph.inputs()) {
+        if (a.stride == 0) continue;
+        Index node = 0, comp = 0;
+        const long s = slab_of(a, node, comp);
+        if (s >= 0) uses[static_cast<size_t>(s)].max_off = std::max(uses[static_cast<size_t>(s)].max_off, node);
+      }
+    }
+    Index cur = 0;
+    for (auto& [s, u] : uses) {
+      u.soff = cur;
+      cur += (W + u.max_off) * nlp_.slabs[s].dim;
+    }
+    // output rows: one region reused by every group (warp-synchronous)
+    struct Out {
+      int kind;
+      Index per_k, pitch, soff;
+      std::string dst;
+    };
+    std::vector<std::vector<Out>> outs(members.size());
+    Index region = 0;
+    for (size_t q = 0; q < members.size(); ++q) {
+      const Inst& mb = members[q];
+      const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+      const Parts p = parts(m, mb.objective, g);
+      const size_t gi = static_cast<size_t>(mb.gi);
+      Index off = cur;
+      auto add_out = [&](int kind, Index per_k, const std::string& dst) {
+        if (per_k <= 0) return;
+        const Index pitch = per_k;  // unpadded: the copy-out is a plain linear copy
+        outs[q].push_back({kind, per_k, pitch, off, dst});
+        off += W * pitch;
+      };
+      if (p.values) add_out(0, g.out_dim(), "cout + " + G(false, mb.gi, "row_base", g.row_base));
+      if (p.jac)
+        add_out(1, static_cast<Index>(g.pattern.jac.size()), "jac + " + G(false, mb.gi, "jac_off", lay_.jac_off[gi]));
+      if (p.grad)
+        add_out(2, static_cast<Index>(g.pattern.jac.size()), "gout + " + G(true, mb.gi, "grad_off", lay_.grad_off[gi]));
+      if (p.objv) add_out(3, 1, "objv + " + G(true, mb.gi, "objv_off", lay_.objv_off[gi]));
+      if (p.hess)
+        add_out(4, static_cast<Index>(g.pattern.hess.size()),
+                "hess + " + (mb.objective ? G(true, mb.gi, "hess_off", lay_.hess_off_obj[gi])
+                                          : G(false, mb.gi, "hess_off", lay_.hess_off_con[gi])));
+      region = std::max(region, off - cur);
+    }
+    const Index per_warp = cur + region;  // doubles of shared memory per warp
+
+    Emitter E;
+    E.depth = 0;
+    E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK) " + std::string(name) +
+           "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec) {");
+    E.depth = 1;
+    E.line("extern __shared__ double smem_all[];");
+    E.line("const int lane = threadIdx.x & 31;");
+    E.line("double* __restrict__ smem = smem_all + (threadIdx.x >> 5) * " + i64(per_warp) + ";");
+    E.line("double okacc = 0.0;  // fma(v, 0, acc) turns NaN iff some checked v is not finite");
+    E.line("bool ok = true;");
+    E.line("const long long ntiles = (n_main + 31) / 32;");
+    E.line("const long long wpb = OCG_BLOCK / 32;");
+    E.open("for (long long tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb)");
+    E.line("const long long ib = i0 + tile * 32;");
+    E.line("const long long idx = ib + lane;");
+    E.line("const bool in = idx < i0 + n_main;");
+    for (auto& [s, u] : uses) {
+      const Slab& sl = nlp_.slabs[s];
+      const Index n = (W + u.max_off) * sl.dim;
+      const std::string sb = P("slab" + std::to_string(s) + ".base", sl.base);
+      const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
+      E.line("{ const long long gb = " + sb + " + ib * " + i64(sl.dim) + "; long long nv = " + se +
+             " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) +
+             "; for (int j = lane; j < (int)nv; j += 32) smem[" + i64(u.soff) + " + j] = __ldg(x + gb + j); }");
+    }
+    if (!uses.empty()) E.line("__syncwarp();");
+    load_from_ = [&](const Addr& a) -> std::string {
+      if (a.stride == 0) return "";
+      Index node = 0, comp = 0;
+      const long s = slab_of(a, node, comp);
+      if (s < 0) return "";
+      const Index dim = nlp_.slabs[static_cast<size_t>(s)].dim;
+      return "smem[" + i64(uses.at(static_cast<size_t>(s)).soff + node * dim + comp) + " + lane * " + i64(dim) + "]";
+    };
+    for (size_t q = 0; q < members.size(); ++q) {
+      const Inst& mb = members[q];
+      const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+      const Parts p = parts(m, mb.objective, g);
+      const std::string lo = G(mb.objective, mb.gi, "lo", g.range.lo);
+      const std::string hi = G(mb.objective, mb.gi, "hi", g.range.hi);
+      store_to_ = [&](int kind, Index e) -> std::string {
+        for (const Out& o : outs[q])
+          if (o.kind == kind) return "smem[" + i64(o.soff + e) + " + lane * " + i64(o.pitch) + "]";
+        return "";
+      };
+      E.line("// ---- " + std::string(mb.objective ? "objective" : "constraint") + " group " +
+             std::to_string(mb.gi) + ": " + g.label);
+      E.open("if (in && idx >= " + lo + " && idx < " + hi + ")");
+      E.line("const long long k = idx - " + lo + ";");
+      std::vector<Check> sc;
+      Fwd f = forward(E, g, "idx", false, p.partials, 0, sc);
+      for (const auto& c : sc) check_inline(E, c.v);
+      group_body(E, m, mb.objective, mb.gi, f, "k");
+      E.close();
+      store_to_ = nullptr;
+      if (outs[q].empty()) continue;
+      E.line("__syncwarp();");
+      E.open("");
+      E.line("const long long kb = ib - " + lo + ";");
+      E.line("const long long k0 = kb > 0 ? kb : 0;");
+      E.line("long long k1 = kb + 32; if (k1 > " + hi + " - " + lo + ") k1 = " + hi + " - " + lo +
+             "; if (k1 > i0 + n_main - " + lo + ") k1 = i0 + n_main - " + lo + ";");
+      E.line("const int nk = (int)(k1 - k0), r0 = (int)(k0 - kb);");
+      for (const Out& o : outs[q]) {
+        const std::string S = std::to_string(o.per_k);
+        // rows are unpadded (pitch == per_k): the warp's segment is contiguous
+        // in shared memory and in the COO array
+        E.line("{ double* __restrict__ dst = " + o.dst + " + k0 * " + S + "LL; const double* src = smem + " +
+               i64(o.soff) + " + r0 * " + S + "; for (int j = lane; j < nk * " + S +
+               "; j += 32) dst[j] = src[j]; }");
+      }
+      E.close();
+      E.line("__syncwarp();");
+    }
+    load_from_ = nullptr;
+    E.close();  // tile loop
+
+    if (!tails.empty()) {
+      E.open("if (blockIdx.x == gridDim.x - 1)");
+      E.open("for (int s = threadIdx.x; s < (int)n_spec; s += OCG_BLOCK)");
+      E.line("switch (s) {");
+      for (size_t s = 0; s < tails.size(); ++s) {
+        const Inst& in = tails[s];
+        const Group& g = in.objective ? nlp_.objs[static_cast<size_t>(in.gi)] : nlp_.cons[static_cast<size_t>(in.gi)];
+        const Parts p = parts(m, in.objective, g);
+        E.open("case " + std::to_string(s) + ":");
+        const std::string idx = in.k == 0 ? G(in.objective, in.gi, "lo", g.range.lo)
+                                          : G(in.objective, in.gi, "hi", g.range.hi);
+        E.line("const long long sidx = " + idx + ";");
+        std::vector<Check> sc;
+        Fwd f = forward(E, g, "sidx", false, p.partials, 0, sc);
+        for (const auto& c : sc) check_inline(E, c.v);
+        group_body(E, m, in.objective, in.gi, f, i64(in.k));
+        E.line("break;");
+        E.close();
+      }
+      E.line("default: break;");
+      E.line("}");
+      E.close();
+      E.close();
+    }
+    E.line("if (!ok || !fin(okacc)) *flag = 1;");
+    E.depth = 0;
+    E.line("}");
+    E.line("");
+    slices = 1;
+    tail = static_cast<int>(tails.size());
+    smem_out_ = per_warp * 8 * (opt_.block / 32);
+    return E.out;
+  }
+};
+
+}  // namespace
+
+Generated generate(const Nlp& nlp, const Layout& lay, const GenOptions& opt) {
+  Generator gen(nlp, lay, opt);
+  return gen.module();
+}
+
+}  // namespace ocg
+

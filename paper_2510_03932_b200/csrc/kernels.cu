@@ -1,0 +1,188 @@
+// Hand-written sm_100a kernels: deterministic reductions and gathers around
+// the generated per-node kernels. See kernels.hpp for the reference each one
+// mirrors. All of them are HBM-bound streaming/gather kernels; grids are
+// sized in multiples of the 148 SMs x resident blocks.
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace ocg::dev {
+
+namespace {
+
+constexpr int kChunk = 512;  // Backend::kChunkSize (backend.hpp:50)
+constexpr int kSms = 148;
+
+__device__ __forceinline__ bool finite(double v) { return fabs(v) <= 1.7976931348623157e308; }
+
+// One warp per 512-instance chunk: coalesced loads into shared memory, then
+// lane 0 adds in index order (the reference's `s += v` loop).
+__global__ void __launch_bounds__(256) chunk_sums(const double* __restrict__ objv, const int64_t* __restrict__ goff,
+                                                  const int64_t* __restrict__ gcount,
+                                                  const int64_t* __restrict__ cbase, int64_t n_chunks,
+                                                  int n_groups, double* __restrict__ partials) {
+  __shared__ double buf[8][kChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (c >= n_chunks) return;
+  int g = 0;
+  while (g + 1 < n_groups && cbase[g + 1] <= c) ++g;
+  const int64_t lo = (c - cbase[g]) * kChunk;
+  const int64_t hi = min(gcount[g], lo + kChunk);
+  const int64_t n = hi - lo;
+  const double* src = objv + goff[g] + lo;
+  for (int64_t i = lane; i < n; i += 32) buf[warp][i] = src[i];
+  __syncwarp();
+  if (lane == 0) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += buf[warp][i];
+    partials[c] = s;
+  }
+}
+
+__global__ void combine_chunks(const double* __restrict__ partials, const int64_t* __restrict__ cbase,
+                               const double* __restrict__ weights, int n_groups, double obj_scale,
+                               double* __restrict__ f, int* __restrict__ flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double total = 0.0;
+  for (int g = 0; g < n_groups; ++g) {
+    double part = 0.0;
+    for (int64_t c = cbase[g]; c < cbase[g + 1]; ++c) part += partials[c];
+    total += weights[g] * part;
+  }
+  const double fs = obj_scale * total;
+  *f = fs;
+  if (!finite(fs)) *flag = 1;
+}
+
+__global__ void __launch_bounds__(256) gather_sum_k(const double* __restrict__ src, const int64_t* __restrict__ ptr,
+                                                    const int32_t* __restrict__ idx, int64_t n,
+                                                    double* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) s += src[idx[p]];
+    out[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) kkt_assemble_k(const double* __restrict__ hess, const double* __restrict__ jac,
+                                                      const double* __restrict__ sigma,
+                                                      const int64_t* __restrict__ ptr,
+                                                      const int64_t* __restrict__ code, int64_t nnz, int64_t H,
+                                                      int64_t J, int64_t S, double* __restrict__ val) {
+  const int64_t HJ = H + J, HJS = H + J + S;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t q = ptr[p]; q < ptr[p + 1]; ++q) {
+      const int64_t c = code[q];
+      double v;
+      if (c < H)
+        v = hess[c];
+      else if (c < HJ)
+        v = jac[c - H];
+      else if (c < HJS)
+        v = -1.0;
+      else
+        v = sigma[c - HJS];
+      s += v;
+    }
+    val[p] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) sym_matvec_k(const double* __restrict__ val, const int64_t* __restrict__ rptr,
+                                                    const int64_t* __restrict__ col,
+                                                    const int64_t* __restrict__ vidx, int64_t n,
+                                                    const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = rptr[i]; p < rptr[i + 1]; ++p) s += val[vidx[p]] * x[col[p]];
+    y[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) jt_lambda_k(const double* __restrict__ jac, const double* __restrict__ lam,
+                                                   const int64_t* __restrict__ ptr, const int64_t* __restrict__ e_idx,
+                                                   const int64_t* __restrict__ dual_idx, int64_t n_free,
+                                                   const int64_t* __restrict__ slack_dual, int64_t n_slack,
+                                                   double* __restrict__ out) {
+  const int64_t ntot = n_free + n_slack;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ntot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) s += jac[e_idx[p]] * lam[dual_idx[p]];
+    if (i >= n_free) s -= lam[slack_dual[i - n_free]];
+    out[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) max_abs_k(const double* __restrict__ v, int64_t n,
+                                                 unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = fmax(m, fabs(v[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmax(m, wm[w]);
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+int grid_for(int64_t n, int block) {
+  const int64_t want = (n + block - 1) / block;
+  const int64_t cap = static_cast<int64_t>(kSms) * 16;
+  return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace
+
+void objective_reduce(const double* objv, const int64_t* group_off, const int64_t* group_count,
+                      const int64_t* chunk_base, int64_t n_chunks, const double* weights, int n_groups,
+                      double obj_scale, double* partials, double* f, int* flag, cudaStream_t s) {
+  if (n_chunks > 0) {
+    const int blocks = static_cast<int>((n_chunks + 7) / 8);
+    chunk_sums<<<blocks, 256, 0, s>>>(objv, group_off, group_count, chunk_base, n_chunks, n_groups, partials);
+  }
+  combine_chunks<<<1, 32, 0, s>>>(partials, chunk_base, weights, n_groups, obj_scale, f, flag);
+}
+
+void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,
+                cudaStream_t s) {
+  if (n <= 0) return;
+  gather_sum_k<<<grid_for(n, 256), 256, 0, s>>>(src, ptr, idx, n, out);
+}
+
+void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
+                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, double* val, cudaStream_t s) {
+  if (nnz <= 0) return;
+  kkt_assemble_k<<<grid_for(nnz, 256), 256, 0, s>>>(hess, jac, sigma, ptr, code, nnz, H, J, S, val);
+}
+
+void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
+                const double* x, double* y, cudaStream_t s) {
+  if (n <= 0) return;
+  sym_matvec_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, col, vidx, n, x, y);
+}
+
+void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
+               const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
+               cudaStream_t s) {
+  const int64_t n = n_free + n_slack;
+  if (n <= 0) return;
+  jt_lambda_k<<<grid_for(n, 256), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx, n_free, slack_dual, n_slack, out);
+}
+
+void max_abs(const double* v, int64_t n, double* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (n <= 0) return;
+  max_abs_k<<<grid_for(n, 256), 256, 0, s>>>(v, n, reinterpret_cast<unsigned long long*>(out));
+}
+
+}  // namespace ocg::dev

@@ -1,0 +1,47 @@
+// Hand-written sm_100a kernels around the generated per-node kernels:
+// deterministic reductions, gathers and the KKT value assembly. Every sum is
+// taken in the reference's accumulation order (starting from 0.0, sources in
+// increasing order) so the results are bit-identical to the CPU reference;
+// no floating-point atomics anywhere (max via integer atomics on the bit
+// pattern of non-negative doubles is exact and order-free).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ocg::dev {
+
+// Objective: per-instance values -> f (EvalContext::eval_objective + Backend::par_reduce,
+// eval.cpp:175-200, backend.cpp:119-133): chunks of 512 summed in index
+// order, chunk partials combined in chunk order, total += weight*part per group,
+// f = obj_scale * total. group_* arrays are device arrays of length n_groups.
+void objective_reduce(const double* objv, const int64_t* group_off, const int64_t* group_count,
+                      const int64_t* chunk_base, int64_t n_chunks, const double* weights, int n_groups,
+                      double obj_scale, double* partials, double* f, int* flag, cudaStream_t s);
+
+// out[i] = sum_{p in [ptr[i], ptr[i+1])} src[idx[p]]  (0.0-based, in p order)
+void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,
+                cudaStream_t s);
+
+// K.val[p] = sum of its sources in code order (KktAssembler::assemble,
+// eval.cpp:429-440): code < H: hess[code]; < H+J: jac[code-H]; < H+J+S: -1.0;
+// else sigma[code-H-J-S].
+void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
+                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, double* val, cudaStream_t s);
+
+// y[i] = sum over the full symmetric row i (increasing column) of K_ij x_j —
+// the accumulation order of sparse::matvec_sym (sparse.cpp:51-61).
+void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
+                const double* x, double* y, cudaStream_t s);
+
+// out[i] = sum_p jac[e_p] * lam[dual_p] (p in increasing e), then for slack
+// rows out[i] -= lam[dual] (Solver::compute_jt_lambda, solver.cpp:244-257).
+void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
+               const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
+               cudaStream_t s);
+
+// max |v| over n entries into *out (device scalar); exact.
+void max_abs(const double* v, int64_t n, double* out, cudaStream_t s);
+
+}  // namespace ocg::dev

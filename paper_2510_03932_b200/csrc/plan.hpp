@@ -1,0 +1,60 @@
+// Device evaluation plan: COO offsets, thread mapping and generated kernels.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "model.hpp"
+
+namespace ocg {
+
+// COO layout of the reference EvalContext (eval.cpp:44-81): constraint groups
+// first (jac, hess), then objective groups (grad, hess), group-major then
+// index-major. Thread mapping: every contiguous-range group is evaluated by
+// the thread of its grid index (k = idx - lo); endpoint-pair groups are
+// "special" instances handled by a short tail of extra threads.
+struct Layout {
+  std::vector<Index> jac_off, hess_off_con, hess_off_obj, grad_off, objv_off;
+  Index jac_nnz = 0, hess_nnz = 0, grad_nnz = 0, objv_n = 0;
+  Index idx_lo = 0, idx_hi = 0;  // main grid-index space [idx_lo, idx_hi)
+  struct Special {
+    bool objective;
+    int group;
+    Index k;
+  };
+  std::vector<Special> specials;
+};
+
+Layout make_layout(const Nlp& nlp);
+
+struct GenOptions {
+  bool fma = false;  // false: no FMA contraction (bit-compatible with the x86 reference)
+  int block = 128;
+};
+
+struct Generated {
+  std::string source;
+  // kernel name -> gridDim.y it expects (1 for the merged mapping)
+  std::map<std::string, int> slices;
+  // kernel name -> threads of the tail (endpoint / small-range instances)
+  std::map<std::string, int> tail;
+  // kernel name -> dynamic shared memory bytes per block
+  std::map<std::string, int> smem;
+  // values of the by-value parameter block (first kernel argument)
+  std::vector<long long> params;
+};
+
+// Kernel entry points in the generated module (all extern "C"):
+//   ocg_c     (x, row_scale, c, flag, i0, n_main, n_spec)
+//   ocg_cjac  (x, row_scale, c, jac, flag, i0, n_main, n_spec)
+//   ocg_hess  (x, lambda, row_scale, objw, hess, flag, i0, n_main, n_spec)
+//   ocg_cjh   (x, lambda, row_scale, objw, c, jac, hess, flag, i0, n_main, n_spec)
+//   ocg_objv  (x, objv, flag, i0, n_main, n_spec)
+//   ocg_grad  (x, objw, grad, flag, i0, n_main, n_spec)
+Generated generate(const Nlp& nlp, const Layout& lay, const GenOptions& opt);
+inline std::string generate_source(const Nlp& nlp, const Layout& lay, const GenOptions& opt) {
+  return generate(nlp, lay, opt).source;
+}
+
+}  // namespace ocg

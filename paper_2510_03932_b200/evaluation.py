@@ -1,0 +1,292 @@
+"""Python host mirror of the reference evaluation interface.
+
+`Model` is transcribe::StructuredNlp built from model text
+(/root/reference/proj/src/transcribe/transcribe.cpp:180), `EvalContext` is
+ipm::detail::EvalContext (/root/reference/proj/src/ipm/ipm_internal.hpp:40-95)
+and `KktAssembler` is Reduction + KktAssembler (ipm_internal.hpp:102-146):
+same member names, same argument meaning, same bool results. Values live in
+device memory (torch CUDA tensors bound into the library); every computation
+runs in libocgpu.so's sm_100a kernels — there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import LIB, check
+
+SCHEMES = {"euler": 0, "trapezoid": 1}
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Model:
+    """Parsed + transcribed OCP (dsl::parse_ocp + transcribe::transcribe)."""
+
+    def __init__(self, source: str, N: int, scheme: str = "trapezoid", boxes_as_bounds: bool = False):
+        h = C.c_void_p()
+        check(LIB.ocg_model_create(source.encode(), SCHEMES[scheme], int(N), int(boxes_as_bounds), C.byref(h)),
+              "ocg_model_create")
+        self._h = h
+        self.source = source
+        self.N = int(N)
+        self.scheme = scheme
+        self.nvar = LIB.ocg_model_nvar(h)
+        self.m_con = LIB.ocg_model_mcon(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_model_destroy(self._h)
+            self._h = None
+
+    def arrays(self) -> dict:
+        nv, m = self.nvar, self.m_con
+        out = {k: np.empty(nv) for k in ("lvar", "uvar", "x_start", "clip_lo", "clip_hi")}
+        out.update({k: np.empty(m) for k in ("lcon", "ucon")})
+        check(LIB.ocg_model_arrays(self._h, *[out[k].ctypes.data for k in
+                                               ("lvar", "uvar", "x_start", "clip_lo", "clip_hi", "lcon", "ucon")]))
+        return out
+
+    def structure(self) -> dict:
+        return json.loads(_lib.take_string(LIB.ocg_model_structure_json(self._h)))
+
+    def synth_acceptance(self, seed: int = 20250808) -> tuple[np.ndarray, np.ndarray]:
+        x, lam = np.empty(self.nvar), np.empty(self.m_con)
+        check(LIB.ocg_model_synth_acceptance(self._h, seed, x.ctypes.data, lam.ctypes.data))
+        return x, lam
+
+    def generated_source(self, fma: bool = False, block: int = 128) -> str:
+        return _lib.take_string(LIB.ocg_debug_generated_source(self._h, int(fma), block))
+
+
+def synth_uniform(seed: int, lo: float, hi: float, n: int) -> np.ndarray:
+    out = np.empty(n)
+    check(LIB.ocg_synth_uniform(seed, lo, hi, n, out.ctypes.data))
+    return out
+
+
+class EvalContext:
+    """Device EvalContext: COO structure bit-identical to the reference's; values
+    in `jac_val`, `hess_val`, `grad_val` (CUDA tensors); `obj_scale`/`row_scale`
+    as in the reference. Methods return the reference's bool."""
+
+    def __init__(self, model: Model, device: int = 0, fma: bool = False, block: int = 128,
+                 idx_lo: int = 0, idx_hi: int = -1, specials: bool = True):
+        if not torch.cuda.is_available():
+            raise RuntimeError("octgpu EvalContext needs a CUDA device (no CPU fallback)")
+        self.model = model
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials))
+        h = C.c_void_p()
+        check(LIB.ocg_eval_create(model._h, C.byref(opts), C.byref(h)), "ocg_eval_create")
+        self._h = h
+        j, hh, g = C.c_int64(), C.c_int64(), C.c_int64()
+        check(LIB.ocg_eval_sizes(h, C.byref(j), C.byref(hh), C.byref(g)))
+        self.jac_nnz, self.hess_nnz, self.grad_nnz = j.value, hh.value, g.value
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.jac_val = torch.zeros(max(self.jac_nnz, 1), **f64)[: self.jac_nnz]
+        self.hess_val = torch.zeros(max(self.hess_nnz, 1), **f64)[: self.hess_nnz]
+        self.grad_val = torch.zeros(max(self.grad_nnz, 1), **f64)[: self.grad_nnz]
+        self._rs = torch.ones(max(model.m_con, 1), **f64)
+        self.row_scale = self._rs[: model.m_con]
+        for which, t in ((_lib.OCG_BUF_JAC, self.jac_val), (_lib.OCG_BUF_HESS, self.hess_val),
+                         (_lib.OCG_BUF_GRAD, self.grad_val), (_lib.OCG_BUF_ROWSCALE, self._rs)):
+            check(LIB.ocg_eval_bind_buffer(h, which, _ptr(t)), "bind")
+        self._f = torch.zeros(1, **f64)
+        self._scratch = torch.zeros(1, **f64)
+        self.obj_scale = 1.0
+        self.time_derivatives = 0.0
+        self._structure = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_eval_destroy(self._h)
+            self._h = None
+
+    # ---- structure queries (host int64, EvalContext's public members) ----
+    def structure(self) -> dict:
+        if self._structure is None:
+            a = [np.empty(n, dtype=np.int64) for n in
+                 (self.jac_nnz, self.jac_nnz, self.hess_nnz, self.hess_nnz, self.grad_nnz)]
+            check(LIB.ocg_eval_structure(self._h, *[v.ctypes.data for v in a]))
+            self._structure = dict(zip(["jac_row", "jac_col", "hess_row", "hess_col", "grad_col"], a))
+        return self._structure
+
+    @property
+    def jac_row(self):
+        return self.structure()["jac_row"]
+
+    @property
+    def jac_col(self):
+        return self.structure()["jac_col"]
+
+    @property
+    def hess_row(self):
+        return self.structure()["hess_row"]
+
+    @property
+    def hess_col(self):
+        return self.structure()["hess_col"]
+
+    @property
+    def grad_col(self):
+        return self.structure()["grad_col"]
+
+    # ---- scaling ----
+    def set_scaling(self, obj_scale: float, row_scale=None) -> None:
+        rs = None if row_scale is None else np.ascontiguousarray(row_scale, dtype=np.float64)
+        check(LIB.ocg_eval_set_scaling(self._h, float(obj_scale), None if rs is None else rs.ctypes.data))
+        self.obj_scale = float(obj_scale)
+
+    def compute_scaling(self, x0, enabled: bool = True) -> None:
+        x0 = self._dev(x0)
+        check(LIB.ocg_eval_compute_scaling(self._h, _ptr(x0), int(enabled), _stream()))
+        o = C.c_double()
+        check(LIB.ocg_eval_get_scaling(self._h, C.byref(o), None))
+        self.obj_scale = o.value
+
+    # ---- evaluation (reference bool semantics) ----
+    def _dev(self, a) -> torch.Tensor:
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=torch.float64).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)
+
+    def status(self, stream=None) -> bool:
+        return check(LIB.ocg_eval_status(self._h, _stream(stream))) == _lib.OCG_OK
+
+    def eval_constraints(self, x, c_scaled: torch.Tensor) -> bool:
+        x = self._dev(x)
+        check(LIB.ocg_eval_constraints(self._h, _ptr(x), _ptr(c_scaled), _stream()))
+        return self.status()
+
+    def eval_constraints_jacobian(self, x, c_scaled: torch.Tensor) -> bool:
+        x = self._dev(x)
+        check(LIB.ocg_eval_constraints_jacobian(self._h, _ptr(x), _ptr(c_scaled), _stream()))
+        return self.status()
+
+    def eval_objective(self, x) -> tuple[bool, float]:
+        x = self._dev(x)
+        check(LIB.ocg_eval_objective(self._h, _ptr(x), _ptr(self._f), _stream()))
+        ok = self.status()
+        return ok, float(self._f.item())
+
+    def eval_gradient(self, x, grad_dense: torch.Tensor) -> bool:
+        x = self._dev(x)
+        check(LIB.ocg_eval_gradient(self._h, _ptr(x), _ptr(grad_dense), _stream()))
+        return self.status()
+
+    def eval_hessian(self, x, lambda_scaled) -> bool:
+        x, lam = self._dev(x), self._dev(lambda_scaled)
+        check(LIB.ocg_eval_hessian(self._h, _ptr(x), _ptr(lam), _stream()))
+        return self.status()
+
+    def eval_jac_hess(self, x, lambda_scaled, c_scaled: torch.Tensor) -> bool:
+        """Fused eval_constraints_jacobian + eval_hessian at one point."""
+        x, lam = self._dev(x), self._dev(lambda_scaled)
+        check(LIB.ocg_eval_jac_hess(self._h, _ptr(x), _ptr(lam), _ptr(c_scaled), _stream()))
+        return self.status()
+
+    def max_abs_hessian(self) -> float:
+        check(LIB.ocg_eval_max_abs_hessian(self._h, _ptr(self._scratch), _stream()))
+        return float(self._scratch.item())
+
+    # ---- raw async entry points (device pointers, caller's stream) ----
+    def launch_constraints_jacobian(self, x: torch.Tensor, c: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_constraints_jacobian(self._h, _ptr(x), _ptr(c), _stream(stream)))
+
+    def launch_hessian(self, x: torch.Tensor, lam: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_hessian(self._h, _ptr(x), _ptr(lam), _stream(stream)))
+
+    def launch_jac_hess(self, x: torch.Tensor, lam: torch.Tensor, c: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_jac_hess(self._h, _ptr(x), _ptr(lam), _ptr(c), _stream(stream)))
+
+    def launch_constraints(self, x: torch.Tensor, c: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_constraints(self._h, _ptr(x), _ptr(c), _stream(stream)))
+
+    def launch_objective(self, x: torch.Tensor, f: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_objective(self._h, _ptr(x), _ptr(f), _stream(stream)))
+
+    def launch_gradient(self, x: torch.Tensor, g: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_gradient(self._h, _ptr(x), _ptr(g), _stream(stream)))
+
+    @property
+    def launch_count(self) -> int:
+        return LIB.ocg_eval_launch_count(self._h)
+
+
+class KktAssembler:
+    """Reduction + KktAssembler on the device: K (lower CSC) with the reference's
+    pattern; `assemble(sigma)` rewrites K.val from the EvalContext's buffers."""
+
+    def __init__(self, model: Model, ec: EvalContext):
+        h = C.c_void_p()
+        check(LIB.ocg_kkt_create(model._h, ec._h, C.byref(h)), "ocg_kkt_create")
+        self._h, self.ec, self.model = h, ec, model
+        d = np.zeros(7, dtype=np.int64)
+        check(LIB.ocg_kkt_dims(h, d.ctypes.data))
+        self.n_free, self.n_slack, self.ntot, self.m, self.dim, self.nnz, contra = (int(v) for v in d)
+        self.contradictory = bool(contra)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_kkt_destroy(self._h)
+            self._h = None
+
+    def pattern(self) -> tuple[np.ndarray, np.ndarray]:
+        colp, rowi = np.empty(self.dim + 1, dtype=np.int64), np.empty(self.nnz, dtype=np.int64)
+        check(LIB.ocg_kkt_pattern(self._h, colp.ctypes.data, rowi.ctypes.data))
+        return colp, rowi
+
+    def maps(self) -> dict:
+        nv, m = self.model.nvar, self.model.m_con
+        out = dict(prim_index=np.empty(nv, dtype=np.int64), slack_index=np.empty(m, dtype=np.int64),
+                   dual_index=np.empty(m, dtype=np.int64), row_slot=np.empty(m, dtype=np.int64),
+                   xlo=np.empty(nv), xhi=np.empty(nv))
+        check(LIB.ocg_kkt_maps(self._h, *[out[k].ctypes.data for k in
+                                           ("prim_index", "slack_index", "dual_index", "row_slot", "xlo", "xhi")]))
+        return out
+
+    def values(self) -> torch.Tensor:
+        """K.val copied into a tensor."""
+        ptr = LIB.ocg_kkt_values(self._h)
+        out = torch.empty(self.nnz, dtype=torch.float64, device=self.ec.device)
+        torch.cuda.current_stream().synchronize()
+        _cuda_memcpy_d2d(_ptr(out), ptr, self.nnz * 8)
+        return out
+
+    def assemble(self, sigma) -> None:
+        s = self.ec._dev(sigma)
+        check(LIB.ocg_kkt_assemble(self._h, _ptr(s), _stream()))
+        torch.cuda.current_stream().synchronize()
+
+    def matvec(self, x) -> torch.Tensor:
+        x = self.ec._dev(x)
+        y = torch.empty(self.dim, dtype=torch.float64, device=self.ec.device)
+        check(LIB.ocg_kkt_matvec(self._h, _ptr(x), _ptr(y), _stream()))
+        return y
+
+    def jt_lambda(self, lam) -> torch.Tensor:
+        lam = self.ec._dev(lam)
+        out = torch.empty(self.ntot, dtype=torch.float64, device=self.ec.device)
+        check(LIB.ocg_kkt_jt_lambda(self._h, _ptr(lam), _ptr(out), _stream()))
+        return out
+
+
+def _cuda_memcpy_d2d(dst: int, src: int, nbytes: int) -> None:
+    cudart = C.CDLL("libcudart.so.12")
+    cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+    rc = cudart.cudaMemcpy(dst, src, nbytes, 3)
+    if rc != 0:
+        raise RuntimeError(f"cudaMemcpy failed ({rc})")
