@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""bench.py — the derivative-evaluation hot path of arXiv 2510.03932's `octrans`
+on B200, in the driver's one-JSON-line contract.
+
+Step = one fused `eval_constraints_jacobian` + `eval_hessian` pass (the
+reference's EvalContext J+H node-step) over every time node of
+the configured OCP, through the C ABI (include/octgpu.h: ocg_eval_jac_hess).
+Default workload = BASELINE.json configs[1]: Goddard rocket, trapezoidal
+transcription, N = 1e5 nodes per GPU (weak scaling: N per GPU fixed, the
+problem has N x world nodes, each rank evaluates its contiguous node range).
+
+metric "jac+hess eval ns/node" (lower is better): max-over-ranks device time
+per step / total nodes. Inputs are the reference's acceptance recipe
+(acceptance_main.cpp:179-193, mt19937(20250808)); L2 is flushed (a 512 MiB
+read) before every timed step, outside the events.
+
+--impl reference: the reference's own CPU EvalContext (oracle/_ref/libref.so,
+the unmodified reference sources) with its parallel Backend on all host
+cores, same model/N/metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="goddard")
+    ap.add_argument("--N", type=int, default=100_000, help="time nodes per GPU")
+    ap.add_argument("--scheme", default="trapezoid")
+    ap.add_argument("--block", type=int, default=128)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", action="store_true",
+                    help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
+    return ap.parse_args()
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            for k in ("hbm_gbs", "hbm_GBs", "hbm"):
+                if k in d:
+                    return float(d[k]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload geometry: shard ranges and algorithmic bytes
+# ---------------------------------------------------------------------------
+
+def main_space(st: dict) -> tuple[int, int]:
+    lo, hi = None, None
+    for g in st["con_groups"] + st["obj_groups"]:
+        a, b, ends = g["range"]
+        if ends:
+            continue
+        lo = a if lo is None else min(lo, a)
+        hi = b if hi is None else max(hi, b)
+    return lo or 0, hi or 0
+
+
+def shard_of(st: dict, rank: int, world: int, n_per: int) -> tuple[int, int]:
+    lo, hi = main_space(st)
+    a = lo + rank * n_per
+    b = hi if rank == world - 1 else lo + (rank + 1) * n_per
+    return a, b
+
+
+def _is_tail(g: dict) -> bool:
+    return bool(g["range"][2]) or g.get("kind", -1) == 2
+
+
+def _count(g: dict, a: int, b: int, specials: bool) -> int:
+    lo, hi, ends = g["range"]
+    if _is_tail(g):
+        return (2 if ends else hi - lo) if specials else 0
+    return max(0, min(hi, b) - max(lo, a))
+
+
+def algorithmic_bytes(st: dict, a: int, b: int, specials: bool) -> int:
+    """8 x [x reads + lambda reads + row_scale reads + c writes + J + H] for
+    the shard's instances (SURVEY.md §8d B_node; index arrays not counted)."""
+    words = 0
+    for kind, dim, base, nodes in st["layout"]:
+        if nodes > 1:
+            words += dim * max(0, min(nodes, b + 1) - a)  # node slab incl. the one-node halo
+        elif specials:
+            words += dim * nodes
+    for g in st["con_groups"]:
+        n = _count(g, a, b, specials)
+        od = g["out_dim"]
+        words += n * (2 * od + len(g["jac"]) + len(g["hess"]) + (od if g["hess"] else 0))
+    for g in st["obj_groups"]:
+        words += _count(g, a, b, specials) * len(g["hess"])
+    return 8 * words
+
+
+def output_segments(st: dict, a: int, b: int, specials: bool) -> list[tuple[str, int, int]]:
+    """(buffer, start, count) of every COO/c segment this shard writes; adjacent
+    segments merged. Used for the end-to-end device->host copies."""
+    segs = []
+    joff = hoff = 0
+    for g in st["con_groups"]:
+        lo, hi, _ = g["range"]
+        cnt = (hi - lo) if not g["range"][2] else 2
+        nj, nh, od = len(g["jac"]), len(g["hess"]), g["out_dim"]
+        if _is_tail(g):
+            k0, k1 = (0, cnt) if specials else (0, 0)
+        else:
+            k0, k1 = max(0, max(lo, a) - lo), max(0, min(hi, b) - lo)
+        if k1 > k0:
+            segs.append(("c", g["row_base"] + k0 * od, (k1 - k0) * od))
+            segs.append(("jac", joff + k0 * nj, (k1 - k0) * nj))
+            segs.append(("hess", hoff + k0 * nh, (k1 - k0) * nh))
+        joff += cnt * nj
+        hoff += cnt * nh
+    for g in st["obj_groups"]:
+        lo, hi, ends = g["range"]
+        cnt = (hi - lo) if not ends else 2
+        nh = len(g["hess"])
+        if _is_tail(g):
+            k0, k1 = (0, cnt) if specials else (0, 0)
+        else:
+            k0, k1 = max(0, max(lo, a) - lo), max(0, min(hi, b) - lo)
+        if k1 > k0 and nh:
+            segs.append(("hess", hoff + k0 * nh, (k1 - k0) * nh))
+        hoff += cnt * nh
+    merged: list[list] = []
+    for buf, s, n in sorted((x for x in segs if x[2] > 0), key=lambda t: (t[0], t[1])):
+        if merged and merged[-1][0] == buf and merged[-1][1] + merged[-1][2] == s:
+            merged[-1][2] += n
+        else:
+            merged.append([buf, s, n])
+    return [tuple(m) for m in merged]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the reference EvalContext (oracle/_ref/libref.so)
+# ---------------------------------------------------------------------------
+
+def _ref_modules():
+    sys.path.insert(0, str(ROOT / "tests"))
+    from _oracle import RefEval, RefModel  # noqa: E402  (checker: cpu_baseline / reference arm only)
+    return RefEval, RefModel
+
+
+def cpu_reference_eval(src: str, N: int, scheme: str, budget_s: float, steps: int | None = None,
+                       warmup: int = 0) -> dict:
+    RefEval, RefModel = _ref_modules()
+    cores = os.cpu_count() or 1
+    rm = RefModel(src, N, 1 if scheme == "trapezoid" else 0)
+    x, lam = rm.synth_acceptance(20250808)
+    re = RefEval(rm, parallel=True, workers=cores)
+    for _ in range(max(warmup, 1)):
+        t1, ok = re.step_seconds(x, lam, 1)
+        assert ok, "reference evaluation failed on the synthetic point"
+    reps = steps if steps is not None else max(1, min(50, int(budget_s / max(t1, 1e-6))))
+    times = [re.step_seconds(x, lam, 1)[0] for _ in range(reps)]
+    return {"times": times, "cores": re_workers(re), "reps": reps}
+
+
+def re_workers(re) -> int:
+    from _oracle import ref_lib
+    return int(ref_lib().ref_eval_workers(re.h))
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2510_03932_b200.models import MODELS
+    src = MODELS[args.model]
+    N = args.N * args.gpus
+    r = cpu_reference_eval(src, N, args.scheme, 0.0, steps=args.steps, warmup=args.warmup)
+    t = float(np.mean(r["times"]))
+    val = t * 1e9 / N
+    line = {
+        "metric": "jac+hess eval ns/node", "value": val, "unit": "ns/node", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.model} {args.scheme} N={N} J+H eval (EvalContext::eval_constraints_jacobian"
+                               f" + eval_hessian)", "model": args.model, "N": N, "scheme": args.scheme},
+        "cpu_baseline": {"value": val, "unit": "ns/node", "cores": r["cores"], "kind": "reference",
+                         "sample": f"full workload (N={N}), {args.steps} steps after {args.warmup} warm-up, "
+                                   f"Backend::parallel x{r['cores']} workers"},
+        "e2e": {"value": val, "unit": "ns/node", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def time_eval_config(ec, xd, ld, c, flush, sink, stream, steps: int, warmup: int):
+    """Per-step CUDA events around exactly one fused J+H launch; the L2 flush
+    (a 512 MiB read) runs before each step outside the events."""
+    import torch
+    for _ in range(warmup):
+        torch.sum(flush, dim=0, out=sink)
+        ec.launch_jac_hess(xd, ld, c, stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    n0 = ec.launch_count
+    for s, e in ev:
+        torch.sum(flush, dim=0, out=sink)
+        s.record(stream)
+        ec.launch_jac_hess(xd, ld, c, stream)
+        e.record(stream)
+    stream.synchronize()
+    launches = ec.launch_count - n0
+    return [s.elapsed_time(e) * 1e-3 for s, e in ev], launches
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_03932_b200 import MODELS, EvalContext, Model
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    src = MODELS[args.model]
+    N = args.N * world
+    m = Model(src, N, args.scheme)
+    st = m.structure()
+    a, b = shard_of(st, rank, world, args.N)
+    specials = rank == 0
+    ec = EvalContext(m, device=local, block=args.block, idx_lo=a, idx_hi=b if rank < world - 1 else -1,
+                     specials=specials)
+    x, lam = m.synth_acceptance(20250808)
+    xd = torch.as_tensor(x, device=dev)
+    ld = torch.as_tensor(lam, device=dev)
+    c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
+    assert ec.eval_jac_hess(xd, ld, c), "evaluation flagged a domain error on the synthetic point"
+    flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    sink = torch.zeros((), dtype=torch.float64, device=dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # warm-up, then exactly K timed steps bracketed by barrier + synchronize
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.perf_counter()
+    times, launches = time_eval_config(ec, xd, ld, c, flush, sink, stream, args.steps, args.warmup)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall0
+    t_local = float(np.mean(times))
+    ok = ec.status(stream)
+
+    # end to end through the public API with host buffers: pinned x, lambda in;
+    # c, jac_val, hess_val segments this rank owns back to pinned host memory
+    segs = output_segments(st, a, b, specials)
+    xh = torch.as_tensor(x).pin_memory()
+    lh = torch.as_tensor(lam).pin_memory()
+    host = {"c": torch.empty(m.m_con, dtype=torch.float64).pin_memory(),
+            "jac": torch.empty(ec.jac_nnz, dtype=torch.float64).pin_memory(),
+            "hess": torch.empty(ec.hess_nnz, dtype=torch.float64).pin_memory()}
+    devbuf = {"c": c, "jac": ec.jac_val, "hess": ec.hess_val}
+    h2d = 8 * (m.nvar + m.m_con)
+    d2h = 8 * sum(n for _, _, n in segs)
+    e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        ld.copy_(lh, non_blocking=True)
+        ec.launch_jac_hess(xd, ld, c, stream)
+        for buf, s0, n in segs:
+            host[buf][s0:s0 + n].copy_(devbuf[buf][s0:s0 + n], non_blocking=True)
+
+    for _ in range(args.warmup):
+        torch.sum(flush, dim=0, out=sink)
+        e2e_step()
+    stream.synchronize()
+    e2e_t = []
+    for _ in range(e2e_steps):
+        torch.sum(flush, dim=0, out=sink)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        e2e_step()
+        e.record(stream)
+        e.synchronize()
+        e2e_t.append(s.elapsed_time(e) * 1e-3)
+    ok = ok and ec.status(stream)
+    clk = clocks.stop()
+    # a result read back must match the device copy
+    for buf, s0, n in segs[:3]:
+        assert torch.equal(host[buf][s0:s0 + n], devbuf[buf][s0:s0 + n].cpu())
+
+    t_e2e_local = float(np.mean(e2e_t))
+    tt = torch.tensor([t_local, t_e2e_local, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max, t_e2e_max, bad = (float(v) for v in tt.cpu())
+
+    nbytes = algorithmic_bytes(st, a, b, specials)
+    peak, peak_kind = peaks()
+    achieved = nbytes / t_local / 1e9
+
+    out = None
+    if rank == 0:
+        value = t_max * 1e9 / N
+        out = {
+            "metric": "jac+hess eval ns/node", "value": value, "unit": "ns/node", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.model} {args.scheme} N={N} ({args.N} nodes/GPU) fused J+H eval "
+                                   "(EvalContext::eval_constraints_jacobian + eval_hessian)",
+                       "model": args.model, "N": N, "nodes_per_gpu": args.N, "scheme": args.scheme,
+                       "parallelism": f"node-range shards x{world}", "block": ec_block(ec),
+                       "l2": "flushed (512 MiB read) before every timed step",
+                       "inputs": "acceptance recipe mt19937(20250808)"},
+            "ok": not bad,
+            "nodes_per_s": N / t_max,
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
+                         "traffic": None, "kernel": "ocg_cjh (generated per model, NVRTC sm_100a)",
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "bytes_per_node": nbytes / max(1, b - a)},
+            "e2e": {"value": t_e2e_max * 1e9 / N, "unit": "ns/node", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "ocg_eval_jac_hess via the Python EvalContext mirror; pinned host x,lambda in, "
+                            "c/jac_val/hess_val out"},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "wall_s_timed_region": wall,
+        }
+        prof = ROOT / "profiles" / "ncu_traffic.json"
+        if prof.exists():
+            try:
+                d = json.loads(prof.read_text())
+                key = f"{args.model}:{N}"
+                if key in d:
+                    out["roofline"]["traffic"] = d[key]["dram_bytes_per_launch"]
+                    out["roofline"]["traffic_source"] = d[key].get("source")
+            except Exception:
+                pass
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                r = cpu_reference_eval(src, N, args.scheme, args.cpu_seconds)
+                tc = float(np.mean(r["times"]))
+                out["cpu_baseline"] = {"value": tc * 1e9 / N, "unit": "ns/node", "cores": r["cores"],
+                                       "kind": "reference",
+                                       "sample": f"full workload (N={N}) x{r['reps']} J+H evaluations, reference "
+                                                 f"EvalContext with Backend::parallel ({r['cores']} workers)"}
+            except Exception as ex:  # the checker library is missing on this box
+                out["cpu_baseline"] = {"value": None, "unit": "ns/node", "cores": 0, "kind": "reference",
+                                       "sample": f"unavailable: {ex}"}
+        if args.secondary and world == 1:
+            out["extra"] = secondary(dev, stream, flush, sink, peak)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ec_block(ec) -> int:
+    return getattr(ec, "block", 128)
+
+
+def secondary(dev, stream, flush, sink, peak) -> list[dict]:
+    """The other eval-only configs (BASELINE.json configs[2..3]) at N=1 GPU."""
+    import torch
+
+    from paper_2510_03932_b200 import MODELS, EvalContext, Model
+    res = []
+    for name, N in (("quadrotor", 1_000_000), ("quadrotor", 100_000), ("hang_glider", 100_000),
+                    ("shuttle", 100_000)):
+        m = Model(MODELS[name], N)
+        st = m.structure()
+        ec = EvalContext(m, device=dev.index)
+        x, lam = m.synth_acceptance(20250808)
+        xd, ld = torch.as_tensor(x, device=dev), torch.as_tensor(lam, device=dev)
+        c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
+        ok = ec.eval_jac_hess(xd, ld, c)
+        ts, _ = time_eval_config(ec, xd, ld, c, flush, sink, stream, 20, 3)
+        t = float(np.mean(ts))
+        nb = algorithmic_bytes(st, *main_space(st), True)
+        res.append({"model": name, "N": N, "ok": ok, "ns_per_node": t * 1e9 / N, "us_per_step": t * 1e6,
+                    "gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak, "bytes_per_node": nb / N})
+        del ec
+    return res
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -75,7 +75,11 @@ def test_values_acceptance_recipe(name, N):
     assert ec.eval_hessian(x, lam) == ok_r
     if ok_r:
         assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} hess")
-        assert ec.max_abs_hessian() == re.max_abs_hessian()
+        # max|H| is exact over our own values and within tolerance of the
+        # reference's (the entries themselves agree to 1e-12, not bitwise)
+        mh = ec.max_abs_hessian()
+        assert mh == float(np.max(np.abs(ec.hess_val.cpu().numpy()))) if ec.hess_nnz else mh == 0.0
+        assert_close(np.array([mh]), np.array([re.max_abs_hessian()]), f"{name} max|H|")
 
 
 @pytest.mark.parametrize("N", [1000])
