@@ -240,8 +240,7 @@ def cpu_reference_eval(src: str, N: int, scheme: str, budget_s: float, steps: in
 
 
 def re_workers(re) -> int:
-    from _oracle import ref_lib
-    return int(ref_lib().ref_eval_workers(re.h))
+    return int(re.L.ref_eval_workers(re.h))
 
 
 # ---------------------------------------------------------------------------

@@ -59,6 +59,62 @@ int64_t ocg_model_grid(const ocg_model* m);
  * and lcon/ucon (m_con); any pointer may be NULL. */
 int ocg_model_arrays(const ocg_model* m, double* lvar, double* uvar, double* x_start, double* clip_lo,
                      double* clip_hi, double* lcon, double* ucon);
+/* A StructuredNlp built by another front end (the reference's own
+ * dsl::parse_ocp + transcribe::transcribe), handed over as flat arrays — the
+ * drop-in path of INTEGRATION.md. Field meanings follow
+ * /root/reference/proj/include/octrans/transcribe/nlp.hpp:36-117 and
+ * kernel/graph.hpp:35-133; node ops use the kernel::Op numbering. The
+ * structural pattern is re-derived and checked against jac/hess when given. */
+typedef struct {
+  int32_t kind;            /* ConstraintGroup::Kind: 0 dynamics, 1 path, 2 boundary (objective: ignored) */
+  int32_t n_nodes;
+  const int32_t* node_op;  /* kernel::Op */
+  const int32_t* node_a;
+  const int32_t* node_b;
+  const double* node_c;
+  int32_t n_inputs;
+  const int64_t* input_base;   /* InputAddress */
+  const int64_t* input_stride;
+  int32_t out_dim;
+  const int32_t* roots;
+  int64_t range_lo, range_hi;  /* IndexRange */
+  int32_t range_endpoints;
+  int64_t row_base;        /* constraint groups */
+  const double* lower;     /* [out_dim] constraint groups */
+  const double* upper;
+  double weight;           /* objective groups */
+  int32_t n_jac, n_hess;   /* Pattern (pairs, optional: NULL/0 = derive only) */
+  const int32_t* jac;
+  const int32_t* hess;
+  const char* label;              /* optional */
+  const char* const* input_labels; /* [n_inputs], optional */
+} ocg_group_desc;
+
+typedef struct {
+  int32_t scheme;          /* 0 euler, 1 trapezoid */
+  int64_t N;
+  int32_t n_slabs;         /* VariableLayout::slabs */
+  const int32_t* slab_kind;  /* dsl::VarKind: 0 state, 1 control, 2 variable */
+  const int32_t* slab_dim;
+  const int64_t* slab_base;
+  const int64_t* slab_nodes;
+  int64_t nvar, m_con;
+  const double* lvar;      /* [nvar] */
+  const double* uvar;
+  const double* x_start;
+  const double* clip_lo;   /* [nvar], may be NULL */
+  const double* clip_hi;
+  const double* lcon;      /* [m_con] */
+  const double* ucon;
+  int32_t maximize;
+  int32_t n_con_groups;
+  const ocg_group_desc* con_groups;
+  int32_t n_obj_groups;
+  const ocg_group_desc* obj_groups;
+} ocg_nlp_desc;
+
+int ocg_model_create_from_nlp(const ocg_nlp_desc* d, ocg_model** out);
+
 /* Graphs, patterns, ranges, layout as JSON (caller frees with ocg_free). */
 char* ocg_model_structure_json(const ocg_model* m);
 /* Synthetic inputs with libstdc++'s mt19937 (reference recipes):
@@ -75,6 +131,9 @@ typedef struct {
   int64_t idx_lo;   /* shard: first main grid index (0 with idx_hi = -1: whole grid) */
   int64_t idx_hi;   /* shard: one past the last main grid index, -1 = all */
   int specials;     /* evaluate the endpoint-pair instances on this shard (1 = yes) */
+  int min_blocks;   /* resident blocks per SM the kernels are register-budgeted for
+                       (__launch_bounds__); 0 = auto: the largest budget <= 6 that the
+                       shared memory allows and that compiles without spills */
 } ocg_eval_options;
 
 void ocg_eval_default_options(ocg_eval_options* o);
@@ -126,6 +185,9 @@ int64_t ocg_eval_launch_count(const ocg_eval* e);
  */
 char* ocg_debug_generated_source(const ocg_model* m, int fma, int block);
 int ocg_debug_compile(const ocg_model* m, int fma, int block);
+/* NVRTC/ptxas log (registers, spills per kernel) of the module an eval
+ * context with these options would load; NULL on failure (ocg_free it). */
+char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_options* opts);
 
 /* ---- Reduction + KktAssembler (eval.cpp:290-440) -------------------------- */
 int ocg_kkt_create(const ocg_model* m, ocg_eval* e, ocg_kkt** out);

@@ -87,6 +87,10 @@ char* dup_string(const std::string& s) {
 
 }  // namespace
 
+// Defined only when the harness is linked into integration/_out/libref_accel.so
+// (the drop-in build): releases the device state of finished solves.
+extern "C" void octrans_accel_release_all() __attribute__((weak));
+
 extern "C" {
 
 void ref_free(void* p) { std::free(p); }
@@ -107,6 +111,9 @@ void* ref_model_create(const char* src, int scheme, int64_t N, int boxes_as_boun
 }
 
 void ref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
+
+// the StructuredNlp itself (for the drop-in build's descriptor checks)
+const void* ref_model_nlp_ptr(void* h) { return &static_cast<RefModel*>(h)->nlp; }
 
 int64_t ref_model_nvar(void* h) { return static_cast<RefModel*>(h)->nlp.nvar(); }
 int64_t ref_model_mcon(void* h) { return static_cast<RefModel*>(h)->nlp.m_con; }
@@ -353,6 +360,7 @@ int ref_solve(void* model, int parallel, int workers, int max_iter, double tol, 
   if (max_iter > 0) opts.max_iter = max_iter;
   if (tol > 0) opts.tol = tol;
   auto sol = ipm::solve(m->nlp, opts, be);
+  if (octrans_accel_release_all) octrans_accel_release_all();
   out[0] = sol.objective;
   out[1] = sol.iterations;
   out[2] = sol.stats.time_total;

@@ -17,14 +17,14 @@ OCG_BUF_JAC, OCG_BUF_HESS, OCG_BUF_GRAD, OCG_BUF_ROWSCALE, OCG_BUF_OBJV = range(
 # every symbol include/octgpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "ocg_last_error", "ocg_free", "ocg_version",
-    "ocg_model_create", "ocg_model_destroy", "ocg_model_nvar", "ocg_model_mcon", "ocg_model_grid",
+    "ocg_model_create", "ocg_model_create_from_nlp", "ocg_model_destroy", "ocg_model_nvar", "ocg_model_mcon", "ocg_model_grid",
     "ocg_model_arrays", "ocg_model_structure_json", "ocg_model_synth_acceptance", "ocg_synth_uniform",
     "ocg_eval_default_options", "ocg_eval_create", "ocg_eval_destroy", "ocg_eval_sizes", "ocg_eval_structure",
     "ocg_eval_buffer", "ocg_eval_bind_buffer", "ocg_eval_set_scaling", "ocg_eval_get_scaling", "ocg_eval_compute_scaling",
     "ocg_eval_constraints", "ocg_eval_constraints_jacobian", "ocg_eval_objective", "ocg_eval_gradient",
     "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_max_abs_hessian", "ocg_eval_status",
     "ocg_eval_launch_count",
-    "ocg_debug_generated_source", "ocg_debug_compile",
+    "ocg_debug_generated_source", "ocg_debug_compile", "ocg_debug_compile_log",
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
 ]
@@ -32,7 +32,7 @@ EXPORTS = [
 
 class EvalOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("fma", C.c_int), ("block", C.c_int), ("idx_lo", C.c_int64),
-                ("idx_hi", C.c_int64), ("specials", C.c_int)]
+                ("idx_hi", C.c_int64), ("specials", C.c_int), ("min_blocks", C.c_int)]
 
 
 class OcgError(RuntimeError):
@@ -50,6 +50,7 @@ def _load() -> C.CDLL:
         "ocg_free": (None, [vp]),
         "ocg_version": (C.c_char_p, []),
         "ocg_model_create": (i32, [C.c_char_p, i32, i64, i32, C.POINTER(vp)]),
+        "ocg_model_create_from_nlp": (i32, [vp, C.POINTER(vp)]),
         "ocg_model_destroy": (None, [vp]),
         "ocg_model_nvar": (i64, [vp]),
         "ocg_model_mcon": (i64, [vp]),
@@ -79,6 +80,7 @@ def _load() -> C.CDLL:
         "ocg_eval_launch_count": (i64, [vp]),
         "ocg_debug_generated_source": (vp, [vp, i32, i32]),
         "ocg_debug_compile": (i32, [vp, i32, i32]),
+        "ocg_debug_compile_log": (vp, [vp, C.POINTER(EvalOptions)]),
         "ocg_kkt_create": (i32, [vp, vp, C.POINTER(vp)]),
         "ocg_kkt_destroy": (None, [vp]),
         "ocg_kkt_dims": (i32, [vp, dp]),

@@ -12,7 +12,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <stdexcept>
 #include <numeric>
 #include <random>
 #include <string>
@@ -112,6 +114,7 @@ struct ocg_eval {
   DBuf<int32_t> gg_idx;
 
   int64_t launches = 0;
+  std::map<std::string, int> min_blocks;  // register budget the kernels were compiled for
 
   // tail instances this shard runs for kernel `name`
   Index n_spec(const char* name) const { return specials ? tail.at(name) : 0; }
@@ -193,6 +196,94 @@ void host_structure(const ocg::Nlp& nlp, std::vector<Index>* jr, std::vector<Ind
   }
 }
 
+const char* const kKernelNames[] = {"ocg_c", "ocg_cjac", "ocg_hess", "ocg_cjh", "ocg_objv", "ocg_grad"};
+
+// per-kernel (registers, spill-store bytes) from the ptxas -v part of an NVRTC log
+std::map<std::string, std::pair<int, int>> ptxas_stats(const std::string& log) {
+  std::map<std::string, std::pair<int, int>> out;
+  std::string cur;
+  size_t pos = 0;
+  while (pos < log.size()) {
+    size_t eol = log.find('\n', pos);
+    if (eol == std::string::npos) eol = log.size();
+    const std::string ln = log.substr(pos, eol - pos);
+    pos = eol + 1;
+    size_t a = ln.find("entry function '");
+    if (a != std::string::npos) {
+      a += 16;
+      cur = ln.substr(a, ln.find('\'', a) - a);
+      continue;
+    }
+    a = ln.find("Function properties for ");
+    if (a != std::string::npos) {  // also device functions (e.g. libdevice slow paths)
+      cur = ln.substr(a + 24);
+      while (!cur.empty() && (cur.back() == ' ' || cur.back() == '\r')) cur.pop_back();
+      continue;
+    }
+    if (cur.empty()) continue;
+    a = ln.find("bytes spill stores");
+    if (a != std::string::npos) {
+      size_t b = ln.rfind(',', a);
+      b = b == std::string::npos ? ln.find(':') + 1 : b + 1;
+      out[cur].second = std::atoi(ln.c_str() + b);
+    }
+    a = ln.find("Used ");
+    if (a != std::string::npos) out[cur].first = std::atoi(ln.c_str() + a + 5);
+  }
+  return out;
+}
+
+// Code generation + NVRTC with a register budget per kernel: each kernel is
+// compiled for `target` resident blocks per SM (capped by what its shared
+// memory allows), stepping the budget down for kernels whose code would spill.
+ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, ocg::GenOptions go, int target,
+                                 int smem_per_sm, int smem_per_block_max, std::string* log_out) {
+  ocg::Generated gen = ocg::generate(nlp, lay, go);
+  auto max_smem = [](const ocg::Generated& g) {
+    int mx = 0;
+    for (const auto& kv : g.smem) mx = std::max(mx, kv.second);
+    return mx;
+  };
+  // shared memory per block scales with warps per block: halve the block
+  // until every kernel fits the per-block limit
+  while (max_smem(gen) > smem_per_block_max && go.block > 32) {
+    go.block /= 2;
+    gen = ocg::generate(nlp, lay, go);
+  }
+  if (max_smem(gen) > smem_per_block_max)
+    throw std::runtime_error("model needs more shared memory per warp than one block provides");
+  for (const char* k : kKernelNames) {
+    const int sm = gen.smem.at(k) + 1024;  // + per-block reservation
+    const int by_smem = std::max(1, smem_per_sm / std::max(sm, 1));
+    const int by_threads = std::max(1, 2048 / go.block);
+    go.min_blocks[k] = std::max(1, std::min({target, by_smem, by_threads}));
+  }
+  for (int it = 0; it < 8; ++it) {
+    gen = ocg::generate(nlp, lay, go);
+    std::string cubin, log;
+    ocg::jit_compile_only(gen.source, go.fma, cubin, &log);
+    if (log_out) *log_out = log;
+    bool changed = false;
+    for (const auto& [name, st] : ptxas_stats(log)) {
+      auto f = go.min_blocks.find(name);
+      if (st.second > 0 && f != go.min_blocks.end() && f->second > 1) {
+        f->second -= 1;
+        changed = true;
+      }
+    }
+    if (!changed) break;
+  }
+  gen.min_blocks = go.min_blocks;
+  gen.block = go.block;
+  return gen;
+}
+
+int auto_min_blocks(const ocg_eval_options& o) {
+  if (o.min_blocks > 0) return o.min_blocks;
+  if (const char* e = std::getenv("OCG_MINB")) return std::max(1, std::atoi(e));
+  return 6;
+}
+
 }  // namespace
 
 extern "C" {
@@ -214,6 +305,84 @@ int ocg_model_create(const char* source, int scheme, int64_t N, int boxes_as_bou
     return OCG_OK;
   } catch (const ocg::ParseError& e) {
     return fail(OCG_ERR_PARSE, e.what());
+  } catch (const std::exception& e) {
+    return fail(OCG_ERR_ARG, e.what());
+  }
+}
+
+int ocg_model_create_from_nlp(const ocg_nlp_desc* d, ocg_model** out) {
+  if (!d || !out) return fail(OCG_ERR_ARG, "null argument");
+  try {
+    auto m = std::make_unique<ocg_model>();
+    ocg::Nlp& nlp = m->nlp;
+    nlp.scheme = d->scheme == 0 ? ocg::Scheme::euler : ocg::Scheme::trapezoid;
+    nlp.N = d->N;
+    nlp.nvar = d->nvar;
+    nlp.m_con = d->m_con;
+    nlp.maximize = d->maximize != 0;
+    for (int s = 0; s < d->n_slabs; ++s) {
+      ocg::Slab sl;
+      sl.kind = static_cast<ocg::VarKind>(d->slab_kind[s]);
+      sl.dim = d->slab_dim[s];
+      sl.base = d->slab_base[s];
+      sl.nodes = d->slab_nodes[s];
+      nlp.slabs.push_back(sl);
+    }
+    const auto nv = static_cast<size_t>(d->nvar), mc = static_cast<size_t>(d->m_con);
+    auto vec = [](const double* p, size_t n, double fill) {
+      return p ? std::vector<double>(p, p + n) : std::vector<double>(n, fill);
+    };
+    nlp.lvar = vec(d->lvar, nv, -INFINITY);
+    nlp.uvar = vec(d->uvar, nv, INFINITY);
+    nlp.x_start = vec(d->x_start, nv, 0.0);
+    nlp.clip_lo = d->clip_lo ? vec(d->clip_lo, nv, 0.0) : nlp.lvar;
+    nlp.clip_hi = d->clip_hi ? vec(d->clip_hi, nv, 0.0) : nlp.uvar;
+    nlp.lcon = vec(d->lcon, mc, 0.0);
+    nlp.ucon = vec(d->ucon, mc, 0.0);
+    auto group = [](const ocg_group_desc& gd, bool objective) {
+      ocg::Group g;
+      g.kind = static_cast<ocg::Group::Kind>(objective ? 1 : gd.kind);
+      for (int i = 0; i < gd.n_inputs; ++i)
+        g.kernel.graph.append_raw_input({gd.input_base[i], gd.input_stride[i]},
+                                        gd.input_labels && gd.input_labels[i] ? gd.input_labels[i] : "");
+      if (gd.label) g.label = gd.label;
+      for (int k = 0; k < gd.n_nodes; ++k) {
+        ocg::Node n;
+        n.op = static_cast<ocg::Op>(gd.node_op[k]);
+        n.a = gd.node_a[k];
+        n.b = gd.node_b[k];
+        n.c = gd.node_c[k];
+        if (n.op > ocg::Op::pow || n.a >= (n.op == ocg::Op::input ? gd.n_inputs : k) || n.b >= k)
+          throw std::invalid_argument("group graph is not a topologically ordered kernel::Graph");
+        g.kernel.graph.append_raw(n);
+      }
+      for (int r = 0; r < gd.out_dim; ++r) g.kernel.roots.push_back(gd.roots[r]);
+      g.pattern = ocg::sparsity_of(g.kernel);
+      if (gd.jac) {
+        bool same = static_cast<size_t>(gd.n_jac) == g.pattern.jac.size();
+        for (int e = 0; same && e < gd.n_jac; ++e)
+          same = g.pattern.jac[static_cast<size_t>(e)] == std::pair<int, int>(gd.jac[2 * e], gd.jac[2 * e + 1]);
+        if (!same) throw std::invalid_argument("Jacobian pattern differs from the graph's structural pattern");
+      }
+      if (gd.hess) {
+        bool same = static_cast<size_t>(gd.n_hess) == g.pattern.hess.size();
+        for (int e = 0; same && e < gd.n_hess; ++e)
+          same = g.pattern.hess[static_cast<size_t>(e)] == std::pair<int, int>(gd.hess[2 * e], gd.hess[2 * e + 1]);
+        if (!same) throw std::invalid_argument("Hessian pattern differs from the graph's structural pattern");
+      }
+      g.range.lo = gd.range_lo;
+      g.range.hi = gd.range_hi;
+      g.range.endpoints = gd.range_endpoints != 0;
+      g.row_base = gd.row_base;
+      if (!objective && gd.lower) g.lower.assign(gd.lower, gd.lower + gd.out_dim);
+      if (!objective && gd.upper) g.upper.assign(gd.upper, gd.upper + gd.out_dim);
+      g.weight = gd.weight;
+      return g;
+    };
+    for (int i = 0; i < d->n_con_groups; ++i) nlp.cons.push_back(group(d->con_groups[i], false));
+    for (int i = 0; i < d->n_obj_groups; ++i) nlp.objs.push_back(group(d->obj_groups[i], true));
+    *out = m.release();
+    return OCG_OK;
   } catch (const std::exception& e) {
     return fail(OCG_ERR_ARG, e.what());
   }
@@ -294,6 +463,7 @@ void ocg_eval_default_options(ocg_eval_options* o) {
   o->idx_lo = 0;
   o->idx_hi = -1;
   o->specials = 1;
+  o->min_blocks = 0;
 }
 
 int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval** out) {
@@ -322,21 +492,12 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     ocg::GenOptions go;
     go.fma = o.fma != 0;
     go.block = e->block;
-    ocg::Generated gen = ocg::generate(nlp, e->lay, go);
-    // shared memory per block scales with warps per block: halve the block
-    // until every kernel fits the 227 KB per-block limit
-    auto max_smem = [](const ocg::Generated& g) {
-      int mx = 0;
-      for (const auto& kv : g.smem) mx = std::max(mx, kv.second);
-      return mx;
-    };
-    while (max_smem(gen) > prop.sharedMemPerBlockOptin && go.block > 32) {
-      go.block /= 2;
-      gen = ocg::generate(nlp, e->lay, go);
-    }
-    if (max_smem(gen) > static_cast<int>(prop.sharedMemPerBlockOptin))
-      return fail(OCG_ERR_JIT, "model needs more shared memory per warp than one block provides");
+    ocg::Generated gen =
+        generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), static_cast<int>(prop.sharedMemPerMultiprocessor),
+                          static_cast<int>(prop.sharedMemPerBlockOptin), nullptr);
+    go.block = gen.block;
     e->block = go.block;
+    e->min_blocks = gen.min_blocks;
     e->slices = gen.slices;
     e->tail = gen.tail;
     e->smem = gen.smem;
@@ -906,6 +1067,34 @@ extern "C" char* ocg_debug_generated_source(const ocg_model* m, int fma, int blo
   char* out = static_cast<char*>(std::malloc(s.size() + 1));
   std::memcpy(out, s.c_str(), s.size() + 1);
   return out;
+}
+
+extern "C" char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_options* opts) {
+  if (!m) {
+    fail(OCG_ERR_ARG, "null model");
+    return nullptr;
+  }
+  try {
+    ocg_eval_options o;
+    ocg_eval_default_options(&o);
+    if (opts) o = *opts;
+    ocg::GenOptions go;
+    go.fma = o.fma != 0;
+    go.block = o.block > 0 ? o.block : 128;
+    std::string log;
+    // B200: 228 KB shared memory per SM, 227 KB per block (opt-in)
+    const ocg::Generated gen =
+        generate_budgeted(m->nlp, ocg::make_layout(m->nlp), go, auto_min_blocks(o), 233472, 232448, &log);
+    std::string s = log + "\n// min_blocks:";
+    for (const auto& [k, v] : gen.min_blocks) s += " " + k + "=" + std::to_string(v);
+    s += " block=" + std::to_string(gen.block) + "\n";
+    char* out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return out;
+  } catch (const std::exception& ex) {
+    fail(OCG_ERR_JIT, ex.what());
+    return nullptr;
+  }
 }
 
 extern "C" int ocg_debug_compile(const ocg_model* m, int fma, int block) {

@@ -173,6 +173,13 @@ class Emitter {
   V div(V a, V b) {
     if (b.one()) return a;
     if (a.is_c && b.is_c) return K(a.c / b.c);
+    // division by a power of two is multiplication by its (exact) reciprocal:
+    // both round the same real number once, so the result is bit-identical
+    if (b.is_c && std::isfinite(b.c) && b.c != 0.0) {
+      int e = 0;
+      const double mant = std::frexp(b.c, &e);
+      if ((mant == 0.5 || mant == -0.5) && e > -1020 && e < 1020) return mul(a, K(1.0 / b.c));
+    }
     return emit("/" + s(a) + "," + s(b), s(a) + " / " + s(b));
   }
   V neg(V a) {
@@ -288,6 +295,32 @@ class Generator {
     os << "__device__ __forceinline__ double ocg_pow2(double a) { return a * a; }\n";
     os << "__device__ __forceinline__ double ocg_powm1(double a) { return 1.0 / a; }\n";
     os << "__device__ __forceinline__ double ocg_pow05(double a) { return sqrt(a); }\n";
+    os << "#endif\n";
+    // 8-byte asynchronous global->shared copies (LDGSTS): a tile's loads are
+    // all in flight together and need no registers
+    os << "#ifndef OCG_HOST\n";
+    os << "__device__ __forceinline__ void ocg_cp8(double* s, const double* g) {\n"
+          "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" :: \"r\"((unsigned)__cvta_generic_to_shared(s)), \"l\"(g) : \"memory\");\n}\n";
+    os << "__device__ __forceinline__ void ocg_cp_wait() { asm volatile(\"cp.async.wait_all;\\n\" ::: \"memory\"); }\n";
+    // TMA bulk copy-out (cp.async.bulk shared::cta -> global, SASS UBLKCP):
+    // an 8-byte head/tail goes by plain stores so the bulk part is 16-byte
+    // aligned and a multiple of 16 bytes
+    os << R"(__device__ __forceinline__ int ocg_shift(const double* g, const double* s) {
+  return (int)((((unsigned long long)g) ^ ((unsigned long long)s)) >> 3) & 1;
+}
+__device__ __forceinline__ void ocg_fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void ocg_bulk_store(double* g, const double* s, int n) {
+  if (n <= 0) return;
+  if (((unsigned long long)g) & 15ull) { *g = *s; ++g; ++s; --n; }
+  if (n & 1) { g[n - 1] = s[n - 1]; --n; }
+  if (n > 0)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                 :: "l"(g), "r"((unsigned)__cvta_generic_to_shared(s)), "r"(n * 8) : "memory");
+}
+__device__ __forceinline__ void ocg_bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void ocg_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+)";
     os << "#endif\n\n";
     os << kernels;
     out.source = os.str();
@@ -305,7 +338,15 @@ class Generator {
   // entry); empty string = global memory
   std::function<std::string(const Addr&)> load_from_;
   std::function<std::string(int, Index)> store_to_;
+  // staged row inputs of the current group: what 0 = row_scale, 1 = lambda;
+  // empty string = global memory
+  std::function<std::string(int, int)> row_from_;
   Index smem_out_ = 0;  // dynamic shared memory (bytes) of the last kernel
+  // finiteness accumulator the checks of the code being emitted go to
+  std::string acc_ = "okacc";
+  // emitted right before the first shared-memory store of the current group
+  // (waits until the previous group's bulk copy-out has read the region)
+  std::string before_first_store_;
 
   // Grid-size-dependent integers live in a by-value parameter block keyed by
   // their meaning, so the generated source — and its cached cubin — depends
@@ -416,8 +457,28 @@ class Generator {
     }
     return "(" + base + " + " + i64(node * sl.dim + comp) + " + " + i64(sl.dim) + " * " + idx + ")";
   }
+  // Nodes whose value does not depend on the grid index: constants, absolute
+  // (stride-0) inputs such as a free final time, and operations on those.
+  // Their forward values and partials are hoisted out of the tile loop.
+  static std::vector<char> invariant_nodes(const Graph& gr) {
+    const auto& nodes = gr.nodes();
+    std::vector<char> inv(nodes.size(), 0);
+    for (size_t k = 0; k < nodes.size(); ++k) {
+      const Node& nd = nodes[k];
+      if (nd.op == Op::cnst)
+        inv[k] = 1;
+      else if (nd.op == Op::input)
+        inv[k] = gr.inputs()[static_cast<size_t>(nd.a)].stride == 0;
+      else if (nd.op == Op::index)
+        inv[k] = 0;
+      else
+        inv[k] = inv[static_cast<size_t>(nd.a)] && (nd.b < 0 || inv[static_cast<size_t>(nd.b)]);
+    }
+    return inv;
+  }
+
   Fwd forward(Emitter& E, const Group& g, const std::string& idx, bool clamp, bool partials, int owner,
-              std::vector<Check>& checks) {
+              std::vector<Check>& checks, const std::vector<char>* only = nullptr) {
     const auto& nodes = g.kernel.graph.nodes();
     const auto& ins = g.kernel.graph.inputs();
     Fwd f;
@@ -426,6 +487,7 @@ class Generator {
     f.p1.assign(nodes.size(), K(0.0));
     f.p2.assign(nodes.size(), K(0.0));
     for (size_t k = 0; k < nodes.size(); ++k) {
+      if (only && !(*only)[k]) continue;
       const Node& nd = nodes[k];
       V r, q1 = K(0.0), q2 = K(0.0);
       bool check_q = false;
@@ -516,6 +578,7 @@ class Generator {
       f.v[k] = r;
       f.p1[k] = q1;
       f.p2[k] = q2;
+      if (only) continue;  // hoisting pass: the group's own pass emits the checks
       if (!r.is_c && need[k]) checks.push_back({{owner}, r});
       if (partials && check_q) {
         if (!q1.is_c) checks.push_back({{owner}, q1});
@@ -625,7 +688,9 @@ class Generator {
           case Op::pow: {
             const V s = E.mul(K(nd.c * (nd.c - 1.0)), E.powc(f.v[ia], nd.c - 2.0));
             p1d = E.mul(s, dv[ia]);
-            if (!ak.zero() && !s.is_c) E.line("ok = ok & (fin(" + E.s(s) + ") | (" + E.s(ak) + " == 0.0));");
+            if (!ak.zero() && !s.is_c)
+              E.line(acc_ + " = (fin(" + E.s(s) + ") | (" + E.s(ak) + " == 0.0)) ? " + acc_ +
+                     " : __longlong_as_double(0x7ff8000000000000LL);");
             break;
           }
           default: break;
@@ -648,7 +713,7 @@ class Generator {
 
   // finiteness: one DFMA per checked value (v*0 is NaN iff v is not finite)
   void check_inline(Emitter& E, V v) {
-    if (!v.is_c) E.line("okacc = __fma_rn(" + E.s(v) + ", 0.0, okacc);");
+    if (!v.is_c) E.line(acc_ + " = __fma_rn(" + E.s(v) + ", 0.0, " + acc_ + ");");
   }
 
   static std::string i64(Index v) { return std::to_string(v) + "LL"; }
@@ -664,12 +729,19 @@ class Generator {
     std::vector<V> rsv(static_cast<size_t>(od));
     auto rowscale = [&](int r) {
       V& v = rsv[static_cast<size_t>(r)];
-      if (v.id < 0) v = E.emit("rs" + row_expr(r), "__ldg(rs + " + row_expr(r) + ")");
+      if (v.id < 0) {
+        const std::string st = row_from_ ? row_from_(0, r) : std::string();
+        v = st.empty() ? E.emit("rs" + row_expr(r), "__ldg(rs + " + row_expr(r) + ")") : E.emit("ld" + st, st);
+      }
       return v;
     };
     // store target: staged shared memory when the kernel stages, else global
     auto lv = [&](int kind, Index e, const std::string& global) {
       const std::string s = store_to_ ? store_to_(kind, e) : std::string();
+      if (!s.empty() && !before_first_store_.empty()) {
+        E.line(before_first_store_);
+        before_first_store_.clear();
+      }
       return s.empty() ? global : s;
     };
     if (p.values) {
@@ -710,7 +782,9 @@ class Generator {
         w[0] = E.emit("ow" + std::to_string(gi), "__ldg(objw + " + std::to_string(gi) + ")");
       } else {
         for (int r = 0; r < od; ++r) {
-          const V lam = E.emit("lam" + row_expr(r), "__ldg(lam + " + row_expr(r) + ")");
+          const std::string st = row_from_ ? row_from_(1, r) : std::string();
+          const V lam = st.empty() ? E.emit("lam" + row_expr(r), "__ldg(lam + " + row_expr(r) + ")")
+                                   : E.emit("ld" + st, st);
           w[static_cast<size_t>(r)] = E.mul(lam, rowscale(r));
         }
       }
@@ -779,6 +853,28 @@ class Generator {
       u.soff = cur;
       cur += (W + u.max_off) * nlp_.slabs[s].dim;
     }
+    // row inputs of the member groups (row_scale, lambda): the warp's 32
+    // instances read one contiguous segment of rows per group, staged with the
+    // node slabs so that a tile waits for global memory once
+    struct Rows {
+      Index rs = -1, lam = -1;  // shared-memory offsets, -1 = not read
+    };
+    std::vector<Rows> rows(members.size());
+    for (size_t q = 0; q < members.size(); ++q) {
+      const Inst& mb = members[q];
+      if (mb.objective) continue;
+      const Group& g = nlp_.cons[static_cast<size_t>(mb.gi)];
+      const Parts p = parts(m, false, g);
+      const Index od = g.out_dim();
+      if (p.values || p.jac || p.hess) {
+        rows[q].rs = cur;
+        cur += W * od;
+      }
+      if (p.hess) {
+        rows[q].lam = cur;
+        cur += W * od;
+      }
+    }
     // output rows: one region reused by every group (warp-synchronous)
     struct Out {
       int kind;
@@ -795,9 +891,9 @@ class Generator {
       Index off = cur;
       auto add_out = [&](int kind, Index per_k, const std::string& dst) {
         if (per_k <= 0) return;
-        const Index pitch = per_k;  // unpadded: the copy-out is a plain linear copy
+        const Index pitch = per_k;  // unpadded: the copy-out is one linear bulk copy
         outs[q].push_back({kind, per_k, pitch, off, dst});
-        off += W * pitch;
+        off += W * pitch + 2;  // + slack for the 16-byte alignment shift
       };
       if (p.values) add_out(0, g.out_dim(), "cout + " + G(false, mb.gi, "row_base", g.row_base));
       if (p.jac)
@@ -811,24 +907,38 @@ class Generator {
                                           : G(false, mb.gi, "hess_off", lay_.hess_off_con[gi])));
       region = std::max(region, off - cur);
     }
-    const Index per_warp = cur + region;  // doubles of shared memory per warp
+    Index per_warp = cur + region;  // doubles of shared memory per warp
+    per_warp += per_warp & 1;       // keep every warp's base 16-byte aligned (bulk copies)
 
     Emitter E;
     E.depth = 0;
-    E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK) " + std::string(name) +
+    const auto mb_it = opt_.min_blocks.find(name);
+    const int minb = mb_it == opt_.min_blocks.end() ? 1 : std::max(1, mb_it->second);
+    E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK, " + std::to_string(minb) + ") " + std::string(name) +
            "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec) {");
     E.depth = 1;
-    E.line("extern __shared__ double smem_all[];");
+    E.line("extern __shared__ __align__(16) double smem_all[];");
     E.line("const int lane = threadIdx.x & 31;");
     E.line("double* __restrict__ smem = smem_all + (threadIdx.x >> 5) * " + i64(per_warp) + ";");
     E.line("double okacc = 0.0;  // fma(v, 0, acc) turns NaN iff some checked v is not finite");
     E.line("bool ok = true;");
     E.line("const long long ntiles = (n_main + 31) / 32;");
     E.line("const long long wpb = OCG_BLOCK / 32;");
+    // loop invariants (free variables such as tf and everything computed from
+    // them alone) once per thread, before the tile loop
+    {
+      std::vector<Check> none;
+      for (const Inst& mb : members) {
+        const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+        const std::vector<char> inv = invariant_nodes(g.kernel.graph);
+        forward(E, g, "idx", false, parts(m, mb.objective, g).partials, 0, none, &inv);
+      }
+    }
     E.open("for (long long tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb)");
     E.line("const long long ib = i0 + tile * 32;");
     E.line("const long long idx = ib + lane;");
     E.line("const bool in = idx < i0 + n_main;");
+    // stage every global input of the tile with asynchronous copies, then wait once
     for (auto& [s, u] : uses) {
       const Slab& sl = nlp_.slabs[s];
       const Index n = (W + u.max_off) * sl.dim;
@@ -836,9 +946,35 @@ class Generator {
       const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
       E.line("{ const long long gb = " + sb + " + ib * " + i64(sl.dim) + "; long long nv = " + se +
              " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) +
-             "; for (int j = lane; j < (int)nv; j += 32) smem[" + i64(u.soff) + " + j] = __ldg(x + gb + j); }");
+             "; for (int j = lane; j < (int)nv; j += 32) ocg_cp8(smem + " + i64(u.soff) + " + j, x + gb + j); }");
     }
-    if (!uses.empty()) E.line("__syncwarp();");
+    bool staged_any = !uses.empty();
+    for (size_t q = 0; q < members.size(); ++q) {
+      if (rows[q].rs < 0 && rows[q].lam < 0) continue;
+      const Inst& mb = members[q];
+      const Group& g = nlp_.cons[static_cast<size_t>(mb.gi)];
+      const std::string lo = G(false, mb.gi, "lo", g.range.lo);
+      const std::string hi = G(false, mb.gi, "hi", g.range.hi);
+      const std::string rb = G(false, mb.gi, "row_base", g.row_base);
+      const std::string od = i64(g.out_dim());
+      E.open("");
+      E.line("const long long kb = ib - " + lo + ";");
+      E.line("const long long k0 = kb > 0 ? kb : 0;");
+      E.line("long long k1 = kb + 32; if (k1 > " + hi + " - " + lo + ") k1 = " + hi + " - " + lo +
+             "; if (k1 > i0 + n_main - " + lo + ") k1 = i0 + n_main - " + lo + ";");
+      E.line("const int nr = k1 > k0 ? (int)((k1 - k0) * " + od + ") : 0, so = (int)((k0 - kb) * " + od + ");");
+      E.line("const long long g0 = " + rb + " + k0 * " + od + ";");
+      if (rows[q].rs >= 0)
+        E.line("for (int j = lane; j < nr; j += 32) ocg_cp8(smem + " + i64(rows[q].rs) + " + so + j, rs + g0 + j);");
+      if (rows[q].lam >= 0)
+        E.line("for (int j = lane; j < nr; j += 32) ocg_cp8(smem + " + i64(rows[q].lam) + " + so + j, lam + g0 + j);");
+      E.close();
+      staged_any = true;
+    }
+    if (staged_any) {
+      E.line("ocg_cp_wait();");
+      E.line("__syncwarp();");
+    }
     load_from_ = [&](const Addr& a) -> std::string {
       if (a.stride == 0) return "";
       Index node = 0, comp = 0;
@@ -853,42 +989,76 @@ class Generator {
       const Parts p = parts(m, mb.objective, g);
       const std::string lo = G(mb.objective, mb.gi, "lo", g.range.lo);
       const std::string hi = G(mb.objective, mb.gi, "hi", g.range.hi);
+      // this tile's slice of the group: instances [k0, k1), lanes r0..r0+nk-1;
+      // each output kind's rows start at a shift of 0 or 1 double so that the
+      // shared-memory source and the global destination agree modulo 16 bytes
+      const std::string qn = std::to_string(q);
+      if (!outs[q].empty()) {
+        E.line("const long long kb" + qn + " = ib - " + lo + ";");
+        E.line("const long long k0" + qn + " = kb" + qn + " > 0 ? kb" + qn + " : 0;");
+        E.line("long long k1" + qn + " = kb" + qn + " + 32; if (k1" + qn + " > " + hi + " - " + lo + ") k1" + qn +
+               " = " + hi + " - " + lo + "; if (k1" + qn + " > i0 + n_main - " + lo + ") k1" + qn +
+               " = i0 + n_main - " + lo + ";");
+        E.line("const int nk" + qn + " = k1" + qn + " > k0" + qn + " ? (int)(k1" + qn + " - k0" + qn + ") : 0, r0" +
+               qn + " = (int)(k0" + qn + " - kb" + qn + ");");
+        for (size_t oi = 0; oi < outs[q].size(); ++oi) {
+          const Out& o = outs[q][oi];
+          const std::string S = i64(o.per_k);
+          E.line("const int sh" + qn + "_" + std::to_string(oi) + " = ocg_shift(" + o.dst + " + k0" + qn + " * " + S +
+                 ", smem + " + i64(o.soff) + " + r0" + qn + " * " + S + ");");
+        }
+        before_first_store_ = "if (lane == 0) ocg_bulk_wait_read(); __syncwarp();";
+      }
       store_to_ = [&](int kind, Index e) -> std::string {
-        for (const Out& o : outs[q])
-          if (o.kind == kind) return "smem[" + i64(o.soff + e) + " + lane * " + i64(o.pitch) + "]";
+        for (size_t oi = 0; oi < outs[q].size(); ++oi) {
+          const Out& o = outs[q][oi];
+          if (o.kind == kind)
+            return "smem[" + i64(o.soff + e) + " + sh" + qn + "_" + std::to_string(oi) + " + lane * " + i64(o.pitch) +
+                   "]";
+        }
         return "";
       };
+      row_from_ = [&](int what, int r) -> std::string {
+        const Index off = what == 0 ? rows[q].rs : rows[q].lam;
+        if (off < 0) return "";
+        return "smem[" + i64(off + r) + " + lane * " + i64(g.out_dim()) + "]";
+      };
+      // Every lane evaluates every member group in one scope (so common
+      // subexpressions are shared across groups) and stores its rows to
+      // shared memory unconditionally; lanes outside the group's range write
+      // rows the copy-out skips, and only the finiteness verdict is predicated.
+      const std::string qs = std::to_string(q);
       E.line("// ---- " + std::string(mb.objective ? "objective" : "constraint") + " group " +
              std::to_string(mb.gi) + ": " + g.label);
-      E.open("if (in && idx >= " + lo + " && idx < " + hi + ")");
-      E.line("const long long k = idx - " + lo + ";");
+      E.line("const bool p" + qs + " = in && idx >= " + lo + " && idx < " + hi + ";");
+      E.line("double okg" + qs + " = 0.0;");
+      acc_ = "okg" + qs;
       std::vector<Check> sc;
       Fwd f = forward(E, g, "idx", false, p.partials, 0, sc);
       for (const auto& c : sc) check_inline(E, c.v);
-      group_body(E, m, mb.objective, mb.gi, f, "k");
-      E.close();
+      group_body(E, m, mb.objective, mb.gi, f, "(idx - " + lo + ")");
+      E.line("if (p" + qs + ") okacc += okg" + qs + ";");
+      acc_ = "okacc";
       store_to_ = nullptr;
+      row_from_ = nullptr;
+      before_first_store_.clear();
       if (outs[q].empty()) continue;
-      E.line("__syncwarp();");
-      E.open("");
-      E.line("const long long kb = ib - " + lo + ";");
-      E.line("const long long k0 = kb > 0 ? kb : 0;");
-      E.line("long long k1 = kb + 32; if (k1 > " + hi + " - " + lo + ") k1 = " + hi + " - " + lo +
-             "; if (k1 > i0 + n_main - " + lo + ") k1 = i0 + n_main - " + lo + ";");
-      E.line("const int nk = (int)(k1 - k0), r0 = (int)(k0 - kb);");
-      for (const Out& o : outs[q]) {
-        const std::string S = std::to_string(o.per_k);
-        // rows are unpadded (pitch == per_k): the warp's segment is contiguous
-        // in shared memory and in the COO array
-        E.line("{ double* __restrict__ dst = " + o.dst + " + k0 * " + S + "LL; const double* src = smem + " +
-               i64(o.soff) + " + r0 * " + S + "; for (int j = lane; j < nk * " + S +
-               "; j += 32) dst[j] = src[j]; }");
+      // rows are unpadded (pitch == per_k): the tile's segment of each output
+      // is contiguous in shared memory and in the COO array -> one bulk copy
+      E.line("ocg_fence_async(); __syncwarp();");
+      E.open("if (lane == 0 && nk" + qn + " > 0)");
+      for (size_t oi = 0; oi < outs[q].size(); ++oi) {
+        const Out& o = outs[q][oi];
+        const std::string S = i64(o.per_k);
+        E.line("ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
+               std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn + " * (int)" + S + ");");
       }
+      E.line("ocg_bulk_commit();");
       E.close();
-      E.line("__syncwarp();");
     }
     load_from_ = nullptr;
     E.close();  // tile loop
+    E.line("if (lane == 0) ocg_bulk_wait_all();  // bulk copies done before the block exits");
 
     if (!tails.empty()) {
       E.open("if (blockIdx.x == gridDim.x - 1)");

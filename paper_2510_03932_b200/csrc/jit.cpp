@@ -66,8 +66,8 @@ cudaKernel_t JitModule::kernel(const char* name) const {
 
 void jit_compile_only(const std::string& source, bool fma, std::string& cubin, std::string* logp) {
   const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-default-device", fma ? "--fmad=true" : "--fmad=false",
-                        "-lineinfo", "--extra-device-vectorization"};
-  const int nopt = 6;
+                        "-lineinfo", "--extra-device-vectorization", "--ptxas-options=-v"};
+  const int nopt = 7;
   std::string key;
   for (int i = 0; i < nopt; ++i) key += std::string(opts[i]) + ";";
   int nv = 0;
@@ -81,7 +81,7 @@ void jit_compile_only(const std::string& source, bool fma, std::string& cubin, s
   std::string dummy;
   std::string& outlog = logp ? *logp : dummy;
   if (!std::getenv("OCG_NO_CACHE") && read_file(path, cubin)) {
-    outlog = "cache hit " + path;
+    if (!read_file(path + ".log", outlog)) outlog = "cache hit " + path;
   } else {
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, source.c_str(), "ocg_generated.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
@@ -107,6 +107,11 @@ void jit_compile_only(const std::string& source, bool fma, std::string& cubin, s
       std::ofstream f(tmp, std::ios::binary);
       f.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
     }
+    {
+      std::ofstream f(tmp + ".log", std::ios::binary);
+      f.write(log.data(), static_cast<std::streamsize>(log.size()));
+    }
+    std::rename((tmp + ".log").c_str(), (path + ".log").c_str());
     std::rename(tmp.c_str(), path.c_str());
   }
 }

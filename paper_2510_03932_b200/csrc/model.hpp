@@ -60,6 +60,15 @@ class Graph {
   int neg(int a);
   int pow(int a, double c);
   int unary(Op op, int a);
+  // A graph handed over node for node by another front end (the reference's
+  // StructuredNlp through ocg_model_create_from_nlp): no folding, no interning.
+  // (nodes are still registered for hash-consing, so derivative graphs built
+  // on top fold exactly like the reference's)
+  void append_raw(const Node& n);
+  void append_raw_input(Addr a, const std::string& label) {
+    addrs_.push_back(a);
+    labels_.push_back(label);
+  }
 
   const std::vector<Node>& nodes() const { return nodes_; }
   const Node& at(int i) const { return nodes_[static_cast<size_t>(i)]; }

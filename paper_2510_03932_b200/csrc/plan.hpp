@@ -31,6 +31,9 @@ Layout make_layout(const Nlp& nlp);
 struct GenOptions {
   bool fma = false;  // false: no FMA contraction (bit-compatible with the x86 reference)
   int block = 128;
+  // __launch_bounds__ minimum resident blocks per SM (the register budget),
+  // per kernel name; absent = 1
+  std::map<std::string, int> min_blocks;
 };
 
 struct Generated {
@@ -43,6 +46,9 @@ struct Generated {
   std::map<std::string, int> smem;
   // values of the by-value parameter block (first kernel argument)
   std::vector<long long> params;
+  // options the module was generated with (filled by the budgeted generator)
+  std::map<std::string, int> min_blocks;
+  int block = 128;
 };
 
 // Kernel entry points in the generated module (all extern "C"):

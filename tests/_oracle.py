@@ -2,7 +2,10 @@
 
 - RefModel/RefEval/RefKkt: ctypes over oracle/_ref/libref.so, the UNMODIFIED
   reference sources compiled by oracle/Makefile plus oracle/ref_harness.cpp.
-- port: ctypes over oracle/_ref/liboracle.so, the C restatement (oracle/port).
+- The same classes over integration/_out/libref_accel.so (lib="accel"): the
+  reference's own front end, Solver and factorization linked with the drop-in
+  device evaluation layer (integration/octrans_accel.cpp) in place of
+  proj/src/ipm/eval.cpp — the product seen through the reference's API.
 """
 from __future__ import annotations
 
@@ -14,22 +17,23 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
 REF_SO = ROOT / "oracle" / "_ref" / "libref.so"
-PORT_SO = ROOT / "oracle" / "_ref" / "liboracle.so"
+ACCEL_SO = ROOT / "integration" / "_out" / "libref_accel.so"
 
-_ref = None
+_libs: dict = {}
 
 
-def ref_lib() -> C.CDLL:
-    global _ref
-    if _ref is None:
-        if not REF_SO.exists():
-            raise FileNotFoundError(f"{REF_SO} missing: run `make -C oracle` (needs /root/reference)")
-        L = C.CDLL(str(REF_SO))
+def ref_lib(which: str = "ref") -> C.CDLL:
+    if which not in _libs:
+        path = REF_SO if which == "ref" else ACCEL_SO
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing: run __graft_entry__.build() (needs /root/reference)")
+        L = C.CDLL(str(path))
         vp, i64, i32, dp = C.c_void_p, C.c_int64, C.c_int, C.c_void_p
         sig = {
             "ref_free": (None, [vp]),
             "ref_model_create": (vp, [C.c_char_p, i32, i64, i32, C.c_char_p, i32]),
             "ref_model_destroy": (None, [vp]),
+            "ref_model_nlp_ptr": (vp, [vp]),
             "ref_model_nvar": (i64, [vp]),
             "ref_model_mcon": (i64, [vp]),
             "ref_model_arrays": (None, [vp] + [dp] * 7),
@@ -60,11 +64,13 @@ def ref_lib() -> C.CDLL:
             "ref_synth_acceptance": (None, [vp, C.c_uint32, dp, dp]),
             "ref_synth_uniform": (None, [C.c_uint32, C.c_double, C.c_double, i64, dp]),
         }
+        if which == "accel":
+            sig["octrans_accel_nlp_json"] = (vp, [vp])
         for n, (r, a) in sig.items():
             f = getattr(L, n)
             f.restype, f.argtypes = r, a
-        _ref = L
-    return _ref
+        _libs[which] = L
+    return _libs[which]
 
 
 def _p(a: np.ndarray) -> int:
@@ -72,8 +78,9 @@ def _p(a: np.ndarray) -> int:
 
 
 class RefModel:
-    def __init__(self, source: str, N: int, scheme: int = 1, boxes_as_bounds: bool = False):
-        L = ref_lib()
+    def __init__(self, source: str, N: int, scheme: int = 1, boxes_as_bounds: bool = False, lib: str = "ref"):
+        self.lib = lib
+        self.L = L = ref_lib(lib)
         err = C.create_string_buffer(512)
         self.h = L.ref_model_create(source.encode(), scheme, N, int(boxes_as_bounds), err, 512)
         if not self.h:
@@ -83,10 +90,10 @@ class RefModel:
 
     def __del__(self):
         if getattr(self, "h", None):
-            ref_lib().ref_model_destroy(self.h)
+            self.L.ref_model_destroy(self.h)
 
     def structure(self) -> dict:
-        L = ref_lib()
+        L = self.L
         p = L.ref_model_json(self.h)
         s = C.cast(p, C.c_char_p).value.decode()
         L.ref_free(p)
@@ -96,18 +103,18 @@ class RefModel:
         nv, m = self.nvar, self.m_con
         out = {k: np.empty(nv) for k in ("lvar", "uvar", "x_start", "clip_lo", "clip_hi")}
         out.update({k: np.empty(m) for k in ("lcon", "ucon")})
-        ref_lib().ref_model_arrays(self.h, *[_p(out[k]) for k in
+        self.L.ref_model_arrays(self.h, *[_p(out[k]) for k in
                                              ("lvar", "uvar", "x_start", "clip_lo", "clip_hi", "lcon", "ucon")])
         return out
 
     def synth_acceptance(self, seed: int = 20250808):
         x, lam = np.empty(self.nvar), np.empty(self.m_con)
-        ref_lib().ref_synth_acceptance(self.h, seed, _p(x), _p(lam))
+        self.L.ref_synth_acceptance(self.h, seed, _p(x), _p(lam))
         return x, lam
 
     def solve(self, parallel: bool = True, workers: int = 0, max_iter: int = 0, tol: float = 0.0) -> dict:
         out = np.zeros(10)
-        st = ref_lib().ref_solve(self.h, int(parallel), workers, max_iter, tol, _p(out))
+        st = self.L.ref_solve(self.h, int(parallel), workers, max_iter, tol, _p(out))
         keys = ["objective", "iterations", "time_total", "time_derivatives", "time_factorize", "time_solve",
                 "factorizations", "kkt_nnz", "factor_nnz", "theta"]
         d = dict(zip(keys, out.tolist()))
@@ -124,88 +131,90 @@ def synth_uniform(seed: int, lo: float, hi: float, n: int) -> np.ndarray:
 class RefEval:
     def __init__(self, model: RefModel, parallel: bool = False, workers: int = 0):
         self.model = model
-        self.h = ref_lib().ref_eval_create(model.h, int(parallel), workers)
+        self.L = model.L
+        self.h = self.L.ref_eval_create(model.h, int(parallel), workers)
         s = np.zeros(3, dtype=np.int64)
-        ref_lib().ref_eval_sizes(self.h, _p(s))
+        self.L.ref_eval_sizes(self.h, _p(s))
         self.jac_nnz, self.hess_nnz, self.grad_nnz = (int(v) for v in s)
 
     def __del__(self):
         if getattr(self, "h", None):
-            ref_lib().ref_eval_destroy(self.h)
+            self.L.ref_eval_destroy(self.h)
 
     def structure(self):
         a = [np.empty(n, dtype=np.int64) for n in
              (self.jac_nnz, self.jac_nnz, self.hess_nnz, self.hess_nnz, self.grad_nnz)]
-        ref_lib().ref_eval_structure(self.h, *[_p(v) for v in a])
+        self.L.ref_eval_structure(self.h, *[_p(v) for v in a])
         return dict(zip(["jac_row", "jac_col", "hess_row", "hess_col", "grad_col"], a))
 
     def set_scaling(self, obj_scale: float, row_scale=None):
         rs = None if row_scale is None else np.ascontiguousarray(row_scale, dtype=np.float64)
-        ref_lib().ref_eval_set_scaling(self.h, obj_scale, None if rs is None else _p(rs))
+        self.L.ref_eval_set_scaling(self.h, obj_scale, None if rs is None else _p(rs))
 
     def compute_scaling(self, x0, enabled=True):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
-        ref_lib().ref_eval_compute_scaling(self.h, _p(x0), int(enabled))
+        self.L.ref_eval_compute_scaling(self.h, _p(x0), int(enabled))
         o = np.zeros(1)
         rs = np.empty(self.model.m_con)
-        ref_lib().ref_eval_get_scaling(self.h, _p(o), _p(rs))
+        self.L.ref_eval_get_scaling(self.h, _p(o), _p(rs))
         return float(o[0]), rs
 
     def constraints(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         c = np.empty(self.model.m_con)
-        ok = ref_lib().ref_eval_c(self.h, _p(x), _p(c))
+        ok = self.L.ref_eval_c(self.h, _p(x), _p(c))
         return bool(ok), c
 
     def constraints_jacobian(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         c, j = np.empty(self.model.m_con), np.empty(self.jac_nnz)
-        ok = ref_lib().ref_eval_cjac(self.h, _p(x), _p(c), _p(j))
+        ok = self.L.ref_eval_cjac(self.h, _p(x), _p(c), _p(j))
         return bool(ok), c, j
 
     def objective(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         f = np.zeros(1)
-        ok = ref_lib().ref_eval_obj(self.h, _p(x), _p(f))
+        ok = self.L.ref_eval_obj(self.h, _p(x), _p(f))
         return bool(ok), float(f[0])
 
     def gradient(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         g, gc = np.empty(self.model.nvar), np.empty(self.grad_nnz)
-        ok = ref_lib().ref_eval_grad(self.h, _p(x), _p(g), _p(gc))
+        ok = self.L.ref_eval_grad(self.h, _p(x), _p(g), _p(gc))
         return bool(ok), g, gc
 
     def hessian(self, x, lam):
         x = np.ascontiguousarray(x, dtype=np.float64)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         h = np.empty(self.hess_nnz)
-        ok = ref_lib().ref_eval_hess(self.h, _p(x), _p(lam), _p(h))
+        ok = self.L.ref_eval_hess(self.h, _p(x), _p(lam), _p(h))
         return bool(ok), h
 
     def max_abs_hessian(self) -> float:
-        return ref_lib().ref_eval_max_abs_hessian(self.h)
+        return self.L.ref_eval_max_abs_hessian(self.h)
 
     def step_seconds(self, x, lam, reps: int = 1) -> tuple[float, bool]:
         ok = np.zeros(1, dtype=np.int32)
-        t = ref_lib().ref_eval_step_seconds(self.h, _p(x), _p(lam), reps, _p(ok))
+        t = self.L.ref_eval_step_seconds(self.h, _p(x), _p(lam), reps, _p(ok))
         return t, bool(ok[0])
 
 
 class RefKkt:
     def __init__(self, ev: RefEval):
         self.ev = ev
-        self.h = ref_lib().ref_kkt_create(ev.h)
+        self.L = ev.L
+        self.h = self.L.ref_kkt_create(ev.h)
         d = np.zeros(7, dtype=np.int64)
-        ref_lib().ref_kkt_dims(self.h, _p(d))
+        self.L.ref_kkt_dims(self.h, _p(d))
         self.n_free, self.n_slack, self.ntot, self.m, self.dim, self.nnz, self.contradictory = (int(v) for v in d)
 
     def __del__(self):
         if getattr(self, "h", None):
-            ref_lib().ref_kkt_destroy(self.h)
+            self.L.ref_kkt_destroy(self.h)
 
     def pattern(self):
         colp, rowi = np.empty(self.dim + 1, dtype=np.int64), np.empty(self.nnz, dtype=np.int64)
-        ref_lib().ref_kkt_pattern(self.h, _p(colp), _p(rowi))
+        self.L.ref_kkt_pattern(self.h, _p(colp), _p(rowi))
         return colp, rowi
 
     def maps(self):
@@ -213,19 +222,19 @@ class RefKkt:
         out = dict(prim_index=np.empty(nv, dtype=np.int64), slack_index=np.empty(m, dtype=np.int64),
                    dual_index=np.empty(m, dtype=np.int64), row_slot=np.empty(m, dtype=np.int64),
                    xlo=np.empty(nv), xhi=np.empty(nv))
-        ref_lib().ref_kkt_maps(self.h, *[_p(out[k]) for k in
+        self.L.ref_kkt_maps(self.h, *[_p(out[k]) for k in
                                          ("prim_index", "slack_index", "dual_index", "row_slot", "xlo", "xhi")])
         return out
 
     def assemble(self, sigma):
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
         val = np.empty(self.nnz)
-        ref_lib().ref_kkt_assemble(self.h, _p(sigma), _p(val))
+        self.L.ref_kkt_assemble(self.h, _p(sigma), _p(val))
         return val
 
     def matvec(self, val, x):
         val = np.ascontiguousarray(val, dtype=np.float64)
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty(self.dim)
-        ref_lib().ref_kkt_matvec(self.h, _p(val), _p(x), _p(y))
+        self.L.ref_kkt_matvec(self.h, _p(val), _p(x), _p(y))
         return y

@@ -25,7 +25,8 @@ PRELUDE = r"""
 #define __device__
 #define __forceinline__ inline
 #define __global__
-#define __launch_bounds__(x)
+#define __launch_bounds__(...)
+#define OCG_HOST 1
 #define __restrict__ __restrict
 #define __shared__
 #define __syncthreads() ((void)0)
@@ -34,11 +35,21 @@ PRELUDE = r"""
 #include <vector>
 static std::barrier<>* ocg_warp_barrier = nullptr;
 #define __syncwarp() ocg_warp_barrier->arrive_and_wait()
-double smem_all[1 << 18];  // one warp (OCG_BLOCK = 32) on the host: 32 std::threads
+#define __align__(n) __attribute__((aligned(n)))
+alignas(16) double smem_all[1 << 18];  // one warp (OCG_BLOCK = 32) on the host: 32 std::threads
 struct ocg_dim3 { unsigned x, y; };
 static thread_local ocg_dim3 blockIdx, threadIdx, gridDim;
 static inline double __fma_rn(double a, double b, double c) { return std::fma(a, b, c); }
 template <class T> static inline T __ldg(const T* p) { return *p; }
+// asynchronous copies complete immediately on the host
+static inline void ocg_cp8(double* s, const double* g) { *s = *g; }
+static inline void ocg_cp_wait() {}
+static inline int ocg_shift(const double* g, const double* s) { return (int)((((unsigned long long)g) ^ ((unsigned long long)s)) >> 3) & 1; }
+static inline void ocg_fence_async() {}
+static inline void ocg_bulk_store(double* g, const double* s, int n) { for (int i = 0; i < n; ++i) g[i] = s[i]; }
+static inline void ocg_bulk_commit() {}
+static inline void ocg_bulk_wait_read() {}
+static inline void ocg_bulk_wait_all() {}
 static inline double __longlong_as_double(long long v) { double d; std::memcpy(&d, &v, 8); return d; }
 // the reference evaluates sin and cos separately with glibc
 static inline void ocg_sincos(double a, double* s, double* c) { *s = std::sin(a); *c = std::cos(a); }
