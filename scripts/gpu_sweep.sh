@@ -1,9 +1,9 @@
 #!/bin/bash
-# usage: scripts/gpu_sweep.sh TAG MINB_LIST
+# usage: scripts/gpu_sweep.sh TAG MINB_LIST [pytest-args]
 T=${1:-sweep}
 MB=${2:-0}
 O=gpurun_out
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -q -x > $O/${T}_gputests.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q ${3:-} > $O/${T}_gputests.txt 2>&1
 timeout 1200 python scripts/sweep_eval.py --minb $MB > $O/${T}_sweep.jsonl 2> $O/${T}_sweep.err
 echo done
