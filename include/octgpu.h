@@ -134,6 +134,8 @@ typedef struct {
   int min_blocks;   /* resident blocks per SM the kernels are register-budgeted for
                        (__launch_bounds__); 0 = auto: the largest budget <= 6 that the
                        shared memory allows and that compiles without spills */
+  int split_kinds;  /* stage each output kind (c, J, H) of a group through one shared
+                       region: -1 = auto (when it lets more blocks reside), 0 = no, 1 = yes */
 } ocg_eval_options;
 
 void ocg_eval_default_options(ocg_eval_options* o);

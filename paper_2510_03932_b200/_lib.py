@@ -32,7 +32,8 @@ EXPORTS = [
 
 class EvalOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("fma", C.c_int), ("block", C.c_int), ("idx_lo", C.c_int64),
-                ("idx_hi", C.c_int64), ("specials", C.c_int), ("min_blocks", C.c_int)]
+                ("idx_hi", C.c_int64), ("specials", C.c_int), ("min_blocks", C.c_int),
+                ("split_kinds", C.c_int)]
 
 
 class OcgError(RuntimeError):

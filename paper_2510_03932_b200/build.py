@@ -44,7 +44,7 @@ def build(verbose: bool = False) -> Path:
     for s in HOST_SRCS:
         src, obj = CSRC / s, OUT / (Path(s).stem + ".o")
         if _stale(obj, [src] + hdrs):
-            cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-parameter",
+            cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-pthread", "-Wall", "-Wno-unused-parameter",
                    f"-I{CUDA / 'include'}", "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd))
@@ -60,7 +60,7 @@ def build(verbose: bool = False) -> Path:
             _run(cmd)
         objs.append(obj)
     if _stale(LIB, objs):
-        cmd = [cxx, "-shared", "-Wl,--exclude-libs,ALL", "-o", str(LIB)] + [str(o) for o in objs] + [
+        cmd = [cxx, "-shared", "-pthread", "-Wl,--exclude-libs,ALL", "-o", str(LIB)] + [str(o) for o in objs] + [
             f"-L{CUDA / 'lib64'}", "-lcudart", "-lnvrtc", f"-Wl,-rpath,{CUDA / 'lib64'}"]
         if verbose:
             print(" ".join(cmd))

@@ -18,6 +18,7 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/octgpu.h"
@@ -88,7 +89,7 @@ struct ocg_eval {
   const ocg_model* model = nullptr;
   int device = 0;
   ocg::Layout lay;
-  ocg::JitModule mod;
+  std::map<std::string, std::unique_ptr<ocg::JitModule>> mods;  // one module per kernel
   cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,
                k_grad = nullptr;
   int block = 128;
@@ -237,13 +238,29 @@ std::map<std::string, std::pair<int, int>> ptxas_stats(const std::string& log) {
 // compiled for `target` resident blocks per SM (capped by what its shared
 // memory allows), stepping the budget down for kernels whose code would spill.
 ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, ocg::GenOptions go, int target,
-                                 int smem_per_sm, int smem_per_block_max, std::string* log_out) {
-  ocg::Generated gen = ocg::generate(nlp, lay, go);
+                                 int split, int smem_per_sm, int smem_per_block_max, std::string* log_out,
+                                 std::map<std::string, std::string>* cubins_out = nullptr) {
   auto max_smem = [](const ocg::Generated& g) {
     int mx = 0;
     for (const auto& kv : g.smem) mx = std::max(mx, kv.second);
     return mx;
   };
+  if (const char* e = std::getenv("OCG_SPLIT")) split = std::atoi(e);
+  if (split < 0) {
+    // stage output kinds separately when that lets more blocks of the fused
+    // kernel reside (shared memory is then the occupancy limit)
+    auto blocks = [&](const ocg::Generated& g) {
+      return std::min(target, smem_per_sm / std::max(1, g.smem.at("ocg_cjh") + 1024));
+    };
+    go.split_kinds = false;
+    const int b0 = blocks(ocg::generate(nlp, lay, go));
+    go.split_kinds = true;
+    const int b1 = blocks(ocg::generate(nlp, lay, go));
+    go.split_kinds = b1 > b0;
+  } else {
+    go.split_kinds = split > 0;
+  }
+  ocg::Generated gen = ocg::generate(nlp, lay, go);
   // shared memory per block scales with warps per block: halve the block
   // until every kernel fits the per-block limit
   while (max_smem(gen) > smem_per_block_max && go.block > 32) {
@@ -258,23 +275,42 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
     const int by_threads = std::max(1, 2048 / go.block);
     go.min_blocks[k] = std::max(1, std::min({target, by_smem, by_threads}));
   }
-  for (int it = 0; it < 8; ++it) {
-    gen = ocg::generate(nlp, lay, go);
-    std::string cubin, log;
-    ocg::jit_compile_only(gen.source, go.fma, cubin, &log);
-    if (log_out) *log_out = log;
-    bool changed = false;
-    for (const auto& [name, st] : ptxas_stats(log)) {
-      auto f = go.min_blocks.find(name);
-      if (st.second > 0 && f != go.min_blocks.end() && f->second > 1) {
-        f->second -= 1;
-        changed = true;
+  // every kernel is its own compilation unit, compiled concurrently; each
+  // steps its register budget down while ptxas reports spills
+  std::map<std::string, std::string> logs;
+  std::vector<std::thread> th;
+  std::vector<std::string> errs(std::size(kKernelNames));
+  std::vector<int> mbs(std::size(kKernelNames));
+  std::vector<std::string> cubins(std::size(kKernelNames)), klogs(std::size(kKernelNames));
+  for (size_t i = 0; i < std::size(kKernelNames); ++i) {
+    mbs[i] = go.min_blocks[kKernelNames[i]];
+    th.emplace_back([&, i] {
+      try {
+        const std::string name = kKernelNames[i];
+        for (int it = 0; it < 8; ++it) {
+          const std::string src =
+              "#define OCG_MINB_" + name + " " + std::to_string(mbs[i]) + "\n" + gen.prelude + gen.kernels.at(name);
+          ocg::jit_compile_only(src, go.fma, cubins[i], &klogs[i]);
+          const auto st = ptxas_stats(klogs[i]);
+          const auto f = st.find(name);
+          if (f == st.end() || f->second.second == 0 || mbs[i] <= 1) break;
+          mbs[i] -= 1;
+        }
+      } catch (const std::exception& ex) {
+        errs[i] = ex.what();
       }
-    }
-    if (!changed) break;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (size_t i = 0; i < std::size(kKernelNames); ++i) {
+    if (!errs[i].empty()) throw std::runtime_error(errs[i]);
+    go.min_blocks[kKernelNames[i]] = mbs[i];
+    if (cubins_out) (*cubins_out)[kKernelNames[i]] = cubins[i];
+    if (log_out) *log_out += klogs[i];
   }
   gen.min_blocks = go.min_blocks;
   gen.block = go.block;
+  gen.split_kinds = go.split_kinds;
   return gen;
 }
 
@@ -464,6 +500,7 @@ void ocg_eval_default_options(ocg_eval_options* o) {
   o->idx_hi = -1;
   o->specials = 1;
   o->min_blocks = 0;
+  o->split_kinds = -1;
 }
 
 int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval** out) {
@@ -492,9 +529,11 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     ocg::GenOptions go;
     go.fma = o.fma != 0;
     go.block = e->block;
+    std::map<std::string, std::string> cubins;
     ocg::Generated gen =
-        generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), static_cast<int>(prop.sharedMemPerMultiprocessor),
-                          static_cast<int>(prop.sharedMemPerBlockOptin), nullptr);
+        generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), o.split_kinds,
+                          static_cast<int>(prop.sharedMemPerMultiprocessor),
+                          static_cast<int>(prop.sharedMemPerBlockOptin), nullptr, &cubins);
     go.block = gen.block;
     e->block = go.block;
     e->min_blocks = gen.min_blocks;
@@ -502,19 +541,27 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->tail = gen.tail;
     e->smem = gen.smem;
     e->prm = gen.params;
-    ocg::jit_compile(gen.source, go.fma, e->mod);
-    e->k_c = e->mod.kernel("ocg_c");
-    e->k_cjac = e->mod.kernel("ocg_cjac");
-    e->k_hess = e->mod.kernel("ocg_hess");
-    e->k_cjh = e->mod.kernel("ocg_cjh");
-    e->k_objv = e->mod.kernel("ocg_objv");
-    e->k_grad = e->mod.kernel("ocg_grad");
+    for (const char* k : kKernelNames) {
+      auto mod = std::make_unique<ocg::JitModule>();
+      ocg::jit_load(cubins.at(k), *mod);
+      e->mods[k] = std::move(mod);
+    }
+    e->k_c = e->mods.at("ocg_c")->kernel("ocg_c");
+    e->k_cjac = e->mods.at("ocg_cjac")->kernel("ocg_cjac");
+    e->k_hess = e->mods.at("ocg_hess")->kernel("ocg_hess");
+    e->k_cjh = e->mods.at("ocg_cjh")->kernel("ocg_cjh");
+    e->k_objv = e->mods.at("ocg_objv")->kernel("ocg_objv");
+    e->k_grad = e->mods.at("ocg_grad")->kernel("ocg_grad");
     for (auto [k, name] : {std::pair{e->k_c, "ocg_c"}, {e->k_cjac, "ocg_cjac"}, {e->k_hess, "ocg_hess"},
                            {e->k_cjh, "ocg_cjh"}, {e->k_objv, "ocg_objv"}, {e->k_grad, "ocg_grad"}}) {
       const int bytes = e->smem.at(name);
       if (bytes > 48 * 1024)
         ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
            "dynamic shared memory attribute");
+      // all of the unified L1/shared array as shared memory: blocks per SM
+      // are then limited by registers and the 228 KB, not by the carveout
+      ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+         "carveout attribute");
       int nb = 0;
       ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(k), e->block, bytes),
          "occupancy");
@@ -1053,6 +1100,7 @@ extern "C" char* ocg_debug_generated_source(const ocg_model* m, int fma, int blo
   ocg::GenOptions go;
   go.fma = fma != 0;
   go.block = block > 0 ? block : 128;
+  if (const char* e = std::getenv("OCG_SPLIT")) go.split_kinds = std::atoi(e) > 0;
   const ocg::Generated gen = ocg::generate(m->nlp, ocg::make_layout(m->nlp), go);
   std::string s = gen.source + "// ocg-meta {";
   bool first = true;
@@ -1084,10 +1132,11 @@ extern "C" char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_option
     std::string log;
     // B200: 228 KB shared memory per SM, 227 KB per block (opt-in)
     const ocg::Generated gen =
-        generate_budgeted(m->nlp, ocg::make_layout(m->nlp), go, auto_min_blocks(o), 233472, 232448, &log);
+        generate_budgeted(m->nlp, ocg::make_layout(m->nlp), go, auto_min_blocks(o), o.split_kinds, 233472, 232448,
+                          &log);
     std::string s = log + "\n// min_blocks:";
     for (const auto& [k, v] : gen.min_blocks) s += " " + k + "=" + std::to_string(v);
-    s += " block=" + std::to_string(gen.block) + "\n";
+    s += " block=" + std::to_string(gen.block) + " split_kinds=" + std::to_string(gen.split_kinds ? 1 : 0) + "\n";
     char* out = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(out, s.c_str(), s.size() + 1);
     return out;

@@ -279,7 +279,9 @@ class Generator {
     for (const KSpec& k : ks) {
       int slices = 1, tail = 0;
       smem_out_ = 0;
-      kernels += kernel(k.m, k.name, k.params, slices, tail);
+      const std::string text = kernel(k.m, k.name, k.params, slices, tail);
+      kernels += text;
+      out.kernels[k.name] = text;
       out.slices[k.name] = slices;
       out.tail[k.name] = tail;
       out.smem[k.name] = static_cast<int>(smem_out_);
@@ -322,8 +324,15 @@ __device__ __forceinline__ void ocg_bulk_wait_read() { asm volatile("cp.async.bu
 __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 )";
     os << "#endif\n\n";
+    out.prelude = os.str();
+    std::string defs;
+    for (const KSpec& k : ks) {
+      const auto f = opt_.min_blocks.find(k.name);
+      defs += "#define OCG_MINB_" + std::string(k.name) + " " +
+              std::to_string(f == opt_.min_blocks.end() ? 1 : std::max(1, f->second)) + "\n";
+    }
     os << kernels;
-    out.source = os.str();
+    out.source = defs + os.str();
     out.params.assign(pvals_.begin(), pvals_.end());
     if (out.params.empty()) out.params.push_back(0);
     return out;
@@ -344,9 +353,9 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
   Index smem_out_ = 0;  // dynamic shared memory (bytes) of the last kernel
   // finiteness accumulator the checks of the code being emitted go to
   std::string acc_ = "okacc";
-  // emitted right before the first shared-memory store of the current group
-  // (waits until the previous group's bulk copy-out has read the region)
-  std::string before_first_store_;
+  // called before every shared-memory store of the current group with the
+  // output kind: emits the waits/flushes of the staged copy-out
+  std::function<void(int)> store_hook_;
 
   // Grid-size-dependent integers live in a by-value parameter block keyed by
   // their meaning, so the generated source — and its cached cubin — depends
@@ -738,10 +747,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     // store target: staged shared memory when the kernel stages, else global
     auto lv = [&](int kind, Index e, const std::string& global) {
       const std::string s = store_to_ ? store_to_(kind, e) : std::string();
-      if (!s.empty() && !before_first_store_.empty()) {
-        E.line(before_first_store_);
-        before_first_store_.clear();
-      }
+      if (!s.empty() && store_hook_) store_hook_(kind);
       return s.empty() ? global : s;
     };
     if (p.values) {
@@ -893,7 +899,12 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         if (per_k <= 0) return;
         const Index pitch = per_k;  // unpadded: the copy-out is one linear bulk copy
         outs[q].push_back({kind, per_k, pitch, off, dst});
-        off += W * pitch + 2;  // + slack for the 16-byte alignment shift
+        // + slack for the 16-byte alignment shift; split mode: every output
+        // kind reuses one region, flushed before the next kind is staged
+        if (opt_.split_kinds)
+          region = std::max(region, W * pitch + 2);
+        else
+          off += W * pitch + 2;
       };
       if (p.values) add_out(0, g.out_dim(), "cout + " + G(false, mb.gi, "row_base", g.row_base));
       if (p.jac)
@@ -912,9 +923,10 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
 
     Emitter E;
     E.depth = 0;
-    const auto mb_it = opt_.min_blocks.find(name);
-    const int minb = mb_it == opt_.min_blocks.end() ? 1 : std::max(1, mb_it->second);
-    E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK, " + std::to_string(minb) + ") " + std::string(name) +
+    // register budget: OCG_MINB_<name> resident blocks per SM, defined per
+    // compilation (each kernel is compiled as its own module)
+    E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK, OCG_MINB_" + std::string(name) + ") " +
+           std::string(name) +
            "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec) {");
     E.depth = 1;
     E.line("extern __shared__ __align__(16) double smem_all[];");
@@ -1007,8 +1019,27 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
           E.line("const int sh" + qn + "_" + std::to_string(oi) + " = ocg_shift(" + o.dst + " + k0" + qn + " * " + S +
                  ", smem + " + i64(o.soff) + " + r0" + qn + " * " + S + ");");
         }
-        before_first_store_ = "if (lane == 0) ocg_bulk_wait_read(); __syncwarp();";
       }
+      // staged copy-out of output kind oi of this group
+      auto flush = [&, qn](size_t oi) {
+        const Out& o = outs[q][oi];
+        const std::string S = i64(o.per_k);
+        E.line("ocg_fence_async(); __syncwarp();");
+        E.line("if (lane == 0 && nk" + qn + " > 0) { ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " +
+               i64(o.soff) + " + sh" + qn + "_" + std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn +
+               " * (int)" + S + "); ocg_bulk_commit(); }");
+      };
+      int cur_kind = -2;  // -2: nothing stored yet in this group
+      store_hook_ = [&](int kind) {
+        if (kind == cur_kind) return;
+        if (opt_.split_kinds && cur_kind >= 0) {
+          for (size_t oi = 0; oi < outs[q].size(); ++oi)
+            if (outs[q][oi].kind == cur_kind) flush(oi);
+        }
+        if (cur_kind == -2 || opt_.split_kinds)  // region free again?
+          E.line("if (lane == 0) ocg_bulk_wait_read(); __syncwarp();");
+        cur_kind = kind;
+      };
       store_to_ = [&](int kind, Index e) -> std::string {
         for (size_t oi = 0; oi < outs[q].size(); ++oi) {
           const Out& o = outs[q][oi];
@@ -1041,20 +1072,25 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       acc_ = "okacc";
       store_to_ = nullptr;
       row_from_ = nullptr;
-      before_first_store_.clear();
+      store_hook_ = nullptr;
       if (outs[q].empty()) continue;
       // rows are unpadded (pitch == per_k): the tile's segment of each output
       // is contiguous in shared memory and in the COO array -> one bulk copy
-      E.line("ocg_fence_async(); __syncwarp();");
-      E.open("if (lane == 0 && nk" + qn + " > 0)");
-      for (size_t oi = 0; oi < outs[q].size(); ++oi) {
-        const Out& o = outs[q][oi];
-        const std::string S = i64(o.per_k);
-        E.line("ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
-               std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn + " * (int)" + S + ");");
+      if (opt_.split_kinds) {
+        for (size_t oi = 0; oi < outs[q].size(); ++oi)
+          if (outs[q][oi].kind == cur_kind) flush(oi);
+      } else {
+        E.line("ocg_fence_async(); __syncwarp();");
+        E.open("if (lane == 0 && nk" + qn + " > 0)");
+        for (size_t oi = 0; oi < outs[q].size(); ++oi) {
+          const Out& o = outs[q][oi];
+          const std::string S = i64(o.per_k);
+          E.line("ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
+                 std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn + " * (int)" + S + ");");
+        }
+        E.line("ocg_bulk_commit();");
+        E.close();
       }
-      E.line("ocg_bulk_commit();");
-      E.close();
     }
     load_from_ = nullptr;
     E.close();  // tile loop

@@ -11,6 +11,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <thread>
+
 namespace ocg {
 
 namespace {
@@ -91,6 +93,7 @@ void jit_compile_only(const std::string& source, bool fma, std::string& cubin, s
     nvrtcGetProgramLogSize(prog, &logn);
     std::string log(logn, '\0');
     if (logn) nvrtcGetProgramLog(prog, log.data());
+    while (!log.empty() && log.back() == '\0') log.pop_back();
     outlog = log;
     if (rc != NVRTC_SUCCESS) {
       nvrtcDestroyProgram(&prog);
@@ -102,7 +105,8 @@ void jit_compile_only(const std::string& source, bool fma, std::string& cubin, s
     nvrtcGetCUBIN(prog, cubin.data());
     nvrtcDestroyProgram(&prog);
     mkdirs(dir);
-    const std::string tmp = path + ".tmp" + std::to_string(::getpid());
+    const std::string tmp = path + ".tmp" + std::to_string(::getpid()) + "." +
+                            std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
     {
       std::ofstream f(tmp, std::ios::binary);
       f.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
@@ -116,12 +120,16 @@ void jit_compile_only(const std::string& source, bool fma, std::string& cubin, s
   }
 }
 
-void jit_compile(const std::string& source, bool fma, JitModule& out) {
-  std::string cubin;
-  jit_compile_only(source, fma, cubin, &out.log);
+void jit_load(const std::string& cubin, JitModule& out) {
   cudaError_t e = cudaLibraryLoadData(&out.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess)
     throw std::runtime_error(std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
+}
+
+void jit_compile(const std::string& source, bool fma, JitModule& out) {
+  std::string cubin;
+  jit_compile_only(source, fma, cubin, &out.log);
+  jit_load(cubin, out);
 }
 
 }  // namespace ocg

@@ -21,6 +21,9 @@ struct JitModule {
 // Throws std::runtime_error with the NVRTC log on failure.
 void jit_compile(const std::string& source, bool fma, JitModule& out);
 
+// Load an already compiled cubin.
+void jit_load(const std::string& cubin, JitModule& out);
+
 // Compile (or fetch from the cache) without loading; returns the cubin.
 void jit_compile_only(const std::string& source, bool fma, std::string& cubin, std::string* log = nullptr);
 

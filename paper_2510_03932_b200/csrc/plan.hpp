@@ -34,10 +34,16 @@ struct GenOptions {
   // __launch_bounds__ minimum resident blocks per SM (the register budget),
   // per kernel name; absent = 1
   std::map<std::string, int> min_blocks;
+  // stage one output kind (c, J, H, ...) of a group at a time through a
+  // single shared-memory region (less shared memory, more warps resident)
+  bool split_kinds = false;
 };
 
 struct Generated {
-  std::string source;
+  std::string source;  // whole module (all kernels, OCG_MINB_* defined)
+  // per-kernel compilation units: "#define OCG_MINB_<name> b" + prelude + kernels[name]
+  std::string prelude;
+  std::map<std::string, std::string> kernels;
   // kernel name -> gridDim.y it expects (1 for the merged mapping)
   std::map<std::string, int> slices;
   // kernel name -> threads of the tail (endpoint / small-range instances)
@@ -49,6 +55,7 @@ struct Generated {
   // options the module was generated with (filled by the budgeted generator)
   std::map<std::string, int> min_blocks;
   int block = 128;
+  bool split_kinds = false;
 };
 
 // Kernel entry points in the generated module (all extern "C"):

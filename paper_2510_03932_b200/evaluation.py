@@ -82,13 +82,15 @@ class EvalContext:
     as in the reference. Methods return the reference's bool."""
 
     def __init__(self, model: Model, device: int = 0, fma: bool = False, block: int = 128,
-                 idx_lo: int = 0, idx_hi: int = -1, specials: bool = True, min_blocks: int = 0):
+                 idx_lo: int = 0, idx_hi: int = -1, specials: bool = True, min_blocks: int = 0,
+                 split_kinds: int = -1):
         if not torch.cuda.is_available():
             raise RuntimeError("octgpu EvalContext needs a CUDA device (no CPU fallback)")
         self.model = model
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
-        opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials), int(min_blocks))
+        opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials), int(min_blocks),
+                                int(split_kinds))
         h = C.c_void_p()
         check(LIB.ocg_eval_create(model._h, C.byref(opts), C.byref(h)), "ocg_eval_create")
         self._h = h

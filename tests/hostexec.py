@@ -73,6 +73,8 @@ KERNELS = {
     "ocg_hess": "const double* x, const double* lam, const double* rs, const double* objw, double* hess, int* flag",
     "ocg_objv": "const double* x, double* objv, int* flag",
     "ocg_grad": "const double* x, const double* objw, double* g, int* flag",
+    "ocg_cjh": "const double* x, const double* lam, const double* rs, const double* objw, double* c, double* jac, "
+               "double* hess, int* flag",
 }
 
 
@@ -186,4 +188,8 @@ def run_all(model, x, lam, obj_scale: float = 1.0, row_scale=None):
     gv = np.zeros(max(ngrad, 1))
     out["grad_ok"] = hk._launch("ocg_grad", x, objw, gv)
     out["grad"] = gv[:ngrad]
+    # the fused c + J + H kernel
+    c2, j2, h2 = np.zeros(model.m_con), np.zeros(max(lay["jac_nnz"], 1)), np.zeros(max(lay["hess_nnz"], 1))
+    out["cjh_ok"] = hk._launch("ocg_cjh", x, lam, rs, objw, c2, j2, h2)
+    out["cjh_c"], out["cjh_jac"], out["cjh_hess"] = c2, j2[:lay["jac_nnz"]], h2[:lay["hess_nnz"]]
     return out

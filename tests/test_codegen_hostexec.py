@@ -82,3 +82,20 @@ def test_domain_flags_match_reference(name):
             assert np.array_equal(got["jac"], ref["jac"])
         if ref["hess_ok"]:
             assert np.array_equal(got["hess"], ref["hess"])
+
+
+@pytest.mark.parametrize("name", ["goddard", "quadrotor", "shuttle", "cart_pendulum"])
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_fused_kernel_bit_exact(name, split, monkeypatch):
+    """ocg_cjh (one launch for c, J and H) in both copy-out modes: every output
+    kind staged in its own shared region, or all kinds through one region."""
+    monkeypatch.setenv("OCG_SPLIT", split)
+    m = Model(MODELS[name], 70)
+    r = RefModel(MODELS[name], 70)
+    x, lam = r.synth_acceptance(99)
+    got, ref = run_all(m, x, lam), _ref_all(r, x, lam)
+    assert got["cjh_ok"] == (ref["cjac_ok"] and ref["hess_ok"])
+    assert np.array_equal(got["cjh_c"], ref["c_cjac"])
+    assert np.array_equal(got["cjh_jac"], ref["jac"])
+    assert np.array_equal(got["cjh_hess"], ref["hess"])
+
