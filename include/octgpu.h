@@ -210,6 +210,21 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s);
  * (Solver::compute_jt_lambda, solver.cpp:244-257); lambda indexed by dual ordinal */
 int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s);
 
+/* ---- KKT factorization on the device ---------------------------------------
+ * Stand-in for sparse::factorize / solve (proj/src/sparse/ldl.cpp:139-247) and
+ * for the paper's cuDSS (absent from this image): LDL^T with 1x1 pivots of
+ * P (K + diag(delta_w I_ntot, -delta_c I_m)) P^T in a node-major band-plus-
+ * border ordering, the reference's zero-pivot rule, inertia (pos, neg, zero). */
+typedef struct ocg_ldl ocg_ldl;
+int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out);
+void ocg_ldl_destroy(ocg_ldl* l);
+/* out[5] = dim, banded part, bandwidth, border size, factorizations so far */
+int ocg_ldl_info(const ocg_ldl* l, int64_t* out);
+/* factor the current K.val of `k`; inertia[3] (host, may be NULL) — synchronous when given */
+int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia, ocg_stream s);
+/* x = (K + deltas)^{-1} rhs with the last factorization (device vectors) */
+int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,7 @@ EXPORTS = [
     "ocg_debug_generated_source", "ocg_debug_compile", "ocg_debug_compile_log",
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
+    "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
 ]
 
 
@@ -91,6 +92,11 @@ def _load() -> C.CDLL:
         "ocg_kkt_assemble": (i32, [vp, dp, vp]),
         "ocg_kkt_matvec": (i32, [vp, dp, dp, vp]),
         "ocg_kkt_jt_lambda": (i32, [vp, dp, dp, vp]),
+        "ocg_ldl_create": (i32, [vp, C.POINTER(vp)]),
+        "ocg_ldl_destroy": (None, [vp]),
+        "ocg_ldl_info": (i32, [vp, dp]),
+        "ocg_ldl_factor": (i32, [vp, C.c_double, C.c_double, dp, vp]),
+        "ocg_ldl_solve": (i32, [vp, dp, dp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -23,6 +23,7 @@
 
 #include "../../include/octgpu.h"
 #include "jit.hpp"
+#include "band.hpp"
 #include "kernels.hpp"
 #include "model.hpp"
 #include "plan.hpp"
@@ -156,6 +157,18 @@ struct ocg_kkt {
   DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
   // J^T lambda
   DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
+};
+
+// Band LDL^T of the KKT matrix (band.hpp): plan + device buffers
+struct ocg_ldl {
+  ocg_kkt* kkt = nullptr;
+  ocg::BandPlan plan;
+  DBuf<int64_t> dst, perm;
+  DBuf<int8_t> primal;
+  DBuf<double> buf, Dinv, work;
+  DBuf<long long> inertia;
+  double delta_w = 0.0, delta_c = 0.0;
+  int64_t factorizations = 0;
 };
 
 namespace {
@@ -558,10 +571,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
       if (bytes > 48 * 1024)
         ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
            "dynamic shared memory attribute");
-      // all of the unified L1/shared array as shared memory: blocks per SM
-      // are then limited by registers and the 228 KB, not by the carveout
-      ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-         "carveout attribute");
+
       int nb = 0;
       ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(k), e->block, bytes),
          "occupancy");
@@ -1089,6 +1099,90 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
   ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
                       k->n_slack, out, st(s));
   k->ev->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+// ---- band LDL^T (band.hpp) ---------------------------------------------------
+
+int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
+  if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const ocg::Nlp& nlp = k->ev->model->nlp;
+  // time node of every KKT index: slots by their slab, rows by the last node
+  // their Jacobian touches; free variables (and rows touching only them) are
+  // the dense border
+  std::vector<Index> slot_node(static_cast<size_t>(nlp.nvar), -1);
+  for (const auto& sl : nlp.slabs)
+    if (sl.nodes > 1)
+      for (Index q = 0; q < sl.dim * sl.nodes; ++q) slot_node[static_cast<size_t>(sl.base + q)] = q / sl.dim;
+  std::vector<Index> jr, jc;
+  host_structure(nlp, &jr, &jc, nullptr, nullptr, nullptr);
+  std::vector<Index> row_node(static_cast<size_t>(nlp.m_con), -1);
+  for (size_t q = 0; q < jr.size(); ++q) {
+    const Index nd = slot_node[static_cast<size_t>(jc[q])];
+    auto& rn = row_node[static_cast<size_t>(jr[q])];
+    rn = std::max(rn, nd);
+  }
+  std::vector<int64_t> node(static_cast<size_t>(k->dim), -1);
+  for (Index i = 0; i < k->n_free; ++i) node[static_cast<size_t>(i)] = slot_node[static_cast<size_t>(k->free_slot[static_cast<size_t>(i)])];
+  for (Index q = 0; q < k->n_slack; ++q)
+    node[static_cast<size_t>(k->n_free + q)] = row_node[static_cast<size_t>(k->slack_of[static_cast<size_t>(q)])];
+  for (Index d = 0; d < k->m; ++d)
+    node[static_cast<size_t>(k->ntot + d)] = row_node[static_cast<size_t>(k->dual_row[static_cast<size_t>(d)])];
+  auto L = std::make_unique<ocg_ldl>();
+  L->kkt = k;
+  L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot);
+  L->dst.upload(L->plan.dst);
+  L->perm.upload(L->plan.perm);
+  L->primal.upload(L->plan.primal);
+  L->buf.alloc(static_cast<size_t>(std::max<int64_t>(1, L->plan.buf_len())));
+  L->Dinv.alloc(static_cast<size_t>(std::max<int64_t>(1, k->dim)));
+  L->work.alloc(static_cast<size_t>(std::max<int64_t>(1, k->dim)));
+  L->inertia.alloc(3);
+  *out = L.release();
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+void ocg_ldl_destroy(ocg_ldl* l) { delete l; }
+
+int ocg_ldl_info(const ocg_ldl* l, int64_t* out) {
+  if (!l || !out) return fail(OCG_ERR_ARG, "null argument");
+  out[0] = l->plan.dim;
+  out[1] = l->plan.n;
+  out[2] = l->plan.b;
+  out[3] = l->plan.w;
+  out[4] = l->factorizations;
+  return OCG_OK;
+}
+
+int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia, ocg_stream s) {
+  if (!l) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const ocg::BandPlan& P = l->plan;
+  ocg::dev::band_assemble(l->kkt->val.p, l->dst.p, static_cast<int64_t>(P.dst.size()), l->buf.p, P.buf_len(), st(s));
+  ocg::dev::band_factor(l->buf.p, l->primal.p, P.n, P.b, P.w, delta_w, delta_c, l->Dinv.p, l->inertia.p, st(s));
+  l->kkt->ev->launches += 3;
+  l->delta_w = delta_w;
+  l->delta_c = delta_c;
+  ++l->factorizations;
+  if (inertia) {
+    long long h[3];
+    ck(cudaMemcpyAsync(h, l->inertia.p, sizeof h, cudaMemcpyDeviceToHost, st(s)), "inertia d2h");
+    ck(cudaStreamSynchronize(st(s)), "sync");
+    for (int i = 0; i < 3; ++i) inertia[i] = h[i];
+  }
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
+  if (!l || !rhs || !x) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  const ocg::BandPlan& P = l->plan;
+  ocg::dev::band_solve(l->buf.p, l->Dinv.p, l->perm.p, P.n, P.b, P.w, rhs, x, l->work.p, st(s));
+  l->kkt->ev->launches += 3;
   return OCG_OK;
   OCG_GUARD_END
 }

@@ -292,3 +292,35 @@ def _cuda_memcpy_d2d(dst: int, src: int, nbytes: int) -> None:
     rc = cudart.cudaMemcpy(dst, src, nbytes, 3)
     if rc != 0:
         raise RuntimeError(f"cudaMemcpy failed ({rc})")
+
+
+class BandLdl:
+    """Device LDL^T of the KKT matrix (include/octgpu.h ocg_ldl_*): the
+    stand-in for sparse::factorize/solve and for cuDSS."""
+
+    def __init__(self, kkt: KktAssembler):
+        h = C.c_void_p()
+        check(LIB.ocg_ldl_create(kkt._h, C.byref(h)), "ocg_ldl_create")
+        self._h, self.kkt = h, kkt
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_ldl_destroy(self._h)
+            self._h = None
+
+    def info(self) -> dict:
+        o = np.zeros(5, dtype=np.int64)
+        check(LIB.ocg_ldl_info(self._h, o.ctypes.data))
+        return dict(zip(["dim", "n_band", "bandwidth", "border", "factorizations"], (int(v) for v in o)))
+
+    def factor(self, delta_w: float = 0.0, delta_c: float = 0.0) -> tuple[int, int, int]:
+        """Factor the assembled K.val; returns the inertia (positive, negative, zero)."""
+        inertia = np.zeros(3, dtype=np.int64)
+        check(LIB.ocg_ldl_factor(self._h, float(delta_w), float(delta_c), inertia.ctypes.data, _stream()))
+        return tuple(int(v) for v in inertia)
+
+    def solve(self, rhs) -> torch.Tensor:
+        r = self.kkt.ec._dev(rhs)
+        x = torch.empty_like(r)
+        check(LIB.ocg_ldl_solve(self._h, _ptr(r), _ptr(x), _stream()))
+        return x
