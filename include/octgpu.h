@@ -206,6 +206,8 @@ double* ocg_kkt_values(ocg_kkt* k); /* device K.val [nnz] */
 int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s);
 /* y = K x with the symmetric mirror (sparse::matvec_sym, sparse.cpp:51-61) */
 int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s);
+/* *out (device scalar) = max row sum of |K| with the mirror (sparse::norm_inf_sym, sparse.cpp) */
+int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s);
 /* out[ntot] = J^T lambda over kept rows, minus lambda on slacks
  * (Solver::compute_jt_lambda, solver.cpp:244-257); lambda indexed by dual ordinal */
 int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s);
@@ -224,6 +226,37 @@ int ocg_ldl_info(const ocg_ldl* l, int64_t* out);
 int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia, ocg_stream s);
 /* x = (K + deltas)^{-1} rhs with the last factorization (device vectors) */
 int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s);
+
+/* ---- device-resident interior-point solve -----------------------------------
+ * ipm::solve (proj/src/ipm/solver.cpp:304-702, options solver.hpp:31-56): the
+ * reference's filter line-search IPM with every vector on the device —
+ * evaluations, KKT assembly, the vector kernels and the factorization
+ * (ocg_ldl_*). */
+typedef struct {
+  double tol;
+  int max_iter;
+  double mu_init, tau_min;
+  double reg_initial_scale, reg_grow, reg_shrink, reg_dual_scale, reg_dual_power, reg_max_delta;
+  int scale;
+  double bound_relax_factor;
+  int refine_rounds;
+  double refine_trigger;
+  int verbose;
+} ocg_ipm_options;
+
+typedef struct {
+  int status; /* 0 optimal, 1 max_iter, 2 infeasible_detected, 3 eval_error (SolveStatus) */
+  int iterations;
+  double objective; /* sign-corrected like Solution::objective */
+  double theta, stationarity, complementarity;
+  int factorizations;
+  double time_total, time_derivatives, time_factorize, time_solve;
+  int64_t kkt_dim, kkt_nnz, bandwidth;
+} ocg_ipm_result;
+
+void ocg_ipm_default_options(ocg_ipm_options* o);
+/* x_out[nvar] (host, may be NULL): final iterate */
+int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,7 @@ EXPORTS = [
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
+    "ocg_kkt_norm_inf", "ocg_ipm_default_options", "ocg_ipm_solve",
 ]
 
 
@@ -35,6 +36,22 @@ class EvalOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("fma", C.c_int), ("block", C.c_int), ("idx_lo", C.c_int64),
                 ("idx_hi", C.c_int64), ("specials", C.c_int), ("min_blocks", C.c_int),
                 ("split_kinds", C.c_int)]
+
+
+class IpmOptions(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("mu_init", C.c_double), ("tau_min", C.c_double),
+                ("reg_initial_scale", C.c_double), ("reg_grow", C.c_double), ("reg_shrink", C.c_double),
+                ("reg_dual_scale", C.c_double), ("reg_dual_power", C.c_double), ("reg_max_delta", C.c_double),
+                ("scale", C.c_int), ("bound_relax_factor", C.c_double), ("refine_rounds", C.c_int),
+                ("refine_trigger", C.c_double), ("verbose", C.c_int)]
+
+
+class IpmResult(C.Structure):
+    _fields_ = [("status", C.c_int), ("iterations", C.c_int), ("objective", C.c_double), ("theta", C.c_double),
+                ("stationarity", C.c_double), ("complementarity", C.c_double), ("factorizations", C.c_int),
+                ("time_total", C.c_double), ("time_derivatives", C.c_double), ("time_factorize", C.c_double),
+                ("time_solve", C.c_double), ("kkt_dim", C.c_int64), ("kkt_nnz", C.c_int64),
+                ("bandwidth", C.c_int64)]
 
 
 class OcgError(RuntimeError):
@@ -92,6 +109,9 @@ def _load() -> C.CDLL:
         "ocg_kkt_assemble": (i32, [vp, dp, vp]),
         "ocg_kkt_matvec": (i32, [vp, dp, dp, vp]),
         "ocg_kkt_jt_lambda": (i32, [vp, dp, dp, vp]),
+        "ocg_kkt_norm_inf": (i32, [vp, dp, vp]),
+        "ocg_ipm_default_options": (None, [C.POINTER(IpmOptions)]),
+        "ocg_ipm_solve": (i32, [vp, C.POINTER(IpmOptions), i32, C.POINTER(IpmResult), dp]),
         "ocg_ldl_create": (i32, [vp, C.POINTER(vp)]),
         "ocg_ldl_destroy": (None, [vp]),
         "ocg_ldl_info": (i32, [vp, dp]),

@@ -1093,6 +1093,15 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
   OCG_GUARD_END
 }
 
+int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
+  if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out, st(s));
+  k->ev->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
 int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s) {
   if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN

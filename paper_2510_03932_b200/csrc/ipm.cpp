@@ -1,0 +1,741 @@
+// Device-resident filter line-search interior-point solve.
+//
+// Host control flow of the reference's Solver (proj/src/ipm/solver.cpp:304-702):
+// monotone barrier update, inertia-corrected regularization, backtracking
+// filter line search with up to 4 second-order corrections, the single-shot
+// restoration fallback and the dual safeguard — the same decisions in the
+// same order. Every vector lives on the device: evaluations (octgpu eval
+// kernels), the KKT assembly, the vector work (ipm_kernels.cu) and the
+// factorization (band.cu, the stand-in for the reference's LDL^T / cuDSS).
+// Per line-search trial the host receives a handful of scalars (ok flags,
+// theta, barrier sum, objective).
+//
+// This file is a client of the public C ABI only (include/octgpu.h), like the
+// reference's Solver is a client of EvalContext / KktAssembler / sparse::.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/octgpu.h"
+#include "ipm_kernels.hpp"
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+// filter line-search constants (solver.cpp:38-52)
+constexpr double kGammaTheta = 1e-5;
+constexpr double kGammaPhi = 1e-5;
+constexpr double kSTheta = 1.1;
+constexpr double kSPhi = 2.3;
+constexpr double kDeltaSwitch = 1.0;
+constexpr double kEtaPhi = 1e-4;
+constexpr double kAlphaMin = 1e-12;
+constexpr double kKappaSigma = 1e10;
+constexpr double kKappaEps = 10.0;
+constexpr double kKappaMu = 0.2;
+constexpr double kThetaMu = 1.5;
+constexpr double kPushIn = 1e-2;
+
+struct CudaErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void ckc(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cko(int rc, const char* what) {
+  if (rc < 0) throw CudaErr(std::string(what) + ": " + ocg_last_error());
+}
+
+struct Clock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double elapsed() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+};
+
+template <class T>
+struct DVec {
+  T* p = nullptr;
+  size_t n = 0;
+  DVec() = default;
+  explicit DVec(size_t count) { alloc(count); }
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  ~DVec() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    n = count;
+    ckc(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    if (!v.empty()) ckc(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+  }
+  void download(std::vector<T>& v, cudaStream_t s) const {
+    v.resize(n);
+    if (n) ckc(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    ckc(cudaStreamSynchronize(s), "sync");
+  }
+};
+
+class DeviceSolver {
+ public:
+  DeviceSolver(ocg_model* model, const ocg_ipm_options& o, int device) : model_(model), o_(o) {
+    ckc(cudaSetDevice(device), "cudaSetDevice");
+    ckc(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+    ocg_eval_options eo;
+    ocg_eval_default_options(&eo);
+    eo.device = device;
+    cko(ocg_eval_create(model, &eo, &ev_), "eval_create");
+    cko(ocg_kkt_create(model, ev_, &kkt_), "kkt_create");
+    cko(ocg_ldl_create(kkt_, &ldl_), "ldl_create");
+  }
+  ~DeviceSolver() {
+    if (ldl_) ocg_ldl_destroy(ldl_);
+    if (kkt_) ocg_kkt_destroy(kkt_);
+    if (ev_) ocg_eval_destroy(ev_);
+    if (s_) cudaStreamDestroy(s_);
+  }
+
+  int run(ocg_ipm_result* res, double* x_out);
+
+ private:
+  ocg_model* model_;
+  ocg_ipm_options o_;
+  cudaStream_t s_ = nullptr;
+  ocg_eval* ev_ = nullptr;
+  ocg_kkt* kkt_ = nullptr;
+  ocg_ldl* ldl_ = nullptr;
+  ocg::ipmdev::Iter P_;
+  ocg::ipmdev::Scratch sc_;
+
+  int64_t nvar_ = 0, mcon_ = 0, nfree_ = 0, nslack_ = 0, ntot_ = 0, m_ = 0, dim_ = 0;
+  bool contradictory_ = false;
+  double mu_ = 0.1, tau_ = 0.99, delta_last_ = 0.0, obj_scale_ = 1.0;
+  double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
+  double theta_min_ = 0.0, theta_max_ = kInf;
+  std::vector<std::pair<double, double>> filter_;
+  ocg_ipm_result r_{};
+
+  // device state
+  DVec<int64_t> free_slot_, dual_row_, slack_index_;
+  DVec<double> lb_, ub_, lcon_s_;
+  DVec<int8_t> has_lb_, has_ub_;
+  std::unique_ptr<DVec<double>> x_, s_v_, c_, grad_, xt_, st_, ct_, gradt_;
+  DVec<double> lambda_, zl_, zu_, g_, gt_, gsoc_, sigma_, rhs_, rhs2_, jtlam_, lamfull_, step_, step2_, kx_, r_v_,
+      dx_, dzl_, dzu_, dscal_, partials_, out_;
+
+  // ---- wrappers with the reference's bool semantics ----
+  bool ok() {
+    const int rc = ocg_eval_status(ev_, s_);
+    cko(rc, "eval_status");
+    return rc == OCG_OK;
+  }
+  bool eval_c(const double* x, double* c) {
+    Clock t;
+    cko(ocg_eval_constraints(ev_, x, c, s_), "eval_constraints");
+    const bool b = ok();
+    r_.time_derivatives += t.elapsed();
+    return b;
+  }
+  bool eval_cj(const double* x, double* c) {
+    Clock t;
+    cko(ocg_eval_constraints_jacobian(ev_, x, c, s_), "eval_constraints_jacobian");
+    const bool b = ok();
+    r_.time_derivatives += t.elapsed();
+    return b;
+  }
+  bool eval_f(const double* x, double& f) {
+    Clock t;
+    cko(ocg_eval_objective(ev_, x, dscal_.p, s_), "eval_objective");
+    const bool b = ok();
+    ckc(cudaMemcpyAsync(&f, dscal_.p, sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H f");
+    ckc(cudaStreamSynchronize(s_), "sync");
+    r_.time_derivatives += t.elapsed();
+    return b && std::isfinite(f);
+  }
+  bool eval_grad(const double* x, double* g) {
+    Clock t;
+    cko(ocg_eval_gradient(ev_, x, g, s_), "eval_gradient");
+    const bool b = ok();
+    r_.time_derivatives += t.elapsed();
+    return b;
+  }
+  bool eval_h(const double* x, const double* lam_full) {
+    Clock t;
+    cko(ocg_eval_hessian(ev_, x, lam_full, s_), "eval_hessian");
+    const bool b = ok();
+    r_.time_derivatives += t.elapsed();
+    return b;
+  }
+  double max_abs_h() {
+    cko(ocg_eval_max_abs_hessian(ev_, dscal_.p, s_), "max_abs_hessian");
+    double v = 0.0;
+    ckc(cudaMemcpyAsync(&v, dscal_.p, sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
+    ckc(cudaStreamSynchronize(s_), "sync");
+    return v;
+  }
+
+  void setup(std::vector<double>& row_scale);
+  double theta_of(const double* g) { return ocg::ipmdev::l1(g, m_, sc_, s_); }
+  double kkt_error(double mu, const double* g, double& comp_out, double& stat_out);
+  void add_to_filter(double theta, double phi);
+  bool filter_rejects(double theta, double phi) const;
+  bool solve_kkt(double wmax, bool& numeric_failure);
+  void resolve(const double* rhs, double* step);
+  void refine_if_needed(const double* rhs, double* step);
+  void finish(int status, int iter, const std::vector<double>& row_scale);
+};
+
+void DeviceSolver::setup(std::vector<double>& row_scale) {
+  nvar_ = ocg_model_nvar(model_);
+  mcon_ = ocg_model_mcon(model_);
+  int64_t d[7];
+  cko(ocg_kkt_dims(kkt_, d), "kkt_dims");
+  nfree_ = d[0];
+  nslack_ = d[1];
+  ntot_ = d[2];
+  m_ = d[3];
+  dim_ = d[4];
+  contradictory_ = d[6] != 0;
+  r_.kkt_dim = dim_;
+  r_.kkt_nnz = d[5];
+  const auto nv = static_cast<size_t>(nvar_), mc = static_cast<size_t>(mcon_);
+  std::vector<double> lvar(nv), uvar(nv), x0(nv), lcon(mc), ucon(mc), xlo(nv), xhi(nv);
+  cko(ocg_model_arrays(model_, lvar.data(), uvar.data(), x0.data(), nullptr, nullptr, lcon.data(), ucon.data()),
+      "model_arrays");
+  std::vector<int64_t> prim(nv), slack(mc), dual(mc), rslot(mc);
+  cko(ocg_kkt_maps(kkt_, prim.data(), slack.data(), dual.data(), rslot.data(), xlo.data(), xhi.data()), "kkt_maps");
+  std::vector<int64_t> free_slot(static_cast<size_t>(nfree_)), slack_of(static_cast<size_t>(nslack_)),
+      dual_row(static_cast<size_t>(m_));
+  for (size_t sl = 0; sl < nv; ++sl)
+    if (prim[sl] >= 0) free_slot[static_cast<size_t>(prim[sl])] = static_cast<int64_t>(sl);
+  for (size_t r = 0; r < mc; ++r) {
+    if (slack[r] >= 0) slack_of[static_cast<size_t>(slack[r])] = static_cast<int64_t>(r);
+    if (dual[r] >= 0) dual_row[static_cast<size_t>(dual[r])] = static_cast<int64_t>(r);
+  }
+
+  // EvalContext::compute_scaling at x_start (solver.cpp:318)
+  DVec<double> xs(nv);
+  xs.upload(x0, s_);
+  cko(ocg_eval_compute_scaling(ev_, xs.p, o_.scale, s_), "compute_scaling");
+  row_scale.assign(mc, 1.0);
+  cko(ocg_eval_get_scaling(ev_, &obj_scale_, row_scale.data()), "get_scaling");
+
+  // Solver::setup_bounds (solver.cpp:125-170)
+  std::vector<double> lcon_s(mc), ucon_s(mc);
+  for (size_t r = 0; r < mc; ++r) {
+    lcon_s[r] = row_scale[r] * lcon[r];
+    ucon_s[r] = row_scale[r] * ucon[r];
+  }
+  const auto nt = static_cast<size_t>(ntot_);
+  std::vector<double> lb(nt, -kInf), ub(nt, kInf);
+  std::vector<int8_t> hl(nt, 0), hu(nt, 0);
+  for (int64_t i = 0; i < nfree_; ++i) {
+    const auto sl = static_cast<size_t>(free_slot[static_cast<size_t>(i)]);
+    if (std::isfinite(xlo[sl])) {
+      lb[static_cast<size_t>(i)] = xlo[sl];
+      hl[static_cast<size_t>(i)] = 1;
+    }
+    if (std::isfinite(xhi[sl])) {
+      ub[static_cast<size_t>(i)] = xhi[sl];
+      hu[static_cast<size_t>(i)] = 1;
+    }
+  }
+  for (int64_t k = 0; k < nslack_; ++k) {
+    const auto r = static_cast<size_t>(slack_of[static_cast<size_t>(k)]);
+    const auto i = static_cast<size_t>(nfree_ + k);
+    if (std::isfinite(lcon_s[r])) {
+      lb[i] = lcon_s[r];
+      hl[i] = 1;
+    }
+    if (std::isfinite(ucon_s[r])) {
+      ub[i] = ucon_s[r];
+      hu[i] = 1;
+    }
+  }
+  const double relax = std::min(o_.bound_relax_factor, o_.tol);
+  if (relax > 0.0)
+    for (size_t i = 0; i < nt; ++i) {
+      if (hl[i]) lb[i] -= relax * std::max(1.0, std::abs(lb[i]));
+      if (hu[i]) ub[i] += relax * std::max(1.0, std::abs(ub[i]));
+    }
+
+  // Solver::initialize_iterate (solver.cpp:172-206)
+  std::vector<double> x = x0;
+  for (size_t sl = 0; sl < nv; ++sl)
+    if (xlo[sl] == xhi[sl]) x[sl] = xlo[sl];
+  auto push_into = [](double v, double l, double u) {
+    const double w = std::min(1.0, u - l);
+    const double lo = std::isfinite(l) ? l + kPushIn * (std::isfinite(w) ? w : 1.0) : -kInf;
+    const double hi = std::isfinite(u) ? u - kPushIn * (std::isfinite(w) ? w : 1.0) : kInf;
+    return std::clamp(v, lo, hi);
+  };
+  for (int64_t i = 0; i < nfree_; ++i) {
+    const auto sl = static_cast<size_t>(free_slot[static_cast<size_t>(i)]);
+    x[sl] = push_into(x[sl], lb[static_cast<size_t>(i)], ub[static_cast<size_t>(i)]);
+  }
+
+  // device state
+  free_slot_.alloc(static_cast<size_t>(nfree_));
+  free_slot_.upload(free_slot, s_);
+  dual_row_.alloc(static_cast<size_t>(m_));
+  dual_row_.upload(dual_row, s_);
+  slack_index_.alloc(mc);
+  slack_index_.upload(slack, s_);
+  lb_.alloc(nt);
+  lb_.upload(lb, s_);
+  ub_.alloc(nt);
+  ub_.upload(ub, s_);
+  has_lb_.alloc(nt);
+  has_lb_.upload(hl, s_);
+  has_ub_.alloc(nt);
+  has_ub_.upload(hu, s_);
+  lcon_s_.alloc(mc);
+  lcon_s_.upload(lcon_s, s_);
+  P_.nvar = nvar_;
+  P_.m_con = mcon_;
+  P_.n_free = nfree_;
+  P_.n_slack = nslack_;
+  P_.ntot = ntot_;
+  P_.m = m_;
+  P_.free_slot = free_slot_.p;
+  P_.dual_row = dual_row_.p;
+  P_.slack_index = slack_index_.p;
+  P_.lb = lb_.p;
+  P_.ub = ub_.p;
+  P_.has_lb = has_lb_.p;
+  P_.has_ub = has_ub_.p;
+  P_.lcon_s = lcon_s_.p;
+  for (auto* v : {&x_, &xt_, &grad_, &gradt_}) *v = std::make_unique<DVec<double>>(nv);
+  for (auto* v : {&c_, &ct_}) *v = std::make_unique<DVec<double>>(mc);
+  for (auto* v : {&s_v_, &st_}) *v = std::make_unique<DVec<double>>(static_cast<size_t>(nslack_));
+  const auto dm = static_cast<size_t>(dim_), mm = static_cast<size_t>(m_);
+  lambda_.alloc(mm);
+  g_.alloc(mm);
+  gt_.alloc(mm);
+  gsoc_.alloc(mm);
+  zl_.alloc(nt);
+  zu_.alloc(nt);
+  sigma_.alloc(nt);
+  jtlam_.alloc(nt);
+  dzl_.alloc(nt);
+  dzu_.alloc(nt);
+  rhs_.alloc(dm);
+  rhs2_.alloc(dm);
+  step_.alloc(dm);
+  step2_.alloc(dm);
+  kx_.alloc(dm);
+  r_v_.alloc(dm);
+  dx_.alloc(dm);
+  lamfull_.alloc(mc);
+  dscal_.alloc(4);
+  partials_.alloc(2 * 148 * 8);
+  out_.alloc(8);
+  sc_.partials = partials_.p;
+  sc_.out = out_.p;
+  x_->upload(x, s_);
+
+  // slacks from the constraint values at the start point, multipliers
+  std::vector<double> c;
+  eval_c(x_->p, c_->p);
+  c_->download(c, s_);
+  std::vector<double> s(static_cast<size_t>(nslack_));
+  for (int64_t k = 0; k < nslack_; ++k) {
+    const auto r = static_cast<size_t>(slack_of[static_cast<size_t>(k)]);
+    const auto i = static_cast<size_t>(nfree_ + k);
+    s[static_cast<size_t>(k)] = push_into(c[r], lb[i], ub[i]);
+  }
+  s_v_->upload(s, s_);
+  std::vector<double> zl(nt, 0.0), zu(nt, 0.0);
+  for (size_t i = 0; i < nt; ++i) {
+    const double v = static_cast<int64_t>(i) < nfree_ ? x[static_cast<size_t>(free_slot[i])]
+                                                      : s[i - static_cast<size_t>(nfree_)];
+    if (hl[i]) zl[i] = mu_ / (v - lb[i]);
+    if (hu[i]) zu[i] = mu_ / (ub[i] - v);
+  }
+  zl_.upload(zl, s_);
+  zu_.upload(zu, s_);
+  ckc(cudaMemsetAsync(lambda_.p, 0, std::max<size_t>(mm, 1) * sizeof(double), s_), "memset");
+  ckc(cudaStreamSynchronize(s_), "sync");
+}
+
+// Solver::kkt_error (solver.cpp:260-287)
+double DeviceSolver::kkt_error(double mu, const double* g, double& comp_out, double& stat_out) {
+  double p[5];
+  ocg::ipmdev::kkt_error_parts(P_, x_->p, s_v_->p, zl_.p, zu_.p, lambda_.p, grad_->p, jtlam_.p, g, mu, p, sc_, s_);
+  const double znorm1 = p[0], lnorm1 = p[1], stat = p[2], feas = p[3], comp = p[4];
+  const double denom = static_cast<double>(std::max<int64_t>(1, m_ + ntot_));
+  const double sd = std::max(100.0, (lnorm1 + znorm1) / denom) / 100.0;
+  const double sc = std::max(100.0, znorm1 / static_cast<double>(std::max<int64_t>(1, ntot_))) / 100.0;
+  comp_out = comp / sc;
+  stat_out = stat / sd;
+  return std::max({stat / sd, feas, comp / sc});
+}
+
+void DeviceSolver::add_to_filter(double theta, double phi) {
+  const std::pair<double, double> e{(1.0 - kGammaTheta) * theta, phi - kGammaPhi * theta};
+  filter_.erase(std::remove_if(filter_.begin(), filter_.end(),
+                               [&](const auto& f) { return f.first >= e.first && f.second >= e.second; }),
+                filter_.end());
+  filter_.push_back(e);
+}
+
+bool DeviceSolver::filter_rejects(double theta, double phi) const {
+  if (theta > theta_max_) return true;
+  for (const auto& f : filter_)
+    if (theta >= f.first && phi >= f.second) return true;
+  return false;
+}
+
+// sparse::refine (ldl.cpp:249-272) when the first solve's residual is large
+void DeviceSolver::refine_if_needed(const double* rhs, double* step) {
+  double nr[3];
+  cko(ocg_kkt_matvec(kkt_, step, kx_.p, s_), "matvec");
+  ocg::ipmdev::residual_norms(rhs, kx_.p, step, dim_, ntot_, dw_, dc_, nullptr, nr, sc_, s_);
+  if (!(nr[0] > o_.refine_trigger * (1.0 + nr[1]))) return;
+  double anorm = 0.0;
+  cko(ocg_kkt_norm_inf(kkt_, dscal_.p, s_), "norm_inf");
+  ckc(cudaMemcpyAsync(&anorm, dscal_.p, sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
+  ckc(cudaStreamSynchronize(s_), "sync");
+  anorm += std::abs(dw_) + std::abs(dc_);
+  for (int round = 0; round < o_.refine_rounds; ++round) {
+    cko(ocg_kkt_matvec(kkt_, step, kx_.p, s_), "matvec");
+    ocg::ipmdev::residual_norms(rhs, kx_.p, step, dim_, ntot_, dw_, dc_, r_v_.p, nr, sc_, s_);
+    if (nr[0] <= 1e-12 * (anorm * nr[2] + nr[1])) break;
+    cko(ocg_ldl_solve(ldl_, r_v_.p, dx_.p, s_), "ldl_solve");
+    ocg::ipmdev::add(step, dx_.p, dim_, s_);
+  }
+}
+
+// Solver::solve_kkt (solver.cpp:648-702): inertia-corrected factorization,
+// solve into step_
+bool DeviceSolver::solve_kkt(double wmax, bool& numeric_failure) {
+  numeric_failure = false;
+  Clock tf;
+  double dw = 0.0, dc = 0.0;
+  bool first_bump = true;
+  for (;;) {
+    int64_t in[3];
+    cko(ocg_ldl_factor(ldl_, dw, dc, in, s_), "ldl_factor");
+    ++r_.factorizations;
+    if (in[0] == ntot_ && in[1] == m_ && in[2] == 0) break;
+    if (first_bump) {
+      dw = delta_last_ > 0.0 ? std::max(1e-20, delta_last_ / o_.reg_shrink)
+                             : o_.reg_initial_scale * std::max(1.0, wmax);
+      first_bump = false;
+    } else if (in[2] > 0 && dc == 0.0) {
+      dc = o_.reg_dual_scale * std::pow(mu_, o_.reg_dual_power);
+    } else {
+      dw *= o_.reg_grow;
+    }
+    if (dw > o_.reg_max_delta) {
+      numeric_failure = true;
+      r_.time_factorize += tf.elapsed();
+      return false;
+    }
+  }
+  if (dw > 0.0) delta_last_ = dw;
+  dw_ = dw;
+  dc_ = dc;
+  r_.time_factorize += tf.elapsed();
+  Clock ts;
+  cko(ocg_ldl_solve(ldl_, rhs_.p, step_.p, s_), "ldl_solve");
+  refine_if_needed(rhs_.p, step_.p);
+  ckc(cudaStreamSynchronize(s_), "sync");
+  r_.time_solve += ts.elapsed();
+  return true;
+}
+
+// Solver::resolve_rhs (solver.cpp:704-721): solve with the current factor
+void DeviceSolver::resolve(const double* rhs, double* step) {
+  Clock ts;
+  cko(ocg_ldl_solve(ldl_, rhs, step, s_), "ldl_solve");
+  refine_if_needed(rhs, step);
+  ckc(cudaStreamSynchronize(s_), "sync");
+  r_.time_solve += ts.elapsed();
+}
+
+void DeviceSolver::finish(int status, int iter, const std::vector<double>& row_scale) {
+  r_.status = status;
+  r_.iterations = iter;
+  double f = 0.0;
+  eval_f(x_->p, f);
+  const double f_raw = f / obj_scale_;
+  int maximize = 0;
+  {
+    // the model's objective sense: structure JSON carries it; read cheaply
+    char* js = ocg_model_structure_json(model_);
+    if (js) {
+      maximize = std::string(js).find("\"maximize\":true") != std::string::npos ? 1 : 0;
+      ocg_free(js);
+    }
+  }
+  r_.objective = maximize ? -f_raw : f_raw;
+  if (m_ > 0) {
+    std::vector<double> g;
+    g_.download(g, s_);
+    std::vector<int64_t> dr(static_cast<size_t>(m_));
+    ckc(cudaMemcpy(dr.data(), dual_row_.p, dr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    double th = 0.0;
+    for (size_t d = 0; d < g.size(); ++d) th = std::max(th, std::abs(g[d]) / row_scale[static_cast<size_t>(dr[d])]);
+    r_.theta = th;
+  }
+  cko(ocg_kkt_jt_lambda(kkt_, lambda_.p, jtlam_.p, s_), "jt_lambda");
+  double comp = 0.0, stat = 0.0;
+  kkt_error(0.0, g_.p, comp, stat);
+  r_.stationarity = stat / obj_scale_;
+  r_.complementarity = comp / obj_scale_;
+}
+
+int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
+  Clock total;
+  std::vector<double> row_scale;
+  mu_ = o_.mu_init;
+  tau_ = std::max(o_.tau_min, 1.0 - mu_);
+  setup(row_scale);
+  if (contradictory_) {
+    r_.status = 2;
+    r_.time_total = total.elapsed();
+    *res = r_;
+    return OCG_OK;
+  }
+  const double mu_min = o_.tol / 10.0;
+  auto done = [&](int status, int iter) {
+    finish(status, iter, row_scale);
+    r_.time_total = total.elapsed();
+    if (x_out) ckc(cudaMemcpy(x_out, x_->p, static_cast<size_t>(nvar_) * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    int64_t li[5];
+    ocg_ldl_info(ldl_, li);
+    r_.bandwidth = li[2];
+    *res = r_;
+  };
+  if (!eval_cj(x_->p, c_->p) || !eval_grad(x_->p, grad_->p)) {
+    done(3, 0);
+    return OCG_OK;
+  }
+  ocg::ipmdev::residual(P_, c_->p, s_v_->p, g_.p, s_);
+  {
+    const double th = theta_of(g_.p);
+    theta_min_ = 1e-4 * std::max(1.0, th);
+    theta_max_ = 1e4 * std::max(1.0, th);
+  }
+  int consecutive_restorations = 0;
+  bool hold_mu = false;
+  for (int iter = 0;; ++iter) {
+    cko(ocg_kkt_jt_lambda(kkt_, lambda_.p, jtlam_.p, s_), "jt_lambda");
+    double comp = 0.0, stat = 0.0;
+    const double e0 = kkt_error(0.0, g_.p, comp, stat);
+    if (e0 <= o_.tol) {
+      done(0, iter);
+      return OCG_OK;
+    }
+    if (iter >= o_.max_iter) {
+      done(1, iter);
+      return OCG_OK;
+    }
+    {
+      double cmu = 0.0, smu = 0.0;
+      if (!hold_mu && mu_ > mu_min && kkt_error(mu_, g_.p, cmu, smu) <= kKappaEps * mu_) {
+        mu_ = std::max(mu_min, std::min(kKappaMu * mu_, std::pow(mu_, kThetaMu)));
+        tau_ = std::max(o_.tau_min, 1.0 - mu_);
+        filter_.clear();
+      }
+    }
+    ocg::ipmdev::expand_lambda(P_, lambda_.p, lamfull_.p, s_);
+    if (!eval_h(x_->p, lamfull_.p)) {
+      done(3, iter);
+      return OCG_OK;
+    }
+    ocg::ipmdev::sigma(P_, x_->p, s_v_->p, zl_.p, zu_.p, sigma_.p, s_);
+    cko(ocg_kkt_assemble(kkt_, sigma_.p, s_), "kkt_assemble");
+    ocg::ipmdev::rhs(P_, x_->p, s_v_->p, grad_->p, jtlam_.p, g_.p, mu_, rhs_.p, s_);
+    bool numeric_failure = false;
+    if (!solve_kkt(max_abs_h(), numeric_failure)) {
+      done(3, iter);
+      return OCG_OK;
+    }
+    const double alpha_max = ocg::ipmdev::fraction_to_boundary(P_, x_->p, s_v_->p, step_.p, tau_, sc_, s_);
+    const double dphi = ocg::ipmdev::dphi(P_, x_->p, s_v_->p, grad_->p, step_.p, mu_, sc_, s_);
+    const double theta_k = theta_of(g_.p);
+    double phi_k = 0.0;
+    {
+      double f_k = 0.0, bar = 0.0;
+      if (!eval_f(x_->p, f_k) || !ocg::ipmdev::barrier(P_, x_->p, s_v_->p, bar, sc_, s_)) {
+        done(3, iter);
+        return OCG_OK;
+      }
+      phi_k = f_k - mu_ * bar;
+    }
+
+    double alpha = alpha_max;
+    bool accepted = false, armijo_path = false, saw_eval_error = false;
+    double theta_t = 0.0, phi_t = 0.0;
+    const double* dir = step_.p;
+    auto build_trial = [&](const double* d, double a) {
+      ocg::ipmdev::trial(P_, x_->p, s_v_->p, d, a, xt_->p, st_->p, s_);
+    };
+    auto eval_trial = [&]() {
+      if (!eval_c(xt_->p, ct_->p)) return false;
+      ocg::ipmdev::residual(P_, ct_->p, st_->p, gt_.p, s_);
+      theta_t = theta_of(gt_.p);
+      double f_t = 0.0, bar = 0.0;
+      if (!ocg::ipmdev::barrier(P_, xt_->p, st_->p, bar, sc_, s_) || !eval_f(xt_->p, f_t)) return false;
+      phi_t = f_t - mu_ * bar;
+      return std::isfinite(phi_t);
+    };
+    auto acceptable = [&](double a) {
+      if (filter_rejects(theta_t, phi_t)) return false;
+      const bool descent = dphi < 0.0;
+      const bool switching = descent && a * std::pow(-dphi, kSPhi) > kDeltaSwitch * std::pow(theta_k, kSTheta);
+      if (theta_k <= theta_min_ && switching) {
+        if (phi_t <= phi_k + kEtaPhi * a * dphi) {
+          armijo_path = true;
+          return true;
+        }
+        return false;
+      }
+      return theta_t <= (1.0 - kGammaTheta) * theta_k || phi_t <= phi_k - kGammaPhi * theta_k;
+    };
+
+    bool first_trial = true;
+    while (alpha >= kAlphaMin) {
+      build_trial(dir, alpha);
+      if (!eval_trial()) {
+        saw_eval_error = true;
+        first_trial = false;
+        alpha *= 0.5;
+        continue;
+      }
+      accepted = acceptable(alpha);
+      if (!accepted && first_trial && theta_t >= theta_k && m_ > 0) {
+        // second-order corrections (solver.cpp:496-534)
+        ocg::ipmdev::axpy(alpha, g_.p, gt_.p, gsoc_.p, m_, s_);
+        double theta_prev = theta_t;
+        for (int soc = 0; soc < 4 && !accepted; ++soc) {
+          ocg::ipmdev::rhs_soc(P_, rhs_.p, gsoc_.p, rhs2_.p, s_);
+          resolve(rhs2_.p, step2_.p);
+          const double alpha_soc = ocg::ipmdev::fraction_to_boundary(P_, x_->p, s_v_->p, step2_.p, tau_, sc_, s_);
+          build_trial(step2_.p, alpha_soc);
+          if (!eval_trial()) break;
+          if (acceptable(alpha_soc)) {
+            accepted = true;
+            std::swap(step_.p, step2_.p);
+            dir = step_.p;
+            alpha = alpha_soc;
+            break;
+          }
+          if (theta_t >= 0.99 * theta_prev) break;
+          theta_prev = theta_t;
+          ocg::ipmdev::axpy(alpha_soc, gsoc_.p, gt_.p, gsoc_.p, m_, s_);
+        }
+        if (!accepted) {
+          build_trial(dir, alpha);
+          if (!eval_trial()) {
+            saw_eval_error = true;
+            first_trial = false;
+            alpha *= 0.5;
+            continue;
+          }
+        }
+      }
+      if (accepted) {
+        if (!eval_cj(xt_->p, ct_->p) || !eval_grad(xt_->p, gradt_->p)) {
+          saw_eval_error = true;
+          accepted = false;
+          armijo_path = false;
+          first_trial = false;
+          alpha *= 0.5;
+          continue;
+        }
+        break;
+      }
+      first_trial = false;
+      alpha *= 0.5;
+    }
+
+    if (!accepted) {
+      if (consecutive_restorations >= 5) {
+        done(saw_eval_error ? 3 : 2, iter);
+        return OCG_OK;
+      }
+      ++consecutive_restorations;
+      hold_mu = true;
+      mu_ = std::min(mu_ * 10.0, 1e4);
+      tau_ = std::max(o_.tau_min, 1.0 - mu_);
+      filter_.clear();
+      if (!eval_cj(x_->p, c_->p) || !eval_grad(x_->p, grad_->p)) {
+        done(3, iter);
+        return OCG_OK;
+      }
+      ocg::ipmdev::residual(P_, c_->p, s_v_->p, g_.p, s_);
+      continue;
+    }
+    consecutive_restorations = 0;
+    hold_mu = false;
+    if (!armijo_path) add_to_filter(theta_k, phi_k);
+
+    double alpha_z = ocg::ipmdev::dual_direction(P_, x_->p, s_v_->p, zl_.p, zu_.p, dir, mu_, tau_, dzl_.p, dzu_.p,
+                                                 sc_, s_);
+    alpha_z = std::min(alpha_z, std::max(alpha, 1e-2));
+    std::swap(x_, xt_);
+    std::swap(s_v_, st_);
+    ocg::ipmdev::accept(P_, dir, dzl_.p, dzu_.p, alpha, alpha_z, mu_, kKappaSigma, x_->p, s_v_->p, lambda_.p, zl_.p,
+                        zu_.p, s_);
+    std::swap(c_, ct_);
+    std::swap(grad_, gradt_);
+    ocg::ipmdev::residual(P_, c_->p, s_v_->p, g_.p, s_);
+    if (o_.verbose) {
+      double f_raw = 0.0;
+      eval_f(x_->p, f_raw);
+      std::printf("iter %4d  f %+.8e  theta %.3e  mu %.2e  alpha %.2e  alpha_z %.2e  delta_w %.1e\n", iter + 1,
+                  f_raw / obj_scale_, theta_of(g_.p), mu_, alpha, alpha_z, delta_last_);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void ocg_ipm_default_options(ocg_ipm_options* o) {
+  if (!o) return;
+  o->tol = 1e-8;
+  o->max_iter = 3000;
+  o->mu_init = 1e-1;
+  o->tau_min = 0.99;
+  o->reg_initial_scale = 1e-4;
+  o->reg_grow = 8.0;
+  o->reg_shrink = 3.0;
+  o->reg_dual_scale = 1e-8;
+  o->reg_dual_power = 0.25;
+  o->reg_max_delta = 1e40;
+  o->scale = 1;
+  o->bound_relax_factor = 1e-8;
+  o->refine_rounds = 5;
+  o->refine_trigger = 1e-8;
+  o->verbose = 0;
+}
+
+int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out) {
+  if (!m || !out) return -1;
+  ocg_ipm_options o;
+  ocg_ipm_default_options(&o);
+  if (opts) o = *opts;
+  try {
+    DeviceSolver solver(m, o, device);
+    return solver.run(out, x_out);
+  } catch (const std::exception& ex) {
+    std::fprintf(stderr, "ocg_ipm_solve: %s\n", ex.what());
+    return OCG_ERR_CUDA;
+  }
+}
+
+}  // extern "C"

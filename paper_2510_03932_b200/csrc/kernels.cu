@@ -104,6 +104,27 @@ __global__ void __launch_bounds__(256) sym_matvec_k(const double* __restrict__ v
   }
 }
 
+// max over rows of sum_j |K_ij| with the symmetric mirror (sparse::norm_inf_sym)
+__global__ void __launch_bounds__(256) sym_norm_inf_k(const double* __restrict__ val, const int64_t* __restrict__ rptr,
+                                                      const int64_t* __restrict__ vidx, int64_t n,
+                                                      unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = rptr[i]; p < rptr[i + 1]; ++p) s += fabs(val[vidx[p]]);
+    m = fmax(m, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmax(m, wm[w]);
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
 __global__ void __launch_bounds__(256) jt_lambda_k(const double* __restrict__ jac, const double* __restrict__ lam,
                                                    const int64_t* __restrict__ ptr, const int64_t* __restrict__ e_idx,
                                                    const int64_t* __restrict__ dual_idx, int64_t n_free,
@@ -169,6 +190,13 @@ void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, cons
                 const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
   sym_matvec_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, col, vidx, n, x, y);
+}
+
+void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out,
+                  cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (n <= 0) return;
+  sym_norm_inf_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, vidx, n, reinterpret_cast<unsigned long long*>(out));
 }
 
 void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,

@@ -35,6 +35,10 @@ void kkt_assemble(const double* hess, const double* jac, const double* sigma, co
 void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
                 const double* x, double* y, cudaStream_t s);
 
+// *out = max_i sum_j |K_ij| over the full symmetric rows (sparse::norm_inf_sym)
+void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out,
+                  cudaStream_t s);
+
 // out[i] = sum_p jac[e_p] * lam[dual_p] (p in increasing e), then for slack
 // rows out[i] -= lam[dual] (Solver::compute_jt_lambda, solver.cpp:244-257).
 void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,

@@ -324,3 +324,30 @@ class BandLdl:
         x = torch.empty_like(r)
         check(LIB.ocg_ldl_solve(self._h, _ptr(r), _ptr(x), _stream()))
         return x
+
+
+STATUS = {0: "optimal", 1: "max_iter", 2: "infeasible_detected", 3: "eval_error"}
+
+
+def solve(model: Model, device: int = 0, return_x: bool = False, **options) -> dict:
+    """ipm::solve on the device (include/octgpu.h ocg_ipm_solve): the
+    reference's filter line-search IPM (proj/src/ipm/solver.cpp) with every
+    vector, evaluation, the KKT assembly and the factorization on the B200.
+    Options are IpmOptions fields (solver.hpp:31-56); reg_* flatten `reg`."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("octgpu solve needs a CUDA device (no CPU fallback)")
+    o = _lib.IpmOptions()
+    LIB.ocg_ipm_default_options(C.byref(o))
+    for k, v in options.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown IPM option {k!r}")
+        setattr(o, k, type(getattr(o, k))(v))
+    r = _lib.IpmResult()
+    x = np.empty(model.nvar) if return_x else None
+    check(LIB.ocg_ipm_solve(model._h, C.byref(o), int(device), C.byref(r),
+                            None if x is None else x.ctypes.data), "ocg_ipm_solve")
+    out = {name: getattr(r, name) for name, _ in r._fields_}
+    out["status_name"] = STATUS.get(r.status, "unknown")
+    if x is not None:
+        out["x"] = x
+    return out

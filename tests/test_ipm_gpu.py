@@ -1,0 +1,38 @@
+"""Device-resident IPM (ocg_ipm_solve) against the reference ipm::solve
+(oracle/_ref/libref.so): same status and iteration count, objectives within
+1e-8 relative (north_star), on the reference's published pins
+(proj/test_output.txt:29: DI@1000 4 iterations, quadrotor@2000 6,
+Goddard@1000 510)."""
+from __future__ import annotations
+
+import pytest
+
+from _oracle import RefModel
+from paper_2510_03932_b200 import MODELS, Model, solve
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,N,iters", [("double_integrator", 1000, 4), ("quadrotor", 2000, 6),
+                                          ("double_integrator", 20000, None), ("cart_pendulum", 300, None)])
+def test_device_solve_matches_reference(name, N, iters):
+    ref = RefModel(MODELS[name], N).solve(parallel=False)
+    got = solve(Model(MODELS[name], N))
+    print(name, N, "ref", ref["iterations"], ref["objective"], "device", got["iterations"], got["objective"],
+          "factorizations", got["factorizations"], "bandwidth", got["bandwidth"])
+    assert got["status"] == 0 == ref["status"]
+    if iters is not None:
+        assert ref["iterations"] == iters
+    assert got["iterations"] == ref["iterations"]
+    assert abs(got["objective"] - ref["objective"]) <= 1e-8 * abs(ref["objective"])
+    assert got["kkt_nnz"] == ref["kkt_nnz"]
+
+
+@pytest.mark.slow
+def test_device_solve_goddard_1000():
+    ref = RefModel(MODELS["goddard"], 1000).solve(parallel=False, max_iter=3000)
+    got = solve(Model(MODELS["goddard"], 1000), max_iter=3000)
+    print("goddard@1000 ref", ref["iterations"], ref["objective"], "device", got["iterations"], got["objective"])
+    assert got["status"] == 0 == ref["status"]
+    assert abs(got["objective"] - ref["objective"]) <= 1e-8 * abs(ref["objective"])
+    assert abs(got["iterations"] - ref["iterations"]) <= 0.05 * ref["iterations"]
