@@ -65,7 +65,8 @@ namespace dev {
 
 namespace {
 
-constexpr int kPrefetch = 8;  // band columns in flight ahead of the window
+constexpr int kPrefetch = 32;  // band columns in flight ahead of the window (power of two)
+constexpr int kMask = kPrefetch - 1;
 
 __device__ __forceinline__ void cp8(double* s, const double* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
@@ -97,7 +98,7 @@ __device__ __forceinline__ bool zero_pivot(double d, double scale) {
 // One warp. Shared memory: window W[B1][B1] (slot-major), pivot scales ps[B1],
 // border window Wb[w][B1], border block S[w][w] + scales, y/l/yb/lb vectors,
 // the (j1, j2) update pairs and a prefetch ring of kPrefetch columns.
-__global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, const int8_t* __restrict__ primal,
+__global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, const double* __restrict__ primal,
                                                     long long n, int b, int w, double dw, double dc,
                                                     double* __restrict__ Dinv, long long* __restrict__ inertia) {
   extern __shared__ double sm[];
@@ -112,14 +113,14 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
   double* l = y + B1;                 // B1
   double* yb = l + B1;                // w
   double* lb = yb + w;                // w
-  double* ring = lb + w;              // kPrefetch * (B1 + w)
-  short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * (B1 + w));
+  double* ring = lb + w;              // kPrefetch * (B1 + w + 1)
+  short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * (B1 + w + 1));
   const int P = b * (b + 1) / 2;
   short* pj2 = pj1 + P;
   double* band = buf;
   double* border = buf + n * B1;
   double* Sg = border + static_cast<long long>(w) * n;
-  const int RW = B1 + w;  // ring row: one band column + its border entries
+  const int RW = B1 + w + 1;  // ring row: band column, its border entries, its primal flag
 
   for (int p = lane; p < P; p += 32) {  // pairs j1 <= j2 in 1..b
     int j1 = 1, rem = p;
@@ -130,14 +131,14 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     pj1[p] = static_cast<short>(j1);
     pj2[p] = static_cast<short>(j1 + rem);
   }
-  auto delta = [&](long long pos) { return primal[pos] ? dw : -dc; };
+  auto delta_of = [&](double flag) { return flag != 0.0 ? dw : -dc; };
   // a column entering the window: band entries, its diagonal's regularization
   // and pivot scale, and its border entries
   auto enter = [&](long long c, int slot, const double* src) {
     for (int j = lane; j < B1; j += 32) {
       double v = src[j];
       if (j == 0) {
-        v += delta(c);
+        v += delta_of(src[B1 + w]);
         ps[slot] = fabs(v);
       }
       W[slot * B1 + j] = v;
@@ -153,13 +154,14 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
         dstp[j] = 0.0;
     }
     for (int t = lane; t < w; t += 32) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
+    if (lane == 0) cp8(dstp + B1 + w, primal + c);
   };
   // initial window: columns 0..B1-1 directly; prefetch B1..B1+kPrefetch-1
   for (long long c = 0; c < B1 && c < n; ++c) {
     for (int j = lane; j < B1; j += 32) {
       double v = c + j < n ? band[c * B1 + j] : 0.0;
       if (j == 0) {
-        v += delta(c);
+        v += delta_of(primal[c]);
         ps[c] = fabs(v);
       }
       W[c * B1 + j] = v;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     const int t = q / w, u = q % w;
     double v = Sg[q];
     if (t == u) {
-      v += delta(n + t);
+      v += delta_of(primal[n + t]);
       Sps[t] = fabs(v);
     }
     S[q] = v;
@@ -182,8 +184,8 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
   long long npos = 0, nneg = 0, nzero = 0;
   __syncwarp();
 
-  for (long long k = 0; k < n; ++k) {
-    const int s = static_cast<int>(k % B1);
+  int s = 0;  // slot of column k = k mod B1
+  for (long long k = 0; k < n; ++k, s = (s + 1 == B1 ? 0 : s + 1)) {
     const double d = W[s * B1];
     const bool zero = zero_pivot(d, ps[s]);
     const double dinv = zero ? 0.0 : 1.0 / d;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     for (int p = lane; p < P; p += 32) {
       const int j1 = pj1[p], j2 = pj2[p];
       if (k + j2 < n) {
-        const int s1 = static_cast<int>((k + j1) % B1);
+        const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
         const double upd = l[j2] * y[j1];
         W[s1 * B1 + (j2 - j1)] -= upd;
         if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     }
     for (int q = lane; q < w * b; q += 32) {
       const int t = q / b, j = q % b + 1;
-      if (k + j < n) Wb[t * B1 + static_cast<int>((k + j) % B1)] -= lb[t] * y[j];
+      if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
     }
     for (int q = lane; q < w * w; q += 32) {
       const int t = q / w, u = q % w;
@@ -236,9 +238,9 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     cp_wait<kPrefetch - 1>();
     __syncwarp();
     const long long cin = k + B1;
-    if (cin < n) enter(cin, s, ring + static_cast<int>(k % kPrefetch) * RW);
+    if (cin < n) enter(cin, s, ring + static_cast<int>(k & kMask) * RW);
     __syncwarp();
-    if (cin + kPrefetch < n) fetch(cin + kPrefetch, static_cast<int>(k % kPrefetch));
+    if (cin + kPrefetch < n) fetch(cin + kPrefetch, static_cast<int>(k & kMask));
     cp_commit();
   }
   cp_wait<0>();
@@ -332,20 +334,20 @@ __global__ void __launch_bounds__(32) band_solve_k(const double* __restrict__ bu
     cp_commit();
   }
   __syncwarp();
-  for (long long c = 0; c < n; ++c) {
-    const int s = static_cast<int>(c % B1);
+  int s = 0;
+  for (long long c = 0; c < n; ++c, s = (s + 1 == B1 ? 0 : s + 1)) {
     cp_wait<kPrefetch - 1>();
     __syncwarp();
-    const double* col = ring + static_cast<int>(c % kPrefetch) * (RW + 2);
+    const double* col = ring + static_cast<int>(c & kMask) * (RW + 2);
     const double yc = Y[s];
     if (lane == 0) work[c] = yc;
     for (int j = lane + 1; j < B1; j += 32)
-      if (c + j < n) Y[static_cast<int>((c + j) % B1)] -= col[j] * yc;
+      if (c + j < n) Y[s + j >= B1 ? s + j - B1 : s + j] -= col[j] * yc;
     for (int t = lane; t < w; t += 32) yb[t] -= col[B1 + t] * yc;
     __syncwarp();
     if (lane == 0 && c + B1 < n) Y[s] = col[RW];
     __syncwarp();
-    if (c + kPrefetch < n) fetch(c + kPrefetch, static_cast<int>(c % kPrefetch), true);
+    if (c + kPrefetch < n) fetch(c + kPrefetch, static_cast<int>(c & kMask), true);
     cp_commit();
   }
   cp_wait<0>();
@@ -365,24 +367,25 @@ __global__ void __launch_bounds__(32) band_solve_k(const double* __restrict__ bu
     if (n - 1 - r >= 0) fetch(n - 1 - r, r, false);
     cp_commit();
   }
-  for (long long c = n - 1; c >= 0; --c) {
+  int sc = static_cast<int>((n - 1) % B1);
+  for (long long c = n - 1; c >= 0; --c, sc = (sc == 0 ? B1 - 1 : sc - 1)) {
     const long long it = n - 1 - c;
     cp_wait<kPrefetch - 1>();
     __syncwarp();
-    const double* col = ring + static_cast<int>(it % kPrefetch) * (RW + 2);
+    const double* col = ring + static_cast<int>(it & kMask) * (RW + 2);
     double part = 0.0;
     for (int j = lane + 1; j < B1; j += 32)
-      if (c + j < n) part += col[j] * X[static_cast<int>((c + j) % B1)];
+      if (c + j < n) part += col[j] * X[sc + j >= B1 ? sc + j - B1 : sc + j];
     for (int t = lane; t < w; t += 32) part += col[B1 + t] * yb[t];
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     const double xc = col[RW] * col[RW + 1] - part;
     __syncwarp();
     if (lane == 0) {
-      X[static_cast<int>(c % B1)] = xc;
+      X[sc] = xc;
       work[c] = xc;
     }
     __syncwarp();
-    if (c - kPrefetch >= 0) fetch(c - kPrefetch, static_cast<int>(it % kPrefetch), false);
+    if (c - kPrefetch >= 0) fetch(c - kPrefetch, static_cast<int>(it & kMask), false);
     cp_commit();
   }
   cp_wait<0>();
@@ -400,12 +403,12 @@ void band_assemble(const double* kval, const int64_t* dst, int64_t nnz, double* 
   if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, dst, nnz, buf);
 }
 
-void band_factor(double* buf, const int8_t* primal, int64_t n, int b, int w, double delta_w, double delta_c,
+void band_factor(double* buf, const double* primal, int64_t n, int b, int w, double delta_w, double delta_c,
                  double* Dinv, long long* inertia, cudaStream_t s) {
   const int B1 = b + 1, P = b * (b + 1) / 2;
   const size_t smem = sizeof(double) * (static_cast<size_t>(B1) * B1 + B1 + static_cast<size_t>(w) * B1 +
                                         static_cast<size_t>(w) * w + w + 2 * B1 + 2 * w +
-                                        static_cast<size_t>(kPrefetch) * (B1 + w)) +
+                                        static_cast<size_t>(kPrefetch) * (B1 + w + 1)) +
                       sizeof(short) * 2 * static_cast<size_t>(P) + 16;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(band_factor_k), cudaFuncAttributeMaxDynamicSharedMemorySize,

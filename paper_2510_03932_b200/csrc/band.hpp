@@ -27,7 +27,7 @@ struct BandPlan {
   int w = 0;        // border (dense) rows, ordered last
   std::vector<int64_t> perm;    // position -> KKT index
   std::vector<int64_t> dst;     // K entry p -> flat offset in the factor buffer
-  std::vector<int8_t> primal;   // per position: 1 = primal (+delta_w), 0 = dual (-delta_c)
+  std::vector<double> primal;   // per position: 1 = primal (+delta_w), 0 = dual (-delta_c)
   int64_t buf_len() const { return n * (b + 1) + static_cast<int64_t>(w) * n + static_cast<int64_t>(w) * w; }
 };
 
@@ -43,7 +43,7 @@ namespace dev {
 void band_assemble(const double* kval, const int64_t* dst, int64_t nnz, double* buf, int64_t len, cudaStream_t s);
 
 // in-place LDL^T of buf; Dinv[dim] (position order); inertia[3] (device int64)
-void band_factor(double* buf, const int8_t* primal, int64_t n, int b, int w, double delta_w, double delta_c,
+void band_factor(double* buf, const double* primal, int64_t n, int b, int w, double delta_w, double delta_c,
                  double* Dinv, long long* inertia, cudaStream_t s);
 
 // x = (P^T L D L^T P)^{-1} rhs; rhs, x in KKT index order; work[dim] scratch

@@ -164,8 +164,7 @@ struct ocg_ldl {
   ocg_kkt* kkt = nullptr;
   ocg::BandPlan plan;
   DBuf<int64_t> dst, perm;
-  DBuf<int8_t> primal;
-  DBuf<double> buf, Dinv, work;
+  DBuf<double> primal, buf, Dinv, work;
   DBuf<long long> inertia;
   double delta_w = 0.0, delta_c = 0.0;
   int64_t factorizations = 0;
