@@ -220,7 +220,7 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
 typedef struct ocg_ldl ocg_ldl;
 int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out);
 void ocg_ldl_destroy(ocg_ldl* l);
-/* out[5] = dim, banded part, bandwidth, border size, factorizations so far */
+/* out[5] = dim, time segments, bandwidth, global border rows, factorizations so far */
 int ocg_ldl_info(const ocg_ldl* l, int64_t* out);
 /* factor the current K.val of `k`; inertia[3] (host, may be NULL) — synchronous when given */
 int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia, ocg_stream s);

@@ -1,12 +1,21 @@
-// Device LDL^T in a node-major band-plus-border ordering (see band.hpp).
+// Device LDL^T in a node-major band-plus-border ordering, partitioned in time
+// (see band.hpp for the structure and the conventions kept from the
+// reference's sparse::factorize).
 //
-// The factorization and the triangular solves are sequential along the band,
-// so each runs on ONE warp with the active window of the band in shared
-// memory: the (b+1) x (b+1) trailing triangle rolls through a ring of column
-// slots, and the band columns that enter the window are prefetched kPrefetch
-// columns ahead with cp.async (LDGSTS) so that no global-memory latency sits
-// on the per-column critical path. Gathers/scatters between KKT order and
-// band order are grid-wide streaming kernels.
+// Kernels:
+//   factor_k   one thread block per banded block (segment or separator
+//              system). The (b+1)x(b+1) trailing triangle of the band rolls
+//              through a ring of column slots in shared memory, the border
+//              rows' window likewise, and the band/border columns that enter
+//              are prefetched kPrefetch columns ahead with cp.async (LDGSTS),
+//              so no global-memory latency sits on the per-column path.
+//   solve_k    one warp per block: forward (L), D, backward (L^T) passes with
+//              the same prefetch ring; segments run their forward and
+//              backward halves around the separator system's full solve.
+//   schur/rhs  deterministic assembly of the segments' Schur complements and
+//              right-hand-side contributions into the separator system:
+//              segments of one parity touch disjoint separators; the global
+//              border block is summed in segment order by one thread each.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -18,46 +27,207 @@
 
 namespace ocg {
 
+namespace {
+
+size_t factor_smem(int b, int w) {
+  const size_t B1 = static_cast<size_t>(b) + 1, W = static_cast<size_t>(w);
+  constexpr size_t kPre = 32;
+  const size_t pairs = static_cast<size_t>(b) * (b + 1) / 2;
+  return sizeof(double) * (B1 * B1 + B1 + W * B1 + W * W + W + 2 * B1 + 2 * W + kPre * (B1 + W + 1)) +
+         sizeof(short) * 2 * pairs + 64;
+}
+size_t solve_smem(int b, int w) {
+  constexpr size_t kPre = 32;
+  return sizeof(double) * (static_cast<size_t>(b) + 1 + 2 * static_cast<size_t>(w) +
+                           kPre * (static_cast<size_t>(b) + 3 + w)) +
+         64;
+}
+
+}  // namespace
+
 BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std::vector<int64_t>& colp,
-                        const std::vector<int64_t>& rowi, int64_t ntot) {
+                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments) {
   BandPlan P;
   P.dim = dim;
-  std::vector<int64_t> order(static_cast<size_t>(dim));
-  for (int64_t i = 0; i < dim; ++i) order[static_cast<size_t>(i)] = i;
+  // flat node-major order: band part, then the global border
+  std::vector<int64_t> flat(static_cast<size_t>(dim));
+  for (int64_t i = 0; i < dim; ++i) flat[static_cast<size_t>(i)] = i;
   auto key = [&](int64_t i) { return node[static_cast<size_t>(i)] < 0 ? INT64_MAX : node[static_cast<size_t>(i)]; };
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
-  std::vector<int64_t> pos(static_cast<size_t>(dim));
-  for (int64_t p = 0; p < dim; ++p) pos[static_cast<size_t>(order[static_cast<size_t>(p)])] = p;
-  int64_t w = 0;
-  for (int64_t i = 0; i < dim; ++i) w += node[static_cast<size_t>(i)] < 0 ? 1 : 0;
-  P.n = dim - w;
-  P.w = static_cast<int>(w);
-  P.perm = order;
-  P.primal.resize(static_cast<size_t>(dim));
-  for (int64_t p = 0; p < dim; ++p) P.primal[static_cast<size_t>(p)] = order[static_cast<size_t>(p)] < ntot ? 1 : 0;
+  std::stable_sort(flat.begin(), flat.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+  std::vector<int64_t> fpos(static_cast<size_t>(dim));
+  for (int64_t p = 0; p < dim; ++p) fpos[static_cast<size_t>(flat[static_cast<size_t>(p)])] = p;
+  int64_t wg = 0;
+  for (int64_t i = 0; i < dim; ++i) wg += node[static_cast<size_t>(i)] < 0 ? 1 : 0;
+  const int64_t n = dim - wg;
   int64_t b = 0;
   for (int64_t j = 0; j < dim; ++j)
     for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
-      const int64_t pi = pos[static_cast<size_t>(rowi[static_cast<size_t>(q)])], pj = pos[static_cast<size_t>(j)];
-      if (pi < P.n && pj < P.n) b = std::max<int64_t>(b, pi > pj ? pi - pj : pj - pi);
+      const int64_t pi = fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])], pj = fpos[static_cast<size_t>(j)];
+      if (pi < n && pj < n) b = std::max<int64_t>(b, pi > pj ? pi - pj : pj - pi);
     }
-  if (b > 62) throw std::runtime_error("KKT bandwidth " + std::to_string(b) + " exceeds the band solver's limit (62)");
+  b = std::max<int64_t>(b, 1);
+  if (b > 60) throw std::runtime_error("KKT bandwidth " + std::to_string(b) + " exceeds the band solver's limit (60)");
   P.b = static_cast<int>(b);
-  const int64_t B1 = b + 1, n = P.n;
+  P.wg = static_cast<int>(wg);
+
+  // partition: P segments of >= 8b interior columns separated by b-wide separators
+  int64_t nseg = std::min<int64_t>(target_segments, n / std::max<int64_t>(1, 8 * b));
+  if (nseg < 2) nseg = 1;
+  P.nseg = static_cast<int>(nseg);
+  std::vector<int64_t> seg_lo(static_cast<size_t>(nseg)), seg_len(static_cast<size_t>(nseg));
+  const int64_t interior = n - (nseg - 1) * b;
+  {
+    int64_t f = 0;
+    for (int64_t i = 0; i < nseg; ++i) {
+      seg_len[static_cast<size_t>(i)] = interior / nseg + (i < interior % nseg ? 1 : 0);
+      seg_lo[static_cast<size_t>(i)] = f;
+      f += seg_len[static_cast<size_t>(i)] + (i + 1 < nseg ? b : 0);
+    }
+  }
+  const int64_t n2 = (nseg - 1) * b;  // separator-system band columns
+  const int wmax = nseg > 1 ? static_cast<int>(2 * b + wg) : static_cast<int>(wg);
+  P.wmax = wmax;
+  // positions: segment interiors in order, then separators, then the global border
+  std::vector<int64_t> seg_pos(static_cast<size_t>(nseg));
+  {
+    int64_t p = 0;
+    for (int64_t i = 0; i < nseg; ++i) {
+      seg_pos[static_cast<size_t>(i)] = p;
+      p += seg_len[static_cast<size_t>(i)];
+    }
+  }
+  const int64_t sep_pos0 = interior;  // first separator-system position
+  struct Loc {
+    int kind;  // 0 interior of segment idx, 1 separator idx, 2 global border
+    int64_t idx, local;
+  };
+  auto loc_of_flat = [&](int64_t f) -> Loc {
+    if (f >= n) return {2, 0, f - n};
+    if (nseg == 1) return {0, 0, f};
+    const int64_t i = std::upper_bound(seg_lo.begin(), seg_lo.end(), f) - seg_lo.begin() - 1;
+    const int64_t off = f - seg_lo[static_cast<size_t>(i)];
+    if (off < seg_len[static_cast<size_t>(i)]) return {0, i, off};
+    return {1, i, off - seg_len[static_cast<size_t>(i)]};
+  };
+  P.perm.assign(static_cast<size_t>(dim), -1);
+  for (int64_t f = 0; f < dim; ++f) {
+    const Loc L = loc_of_flat(f);
+    int64_t pos;
+    if (L.kind == 0)
+      pos = seg_pos[static_cast<size_t>(L.idx)] + L.local;
+    else if (L.kind == 1)
+      pos = sep_pos0 + L.idx * b + L.local;
+    else
+      pos = sep_pos0 + n2 + L.local;
+    P.perm[static_cast<size_t>(pos)] = flat[static_cast<size_t>(f)];
+  }
+  P.primal.resize(static_cast<size_t>(dim));
+  for (int64_t p = 0; p < dim; ++p) P.primal[static_cast<size_t>(p)] = P.perm[static_cast<size_t>(p)] < ntot ? 1.0 : 0.0;
+
+  // blocks and their buffers
+  int64_t off = 0;
+  auto add_block = [&](long long nn, int bb, int ww, int early, int fin, long long pos, long long bpos) {
+    BandSeg s;
+    s.n = nn;
+    s.b = bb;
+    s.w = ww;
+    s.w_early = early;
+    s.finalize = fin;
+    s.band = off;
+    off += nn * (bb + 1);
+    s.border = off;
+    off += static_cast<int64_t>(ww) * nn;
+    s.S = off;
+    off += static_cast<int64_t>(ww) * ww;
+    s.pos = pos;
+    s.bpos = bpos;
+    P.segs.push_back(s);
+  };
+  if (nseg == 1) {
+    add_block(n, static_cast<int>(b), static_cast<int>(wg), static_cast<int>(wg), 1, 0, n);
+  } else {
+    for (int64_t i = 0; i < nseg; ++i)
+      add_block(seg_len[static_cast<size_t>(i)], static_cast<int>(b), wmax, static_cast<int>(b + wg), 0,
+                seg_pos[static_cast<size_t>(i)], -1);
+    add_block(n2, static_cast<int>(2 * b - 1), static_cast<int>(wg), static_cast<int>(wg), 1, sep_pos0,
+              sep_pos0 + n2);
+  }
+  P.buf_len = off;
+  // segment border rows [left sep | global | right sep] -> separator-system
+  // local index (n2 + u = global row u), -1 = no such separator
+  P.border_pos.assign(static_cast<size_t>(nseg) * static_cast<size_t>(std::max(wmax, 1)), -1);
+  if (nseg > 1)
+    for (int64_t i = 0; i < nseg; ++i)
+      for (int t = 0; t < wmax; ++t) {
+        int64_t v;
+        if (t < b)
+          v = i > 0 ? (i - 1) * b + t : -1;
+        else if (t < b + wg)
+          v = n2 + (t - b);
+        else
+          v = i + 1 < nseg ? i * b + (t - b - wg) : -1;
+        P.border_pos[static_cast<size_t>(i * wmax + t)] = v;
+      }
+
+  // K entries -> buffer offsets
+  auto sep_target = [&](int64_t R, int64_t C) -> int64_t {  // separator-system local indices
+    const BandSeg& sep = P.segs.back();
+    if (R < C) std::swap(R, C);
+    if (R < n2) return sep.band + C * (sep.b + 1) + (R - C);
+    if (C < n2) return sep.border + (R - n2) * n2 + C;
+    return sep.S + (R - n2) * sep.w + (C - n2);
+  };
   P.dst.resize(rowi.size());
   for (int64_t j = 0; j < dim; ++j)
     for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
-      int64_t r = pos[static_cast<size_t>(rowi[static_cast<size_t>(q)])], c = pos[static_cast<size_t>(j)];
-      if (r < c) std::swap(r, c);
-      int64_t d;
-      if (r < n)
-        d = c * B1 + (r - c);  // band
-      else if (c < n)
-        d = n * B1 + (r - n) * n + c;  // border row r-n, band column c
-      else
-        d = n * B1 + w * n + (r - n) * w + (c - n);  // border block (lower)
+      Loc a = loc_of_flat(fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])]);
+      Loc c = loc_of_flat(fpos[static_cast<size_t>(j)]);
+      int64_t d = -1;
+      if (nseg == 1) {
+        const BandSeg& s = P.segs[0];
+        int64_t r = a.kind == 2 ? n + a.local : a.local, cc = c.kind == 2 ? n + c.local : c.local;
+        if (r < cc) std::swap(r, cc);
+        if (r < n)
+          d = s.band + cc * (b + 1) + (r - cc);
+        else if (cc < n)
+          d = s.border + (r - n) * n + cc;
+        else
+          d = s.S + (r - n) * s.w + (cc - n);
+      } else {
+        if (a.kind == 0 && c.kind != 0) std::swap(a, c);  // interior (if any) in c
+        if (a.kind == 0 && c.kind == 0) {
+          if (a.idx != c.idx) throw std::runtime_error("band plan: entry couples two segments");
+          const BandSeg& s = P.segs[static_cast<size_t>(a.idx)];
+          int64_t r = a.local, cc = c.local;
+          if (r < cc) std::swap(r, cc);
+          if (r - cc > b) throw std::runtime_error("band plan: entry outside the band");
+          d = s.band + cc * (b + 1) + (r - cc);
+        } else if (c.kind == 0) {
+          const BandSeg& s = P.segs[static_cast<size_t>(c.idx)];
+          int64_t t;
+          if (a.kind == 2)
+            t = b + a.local;
+          else if (a.idx == c.idx - 1)
+            t = a.local;
+          else if (a.idx == c.idx)
+            t = b + wg + a.local;
+          else
+            throw std::runtime_error("band plan: separator coupled to a distant segment");
+          d = s.border + t * s.n + c.local;
+        } else {
+          auto sl = [&](const Loc& L) { return L.kind == 1 ? L.idx * b + L.local : n2 + L.local; };
+          d = sep_target(sl(a), sl(c));
+        }
+      }
       P.dst[static_cast<size_t>(q)] = d;
     }
+  size_t sf = 0, ss = 0;
+  for (const BandSeg& s : P.segs) {
+    sf = std::max(sf, factor_smem(s.b, s.w));
+    ss = std::max(ss, solve_smem(s.b, s.w));
+  }
+  P.smem_factor = sf;
+  P.smem_solve = ss;
   return P;
 }
 
@@ -67,6 +237,7 @@ namespace {
 
 constexpr int kPrefetch = 32;  // band columns in flight ahead of the window (power of two)
 constexpr int kMask = kPrefetch - 1;
+constexpr int kFactorThreads = 256;
 
 __device__ __forceinline__ void cp8(double* s, const double* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
@@ -78,51 +249,55 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+#define GRID_LOOP(i, n)                                                                  \
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
 __global__ void scatter_k(const double* __restrict__ kval, const int64_t* __restrict__ dst, int64_t nnz,
                           double* __restrict__ buf) {
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    buf[dst[p]] = kval[p];
+  GRID_LOOP(p, nnz) buf[dst[p]] = kval[p];
 }
 
 __global__ void zero_k(double* __restrict__ buf, int64_t len) {
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < len;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    buf[p] = 0.0;
+  GRID_LOOP(p, len) buf[p] = 0.0;
 }
 
 __device__ __forceinline__ bool zero_pivot(double d, double scale) {
   return !(fabs(d) <= DBL_MAX) || fabs(d) <= 1e-14 * fmax(scale, 1e-30);
 }
 
-// One warp. Shared memory: window W[B1][B1] (slot-major), pivot scales ps[B1],
-// border window Wb[w][B1], border block S[w][w] + scales, y/l/yb/lb vectors,
-// the (j1, j2) update pairs and a prefetch ring of kPrefetch columns.
-__global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, const double* __restrict__ primal,
-                                                    long long n, int b, int w, double dw, double dc,
-                                                    double* __restrict__ Dinv, long long* __restrict__ inertia) {
+// One thread block per banded block (blockIdx.x indexes `segs` from seg0).
+__global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __restrict__ segs, int seg0,
+                                                           double* __restrict__ buf,
+                                                           const double* __restrict__ primal, double dw, double dc,
+                                                           double* __restrict__ Dinv,
+                                                           long long* __restrict__ inertia_parts) {
   extern __shared__ double sm[];
-  const int lane = threadIdx.x;
-  const int B1 = b + 1;
-  double* W = sm;                     // B1 * B1
-  double* ps = W + B1 * B1;           // B1
-  double* Wb = ps + B1;               // w * B1
-  double* S = Wb + w * B1;            // w * w
-  double* Sps = S + w * w;            // w
-  double* y = Sps + w;                // B1
-  double* l = y + B1;                 // B1
-  double* yb = l + B1;                // w
-  double* lb = yb + w;                // w
-  double* ring = lb + w;              // kPrefetch * (B1 + w + 1)
-  short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * (B1 + w + 1));
+  const BandSeg g = segs[seg0 + blockIdx.x];
+  const int tid = threadIdx.x, T = blockDim.x;
+  const long long n = g.n;
+  const int b = g.b, w = g.w, B1 = b + 1;
+  double* W = sm;                 // B1 * B1 (slot-major)
+  double* ps = W + B1 * B1;       // B1
+  double* Wb = ps + B1;           // w * B1
+  double* S = Wb + w * B1;        // w * w
+  double* Sps = S + w * w;        // w
+  double* y = Sps + w;            // B1
+  double* l = y + B1;             // B1
+  double* yb = l + B1;            // w
+  double* lb = yb + w;            // w
+  double* ring = lb + w;          // kPrefetch * RW
+  const int RW = B1 + w + 1;      // ring row: band column, its border entries, its regularization flag
+  short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * RW);
   const int P = b * (b + 1) / 2;
   short* pj2 = pj1 + P;
-  double* band = buf;
-  double* border = buf + n * B1;
-  double* Sg = border + static_cast<long long>(w) * n;
-  const int RW = B1 + w + 1;  // ring row: band column, its border entries, its primal flag
+  double* band = buf + g.band;
+  double* border = buf + g.border;
+  double* Sg = buf + g.S;
+  const double* flag = primal + g.pos;
+  double* dinvp = Dinv + g.pos;
 
-  for (int p = lane; p < P; p += 32) {  // pairs j1 <= j2 in 1..b
+  for (int p = tid; p < P; p += T) {  // pairs j1 <= j2 in 1..b
     int j1 = 1, rem = p;
     while (rem >= b - j1 + 1) {
       rem -= b - j1 + 1;
@@ -131,66 +306,52 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
     pj1[p] = static_cast<short>(j1);
     pj2[p] = static_cast<short>(j1 + rem);
   }
-  auto delta_of = [&](double flag) { return flag != 0.0 ? dw : -dc; };
-  // a column entering the window: band entries, its diagonal's regularization
-  // and pivot scale, and its border entries
-  auto enter = [&](long long c, int slot, const double* src) {
-    for (int j = lane; j < B1; j += 32) {
-      double v = src[j];
-      if (j == 0) {
-        v += delta_of(src[B1 + w]);
-        ps[slot] = fabs(v);
-      }
-      W[slot * B1 + j] = v;
-    }
-    for (int t = lane; t < w; t += 32) Wb[t * B1 + slot] = src[B1 + t];
-  };
+  auto delta_of = [&](double f) { return f != 0.0 ? dw : -dc; };
   auto fetch = [&](long long c, int r) {  // column c -> ring row r (async)
     double* dstp = ring + r * RW;
-    for (int j = lane; j < B1; j += 32) {
+    for (int j = tid; j < B1; j += T) {
       if (c + j < n)
         cp8(dstp + j, band + c * B1 + j);
       else
         dstp[j] = 0.0;
     }
-    for (int t = lane; t < w; t += 32) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
-    if (lane == 0) cp8(dstp + B1 + w, primal + c);
+    for (int t = tid; t < w; t += T) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
+    if (tid == 0) cp8(dstp + B1 + w, flag + c);
   };
-  // initial window: columns 0..B1-1 directly; prefetch B1..B1+kPrefetch-1
   for (long long c = 0; c < B1 && c < n; ++c) {
-    for (int j = lane; j < B1; j += 32) {
+    for (int j = tid; j < B1; j += T) {
       double v = c + j < n ? band[c * B1 + j] : 0.0;
       if (j == 0) {
-        v += delta_of(primal[c]);
+        v += delta_of(flag[c]);
         ps[c] = fabs(v);
       }
       W[c * B1 + j] = v;
     }
-    for (int t = lane; t < w; t += 32) Wb[t * B1 + c] = border[static_cast<long long>(t) * n + c];
+    for (int t = tid; t < w; t += T) Wb[t * B1 + c] = border[static_cast<long long>(t) * n + c];
   }
   for (int r = 0; r < kPrefetch; ++r) {
     if (B1 + r < n) fetch(B1 + r, r);
     cp_commit();
   }
-  for (int q = lane; q < w * w; q += 32) {
+  for (int q = tid; q < w * w; q += T) {
     const int t = q / w, u = q % w;
     double v = Sg[q];
     if (t == u) {
-      v += delta_of(primal[n + t]);
+      if (g.finalize) v += delta_of(primal[g.bpos + t]);
       Sps[t] = fabs(v);
     }
     S[q] = v;
   }
   long long npos = 0, nneg = 0, nzero = 0;
-  __syncwarp();
+  __syncthreads();
 
   int s = 0;  // slot of column k = k mod B1
   for (long long k = 0; k < n; ++k, s = (s + 1 == B1 ? 0 : s + 1)) {
     const double d = W[s * B1];
     const bool zero = zero_pivot(d, ps[s]);
     const double dinv = zero ? 0.0 : 1.0 / d;
-    if (lane == 0) {
-      Dinv[k] = dinv;
+    if (tid == 0) {
+      dinvp[k] = dinv;
       band[k * B1] = d;
       if (zero)
         ++nzero;
@@ -199,21 +360,22 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
       else
         ++nneg;
     }
-    for (int j = lane + 1; j < B1; j += 32) {
+    const int wa = k + b >= n ? w : g.w_early;  // border rows coupled so far
+    for (int j = tid + 1; j < B1; j += T) {
       const double yj = k + j < n ? W[s * B1 + j] : 0.0;
       const double lj = yj * dinv;
       y[j] = yj;
       l[j] = lj;
       if (k + j < n) band[k * B1 + j] = lj;
     }
-    for (int t = lane; t < w; t += 32) {
-      const double v = Wb[t * B1 + s];
+    for (int t = tid; t < w; t += T) {
+      const double v = t < wa ? Wb[t * B1 + s] : 0.0;
       yb[t] = v;
       lb[t] = v * dinv;
       border[static_cast<long long>(t) * n + k] = v * dinv;
     }
-    __syncwarp();
-    for (int p = lane; p < P; p += 32) {
+    __syncthreads();
+    for (int p = tid; p < P; p += T) {
       const int j1 = pj1[p], j2 = pj2[p];
       if (k + j2 < n) {
         const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
@@ -222,92 +384,165 @@ __global__ void __launch_bounds__(32) band_factor_k(double* __restrict__ buf, co
         if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
       }
     }
-    for (int q = lane; q < w * b; q += 32) {
+    for (int q = tid; q < wa * b; q += T) {
       const int t = q / b, j = q % b + 1;
       if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
     }
-    for (int q = lane; q < w * w; q += 32) {
-      const int t = q / w, u = q % w;
+    for (int q = tid; q < wa * wa; q += T) {
+      const int t = q / wa, u = q % wa;
       if (u <= t) {
         const double upd = lb[t] * yb[u];
-        S[q] -= upd;
+        S[t * w + u] -= upd;
         if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
       }
     }
     // column k is final: its slot takes column k + B1 from the prefetch ring
     cp_wait<kPrefetch - 1>();
-    __syncwarp();
+    __syncthreads();
     const long long cin = k + B1;
-    if (cin < n) enter(cin, s, ring + static_cast<int>(k & kMask) * RW);
-    __syncwarp();
+    if (cin < n) {
+      const double* src = ring + static_cast<int>(k & kMask) * RW;
+      for (int j = tid; j < B1; j += T) {
+        double v = src[j];
+        if (j == 0) {
+          v += delta_of(src[B1 + w]);
+          ps[s] = fabs(v);
+        }
+        W[s * B1 + j] = v;
+      }
+      for (int t = tid; t < w; t += T) Wb[t * B1 + s] = src[B1 + t];
+    }
+    __syncthreads();
     if (cin + kPrefetch < n) fetch(cin + kPrefetch, static_cast<int>(k & kMask));
     cp_commit();
   }
   cp_wait<0>();
-  // dense border block: sequential LDL^T with the same pivot rule
-  if (lane == 0) {
-    for (int t = 0; t < w; ++t) {
-      const double d = S[t * w + t];
-      const bool zero = zero_pivot(d, Sps[t]);
-      const double dinv = zero ? 0.0 : 1.0 / d;
-      Dinv[n + t] = dinv;
-      Sg[t * w + t] = d;
-      if (zero)
-        ++nzero;
-      else if (d > 0)
-        ++npos;
-      else
-        ++nneg;
-      for (int u = t + 1; u < w; ++u) {
-        const double yu = S[u * w + t];
-        const double lu = yu * dinv;
-        for (int v = t + 1; v <= u; ++v) {
-          const double upd = lu * S[v * w + t];
-          S[u * w + v] -= upd;
-          if (u == v) Sps[u] = fmax(Sps[u], fabs(upd));
+  __syncthreads();
+  if (g.finalize) {
+    // dense border block: sequential LDL^T with the same pivot rule
+    if (tid == 0) {
+      for (int t = 0; t < w; ++t) {
+        const double d = S[t * w + t];
+        const bool zero = zero_pivot(d, Sps[t]);
+        const double dinv = zero ? 0.0 : 1.0 / d;
+        Dinv[g.bpos + t] = dinv;
+        Sg[t * w + t] = d;
+        if (zero)
+          ++nzero;
+        else if (d > 0)
+          ++npos;
+        else
+          ++nneg;
+        for (int u = t + 1; u < w; ++u) {
+          const double lu = S[u * w + t] * dinv;
+          for (int v = t + 1; v <= u; ++v) {
+            const double upd = lu * S[v * w + t];
+            S[u * w + v] -= upd;
+            if (u == v) Sps[u] = fmax(Sps[u], fabs(upd));
+          }
         }
+        for (int u = t + 1; u < w; ++u) Sg[u * w + t] = S[u * w + t] * dinv;
       }
-      for (int u = t + 1; u < w; ++u) Sg[u * w + t] = S[u * w + t] * dinv;
     }
+  } else {
+    for (int q = tid; q < w * w; q += T) Sg[q] = S[q];  // Schur complement on the border rows
   }
-  // counts from lane 0 only
-  if (lane == 0) {
-    inertia[0] = npos;
-    inertia[1] = nneg;
-    inertia[2] = nzero;
+  if (tid == 0) {
+    long long* o = inertia_parts + 3 * (seg0 + blockIdx.x);
+    o[0] = npos;
+    o[1] = nneg;
+    o[2] = nzero;
   }
+}
+
+// segments of parity `par` add their Schur complements into the separator
+// system (disjoint separators within a parity); global-global entries skipped
+__global__ void schur_add_k(const BandSeg* __restrict__ segs, int nseg, int par, int wmax,
+                            const int64_t* __restrict__ border_pos, double* __restrict__ buf) {
+  const BandSeg sep = segs[nseg];
+  const long long n2 = sep.n;
+  const int64_t per = static_cast<int64_t>(wmax) * wmax;
+  const int64_t cnt = static_cast<int64_t>((nseg - par + 1) / 2) * per;
+  GRID_LOOP(q, cnt) {
+    const int i = par + 2 * static_cast<int>(q / per);
+    const int t = static_cast<int>((q % per) / wmax), u = static_cast<int>(q % wmax);
+    if (u > t) continue;
+    int64_t R = border_pos[static_cast<int64_t>(i) * wmax + t], C = border_pos[static_cast<int64_t>(i) * wmax + u];
+    if (R < 0 || C < 0 || (R >= n2 && C >= n2)) continue;
+    const double v = buf[segs[i].S + static_cast<int64_t>(t) * wmax + u];
+    if (R < C) {
+      const int64_t tmp = R;
+      R = C;
+      C = tmp;
+    }
+    int64_t dst;
+    if (R < n2)
+      dst = sep.band + C * (sep.b + 1) + (R - C);
+    else
+      dst = sep.border + (R - n2) * n2 + C;
+    buf[dst] += v;
+  }
+}
+
+// global-global block: every segment contributes, summed in segment order
+__global__ void schur_global_k(const BandSeg* __restrict__ segs, int nseg, int wmax, int b, int wg,
+                               double* __restrict__ buf) {
+  const BandSeg sep = segs[nseg];
+  GRID_LOOP(q, static_cast<int64_t>(wg) * wg) {
+    const int u = static_cast<int>(q / wg), v = static_cast<int>(q % wg);
+    if (v > u) continue;
+    double acc = 0.0;
+    for (int i = 0; i < nseg; ++i) acc += buf[segs[i].S + static_cast<int64_t>(b + u) * wmax + (b + v)];
+    buf[sep.S + static_cast<int64_t>(u) * sep.w + v] += acc;
+  }
+}
+
+__global__ void inertia_sum_k(const long long* __restrict__ parts, int nblocks, long long* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long a = 0, c = 0, z = 0;
+  for (int i = 0; i < nblocks; ++i) {
+    a += parts[3 * i];
+    c += parts[3 * i + 1];
+    z += parts[3 * i + 2];
+  }
+  out[0] = a;
+  out[1] = c;
+  out[2] = z;
 }
 
 __global__ void gather_k(const double* __restrict__ rhs, const int64_t* __restrict__ perm, int64_t dim,
                          double* __restrict__ out) {
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < dim;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[p] = rhs[perm[p]];
+  GRID_LOOP(p, dim) out[p] = rhs[perm[p]];
 }
 
 __global__ void scatter_back_k(const double* __restrict__ work, const int64_t* __restrict__ perm, int64_t dim,
                                double* __restrict__ x) {
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < dim;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    x[perm[p]] = work[p];
+  GRID_LOOP(p, dim) x[perm[p]] = work[p];
 }
 
-// One warp: forward L y = b, D scaling, backward L^T x = y, on work[] in
-// band order (border last). L columns stream through a cp.async ring.
-__global__ void __launch_bounds__(32) band_solve_k(const double* __restrict__ buf, const double* __restrict__ Dinv,
-                                                   long long n, int b, int w, double* __restrict__ work) {
+// mode 0: full solve of a finalized block (forward, border block, D, backward)
+// mode 1: segment forward; border accumulations -> gparts[blk * wmax + t]
+// mode 2: segment backward with the separator system's solution as border values
+__global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, int seg0, int mode,
+                                              const double* __restrict__ buf, const double* __restrict__ Dinv,
+                                              double* __restrict__ work, double* __restrict__ gparts, int wmax,
+                                              const int64_t* __restrict__ border_pos, long long sep_pos0) {
   extern __shared__ double sm[];
+  const int blk = seg0 + blockIdx.x;
+  const BandSeg g = segs[blk];
   const int lane = threadIdx.x;
-  const int B1 = b + 1;
+  const long long n = g.n;
+  const int b = g.b, w = g.w, B1 = b + 1;
   const int RW = B1 + w;
-  const double* band = buf;
-  const double* border = buf + n * B1;
-  const double* Sg = border + static_cast<long long>(w) * n;
-  double* Y = sm;            // B1 window of the vector
-  double* yb = Y + B1;       // w
-  double* ring = yb + w;     // kPrefetch * (RW + 2)
-  // ring row of column c: L column, border entries, then two vector values
-  // the step needs (forward: rhs of column c + B1; backward: y_c and Dinv_c)
+  const double* band = buf + g.band;
+  const double* border = buf + g.border;
+  const double* Sg = buf + g.S;
+  double* v = work + g.pos;
+  const double* dinv = Dinv + g.pos;
+  double* Y = sm;          // B1 window of the vector
+  double* yb = Y + B1;     // w
+  double* xb = yb + w;     // w
+  double* ring = xb + w;   // kPrefetch * (RW + 2)
   auto fetch = [&](long long c, int r, bool forward) {
     double* dstp = ring + r * (RW + 2);
     for (int j = lane; j < B1; j += 32) {
@@ -319,46 +554,60 @@ __global__ void __launch_bounds__(32) band_solve_k(const double* __restrict__ bu
     for (int t = lane; t < w; t += 32) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
     if (lane == 0) {
       if (forward) {
-        if (c + B1 < n) cp8(dstp + RW, work + c + B1);
+        if (c + B1 < n) cp8(dstp + RW, v + c + B1);
       } else {
-        cp8(dstp + RW, work + c);
-        cp8(dstp + RW + 1, Dinv + c);
+        cp8(dstp + RW, v + c);
+        cp8(dstp + RW + 1, dinv + c);
       }
     }
   };
-  // ---- forward: columns in increasing order
-  for (int j = lane; j < B1; j += 32) Y[j] = j < n ? work[j] : 0.0;
-  for (int t = lane; t < w; t += 32) yb[t] = work[n + t];
-  for (int r = 0; r < kPrefetch; ++r) {
-    if (r < n) fetch(r, r, true);
-    cp_commit();
-  }
-  __syncwarp();
-  int s = 0;
-  for (long long c = 0; c < n; ++c, s = (s + 1 == B1 ? 0 : s + 1)) {
-    cp_wait<kPrefetch - 1>();
+  if (mode != 2) {
+    // ---- forward: columns in increasing order
+    for (int j = lane; j < B1; j += 32) Y[j] = j < n ? v[j] : 0.0;
+    for (int t = lane; t < w; t += 32) yb[t] = mode == 0 ? work[g.bpos + t] : 0.0;
+    for (int r = 0; r < kPrefetch; ++r) {
+      if (r < n) fetch(r, r, true);
+      cp_commit();
+    }
     __syncwarp();
-    const double* col = ring + static_cast<int>(c & kMask) * (RW + 2);
-    const double yc = Y[s];
-    if (lane == 0) work[c] = yc;
-    for (int j = lane + 1; j < B1; j += 32)
-      if (c + j < n) Y[s + j >= B1 ? s + j - B1 : s + j] -= col[j] * yc;
-    for (int t = lane; t < w; t += 32) yb[t] -= col[B1 + t] * yc;
+    int s = 0;
+    for (long long c = 0; c < n; ++c, s = (s + 1 == B1 ? 0 : s + 1)) {
+      cp_wait<kPrefetch - 1>();
+      __syncwarp();
+      const double* col = ring + static_cast<int>(c & kMask) * (RW + 2);
+      const double yc = Y[s];
+      if (lane == 0) v[c] = yc;
+      for (int j = lane + 1; j < B1; j += 32)
+        if (c + j < n) Y[s + j >= B1 ? s + j - B1 : s + j] -= col[j] * yc;
+      for (int t = lane; t < w; t += 32) yb[t] -= col[B1 + t] * yc;
+      __syncwarp();
+      if (lane == 0 && c + B1 < n) Y[s] = col[RW];
+      __syncwarp();
+      if (c + kPrefetch < n) fetch(c + kPrefetch, static_cast<int>(c & kMask), true);
+      cp_commit();
+    }
+    cp_wait<0>();
     __syncwarp();
-    if (lane == 0 && c + B1 < n) Y[s] = col[RW];
+    if (mode == 1) {
+      for (int t = lane; t < w; t += 32) gparts[static_cast<int64_t>(blk) * wmax + t] = yb[t];
+      return;
+    }
+    if (lane == 0) {
+      for (int t = 0; t < w; ++t)
+        for (int u = 0; u < t; ++u) yb[t] -= Sg[t * w + u] * yb[u];
+      for (int t = 0; t < w; ++t) yb[t] *= Dinv[g.bpos + t];
+      for (int t = w - 1; t >= 0; --t)
+        for (int u = t + 1; u < w; ++u) yb[t] -= Sg[u * w + t] * yb[u];
+      for (int t = 0; t < w; ++t) work[g.bpos + t] = yb[t];
+    }
     __syncwarp();
-    if (c + kPrefetch < n) fetch(c + kPrefetch, static_cast<int>(c & kMask), true);
-    cp_commit();
-  }
-  cp_wait<0>();
-  __syncwarp();
-  if (lane == 0) {
-    for (int t = 0; t < w; ++t)
-      for (int u = 0; u < t; ++u) yb[t] -= Sg[t * w + u] * yb[u];
-    for (int t = 0; t < w; ++t) yb[t] *= Dinv[n + t];
-    for (int t = w - 1; t >= 0; --t)
-      for (int u = t + 1; u < w; ++u) yb[t] -= Sg[u * w + t] * yb[u];
-    for (int t = 0; t < w; ++t) work[n + t] = yb[t];
+    for (int t = lane; t < w; t += 32) xb[t] = yb[t];
+  } else {
+    // border values: the separator system's solution at this segment's rows
+    for (int t = lane; t < w; t += 32) {
+      const int64_t q = border_pos[static_cast<int64_t>(blk) * wmax + t];
+      xb[t] = q >= 0 ? work[sep_pos0 + q] : 0.0;
+    }
   }
   __syncwarp();
   // ---- backward: columns in decreasing order; X window holds x[c+1..c+b]
@@ -376,19 +625,39 @@ __global__ void __launch_bounds__(32) band_solve_k(const double* __restrict__ bu
     double part = 0.0;
     for (int j = lane + 1; j < B1; j += 32)
       if (c + j < n) part += col[j] * X[sc + j >= B1 ? sc + j - B1 : sc + j];
-    for (int t = lane; t < w; t += 32) part += col[B1 + t] * yb[t];
+    for (int t = lane; t < w; t += 32) part += col[B1 + t] * xb[t];
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     const double xc = col[RW] * col[RW + 1] - part;
     __syncwarp();
     if (lane == 0) {
       X[sc] = xc;
-      work[c] = xc;
+      v[c] = xc;
     }
     __syncwarp();
     if (c - kPrefetch >= 0) fetch(c - kPrefetch, static_cast<int>(it & kMask), false);
     cp_commit();
   }
   cp_wait<0>();
+}
+
+// segment forward contributions into the separator system's right-hand side
+__global__ void rhs_add_k(int nseg, int par, int wmax, long long n2, const int64_t* __restrict__ border_pos,
+                          const double* __restrict__ gparts, double* __restrict__ sepv) {
+  const int64_t cnt = static_cast<int64_t>((nseg - par + 1) / 2) * wmax;
+  GRID_LOOP(q, cnt) {
+    const int i = par + 2 * static_cast<int>(q / wmax), t = static_cast<int>(q % wmax);
+    const int64_t R = border_pos[static_cast<int64_t>(i) * wmax + t];
+    if (R < 0 || R >= n2) continue;
+    sepv[R] += gparts[static_cast<int64_t>(i) * wmax + t];
+  }
+}
+__global__ void rhs_global_k(int nseg, int wmax, int b, int wg, long long n2, const double* __restrict__ gparts,
+                             double* __restrict__ sepv) {
+  GRID_LOOP(u, wg) {
+    double acc = 0.0;
+    for (int i = 0; i < nseg; ++i) acc += gparts[static_cast<int64_t>(i) * wmax + b + u];
+    sepv[n2 + u] += acc;
+  }
 }
 
 int grid_for(int64_t n) {
@@ -398,31 +667,53 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
-void band_assemble(const double* kval, const int64_t* dst, int64_t nnz, double* buf, int64_t len, cudaStream_t s) {
-  zero_k<<<grid_for(len), 256, 0, s>>>(buf, len);
-  if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, dst, nnz, buf);
+void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, double* buf, cudaStream_t s) {
+  zero_k<<<grid_for(P.buf_len), 256, 0, s>>>(buf, P.buf_len);
+  const int64_t nnz = static_cast<int64_t>(P.dst.size());
+  if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, D.dst, nnz, buf);
 }
 
-void band_factor(double* buf, const double* primal, int64_t n, int b, int w, double delta_w, double delta_c,
-                 double* Dinv, long long* inertia, cudaStream_t s) {
-  const int B1 = b + 1, P = b * (b + 1) / 2;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(B1) * B1 + B1 + static_cast<size_t>(w) * B1 +
-                                        static_cast<size_t>(w) * w + w + 2 * B1 + 2 * w +
-                                        static_cast<size_t>(kPrefetch) * (B1 + w + 1)) +
-                      sizeof(short) * 2 * static_cast<size_t>(P) + 16;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(band_factor_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-  band_factor_k<<<1, 32, smem, s>>>(buf, primal, n, b, w, delta_w, delta_c, Dinv, inertia);
+void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_w, double delta_c, double* Dinv,
+                 long long* inertia_parts, long long* inertia, cudaStream_t s) {
+  if (P.smem_factor > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(factor_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P.smem_factor));
+  factor_k<<<P.nseg, kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv,
+                                                         inertia_parts);
+  int blocks = P.nseg;
+  if (P.nseg > 1) {
+    const int64_t per = static_cast<int64_t>(P.wmax) * P.wmax;
+    for (int par = 0; par < 2; ++par)
+      schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
+    if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
+    factor_k<<<1, kFactorThreads, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv,
+                                                      inertia_parts);
+    blocks += 1;
+  }
+  inertia_sum_k<<<1, 32, 0, s>>>(inertia_parts, blocks, inertia);
 }
 
-void band_solve(const double* buf, const double* Dinv, const int64_t* perm, int64_t n, int b, int w,
-                const double* rhs, double* x, double* work, cudaStream_t s) {
-  const int64_t dim = n + w;
-  gather_k<<<grid_for(dim), 256, 0, s>>>(rhs, perm, dim, work);
-  const size_t smem = sizeof(double) * (static_cast<size_t>(b + 1) + w + static_cast<size_t>(kPrefetch) * (b + 3 + w));
-  band_solve_k<<<1, 32, smem, s>>>(buf, Dinv, n, b, w, work);
-  scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, perm, dim, x);
+void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
+                double* x, double* work, cudaStream_t s) {
+  const int64_t dim = P.dim;
+  double* gparts = work + dim;
+  if (P.smem_solve > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P.smem_solve));
+  gather_k<<<grid_for(dim), 256, 0, s>>>(rhs, D.perm, dim, work);
+  if (P.nseg == 1) {
+    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, 0);
+  } else {
+    const BandSeg& sep = P.segs.back();
+    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    for (int par = 0; par < 2; ++par)
+      rhs_add_k<<<grid_for(((P.nseg + 1) / 2) * P.wmax), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos,
+                                                                        gparts, work + sep.pos);
+    if (P.wg > 0) rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos);
+    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+  }
+  scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, D.perm, dim, x);
 }
 
 }  // namespace dev

@@ -1,4 +1,5 @@
-// Device LDL^T of the KKT matrix in a node-major band-plus-border ordering.
+// Device LDL^T of the KKT matrix in a node-major band-plus-border ordering,
+// partitioned in time for parallelism.
 //
 // Stand-in for the sparse factorization the reference runs on the host
 // (proj/src/sparse/ldl.cpp:139-272) and the paper runs in cuDSS, which this
@@ -6,8 +7,17 @@
 // ordered by time node (each node's primal slots, then the slacks and the
 // duals of the rows whose last coupled node it is), is banded with a
 // bandwidth of a few node blocks; free variables such as a free final time
-// couple every node and are ordered last as a dense border. The factorization
-// keeps the reference's conventions: 1x1 pivots only, +delta_w on primal and
+// couple every node and are ordered last as a dense border.
+//
+// One level of nested dissection makes it parallel: the band is cut into P
+// segments separated by b-wide separators. Every segment's interior is
+// factored independently (one thread block each) together with its border
+// rows (left separator, global border, right separator), leaving a Schur
+// complement on those rows; the separators and the global border then form a
+// block-tridiagonal band system that is factored last. Sylvester's law makes
+// the inertia the sum of the parts'.
+//
+// Conventions of the reference kept: 1x1 pivots only, +delta_w on primal and
 // -delta_c on dual diagonals, a pivot counts as zero when
 // |d| <= 1e-14 * max(|a_kk + delta|, max |update|) and is then skipped by all
 // later updates, and the inertia is reported as (positive, negative, zero).
@@ -20,35 +30,61 @@
 
 namespace ocg {
 
-struct BandPlan {
-  int64_t dim = 0;  // KKT dimension = n + w
-  int64_t n = 0;    // banded part
-  int b = 0;        // lower bandwidth
-  int w = 0;        // border (dense) rows, ordered last
-  std::vector<int64_t> perm;    // position -> KKT index
-  std::vector<int64_t> dst;     // K entry p -> flat offset in the factor buffer
-  std::vector<double> primal;   // per position: 1 = primal (+delta_w), 0 = dual (-delta_c)
-  int64_t buf_len() const { return n * (b + 1) + static_cast<int64_t>(w) * n + static_cast<int64_t>(w) * w; }
+// One banded block with a dense border (a segment, or the separator system).
+struct BandSeg {
+  long long n = 0;       // interior (banded) columns
+  int b = 0;             // lower bandwidth
+  int w = 0;             // border rows
+  int w_early = 0;       // rows [0, w_early) couple from column 0, the rest only to the last b columns
+  int finalize = 0;      // 1: factor the border block too; 0: leave its Schur complement in S
+  long long band = 0;    // offsets (doubles) into the factor buffer: band n*(b+1), column-major by column
+  long long border = 0;  // w*n, row-major (t*n + c)
+  long long S = 0;       // w*w
+  long long pos = 0;     // first position (Dinv / flags / vector index) of the interior columns
+  long long bpos = -1;   // finalize: first position of the border rows
 };
 
-// node[i]: time node of KKT index i, or -1 for a border index. Ordering:
-// (node, i) for banded indices — callers number indices so that primal
-// slots precede slacks precede duals. colp/rowi: lower CSC of K.
+struct BandPlan {
+  int64_t dim = 0;
+  int b = 0;        // segment bandwidth
+  int wg = 0;       // global border rows
+  int nseg = 0;     // P segments (1 = no partition: the single block is finalized)
+  std::vector<BandSeg> segs;  // P segments, then the separator system (when P > 1)
+  std::vector<int64_t> perm;  // position -> KKT index
+  std::vector<int64_t> dst;   // K entry p -> flat offset in the factor buffer
+  std::vector<double> primal; // per position: 1 = primal (+delta_w), 0 = dual (-delta_c)
+  // separator-system position of every segment border row: [seg * wmax + t], -1 = none
+  std::vector<int64_t> border_pos;
+  int wmax = 0;                // border rows per segment (uniform stride)
+  int64_t buf_len = 0;
+  size_t smem_factor = 0, smem_solve = 0;
+};
+
+// node[i]: time node of KKT index i, or -1 for a border index. Indices of one
+// node keep their KKT order (primal slots, slacks, duals). colp/rowi: lower CSC.
 BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std::vector<int64_t>& colp,
-                        const std::vector<int64_t>& rowi, int64_t ntot);
+                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments = 296);
 
 namespace dev {
 
-// buf = P K P^T in band/border layout (zeroed first)
-void band_assemble(const double* kval, const int64_t* dst, int64_t nnz, double* buf, int64_t len, cudaStream_t s);
+struct BandDev {  // device copies of the plan
+  const BandSeg* segs = nullptr;
+  const int64_t* dst = nullptr;
+  const int64_t* perm = nullptr;
+  const double* primal = nullptr;
+  const int64_t* border_pos = nullptr;
+};
 
-// in-place LDL^T of buf; Dinv[dim] (position order); inertia[3] (device int64)
-void band_factor(double* buf, const double* primal, int64_t n, int b, int w, double delta_w, double delta_c,
-                 double* Dinv, long long* inertia, cudaStream_t s);
+// buf = P K P^T scattered into the segment and separator blocks (zeroed first)
+void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, double* buf, cudaStream_t s);
 
-// x = (P^T L D L^T P)^{-1} rhs; rhs, x in KKT index order; work[dim] scratch
-void band_solve(const double* buf, const double* Dinv, const int64_t* perm, int64_t n, int b, int w,
-                const double* rhs, double* x, double* work, cudaStream_t s);
+// in-place LDL^T; Dinv[dim] by position; inertia (device, 3 x int64) = (pos, neg, zero)
+void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_w, double delta_c, double* Dinv,
+                 long long* inertia_parts, long long* inertia, cudaStream_t s);
+
+// x = (K + deltas)^{-1} rhs (KKT index order); work[dim + nseg*wmax] scratch
+void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
+                double* x, double* work, cudaStream_t s);
 
 }  // namespace dev
 }  // namespace ocg

@@ -163,9 +163,11 @@ struct ocg_kkt {
 struct ocg_ldl {
   ocg_kkt* kkt = nullptr;
   ocg::BandPlan plan;
-  DBuf<int64_t> dst, perm;
+  DBuf<int64_t> dst, perm, border_pos;
+  DBuf<ocg::BandSeg> segs;
   DBuf<double> primal, buf, Dinv, work;
-  DBuf<long long> inertia;
+  DBuf<long long> inertia, inertia_parts;
+  ocg::dev::BandDev dev;
   double delta_w = 0.0, delta_c = 0.0;
   int64_t factorizations = 0;
 };
@@ -1140,14 +1142,25 @@ int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
     node[static_cast<size_t>(k->ntot + d)] = row_node[static_cast<size_t>(k->dual_row[static_cast<size_t>(d)])];
   auto L = std::make_unique<ocg_ldl>();
   L->kkt = k;
-  L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot);
-  L->dst.upload(L->plan.dst);
-  L->perm.upload(L->plan.perm);
-  L->primal.upload(L->plan.primal);
-  L->buf.alloc(static_cast<size_t>(std::max<int64_t>(1, L->plan.buf_len())));
+  int target = 2 * 148;
+  if (const char* e = std::getenv("OCG_LDL_SEGMENTS")) target = std::max(1, std::atoi(e));
+  L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot, target);
+  const ocg::BandPlan& P = L->plan;
+  L->dst.upload(P.dst);
+  L->perm.upload(P.perm);
+  L->primal.upload(P.primal);
+  L->border_pos.upload(P.border_pos.empty() ? std::vector<int64_t>{-1} : P.border_pos);
+  L->segs.upload(P.segs);
+  L->buf.alloc(static_cast<size_t>(std::max<int64_t>(1, P.buf_len)));
   L->Dinv.alloc(static_cast<size_t>(std::max<int64_t>(1, k->dim)));
-  L->work.alloc(static_cast<size_t>(std::max<int64_t>(1, k->dim)));
+  L->work.alloc(static_cast<size_t>(std::max<int64_t>(1, k->dim + static_cast<int64_t>(P.nseg) * P.wmax)));
   L->inertia.alloc(3);
+  L->inertia_parts.alloc(static_cast<size_t>(3 * (P.nseg + 1)));
+  L->dev.segs = L->segs.p;
+  L->dev.dst = L->dst.p;
+  L->dev.perm = L->perm.p;
+  L->dev.primal = L->primal.p;
+  L->dev.border_pos = L->border_pos.p;
   *out = L.release();
   return OCG_OK;
   OCG_GUARD_END
@@ -1158,9 +1171,9 @@ void ocg_ldl_destroy(ocg_ldl* l) { delete l; }
 int ocg_ldl_info(const ocg_ldl* l, int64_t* out) {
   if (!l || !out) return fail(OCG_ERR_ARG, "null argument");
   out[0] = l->plan.dim;
-  out[1] = l->plan.n;
+  out[1] = l->plan.nseg;
   out[2] = l->plan.b;
-  out[3] = l->plan.w;
+  out[3] = l->plan.wg;
   out[4] = l->factorizations;
   return OCG_OK;
 }
@@ -1169,9 +1182,9 @@ int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia,
   if (!l) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   const ocg::BandPlan& P = l->plan;
-  ocg::dev::band_assemble(l->kkt->val.p, l->dst.p, static_cast<int64_t>(P.dst.size()), l->buf.p, P.buf_len(), st(s));
-  ocg::dev::band_factor(l->buf.p, l->primal.p, P.n, P.b, P.w, delta_w, delta_c, l->Dinv.p, l->inertia.p, st(s));
-  l->kkt->ev->launches += 3;
+  ocg::dev::band_assemble(P, l->dev, l->kkt->val.p, l->buf.p, st(s));
+  ocg::dev::band_factor(P, l->dev, l->buf.p, delta_w, delta_c, l->Dinv.p, l->inertia_parts.p, l->inertia.p, st(s));
+  l->kkt->ev->launches += P.nseg > 1 ? 7 : 4;
   l->delta_w = delta_w;
   l->delta_c = delta_c;
   ++l->factorizations;
@@ -1189,8 +1202,8 @@ int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
   if (!l || !rhs || !x) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   const ocg::BandPlan& P = l->plan;
-  ocg::dev::band_solve(l->buf.p, l->Dinv.p, l->perm.p, P.n, P.b, P.w, rhs, x, l->work.p, st(s));
-  l->kkt->ev->launches += 3;
+  ocg::dev::band_solve(P, l->dev, l->buf.p, l->Dinv.p, rhs, x, l->work.p, st(s));
+  l->kkt->ev->launches += P.nseg > 1 ? 8 : 3;
   return OCG_OK;
   OCG_GUARD_END
 }

@@ -311,7 +311,7 @@ class BandLdl:
     def info(self) -> dict:
         o = np.zeros(5, dtype=np.int64)
         check(LIB.ocg_ldl_info(self._h, o.ctypes.data))
-        return dict(zip(["dim", "n_band", "bandwidth", "border", "factorizations"], (int(v) for v in o)))
+        return dict(zip(["dim", "segments", "bandwidth", "border", "factorizations"], (int(v) for v in o)))
 
     def factor(self, delta_w: float = 0.0, delta_c: float = 0.0) -> tuple[int, int, int]:
         """Factor the assembled K.val; returns the inertia (positive, negative, zero)."""

@@ -55,14 +55,21 @@ def _dense(k, val, dw, dc):
 
 
 @pytest.mark.parametrize("name", ["double_integrator", "goddard", "quadrotor", "cart_pendulum", "shuttle"])
-def test_band_ldl_inertia_and_solve(name):
+@pytest.mark.parametrize("segments", ["1", "296"])
+def test_band_ldl_inertia_and_solve(name, segments, monkeypatch):
+    """One banded block, or the time-partitioned factorization (segments +
+    separator system): inertia equal to the dense eigenvalue count, solves
+    equal to a dense solve."""
+    monkeypatch.setenv("OCG_LDL_SEGMENTS", segments)
     m, ec, k, _ = _setup(name, 60)
     sigma = np.random.default_rng(5).uniform(0.5, 2.0, k.ntot)
     k.assemble(sigma)
     val = k.values().cpu().numpy()
     ldl = BandLdl(k)
     info = ldl.info()
-    assert info["dim"] == k.dim and info["bandwidth"] <= 62
+    assert info["dim"] == k.dim and info["bandwidth"] <= 60
+    if segments == "1":
+        assert info["segments"] == 1
     for dw, dc in [(0.0, 0.0), (1e-2, 0.0), (10.0, 1e-8)]:
         K = _dense(k, val, dw, dc)
         ev = np.linalg.eigvalsh(K)
