@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--secondary", action="store_true",
                     help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
+    ap.add_argument("--solve", default="quadrotor:100000",
+                    help="model:N of the full IPM solve leg ('ipm_solve' key; 'none' to skip)")
     return ap.parse_args()
 
 
@@ -442,10 +444,50 @@ def run_ours(args) -> None:
                                        "sample": f"unavailable: {ex}"}
         if args.secondary and world == 1:
             out["extra"] = secondary(dev, stream, flush, sink, peak)
+        if args.solve != "none" and world == 1:
+            out["ipm_solve"] = ipm_solve_leg(args.solve, not args.no_cpu_baseline)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ipm_solve_leg(spec: str, with_reference: bool) -> dict:
+    """Full interior-point solve (BASELINE metric: "IPM solve time at N=1e5"):
+    ocg_ipm_solve — the reference's filter line-search IPM with evaluations,
+    KKT assembly, vector work and the time-partitioned band LDL^T all on the
+    device — against the reference's own ipm::solve (oracle/_ref/libref.so,
+    Backend::parallel on all host cores, its CPU LDL^T). Wall times of the
+    solve call; the device time includes the one-time NVRTC compile of the
+    model's kernels (reported separately as jit_s from a second solve)."""
+    from paper_2510_03932_b200 import MODELS, Model, solve
+    name, N = spec.split(":")
+    N = int(N)
+    m = Model(MODELS[name], N)
+    t0 = time.perf_counter()
+    d = solve(m)
+    t_first = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    d2 = solve(m)  # kernels now in the compile cache
+    t_second = time.perf_counter() - t0
+    out = {"model": name, "N": N, "status": d2["status_name"], "iterations": d2["iterations"],
+           "objective": d2["objective"], "device_s": t_second, "device_s_incl_jit": t_first,
+           "jit_s": max(0.0, t_first - t_second), "factorizations": d2["factorizations"],
+           "time_factorize_s": d2["time_factorize"], "time_solve_s": d2["time_solve"],
+           "time_derivatives_s": d2["time_derivatives"], "factorization": "time-partitioned band LDL^T (device)"}
+    if with_reference:
+        RefEval, RefModel = _ref_modules()
+        cores = os.cpu_count() or 1
+        rm = RefModel(MODELS[name], N)
+        t0 = time.perf_counter()
+        r = rm.solve(parallel=True, workers=cores)
+        out["reference"] = {"wall_s": time.perf_counter() - t0, "iterations": int(r["iterations"]),
+                            "objective": r["objective"], "status": int(r["status"]), "cores": cores,
+                            "time_factorize_s": r["time_factorize"], "time_derivatives_s": r["time_derivatives"]}
+        out["iterations_match"] = int(r["iterations"]) == d2["iterations"]
+        out["objective_rel_diff"] = abs(r["objective"] - d2["objective"]) / max(abs(r["objective"]), 1e-300)
+        out["speedup_vs_reference"] = out["reference"]["wall_s"] / t_second
+    return out
 
 
 def ec_block(ec) -> int:
