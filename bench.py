@@ -474,7 +474,10 @@ def ipm_solve_leg(spec: str, with_reference: bool) -> dict:
            "objective": d2["objective"], "device_s": t_second, "device_s_incl_jit": t_first,
            "jit_s": max(0.0, t_first - t_second), "factorizations": d2["factorizations"],
            "time_factorize_s": d2["time_factorize"], "time_solve_s": d2["time_solve"],
-           "time_derivatives_s": d2["time_derivatives"], "factorization": "time-partitioned band LDL^T (device)"}
+           "time_derivatives_s": d2["time_derivatives"], "time_total_s": d2["time_total"],
+           "time_setup_s": d2["time_setup"], "plan_s": {"eval": d2["time_plan_eval"], "kkt": d2["time_plan_kkt"],
+                                                       "ldl": d2["time_plan_ldl"]},
+           "factorization": "time-partitioned band LDL^T (device)"}
     if with_reference:
         RefEval, RefModel = _ref_modules()
         cores = os.cpu_count() or 1

@@ -134,8 +134,9 @@ typedef struct {
   int min_blocks;   /* resident blocks per SM the kernels are register-budgeted for
                        (__launch_bounds__); 0 = auto: the largest budget <= 6 that the
                        shared memory allows and that compiles without spills */
-  int split_kinds;  /* stage each output kind (c, J, H) of a group through one shared
-                       region: -1 = auto (when it lets more blocks reside), 0 = no, 1 = yes */
+  int split_kinds;  /* shared-memory staging of the outputs: 0 = one region reused group
+                       after group, 1 = one region per output kind in turn, 2 = a region
+                       per group (one wait per tile); -1 = auto */
 } ocg_eval_options;
 
 void ocg_eval_default_options(ocg_eval_options* o);
@@ -252,6 +253,9 @@ typedef struct {
   int factorizations;
   double time_total, time_derivatives, time_factorize, time_solve;
   int64_t kkt_dim, kkt_nnz, bandwidth;
+  /* one-time host/device setup, not in time_total: eval plan (incl. NVRTC),
+   * KKT pattern, factorization plan; then bounds/start point (in time_total) */
+  double time_plan_eval, time_plan_kkt, time_plan_ldl, time_setup;
 } ocg_ipm_result;
 
 void ocg_ipm_default_options(ocg_ipm_options* o);

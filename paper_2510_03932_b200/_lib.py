@@ -51,7 +51,8 @@ class IpmResult(C.Structure):
                 ("stationarity", C.c_double), ("complementarity", C.c_double), ("factorizations", C.c_int),
                 ("time_total", C.c_double), ("time_derivatives", C.c_double), ("time_factorize", C.c_double),
                 ("time_solve", C.c_double), ("kkt_dim", C.c_int64), ("kkt_nnz", C.c_int64),
-                ("bandwidth", C.c_int64)]
+                ("bandwidth", C.c_int64), ("time_plan_eval", C.c_double), ("time_plan_kkt", C.c_double),
+                ("time_plan_ldl", C.c_double), ("time_setup", C.c_double)]
 
 
 class OcgError(RuntimeError):

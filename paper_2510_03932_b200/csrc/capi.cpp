@@ -260,19 +260,19 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
     return mx;
   };
   if (const char* e = std::getenv("OCG_SPLIT")) split = std::atoi(e);
+  // output staging: 0 one region reused group after group, 1 one region per
+  // output kind in turn, 2 a region per group (one wait per tile). Auto: a
+  // region per group while three 4-warp blocks of the fused kernel still fit
+  // (the register budget of these kernels rarely allows more), else shared.
   if (split < 0) {
-    // stage output kinds separately when that lets more blocks of the fused
-    // kernel reside (shared memory is then the occupancy limit)
-    auto blocks = [&](const ocg::Generated& g) {
-      return std::min(target, smem_per_sm / std::max(1, g.smem.at("ocg_cjh") + 1024));
-    };
     go.split_kinds = false;
-    const int b0 = blocks(ocg::generate(nlp, lay, go));
-    go.split_kinds = true;
-    const int b1 = blocks(ocg::generate(nlp, lay, go));
-    go.split_kinds = b1 > b0;
+    go.distinct_regions = true;
+    const ocg::Generated g2 = ocg::generate(nlp, lay, go);
+    const int per_block = g2.smem.at("ocg_cjh") * 128 / std::max(1, go.block) + 1024;
+    go.distinct_regions = 3 * per_block <= smem_per_sm;
   } else {
-    go.split_kinds = split > 0;
+    go.split_kinds = split == 1;
+    go.distinct_regions = split == 2;
   }
   ocg::Generated gen = ocg::generate(nlp, lay, go);
   // shared memory per block scales with warps per block: halve the block
@@ -325,6 +325,7 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
   gen.min_blocks = go.min_blocks;
   gen.block = go.block;
   gen.split_kinds = go.split_kinds;
+  gen.distinct_regions = go.distinct_regions;
   return gen;
 }
 
@@ -948,11 +949,20 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   }
   for (Index i = 0; i < K->ntot; ++i) srcs.push_back({i, i, K->H + K->J + S + i});
   for (Index r = 0; r < K->m; ++r) srcs.push_back({K->ntot + r, K->ntot + r, -1});  // dual diagonal: no source
-  std::sort(srcs.begin(), srcs.end(), [](const Src& a, const Src& b) {
-    if (a.col != b.col) return a.col < b.col;
-    if (a.row != b.row) return a.row < b.row;
-    return a.code < b.code;
-  });
+  // (col, row, code) order: counting sort by column, then each (short)
+  // column sorted by (row, code)
+  {
+    std::vector<int64_t> cstart(static_cast<size_t>(K->dim) + 1, 0);
+    for (const Src& e : srcs) cstart[static_cast<size_t>(e.col) + 1]++;
+    for (Index j = 0; j < K->dim; ++j) cstart[static_cast<size_t>(j) + 1] += cstart[static_cast<size_t>(j)];
+    std::vector<Src> sorted(srcs.size());
+    std::vector<int64_t> fill(cstart.begin(), cstart.end() - 1);
+    for (const Src& e : srcs) sorted[static_cast<size_t>(fill[static_cast<size_t>(e.col)]++)] = e;
+    for (Index j = 0; j < K->dim; ++j)
+      std::sort(sorted.begin() + cstart[static_cast<size_t>(j)], sorted.begin() + cstart[static_cast<size_t>(j) + 1],
+                [](const Src& a, const Src& b) { return a.row != b.row ? a.row < b.row : a.code < b.code; });
+    srcs.swap(sorted);
+  }
   K->colp.assign(static_cast<size_t>(K->dim) + 1, 0);
   std::vector<int64_t> sptr{0}, scode;
   for (size_t q = 0; q < srcs.size(); ++q) {
@@ -1215,7 +1225,10 @@ extern "C" char* ocg_debug_generated_source(const ocg_model* m, int fma, int blo
   ocg::GenOptions go;
   go.fma = fma != 0;
   go.block = block > 0 ? block : 128;
-  if (const char* e = std::getenv("OCG_SPLIT")) go.split_kinds = std::atoi(e) > 0;
+  if (const char* e = std::getenv("OCG_SPLIT")) {
+    go.split_kinds = std::atoi(e) == 1;
+    go.distinct_regions = std::atoi(e) == 2;
+  }
   const ocg::Generated gen = ocg::generate(m->nlp, ocg::make_layout(m->nlp), go);
   std::string s = gen.source + "// ocg-meta {";
   bool first = true;
@@ -1251,7 +1264,8 @@ extern "C" char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_option
                           &log);
     std::string s = log + "\n// min_blocks:";
     for (const auto& [k, v] : gen.min_blocks) s += " " + k + "=" + std::to_string(v);
-    s += " block=" + std::to_string(gen.block) + " split_kinds=" + std::to_string(gen.split_kinds ? 1 : 0) + "\n";
+    s += " block=" + std::to_string(gen.block) + " staging=" +
+         std::to_string(gen.split_kinds ? 1 : (gen.distinct_regions ? 2 : 0)) + "\n";
     char* out = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(out, s.c_str(), s.size() + 1);
     return out;

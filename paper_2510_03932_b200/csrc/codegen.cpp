@@ -356,6 +356,15 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
   // called before every shared-memory store of the current group with the
   // output kind: emits the waits/flushes of the staged copy-out
   std::function<void(int)> store_hook_;
+  bool first_store_of_tile_ = false;
+  std::map<std::string, std::string> slices_;  // range params -> slice variable suffix
+  // range bounds as parameters keyed by value, so groups with equal ranges
+  // share them (and their per-tile slice)
+  std::string range_param(const Range& r, bool lo) {
+    const Index v = lo ? r.lo : r.hi;
+    return P(std::string(lo ? "range.lo=" : "range.hi=") + std::to_string(v), v);
+  }
+  std::string slice_of(const Range& r) { return slices_.at(range_param(r, true) + "," + range_param(r, false)); }
 
   // Grid-size-dependent integers live in a by-value parameter block keyed by
   // their meaning, so the generated source — and its cached cubin — depends
@@ -889,12 +898,13 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     };
     std::vector<std::vector<Out>> outs(members.size());
     Index region = 0;
+    Index running = cur;  // distinct regions: every group's outputs at their own offsets
     for (size_t q = 0; q < members.size(); ++q) {
       const Inst& mb = members[q];
       const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
       const Parts p = parts(m, mb.objective, g);
       const size_t gi = static_cast<size_t>(mb.gi);
-      Index off = cur;
+      Index off = opt_.distinct_regions ? running : cur;
       auto add_out = [&](int kind, Index per_k, const std::string& dst) {
         if (per_k <= 0) return;
         const Index pitch = per_k;  // unpadded: the copy-out is one linear bulk copy
@@ -917,6 +927,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
                 "hess + " + (mb.objective ? G(true, mb.gi, "hess_off", lay_.hess_off_obj[gi])
                                           : G(false, mb.gi, "hess_off", lay_.hess_off_con[gi])));
       region = std::max(region, off - cur);
+      running = off;
     }
     Index per_warp = cur + region;  // doubles of shared memory per warp
     per_warp += per_warp & 1;       // keep every warp's base 16-byte aligned (bulk copies)
@@ -950,6 +961,23 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     E.line("const long long ib = i0 + tile * 32;");
     E.line("const long long idx = ib + lane;");
     E.line("const bool in = idx < i0 + n_main;");
+    // the tile's slice of every distinct group range
+    slices_.clear();
+    for (const Inst& mb : members) {
+      const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+      const std::string key = range_param(g.range, true) + "," + range_param(g.range, false);
+      if (slices_.count(key)) continue;
+      const std::string R = std::to_string(slices_.size());
+      slices_[key] = R;
+      const std::string lo = range_param(g.range, true), hi = range_param(g.range, false);
+      E.line("const long long kb" + R + " = ib - " + lo + ";");
+      E.line("const long long k0" + R + " = kb" + R + " > 0 ? kb" + R + " : 0;");
+      E.line("long long k1" + R + " = kb" + R + " + 32; if (k1" + R + " > " + hi + " - " + lo + ") k1" + R + " = " + hi +
+             " - " + lo + "; if (k1" + R + " > i0 + n_main - " + lo + ") k1" + R + " = i0 + n_main - " + lo + ";");
+      E.line("const int nk" + R + " = k1" + R + " > k0" + R + " ? (int)(k1" + R + " - k0" + R + ") : 0, r0" + R +
+             " = (int)(k0" + R + " - kb" + R + ");");
+    }
+    first_store_of_tile_ = true;
     // stage every global input of the tile with asynchronous copies, then wait once
     for (auto& [s, u] : uses) {
       const Slab& sl = nlp_.slabs[s];
@@ -965,17 +993,12 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       if (rows[q].rs < 0 && rows[q].lam < 0) continue;
       const Inst& mb = members[q];
       const Group& g = nlp_.cons[static_cast<size_t>(mb.gi)];
-      const std::string lo = G(false, mb.gi, "lo", g.range.lo);
-      const std::string hi = G(false, mb.gi, "hi", g.range.hi);
       const std::string rb = G(false, mb.gi, "row_base", g.row_base);
       const std::string od = i64(g.out_dim());
+      const std::string R = slice_of(g.range);
       E.open("");
-      E.line("const long long kb = ib - " + lo + ";");
-      E.line("const long long k0 = kb > 0 ? kb : 0;");
-      E.line("long long k1 = kb + 32; if (k1 > " + hi + " - " + lo + ") k1 = " + hi + " - " + lo +
-             "; if (k1 > i0 + n_main - " + lo + ") k1 = i0 + n_main - " + lo + ";");
-      E.line("const int nr = k1 > k0 ? (int)((k1 - k0) * " + od + ") : 0, so = (int)((k0 - kb) * " + od + ");");
-      E.line("const long long g0 = " + rb + " + k0 * " + od + ";");
+      E.line("const int nr = nk" + R + " * (int)" + od + ", so = r0" + R + " * (int)" + od + ";");
+      E.line("const long long g0 = " + rb + " + k0" + R + " * " + od + ";");
       if (rows[q].rs >= 0)
         E.line("for (int j = lane; j < nr; j += 32) ocg_cp8(smem + " + i64(rows[q].rs) + " + so + j, rs + g0 + j);");
       if (rows[q].lam >= 0)
@@ -999,34 +1022,29 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       const Inst& mb = members[q];
       const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
       const Parts p = parts(m, mb.objective, g);
-      const std::string lo = G(mb.objective, mb.gi, "lo", g.range.lo);
-      const std::string hi = G(mb.objective, mb.gi, "hi", g.range.hi);
-      // this tile's slice of the group: instances [k0, k1), lanes r0..r0+nk-1;
-      // each output kind's rows start at a shift of 0 or 1 double so that the
-      // shared-memory source and the global destination agree modulo 16 bytes
+      const std::string lo = range_param(g.range, true);
+      const std::string hi = range_param(g.range, false);
+      // this tile's slice of the group (shared by every group of the same
+      // range): instances [k0, k1), lanes r0..r0+nk-1; each output kind's rows
+      // start at a shift of 0 or 1 double so that the shared-memory source and
+      // the global destination agree modulo 16 bytes
       const std::string qn = std::to_string(q);
+      const std::string R = slice_of(g.range);
       if (!outs[q].empty()) {
-        E.line("const long long kb" + qn + " = ib - " + lo + ";");
-        E.line("const long long k0" + qn + " = kb" + qn + " > 0 ? kb" + qn + " : 0;");
-        E.line("long long k1" + qn + " = kb" + qn + " + 32; if (k1" + qn + " > " + hi + " - " + lo + ") k1" + qn +
-               " = " + hi + " - " + lo + "; if (k1" + qn + " > i0 + n_main - " + lo + ") k1" + qn +
-               " = i0 + n_main - " + lo + ";");
-        E.line("const int nk" + qn + " = k1" + qn + " > k0" + qn + " ? (int)(k1" + qn + " - k0" + qn + ") : 0, r0" +
-               qn + " = (int)(k0" + qn + " - kb" + qn + ");");
         for (size_t oi = 0; oi < outs[q].size(); ++oi) {
           const Out& o = outs[q][oi];
           const std::string S = i64(o.per_k);
-          E.line("const int sh" + qn + "_" + std::to_string(oi) + " = ocg_shift(" + o.dst + " + k0" + qn + " * " + S +
-                 ", smem + " + i64(o.soff) + " + r0" + qn + " * " + S + ");");
+          E.line("const int sh" + qn + "_" + std::to_string(oi) + " = ocg_shift(" + o.dst + " + k0" + R + " * " + S +
+                 ", smem + " + i64(o.soff) + " + r0" + R + " * " + S + ");");
         }
       }
       // staged copy-out of output kind oi of this group
-      auto flush = [&, qn](size_t oi) {
+      auto flush = [&, qn, R](size_t oi) {
         const Out& o = outs[q][oi];
         const std::string S = i64(o.per_k);
         E.line("ocg_fence_async(); __syncwarp();");
-        E.line("if (lane == 0 && nk" + qn + " > 0) { ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " +
-               i64(o.soff) + " + sh" + qn + "_" + std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn +
+        E.line("if (lane == 0 && nk" + R + " > 0) { ocg_bulk_store(" + o.dst + " + k0" + R + " * " + S + ", smem + " +
+               i64(o.soff) + " + sh" + qn + "_" + std::to_string(oi) + " + r0" + R + " * " + S + ", nk" + R +
                " * (int)" + S + "); ocg_bulk_commit(); }");
       };
       int cur_kind = -2;  // -2: nothing stored yet in this group
@@ -1036,8 +1054,11 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
           for (size_t oi = 0; oi < outs[q].size(); ++oi)
             if (outs[q][oi].kind == cur_kind) flush(oi);
         }
-        if (cur_kind == -2 || opt_.split_kinds)  // region free again?
+        // region free again? (distinct regions: only the tile's first store
+        // waits, for the previous tile's copy-out)
+        if ((cur_kind == -2 && (!opt_.distinct_regions || first_store_of_tile_)) || opt_.split_kinds)
           E.line("if (lane == 0) ocg_bulk_wait_read(); __syncwarp();");
+        first_store_of_tile_ = false;
         cur_kind = kind;
       };
       store_to_ = [&](int kind, Index e) -> std::string {
@@ -1081,12 +1102,12 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
           if (outs[q][oi].kind == cur_kind) flush(oi);
       } else {
         E.line("ocg_fence_async(); __syncwarp();");
-        E.open("if (lane == 0 && nk" + qn + " > 0)");
+        E.open("if (lane == 0 && nk" + R + " > 0)");
         for (size_t oi = 0; oi < outs[q].size(); ++oi) {
           const Out& o = outs[q][oi];
           const std::string S = i64(o.per_k);
-          E.line("ocg_bulk_store(" + o.dst + " + k0" + qn + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
-                 std::to_string(oi) + " + r0" + qn + " * " + S + ", nk" + qn + " * (int)" + S + ");");
+          E.line("ocg_bulk_store(" + o.dst + " + k0" + R + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
+                 std::to_string(oi) + " + r0" + R + " * " + S + ", nk" + R + " * (int)" + S + ");");
         }
         E.line("ocg_bulk_commit();");
         E.close();

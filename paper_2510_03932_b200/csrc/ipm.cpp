@@ -88,14 +88,20 @@ struct DVec {
 class DeviceSolver {
  public:
   DeviceSolver(ocg_model* model, const ocg_ipm_options& o, int device) : model_(model), o_(o) {
+    Clock t;
     ckc(cudaSetDevice(device), "cudaSetDevice");
     ckc(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
     ocg_eval_options eo;
     ocg_eval_default_options(&eo);
     eo.device = device;
     cko(ocg_eval_create(model, &eo, &ev_), "eval_create");
+    r_.time_plan_eval = t.elapsed();
+    Clock t2;
     cko(ocg_kkt_create(model, ev_, &kkt_), "kkt_create");
+    r_.time_plan_kkt = t2.elapsed();
+    Clock t3;
     cko(ocg_ldl_create(kkt_, &ldl_), "ldl_create");
+    r_.time_plan_ldl = t3.elapsed();
   }
   ~DeviceSolver() {
     if (ldl_) ocg_ldl_destroy(ldl_);
@@ -501,6 +507,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
   mu_ = o_.mu_init;
   tau_ = std::max(o_.tau_min, 1.0 - mu_);
   setup(row_scale);
+  r_.time_setup = total.elapsed();
   if (contradictory_) {
     r_.status = 2;
     r_.time_total = total.elapsed();

@@ -37,6 +37,9 @@ struct GenOptions {
   // stage one output kind (c, J, H, ...) of a group at a time through a
   // single shared-memory region (less shared memory, more warps resident)
   bool split_kinds = false;
+  // every group's outputs in their own shared region: one wait per tile
+  // instead of one per group (more shared memory per warp)
+  bool distinct_regions = false;
 };
 
 struct Generated {
@@ -56,6 +59,7 @@ struct Generated {
   std::map<std::string, int> min_blocks;
   int block = 128;
   bool split_kinds = false;
+  bool distinct_regions = false;
 };
 
 // Kernel entry points in the generated module (all extern "C"):

@@ -85,7 +85,7 @@ def test_domain_flags_match_reference(name):
 
 
 @pytest.mark.parametrize("name", ["goddard", "quadrotor", "shuttle", "cart_pendulum"])
-@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("split", ["0", "1", "2"])
 def test_fused_kernel_bit_exact(name, split, monkeypatch):
     """ocg_cjh (one launch for c, J and H) in both copy-out modes: every output
     kind staged in its own shared region, or all kinds through one region."""
