@@ -174,40 +174,94 @@ struct ocg_ldl {
 
 namespace {
 
+// parallel loop over [0, n) in contiguous chunks on the host's cores
+template <class F>
+void parallel_for(Index n, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const Index nt = std::min<Index>(static_cast<Index>(hw), std::max<Index>(1, n / 65536));
+  if (nt <= 1) {
+    f(Index{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (Index t = 0; t < nt; ++t) th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
+
 // host COO structure, exactly as EvalContext's constructor materialises it
-// (eval.cpp:83-119)
+// (eval.cpp:83-119): group-major, then index-major, pattern order within
 void host_structure(const ocg::Nlp& nlp, std::vector<Index>* jr, std::vector<Index>* jc, std::vector<Index>* hr,
                     std::vector<Index>* hc, std::vector<Index>* gc) {
+  Index nj = 0, nh = 0, ng = 0;
   for (const auto& g : nlp.cons) {
+    nj += static_cast<Index>(g.pattern.jac.size()) * g.range.count();
+    nh += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  }
+  for (const auto& g : nlp.objs) {
+    ng += static_cast<Index>(g.pattern.jac.size()) * g.range.count();
+    nh += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  }
+  if (jr) {
+    jr->resize(static_cast<size_t>(nj));
+    jc->resize(static_cast<size_t>(nj));
+  }
+  if (hr) {
+    hr->resize(static_cast<size_t>(nh));
+    hc->resize(static_cast<size_t>(nh));
+  }
+  if (gc) gc->resize(static_cast<size_t>(ng));
+  Index joff = 0, hoff = 0, goff = 0;
+  auto hess_fill = [&](const ocg::Group& g, Index base) {
     const auto& ins = g.kernel.graph.inputs();
-    for (Index k = 0; k < g.range.count(); ++k) {
-      const Index idx = g.range.at(k);
-      if (jr)
-        for (const auto& [r, j] : g.pattern.jac) {
-          jr->push_back(g.row_base + k * g.out_dim() + r);
-          jc->push_back(ins[static_cast<size_t>(j)].slot(idx));
-        }
-      if (hr)
+    const Index nnz = static_cast<Index>(g.pattern.hess.size());
+    parallel_for(g.range.count(), [&](Index k0, Index k1) {
+      for (Index k = k0; k < k1; ++k) {
+        const Index idx = g.range.at(k);
+        Index e = base + k * nnz;
         for (const auto& [a, b] : g.pattern.hess) {
           const Index sa = ins[static_cast<size_t>(a)].slot(idx), sb = ins[static_cast<size_t>(b)].slot(idx);
-          hr->push_back(std::max(sa, sb));
-          hc->push_back(std::min(sa, sb));
+          (*hr)[static_cast<size_t>(e)] = std::max(sa, sb);
+          (*hc)[static_cast<size_t>(e++)] = std::min(sa, sb);
         }
+      }
+    });
+  };
+  for (const auto& g : nlp.cons) {
+    const auto& ins = g.kernel.graph.inputs();
+    const Index cnt = g.range.count();
+    if (jr) {
+      const Index nnz = static_cast<Index>(g.pattern.jac.size());
+      parallel_for(cnt, [&](Index k0, Index k1) {
+        for (Index k = k0; k < k1; ++k) {
+          const Index idx = g.range.at(k);
+          Index e = joff + k * nnz;
+          for (const auto& [r, j] : g.pattern.jac) {
+            (*jr)[static_cast<size_t>(e)] = g.row_base + k * g.out_dim() + r;
+            (*jc)[static_cast<size_t>(e++)] = ins[static_cast<size_t>(j)].slot(idx);
+          }
+        }
+      });
     }
+    if (hr) hess_fill(g, hoff);
+    joff += static_cast<Index>(g.pattern.jac.size()) * cnt;
+    hoff += static_cast<Index>(g.pattern.hess.size()) * cnt;
   }
   for (const auto& g : nlp.objs) {
     const auto& ins = g.kernel.graph.inputs();
-    for (Index k = 0; k < g.range.count(); ++k) {
-      const Index idx = g.range.at(k);
-      if (gc)
-        for (const auto& e : g.pattern.jac) gc->push_back(ins[static_cast<size_t>(e.second)].slot(idx));
-      if (hr)
-        for (const auto& [a, b] : g.pattern.hess) {
-          const Index sa = ins[static_cast<size_t>(a)].slot(idx), sb = ins[static_cast<size_t>(b)].slot(idx);
-          hr->push_back(std::max(sa, sb));
-          hc->push_back(std::min(sa, sb));
+    const Index cnt = g.range.count();
+    if (gc) {
+      const Index nnz = static_cast<Index>(g.pattern.jac.size());
+      parallel_for(cnt, [&](Index k0, Index k1) {
+        for (Index k = k0; k < k1; ++k) {
+          const Index idx = g.range.at(k);
+          Index e = goff + k * nnz;
+          for (const auto& pr : g.pattern.jac) (*gc)[static_cast<size_t>(e++)] = ins[static_cast<size_t>(pr.second)].slot(idx);
         }
+      });
     }
+    if (hr) hess_fill(g, hoff);
+    goff += static_cast<Index>(g.pattern.jac.size()) * cnt;
+    hoff += static_cast<Index>(g.pattern.hess.size()) * cnt;
   }
 }
 
@@ -961,9 +1015,11 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     std::vector<Src> sorted(srcs.size());
     std::vector<int64_t> fill(cstart.begin(), cstart.end() - 1);
     for (const Src& e : srcs) sorted[static_cast<size_t>(fill[static_cast<size_t>(e.col)]++)] = e;
-    for (Index j = 0; j < K->dim; ++j)
-      std::sort(sorted.begin() + cstart[static_cast<size_t>(j)], sorted.begin() + cstart[static_cast<size_t>(j) + 1],
-                [](const Src& a, const Src& b) { return a.row != b.row ? a.row < b.row : a.code < b.code; });
+    parallel_for(K->dim, [&](Index j0, Index j1) {
+      for (Index j = j0; j < j1; ++j)
+        std::sort(sorted.begin() + cstart[static_cast<size_t>(j)], sorted.begin() + cstart[static_cast<size_t>(j) + 1],
+                  [](const Src& a, const Src& b) { return a.row != b.row ? a.row < b.row : a.code < b.code; });
+    });
     srcs.swap(sorted);
   }
   K->colp.assign(static_cast<size_t>(K->dim) + 1, 0);
