@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <numeric>
 #include <random>
@@ -55,25 +56,34 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
+  // Stream-ordered pool allocations on the calling thread's default stream:
+  // unlike cudaMalloc/cudaFree they never synchronize the device, so plans
+  // created and destroyed by concurrent host threads (batched solves) do not
+  // serialize each other's streams.
   ~DBuf() {
-    if (p && owned) cudaFree(p);
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
   }
   // caller-owned device memory of the same size replaces the library buffer
   void bind(T* ext) {
-    if (p && owned) cudaFree(p);
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
     p = ext;
     owned = false;
   }
   void alloc(size_t count) {
-    if (p && owned) cudaFree(p);
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
     owned = true;
     p = nullptr;
     n = count;
-    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
+       "cudaMallocAsync");
+    ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
   }
   void upload(const std::vector<T>& v) {
     alloc(v.size());
-    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    if (!v.empty()) {
+      ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, cudaStreamPerThread), "upload");
+      ck(cudaStreamSynchronize(cudaStreamPerThread), "upload sync");
+    }
   }
 };
 
@@ -90,7 +100,7 @@ struct ocg_eval {
   const ocg_model* model = nullptr;
   int device = 0;
   ocg::Layout lay;
-  std::map<std::string, std::unique_ptr<ocg::JitModule>> mods;  // one module per kernel
+  std::map<std::string, std::shared_ptr<ocg::JitModule>> mods;  // one module per kernel (process-wide cache)
   cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,
                k_grad = nullptr;
   int block = 128;
@@ -386,6 +396,24 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
   return gen;
 }
 
+// Loaded modules are shared by every eval context whose kernel compiled to the
+// same cubin (e.g. batch instances that differ only in bounds): one
+// cudaLibrary per distinct cubin per device per process.
+std::shared_ptr<ocg::JitModule> loaded_module(const std::string& cubin) {
+  static std::mutex mu;
+  static std::map<std::pair<size_t, size_t>, std::shared_ptr<ocg::JitModule>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(std::hash<std::string>{}(cubin) ^ static_cast<size_t>(dev), cubin.size());
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  auto mod = std::make_shared<ocg::JitModule>();
+  ocg::jit_load(cubin, *mod);
+  cache.emplace(key, mod);
+  return mod;
+}
+
 int auto_min_blocks(const ocg_eval_options& o) {
   if (o.min_blocks > 0) return o.min_blocks;
   if (const char* e = std::getenv("OCG_MINB")) return std::max(1, std::atoi(e));
@@ -613,11 +641,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->tail = gen.tail;
     e->smem = gen.smem;
     e->prm = gen.params;
-    for (const char* k : kKernelNames) {
-      auto mod = std::make_unique<ocg::JitModule>();
-      ocg::jit_load(cubins.at(k), *mod);
-      e->mods[k] = std::move(mod);
-    }
+    for (const char* k : kKernelNames) e->mods[k] = loaded_module(cubins.at(k));
     e->k_c = e->mods.at("ocg_c")->kernel("ocg_c");
     e->k_cjac = e->mods.at("ocg_cjac")->kernel("ocg_cjac");
     e->k_hess = e->mods.at("ocg_hess")->kernel("ocg_hess");
@@ -674,7 +698,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     for (size_t q = 0; q < gc.size(); ++q) idx[static_cast<size_t>(fill[static_cast<size_t>(gc[q])]++)] = static_cast<int32_t>(q);
     e->gg_ptr.upload(ptr);
     e->gg_idx.upload(idx);
-    ck(cudaDeviceSynchronize(), "sync");
+    ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
     *out = e.release();
     return OCG_OK;
   } catch (const CudaError& ex) {

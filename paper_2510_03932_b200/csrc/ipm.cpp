@@ -69,11 +69,13 @@ struct DVec {
   DVec(const DVec&) = delete;
   DVec& operator=(const DVec&) = delete;
   ~DVec() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamPerThread);  // stream-ordered: no device-wide sync
   }
   void alloc(size_t count) {
     n = count;
-    ckc(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    ckc(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
+        "cudaMallocAsync");
+    ckc(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     if (!v.empty()) ckc(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
