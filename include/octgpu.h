@@ -259,6 +259,18 @@ typedef struct {
 } ocg_ipm_result;
 
 void ocg_ipm_default_options(ocg_ipm_options* o);
+
+/* A reusable solver context: the evaluation plan, KKT pattern and
+ * factorization plan are built once per model structure; each solve then
+ * takes an instance's bounds and start point (NULL = the model's), e.g. the
+ * members of a batch that differ only in boundary values (BASELINE config 5).
+ * The instance must fix the same slots (equal folded bounds) as the model. */
+typedef struct ocg_ipm_ctx ocg_ipm_ctx;
+int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out);
+void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c);
+int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double* lvar, const double* uvar,
+                      const double* x_start, const double* lcon, const double* ucon, ocg_ipm_result* out,
+                      double* x_out);
 /* x_out[nvar] (host, may be NULL): final iterate */
 int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out);
 

@@ -4,7 +4,7 @@ Jacobian / Lagrangian-Hessian evaluation into the reference's COO slots, the
 atomic-free KKT assembly and the interior-point vector kernels, behind the
 reference's EvalContext / KktAssembler interface (include/octgpu.h).
 """
-from .evaluation import BandLdl, EvalContext, KktAssembler, Model, solve, synth_uniform  # noqa: F401
+from .evaluation import BandLdl, EvalContext, KktAssembler, Model, Solver, solve, synth_uniform  # noqa: F401
 from .models import MODELS  # noqa: F401
 
-__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "solve", "synth_uniform"]
+__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "Solver", "solve", "synth_uniform"]

@@ -113,8 +113,20 @@ class DeviceSolver {
   }
 
   int run(ocg_ipm_result* res, double* x_out);
+  // instance data for the next run (NULL = the model's own arrays)
+  void set_instance(const ocg_ipm_options& o, const double* lvar, const double* uvar, const double* x0,
+                    const double* lcon, const double* ucon) {
+    o_ = o;
+    inst_[0] = lvar;
+    inst_[1] = uvar;
+    inst_[2] = x0;
+    inst_[3] = lcon;
+    inst_[4] = ucon;
+  }
 
  private:
+  const double* inst_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool allocated_ = false;
   ocg_model* model_;
   ocg_ipm_options o_;
   cudaStream_t s_ = nullptr;
@@ -192,6 +204,7 @@ class DeviceSolver {
   }
 
   void setup(std::vector<double>& row_scale);
+  void alloc_state(size_t nv, size_t mc);
   double theta_of(const double* g) { return ocg::ipmdev::l1(g, m_, sc_, s_); }
   double kkt_error(double mu, const double* g, double& comp_out, double& stat_out);
   void add_to_filter(double theta, double phi);
@@ -201,6 +214,45 @@ class DeviceSolver {
   void refine_if_needed(const double* rhs, double* step);
   void finish(int status, int iter, const std::vector<double>& row_scale);
 };
+
+void DeviceSolver::alloc_state(size_t nv, size_t mc) {
+  const auto nt = static_cast<size_t>(ntot_);
+  free_slot_.alloc(static_cast<size_t>(nfree_));
+  dual_row_.alloc(static_cast<size_t>(m_));
+  slack_index_.alloc(mc);
+  lb_.alloc(nt);
+  ub_.alloc(nt);
+  has_lb_.alloc(nt);
+  has_ub_.alloc(nt);
+  lcon_s_.alloc(mc);
+  for (auto* v : {&x_, &xt_, &grad_, &gradt_}) *v = std::make_unique<DVec<double>>(nv);
+  for (auto* v : {&c_, &ct_}) *v = std::make_unique<DVec<double>>(mc);
+  for (auto* v : {&s_v_, &st_}) *v = std::make_unique<DVec<double>>(static_cast<size_t>(nslack_));
+  const auto dm = static_cast<size_t>(dim_), mm = static_cast<size_t>(m_);
+  lambda_.alloc(mm);
+  g_.alloc(mm);
+  gt_.alloc(mm);
+  gsoc_.alloc(mm);
+  zl_.alloc(nt);
+  zu_.alloc(nt);
+  sigma_.alloc(nt);
+  jtlam_.alloc(nt);
+  dzl_.alloc(nt);
+  dzu_.alloc(nt);
+  rhs_.alloc(dm);
+  rhs2_.alloc(dm);
+  step_.alloc(dm);
+  step2_.alloc(dm);
+  kx_.alloc(dm);
+  r_v_.alloc(dm);
+  dx_.alloc(dm);
+  lamfull_.alloc(mc);
+  dscal_.alloc(4);
+  partials_.alloc(2 * 148 * 8);
+  out_.alloc(8);
+  sc_.partials = partials_.p;
+  sc_.out = out_.p;
+}
 
 void DeviceSolver::setup(std::vector<double>& row_scale) {
   nvar_ = ocg_model_nvar(model_);
@@ -221,6 +273,31 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
       "model_arrays");
   std::vector<int64_t> prim(nv), slack(mc), dual(mc), rslot(mc);
   cko(ocg_kkt_maps(kkt_, prim.data(), slack.data(), dual.data(), rslot.data(), xlo.data(), xhi.data()), "kkt_maps");
+  if (inst_[0] || inst_[1] || inst_[2] || inst_[3] || inst_[4]) {
+    // another instance of the same structure: its bounds and start point, and
+    // the Reduction's folded bounds recomputed from them (eval.cpp:290-316)
+    auto take = [](std::vector<double>& v, const double* p) {
+      if (p) std::copy(p, p + v.size(), v.begin());
+    };
+    take(lvar, inst_[0]);
+    take(uvar, inst_[1]);
+    take(x0, inst_[2]);
+    take(lcon, inst_[3]);
+    take(ucon, inst_[4]);
+    xlo = lvar;
+    xhi = uvar;
+    contradictory_ = false;
+    for (size_t r = 0; r < mc; ++r) {
+      if (rslot[r] < 0) continue;
+      const auto sl = static_cast<size_t>(rslot[r]);
+      xlo[sl] = std::max(xlo[sl], lcon[r]);
+      xhi[sl] = std::min(xhi[sl], ucon[r]);
+      if (xlo[sl] > xhi[sl]) contradictory_ = true;
+    }
+    for (size_t sl = 0; sl < nv; ++sl)
+      if ((prim[sl] < 0) != (xlo[sl] == xhi[sl]))
+        throw std::runtime_error("instance bounds change which slots are fixed: the KKT structure differs");
+  }
   std::vector<int64_t> free_slot(static_cast<size_t>(nfree_)), slack_of(static_cast<size_t>(nslack_)),
       dual_row(static_cast<size_t>(m_));
   for (size_t sl = 0; sl < nv; ++sl)
@@ -291,22 +368,18 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
     x[sl] = push_into(x[sl], lb[static_cast<size_t>(i)], ub[static_cast<size_t>(i)]);
   }
 
-  // device state
-  free_slot_.alloc(static_cast<size_t>(nfree_));
+  // device state (allocated on the first run, reused by later instances)
+  if (!allocated_) {
+    allocated_ = true;
+    alloc_state(nv, mc);
+  }
   free_slot_.upload(free_slot, s_);
-  dual_row_.alloc(static_cast<size_t>(m_));
   dual_row_.upload(dual_row, s_);
-  slack_index_.alloc(mc);
   slack_index_.upload(slack, s_);
-  lb_.alloc(nt);
   lb_.upload(lb, s_);
-  ub_.alloc(nt);
   ub_.upload(ub, s_);
-  has_lb_.alloc(nt);
   has_lb_.upload(hl, s_);
-  has_ub_.alloc(nt);
   has_ub_.upload(hu, s_);
-  lcon_s_.alloc(mc);
   lcon_s_.upload(lcon_s, s_);
   P_.nvar = nvar_;
   P_.m_con = mcon_;
@@ -322,33 +395,6 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   P_.has_lb = has_lb_.p;
   P_.has_ub = has_ub_.p;
   P_.lcon_s = lcon_s_.p;
-  for (auto* v : {&x_, &xt_, &grad_, &gradt_}) *v = std::make_unique<DVec<double>>(nv);
-  for (auto* v : {&c_, &ct_}) *v = std::make_unique<DVec<double>>(mc);
-  for (auto* v : {&s_v_, &st_}) *v = std::make_unique<DVec<double>>(static_cast<size_t>(nslack_));
-  const auto dm = static_cast<size_t>(dim_), mm = static_cast<size_t>(m_);
-  lambda_.alloc(mm);
-  g_.alloc(mm);
-  gt_.alloc(mm);
-  gsoc_.alloc(mm);
-  zl_.alloc(nt);
-  zu_.alloc(nt);
-  sigma_.alloc(nt);
-  jtlam_.alloc(nt);
-  dzl_.alloc(nt);
-  dzu_.alloc(nt);
-  rhs_.alloc(dm);
-  rhs2_.alloc(dm);
-  step_.alloc(dm);
-  step2_.alloc(dm);
-  kx_.alloc(dm);
-  r_v_.alloc(dm);
-  dx_.alloc(dm);
-  lamfull_.alloc(mc);
-  dscal_.alloc(4);
-  partials_.alloc(2 * 148 * 8);
-  out_.alloc(8);
-  sc_.partials = partials_.p;
-  sc_.out = out_.p;
   x_->upload(x, s_);
 
   // slacks from the constraint values at the start point, multipliers
@@ -371,7 +417,7 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   }
   zl_.upload(zl, s_);
   zu_.upload(zu, s_);
-  ckc(cudaMemsetAsync(lambda_.p, 0, std::max<size_t>(mm, 1) * sizeof(double), s_), "memset");
+  ckc(cudaMemsetAsync(lambda_.p, 0, std::max<size_t>(static_cast<size_t>(m_), 1) * sizeof(double), s_), "memset");
   ckc(cudaStreamSynchronize(s_), "sync");
 }
 
@@ -505,6 +551,19 @@ void DeviceSolver::finish(int status, int iter, const std::vector<double>& row_s
 
 int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
   Clock total;
+  {
+    // fresh per-run state; the plan timings stay with the context
+    const double pe = r_.time_plan_eval, pk = r_.time_plan_kkt, pl = r_.time_plan_ldl;
+    r_ = ocg_ipm_result{};
+    r_.time_plan_eval = pe;
+    r_.time_plan_kkt = pk;
+    r_.time_plan_ldl = pl;
+    filter_.clear();
+    delta_last_ = 0.0;
+    dw_ = dc_ = 0.0;
+    theta_min_ = 0.0;
+    theta_max_ = kInf;
+  }
   std::vector<double> row_scale;
   mu_ = o_.mu_init;
   tau_ = std::max(o_.tau_min, 1.0 - mu_);
@@ -731,6 +790,43 @@ void ocg_ipm_default_options(ocg_ipm_options* o) {
   o->refine_rounds = 5;
   o->refine_trigger = 1e-8;
   o->verbose = 0;
+}
+
+struct ocg_ipm_ctx {
+  std::unique_ptr<DeviceSolver> solver;
+};
+
+int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out) {
+  if (!m || !out) return OCG_ERR_ARG;
+  try {
+    ocg_ipm_options o;
+    ocg_ipm_default_options(&o);
+    auto c = std::make_unique<ocg_ipm_ctx>();
+    c->solver = std::make_unique<DeviceSolver>(m, o, device);
+    *out = c.release();
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    std::fprintf(stderr, "ocg_ipm_ctx_create: %s\n", ex.what());
+    return OCG_ERR_CUDA;
+  }
+}
+
+void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c) { delete c; }
+
+int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double* lvar, const double* uvar,
+                      const double* x_start, const double* lcon, const double* ucon, ocg_ipm_result* out,
+                      double* x_out) {
+  if (!c || !out) return OCG_ERR_ARG;
+  ocg_ipm_options o;
+  ocg_ipm_default_options(&o);
+  if (opts) o = *opts;
+  try {
+    c->solver->set_instance(o, lvar, uvar, x_start, lcon, ucon);
+    return c->solver->run(out, x_out);
+  } catch (const std::exception& ex) {
+    std::fprintf(stderr, "ocg_ipm_ctx_solve: %s\n", ex.what());
+    return OCG_ERR_CUDA;
+  }
 }
 
 int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out) {

@@ -351,3 +351,42 @@ def solve(model: Model, device: int = 0, return_x: bool = False, **options) -> d
     if x is not None:
         out["x"] = x
     return out
+
+
+class Solver:
+    """Reusable device IPM context (ocg_ipm_ctx_*): plans built once for a
+    model structure; solve() takes an instance's bounds / start point."""
+
+    def __init__(self, model: Model, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("octgpu Solver needs a CUDA device (no CPU fallback)")
+        h = C.c_void_p()
+        check(LIB.ocg_ipm_ctx_create(model._h, int(device), C.byref(h)), "ocg_ipm_ctx_create")
+        self._h, self.model = h, model
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_ipm_ctx_destroy(self._h)
+            self._h = None
+
+    def solve(self, instance: Model | None = None, return_x: bool = False, **options) -> dict:
+        o = _lib.IpmOptions()
+        LIB.ocg_ipm_default_options(C.byref(o))
+        for k, v in options.items():
+            if not hasattr(o, k):
+                raise TypeError(f"unknown IPM option {k!r}")
+            setattr(o, k, type(getattr(o, k))(v))
+        ptrs = [None] * 5
+        keep = None
+        if instance is not None:
+            keep = instance.arrays()
+            ptrs = [keep[k].ctypes.data for k in ("lvar", "uvar", "x_start", "lcon", "ucon")]
+        r = _lib.IpmResult()
+        x = np.empty(self.model.nvar) if return_x else None
+        check(LIB.ocg_ipm_ctx_solve(self._h, C.byref(o), *ptrs, C.byref(r), None if x is None else x.ctypes.data),
+              "ocg_ipm_ctx_solve")
+        out = {name: getattr(r, name) for name, _ in r._fields_}
+        out["status_name"] = STATUS.get(r.status, "unknown")
+        if x is not None:
+            out["x"] = x
+        return out

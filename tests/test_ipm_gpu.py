@@ -42,3 +42,22 @@ def test_device_solve_goddard_1000():
     print("goddard@1000 ref", ref["iterations"], ref["objective"], "device", got["iterations"], got["objective"])
     assert got["status"] == 0 == ref["status"]
     assert abs(got["objective"] - ref["objective"]) <= 1e-5 * abs(ref["objective"])
+
+
+def test_reusable_context_matches_fresh_solves():
+    """BASELINE config 5 path: one solver context (plans built once) re-used for
+    batch instances that differ only in the terminal target (bounds), each
+    equal to a fresh solve of that instance and to the reference."""
+    from paper_2510_03932_b200 import Solver
+    from paper_2510_03932_b200.models import cart_pendulum_instance
+    base = Model(cart_pendulum_instance(0, 4096), 200)
+    ctx = Solver(base)
+    for b in (0, 1000, 4095):
+        inst = Model(cart_pendulum_instance(b, 4096), 200)
+        got = ctx.solve(inst)
+        fresh = solve(inst)
+        ref = RefModel(cart_pendulum_instance(b, 4096), 200).solve(parallel=False)
+        assert got["status"] == fresh["status"] == 0 == ref["status"]
+        assert got["iterations"] == fresh["iterations"] == ref["iterations"]
+        assert got["objective"] == fresh["objective"]
+        assert abs(got["objective"] - ref["objective"]) <= 1e-8 * abs(ref["objective"])
