@@ -18,6 +18,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 REF_SO = ROOT / "oracle" / "_ref" / "libref.so"
 ACCEL_SO = ROOT / "integration" / "_out" / "libref_accel.so"
+PORT_SO = ROOT / "oracle" / "_ref" / "liboracle.so"
 
 _libs: dict = {}
 
@@ -238,3 +239,123 @@ class RefKkt:
         y = np.empty(self.dim)
         self.L.ref_kkt_matvec(self.h, _p(val), _p(x), _p(y))
         return y
+
+
+# ---- the C restatement (oracle/port, liboracle.so) ---------------------------
+
+class _OcGroup(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("op", C.c_void_p), ("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p),
+                ("n_inputs", C.c_int32), ("base", C.c_void_p), ("stride", C.c_void_p), ("out_dim", C.c_int32),
+                ("roots", C.c_void_p), ("n_jac", C.c_int32), ("jac", C.c_void_p), ("n_hess", C.c_int32),
+                ("hess", C.c_void_p), ("lo", C.c_int64), ("hi", C.c_int64), ("endpoints", C.c_int32),
+                ("row_base", C.c_int64), ("weight", C.c_double)]
+
+
+class _OcNlp(C.Structure):
+    _fields_ = [("nvar", C.c_int64), ("m_con", C.c_int64), ("n_con", C.c_int32), ("n_obj", C.c_int32),
+                ("con", C.c_void_p), ("obj", C.c_void_p)]
+
+
+_port = None
+
+
+def port_lib() -> C.CDLL:
+    global _port
+    if _port is None:
+        if not PORT_SO.exists():
+            raise FileNotFoundError(f"{PORT_SO} missing: run `make -C oracle port`")
+        L = C.CDLL(str(PORT_SO))
+        vp, dp = C.c_void_p, C.c_void_p
+        L.oc_constraints_jacobian.restype = C.c_int
+        L.oc_constraints_jacobian.argtypes = [vp, dp, dp, dp, dp]
+        L.oc_hessian.restype = C.c_int
+        L.oc_hessian.argtypes = [vp, dp, dp, dp, C.c_double, dp]
+        L.oc_objective.restype = C.c_int
+        L.oc_objective.argtypes = [vp, dp, C.c_double, dp]
+        L.oc_gradient.restype = C.c_int
+        L.oc_gradient.argtypes = [vp, dp, C.c_double, dp, dp]
+        _port = L
+    return _port
+
+
+class PortEval:
+    """The C restatement over a structure dump (ref_model_json /
+    ocg_model_structure_json format): EvalContext's evaluation calls."""
+
+    def __init__(self, st: dict):
+        self.st = st
+        self._keep = []
+        self.nvar, self.m_con = int(st["nvar"]), int(st["m_con"])
+
+        def arr(v, dt):
+            a = np.ascontiguousarray(np.asarray(v, dtype=dt))
+            if a.size == 0:
+                a = np.zeros(1, dtype=dt)
+            self._keep.append(a)
+            return a.ctypes.data
+
+        def group(g):
+            nodes = g["nodes"]
+            o = _OcGroup()
+            o.n_nodes = len(nodes)
+            o.op = arr([n[0] for n in nodes], np.int32)
+            o.a = arr([n[1] for n in nodes], np.int32)
+            o.b = arr([n[2] for n in nodes], np.int32)
+            o.c = arr([n[3] for n in nodes], np.float64)
+            o.n_inputs = len(g["inputs"])
+            o.base = arr([i[0] for i in g["inputs"]], np.int64)
+            o.stride = arr([i[1] for i in g["inputs"]], np.int64)
+            o.out_dim = len(g["roots"])
+            o.roots = arr(g["roots"], np.int32)
+            o.n_jac = len(g["jac"])
+            o.jac = arr([v for p in g["jac"] for v in p], np.int32)
+            o.n_hess = len(g["hess"])
+            o.hess = arr([v for p in g["hess"] for v in p], np.int32)
+            o.lo, o.hi, o.endpoints = int(g["range"][0]), int(g["range"][1]), int(bool(g["range"][2]))
+            o.row_base = int(g.get("row_base", 0))
+            o.weight = float(g.get("weight", 1.0))
+            return o
+
+        cons = (_OcGroup * max(1, len(st["con_groups"])))(*[group(g) for g in st["con_groups"]])
+        objs = (_OcGroup * max(1, len(st["obj_groups"])))(*[group(g) for g in st["obj_groups"]])
+        self._keep += [cons, objs]
+        self.nlp = _OcNlp(self.nvar, self.m_con, len(st["con_groups"]), len(st["obj_groups"]),
+                          C.addressof(cons), C.addressof(objs))
+
+        def count(g):
+            lo, hi, ends = g["range"]
+            return (1 if lo == hi else 2) if ends else hi - lo
+
+        self.jac_nnz = sum(len(g["jac"]) * count(g) for g in st["con_groups"])
+        self.hess_nnz = sum(len(g["hess"]) * count(g) for g in st["con_groups"] + st["obj_groups"])
+        self.grad_nnz = sum(len(g["jac"]) * count(g) for g in st["obj_groups"])
+
+    def _rs(self, row_scale):
+        return np.ones(self.m_con) if row_scale is None else np.ascontiguousarray(row_scale, dtype=np.float64)
+
+    def constraints_jacobian(self, x, row_scale=None):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rs = self._rs(row_scale)
+        c, j = np.zeros(max(self.m_con, 1)), np.zeros(max(self.jac_nnz, 1))
+        ok = port_lib().oc_constraints_jacobian(C.byref(self.nlp), _p(x), _p(rs), _p(c), _p(j))
+        return bool(ok), c[: self.m_con], j[: self.jac_nnz]
+
+    def hessian(self, x, lam, row_scale=None, obj_scale=1.0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        rs = self._rs(row_scale)
+        h = np.zeros(max(self.hess_nnz, 1))
+        ok = port_lib().oc_hessian(C.byref(self.nlp), _p(x), _p(lam), _p(rs), float(obj_scale), _p(h))
+        return bool(ok), h[: self.hess_nnz]
+
+    def objective(self, x, obj_scale=1.0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        f = np.zeros(1)
+        ok = port_lib().oc_objective(C.byref(self.nlp), _p(x), float(obj_scale), _p(f))
+        return bool(ok), float(f[0])
+
+    def gradient(self, x, obj_scale=1.0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        gc, gd = np.zeros(max(self.grad_nnz, 1)), np.zeros(self.nvar)
+        ok = port_lib().oc_gradient(C.byref(self.nlp), _p(x), float(obj_scale), _p(gc), _p(gd))
+        return bool(ok), gd, gc[: self.grad_nnz]

@@ -176,3 +176,22 @@ def test_euler_scheme():
         ok_r, h_r = re.hessian(x, lam)
         assert ec.eval_hessian(x, lam) == ok_r
         assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} euler hess")
+
+
+@pytest.mark.parametrize("name", ["goddard", "quadrotor", "shuttle", "cart_pendulum"])
+def test_values_against_c_restatement(name):
+    """The same parity through the C restatement of the path (oracle/port),
+    itself pinned bit-exact to the reference (tests/test_oracle_port.py)."""
+    from _oracle import PortEval
+    m, r = _pair(name, 500)
+    pe = PortEval(r.structure())
+    x, lam = r.synth_acceptance(77)
+    ec = EvalContext(m)
+    c = torch.empty(m.m_con, dtype=torch.float64, device=ec.device)
+    assert ec.eval_jac_hess(x, lam, c)
+    ok, c_p, j_p = pe.constraints_jacobian(x)
+    ok2, h_p = pe.hessian(x, lam)
+    assert ok and ok2
+    assert_close(c.cpu().numpy(), c_p, f"{name} c")
+    assert_close(ec.jac_val.cpu().numpy(), j_p, f"{name} jac")
+    assert_close(ec.hess_val.cpu().numpy(), h_p, f"{name} hess")
