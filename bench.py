@@ -305,9 +305,17 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ngpu >= world:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            # fewer GPUs than ranks (a functional check of the sharded path on
+            # one device): ranks share devices, host-side collectives over gloo
+            local = local % max(1, ngpu)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
@@ -383,7 +391,8 @@ def run_ours(args) -> None:
         assert torch.equal(host[buf][s0:s0 + n], devbuf[buf][s0:s0 + n].cpu())
 
     t_e2e_local = float(np.mean(e2e_t))
-    tt = torch.tensor([t_local, t_e2e_local, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+    tt = torch.tensor([t_local, t_e2e_local, 0.0 if ok else 1.0], dtype=torch.float64,
+                      device=dev if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_max, t_e2e_max, bad = (float(v) for v in tt.cpu())
