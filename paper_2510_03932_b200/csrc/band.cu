@@ -50,10 +50,20 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   BandPlan P;
   P.dim = dim;
   // flat node-major order: band part, then the global border
+  // stable counting sort by node (border indices, node -1, last)
   std::vector<int64_t> flat(static_cast<size_t>(dim));
-  for (int64_t i = 0; i < dim; ++i) flat[static_cast<size_t>(i)] = i;
-  auto key = [&](int64_t i) { return node[static_cast<size_t>(i)] < 0 ? INT64_MAX : node[static_cast<size_t>(i)]; };
-  std::stable_sort(flat.begin(), flat.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+  {
+    int64_t max_node = -1;
+    for (int64_t i = 0; i < dim; ++i) max_node = std::max(max_node, node[static_cast<size_t>(i)]);
+    std::vector<int64_t> start(static_cast<size_t>(max_node) + 3, 0);
+    auto bucket = [&](int64_t i) {
+      const int64_t v = node[static_cast<size_t>(i)];
+      return static_cast<size_t>(v < 0 ? max_node + 1 : v);
+    };
+    for (int64_t i = 0; i < dim; ++i) start[bucket(i) + 1]++;
+    for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+    for (int64_t i = 0; i < dim; ++i) flat[static_cast<size_t>(start[bucket(i)]++)] = i;
+  }
   std::vector<int64_t> fpos(static_cast<size_t>(dim));
   for (int64_t p = 0; p < dim; ++p) fpos[static_cast<size_t>(flat[static_cast<size_t>(p)])] = p;
   int64_t wg = 0;
@@ -109,9 +119,11 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     if (off < seg_len[static_cast<size_t>(i)]) return {0, i, off};
     return {1, i, off - seg_len[static_cast<size_t>(i)]};
   };
+  std::vector<Loc> loc(static_cast<size_t>(dim));
+  for (int64_t f = 0; f < dim; ++f) loc[static_cast<size_t>(f)] = loc_of_flat(f);
   P.perm.assign(static_cast<size_t>(dim), -1);
   for (int64_t f = 0; f < dim; ++f) {
-    const Loc L = loc_of_flat(f);
+    const Loc L = loc[static_cast<size_t>(f)];
     int64_t pos;
     if (L.kind == 0)
       pos = seg_pos[static_cast<size_t>(L.idx)] + L.local;
@@ -180,8 +192,8 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   P.dst.resize(rowi.size());
   for (int64_t j = 0; j < dim; ++j)
     for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
-      Loc a = loc_of_flat(fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])]);
-      Loc c = loc_of_flat(fpos[static_cast<size_t>(j)]);
+      Loc a = loc[static_cast<size_t>(fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])])];
+      Loc c = loc[static_cast<size_t>(fpos[static_cast<size_t>(j)])];
       int64_t d = -1;
       if (nseg == 1) {
         const BandSeg& s = P.segs[0];

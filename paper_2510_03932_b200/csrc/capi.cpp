@@ -10,7 +10,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -25,6 +27,7 @@
 #include "../../include/octgpu.h"
 #include "jit.hpp"
 #include "band.hpp"
+#include "kktbuild.hpp"
 #include "kernels.hpp"
 #include "model.hpp"
 #include "plan.hpp"
@@ -68,6 +71,13 @@ struct DBuf {
     if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
     p = ext;
     owned = false;
+  }
+  // take ownership of device memory from cudaMallocAsync
+  void adopt(T* ptr, size_t count) {
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    p = ptr;
+    n = count;
+    owned = true;
   }
   void alloc(size_t count) {
     if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
@@ -951,6 +961,14 @@ int ocg_eval_compute_scaling(ocg_eval* e, const double* x0, int enabled, ocg_str
 int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   if (!mdl || !e || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ocg_kkt_create] %-16s %8.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+    tprev = now;
+  };
   const ocg::Nlp& nlp = mdl->nlp;
   auto K = std::make_unique<ocg_kkt>();
   K->ev = e;
@@ -984,6 +1002,7 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     K->dual_index[r] = K->m++;
     K->dual_row.push_back(static_cast<Index>(r));
   }
+  lap("reduction");
   // KktAssembler (eval.cpp:318-403)
   K->prim_index.assign(nv, -1);
   for (size_t s = 0; s < nv; ++s) {
@@ -1000,128 +1019,57 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   K->ntot = K->n_free + K->n_slack;
   K->dim = K->ntot + K->m;
 
+  lap("maps");
   std::vector<Index> jr, jc, hr, hc;
   host_structure(nlp, &jr, &jc, &hr, &hc, nullptr);
   K->H = static_cast<Index>(hr.size());
   K->J = static_cast<Index>(jr.size());
-  // structural entries as (key=(col,row), source code); code order == the
-  // reference's accumulation order
-  struct Src {
-    Index col, row, code;
-  };
-  std::vector<Src> srcs;
-  srcs.reserve(hr.size() + jr.size() + static_cast<size_t>(K->ntot + K->m));
-  for (size_t q = 0; q < hr.size(); ++q) {
-    const Index pi = K->prim_index[static_cast<size_t>(hr[q])], pj = K->prim_index[static_cast<size_t>(hc[q])];
-    if (pi < 0 || pj < 0) continue;
-    srcs.push_back({std::min(pi, pj), std::max(pi, pj), static_cast<Index>(q)});
-  }
-  for (size_t q = 0; q < jr.size(); ++q) {
-    const Index d = K->dual_index[static_cast<size_t>(jr[q])];
-    if (d < 0) continue;
-    const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
-    if (pj < 0) continue;
-    srcs.push_back({pj, K->ntot + d, K->H + static_cast<Index>(q)});
-  }
-  const Index S = K->n_slack;
-  for (Index k = 0; k < S; ++k) {
-    const Index d = K->dual_index[static_cast<size_t>(K->slack_of[static_cast<size_t>(k)])];
-    srcs.push_back({K->n_free + k, K->ntot + d, K->H + K->J + k});
-  }
-  for (Index i = 0; i < K->ntot; ++i) srcs.push_back({i, i, K->H + K->J + S + i});
-  for (Index r = 0; r < K->m; ++r) srcs.push_back({K->ntot + r, K->ntot + r, -1});  // dual diagonal: no source
-  // (col, row, code) order: counting sort by column, then each (short)
-  // column sorted by (row, code)
+  lap("structure");
+  // pattern, assembly sources, matvec CSR and J^T lambda gather: sorted on
+  // the device (kktbuild.cu); sources keep the reference's accumulation order
   {
-    std::vector<int64_t> cstart(static_cast<size_t>(K->dim) + 1, 0);
-    for (const Src& e : srcs) cstart[static_cast<size_t>(e.col) + 1]++;
-    for (Index j = 0; j < K->dim; ++j) cstart[static_cast<size_t>(j) + 1] += cstart[static_cast<size_t>(j)];
-    std::vector<Src> sorted(srcs.size());
-    std::vector<int64_t> fill(cstart.begin(), cstart.end() - 1);
-    for (const Src& e : srcs) sorted[static_cast<size_t>(fill[static_cast<size_t>(e.col)]++)] = e;
-    parallel_for(K->dim, [&](Index j0, Index j1) {
-      for (Index j = j0; j < j1; ++j)
-        std::sort(sorted.begin() + cstart[static_cast<size_t>(j)], sorted.begin() + cstart[static_cast<size_t>(j) + 1],
-                  [](const Src& a, const Src& b) { return a.row != b.row ? a.row < b.row : a.code < b.code; });
-    });
-    srcs.swap(sorted);
-  }
-  K->colp.assign(static_cast<size_t>(K->dim) + 1, 0);
-  std::vector<int64_t> sptr{0}, scode;
-  for (size_t q = 0; q < srcs.size(); ++q) {
-    const bool fresh = q == 0 || srcs[q].col != srcs[q - 1].col || srcs[q].row != srcs[q - 1].row;
-    if (fresh) {
-      if (q) sptr.push_back(static_cast<int64_t>(scode.size()));
-      K->rowi.push_back(srcs[q].row);
-      K->colp[static_cast<size_t>(srcs[q].col) + 1]++;
-    }
-    if (srcs[q].code >= 0) scode.push_back(srcs[q].code);
-  }
-  sptr.push_back(static_cast<int64_t>(scode.size()));
-  for (Index j = 0; j < K->dim; ++j) K->colp[static_cast<size_t>(j) + 1] += K->colp[static_cast<size_t>(j)];
-  K->nnz = static_cast<Index>(K->rowi.size());
-  K->src_ptr.upload(sptr);
-  K->src_code.upload(scode);
-  K->val.alloc(static_cast<size_t>(K->nnz));
-  ck(cudaMemset(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double)), "memset");
-
-  // full symmetric CSR for matvec, rows in increasing column order
-  {
-    const auto n = static_cast<size_t>(K->dim);
-    std::vector<int64_t> cnt(n + 1, 0);
-    for (size_t j = 0; j < n; ++j)
-      for (Index p = K->colp[j]; p < K->colp[j + 1]; ++p) {
-        const auto i = static_cast<size_t>(K->rowi[static_cast<size_t>(p)]);
-        cnt[i + 1]++;
-        if (i != j) cnt[j + 1]++;
-      }
-    for (size_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-    std::vector<int64_t> col(static_cast<size_t>(cnt[n])), vidx(static_cast<size_t>(cnt[n]));
-    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (size_t j = 0; j < n; ++j)
-      for (Index p = K->colp[j]; p < K->colp[j + 1]; ++p) {
-        const auto i = static_cast<size_t>(K->rowi[static_cast<size_t>(p)]);
-        col[static_cast<size_t>(fill[i])] = static_cast<int64_t>(j);
-        vidx[static_cast<size_t>(fill[i]++)] = p;
-        if (i != j) {
-          col[static_cast<size_t>(fill[j])] = static_cast<int64_t>(i);
-          vidx[static_cast<size_t>(fill[j]++)] = p;
-        }
-      }
-    K->mv_ptr.upload(cnt);
-    K->mv_col.upload(col);
-    K->mv_vidx.upload(vidx);
-  }
-  // J^T lambda gather: per primal column, jac entries in increasing order
-  {
-    const auto nf = static_cast<size_t>(K->n_free);
-    const auto nt = static_cast<size_t>(K->ntot);
-    std::vector<int64_t> ptr(nt + 1, 0);
-    for (size_t q = 0; q < jr.size(); ++q) {
-      const Index d = K->dual_index[static_cast<size_t>(jr[q])];
-      const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
-      if (d < 0 || pj < 0) continue;
-      ptr[static_cast<size_t>(pj) + 1]++;
-    }
-    for (size_t i = 0; i < nt; ++i) ptr[i + 1] += ptr[i];
-    std::vector<int64_t> ei(static_cast<size_t>(ptr[nt])), di(static_cast<size_t>(ptr[nt]));
-    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
-    for (size_t q = 0; q < jr.size(); ++q) {
-      const Index d = K->dual_index[static_cast<size_t>(jr[q])];
-      const Index pj = K->prim_index[static_cast<size_t>(jc[q])];
-      if (d < 0 || pj < 0) continue;
-      ei[static_cast<size_t>(fill[static_cast<size_t>(pj)])] = static_cast<int64_t>(q);
-      di[static_cast<size_t>(fill[static_cast<size_t>(pj)]++)] = d;
-    }
     std::vector<int64_t> sd(static_cast<size_t>(K->n_slack));
     for (Index k = 0; k < K->n_slack; ++k)
       sd[static_cast<size_t>(k)] = K->dual_index[static_cast<size_t>(K->slack_of[static_cast<size_t>(k)])];
-    (void)nf;
-    K->jt_ptr.upload(ptr);
-    K->jt_e.upload(ei);
-    K->jt_dual.upload(di);
+    DBuf<int64_t> dhr, dhc, djr, djc, dprim, ddual;
+    dhr.upload(hr);
+    dhc.upload(hc);
+    djr.upload(jr);
+    djc.upload(jc);
+    dprim.upload(K->prim_index);
+    ddual.upload(K->dual_index);
     K->jt_slack_dual.upload(sd);
+    ocg::dev::KktBuildIn bi;
+    bi.hr = dhr.p;
+    bi.hc = dhc.p;
+    bi.jr = djr.p;
+    bi.jc = djc.p;
+    bi.H = K->H;
+    bi.J = K->J;
+    bi.prim = dprim.p;
+    bi.dual = ddual.p;
+    bi.slack_dual = K->jt_slack_dual.p;
+    bi.n_free = K->n_free;
+    bi.n_slack = K->n_slack;
+    bi.m = K->m;
+    ocg::dev::KktBuildOut bo;
+    ocg::dev::build_kkt(bi, cudaStreamPerThread, bo);
+    K->colp = std::move(bo.colp);
+    K->rowi = std::move(bo.rowi);
+    K->nnz = bo.nnz;
+    K->src_ptr.adopt(bo.src_ptr, static_cast<size_t>(bo.nnz) + 1);
+    K->src_code.adopt(bo.src_code, static_cast<size_t>(bo.ncode));
+    K->mv_ptr.adopt(bo.mv_ptr, static_cast<size_t>(K->dim) + 1);
+    K->mv_col.adopt(bo.mv_col, 0);
+    K->mv_vidx.adopt(bo.mv_vidx, 0);
+    K->jt_ptr.adopt(bo.jt_ptr, static_cast<size_t>(K->ntot) + 1);
+    K->jt_e.adopt(bo.jt_e, 0);
+    K->jt_dual.adopt(bo.jt_dual, 0);
   }
+  K->val.alloc(static_cast<size_t>(K->nnz));
+  ck(cudaMemsetAsync(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double), cudaStreamPerThread), "memset");
+  ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
+  lap("jt gather");
   *out = K.release();
   return OCG_OK;
   OCG_GUARD_END
@@ -1172,7 +1120,7 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
   if (!k || !sigma) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
-                         k->n_slack, k->val.p, st(s));
+                         k->n_slack, k->ntot, k->val.p, st(s));
   k->ev->launches += 1;
   return OCG_OK;
   OCG_GUARD_END

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) kkt_assemble_k(const double* __restrict__
                                                       const double* __restrict__ sigma,
                                                       const int64_t* __restrict__ ptr,
                                                       const int64_t* __restrict__ code, int64_t nnz, int64_t H,
-                                                      int64_t J, int64_t S, double* __restrict__ val) {
+                                                      int64_t J, int64_t S, int64_t ntot, double* __restrict__ val) {
   const int64_t HJ = H + J, HJS = H + J + S;
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(256) kkt_assemble_k(const double* __restrict__
         v = jac[c - H];
       else if (c < HJS)
         v = -1.0;
-      else
+      else if (c < HJS + ntot)
         v = sigma[c - HJS];
+      else
+        v = 0.0;  // dual diagonal: structural, no value (-delta_c is the factorization's)
       s += v;
     }
     val[p] = s;
@@ -181,9 +183,10 @@ void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64
 }
 
 void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
-                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, double* val, cudaStream_t s) {
+                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
+                  cudaStream_t s) {
   if (nnz <= 0) return;
-  kkt_assemble_k<<<grid_for(nnz, 256), 256, 0, s>>>(hess, jac, sigma, ptr, code, nnz, H, J, S, val);
+  kkt_assemble_k<<<grid_for(nnz, 256), 256, 0, s>>>(hess, jac, sigma, ptr, code, nnz, H, J, S, ntot, val);
 }
 
 void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,

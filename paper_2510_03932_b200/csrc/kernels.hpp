@@ -26,9 +26,10 @@ void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64
 
 // K.val[p] = sum of its sources in code order (KktAssembler::assemble,
 // eval.cpp:429-440): code < H: hess[code]; < H+J: jac[code-H]; < H+J+S: -1.0;
-// else sigma[code-H-J-S].
+// < H+J+S+ntot: sigma[code-H-J-S]; else 0 (the dual diagonal's structural slot).
 void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
-                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, double* val, cudaStream_t s);
+                  const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
+                  cudaStream_t s);
 
 // y[i] = sum over the full symmetric row i (increasing column) of K_ij x_j —
 // the accumulation order of sparse::matvec_sym (sparse.cpp:51-61).
