@@ -619,6 +619,14 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
   ocg_eval_default_options(&o);
   if (opts) o = *opts;
   try {
+    const bool timing = std::getenv("OCG_TIMING") != nullptr;
+    auto tprev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[ocg_eval_create] %-16s %8.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+      tprev = now;
+    };
     auto e = std::make_unique<ocg_eval>();
     e->model = m;
     e->device = o.device;
@@ -639,6 +647,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     ocg::GenOptions go;
     go.fma = o.fma != 0;
     go.block = e->block;
+    lap("device props");
     std::map<std::string, std::string> cubins;
     ocg::Generated gen =
         generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), o.split_kinds,
@@ -651,7 +660,9 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->tail = gen.tail;
     e->smem = gen.smem;
     e->prm = gen.params;
+    lap("generate+compile");
     for (const char* k : kKernelNames) e->mods[k] = loaded_module(cubins.at(k));
+    lap("load modules");
     e->k_c = e->mods.at("ocg_c")->kernel("ocg_c");
     e->k_cjac = e->mods.at("ocg_cjac")->kernel("ocg_cjac");
     e->k_hess = e->mods.at("ocg_hess")->kernel("ocg_hess");
@@ -672,6 +683,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     }
     e->sm_count = prop.multiProcessorCount;
 
+    lap("kernel attrs");
     e->jac.alloc(static_cast<size_t>(e->lay.jac_nnz));
     e->hess.alloc(static_cast<size_t>(e->lay.hess_nnz));
     e->grad.alloc(static_cast<size_t>(e->lay.grad_nnz));
@@ -697,6 +709,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->og_weight.upload(e->obj_weight);
     e->partials.alloc(static_cast<size_t>(std::max<Index>(1, e->n_chunks)));
 
+    lap("buffers");
     // dense gradient: per slot, grad COO entries in increasing order
     std::vector<Index> gc;
     host_structure(nlp, nullptr, nullptr, nullptr, nullptr, &gc);
@@ -709,6 +722,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->gg_ptr.upload(ptr);
     e->gg_idx.upload(idx);
     ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
+    lap("gradient gather");
     *out = e.release();
     return OCG_OK;
   } catch (const CudaError& ex) {

@@ -984,9 +984,14 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       const Index n = (W + u.max_off) * sl.dim;
       const std::string sb = P("slab" + std::to_string(s) + ".base", sl.base);
       const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
+      // the copy count is bounded at generation time: straight-line
+      // predicated copies, no loop control
       E.line("{ const long long gb = " + sb + " + ib * " + i64(sl.dim) + "; long long nv = " + se +
-             " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) +
-             "; for (int j = lane; j < (int)nv; j += 32) ocg_cp8(smem + " + i64(u.soff) + " + j, x + gb + j); }");
+             " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) + "; const int nvi = (int)nv;");
+      for (Index j0 = 0; j0 < n; j0 += 32)
+        E.line("  if (lane + " + std::to_string(j0) + " < nvi) ocg_cp8(smem + " + i64(u.soff + j0) + " + lane, x + gb + " +
+               std::to_string(j0) + " + lane);");
+      E.line("}");
     }
     bool staged_any = !uses.empty();
     for (size_t q = 0; q < members.size(); ++q) {
@@ -999,10 +1004,14 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       E.open("");
       E.line("const int nr = nk" + R + " * (int)" + od + ", so = r0" + R + " * (int)" + od + ";");
       E.line("const long long g0 = " + rb + " + k0" + R + " * " + od + ";");
-      if (rows[q].rs >= 0)
-        E.line("for (int j = lane; j < nr; j += 32) ocg_cp8(smem + " + i64(rows[q].rs) + " + so + j, rs + g0 + j);");
-      if (rows[q].lam >= 0)
-        E.line("for (int j = lane; j < nr; j += 32) ocg_cp8(smem + " + i64(rows[q].lam) + " + so + j, lam + g0 + j);");
+      const Index nmax = W * g.out_dim();
+      for (Index j0 = 0; j0 < nmax; j0 += 32) {
+        const std::string j = std::to_string(j0) + " + lane";
+        if (rows[q].rs >= 0)
+          E.line("if (" + j + " < nr) ocg_cp8(smem + " + i64(rows[q].rs) + " + so + " + j + ", rs + g0 + " + j + ");");
+        if (rows[q].lam >= 0)
+          E.line("if (" + j + " < nr) ocg_cp8(smem + " + i64(rows[q].lam) + " + so + " + j + ", lam + g0 + " + j + ");");
+      }
       E.close();
       staged_any = true;
     }
@@ -1057,7 +1066,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         // region free again? (distinct regions: only the tile's first store
         // waits, for the previous tile's copy-out)
         if ((cur_kind == -2 && (!opt_.distinct_regions || first_store_of_tile_)) || opt_.split_kinds)
-          E.line("if (lane == 0) ocg_bulk_wait_read(); __syncwarp();");
+          E.line("ocg_bulk_wait_read(); __syncwarp();");
         first_store_of_tile_ = false;
         cur_kind = kind;
       };
@@ -1101,21 +1110,30 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         for (size_t oi = 0; oi < outs[q].size(); ++oi)
           if (outs[q][oi].kind == cur_kind) flush(oi);
       } else {
+        // one output kind per lane: lanes 0..K-1 select their copy's
+        // arguments (no divergent branches) and issue the bulk copies together
         E.line("ocg_fence_async(); __syncwarp();");
-        E.open("if (lane == 0 && nk" + R + " > 0)");
-        for (size_t oi = 0; oi < outs[q].size(); ++oi) {
+        E.open("");
+        std::string dsel = "nullptr", ssel = "nullptr", nsel = "0";
+        for (size_t oi = outs[q].size(); oi-- > 0;) {
           const Out& o = outs[q][oi];
           const std::string S = i64(o.per_k);
-          E.line("ocg_bulk_store(" + o.dst + " + k0" + R + " * " + S + ", smem + " + i64(o.soff) + " + sh" + qn + "_" +
-                 std::to_string(oi) + " + r0" + R + " * " + S + ", nk" + R + " * (int)" + S + ");");
+          const std::string cond = "lane == " + std::to_string(oi);
+          dsel = "(" + cond + " ? " + o.dst + " + k0" + R + " * " + S + " : " + dsel + ")";
+          ssel = "(" + cond + " ? smem + " + i64(o.soff) + " + sh" + qn + "_" + std::to_string(oi) + " + r0" + R +
+                 " * " + S + " : " + ssel + ")";
+          nsel = "(" + cond + " ? nk" + R + " * (int)" + S + " : " + nsel + ")";
         }
-        E.line("ocg_bulk_commit();");
+        E.line("double* const bd = " + dsel + ";");
+        E.line("const double* const bs = " + ssel + ";");
+        E.line("const int bn = " + nsel + ";");
+        E.line("if (lane < " + std::to_string(outs[q].size()) + " && bn > 0) { ocg_bulk_store(bd, bs, bn); ocg_bulk_commit(); }");
         E.close();
       }
     }
     load_from_ = nullptr;
     E.close();  // tile loop
-    E.line("if (lane == 0) ocg_bulk_wait_all();  // bulk copies done before the block exits");
+    E.line("ocg_bulk_wait_all();  // bulk copies done before the block exits");
 
     if (!tails.empty()) {
       E.open("if (blockIdx.x == gridDim.x - 1)");
