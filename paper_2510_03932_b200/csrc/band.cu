@@ -46,9 +46,11 @@ size_t solve_smem(int b, int w) {
 }  // namespace
 
 BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std::vector<int64_t>& colp,
-                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments) {
+                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments, const DeviceCsc* dcsc,
+                        int64_t** d_dst) {
   BandPlan P;
   P.dim = dim;
+  P.nnz = static_cast<int64_t>(rowi.size());
   // flat node-major order: band part, then the global border
   // stable counting sort by node (border indices, node -1, last)
   std::vector<int64_t> flat(static_cast<size_t>(dim));
@@ -70,11 +72,17 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   for (int64_t i = 0; i < dim; ++i) wg += node[static_cast<size_t>(i)] < 0 ? 1 : 0;
   const int64_t n = dim - wg;
   int64_t b = 0;
-  for (int64_t j = 0; j < dim; ++j)
-    for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
-      const int64_t pi = fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])], pj = fpos[static_cast<size_t>(j)];
-      if (pi < n && pj < n) b = std::max<int64_t>(b, pi > pj ? pi - pj : pj - pi);
-    }
+  int64_t* d_fpos = nullptr;
+  if (dcsc) {
+    d_fpos = dev::upload_i64(fpos, dcsc->stream);
+    b = dev::bandwidth(dcsc->colp, dcsc->rowi, d_fpos, n, dim, dcsc->stream);
+  } else {
+    for (int64_t j = 0; j < dim; ++j)
+      for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
+        const int64_t pi = fpos[static_cast<size_t>(rowi[static_cast<size_t>(q)])], pj = fpos[static_cast<size_t>(j)];
+        if (pi < n && pj < n) b = std::max<int64_t>(b, pi > pj ? pi - pj : pj - pi);
+      }
+  }
   b = std::max<int64_t>(b, 1);
   if (b > 60) throw std::runtime_error("KKT bandwidth " + std::to_string(b) + " exceeds the band solver's limit (60)");
   P.b = static_cast<int>(b);
@@ -189,6 +197,28 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     if (C < n2) return sep.border + (R - n2) * n2 + C;
     return sep.S + (R - n2) * sep.w + (C - n2);
   };
+  if (dcsc) {
+    // the same classification per entry, on the device (dev::band_dst)
+    std::vector<int8_t> lk(static_cast<size_t>(dim));
+    std::vector<int64_t> li(static_cast<size_t>(dim)), ll(static_cast<size_t>(dim));
+    for (int64_t f = 0; f < dim; ++f) {
+      lk[static_cast<size_t>(f)] = static_cast<int8_t>(loc[static_cast<size_t>(f)].kind);
+      li[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].idx;
+      ll[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].local;
+    }
+    dev::BandDstIn in;
+    in.colp = dcsc->colp;
+    in.rowi = dcsc->rowi;
+    in.fpos = d_fpos;
+    in.dim = dim;
+    in.n = n;
+    in.b = b;
+    in.wg = wg;
+    in.n2 = n2;
+    in.nseg = nseg;
+    *d_dst = dev::band_dst(in, lk, li, ll, P.segs, dcsc->nnz, dcsc->stream);
+    cudaFreeAsync(d_fpos, dcsc->stream);
+  } else {
   P.dst.resize(rowi.size());
   for (int64_t j = 0; j < dim; ++j)
     for (int64_t q = colp[static_cast<size_t>(j)]; q < colp[static_cast<size_t>(j) + 1]; ++q) {
@@ -233,6 +263,7 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
       }
       P.dst[static_cast<size_t>(q)] = d;
     }
+  }
   size_t sf = 0, ss = 0;
   for (const BandSeg& s : P.segs) {
     sf = std::max(sf, factor_smem(s.b, s.w));
@@ -679,9 +710,154 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
+namespace {
+__global__ void bandwidth_k(const int64_t* __restrict__ colp, const int64_t* __restrict__ rowi,
+                            const int64_t* __restrict__ fpos, int64_t n, int64_t dim, unsigned long long* out) {
+  unsigned long long m = 0;
+  GRID_LOOP(j, dim) {
+    const int64_t pj = fpos[j];
+    for (int64_t q = colp[j]; q < colp[j + 1]; ++q) {
+      const int64_t pi = fpos[rowi[q]];
+      if (pi < n && pj < n) m = max(m, static_cast<unsigned long long>(pi > pj ? pi - pj : pj - pi));
+    }
+  }
+  atomicMax(out, m);
+}
+
+__global__ void band_dst_k(BandDstIn in, const int8_t* __restrict__ lk, const int64_t* __restrict__ li,
+                           const int64_t* __restrict__ ll, const BandSeg* __restrict__ segs,
+                           int64_t* __restrict__ dst, int* __restrict__ err) {
+  const int64_t n = in.n, b = in.b, wg = in.wg, n2 = in.n2;
+  GRID_LOOP(j, in.dim) {
+    const int64_t fc = in.fpos[j];
+    for (int64_t q = in.colp[j]; q < in.colp[j + 1]; ++q) {
+      const int64_t fa = in.fpos[in.rowi[q]];
+      int ak = lk[fa], ck_ = lk[fc];
+      int64_t ai = li[fa], al = ll[fa], ci = li[fc], cl = ll[fc];
+      int64_t d = -1;
+      if (in.nseg == 1) {
+        const BandSeg& sg = segs[0];
+        int64_t r = ak == 2 ? n + al : al, cc = ck_ == 2 ? n + cl : cl;
+        if (r < cc) {
+          const int64_t t = r;
+          r = cc;
+          cc = t;
+        }
+        if (r < n)
+          d = sg.band + cc * (b + 1) + (r - cc);
+        else if (cc < n)
+          d = sg.border + (r - n) * n + cc;
+        else
+          d = sg.S + (r - n) * sg.w + (cc - n);
+      } else {
+        if (ak == 0 && ck_ != 0) {  // interior (if any) in c
+          int ti = ak;
+          ak = ck_;
+          ck_ = ti;
+          int64_t t = ai;
+          ai = ci;
+          ci = t;
+          t = al;
+          al = cl;
+          cl = t;
+        }
+        if (ak == 0 && ck_ == 0) {
+          if (ai != ci) atomicOr(err, 1);
+          const BandSeg& sg = segs[ai];
+          int64_t r = al, cc = cl;
+          if (r < cc) {
+            const int64_t t = r;
+            r = cc;
+            cc = t;
+          }
+          if (r - cc > b) atomicOr(err, 2);
+          d = sg.band + cc * (b + 1) + (r - cc);
+        } else if (ck_ == 0) {
+          const BandSeg& sg = segs[ci];
+          int64_t t;
+          if (ak == 2)
+            t = b + al;
+          else if (ai == ci - 1)
+            t = al;
+          else if (ai == ci)
+            t = b + wg + al;
+          else {
+            atomicOr(err, 4);
+            t = 0;
+          }
+          d = sg.border + t * sg.n + cl;
+        } else {
+          const BandSeg& sep = segs[in.nseg];
+          int64_t R = ak == 1 ? ai * b + al : n2 + al, C = ck_ == 1 ? ci * b + cl : n2 + cl;
+          if (R < C) {
+            const int64_t t = R;
+            R = C;
+            C = t;
+          }
+          if (R < n2)
+            d = sep.band + C * (sep.b + 1) + (R - C);
+          else if (C < n2)
+            d = sep.border + (R - n2) * n2 + C;
+          else
+            d = sep.S + (R - n2) * sep.w + (C - n2);
+        }
+      }
+      dst[q] = d;
+    }
+  }
+}
+}  // namespace
+
+int64_t* upload_i64(const std::vector<int64_t>& v, cudaStream_t s) {
+  int64_t* p = nullptr;
+  cudaMallocAsync(reinterpret_cast<void**>(&p), (v.empty() ? 1 : v.size()) * sizeof(int64_t), s);
+  if (!v.empty()) cudaMemcpyAsync(p, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  return p;
+}
+
+int64_t bandwidth(const int64_t* colp, const int64_t* rowi, const int64_t* fpos, int64_t n, int64_t dim,
+                  cudaStream_t s) {
+  unsigned long long* d = nullptr;
+  cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), s);
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), s);
+  bandwidth_k<<<grid_for(dim), 256, 0, s>>>(colp, rowi, fpos, n, dim, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  cudaStreamSynchronize(s);
+  return static_cast<int64_t>(h);
+}
+
+int64_t* band_dst(const BandDstIn& in, const std::vector<int8_t>& lk, const std::vector<int64_t>& li,
+                  const std::vector<int64_t>& ll, const std::vector<BandSeg>& segs, int64_t nnz, cudaStream_t s) {
+  int8_t* dlk = nullptr;
+  BandSeg* dseg = nullptr;
+  int* derr = nullptr;
+  int64_t* dst = nullptr;
+  cudaMallocAsync(reinterpret_cast<void**>(&dlk), std::max<size_t>(1, lk.size()), s);
+  cudaMemcpyAsync(dlk, lk.data(), lk.size(), cudaMemcpyHostToDevice, s);
+  int64_t* dli = upload_i64(li, s);
+  int64_t* dll = upload_i64(ll, s);
+  cudaMallocAsync(reinterpret_cast<void**>(&dseg), segs.size() * sizeof(BandSeg), s);
+  cudaMemcpyAsync(dseg, segs.data(), segs.size() * sizeof(BandSeg), cudaMemcpyHostToDevice, s);
+  cudaMallocAsync(reinterpret_cast<void**>(&derr), sizeof(int), s);
+  cudaMemsetAsync(derr, 0, sizeof(int), s);
+  cudaMallocAsync(reinterpret_cast<void**>(&dst), std::max<int64_t>(1, nnz) * sizeof(int64_t), s);
+  band_dst_k<<<grid_for(in.dim), 256, 0, s>>>(in, dlk, dli, dll, dseg, dst, derr);
+  int err = 0;
+  cudaMemcpyAsync(&err, derr, sizeof(int), cudaMemcpyDeviceToHost, s);
+  for (void* p : {static_cast<void*>(dlk), static_cast<void*>(dli), static_cast<void*>(dll), static_cast<void*>(dseg),
+                  static_cast<void*>(derr)})
+    cudaFreeAsync(p, s);
+  cudaStreamSynchronize(s);
+  if (err) throw std::runtime_error("band plan: KKT entry outside the partitioned band structure (" +
+                                    std::to_string(err) + ")");
+  return dst;
+}
+
 void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, double* buf, cudaStream_t s) {
   zero_k<<<grid_for(P.buf_len), 256, 0, s>>>(buf, P.buf_len);
-  const int64_t nnz = static_cast<int64_t>(P.dst.size());
+  const int64_t nnz = P.nnz;
   if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, D.dst, nnz, buf);
 }
 

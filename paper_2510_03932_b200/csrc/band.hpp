@@ -57,15 +57,40 @@ struct BandPlan {
   std::vector<int64_t> border_pos;
   int wmax = 0;                // border rows per segment (uniform stride)
   int64_t buf_len = 0;
+  int64_t nnz = 0;  // KKT entries scattered by band_assemble
   size_t smem_factor = 0, smem_solve = 0;
 };
 
+// device copy of the KKT pattern: with it the O(nnz) parts of the plan
+// (bandwidth, entry -> buffer offsets) run on the device
+struct DeviceCsc {
+  const int64_t* colp = nullptr;
+  const int64_t* rowi = nullptr;
+  int64_t nnz = 0;
+  cudaStream_t stream = nullptr;
+};
+
 // node[i]: time node of KKT index i, or -1 for a border index. Indices of one
-// node keep their KKT order (primal slots, slacks, duals). colp/rowi: lower CSC.
+// node keep their KKT order (primal slots, slacks, duals). colp/rowi: lower
+// CSC. With dcsc the entry offsets come back in *d_dst (device,
+// cudaMallocAsync'd, caller owns) and P.dst stays empty.
 BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std::vector<int64_t>& colp,
-                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments = 296);
+                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments = 296,
+                        const DeviceCsc* dcsc = nullptr, int64_t** d_dst = nullptr);
 
 namespace dev {
+
+struct BandDstIn {
+  const int64_t* colp = nullptr;
+  const int64_t* rowi = nullptr;
+  const int64_t* fpos = nullptr;
+  int64_t dim = 0, n = 0, b = 0, wg = 0, n2 = 0, nseg = 1;
+};
+int64_t* upload_i64(const std::vector<int64_t>& v, cudaStream_t s);
+int64_t bandwidth(const int64_t* colp, const int64_t* rowi, const int64_t* fpos, int64_t n, int64_t dim,
+                  cudaStream_t s);
+int64_t* band_dst(const BandDstIn& in, const std::vector<int8_t>& lk, const std::vector<int64_t>& li,
+                  const std::vector<int64_t>& ll, const std::vector<BandSeg>& segs, int64_t nnz, cudaStream_t s);
 
 struct BandDev {  // device copies of the plan
   const BandSeg* segs = nullptr;

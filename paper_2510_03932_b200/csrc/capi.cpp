@@ -1199,9 +1199,21 @@ int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
   L->kkt = k;
   int target = 2 * 148;
   if (const char* e = std::getenv("OCG_LDL_SEGMENTS")) target = std::max(1, std::atoi(e));
-  L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot, target);
+  {
+    // the O(nnz) parts of the plan on the device
+    DBuf<int64_t> dcolp, drowi;
+    dcolp.upload(k->colp);
+    drowi.upload(k->rowi);
+    ocg::DeviceCsc csc;
+    csc.colp = dcolp.p;
+    csc.rowi = drowi.p;
+    csc.nnz = static_cast<int64_t>(k->rowi.size());
+    csc.stream = cudaStreamPerThread;
+    int64_t* ddst = nullptr;
+    L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot, target, &csc, &ddst);
+    L->dst.adopt(ddst, static_cast<size_t>(csc.nnz));
+  }
   const ocg::BandPlan& P = L->plan;
-  L->dst.upload(P.dst);
   L->perm.upload(P.perm);
   L->primal.upload(P.primal);
   L->border_pos.upload(P.border_pos.empty() ? std::vector<int64_t>{-1} : P.border_pos);
