@@ -20,6 +20,8 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -281,6 +283,9 @@ namespace {
 constexpr int kPrefetch = 32;  // band columns in flight ahead of the window (power of two)
 constexpr int kMask = kPrefetch - 1;
 constexpr int kFactorThreads = 256;
+constexpr int kMaxPairs = 12;  // register-resident update pairs per thread
+constexpr int kMaxB = 8;       // register-resident border (row, offset) updates per thread
+constexpr int kMaxS = 4;       // register-resident border-block (row, row) updates per thread
 
 __device__ __forceinline__ void cp8(double* s, const double* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
@@ -348,6 +353,43 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
     }
     pj1[p] = static_cast<short>(j1);
     pj2[p] = static_cast<short>(j1 + rem);
+  }
+  __syncthreads();
+  // this thread's update pairs, resident in registers for the whole block
+  int rj1[kMaxPairs], rj2[kMaxPairs];
+  int mypairs = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxPairs; ++q) {
+    const int p = tid + q * T;
+    rj1[q] = p < P ? pj1[p] : 1;
+    rj2[q] = p < P ? pj2[p] : 1;
+    mypairs += p < P ? 1 : 0;
+  }
+  // ... and its border-row updates for the early border rows [0, w_early)
+  int rbt[kMaxB], rbj[kMaxB], rst[kMaxS], rsu[kMaxS];
+  int myb = 0, mys = 0;
+  {
+    const int we = g.w_early;
+    for (int q = tid; q < we * b; q += T) {
+      if (myb < kMaxB) {
+        rbt[myb] = q / b;
+        rbj[myb] = q % b + 1;
+      }
+      ++myb;
+    }
+    const int ns = we * (we + 1) / 2;
+    for (int q = tid; q < ns; q += T) {
+      if (mys < kMaxS) {
+        int t = 0, rem = q;  // q -> (t, u), u <= t, row-major lower triangle
+        while (rem > t) {
+          rem -= t + 1;
+          ++t;
+        }
+        rst[mys] = t;
+        rsu[mys] = rem;
+      }
+      ++mys;
+    }
   }
   auto delta_of = [&](double f) { return f != 0.0 ? dw : -dc; };
   auto fetch = [&](long long c, int r) {  // column c -> ring row r (async)
@@ -418,7 +460,18 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
       border[static_cast<long long>(t) * n + k] = v * dinv;
     }
     __syncthreads();
-    for (int p = tid; p < P; p += T) {
+#pragma unroll
+    for (int q = 0; q < kMaxPairs; ++q) {
+      if (q >= mypairs) break;
+      const int j1 = rj1[q], j2 = rj2[q];
+      if (k + j2 < n) {
+        const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
+        const double upd = l[j2] * y[j1];
+        W[s1 * B1 + (j2 - j1)] -= upd;
+        if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
+      }
+    }
+    for (int p = tid + kMaxPairs * T; p < P; p += T) {  // beyond the register-resident pairs
       const int j1 = pj1[p], j2 = pj2[p];
       if (k + j2 < n) {
         const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
@@ -427,16 +480,34 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
         if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
       }
     }
-    for (int q = tid; q < wa * b; q += T) {
-      const int t = q / b, j = q % b + 1;
-      if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
-    }
-    for (int q = tid; q < wa * wa; q += T) {
-      const int t = q / wa, u = q % wa;
-      if (u <= t) {
+    if (wa == g.w_early && myb <= kMaxB && mys <= kMaxS) {
+      // the common case: (row, offset) and lower (row, row) pairs from registers
+#pragma unroll
+      for (int q = 0; q < kMaxB; ++q) {
+        if (q >= myb) break;
+        const int t = rbt[q], j = rbj[q];
+        if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxS; ++q) {
+        if (q >= mys) break;
+        const int t = rst[q], u = rsu[q];
         const double upd = lb[t] * yb[u];
         S[t * w + u] -= upd;
         if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
+      }
+    } else {
+      for (int q = tid; q < wa * b; q += T) {
+        const int t = q / b, j = q % b + 1;
+        if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
+      }
+      for (int q = tid; q < wa * wa; q += T) {
+        const int t = q / wa, u = q % wa;
+        if (u <= t) {
+          const double upd = lb[t] * yb[u];
+          S[t * w + u] -= upd;
+          if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
+        }
       }
     }
     // column k is final: its slot takes column k + B1 from the prefetch ring
@@ -866,18 +937,37 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   if (P.smem_factor > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(factor_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(P.smem_factor));
+  static const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  cudaEvent_t ev[4];
+  if (timing)
+    for (auto& e : ev) cudaEventCreate(&e);
+  if (timing) cudaEventRecord(ev[0], s);
   factor_k<<<P.nseg, kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv,
                                                          inertia_parts);
+  if (timing) cudaEventRecord(ev[1], s);
   int blocks = P.nseg;
   if (P.nseg > 1) {
     const int64_t per = static_cast<int64_t>(P.wmax) * P.wmax;
     for (int par = 0; par < 2; ++par)
       schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
     if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
+    if (timing) cudaEventRecord(ev[2], s);
     factor_k<<<1, kFactorThreads, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv,
                                                       inertia_parts);
+    if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
+  if (timing && P.nseg > 1) {
+    cudaEventSynchronize(ev[3]);
+    float a = 0, b2 = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b2, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    std::fprintf(stderr, "[band_factor] segments %.3f ms  schur %.3f ms  separator system %.3f ms (%lld cols, b %d)\n",
+                 a, b2, c, static_cast<long long>(P.segs.back().n), P.segs.back().b);
+  }
+  if (timing)
+    for (auto& e : ev) cudaEventDestroy(e);
   inertia_sum_k<<<1, 32, 0, s>>>(inertia_parts, blocks, inertia);
 }
 
