@@ -283,9 +283,7 @@ namespace {
 constexpr int kPrefetch = 32;  // band columns in flight ahead of the window (power of two)
 constexpr int kMask = kPrefetch - 1;
 constexpr int kFactorThreads = 256;
-constexpr int kMaxPairs = 12;  // register-resident update pairs per thread
-constexpr int kMaxB = 8;       // register-resident border (row, offset) updates per thread
-constexpr int kMaxS = 4;       // register-resident border-block (row, row) updates per thread
+
 
 __device__ __forceinline__ void cp8(double* s, const double* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
@@ -315,6 +313,11 @@ __device__ __forceinline__ bool zero_pivot(double d, double scale) {
 }
 
 // One thread block per banded block (blockIdx.x indexes `segs` from seg0).
+// Specialized at compile time on the bandwidth and border widths of the
+// blocks a model produces (BC = b + 1, WC = border rows, WEC = rows coupled
+// from column 0; 0 / -1 = read them from the descriptor), so the per-column
+// loops have constant trip counts and constant divisors.
+template <int BC, int WC, int WEC>
 __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __restrict__ segs, int seg0,
                                                            double* __restrict__ buf,
                                                            const double* __restrict__ primal, double dw, double dc,
@@ -322,9 +325,13 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
                                                            long long* __restrict__ inertia_parts) {
   extern __shared__ double sm[];
   const BandSeg g = segs[seg0 + blockIdx.x];
-  const int tid = threadIdx.x, T = blockDim.x;
+  constexpr int T = kFactorThreads;
+  const int tid = threadIdx.x;
   const long long n = g.n;
-  const int b = g.b, w = g.w, B1 = b + 1;
+  const int B1 = BC > 0 ? BC : g.b + 1;
+  const int b = B1 - 1;
+  const int w = WC >= 0 ? WC : g.w;
+  const int we = WEC >= 0 ? WEC : g.w_early;
   double* W = sm;                 // B1 * B1 (slot-major)
   double* ps = W + B1 * B1;       // B1
   double* Wb = ps + B1;           // w * B1
@@ -354,52 +361,17 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
     pj1[p] = static_cast<short>(j1);
     pj2[p] = static_cast<short>(j1 + rem);
   }
-  __syncthreads();
-  // this thread's update pairs, resident in registers for the whole block
-  int rj1[kMaxPairs], rj2[kMaxPairs];
-  int mypairs = 0;
-#pragma unroll
-  for (int q = 0; q < kMaxPairs; ++q) {
-    const int p = tid + q * T;
-    rj1[q] = p < P ? pj1[p] : 1;
-    rj2[q] = p < P ? pj2[p] : 1;
-    mypairs += p < P ? 1 : 0;
-  }
-  // ... and its border-row updates for the early border rows [0, w_early)
-  int rbt[kMaxB], rbj[kMaxB], rst[kMaxS], rsu[kMaxS];
-  int myb = 0, mys = 0;
-  {
-    const int we = g.w_early;
-    for (int q = tid; q < we * b; q += T) {
-      if (myb < kMaxB) {
-        rbt[myb] = q / b;
-        rbj[myb] = q % b + 1;
-      }
-      ++myb;
-    }
-    const int ns = we * (we + 1) / 2;
-    for (int q = tid; q < ns; q += T) {
-      if (mys < kMaxS) {
-        int t = 0, rem = q;  // q -> (t, u), u <= t, row-major lower triangle
-        while (rem > t) {
-          rem -= t + 1;
-          ++t;
-        }
-        rst[mys] = t;
-        rsu[mys] = rem;
-      }
-      ++mys;
-    }
-  }
   auto delta_of = [&](double f) { return f != 0.0 ? dw : -dc; };
   auto fetch = [&](long long c, int r) {  // column c -> ring row r (async)
     double* dstp = ring + r * RW;
+#pragma unroll
     for (int j = tid; j < B1; j += T) {
       if (c + j < n)
         cp8(dstp + j, band + c * B1 + j);
       else
         dstp[j] = 0.0;
     }
+#pragma unroll
     for (int t = tid; t < w; t += T) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
     if (tid == 0) cp8(dstp + B1 + w, flag + c);
   };
@@ -445,7 +417,9 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
       else
         ++nneg;
     }
-    const int wa = k + b >= n ? w : g.w_early;  // border rows coupled so far
+    const bool late = k + b >= n;  // the last b columns: every border row coupled
+    const int wa = late ? w : we;
+#pragma unroll
     for (int j = tid + 1; j < B1; j += T) {
       const double yj = k + j < n ? W[s * B1 + j] : 0.0;
       const double lj = yj * dinv;
@@ -453,6 +427,7 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
       l[j] = lj;
       if (k + j < n) band[k * B1 + j] = lj;
     }
+#pragma unroll
     for (int t = tid; t < w; t += T) {
       const double v = t < wa ? Wb[t * B1 + s] : 0.0;
       yb[t] = v;
@@ -460,49 +435,38 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
       border[static_cast<long long>(t) * n + k] = v * dinv;
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kMaxPairs; ++q) {
-      if (q >= mypairs) break;
-      const int j1 = rj1[q], j2 = rj2[q];
-      if (k + j2 < n) {
-        const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
-        const double upd = l[j2] * y[j1];
-        W[s1 * B1 + (j2 - j1)] -= upd;
-        if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
-      }
-    }
-    for (int p = tid + kMaxPairs * T; p < P; p += T) {  // beyond the register-resident pairs
+#pragma unroll 4
+    for (int p = tid; p < P; p += T) {
       const int j1 = pj1[p], j2 = pj2[p];
-      if (k + j2 < n) {
+      if (!late || k + j2 < n) {
         const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
         const double upd = l[j2] * y[j1];
         W[s1 * B1 + (j2 - j1)] -= upd;
         if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
       }
     }
-    if (wa == g.w_early && myb <= kMaxB && mys <= kMaxS) {
-      // the common case: (row, offset) and lower (row, row) pairs from registers
-#pragma unroll
-      for (int q = 0; q < kMaxB; ++q) {
-        if (q >= myb) break;
-        const int t = rbt[q], j = rbj[q];
-        if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
+    if (!late) {
+#pragma unroll 4
+      for (int q = tid; q < we * b; q += T) {
+        const int t = q / b, j = q - t * b + 1;
+        Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
       }
-#pragma unroll
-      for (int q = 0; q < kMaxS; ++q) {
-        if (q >= mys) break;
-        const int t = rst[q], u = rsu[q];
-        const double upd = lb[t] * yb[u];
-        S[t * w + u] -= upd;
-        if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
+#pragma unroll 4
+      for (int q = tid; q < we * we; q += T) {
+        const int t = q / we, u = q - t * we;
+        if (u <= t) {
+          const double upd = lb[t] * yb[u];
+          S[t * w + u] -= upd;
+          if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
+        }
       }
     } else {
-      for (int q = tid; q < wa * b; q += T) {
-        const int t = q / b, j = q % b + 1;
+      for (int q = tid; q < w * b; q += T) {
+        const int t = q / b, j = q - t * b + 1;
         if (k + j < n) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
       }
-      for (int q = tid; q < wa * wa; q += T) {
-        const int t = q / wa, u = q % wa;
+      for (int q = tid; q < w * w; q += T) {
+        const int t = q / w, u = q - t * w;
         if (u <= t) {
           const double upd = lb[t] * yb[u];
           S[t * w + u] -= upd;
@@ -516,6 +480,7 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
     const long long cin = k + B1;
     if (cin < n) {
       const double* src = ring + static_cast<int>(k & kMask) * RW;
+#pragma unroll
       for (int j = tid; j < B1; j += T) {
         double v = src[j];
         if (j == 0) {
@@ -524,6 +489,7 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
         }
         W[s * B1 + j] = v;
       }
+#pragma unroll
       for (int t = tid; t < w; t += T) Wb[t * B1 + s] = src[B1 + t];
     }
     __syncthreads();
@@ -567,6 +533,29 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
     o[1] = nneg;
     o[2] = nzero;
   }
+}
+
+using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, double, double, double*, long long*);
+
+// instantiations for the blocks of the shipped models (segment: b + 1,
+// 2b + wg, b + wg; separator system: 2b, wg, wg), else the generic kernel
+FactorKernel factor_kernel_for(int B1, int w, int we) {
+#define OCG_FK(a, c, e) \
+  if (B1 == (a) && w == (c) && we == (e)) return factor_k<a, c, e>;
+  OCG_FK(9, 16, 8)    // double integrator (b 8, wg 0)
+  OCG_FK(16, 0, 0)
+  OCG_FK(13, 25, 13)  // Goddard (b 12, wg 1)
+  OCG_FK(24, 1, 1)
+  OCG_FK(17, 32, 16)  // cart-pendulum (b 16, wg 0)
+  OCG_FK(32, 0, 0)
+  OCG_FK(18, 35, 18)  // hang glider (b 17, wg 1)
+  OCG_FK(34, 1, 1)
+  OCG_FK(28, 55, 28)  // shuttle (b 27, wg 1)
+  OCG_FK(54, 1, 1)
+  OCG_FK(38, 74, 37)  // quadrotor (b 37, wg 0)
+  OCG_FK(74, 0, 0)
+#undef OCG_FK
+  return factor_k<0, -1, -1>;
 }
 
 // segments of parity `par` add their Schur complements into the separator
@@ -934,16 +923,21 @@ void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, doub
 
 void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_w, double delta_c, double* Dinv,
                  long long* inertia_parts, long long* inertia, cudaStream_t s) {
+  const BandSeg& s0 = P.segs[0];
+  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early);
+  const FactorKernel fsep =
+      P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early) : fseg;
   if (P.smem_factor > 48 * 1024)
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(factor_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(P.smem_factor));
+    for (FactorKernel f : {fseg, fsep})
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(P.smem_factor));
   static const bool timing = std::getenv("OCG_TIMING") != nullptr;
   cudaEvent_t ev[4];
   if (timing)
     for (auto& e : ev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(ev[0], s);
-  factor_k<<<P.nseg, kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv,
-                                                         inertia_parts);
+  fseg<<<P.nseg, kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv,
+                                                      inertia_parts);
   if (timing) cudaEventRecord(ev[1], s);
   int blocks = P.nseg;
   if (P.nseg > 1) {
@@ -952,8 +946,8 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
       schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
     if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
     if (timing) cudaEventRecord(ev[2], s);
-    factor_k<<<1, kFactorThreads, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv,
-                                                      inertia_parts);
+    fsep<<<1, kFactorThreads, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv,
+                                                   inertia_parts);
     if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
