@@ -317,15 +317,15 @@ __device__ __forceinline__ bool zero_pivot(double d, double scale) {
 // blocks a model produces (BC = b + 1, WC = border rows, WEC = rows coupled
 // from column 0; 0 / -1 = read them from the descriptor), so the per-column
 // loops have constant trip counts and constant divisors.
-template <int BC, int WC, int WEC>
-__global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __restrict__ segs, int seg0,
+template <int BC, int WC, int WEC, int TT>
+__global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs, int seg0,
                                                            double* __restrict__ buf,
                                                            const double* __restrict__ primal, double dw, double dc,
                                                            double* __restrict__ Dinv,
                                                            long long* __restrict__ inertia_parts) {
   extern __shared__ double sm[];
   const BandSeg g = segs[seg0 + blockIdx.x];
-  constexpr int T = kFactorThreads;
+  constexpr int T = TT;
   const int tid = threadIdx.x;
   const long long n = g.n;
   const int B1 = BC > 0 ? BC : g.b + 1;
@@ -538,24 +538,25 @@ __global__ void __launch_bounds__(kFactorThreads) factor_k(const BandSeg* __rest
 using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, double, double, double*, long long*);
 
 // instantiations for the blocks of the shipped models (segment: b + 1,
-// 2b + wg, b + wg; separator system: 2b, wg, wg), else the generic kernel
-FactorKernel factor_kernel_for(int B1, int w, int we) {
-#define OCG_FK(a, c, e) \
-  if (B1 == (a) && w == (c) && we == (e)) return factor_k<a, c, e>;
-  OCG_FK(9, 16, 8)    // double integrator (b 8, wg 0)
-  OCG_FK(16, 0, 0)
-  OCG_FK(13, 25, 13)  // Goddard (b 12, wg 1)
-  OCG_FK(24, 1, 1)
-  OCG_FK(17, 32, 16)  // cart-pendulum (b 16, wg 0)
-  OCG_FK(32, 0, 0)
-  OCG_FK(18, 35, 18)  // hang glider (b 17, wg 1)
-  OCG_FK(34, 1, 1)
-  OCG_FK(28, 55, 28)  // shuttle (b 27, wg 1)
-  OCG_FK(54, 1, 1)
-  OCG_FK(38, 74, 37)  // quadrotor (b 37, wg 0)
-  OCG_FK(74, 0, 0)
+// 2b + wg, b + wg, many blocks of 256 threads; separator system: 2b, wg, wg,
+// one block of 1024 threads), else the generic kernels
+FactorKernel factor_kernel_for(int B1, int w, int we, bool single) {
+#define OCG_FK(a, c, e, t) \
+  if (B1 == (a) && w == (c) && we == (e) && single == ((t) == 1024)) return factor_k<a, c, e, t>;
+  OCG_FK(9, 16, 8, 256)    // double integrator (b 8, wg 0)
+  OCG_FK(16, 0, 0, 1024)
+  OCG_FK(13, 25, 13, 256)  // Goddard (b 12, wg 1)
+  OCG_FK(24, 1, 1, 1024)
+  OCG_FK(17, 32, 16, 256)  // cart-pendulum (b 16, wg 0)
+  OCG_FK(32, 0, 0, 1024)
+  OCG_FK(18, 35, 18, 256)  // hang glider (b 17, wg 1)
+  OCG_FK(34, 1, 1, 1024)
+  OCG_FK(28, 55, 28, 256)  // shuttle (b 27, wg 1)
+  OCG_FK(54, 1, 1, 1024)
+  OCG_FK(38, 74, 37, 256)  // quadrotor (b 37, wg 0)
+  OCG_FK(74, 0, 0, 1024)
 #undef OCG_FK
-  return factor_k<0, -1, -1>;
+  return single ? factor_k<0, -1, -1, 1024> : factor_k<0, -1, -1, 256>;
 }
 
 // segments of parity `par` add their Schur complements into the separator
@@ -923,10 +924,13 @@ void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, doub
 
 void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_w, double delta_c, double* Dinv,
                  long long* inertia_parts, long long* inertia, cudaStream_t s) {
+  // many segments: 256-thread blocks, two per SM; a single sequential block
+  // (the separator system, or an unpartitioned band): 1024 threads
   const BandSeg& s0 = P.segs[0];
-  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early);
+  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, P.nseg == 1);
   const FactorKernel fsep =
-      P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early) : fseg;
+      P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true) : fseg;
+  const int tseg = P.nseg == 1 ? 1024 : kFactorThreads;
   if (P.smem_factor > 48 * 1024)
     for (FactorKernel f : {fseg, fsep})
       cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -936,8 +940,7 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   if (timing)
     for (auto& e : ev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(ev[0], s);
-  fseg<<<P.nseg, kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv,
-                                                      inertia_parts);
+  fseg<<<P.nseg, tseg, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts);
   if (timing) cudaEventRecord(ev[1], s);
   int blocks = P.nseg;
   if (P.nseg > 1) {
@@ -946,8 +949,7 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
       schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
     if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
     if (timing) cudaEventRecord(ev[2], s);
-    fsep<<<1, kFactorThreads, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv,
-                                                   inertia_parts);
+    fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts);
     if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
