@@ -175,6 +175,17 @@ int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_str
 /* fused eval_constraints_jacobian + eval_hessian at one x (one forward pass) */
 int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double* c, ocg_stream s);
 int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s); /* out: device scalar */
+/* Node-range shards: the objective's 512-instance chunk
+ * partials (Backend::par_reduce, backend.cpp:119-133) of this context's
+ * instances — device array of ocg_eval_objective_chunks() doubles, chunks of
+ * other shards left as whatever the kernel computes from the stale values —
+ * and the fixed-order combine of a partials array gathered over all shards
+ * (each chunk taken from its owner) into the scaled objective. With shard
+ * boundaries on chunk boundaries the result equals ocg_eval_objective's
+ * bit for bit. */
+int64_t ocg_eval_objective_chunks(const ocg_eval* e);
+int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, ocg_stream s);
+int ocg_eval_objective_combine(ocg_eval* e, const double* partials, double* f, ocg_stream s);
 /* Synchronise s; OCG_OK if every evaluation since the last call was finite,
  * else OCG_EVAL_DOMAIN. Clears the flag. */
 int ocg_eval_status(ocg_eval* e, ocg_stream s);

@@ -4,7 +4,9 @@ Jacobian / Lagrangian-Hessian evaluation into the reference's COO slots, the
 atomic-free KKT assembly and the interior-point vector kernels, behind the
 reference's EvalContext / KktAssembler interface (include/octgpu.h).
 """
-from .evaluation import BandLdl, EvalContext, KktAssembler, Model, Solver, solve, synth_uniform  # noqa: F401
+from .evaluation import (BandLdl, EvalContext, KktAssembler, Model, Solver, objective_chunk_owners,  # noqa: F401
+                         solve, synth_uniform)
 from .models import MODELS  # noqa: F401
 
-__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "Solver", "solve", "synth_uniform"]
+__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "Solver", "objective_chunk_owners", "solve",
+           "synth_uniform"]

@@ -23,6 +23,7 @@ EXPORTS = [
     "ocg_eval_buffer", "ocg_eval_bind_buffer", "ocg_eval_set_scaling", "ocg_eval_get_scaling", "ocg_eval_compute_scaling",
     "ocg_eval_constraints", "ocg_eval_constraints_jacobian", "ocg_eval_objective", "ocg_eval_gradient",
     "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_max_abs_hessian", "ocg_eval_status",
+    "ocg_eval_objective_chunks", "ocg_eval_objective_partials", "ocg_eval_objective_combine",
     "ocg_eval_launch_count",
     "ocg_debug_generated_source", "ocg_debug_compile", "ocg_debug_compile_log",
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
@@ -98,6 +99,9 @@ def _load() -> C.CDLL:
         "ocg_eval_jac_hess": (i32, [vp, dp, dp, dp, vp]),
         "ocg_eval_max_abs_hessian": (i32, [vp, dp, vp]),
         "ocg_eval_status": (i32, [vp, vp]),
+        "ocg_eval_objective_chunks": (i64, [vp]),
+        "ocg_eval_objective_partials": (i32, [vp, dp, dp, vp]),
+        "ocg_eval_objective_combine": (i32, [vp, dp, dp, vp]),
         "ocg_eval_launch_count": (i64, [vp]),
         "ocg_debug_generated_source": (vp, [vp, i32, i32]),
         "ocg_debug_compile": (i32, [vp, i32, i32]),

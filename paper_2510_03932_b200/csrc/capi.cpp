@@ -894,6 +894,33 @@ int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
   OCG_GUARD_END
 }
 
+int64_t ocg_eval_objective_chunks(const ocg_eval* e) { return e ? e->n_chunks : -1; }
+
+int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, ocg_stream s) {
+  if (!e || !x || !partials) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  double* ov = e->objv.p;
+  int* fl = e->flag.p;
+  Index ns = e->n_spec("ocg_objv");
+  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns};
+  e->launch(e->k_objv, "ocg_objv", args, st(s));
+  ocg::dev::objective_chunk_sums(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks,
+                                 static_cast<int>(e->obj_weight.size()), partials, st(s));
+  e->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_eval_objective_combine(ocg_eval* e, const double* partials, double* f, ocg_stream s) {
+  if (!e || !partials || !f) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::dev::objective_combine(partials, e->og_cbase.p, e->og_weight.p, static_cast<int>(e->obj_weight.size()),
+                              e->obj_scale, f, e->flag.p, st(s));
+  e->launches += 1;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
 int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stream s) {
   if (!e || !x || !grad_dense) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN

@@ -166,14 +166,24 @@ int grid_for(int64_t n, int block) {
 
 }  // namespace
 
+void objective_chunk_sums(const double* objv, const int64_t* group_off, const int64_t* group_count,
+                          const int64_t* chunk_base, int64_t n_chunks, int n_groups, double* partials,
+                          cudaStream_t s) {
+  if (n_chunks <= 0) return;
+  const int blocks = static_cast<int>((n_chunks + 7) / 8);
+  chunk_sums<<<blocks, 256, 0, s>>>(objv, group_off, group_count, chunk_base, n_chunks, n_groups, partials);
+}
+
+void objective_combine(const double* partials, const int64_t* chunk_base, const double* weights, int n_groups,
+                       double obj_scale, double* f, int* flag, cudaStream_t s) {
+  combine_chunks<<<1, 32, 0, s>>>(partials, chunk_base, weights, n_groups, obj_scale, f, flag);
+}
+
 void objective_reduce(const double* objv, const int64_t* group_off, const int64_t* group_count,
                       const int64_t* chunk_base, int64_t n_chunks, const double* weights, int n_groups,
                       double obj_scale, double* partials, double* f, int* flag, cudaStream_t s) {
-  if (n_chunks > 0) {
-    const int blocks = static_cast<int>((n_chunks + 7) / 8);
-    chunk_sums<<<blocks, 256, 0, s>>>(objv, group_off, group_count, chunk_base, n_chunks, n_groups, partials);
-  }
-  combine_chunks<<<1, 32, 0, s>>>(partials, chunk_base, weights, n_groups, obj_scale, f, flag);
+  objective_chunk_sums(objv, group_off, group_count, chunk_base, n_chunks, n_groups, partials, s);
+  objective_combine(partials, chunk_base, weights, n_groups, obj_scale, f, flag, s);
 }
 
 void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,

@@ -20,6 +20,15 @@ void objective_reduce(const double* objv, const int64_t* group_off, const int64_
                       const int64_t* chunk_base, int64_t n_chunks, const double* weights, int n_groups,
                       double obj_scale, double* partials, double* f, int* flag, cudaStream_t s);
 
+// the two halves of objective_reduce, for node-range shards: per-chunk
+// partials of this shard's instances, then the fixed-order combine of the
+// chunk partials (gathered from every shard)
+void objective_chunk_sums(const double* objv, const int64_t* group_off, const int64_t* group_count,
+                          const int64_t* chunk_base, int64_t n_chunks, int n_groups, double* partials,
+                          cudaStream_t s);
+void objective_combine(const double* partials, const int64_t* chunk_base, const double* weights, int n_groups,
+                       double obj_scale, double* f, int* flag, cudaStream_t s);
+
 // out[i] = sum_{p in [ptr[i], ptr[i+1])} src[idx[p]]  (0.0-based, in p order)
 void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,
                 cudaStream_t s);

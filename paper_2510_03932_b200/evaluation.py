@@ -223,9 +223,68 @@ class EvalContext:
     def launch_gradient(self, x: torch.Tensor, g: torch.Tensor, stream=None) -> None:
         check(LIB.ocg_eval_gradient(self._h, _ptr(x), _ptr(g), _stream(stream)))
 
+    # ---- node-range shards: the objective as chunk partials + combine ----
+    @property
+    def objective_chunks(self) -> int:
+        return int(LIB.ocg_eval_objective_chunks(self._h))
+
+    def launch_objective_partials(self, x: torch.Tensor, partials: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_objective_partials(self._h, _ptr(x), _ptr(partials), _stream(stream)))
+
+    def launch_objective_combine(self, partials: torch.Tensor, f: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_objective_combine(self._h, _ptr(partials), _ptr(f), _stream(stream)))
+
+    def eval_objective_sharded(self, x, owners: torch.Tensor, group=None) -> tuple[bool, float]:
+        """eval_objective over node-range shards, one context per rank: each
+        rank's chunk partials are kept where `owners` (objective_chunk_owners)
+        says the chunk is its own and zeroed elsewhere, summed over the ranks
+        (each chunk has one nonzero term, so the sum is exact) and combined in
+        the reference's fixed order (backend.cpp:119-133) — bit-identical to an
+        unsharded eval_objective. Without an initialised process group this is
+        the single-rank case."""
+        import torch.distributed as dist
+        x = self._dev(x)
+        n = max(1, self.objective_chunks)
+        part = torch.empty(n, dtype=torch.float64, device=self.device)
+        self.launch_objective_partials(x, part)
+        part = torch.where(owners.to(self.device), part, torch.zeros((), dtype=torch.float64, device=self.device))
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+        ok = self.status()  # this shard's domain errors, then every rank's
+        if dist.is_available() and dist.is_initialized():
+            t = torch.tensor([int(ok)], dtype=torch.int32, device=self.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            ok = bool(t.item())
+        self.launch_objective_combine(part, self._f)
+        ok = self.status() and ok
+        return ok, float(self._f.item())
+
     @property
     def launch_count(self) -> int:
         return LIB.ocg_eval_launch_count(self._h)
+
+
+def objective_chunk_owners(structure: dict, idx_lo: int, idx_hi: int, specials: bool) -> np.ndarray:
+    """Which of the objective's 512-instance chunks (in EvalContext order:
+    objective groups in model order, chunks in index order) a shard evaluating
+    grid indices [idx_lo, idx_hi) — plus the endpoint instances when
+    `specials` — computes in full. A chunk the shard only partly covers is an
+    error: shard boundaries must fall on chunk boundaries of every objective
+    group (multiples of 512 from the group's first index)."""
+    owned = []
+    for g in structure["obj_groups"]:
+        lo, hi, ends = g["range"]
+        count = 2 if ends else hi - lo
+        for j in range((count + 511) // 512):
+            if ends:
+                owned.append(bool(specials))
+                continue
+            a, b = lo + 512 * j, min(hi, lo + 512 * (j + 1))
+            inside = idx_lo <= a and b <= idx_hi
+            if not inside and max(a, idx_lo) < min(b, idx_hi):
+                raise ValueError(f"objective chunk [{a}, {b}) straddles the shard [{idx_lo}, {idx_hi})")
+            owned.append(inside)
+    return np.array(owned, dtype=bool)
 
 
 class KktAssembler:
