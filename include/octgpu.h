@@ -285,6 +285,19 @@ int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double*
 /* x_out[nvar] (host, may be NULL): final iterate */
 int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out);
 
+/* nb independent instances of the model's structure solved together
+ * (BASELINE config 5): each instance follows exactly the
+ * decisions of ocg_ipm_solve / the reference Solver, while every device step
+ * is ONE launch over all instances that reached it (instance x node grids).
+ * Instance arrays are host [nb][nvar] (lvar, uvar, x_start) and [nb][m_con]
+ * (lcon, ucon), NULL = the model's own for every instance; each instance must
+ * fix the same slots as the model. out[nb]; x_out[nb][nvar] may be NULL.
+ * time_total / time_setup / time_plan_* are the batch's; time_derivatives and
+ * time_solve carry the batch's launch rounds and launch groups. nb <= 65535. */
+int ocg_ipm_batch_solve(ocg_model* m, const ocg_ipm_options* opts, int device, int nb, const double* lvar,
+                        const double* uvar, const double* x_start, const double* lcon, const double* ucon,
+                        ocg_ipm_result* out, double* x_out);
+
 #ifdef __cplusplus
 }
 #endif

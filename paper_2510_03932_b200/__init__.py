@@ -5,8 +5,8 @@ atomic-free KKT assembly and the interior-point vector kernels, behind the
 reference's EvalContext / KktAssembler interface (include/octgpu.h).
 """
 from .evaluation import (BandLdl, EvalContext, KktAssembler, Model, Solver, objective_chunk_owners,  # noqa: F401
-                         solve, synth_uniform)
+                         solve, solve_batch, synth_uniform)
 from .models import MODELS  # noqa: F401
 
-__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "Solver", "objective_chunk_owners", "solve",
+__all__ = ["BandLdl", "EvalContext", "KktAssembler", "Model", "MODELS", "Solver", "objective_chunk_owners", "solve", "solve_batch",
            "synth_uniform"]

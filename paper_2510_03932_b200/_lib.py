@@ -30,7 +30,7 @@ EXPORTS = [
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
     "ocg_kkt_norm_inf", "ocg_ipm_default_options", "ocg_ipm_solve",
-    "ocg_ipm_ctx_create", "ocg_ipm_ctx_destroy", "ocg_ipm_ctx_solve",
+    "ocg_ipm_ctx_create", "ocg_ipm_ctx_destroy", "ocg_ipm_ctx_solve", "ocg_ipm_batch_solve",
 ]
 
 
@@ -121,6 +121,8 @@ def _load() -> C.CDLL:
         "ocg_ipm_ctx_create": (i32, [vp, i32, C.POINTER(vp)]),
         "ocg_ipm_ctx_destroy": (None, [vp]),
         "ocg_ipm_ctx_solve": (i32, [vp, C.POINTER(IpmOptions), dp, dp, dp, dp, dp, C.POINTER(IpmResult), dp]),
+        "ocg_ipm_batch_solve": (i32, [vp, C.POINTER(IpmOptions), i32, i32, dp, dp, dp, dp, dp, C.POINTER(IpmResult),
+                                      dp]),
         "ocg_ldl_create": (i32, [vp, C.POINTER(vp)]),
         "ocg_ldl_destroy": (None, [vp]),
         "ocg_ldl_info": (i32, [vp, dp]),

@@ -299,12 +299,19 @@ __device__ __forceinline__ void cp_wait() {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
+// batched launches (BandBatch::ids != NULL): grid row y works on system ids[y]
+__device__ __forceinline__ long long batch_id(const BandBatch& bb) { return bb.ids ? bb.ids[blockIdx.y] : 0; }
+
 __global__ void scatter_k(const double* __restrict__ kval, const int64_t* __restrict__ dst, int64_t nnz,
-                          double* __restrict__ buf) {
+                          double* __restrict__ buf, BandBatch bb) {
+  const long long bi = batch_id(bb);
+  kval += bi * nnz;
+  buf += bi * bb.sbuf;
   GRID_LOOP(p, nnz) buf[dst[p]] = kval[p];
 }
 
-__global__ void zero_k(double* __restrict__ buf, int64_t len) {
+__global__ void zero_k(double* __restrict__ buf, int64_t len, BandBatch bb) {
+  buf += batch_id(bb) * bb.sbuf;
   GRID_LOOP(p, len) buf[p] = 0.0;
 }
 
@@ -322,9 +329,19 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
                                                            double* __restrict__ buf,
                                                            const double* __restrict__ primal, double dw, double dc,
                                                            double* __restrict__ Dinv,
-                                                           long long* __restrict__ inertia_parts) {
+                                                           long long* __restrict__ inertia_parts, BandBatch bb) {
   extern __shared__ double sm[];
   const BandSeg g = segs[seg0 + blockIdx.x];
+  if (bb.ids) {
+    const long long bi = bb.ids[blockIdx.y];
+    buf += bi * bb.sbuf;
+    Dinv += bi * bb.sdim;
+    inertia_parts += bi * bb.sparts;
+    if (bb.dw) {
+      dw = bb.dw[blockIdx.y];
+      dc = bb.dc[blockIdx.y];
+    }
+  }
   constexpr int T = TT;
   const int tid = threadIdx.x;
   const long long n = g.n;
@@ -535,7 +552,8 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
   }
 }
 
-using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, double, double, double*, long long*);
+using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, double, double, double*, long long*,
+                              BandBatch);
 
 // instantiations for the blocks of the shipped models (segment: b + 1,
 // 2b + wg, b + wg, many blocks of 256 threads; separator system: 2b, wg, wg,
@@ -557,6 +575,21 @@ FactorKernel factor_kernel_for(int B1, int w, int we, bool single) {
   OCG_FK(74, 0, 0, 1024)
 #undef OCG_FK
   return single ? factor_k<0, -1, -1, 1024> : factor_k<0, -1, -1, 256>;
+}
+
+// unpartitioned bands of many small systems (batched solves): 128 threads per
+// system, several systems per SM
+FactorKernel factor_kernel_batch(int B1, int w, int we) {
+#define OCG_FKB(a, c, e) \
+  if (B1 == (a) && w == (c) && we == (e)) return factor_k<a, c, e, 128>;
+  OCG_FKB(9, 0, 0)    // double integrator
+  OCG_FKB(13, 1, 1)   // Goddard
+  OCG_FKB(17, 0, 0)   // cart-pendulum
+  OCG_FKB(18, 1, 1)   // hang glider
+  OCG_FKB(28, 1, 1)   // shuttle
+  OCG_FKB(38, 0, 0)   // quadrotor
+#undef OCG_FKB
+  return factor_k<0, -1, -1, 128>;
 }
 
 // segments of parity `par` add their Schur complements into the separator
@@ -615,12 +648,18 @@ __global__ void inertia_sum_k(const long long* __restrict__ parts, int nblocks, 
 }
 
 __global__ void gather_k(const double* __restrict__ rhs, const int64_t* __restrict__ perm, int64_t dim,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, BandBatch bb) {
+  const long long bi = batch_id(bb);
+  rhs += bi * bb.sdim;
+  out += bi * bb.swork;
   GRID_LOOP(p, dim) out[p] = rhs[perm[p]];
 }
 
 __global__ void scatter_back_k(const double* __restrict__ work, const int64_t* __restrict__ perm, int64_t dim,
-                               double* __restrict__ x) {
+                               double* __restrict__ x, BandBatch bb) {
+  const long long bi = batch_id(bb);
+  work += bi * bb.swork;
+  x += bi * bb.sdim;
   GRID_LOOP(p, dim) x[perm[p]] = work[p];
 }
 
@@ -630,9 +669,16 @@ __global__ void scatter_back_k(const double* __restrict__ work, const int64_t* _
 __global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, int seg0, int mode,
                                               const double* __restrict__ buf, const double* __restrict__ Dinv,
                                               double* __restrict__ work, double* __restrict__ gparts, int wmax,
-                                              const int64_t* __restrict__ border_pos, long long sep_pos0) {
+                                              const int64_t* __restrict__ border_pos, long long sep_pos0,
+                                              BandBatch bb) {
   extern __shared__ double sm[];
   const int blk = seg0 + blockIdx.x;
+  if (bb.ids) {
+    const long long bi = bb.ids[blockIdx.y];
+    buf += bi * bb.sbuf;
+    Dinv += bi * bb.sdim;
+    work += bi * bb.swork;
+  }
   const BandSeg g = segs[blk];
   const int lane = threadIdx.x;
   const long long n = g.n;
@@ -917,9 +963,9 @@ int64_t* band_dst(const BandDstIn& in, const std::vector<int8_t>& lk, const std:
 }
 
 void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, double* buf, cudaStream_t s) {
-  zero_k<<<grid_for(P.buf_len), 256, 0, s>>>(buf, P.buf_len);
+  zero_k<<<grid_for(P.buf_len), 256, 0, s>>>(buf, P.buf_len, BandBatch{});
   const int64_t nnz = P.nnz;
-  if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, D.dst, nnz, buf);
+  if (nnz > 0) scatter_k<<<grid_for(nnz), 256, 0, s>>>(kval, D.dst, nnz, buf, BandBatch{});
 }
 
 void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_w, double delta_c, double* Dinv,
@@ -940,7 +986,7 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   if (timing)
     for (auto& e : ev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(ev[0], s);
-  fseg<<<P.nseg, tseg, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts);
+  fseg<<<P.nseg, tseg, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
   if (timing) cudaEventRecord(ev[1], s);
   int blocks = P.nseg;
   if (P.nseg > 1) {
@@ -949,7 +995,7 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
       schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
     if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
     if (timing) cudaEventRecord(ev[2], s);
-    fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts);
+    fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
@@ -974,20 +1020,65 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
   if (P.smem_solve > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(P.smem_solve));
-  gather_k<<<grid_for(dim), 256, 0, s>>>(rhs, D.perm, dim, work);
+  gather_k<<<grid_for(dim), 256, 0, s>>>(rhs, D.perm, dim, work, BandBatch{});
   if (P.nseg == 1) {
-    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, 0);
+    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, 0, BandBatch{});
   } else {
     const BandSeg& sep = P.segs.back();
-    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
     for (int par = 0; par < 2; ++par)
       rhs_add_k<<<grid_for(((P.nseg + 1) / 2) * P.wmax), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos,
                                                                         gparts, work + sep.pos);
     if (P.wg > 0) rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos);
-    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
-    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
   }
-  scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, D.perm, dim, x);
+  scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, D.perm, dim, x, BandBatch{});
+}
+
+void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, double* buf, double* Dinv,
+                       long long* inertia, const int* ids, int nb, const double* dws, const double* dcs,
+                       cudaStream_t s) {
+  if (P.nseg != 1) throw std::runtime_error("band_factor_batch: the batched plan must be unpartitioned");
+  if (nb <= 0) return;
+  BandBatch bb;
+  bb.ids = ids;
+  bb.sbuf = P.buf_len;
+  bb.sdim = P.dim;
+  bb.swork = P.dim + P.wmax;
+  bb.sparts = 3;
+  bb.dw = dws;
+  bb.dc = dcs;
+  const unsigned ny = static_cast<unsigned>(nb);
+  const int gz = std::max(1, std::min(grid_for(P.buf_len), 8));
+  zero_k<<<dim3(gz, ny), 256, 0, s>>>(buf, P.buf_len, bb);
+  if (P.nnz > 0) scatter_k<<<dim3(std::max(1, std::min(grid_for(P.nnz), 8)), ny), 256, 0, s>>>(kval, D.dst, P.nnz, buf, bb);
+  const BandSeg& s0 = P.segs[0];
+  const FactorKernel f = factor_kernel_batch(s0.b + 1, s0.w, s0.w_early);
+  if (P.smem_factor > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P.smem_factor));
+  f<<<dim3(1, ny), 128, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, inertia, bb);
+}
+
+void band_solve_batch(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
+                      double* x, double* work, const int* ids, int nb, cudaStream_t s) {
+  if (P.nseg != 1) throw std::runtime_error("band_solve_batch: the batched plan must be unpartitioned");
+  if (nb <= 0) return;
+  BandBatch bb;
+  bb.ids = ids;
+  bb.sbuf = P.buf_len;
+  bb.sdim = P.dim;
+  bb.swork = P.dim + P.wmax;
+  const unsigned ny = static_cast<unsigned>(nb);
+  const int gd = std::max(1, std::min(grid_for(P.dim), 8));
+  if (P.smem_solve > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P.smem_solve));
+  gather_k<<<dim3(gd, ny), 256, 0, s>>>(rhs, D.perm, P.dim, work, bb);
+  solve_k<<<dim3(1, ny), 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, work + P.dim, P.wmax, D.border_pos, 0,
+                                               bb);
+  scatter_back_k<<<dim3(gd, ny), 256, 0, s>>>(work, D.perm, P.dim, x, bb);
 }
 
 }  // namespace dev

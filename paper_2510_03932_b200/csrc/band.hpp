@@ -80,6 +80,15 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
 
 namespace dev {
 
+// Batched launches over many systems of one plan (ids != NULL): grid row y
+// factors / solves system ids[y]; per-system arrays are [system][stride].
+struct BandBatch {
+  const int* ids = nullptr;
+  long long sbuf = 0, sdim = 0, swork = 0, sparts = 0;  // strides: factor buffer, Dinv / vectors, work, inertia
+  const double* dw = nullptr;  // [y] regularization per launched system (NULL: the scalar arguments)
+  const double* dc = nullptr;
+};
+
 struct BandDstIn {
   const int64_t* colp = nullptr;
   const int64_t* rowi = nullptr;
@@ -110,6 +119,15 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
 // x = (K + deltas)^{-1} rhs (KKT index order); work[dim + nseg*wmax] scratch
 void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
                 double* x, double* work, cudaStream_t s);
+
+// Batched factor / solve of the systems ids[0..nb) (unpartitioned plans only):
+// kval [system][nnz] -> buf [system][buf_len], Dinv [system][dim], inertia
+// [system][3] = (pos, neg, zero); rhs, x [system][dim], work [system][dim + wmax].
+void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, double* buf, double* Dinv,
+                       long long* inertia, const int* ids, int nb, const double* dws, const double* dcs,
+                       cudaStream_t s);
+void band_solve_batch(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
+                      double* x, double* work, const int* ids, int nb, cudaStream_t s);
 
 }  // namespace dev
 }  // namespace ocg

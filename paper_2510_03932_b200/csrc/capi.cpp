@@ -31,6 +31,7 @@
 #include "kernels.hpp"
 #include "model.hpp"
 #include "plan.hpp"
+#include "handles.hpp"
 
 using ocg::Index;
 
@@ -43,154 +44,12 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  bool owned = true;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  // Stream-ordered pool allocations on the calling thread's default stream:
-  // unlike cudaMalloc/cudaFree they never synchronize the device, so plans
-  // created and destroyed by concurrent host threads (batched solves) do not
-  // serialize each other's streams.
-  ~DBuf() {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
-  }
-  // caller-owned device memory of the same size replaces the library buffer
-  void bind(T* ext) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
-    p = ext;
-    owned = false;
-  }
-  // take ownership of device memory from cudaMallocAsync
-  void adopt(T* ptr, size_t count) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
-    p = ptr;
-    n = count;
-    owned = true;
-  }
-  void alloc(size_t count) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
-    owned = true;
-    p = nullptr;
-    n = count;
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
-       "cudaMallocAsync");
-    ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
-  }
-  void upload(const std::vector<T>& v) {
-    alloc(v.size());
-    if (!v.empty()) {
-      ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, cudaStreamPerThread), "upload");
-      ck(cudaStreamSynchronize(cudaStreamPerThread), "upload sync");
-    }
-  }
-};
-
 cudaStream_t st(ocg_stream s) { return static_cast<cudaStream_t>(s); }
+using ocg::hd::ck;
+using ocg::hd::CudaError;
+using ocg::hd::kNoBatch;
 
 }  // namespace
-
-struct ocg_model {
-  ocg::Problem prob;
-  ocg::Nlp nlp;
-};
-
-struct ocg_eval {
-  const ocg_model* model = nullptr;
-  int device = 0;
-  ocg::Layout lay;
-  std::map<std::string, std::shared_ptr<ocg::JitModule>> mods;  // one module per kernel (process-wide cache)
-  cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,
-               k_grad = nullptr;
-  int block = 128;
-  bool specials = true;
-  std::map<std::string, int> slices, tail, smem;
-  std::vector<long long> prm;  // by-value parameter block of the generated kernels
-  std::map<std::string, int> resident;  // resident blocks per SM per kernel
-  int sm_count = 148;
-  Index i0 = 0, n_main = 0;
-
-  DBuf<double> jac, hess, grad, row_scale, objv, objw, partials, scratch;
-  DBuf<int> flag;
-  double obj_scale = 1.0;
-  std::vector<double> obj_weight;  // group weights (host)
-
-  // objective reduction plan
-  DBuf<int64_t> og_off, og_count, og_cbase;
-  Index n_chunks = 0;
-  DBuf<double> og_weight;
-
-  // dense gradient gather (slot -> grad COO entries)
-  DBuf<int64_t> gg_ptr;
-  DBuf<int32_t> gg_idx;
-
-  int64_t launches = 0;
-  std::map<std::string, int> min_blocks;  // register budget the kernels were compiled for
-
-  // tail instances this shard runs for kernel `name`
-  Index n_spec(const char* name) const { return specials ? tail.at(name) : 0; }
-
-  // persistent grid: min(tiles, SMs x resident blocks per SM)
-  void launch(cudaKernel_t k, const char* name, void** args, cudaStream_t s) {
-    const Index ns = n_spec(name);
-    const Index tiles = (n_main + block - 1) / block;
-    if (tiles <= 0 && ns <= 0) return;
-    const Index cap = static_cast<Index>(sm_count) * std::max(1, resident.at(name));
-    const unsigned grid = static_cast<unsigned>(std::max<Index>(1, std::min(tiles, cap)));
-    ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(static_cast<unsigned>(block)), args,
-                        static_cast<size_t>(smem.at(name)), s),
-       "launch generated kernel");
-    ++launches;
-  }
-
-  void refresh_objw(cudaStream_t s) {
-    std::vector<double> w(obj_weight.size());
-    for (size_t g = 0; g < w.size(); ++g) w[g] = obj_scale * obj_weight[g];  // eval.cpp:206,246
-    if (!w.empty()) ck(cudaMemcpyAsync(objw.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, s), "objw");
-    ck(cudaStreamSynchronize(s), "sync");
-  }
-};
-
-struct ocg_kkt {
-  ocg_eval* ev = nullptr;
-  Index nvar = 0, m_con = 0;
-  Index n_free = 0, n_slack = 0, ntot = 0, m = 0, dim = 0, nnz = 0;
-  bool contradictory = false;
-  std::vector<Index> prim_index, free_slot, slack_index, slack_of, dual_index, dual_row, row_slot;
-  std::vector<double> xlo, xhi;
-  std::vector<Index> colp, rowi;
-  DBuf<double> val;
-  DBuf<int64_t> src_ptr, src_code;
-  Index H = 0, J = 0;
-  // matvec (full symmetric CSR in increasing column order)
-  DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
-  // J^T lambda
-  DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
-};
-
-// Band LDL^T of the KKT matrix (band.hpp): plan + device buffers
-struct ocg_ldl {
-  ocg_kkt* kkt = nullptr;
-  ocg::BandPlan plan;
-  DBuf<int64_t> dst, perm, border_pos;
-  DBuf<ocg::BandSeg> segs;
-  DBuf<double> primal, buf, Dinv, work;
-  DBuf<long long> inertia, inertia_parts;
-  ocg::dev::BandDev dev;
-  double delta_w = 0.0, delta_c = 0.0;
-  int64_t factorizations = 0;
-};
 
 namespace {
 
@@ -831,7 +690,7 @@ int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s) 
   const double* rs = e->row_scale.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_c");
-  void* args[] = {e->prm.data(), &x, &rs, &c, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &rs, &c, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_c, "ocg_c", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -844,7 +703,7 @@ int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_s
   double* jac = e->jac.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_cjac");
-  void* args[] = {e->prm.data(), &x, &rs, &c, &jac, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &rs, &c, &jac, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_cjac, "ocg_cjac", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -858,7 +717,7 @@ int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_str
   double* hess = e->hess.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_hess");
-  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &hess, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_hess, "ocg_hess", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -873,7 +732,7 @@ int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double
   double* hess = e->hess.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_cjh");
-  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &c, &jac, &hess, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &c, &jac, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_cjh, "ocg_cjh", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -885,7 +744,7 @@ int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
-  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_objv, "ocg_objv", args, st(s));
   ocg::dev::objective_reduce(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks, e->og_weight.p,
                              static_cast<int>(e->obj_weight.size()), e->obj_scale, e->partials.p, f, e->flag.p, st(s));
@@ -902,7 +761,7 @@ int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, 
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
-  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_objv, "ocg_objv", args, st(s));
   ocg::dev::objective_chunk_sums(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks,
                                  static_cast<int>(e->obj_weight.size()), partials, st(s));
@@ -928,7 +787,7 @@ int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stre
   double* g = e->grad.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_grad");
-  void* args[] = {e->prm.data(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns};
+  void* args[] = {e->prm.data(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_grad, "ocg_grad", args, st(s));
   ocg::dev::gather_sum(e->grad.p, e->gg_ptr.p, e->gg_idx.p, e->model->nlp.nvar, grad_dense, st(s));
   e->launches += 1;
@@ -1198,6 +1057,16 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
 // ---- band LDL^T (band.hpp) ---------------------------------------------------
 
 int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
+  int target = 2 * 148;
+  if (const char* e = std::getenv("OCG_LDL_SEGMENTS")) target = std::max(1, std::atoi(e));
+  return ocg::hd::ldl_create(k, target, out);
+}
+
+}  // extern "C"
+
+int ocg::hd::set_error(int code, const std::string& msg) { return fail(code, msg); }
+
+int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   const ocg::Nlp& nlp = k->ev->model->nlp;
@@ -1224,8 +1093,6 @@ int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
     node[static_cast<size_t>(k->ntot + d)] = row_node[static_cast<size_t>(k->dual_row[static_cast<size_t>(d)])];
   auto L = std::make_unique<ocg_ldl>();
   L->kkt = k;
-  int target = 2 * 148;
-  if (const char* e = std::getenv("OCG_LDL_SEGMENTS")) target = std::max(1, std::atoi(e));
   {
     // the O(nnz) parts of the plan on the device
     DBuf<int64_t> dcolp, drowi;
@@ -1259,6 +1126,8 @@ int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
   return OCG_OK;
   OCG_GUARD_END
 }
+
+extern "C" {
 
 void ocg_ldl_destroy(ocg_ldl* l) { delete l; }
 

@@ -292,6 +292,11 @@ class Generator {
     os << "// grid-size-dependent integers (offsets, ranges, slab bases) arrive by value:\n";
     for (size_t i = 0; i < pkeys_.size(); ++i) os << "//   prm.v[" << i << "] = " << pkeys_[i] << "\n";
     os << "struct OcgParams { long long v[" << std::max<size_t>(1, pkeys_.size()) << "]; };\n";
+    // batched launches over independent instances of one structure: block z
+    // evaluates instance ids[z]; every array argument advances by its
+    // per-instance stride (roles: x, lam, rs, objw, c, jac, hess, objv, grad,
+    // flag). ids == NULL: one instance, no offsets.
+    os << "struct OcgBatch { const int* ids; long long s[10]; };\n";
     os << "__device__ __forceinline__ bool fin(double v) { return fabs(v) <= 1.7976931348623157e308; }\n";
     os << "#ifndef OCG_HOST_POW\n";
     os << "__device__ __forceinline__ double ocg_pow2(double a) { return a * a; }\n";
@@ -938,8 +943,18 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     // compilation (each kernel is compiled as its own module)
     E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK, OCG_MINB_" + std::string(name) + ") " +
            std::string(name) +
-           "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec) {");
+           "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec, const OcgBatch bt) {");
     E.depth = 1;
+    {
+      static const char* const roles[] = {"x", "lam", "rs", "objw", "cout", "jac", "hess", "objv", "gout", "flag"};
+      std::set<std::string> names;  // last token of every parameter declaration
+      std::stringstream ps(params);
+      for (std::string decl; std::getline(ps, decl, ',');) names.insert(decl.substr(decl.find_last_of(" *") + 1));
+      std::string adv;
+      for (int r = 0; r < 10; ++r)
+        if (names.count(roles[r])) adv += std::string(" ") + roles[r] + " += bz * bt.s[" + std::to_string(r) + "];";
+      E.line("if (bt.ids) { const long long bz = bt.ids[blockIdx.z];" + adv + " }");
+    }
     E.line("extern __shared__ __align__(16) double smem_all[];");
     E.line("const int lane = threadIdx.x & 31;");
     E.line("double* __restrict__ smem = smem_all + (threadIdx.x >> 5) * " + i64(per_warp) + ";");

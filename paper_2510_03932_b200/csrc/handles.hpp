@@ -1,0 +1,192 @@
+// Library-internal definitions of the C ABI's opaque handles (include/octgpu.h),
+// shared by the ABI implementation (capi.cpp) and the batched solver
+// (batch.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/octgpu.h"
+#include "band.hpp"
+#include "jit.hpp"
+#include "model.hpp"
+#include "plan.hpp"
+
+namespace ocg::hd {
+
+using ocg::Index;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  bool owned = true;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  // Stream-ordered pool allocations on the calling thread's default stream:
+  // unlike cudaMalloc/cudaFree they never synchronize the device, so plans
+  // created and destroyed by concurrent host threads (batched solves) do not
+  // serialize each other's streams.
+  ~DBuf() {
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+  }
+  // caller-owned device memory of the same size replaces the library buffer
+  void bind(T* ext) {
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    p = ext;
+    owned = false;
+  }
+  // take ownership of device memory from cudaMallocAsync
+  void adopt(T* ptr, size_t count) {
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    p = ptr;
+    n = count;
+    owned = true;
+  }
+  void alloc(size_t count) {
+    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    owned = true;
+    p = nullptr;
+    n = count;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
+       "cudaMallocAsync");
+    ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) {
+      ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, cudaStreamPerThread), "upload");
+      ck(cudaStreamSynchronize(cudaStreamPerThread), "upload sync");
+    }
+  }
+};
+
+// by-value batch descriptor of the generated kernels (codegen.cpp OcgBatch)
+struct GenBatch {
+  const int* ids;
+  long long s[10];
+};
+inline GenBatch kNoBatch{};
+
+}  // namespace ocg::hd
+
+using ocg::hd::DBuf;
+using ocg::hd::GenBatch;
+using ocg::Index;
+
+
+struct ocg_model {
+  ocg::Problem prob;
+  ocg::Nlp nlp;
+};
+
+struct ocg_eval {
+  const ocg_model* model = nullptr;
+  int device = 0;
+  ocg::Layout lay;
+  std::map<std::string, std::shared_ptr<ocg::JitModule>> mods;  // one module per kernel (process-wide cache)
+  cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,
+               k_grad = nullptr;
+  int block = 128;
+  bool specials = true;
+  std::map<std::string, int> slices, tail, smem;
+  std::vector<long long> prm;  // by-value parameter block of the generated kernels
+  std::map<std::string, int> resident;  // resident blocks per SM per kernel
+  int sm_count = 148;
+  Index i0 = 0, n_main = 0;
+
+  DBuf<double> jac, hess, grad, row_scale, objv, objw, partials, scratch;
+  DBuf<int> flag;
+  double obj_scale = 1.0;
+  std::vector<double> obj_weight;  // group weights (host)
+
+  // objective reduction plan
+  DBuf<int64_t> og_off, og_count, og_cbase;
+  Index n_chunks = 0;
+  DBuf<double> og_weight;
+
+  // dense gradient gather (slot -> grad COO entries)
+  DBuf<int64_t> gg_ptr;
+  DBuf<int32_t> gg_idx;
+
+  int64_t launches = 0;
+  std::map<std::string, int> min_blocks;  // register budget the kernels were compiled for
+
+  // tail instances this shard runs for kernel `name`
+  Index n_spec(const char* name) const { return specials ? tail.at(name) : 0; }
+
+  // persistent grid: min(tiles, SMs x resident blocks per SM)
+  // batched (nz > 1): grid z = instances, the persistent cap shared out
+  void launch(cudaKernel_t k, const char* name, void** args, cudaStream_t s, unsigned nz = 1) {
+    const Index ns = n_spec(name);
+    const Index tiles = (n_main + block - 1) / block;
+    if (tiles <= 0 && ns <= 0) return;
+    const Index cap = static_cast<Index>(sm_count) * std::max(1, resident.at(name));
+    const unsigned grid =
+        static_cast<unsigned>(std::max<Index>(1, std::min(tiles, std::max<Index>(1, cap / static_cast<Index>(nz)))));
+    ocg::hd::ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid, 1, nz), dim3(static_cast<unsigned>(block)), args,
+                        static_cast<size_t>(smem.at(name)), s),
+       "launch generated kernel");
+    ++launches;
+  }
+
+  void refresh_objw(cudaStream_t s) {
+    std::vector<double> w(obj_weight.size());
+    for (size_t g = 0; g < w.size(); ++g) w[g] = obj_scale * obj_weight[g];  // eval.cpp:206,246
+    if (!w.empty()) ocg::hd::ck(cudaMemcpyAsync(objw.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, s), "objw");
+    ocg::hd::ck(cudaStreamSynchronize(s), "sync");
+  }
+};
+
+struct ocg_kkt {
+  ocg_eval* ev = nullptr;
+  Index nvar = 0, m_con = 0;
+  Index n_free = 0, n_slack = 0, ntot = 0, m = 0, dim = 0, nnz = 0;
+  bool contradictory = false;
+  std::vector<Index> prim_index, free_slot, slack_index, slack_of, dual_index, dual_row, row_slot;
+  std::vector<double> xlo, xhi;
+  std::vector<Index> colp, rowi;
+  DBuf<double> val;
+  DBuf<int64_t> src_ptr, src_code;
+  Index H = 0, J = 0;
+  // matvec (full symmetric CSR in increasing column order)
+  DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
+  // J^T lambda
+  DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
+};
+
+// Band LDL^T of the KKT matrix (band.hpp): plan + device buffers
+struct ocg_ldl {
+  ocg_kkt* kkt = nullptr;
+  ocg::BandPlan plan;
+  DBuf<int64_t> dst, perm, border_pos;
+  DBuf<ocg::BandSeg> segs;
+  DBuf<double> primal, buf, Dinv, work;
+  DBuf<long long> inertia, inertia_parts;
+  ocg::dev::BandDev dev;
+  double delta_w = 0.0, delta_c = 0.0;
+  int64_t factorizations = 0;
+};
+
+
+namespace ocg::hd {
+// ocg_ldl_create with an explicit segment target (1 = unpartitioned band)
+int ldl_create(ocg_kkt* k, int target, ocg_ldl** out);
+// ocg_last_error's message for this thread; returns code
+int set_error(int code, const std::string& msg);
+}  // namespace ocg::hd

@@ -412,6 +412,63 @@ def solve(model: Model, device: int = 0, return_x: bool = False, **options) -> d
     return out
 
 
+def solve_batch(model: Model, instances: list[Model] | None = None, n: int | None = None, device: int = 0,
+                return_x: bool = False, lvar=None, uvar=None, x_start=None, lcon=None, ucon=None,
+                **options) -> list[dict]:
+    """Batched device IPM (include/octgpu.h ocg_ipm_batch_solve): instances of
+    `model`'s structure solved together, every device step one launch over
+    all instances. The instances are given as Models of the same structure
+    (e.g. models.cart_pendulum_instance(b)), or as [n][nvar] / [n][m_con]
+    arrays of their bounds and start points (None = the model's own), or as
+    `n` copies of `model`. Each result dict is what solve() returns for that
+    instance; time_total is the batch's wall time."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("octgpu solve_batch needs a CUDA device (no CPU fallback)")
+    o = _lib.IpmOptions()
+    LIB.ocg_ipm_default_options(C.byref(o))
+    for k, v in options.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown IPM option {k!r}")
+        setattr(o, k, type(getattr(o, k))(v))
+    given = {"lvar": lvar, "uvar": uvar, "x_start": x_start, "lcon": lcon, "ucon": ucon}
+    if instances is not None:
+        base = model.arrays()
+        arrs = [m.arrays() for m in instances]
+        for key in given:
+            stacked = np.stack([r[key] for r in arrs])
+            # arrays every instance shares with the model are passed as NULL
+            given[key] = None if np.array_equal(stacked, np.broadcast_to(base[key], stacked.shape)) else stacked
+        nb = len(instances)
+    else:
+        sizes = [len(v) for v in given.values() if v is not None]
+        nb = sizes[0] if sizes else int(n or 1)
+    keep, ptrs = [], []
+    for key, v in given.items():
+        if v is None:
+            ptrs.append(None)
+            continue
+        width = model.nvar if key in ("lvar", "uvar", "x_start") else model.m_con
+        a = np.ascontiguousarray(v, dtype=np.float64)
+        if a.shape != (nb, width):
+            raise ValueError(f"{key}: expected shape {(nb, width)}, got {a.shape}")
+        keep.append(a)
+        ptrs.append(a.ctypes.data)
+    res = (_lib.IpmResult * nb)()
+    x = np.empty((nb, model.nvar)) if return_x else None
+    check(LIB.ocg_ipm_batch_solve(model._h, C.byref(o), int(device), nb, *ptrs, res,
+                                  None if x is None else x.ctypes.data), "ocg_ipm_batch_solve")
+    out = []
+    for b in range(nb):
+        d = {name: getattr(res[b], name) for name, _ in res[b]._fields_}
+        d["status_name"] = STATUS.get(res[b].status, "unknown")
+        d["rounds"] = int(d.pop("time_derivatives"))
+        d["launch_groups"] = int(d.pop("time_solve"))
+        if x is not None:
+            d["x"] = x[b]
+        out.append(d)
+    return out
+
+
 class Solver:
     """Reusable device IPM context (ocg_ipm_ctx_*): plans built once for a
     model structure; solve() takes an instance's bounds / start point."""

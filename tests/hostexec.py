@@ -37,7 +37,7 @@ static std::barrier<>* ocg_warp_barrier = nullptr;
 #define __syncwarp() ocg_warp_barrier->arrive_and_wait()
 #define __align__(n) __attribute__((aligned(n)))
 alignas(16) double smem_all[1 << 18];  // one warp (OCG_BLOCK = 32) on the host: 32 std::threads
-struct ocg_dim3 { unsigned x, y; };
+struct ocg_dim3 { unsigned x, y, z; };
 static thread_local ocg_dim3 blockIdx, threadIdx, gridDim;
 static inline double __fma_rn(double a, double b, double c) { return std::fma(a, b, c); }
 template <class T> static inline T __ldg(const T* p) { return *p; }
@@ -89,8 +89,8 @@ def _driver(name: str, params: str) -> str:
             f"  std::barrier<> bar(32); ocg_warp_barrier = &bar;\n"
             f"  std::vector<std::thread> lanes;\n"
             f"  for (unsigned l = 0; l < 32; ++l) lanes.emplace_back([&, l] {{\n"
-            f"    gridDim.x = 1; blockIdx.x = 0; blockIdx.y = 0; threadIdx.x = l;\n"
-            f"    {name}(prm, {args}, i0, n_main, n_spec); }});\n"
+            f"    gridDim.x = 1; blockIdx.x = 0; blockIdx.y = 0; blockIdx.z = 0; threadIdx.x = l;\n"
+            f"    {name}(prm, {args}, i0, n_main, n_spec, OcgBatch{{}}); }});\n"
             f"  for (auto& th : lanes) th.join();\n}}\n")
 
 
