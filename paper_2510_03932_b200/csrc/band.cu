@@ -577,6 +577,219 @@ FactorKernel factor_kernel_for(int B1, int w, int we, bool single) {
   return single ? factor_k<0, -1, -1, 1024> : factor_k<0, -1, -1, 256>;
 }
 
+// ---- one warp per system: unpartitioned bands without a border, b + 1 <= 32 ----
+//
+// factor_k's algorithm and arithmetic for one small band per warp: the
+// (b+1) x (b+1) window in the warp's shared memory as a ring of column slots
+// (column k in slot k mod (b+1)), the rank-1 update spread over the lanes by
+// a fixed pair assignment held in registers, __syncwarp instead of block
+// barriers, and the column entering the window loaded PF columns ahead into
+// registers (lane j holds its entry j: coalesced).
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int B1, int PF>
+__global__ void __launch_bounds__(128) factor_warp_k(const BandSeg* __restrict__ segs, double* __restrict__ buf,
+                                                     const double* __restrict__ primal, double* __restrict__ Dinv,
+                                                     long long* __restrict__ inertia, BandBatch bb, int nb) {
+  constexpr int b = B1 - 1;
+  constexpr int P = b * (b + 1) / 2;     // update pairs j1 <= j2 in 1..b
+  constexpr int T = (P + 31) / 32;       // pairs per lane
+  constexpr int WS = B1 * B1 + 3 * B1;   // shared doubles per warp: window, pivot scales, y, l
+  __shared__ double smem[4 * WS];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int yidx = blockIdx.x * 4 + wib;
+  if (yidx >= nb) return;  // warp-uniform
+  double* W = smem + wib * WS;
+  double* ps = W + B1 * B1;
+  double* yv = ps + B1;
+  double* lv = yv + B1;
+  const long long bi = bb.ids[yidx];
+  const double dw = bb.dw[yidx], dc = bb.dc[yidx];
+  const BandSeg g = segs[0];
+  const long long n = g.n;
+  double* band = buf + bi * bb.sbuf + g.band;
+  double* dinvp = Dinv + bi * bb.sdim + g.pos;
+  const double* flag = primal + g.pos;
+  // this lane's update pairs (fixed for the whole factorization)
+  int pj1[T], pj2[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int p = lane + 32 * t;
+    int j1 = 1, rem = p < P ? p : 0;
+    while (rem >= b - j1 + 1) {
+      rem -= b - j1 + 1;
+      ++j1;
+    }
+    pj1[t] = p < P ? j1 : 0;
+    pj2[t] = p < P ? j1 + rem : 0;
+  }
+  // column c entry `lane` (+ delta on the diagonal), 0 outside the matrix
+  auto column = [&](long long c) -> double {
+    if (lane >= B1 || c >= n || c + lane >= n) return 0.0;
+    double v = band[c * B1 + lane];
+    if (lane == 0) v += flag[c] != 0.0 ? dw : -dc;
+    return v;
+  };
+  for (int c = 0; c < B1; ++c) {
+    const double v = column(c);
+    if (lane < B1) W[c * B1 + lane] = v;
+    if (lane == 0) ps[c] = fabs(v);
+  }
+  double pf[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) pf[q] = column(B1 + q);
+  __syncwarp();
+  long long npos = 0, nneg = 0, nzero = 0;
+  int s = 0;
+  for (long long k0 = 0; k0 < n; k0 += PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const long long k = k0 + q;
+      if (k >= n) break;
+      const double d = W[s * B1];
+      const bool zero = zero_pivot(d, ps[s]);
+      const double dinv = zero ? 0.0 : 1.0 / d;
+      if (lane == 0) {
+        dinvp[k] = dinv;
+        band[k * B1] = d;
+        if (zero)
+          ++nzero;
+        else if (d > 0)
+          ++npos;
+        else
+          ++nneg;
+      } else if (lane < B1) {
+        const double yj = k + lane < n ? W[s * B1 + lane] : 0.0;
+        const double lj = yj * dinv;
+        yv[lane] = yj;
+        lv[lane] = lj;
+        if (k + lane < n) band[k * B1 + lane] = lj;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (lane + 32 * t < P) {
+          const int j1 = pj1[t], j2 = pj2[t];
+          const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
+          const double upd = lv[j2] * yv[j1];
+          W[s1 * B1 + (j2 - j1)] -= upd;
+          if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
+        }
+      }
+      __syncwarp();
+      // column k is final: its slot takes column k + B1
+      if (lane < B1) W[s * B1 + lane] = pf[q];
+      if (lane == 0) ps[s] = fabs(pf[q]);
+      pf[q] = column(k + B1 + PF);
+      s = s + 1 == B1 ? 0 : s + 1;
+      __syncwarp();
+    }
+  }
+  if (lane == 0) {
+    long long* o = inertia + bi * bb.sparts;
+    o[0] = npos;
+    o[1] = nneg;
+    o[2] = nzero;
+  }
+}
+
+// forward, diagonal and backward substitution with the factor of factor_warp_k
+// (solve_k mode 0's arithmetic): the forward window z[c+j] and the backward
+// window x[c+j] sit one entry per lane
+template <int B1, int PF>
+__global__ void __launch_bounds__(128) solve_warp_k(const BandSeg* __restrict__ segs, const double* __restrict__ buf,
+                                                    const double* __restrict__ Dinv, double* __restrict__ work,
+                                                    BandBatch bb, int nb) {
+  const int lane = threadIdx.x & 31;
+  const int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (y >= nb) return;
+  const long long bi = bb.ids[y];
+  const BandSeg g = segs[0];
+  const long long n = g.n;
+  constexpr int b = B1 - 1;
+  const double* band = buf + bi * bb.sbuf + g.band;
+  const double* dinv = Dinv + bi * bb.sdim + g.pos;
+  double* v = work + bi * bb.swork + g.pos;
+  const bool col_lane = lane >= 1 && lane < B1;
+  auto lcol = [&](long long c) -> double {  // L(c + lane, c)
+    return (col_lane && c >= 0 && c + lane < n) ? band[c * B1 + lane] : 0.0;
+  };
+  // ---- forward: L z = rhs
+  double z = lane < B1 && lane < n ? v[lane] : 0.0;
+  double pl[PF], pv[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    pl[q] = lcol(q);
+    pv[q] = (lane == b && q + B1 < n) ? v[q + B1] : 0.0;
+  }
+  for (long long c0 = 0; c0 < n; c0 += PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const long long c = c0 + q;
+      if (c >= n) break;
+      const double yc = __shfl_sync(kFull, z, 0);
+      if (lane == 0) v[c] = yc;
+      z -= pl[q] * yc;
+      z = __shfl_down_sync(kFull, z, 1);
+      if (lane == b) z = pv[q];
+      pl[q] = lcol(c + PF);
+      pv[q] = (lane == b && c + PF + B1 < n) ? v[c + PF + B1] : 0.0;
+    }
+  }
+  // ---- backward: x_c = z_c * dinv_c - sum_j L(c+j, c) x_{c+j}
+  double xw = 0.0;  // lane j: x[c + j]
+  double pz[PF], pd[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    const long long c = n - 1 - q;
+    pl[q] = lcol(c);
+    pz[q] = c >= 0 ? v[c] : 0.0;
+    pd[q] = c >= 0 ? dinv[c] : 0.0;
+  }
+  for (long long c0 = n - 1; c0 >= 0; c0 -= PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const long long c = c0 - q;
+      if (c < 0) break;
+      double part = pl[q] * xw;
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+      const double xc = pz[q] * pd[q] - part;
+      if (lane == 0) v[c] = xc;
+      xw = __shfl_up_sync(kFull, xw, 1);
+      if (lane == 1) xw = xc;
+      const long long cn = c - PF;
+      pl[q] = lcol(cn);
+      pz[q] = cn >= 0 ? v[cn] : 0.0;
+      pd[q] = cn >= 0 ? dinv[cn] : 0.0;
+    }
+  }
+}
+
+using FactorWarpKernel = void (*)(const BandSeg*, double*, const double*, double*, long long*, BandBatch, int);
+using SolveWarpKernel = void (*)(const BandSeg*, const double*, const double*, double*, BandBatch, int);
+
+template <int B1>
+void warp_kernels(FactorWarpKernel& f, SolveWarpKernel& s) {
+  f = factor_warp_k<B1, 8>;
+  s = solve_warp_k<B1, 8>;
+}
+
+bool warp_kernels_for(int B1, FactorWarpKernel& f, SolveWarpKernel& s) {
+  switch (B1) {
+#define OCG_WK(a) \
+  case a:         \
+    warp_kernels<a>(f, s); \
+    return true;
+    OCG_WK(2) OCG_WK(3) OCG_WK(4) OCG_WK(5) OCG_WK(6) OCG_WK(7) OCG_WK(8) OCG_WK(9) OCG_WK(10) OCG_WK(11)
+    OCG_WK(12) OCG_WK(13) OCG_WK(14) OCG_WK(15) OCG_WK(16) OCG_WK(17) OCG_WK(18) OCG_WK(19) OCG_WK(20)
+    OCG_WK(21) OCG_WK(22) OCG_WK(23) OCG_WK(24) OCG_WK(25) OCG_WK(26) OCG_WK(27) OCG_WK(28) OCG_WK(29)
+    OCG_WK(30) OCG_WK(31) OCG_WK(32)
+#undef OCG_WK
+    default:
+      return false;
+  }
+}
+
 // unpartitioned bands of many small systems (batched solves): 128 threads per
 // system, several systems per SM
 FactorKernel factor_kernel_batch(int B1, int w, int we) {
@@ -595,7 +808,8 @@ FactorKernel factor_kernel_batch(int B1, int w, int we) {
 // segments of parity `par` add their Schur complements into the separator
 // system (disjoint separators within a parity); global-global entries skipped
 __global__ void schur_add_k(const BandSeg* __restrict__ segs, int nseg, int par, int wmax,
-                            const int64_t* __restrict__ border_pos, double* __restrict__ buf) {
+                            const int64_t* __restrict__ border_pos, double* __restrict__ buf, BandBatch bb) {
+  buf += batch_id(bb) * bb.sbuf;
   const BandSeg sep = segs[nseg];
   const long long n2 = sep.n;
   const int64_t per = static_cast<int64_t>(wmax) * wmax;
@@ -623,7 +837,8 @@ __global__ void schur_add_k(const BandSeg* __restrict__ segs, int nseg, int par,
 
 // global-global block: every segment contributes, summed in segment order
 __global__ void schur_global_k(const BandSeg* __restrict__ segs, int nseg, int wmax, int b, int wg,
-                               double* __restrict__ buf) {
+                               double* __restrict__ buf, BandBatch bb) {
+  buf += batch_id(bb) * bb.sbuf;
   const BandSeg sep = segs[nseg];
   GRID_LOOP(q, static_cast<int64_t>(wg) * wg) {
     const int u = static_cast<int>(q / wg), v = static_cast<int>(q % wg);
@@ -634,8 +849,14 @@ __global__ void schur_global_k(const BandSeg* __restrict__ segs, int nseg, int w
   }
 }
 
-__global__ void inertia_sum_k(const long long* __restrict__ parts, int nblocks, long long* __restrict__ out) {
+__global__ void inertia_sum_k(const long long* __restrict__ parts, int nblocks, long long* __restrict__ out,
+                              BandBatch bb) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (bb.ids) {
+    const long long bi = bb.ids[blockIdx.y];
+    parts += bi * bb.sparts;
+    out += bi * 3;
+  }
   long long a = 0, c = 0, z = 0;
   for (int i = 0; i < nblocks; ++i) {
     a += parts[3 * i];
@@ -678,6 +899,7 @@ __global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, 
     buf += bi * bb.sbuf;
     Dinv += bi * bb.sdim;
     work += bi * bb.swork;
+    gparts += bi * bb.swork;
   }
   const BandSeg g = segs[blk];
   const int lane = threadIdx.x;
@@ -792,7 +1014,12 @@ __global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, 
 
 // segment forward contributions into the separator system's right-hand side
 __global__ void rhs_add_k(int nseg, int par, int wmax, long long n2, const int64_t* __restrict__ border_pos,
-                          const double* __restrict__ gparts, double* __restrict__ sepv) {
+                          const double* __restrict__ gparts, double* __restrict__ sepv, BandBatch bb) {
+  {
+    const long long bi = batch_id(bb);
+    gparts += bi * bb.swork;
+    sepv += bi * bb.swork;
+  }
   const int64_t cnt = static_cast<int64_t>((nseg - par + 1) / 2) * wmax;
   GRID_LOOP(q, cnt) {
     const int i = par + 2 * static_cast<int>(q / wmax), t = static_cast<int>(q % wmax);
@@ -802,7 +1029,12 @@ __global__ void rhs_add_k(int nseg, int par, int wmax, long long n2, const int64
   }
 }
 __global__ void rhs_global_k(int nseg, int wmax, int b, int wg, long long n2, const double* __restrict__ gparts,
-                             double* __restrict__ sepv) {
+                             double* __restrict__ sepv, BandBatch bb) {
+  {
+    const long long bi = batch_id(bb);
+    gparts += bi * bb.swork;
+    sepv += bi * bb.swork;
+  }
   GRID_LOOP(u, wg) {
     double acc = 0.0;
     for (int i = 0; i < nseg; ++i) acc += gparts[static_cast<int64_t>(i) * wmax + b + u];
@@ -992,8 +1224,9 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   if (P.nseg > 1) {
     const int64_t per = static_cast<int64_t>(P.wmax) * P.wmax;
     for (int par = 0; par < 2; ++par)
-      schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf);
-    if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf);
+      schur_add_k<<<grid_for(((P.nseg + 1) / 2) * per), 256, 0, s>>>(D.segs, P.nseg, par, P.wmax, D.border_pos, buf,
+                                                                        BandBatch{});
+    if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf, BandBatch{});
     if (timing) cudaEventRecord(ev[2], s);
     fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
@@ -1010,7 +1243,7 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   }
   if (timing)
     for (auto& e : ev) cudaEventDestroy(e);
-  inertia_sum_k<<<1, 32, 0, s>>>(inertia_parts, blocks, inertia);
+  inertia_sum_k<<<1, 32, 0, s>>>(inertia_parts, blocks, inertia, BandBatch{});
 }
 
 void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
@@ -1028,8 +1261,9 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
     solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
     for (int par = 0; par < 2; ++par)
       rhs_add_k<<<grid_for(((P.nseg + 1) / 2) * P.wmax), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos,
-                                                                        gparts, work + sep.pos);
-    if (P.wg > 0) rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos);
+                                                                        gparts, work + sep.pos, BandBatch{});
+    if (P.wg > 0)
+      rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos, BandBatch{});
     solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
     solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
   }
@@ -1037,23 +1271,54 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
 }
 
 void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, double* buf, double* Dinv,
-                       long long* inertia, const int* ids, int nb, const double* dws, const double* dcs,
-                       cudaStream_t s) {
-  if (P.nseg != 1) throw std::runtime_error("band_factor_batch: the batched plan must be unpartitioned");
+                       long long* inertia, long long* parts, const int* ids, int nb, const double* dws,
+                       const double* dcs, cudaStream_t s) {
   if (nb <= 0) return;
   BandBatch bb;
   bb.ids = ids;
   bb.sbuf = P.buf_len;
   bb.sdim = P.dim;
-  bb.swork = P.dim + P.wmax;
+  bb.swork = P.dim + static_cast<long long>(P.nseg) * P.wmax;
   bb.sparts = 3;
   bb.dw = dws;
   bb.dc = dcs;
+  if (P.nseg > 1) {
+    // every system's segments in one launch (grid segments x systems), the
+    // Schur complements, then every system's separator system
+    const unsigned ny = static_cast<unsigned>(nb);
+    zero_k<<<dim3(std::max(1, std::min(grid_for(P.buf_len), 16)), ny), 256, 0, s>>>(buf, P.buf_len, bb);
+    if (P.nnz > 0)
+      scatter_k<<<dim3(std::max(1, std::min(grid_for(P.nnz), 16)), ny), 256, 0, s>>>(kval, D.dst, P.nnz, buf, bb);
+    const BandSeg& s0 = P.segs[0];
+    const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, false);
+    const FactorKernel fsep = factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true);
+    if (P.smem_factor > 48 * 1024)
+      for (FactorKernel f : {fseg, fsep})
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(P.smem_factor));
+    BandBatch pb = bb;
+    pb.sparts = 3 * (P.nseg + 1);
+    fseg<<<dim3(P.nseg, ny), kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
+    const int64_t per = static_cast<int64_t>(P.wmax) * P.wmax;
+    for (int par = 0; par < 2; ++par)
+      schur_add_k<<<dim3(std::max(1, std::min(grid_for(((P.nseg + 1) / 2) * per), 8)), ny), 256, 0, s>>>(
+          D.segs, P.nseg, par, P.wmax, D.border_pos, buf, pb);
+    if (P.wg > 0) schur_global_k<<<dim3(1, ny), 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf, pb);
+    fsep<<<dim3(1, ny), 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
+    inertia_sum_k<<<dim3(1, ny), 32, 0, s>>>(parts, P.nseg + 1, inertia, pb);
+    return;
+  }
   const unsigned ny = static_cast<unsigned>(nb);
   const int gz = std::max(1, std::min(grid_for(P.buf_len), 8));
   zero_k<<<dim3(gz, ny), 256, 0, s>>>(buf, P.buf_len, bb);
   if (P.nnz > 0) scatter_k<<<dim3(std::max(1, std::min(grid_for(P.nnz), 8)), ny), 256, 0, s>>>(kval, D.dst, P.nnz, buf, bb);
   const BandSeg& s0 = P.segs[0];
+  FactorWarpKernel fw = nullptr;
+  SolveWarpKernel sw = nullptr;
+  if (s0.w == 0 && !std::getenv("OCG_BATCH_BLOCK_LDL") && warp_kernels_for(s0.b + 1, fw, sw)) {
+    fw<<<(nb + 3) / 4, 128, 0, s>>>(D.segs, buf, D.primal, Dinv, inertia, bb, nb);
+    return;
+  }
   const FactorKernel f = factor_kernel_batch(s0.b + 1, s0.w, s0.w_early);
   if (P.smem_factor > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1063,21 +1328,46 @@ void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, 
 
 void band_solve_batch(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
                       double* x, double* work, const int* ids, int nb, cudaStream_t s) {
-  if (P.nseg != 1) throw std::runtime_error("band_solve_batch: the batched plan must be unpartitioned");
   if (nb <= 0) return;
   BandBatch bb;
   bb.ids = ids;
   bb.sbuf = P.buf_len;
   bb.sdim = P.dim;
-  bb.swork = P.dim + P.wmax;
+  bb.swork = P.dim + static_cast<long long>(P.nseg) * P.wmax;
   const unsigned ny = static_cast<unsigned>(nb);
+  if (P.nseg > 1) {
+    if (P.smem_solve > 48 * 1024)
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(P.smem_solve));
+    const int gd = std::max(1, std::min(grid_for(P.dim), 8));
+    const BandSeg& sep = P.segs.back();
+    double* gparts = work + P.dim;
+    gather_k<<<dim3(gd, ny), 256, 0, s>>>(rhs, D.perm, P.dim, work, bb);
+    solve_k<<<dim3(P.nseg, ny), 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos,
+                                                       sep.pos, bb);
+    for (int par = 0; par < 2; ++par)
+      rhs_add_k<<<dim3(1, ny), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos, gparts, work + sep.pos, bb);
+    if (P.wg > 0) rhs_global_k<<<dim3(1, ny), 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos, bb);
+    solve_k<<<dim3(1, ny), 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos,
+                                                 sep.pos, bb);
+    solve_k<<<dim3(P.nseg, ny), 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos,
+                                                       sep.pos, bb);
+    scatter_back_k<<<dim3(gd, ny), 256, 0, s>>>(work, D.perm, P.dim, x, bb);
+    return;
+  }
   const int gd = std::max(1, std::min(grid_for(P.dim), 8));
   if (P.smem_solve > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(P.smem_solve));
   gather_k<<<dim3(gd, ny), 256, 0, s>>>(rhs, D.perm, P.dim, work, bb);
-  solve_k<<<dim3(1, ny), 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, work + P.dim, P.wmax, D.border_pos, 0,
-                                               bb);
+  const BandSeg& s0 = P.segs[0];
+  FactorWarpKernel fw = nullptr;
+  SolveWarpKernel sw = nullptr;
+  if (s0.w == 0 && !std::getenv("OCG_BATCH_BLOCK_LDL") && warp_kernels_for(s0.b + 1, fw, sw))
+    sw<<<(nb + 3) / 4, 128, 0, s>>>(D.segs, buf, Dinv, work, bb, nb);
+  else
+    solve_k<<<dim3(1, ny), 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, work + P.dim, P.wmax, D.border_pos,
+                                                 0, bb);
   scatter_back_k<<<dim3(gd, ny), 256, 0, s>>>(work, D.perm, P.dim, x, bb);
 }
 

@@ -120,12 +120,15 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
 void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
                 double* x, double* work, cudaStream_t s);
 
-// Batched factor / solve of the systems ids[0..nb) (unpartitioned plans only):
-// kval [system][nnz] -> buf [system][buf_len], Dinv [system][dim], inertia
-// [system][3] = (pos, neg, zero); rhs, x [system][dim], work [system][dim + wmax].
+// Batched factor / solve of the systems ids[0..nb): kval [system][nnz] -> buf
+// [system][buf_len], Dinv [system][dim], inertia [system][3] = (pos, neg,
+// zero), parts [system][3 (nseg + 1)] scratch; rhs, x [system][dim], work
+// [system][dim + nseg * wmax]. Unpartitioned bands without a border and
+// b + 1 <= 32 run one warp per system; partitioned plans run segments x
+// systems in one launch.
 void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, double* buf, double* Dinv,
-                       long long* inertia, const int* ids, int nb, const double* dws, const double* dcs,
-                       cudaStream_t s);
+                       long long* inertia, long long* parts, const int* ids, int nb, const double* dws,
+                       const double* dcs, cudaStream_t s);
 void band_solve_batch(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,
                       double* x, double* work, const int* ids, int nb, cudaStream_t s);
 

@@ -180,8 +180,11 @@ class Batch {
     auto t1 = std::chrono::steady_clock::now();
     if (ocg_kkt_create(m, ev_, &kkt_) != OCG_OK) throw std::runtime_error(ocg_last_error());
     auto t2 = std::chrono::steady_clock::now();
-    // one unpartitioned band per instance: the batch supplies the parallelism
-    if (ocg::hd::ldl_create(kkt_, 1, &ldl_) != OCG_OK) throw std::runtime_error(ocg_last_error());
+    // a few time segments per instance: short sequential chains per factor /
+    // solve, the batch supplying the rest of the parallelism (OCG_BATCH_SEGMENTS)
+    int target = 1;
+    if (const char* e = std::getenv("OCG_BATCH_SEGMENTS")) target = std::max(1, std::atoi(e));
+    if (ocg::hd::ldl_create(kkt_, target, &ldl_) != OCG_OK) throw std::runtime_error(ocg_last_error());
     auto t3 = std::chrono::steady_clock::now();
     plan_eval_ = std::chrono::duration<double>(t1 - t0).count();
     plan_kkt_ = std::chrono::duration<double>(t2 - t1).count();
@@ -232,7 +235,7 @@ class Batch {
       st_, lambda_, g_, gt_, gsoc_, zl_, zu_, sigma_, jtlam_, dzl_, dzu_, lb_, ub_, rhs_, rhs2_, step_, step2_, kx_,
       rv_, dx_, jac_, hess_, objv_, partials_, kval_, band_, dinv_, work_, objs_, objw_, tmpf_;
   DBuf<int8_t> hl_, hu_;
-  DBuf<long long> inertia_;
+  DBuf<long long> inertia_, parts_;
   // per-kind staging
   DBuf<int> ids_[NOPS];
   DBuf<double> args_[NOPS], res_[NOPS];
@@ -362,13 +365,14 @@ void Batch::alloc_all() {
   A(partials_, D_.n_chunks);
   A(kval_, D_.knnz);
   A(band_, ldl_->plan.buf_len);
-  A(work_, D_.dim + ldl_->plan.wmax);
+  A(work_, D_.dim + static_cast<int64_t>(ldl_->plan.nseg) * ldl_->plan.wmax);
   A(objs_, 1);
   A(objw_, D_.n_obj);
   A(tmpf_, kRes);
   A(hl_, D_.ntot);
   A(hu_, D_.ntot);
   A(inertia_, 3);
+  A(parts_, 3 * (ldl_->plan.nseg + 1));
   A(flag_, 1);
   for (int k = 0; k < NOPS; ++k) {
     A(ids_[k], 1);
@@ -397,7 +401,7 @@ void Batch::alloc_all() {
                           &partials_, &kval_, &band_, &dinv_, &work_, &objs_, &objw_, &tmpf_})
     v->owned = false;
   hl_.owned = hu_.owned = false;
-  inertia_.owned = false;
+  inertia_.owned = parts_.owned = false;
   flag_.owned = false;
   for (int k = 0; k < NOPS; ++k) ids_[k].owned = args_[k].owned = res_[k].owned = false;
   ck(cudaMemsetAsync(flag_.p, 0, B * sizeof(int), s_), "memset");
@@ -455,74 +459,70 @@ void Batch::setup(const double* lvar, const double* uvar, const double* x0, cons
       ocg_free(js);
     }
   }
-  // host: every instance's folded bounds (Reduction, eval.cpp:290-316)
-  std::vector<double> hxlo(B * nv), hxhi(B * nv), hx0(B * nv), hlc(B * mc), huc(B * mc);
-  std::vector<char> contra(B, 0), bad(B, 0);
-  auto work = [&](size_t b0, size_t b1) {
-    for (size_t b = b0; b < b1; ++b) {
-      auto pick = [&](const double* p, const std::vector<double>& def, size_t n, double* dst) {
-        if (p)
-          std::memcpy(dst, p + b * n, n * sizeof(double));
-        else
-          std::memcpy(dst, def.data(), n * sizeof(double));
-      };
-      double* xl = hxlo.data() + b * nv;
-      double* xh = hxhi.data() + b * nv;
-      pick(lvar, mlv, nv, xl);
-      pick(uvar, muv, nv, xh);
-      pick(x0, mx0, nv, hx0.data() + b * nv);
-      pick(lcon, mlc, mc, hlc.data() + b * mc);
-      pick(ucon, muc, mc, huc.data() + b * mc);
-      const double* lc = hlc.data() + b * mc;
-      const double* uc = huc.data() + b * mc;
-      for (size_t r = 0; r < mc; ++r) {
-        if (rslot[r] < 0) continue;
-        const auto sl = static_cast<size_t>(rslot[r]);
-        xl[sl] = std::max(xl[sl], lc[r]);
-        xh[sl] = std::min(xh[sl], uc[r]);
-        if (xl[sl] > xh[sl]) contra[b] = 1;
-      }
-      for (size_t sl = 0; sl < nv; ++sl)
-        if ((prim[sl] < 0) != (xl[sl] == xh[sl])) bad[b] = 1;
+  // every instance's data on the device (the model's own, uploaded once and
+  // broadcast, where the caller passes NULL), then the Reduction's folded
+  // bounds (eval.cpp:290-316) per instance
+  auto put = [&](DBuf<double>& d, const double* p, const std::vector<double>& def, size_t n) {
+    if (p) {
+      ck(cudaMemcpyAsync(d.p, p, B * n * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
+    } else {
+      ck(cudaMemcpyAsync(d.p, def.data(), n * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
+      bd::broadcast_rows(d.p, static_cast<int64_t>(n), nb_, s_);
     }
   };
+  put(xlo_, lvar, mlv, nv);
+  put(xhi_, uvar, muv, nv);
+  put(x0_, x0, mx0, nv);
+  put(lcon_, lcon, mlc, mc);
+  put(ucon_, ucon, muc, mc);
+  std::vector<int64_t> fptr(nv + 1, 0), frow;
+  for (size_t r = 0; r < mc; ++r)
+    if (rslot[r] >= 0) ++fptr[static_cast<size_t>(rslot[r]) + 1];
+  for (size_t sl = 0; sl < nv; ++sl) fptr[sl + 1] += fptr[sl];
+  frow.resize(static_cast<size_t>(fptr[nv]));
   {
-    const size_t nt = std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<size_t>(1, B / 64));
-    std::vector<std::thread> th;
-    for (size_t t = 0; t < nt; ++t) th.emplace_back(work, B * t / nt, B * (t + 1) / nt);
-    for (auto& t : th) t.join();
+    std::vector<int64_t> fill(fptr.begin(), fptr.end() - 1);
+    for (size_t r = 0; r < mc; ++r)  // rows in index order per slot, like the host loop
+      if (rslot[r] >= 0) frow[static_cast<size_t>(fill[static_cast<size_t>(rslot[r])]++)] = static_cast<int64_t>(r);
   }
+  DBuf<int64_t> dfptr, dfrow;
+  dfptr.upload(fptr);
+  dfrow.upload(frow.empty() ? std::vector<int64_t>{0} : frow);
+  DBuf<int> dflags;
+  dflags.alloc(2 * B);
+  ck(cudaMemsetAsync(dflags.p, 0, 2 * B * sizeof(int), s_), "memset");
+  std::vector<int> all(B);
+  for (size_t b = 0; b < B; ++b) all[b] = static_cast<int>(b);
+  ck(cudaMemcpyAsync(ids_[0].p, all.data(), B * sizeof(int), cudaMemcpyHostToDevice, s_), "ids");
+  bd::fold_bounds(D_, dfptr.p, dfrow.p, prim_index_.p, xlo_.p, xhi_.p, lcon_.p, ucon_.p, dflags.p, dflags.p + B,
+                  bd::BL{ids_[0].p, nb_, s_});
+  std::vector<int> flags(2 * B);
+  ck(cudaMemcpyAsync(flags.data(), dflags.p, 2 * B * sizeof(int), cudaMemcpyDeviceToHost, s_), "D2H");
+  ck(cudaStreamSynchronize(s_), "fold sync");
   for (size_t b = 0; b < B; ++b)
-    if (bad[b])
+    if (flags[B + b])
       throw std::runtime_error("instance " + std::to_string(b) +
                                ": its bounds change which slots are fixed (the KKT structure differs)");
-  auto up = [&](DBuf<double>& d, const std::vector<double>& h) {
-    ck(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
-  };
-  up(xlo_, hxlo);
-  up(xhi_, hxhi);
-  up(x0_, hx0);
-  up(lcon_, hlc);
-  up(ucon_, huc);
 
   insts_.resize(B);
-  std::vector<int> all(B);
   for (size_t b = 0; b < B; ++b) {
-    all[b] = static_cast<int>(b);
     insts_[b].id = static_cast<int>(b);
-    insts_[b].contradictory = contra[b] != 0;
+    insts_[b].contradictory = flags[b] != 0;
   }
-  ck(cudaMemcpyAsync(ids_[0].p, all.data(), B * sizeof(int), cudaMemcpyHostToDevice, s_), "ids");
   const bd::BL L{ids_[0].p, nb_, s_};
 
   // EvalContext::compute_scaling at x_start (solver.cpp:318): unit-scale
   // gradient and Jacobian, then the reference's max rules
   {
-    std::vector<double> ones(B * mc, 1.0), w(B * static_cast<size_t>(D_.n_obj));
-    for (size_t b = 0; b < B; ++b)
-      for (int q = 0; q < D_.n_obj; ++q) w[b * static_cast<size_t>(D_.n_obj) + static_cast<size_t>(q)] = ev_->obj_weight[static_cast<size_t>(q)];
-    up(rs_, ones);
-    up(objw_, w);
+    std::vector<double> ones(mc, 1.0);
+    ck(cudaMemcpyAsync(rs_.p, ones.data(), mc * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
+    bd::broadcast_rows(rs_.p, static_cast<int64_t>(mc), nb_, s_);
+    if (D_.n_obj > 0) {
+      ck(cudaMemcpyAsync(objw_.p, ev_->obj_weight.data(), static_cast<size_t>(D_.n_obj) * sizeof(double),
+                         cudaMemcpyHostToDevice, s_),
+         "H2D");
+      bd::broadcast_rows(objw_.p, D_.n_obj, nb_, s_);
+    }
     const double* xp = x0_.p;
     const double* ow = objw_.p;
     double* gc = gcoo_.p;
@@ -613,7 +613,8 @@ void Batch::execute(int kind, int nb, cudaStream_t st) {
       break;
     }
     case FACTOR:
-      ocg::dev::band_factor_batch(P, ldl_->dev, kval_.p, band_.p, dinv_.p, inertia_.p, L.ids, nb, a0, a1, st);
+      ocg::dev::band_factor_batch(P, ldl_->dev, kval_.p, band_.p, dinv_.p, inertia_.p, parts_.p, L.ids, nb, a0, a1,
+                                  st);
       bd::take_i64x3(inertia_.p, R, kRes, L);
       break;
     case SOLVE_0:

@@ -286,6 +286,39 @@ __global__ void __launch_bounds__(256) jt_lambda_k(BDims D, const double* __rest
 
 // ---- setup ----------------------------------------------------------------------
 
+__global__ void broadcast_rows_k(double* __restrict__ a, int64_t n, int nb) {
+  const int64_t total = n * (nb - 1);
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    a[n + q] = a[q % n];
+}
+
+// ipm.cpp setup(): xlo = max(lvar, lcon rows), xhi = min(uvar, ucon rows) per
+// folded slot (std::max / std::min expressions, rows in index order)
+__global__ void fold_bounds_k(BDims D, const int64_t* __restrict__ fptr, const int64_t* __restrict__ frow,
+                              const int64_t* __restrict__ prim_index, double* __restrict__ xlo,
+                              double* __restrict__ xhi, const double* __restrict__ lcon,
+                              const double* __restrict__ ucon, int* __restrict__ contra, int* __restrict__ bad,
+                              const int* __restrict__ ids) {
+  const int64_t b = inst(ids);
+  xlo += b * D.nvar;
+  xhi += b * D.nvar;
+  lcon += b * D.m_con;
+  ucon += b * D.m_con;
+  ELOOP(sl, D.nvar) {
+    double lo = xlo[sl], hi = xhi[sl];
+    for (int64_t p = fptr[sl]; p < fptr[sl + 1]; ++p) {
+      const int64_t r = frow[p];
+      lo = lo < lcon[r] ? lcon[r] : lo;
+      hi = ucon[r] < hi ? ucon[r] : hi;
+    }
+    xlo[sl] = lo;
+    xhi[sl] = hi;
+    if (lo > hi) atomicOr(contra + b, 1);
+    if ((prim_index[sl] < 0) != (lo == hi)) atomicOr(bad + b, 1);
+  }
+}
+
 // Solver::setup_bounds (solver.cpp:125-170) as ipm.cpp's setup() computes it
 __global__ void setup_bounds_k(BDims D, BMaps M, const double* __restrict__ xlo, const double* __restrict__ xhi,
                                const double* __restrict__ lcon, const double* __restrict__ ucon,
@@ -824,6 +857,17 @@ void jt_lambda(const BDims& D, const double* jac, const double* lam, const int64
                const int64_t* dual_idx, const int64_t* slack_dual, double* out, const BL& L) {
   if (L.nb <= 0 || D.ntot <= 0) return;
   jt_lambda_k<<<grid2(D.ntot, L.nb), kT, 0, L.s>>>(D, jac, lam, ptr, e_idx, dual_idx, slack_dual, out, L.ids);
+}
+
+void broadcast_rows(double* a, int64_t n, int nb, cudaStream_t s) {
+  if (nb <= 1 || n <= 0) return;
+  broadcast_rows_k<<<2 * 148 * 4, 256, 0, s>>>(a, n, nb);
+}
+void fold_bounds(const BDims& D, const int64_t* fptr, const int64_t* frow, const int64_t* prim_index, double* xlo,
+                 double* xhi, const double* lcon, const double* ucon, int* contra, int* bad, const BL& L) {
+  if (L.nb <= 0) return;
+  fold_bounds_k<<<grid2(D.nvar, L.nb), kT, 0, L.s>>>(D, fptr, frow, prim_index, xlo, xhi, lcon, ucon, contra, bad,
+                                                    L.ids);
 }
 
 void setup_bounds(const BDims& D, const BMaps& M, const double* xlo, const double* xhi, const double* lcon,

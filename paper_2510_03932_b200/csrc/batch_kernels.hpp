@@ -81,6 +81,14 @@ void jt_lambda(const BDims& D, const double* jac, const double* lam, const int64
                const int64_t* dual_idx, const int64_t* slack_dual, double* out, const BL& L);
 
 // ---- setup (Solver::setup_bounds / initialize_iterate, solver.cpp:125-206) ----
+// rows 1..nb-1 of a [nb][n] array <- row 0 (instances sharing the model's data)
+void broadcast_rows(double* a, int64_t n, int nb, cudaStream_t s);
+// Reduction's folded bounds (eval.cpp:290-316) in place on xlo / xhi (holding
+// lvar / uvar): slot sl takes the rows frow[fptr[sl]..fptr[sl+1]); contra[inst]
+// = 1 if some slot ends with lo > hi, bad[inst] = 1 if the fixed slots differ
+// from the structure's (prim_index < 0 <=> lo == hi)
+void fold_bounds(const BDims& D, const int64_t* fptr, const int64_t* frow, const int64_t* prim_index, double* xlo,
+                 double* xhi, const double* lcon, const double* ucon, int* contra, int* bad, const BL& L);
 void setup_bounds(const BDims& D, const BMaps& M, const double* xlo, const double* xhi, const double* lcon,
                   const double* ucon, const double* row_scale, double relax, double* lb, double* ub, int8_t* has_lb,
                   int8_t* has_ub, double* lcon_s, const BL& L);
