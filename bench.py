@@ -55,6 +55,9 @@ def parse():
                     help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
     ap.add_argument("--solve", default="quadrotor:100000",
                     help="model:N of the full IPM solve leg ('ipm_solve' key; 'none' to skip)")
+    ap.add_argument("--batch", default="4096:500",
+                    help="instances:N of the batched cart-pendulum solve leg (BASELINE config 5, 'batch_solve' "
+                         "key; 'none' to skip)")
     return ap.parse_args()
 
 
@@ -455,6 +458,8 @@ def run_ours(args) -> None:
             out["extra"] = secondary(dev, stream, flush, sink, peak)
         if args.solve != "none" and world == 1:
             out["ipm_solve"] = ipm_solve_leg(args.solve, not args.no_cpu_baseline)
+        if args.batch != "none" and world == 1:
+            out["batch_solve"] = batch_solve_leg(args.batch, not args.no_cpu_baseline)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -499,6 +504,57 @@ def ipm_solve_leg(spec: str, with_reference: bool) -> dict:
         out["iterations_match"] = int(r["iterations"]) == d2["iterations"]
         out["objective_rel_diff"] = abs(r["objective"] - d2["objective"]) / max(abs(r["objective"]), 1e-300)
         out["speedup_vs_reference"] = out["reference"]["wall_s"] / t_second
+    return out
+
+
+def batch_solve_leg(spec: str, with_reference: bool, ref_sample: int = 64) -> dict:
+    """BASELINE config 5: cart-pendulum instances b = 0..B-1 at N (terminal
+    target p(2) = 1 + b/4096) solved by ocg_ipm_batch_solve — every instance
+    the reference's IPM decisions, every device step one launch over all
+    instances — against the reference ipm::solve run one instance per host
+    core (Backend::serial each, all cores busy) on an evenly spaced sample.
+    Instance data (their terminal-target rows) and the reference models are
+    prepared outside both timed regions."""
+    from paper_2510_03932_b200 import Model, solve_batch
+    from paper_2510_03932_b200.models import cart_pendulum_instance
+    B, N = (int(v) for v in spec.split(":"))
+    base = Model(cart_pendulum_instance(0, 4096), N)
+    insts = [Model(cart_pendulum_instance(b, 4096), N) for b in range(B)]
+    arrs = [m.arrays() for m in insts]
+    lcon = np.ascontiguousarray(np.stack([r["lcon"] for r in arrs]))
+    ucon = np.ascontiguousarray(np.stack([r["ucon"] for r in arrs]))
+    solve_batch(base, insts[:2])  # kernels into the compile cache
+    t0 = time.perf_counter()
+    res = solve_batch(base, lcon=lcon, ucon=ucon)
+    wall = time.perf_counter() - t0
+    out = {"model": "cart_pendulum", "N": N, "instances": B, "wall_s": wall, "instances_per_s": B / wall,
+           "optimal": sum(1 for r in res if r["status"] == 0),
+           "mean_iterations": float(np.mean([r["iterations"] for r in res])),
+           "launch_rounds": res[0]["rounds"], "launch_groups": res[0]["launch_groups"],
+           "batch_setup_s": res[0]["time_setup"],
+           "plan_s": res[0]["time_plan_eval"] + res[0]["time_plan_kkt"] + res[0]["time_plan_ldl"]}
+    if with_reference:
+        from concurrent.futures import ThreadPoolExecutor
+        RefEval, RefModel = _ref_modules()
+        cores = os.cpu_count() or 1
+        sample = list(range(0, B, max(1, B // ref_sample)))[:ref_sample]
+        models = {b: RefModel(cart_pendulum_instance(b, 4096), N) for b in sample}
+
+        def one(b):
+            r = models[b].solve(parallel=False)
+            return b, int(r["status"]), int(r["iterations"]), r["objective"]
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:  # one solve per core (the harness releases the GIL)
+            refs = list(ex.map(one, sample))
+        rwall = time.perf_counter() - t0
+        match = sum(1 for b, st, it, obj in refs
+                    if st == res[b]["status"] and it == res[b]["iterations"]
+                    and abs(obj - res[b]["objective"]) <= 1e-8 * abs(obj))
+        out["reference"] = {"sample": len(sample), "cores": cores, "wall_s": rwall,
+                            "instances_per_s": len(sample) / rwall}
+        out["parity"] = {"compared": len(refs), "status_iterations_objective_match": match}
+        out["speedup_vs_reference"] = out["instances_per_s"] / out["reference"]["instances_per_s"]
     return out
 
 
