@@ -56,6 +56,7 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   // flat node-major order: band part, then the global border
   // stable counting sort by node (border indices, node -1, last)
   std::vector<int64_t> flat(static_cast<size_t>(dim));
+  std::vector<int64_t> node_start;
   {
     int64_t max_node = -1;
     for (int64_t i = 0; i < dim; ++i) max_node = std::max(max_node, node[static_cast<size_t>(i)]);
@@ -66,6 +67,7 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     };
     for (int64_t i = 0; i < dim; ++i) start[bucket(i) + 1]++;
     for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+    node_start.assign(start.begin(), start.begin() + (max_node + 1));  // flat position of each node's first index
     for (int64_t i = 0; i < dim; ++i) flat[static_cast<size_t>(start[bucket(i)]++)] = i;
   }
   std::vector<int64_t> fpos(static_cast<size_t>(dim));
@@ -97,12 +99,26 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   std::vector<int64_t> seg_lo(static_cast<size_t>(nseg)), seg_len(static_cast<size_t>(nseg));
   const int64_t interior = n - (nseg - 1) * b;
   {
+    // Every segment after the first starts at a time node's first index (its
+    // primal slots): the segment's first pivots are then primal blocks, not
+    // duals whose primal partners sit in the separator before them — those
+    // would be pivots of size ~delta_c and ruin the accuracy.
     int64_t f = 0;
     for (int64_t i = 0; i < nseg; ++i) {
-      seg_len[static_cast<size_t>(i)] = interior / nseg + (i < interior % nseg ? 1 : 0);
       seg_lo[static_cast<size_t>(i)] = f;
-      f += seg_len[static_cast<size_t>(i)] + (i + 1 < nseg ? b : 0);
+      f += interior / nseg + (i < interior % nseg ? 1 : 0) + (i + 1 < nseg ? b : 0);
     }
+    for (int64_t i = 1; i < nseg; ++i) {
+      auto it = std::lower_bound(node_start.begin(), node_start.end(), seg_lo[static_cast<size_t>(i)]);
+      if (it != node_start.end() && *it < n && *it - b > seg_lo[static_cast<size_t>(i) - 1]) seg_lo[static_cast<size_t>(i)] = *it;
+    }
+    for (int64_t i = 1; i < nseg; ++i)
+      if (seg_lo[static_cast<size_t>(i)] - b <= seg_lo[static_cast<size_t>(i) - 1] ||
+          seg_lo[static_cast<size_t>(i)] >= n)
+        throw std::runtime_error("band plan: degenerate time partition");
+    for (int64_t i = 0; i < nseg; ++i)
+      seg_len[static_cast<size_t>(i)] =
+          (i + 1 < nseg ? seg_lo[static_cast<size_t>(i) + 1] - b : n) - seg_lo[static_cast<size_t>(i)];
   }
   const int64_t n2 = (nseg - 1) * b;  // separator-system band columns
   const int wmax = nseg > 1 ? static_cast<int>(2 * b + wg) : static_cast<int>(wg);

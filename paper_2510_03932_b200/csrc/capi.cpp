@@ -495,6 +495,17 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     ck(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
     if (prop.major != 10) return fail(OCG_ERR_CUDA, "octgpu kernels target sm_100a; device is sm_" +
                                                         std::to_string(prop.major) + std::to_string(prop.minor));
+    {
+      // Plans allocate and free GBs through the stream-ordered pool; keep what
+      // is freed mapped (like a caching allocator) instead of returning it to
+      // the driver at every synchronization, so rebuilding a plan is not paid
+      // in page mappings.
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
     const ocg::Nlp& nlp = m->nlp;
     e->lay = ocg::make_layout(nlp);
     const Index lo = std::max(e->lay.idx_lo, o.idx_lo);
