@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <json.hpp>
 #include <memory>
 #include <random>
@@ -359,6 +360,8 @@ int ref_solve(void* model, int parallel, int workers, int max_iter, double tol, 
   ipm::IpmOptions opts;
   if (max_iter > 0) opts.max_iter = max_iter;
   if (tol > 0) opts.tol = tol;
+  opts.verbose = std::getenv("REF_VERBOSE") != nullptr;  // per-iteration trace (solver.cpp:623-628)
+  if (const char* d = std::getenv("REF_DUMP_KKT")) opts.dump_kkt = d;  // first assembled KKT, Matrix Market
   auto sol = ipm::solve(m->nlp, opts, be);
   if (octrans_accel_release_all) octrans_accel_release_all();
   out[0] = sol.objective;

@@ -35,7 +35,7 @@ size_t factor_smem(int b, int w) {
   const size_t B1 = static_cast<size_t>(b) + 1, W = static_cast<size_t>(w);
   constexpr size_t kPre = 32;
   const size_t pairs = static_cast<size_t>(b) * (b + 1) / 2;
-  return sizeof(double) * (B1 * B1 + B1 + W * B1 + W * W + W + 2 * B1 + 2 * W + kPre * (B1 + W + 1)) +
+  return sizeof(double) * (B1 * B1 + B1 + W * B1 + W * W + W + 2 * B1 + 2 * W + kPre * (B1 + W + 2)) +
          sizeof(short) * 2 * pairs + 64;
 }
 size_t solve_smem(int b, int w) {
@@ -177,6 +177,8 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     off += static_cast<int64_t>(ww) * nn;
     s.S = off;
     off += static_cast<int64_t>(ww) * ww;
+    s.ps0 = off;
+    off += nn + ww;
     s.pos = pos;
     s.bpos = bpos;
     P.segs.push_back(s);
@@ -375,13 +377,14 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
   double* yb = l + B1;            // w
   double* lb = yb + w;            // w
   double* ring = lb + w;          // kPrefetch * RW
-  const int RW = B1 + w + 1;      // ring row: band column, its border entries, its regularization flag
+  const int RW = B1 + w + 2;      // ring row: band column, its border entries, regularization flag, pivot-scale seed
   short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * RW);
   const int P = b * (b + 1) / 2;
   short* pj2 = pj1 + P;
   double* band = buf + g.band;
   double* border = buf + g.border;
   double* Sg = buf + g.S;
+  double* ps0 = buf + g.ps0;  // pivot-scale seeds: [n] interior, then [w] border
   const double* flag = primal + g.pos;
   double* dinvp = Dinv + g.pos;
 
@@ -406,14 +409,17 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     }
 #pragma unroll
     for (int t = tid; t < w; t += T) cp8(dstp + B1 + t, border + static_cast<long long>(t) * n + c);
-    if (tid == 0) cp8(dstp + B1 + w, flag + c);
+    if (tid == 0) {
+      cp8(dstp + B1 + w, flag + c);
+      cp8(dstp + B1 + w + 1, ps0 + c);
+    }
   };
   for (long long c = 0; c < B1 && c < n; ++c) {
     for (int j = tid; j < B1; j += T) {
       double v = c + j < n ? band[c * B1 + j] : 0.0;
       if (j == 0) {
         v += delta_of(flag[c]);
-        ps[c] = fabs(v);
+        ps[c] = fmax(fabs(v), ps0[c]);
       }
       W[c * B1 + j] = v;
     }
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     double v = Sg[q];
     if (t == u) {
       if (g.finalize) v += delta_of(primal[g.bpos + t]);
-      Sps[t] = fabs(v);
+      Sps[t] = fmax(fabs(v), ps0[n + t]);
     }
     S[q] = v;
   }
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
         double v = src[j];
         if (j == 0) {
           v += delta_of(src[B1 + w]);
-          ps[s] = fabs(v);
+          ps[s] = fmax(fabs(v), src[B1 + w + 1]);
         }
         W[s * B1 + j] = v;
       }
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     }
   } else {
     for (int q = tid; q < w * w; q += T) Sg[q] = S[q];  // Schur complement on the border rows
+    for (int t = tid; t < w; t += T) ps0[n + t] = Sps[t];   // and its diagonal's largest single update
   }
   if (tid == 0) {
     long long* o = inertia_parts + 3 * (seg0 + blockIdx.x);
@@ -848,6 +855,10 @@ __global__ void schur_add_k(const BandSeg* __restrict__ segs, int nseg, int par,
     else
       dst = sep.border + (R - n2) * n2 + C;
     buf[dst] += v;
+    if (t == u) {  // R == C < n2: a separator pivot; separators are disjoint within a parity
+      double& sc = buf[sep.ps0 + R];
+      sc = fmax(sc, buf[segs[i].ps0 + segs[i].n + t]);
+    }
   }
 }
 
@@ -859,9 +870,13 @@ __global__ void schur_global_k(const BandSeg* __restrict__ segs, int nseg, int w
   GRID_LOOP(q, static_cast<int64_t>(wg) * wg) {
     const int u = static_cast<int>(q / wg), v = static_cast<int>(q % wg);
     if (v > u) continue;
-    double acc = 0.0;
-    for (int i = 0; i < nseg; ++i) acc += buf[segs[i].S + static_cast<int64_t>(b + u) * wmax + (b + v)];
+    double acc = 0.0, sc = 0.0;
+    for (int i = 0; i < nseg; ++i) {
+      acc += buf[segs[i].S + static_cast<int64_t>(b + u) * wmax + (b + v)];
+      if (u == v) sc = fmax(sc, buf[segs[i].ps0 + segs[i].n + b + u]);
+    }
     buf[sep.S + static_cast<int64_t>(u) * sep.w + v] += acc;
+    if (u == v) buf[sep.ps0 + sep.n + u] = sc;
   }
 }
 
@@ -1269,21 +1284,40 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
   if (P.smem_solve > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(solve_k), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(P.smem_solve));
+  static const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  cudaEvent_t ev[5];
+  if (timing)
+    for (auto& e : ev) {
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+    }
   gather_k<<<grid_for(dim), 256, 0, s>>>(rhs, D.perm, dim, work, BandBatch{});
   if (P.nseg == 1) {
     solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, 0, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, 0, BandBatch{});
   } else {
     const BandSeg& sep = P.segs.back();
+    if (timing) cudaEventRecord(ev[1], s);
     solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    if (timing) cudaEventRecord(ev[2], s);
     for (int par = 0; par < 2; ++par)
       rhs_add_k<<<grid_for(((P.nseg + 1) / 2) * P.wmax), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos,
                                                                         gparts, work + sep.pos, BandBatch{});
     if (P.wg > 0)
       rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos, BandBatch{});
     solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    if (timing) cudaEventRecord(ev[3], s);
     solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
   }
   scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, D.perm, dim, x, BandBatch{});
+  if (timing) {
+    cudaEventRecord(ev[4], s);
+    cudaEventSynchronize(ev[4]);
+    float t[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    std::fprintf(stderr, "[band_solve] gather %.3f ms  segments forward %.3f ms  separator system %.3f ms  "
+                 "segments backward + scatter %.3f ms\n", t[0], t[1], t[2], t[3]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
 }
 
 void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, double* buf, double* Dinv,

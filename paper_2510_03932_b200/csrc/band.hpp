@@ -42,6 +42,11 @@ struct BandSeg {
   long long S = 0;       // w*w
   long long pos = 0;     // first position (Dinv / flags / vector index) of the interior columns
   long long bpos = -1;   // finalize: first position of the border rows
+  // n + w pivot-scale seeds (interior columns, then border rows): a block
+  // factored after others starts each pivot's scale at max(|a_kk + delta|,
+  // seed), the seed being the largest single update the earlier blocks
+  // applied to that diagonal. A segment leaves its border rows' scales here.
+  long long ps0 = 0;
 };
 
 struct BandPlan {

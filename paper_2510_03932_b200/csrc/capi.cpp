@@ -591,6 +591,11 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     for (size_t q = 0; q < gc.size(); ++q) idx[static_cast<size_t>(fill[static_cast<size_t>(gc[q])]++)] = static_cast<int32_t>(q);
     e->gg_ptr.upload(ptr);
     e->gg_idx.upload(idx);
+    {
+      const auto lr = ocg::dev::long_rows(ptr);
+      e->gg_long.upload(lr);
+      e->n_gg_long = static_cast<int64_t>(lr.size());
+    }
     ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
     lap("gradient gather");
     *out = e.release();
@@ -800,7 +805,8 @@ int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stre
   Index ns = e->n_spec("ocg_grad");
   void* args[] = {e->prm.data(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_grad, "ocg_grad", args, st(s));
-  ocg::dev::gather_sum(e->grad.p, e->gg_ptr.p, e->gg_idx.p, e->model->nlp.nvar, grad_dense, st(s));
+  ocg::dev::gather_sum(e->grad.p, e->gg_ptr.p, e->gg_idx.p, e->model->nlp.nvar, grad_dense,
+                       {e->gg_long.p, e->n_gg_long}, st(s));
   e->launches += 1;
   return OCG_OK;
   OCG_GUARD_END
@@ -977,6 +983,21 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     K->jt_e.adopt(bo.jt_e, 0);
     K->jt_dual.adopt(bo.jt_dual, 0);
   }
+  {
+    // long rows of the three gathers (a free final time's diagonal, J^T lambda entry, matvec row)
+    auto longs = [&](const DBuf<int64_t>& ptr, size_t n, DBuf<int64_t>& out, int64_t& count) {
+      std::vector<int64_t> h(n + 1);
+      ck(cudaMemcpyAsync(h.data(), ptr.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, cudaStreamPerThread),
+         "D2H ptr");
+      ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
+      const auto lr = ocg::dev::long_rows(h);
+      out.upload(lr);
+      count = static_cast<int64_t>(lr.size());
+    };
+    longs(K->src_ptr, static_cast<size_t>(K->nnz), K->src_long, K->n_src_long);
+    longs(K->mv_ptr, static_cast<size_t>(K->dim), K->mv_long, K->n_mv_long);
+    longs(K->jt_ptr, static_cast<size_t>(K->ntot), K->jt_long, K->n_jt_long);
+  }
   K->val.alloc(static_cast<size_t>(K->nnz));
   ck(cudaMemsetAsync(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double), cudaStreamPerThread), "memset");
   ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
@@ -1031,8 +1052,8 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
   if (!k || !sigma) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
-                         k->n_slack, k->ntot, k->val.p, st(s));
-  k->ev->launches += 1;
+                         k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s));
+  k->ev->launches += k->n_src_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }
@@ -1040,8 +1061,9 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
 int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
   if (!k || !x || !y) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
-  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y, st(s));
-  k->ev->launches += 1;
+  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y, {k->mv_long.p, k->n_mv_long},
+                       st(s));
+  k->ev->launches += k->n_mv_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }
@@ -1049,8 +1071,8 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
 int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
-  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out, st(s));
-  k->ev->launches += 1;
+  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out, {k->mv_long.p, k->n_mv_long}, st(s));
+  k->ev->launches += k->n_mv_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }
@@ -1059,8 +1081,8 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
   if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
-                      k->n_slack, out, st(s));
-  k->ev->launches += 1;
+                      k->n_slack, out, {k->jt_long.p, k->n_jt_long}, st(s));
+  k->ev->launches += k->n_jt_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }

@@ -123,6 +123,8 @@ struct ocg_eval {
   // dense gradient gather (slot -> grad COO entries)
   DBuf<int64_t> gg_ptr;
   DBuf<int32_t> gg_idx;
+  DBuf<int64_t> gg_long;  // slots with more than kLongRow gradient entries
+  int64_t n_gg_long = 0;
 
   int64_t launches = 0;
   std::map<std::string, int> min_blocks;  // register budget the kernels were compiled for
@@ -168,6 +170,9 @@ struct ocg_kkt {
   DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
   // J^T lambda
   DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
+  // rows of src_ptr / mv_ptr / jt_ptr longer than kLongRow (kernels.hpp)
+  DBuf<int64_t> src_long, mv_long, jt_long;
+  int64_t n_src_long = 0, n_mv_long = 0, n_jt_long = 0;
 };
 
 // Band LDL^T of the KKT matrix (band.hpp): plan + device buffers

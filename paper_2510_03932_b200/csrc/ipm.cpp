@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -139,6 +140,8 @@ class DeviceSolver {
   int64_t nvar_ = 0, mcon_ = 0, nfree_ = 0, nslack_ = 0, ntot_ = 0, m_ = 0, dim_ = 0;
   bool contradictory_ = false;
   double mu_ = 0.1, tau_ = 0.99, delta_last_ = 0.0, obj_scale_ = 1.0;
+  // OCG_TIMING diagnostics: solves, refinement rounds, line-search trials
+  long long n_solves_ = 0, n_refine_ = 0, n_trials_ = 0;
   double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
   double theta_min_ = 0.0, theta_max_ = kInf;
   std::vector<std::pair<double, double>> filter_;
@@ -465,6 +468,7 @@ void DeviceSolver::refine_if_needed(const double* rhs, double* step) {
     ocg::ipmdev::residual_norms(rhs, kx_.p, step, dim_, ntot_, dw_, dc_, r_v_.p, nr, sc_, s_);
     if (nr[0] <= 1e-12 * (anorm * nr[2] + nr[1])) break;
     cko(ocg_ldl_solve(ldl_, r_v_.p, dx_.p, s_), "ldl_solve");
+    ++n_refine_;
     ocg::ipmdev::add(step, dx_.p, dim_, s_);
   }
 }
@@ -502,6 +506,7 @@ bool DeviceSolver::solve_kkt(double wmax, bool& numeric_failure) {
   r_.time_factorize += tf.elapsed();
   Clock ts;
   cko(ocg_ldl_solve(ldl_, rhs_.p, step_.p, s_), "ldl_solve");
+  ++n_solves_;
   refine_if_needed(rhs_.p, step_.p);
   ckc(cudaStreamSynchronize(s_), "sync");
   r_.time_solve += ts.elapsed();
@@ -512,6 +517,7 @@ bool DeviceSolver::solve_kkt(double wmax, bool& numeric_failure) {
 void DeviceSolver::resolve(const double* rhs, double* step) {
   Clock ts;
   cko(ocg_ldl_solve(ldl_, rhs, step, s_), "ldl_solve");
+  ++n_solves_;
   refine_if_needed(rhs, step);
   ckc(cudaStreamSynchronize(s_), "sync");
   r_.time_solve += ts.elapsed();
@@ -584,6 +590,12 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     ocg_ldl_info(ldl_, li);
     r_.bandwidth = li[2];
     *res = r_;
+    if (std::getenv("OCG_TIMING"))
+      std::fprintf(stderr,
+                   "[ipm] %d iterations: total %.3f s, factorize %.3f s (%d), solve %.3f s (%lld solves + %lld "
+                   "refinement rounds), derivatives %.3f s, %lld line-search trials\n",
+                   iter, r_.time_total, r_.time_factorize, r_.factorizations, r_.time_solve, n_solves_, n_refine_,
+                   r_.time_derivatives, n_trials_);
   };
   if (!eval_cj(x_->p, c_->p) || !eval_grad(x_->p, grad_->p)) {
     done(3, 0);
@@ -651,6 +663,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
       ocg::ipmdev::trial(P_, x_->p, s_v_->p, d, a, xt_->p, st_->p, s_);
     };
     auto eval_trial = [&]() {
+      ++n_trials_;
       if (!eval_c(xt_->p, ct_->p)) return false;
       ocg::ipmdev::residual(P_, ct_->p, st_->p, gt_.p, s_);
       theta_t = theta_of(gt_.p);

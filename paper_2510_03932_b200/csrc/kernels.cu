@@ -3,6 +3,7 @@
 // mirrors. All of them are HBM-bound streaming/gather kernels; grids are
 // sized in multiples of the 148 SMs x resident blocks.
 #include <cstdint>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -14,6 +15,9 @@ constexpr int kChunk = 512;  // Backend::kChunkSize (backend.hpp:50)
 constexpr int kSms = 148;
 
 __device__ __forceinline__ bool finite(double v) { return fabs(v) <= 1.7976931348623157e308; }
+
+// rows longer than kLongRow go to the one-block-per-row kernels below
+__device__ __forceinline__ bool is_long(const int64_t* ptr, int64_t i) { return ptr[i + 1] - ptr[i] > kLongRow; }
 
 // One warp per 512-instance chunk: coalesced loads into shared memory, then
 // lane 0 adds in index order (the reference's `s += v` loop).
@@ -60,6 +64,7 @@ __global__ void __launch_bounds__(256) gather_sum_k(const double* __restrict__ s
                                                     double* __restrict__ out) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (is_long(ptr, i)) continue;
     double s = 0.0;
     for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) s += src[idx[p]];
     out[i] = s;
@@ -74,6 +79,7 @@ __global__ void __launch_bounds__(256) kkt_assemble_k(const double* __restrict__
   const int64_t HJ = H + J, HJS = H + J + S;
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (is_long(ptr, p)) continue;
     double s = 0.0;
     for (int64_t q = ptr[p]; q < ptr[p + 1]; ++q) {
       const int64_t c = code[q];
@@ -100,6 +106,7 @@ __global__ void __launch_bounds__(256) sym_matvec_k(const double* __restrict__ v
                                                     const double* __restrict__ x, double* __restrict__ y) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (is_long(rptr, i)) continue;
     double s = 0.0;
     for (int64_t p = rptr[i]; p < rptr[i + 1]; ++p) s += val[vidx[p]] * x[col[p]];
     y[i] = s;
@@ -113,6 +120,7 @@ __global__ void __launch_bounds__(256) sym_norm_inf_k(const double* __restrict__
   double m = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (is_long(rptr, i)) continue;
     double s = 0.0;
     for (int64_t p = rptr[i]; p < rptr[i + 1]; ++p) s += fabs(val[vidx[p]]);
     m = fmax(m, s);
@@ -135,6 +143,7 @@ __global__ void __launch_bounds__(256) jt_lambda_k(const double* __restrict__ ja
   const int64_t ntot = n_free + n_slack;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ntot;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (is_long(ptr, i)) continue;
     double s = 0.0;
     for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) s += jac[e_idx[p]] * lam[dual_idx[p]];
     if (i >= n_free) s -= lam[slack_dual[i - n_free]];
@@ -155,6 +164,107 @@ __global__ void __launch_bounds__(256) max_abs_k(const double* __restrict__ v, i
   if (threadIdx.x == 0) {
     for (int w = 1; w < 8; ++w) m = fmax(m, wm[w]);
     atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// ---- long rows ------------------------------------------------------------------
+// A row whose source list is longer than kLongRow (e.g. the free final time
+// tf of a free-horizon problem: its KKT diagonal gathers one Hessian entry per
+// time step, its J^T lambda entry one Jacobian entry per dynamics row) would
+// be one thread's serial chain of dependent gathers. The thread-per-row
+// kernels skip such rows; one block per long row keeps the reference's order
+// (increasing source index, one `s += term` accumulator): threads 32.. gather
+// the terms into shared memory, double-buffered, while thread 0 adds the
+// previous stage in order.
+constexpr int kStage = 2048;
+
+template <class Term>
+__device__ double ordered_block_sum(int64_t lo, int64_t hi, Term term) {
+  __shared__ double sb[2][kStage];
+  const int64_t n = hi - lo;
+  const int tid = static_cast<int>(threadIdx.x), nl = static_cast<int>(blockDim.x) - 32;
+  auto stage = [&](int64_t k, double* dst) {
+    const int64_t b = lo + k * kStage, e = min(hi, b + kStage);
+    for (int64_t p = b + (tid - 32); p < e; p += nl) dst[p - b] = term(p);
+  };
+  double s = 0.0;
+  const int64_t nst = (n + kStage - 1) / kStage;
+  if (tid >= 32 && nst > 0) stage(0, sb[0]);
+  __syncthreads();
+  for (int64_t k = 0; k < nst; ++k) {
+    if (tid >= 32) {
+      if (k + 1 < nst) stage(k + 1, sb[(k + 1) & 1]);
+    } else if (tid == 0) {
+      const double* c = sb[k & 1];
+      const int m = static_cast<int>(min(static_cast<int64_t>(kStage), n - k * kStage));
+#pragma unroll 8
+      for (int i = 0; i < m; ++i) s += c[i];
+    }
+    __syncthreads();
+  }
+  return s;
+}
+
+
+__global__ void __launch_bounds__(256) gather_sum_long_k(const double* __restrict__ src,
+                                                         const int64_t* __restrict__ ptr,
+                                                         const int32_t* __restrict__ idx, LongRows lr,
+                                                         double* __restrict__ out) {
+  const int64_t i = lr.idx[blockIdx.x];
+  const double s = ordered_block_sum(ptr[i], ptr[i + 1], [&](int64_t p) { return src[idx[p]]; });
+  if (threadIdx.x == 0) out[i] = s;
+}
+
+__global__ void __launch_bounds__(256) kkt_assemble_long_k(const double* __restrict__ hess,
+                                                           const double* __restrict__ jac,
+                                                           const double* __restrict__ sigma,
+                                                           const int64_t* __restrict__ ptr,
+                                                           const int64_t* __restrict__ code, LongRows lr, int64_t H,
+                                                           int64_t J, int64_t S, int64_t ntot,
+                                                           double* __restrict__ val) {
+  const int64_t p = lr.idx[blockIdx.x];
+  const int64_t HJ = H + J, HJS = H + J + S;
+  const double s = ordered_block_sum(ptr[p], ptr[p + 1], [&](int64_t q) {
+    const int64_t c = code[q];
+    if (c < H) return hess[c];
+    if (c < HJ) return jac[c - H];
+    if (c < HJS) return -1.0;
+    if (c < HJS + ntot) return sigma[c - HJS];
+    return 0.0;
+  });
+  if (threadIdx.x == 0) val[p] = s;
+}
+
+__global__ void __launch_bounds__(256) sym_matvec_long_k(const double* __restrict__ val,
+                                                         const int64_t* __restrict__ rptr,
+                                                         const int64_t* __restrict__ col,
+                                                         const int64_t* __restrict__ vidx, LongRows lr,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t i = lr.idx[blockIdx.x];
+  const double s = ordered_block_sum(rptr[i], rptr[i + 1], [&](int64_t p) { return val[vidx[p]] * x[col[p]]; });
+  if (threadIdx.x == 0) y[i] = s;
+}
+
+__global__ void __launch_bounds__(256) sym_norm_inf_long_k(const double* __restrict__ val,
+                                                           const int64_t* __restrict__ rptr,
+                                                           const int64_t* __restrict__ vidx, LongRows lr,
+                                                           unsigned long long* __restrict__ out) {
+  const int64_t i = lr.idx[blockIdx.x];
+  const double s = ordered_block_sum(rptr[i], rptr[i + 1], [&](int64_t p) { return fabs(val[vidx[p]]); });
+  if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(s)));
+}
+
+__global__ void __launch_bounds__(256) jt_lambda_long_k(const double* __restrict__ jac, const double* __restrict__ lam,
+                                                        const int64_t* __restrict__ ptr,
+                                                        const int64_t* __restrict__ e_idx,
+                                                        const int64_t* __restrict__ dual_idx, int64_t n_free,
+                                                        const int64_t* __restrict__ slack_dual, LongRows lr,
+                                                        double* __restrict__ out) {
+  const int64_t i = lr.idx[blockIdx.x];
+  double s = ordered_block_sum(ptr[i], ptr[i + 1], [&](int64_t p) { return jac[e_idx[p]] * lam[dual_idx[p]]; });
+  if (threadIdx.x == 0) {
+    if (i >= n_free) s -= lam[slack_dual[i - n_free]];
+    out[i] = s;
   }
 }
 
@@ -186,44 +296,62 @@ void objective_reduce(const double* objv, const int64_t* group_off, const int64_
   objective_combine(partials, chunk_base, weights, n_groups, obj_scale, f, flag, s);
 }
 
-void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,
+void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out, LongRows lr,
                 cudaStream_t s) {
   if (n <= 0) return;
   gather_sum_k<<<grid_for(n, 256), 256, 0, s>>>(src, ptr, idx, n, out);
+  if (lr.n > 0) gather_sum_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(src, ptr, idx, lr, out);
 }
 
 void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
                   const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
-                  cudaStream_t s) {
+                  LongRows lr, cudaStream_t s) {
   if (nnz <= 0) return;
   kkt_assemble_k<<<grid_for(nnz, 256), 256, 0, s>>>(hess, jac, sigma, ptr, code, nnz, H, J, S, ntot, val);
+  if (lr.n > 0)
+    kkt_assemble_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(hess, jac, sigma, ptr, code, lr, H, J, S, ntot,
+                                                                   val);
 }
 
 void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
-                const double* x, double* y, cudaStream_t s) {
+                const double* x, double* y, LongRows lr, cudaStream_t s) {
   if (n <= 0) return;
   sym_matvec_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, col, vidx, n, x, y);
+  if (lr.n > 0) sym_matvec_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(val, rptr, col, vidx, lr, x, y);
 }
 
-void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out,
+void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out, LongRows lr,
                   cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(double), s);
   if (n <= 0) return;
   sym_norm_inf_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, vidx, n, reinterpret_cast<unsigned long long*>(out));
+  if (lr.n > 0)
+    sym_norm_inf_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(val, rptr, vidx, lr,
+                                                                    reinterpret_cast<unsigned long long*>(out));
 }
 
 void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
                const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
-               cudaStream_t s) {
+               LongRows lr, cudaStream_t s) {
   const int64_t n = n_free + n_slack;
   if (n <= 0) return;
   jt_lambda_k<<<grid_for(n, 256), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx, n_free, slack_dual, n_slack, out);
+  if (lr.n > 0)
+    jt_lambda_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx, n_free, slack_dual,
+                                                                lr, out);
 }
 
 void max_abs(const double* v, int64_t n, double* out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(double), s);
   if (n <= 0) return;
   max_abs_k<<<grid_for(n, 256), 256, 0, s>>>(v, n, reinterpret_cast<unsigned long long*>(out));
+}
+
+std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr) {
+  std::vector<int64_t> out;
+  for (size_t i = 0; i + 1 < ptr.size(); ++i)
+    if (ptr[i + 1] - ptr[i] > kLongRow) out.push_back(static_cast<int64_t>(i));
+  return out;
 }
 
 }  // namespace ocg::dev

@@ -9,8 +9,21 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace ocg::dev {
+
+// Rows (source lists) longer than kLongRow — e.g. a free final time's KKT
+// diagonal, which gathers one Hessian entry per time step — are skipped by
+// the thread-per-row kernels and summed by one block each, in the same order
+// (increasing source index, one accumulator). `idx`: device array of the
+// long rows of that pointer array (long_rows() on its host copy).
+constexpr int64_t kLongRow = 1024;
+struct LongRows {
+  const int64_t* idx = nullptr;
+  int64_t n = 0;
+};
+std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr);
 
 // Objective: per-instance values -> f (EvalContext::eval_objective + Backend::par_reduce,
 // eval.cpp:175-200, backend.cpp:119-133): chunks of 512 summed in index
@@ -30,7 +43,7 @@ void objective_combine(const double* partials, const int64_t* chunk_base, const 
                        double obj_scale, double* f, int* flag, cudaStream_t s);
 
 // out[i] = sum_{p in [ptr[i], ptr[i+1])} src[idx[p]]  (0.0-based, in p order)
-void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out,
+void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64_t n, double* out, LongRows lr,
                 cudaStream_t s);
 
 // K.val[p] = sum of its sources in code order (KktAssembler::assemble,
@@ -38,22 +51,22 @@ void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64
 // < H+J+S+ntot: sigma[code-H-J-S]; else 0 (the dual diagonal's structural slot).
 void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
                   const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
-                  cudaStream_t s);
+                  LongRows lr, cudaStream_t s);
 
 // y[i] = sum over the full symmetric row i (increasing column) of K_ij x_j —
 // the accumulation order of sparse::matvec_sym (sparse.cpp:51-61).
 void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
-                const double* x, double* y, cudaStream_t s);
+                const double* x, double* y, LongRows lr, cudaStream_t s);
 
 // *out = max_i sum_j |K_ij| over the full symmetric rows (sparse::norm_inf_sym)
-void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out,
+void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out, LongRows lr,
                   cudaStream_t s);
 
 // out[i] = sum_p jac[e_p] * lam[dual_p] (p in increasing e), then for slack
 // rows out[i] -= lam[dual] (Solver::compute_jt_lambda, solver.cpp:244-257).
 void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
                const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
-               cudaStream_t s);
+               LongRows lr, cudaStream_t s);
 
 // max |v| over n entries into *out (device scalar); exact.
 void max_abs(const double* v, int64_t n, double* out, cudaStream_t s);
