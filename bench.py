@@ -55,6 +55,9 @@ def parse():
                     help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
     ap.add_argument("--solve", default="quadrotor:100000",
                     help="model:N of the full IPM solve leg ('ipm_solve' key; 'none' to skip)")
+    ap.add_argument("--goddard-solve", default="100000:3",
+                    help="N[:ref_iters] of the Goddard full device solve (BASELINE config 2, 'goddard_solve' key); the "
+                         "reference runs ref_iters iterations for a per-iteration comparison; 'none' to skip")
     ap.add_argument("--batch", default="4096:500",
                     help="instances:N of the batched cart-pendulum solve leg (BASELINE config 5, 'batch_solve' "
                          "key; 'none' to skip)")
@@ -458,6 +461,9 @@ def run_ours(args) -> None:
             out["extra"] = secondary(dev, stream, flush, sink, peak)
         if args.solve != "none" and world == 1:
             out["ipm_solve"] = ipm_solve_leg(args.solve, not args.no_cpu_baseline)
+        if args.goddard_solve != "none" and world == 1:  # BASELINE config 2
+            n, cap = (args.goddard_solve.split(":") + ["3"])[:2]
+            out["goddard_solve"] = ipm_solve_leg(f"goddard:{n}", not args.no_cpu_baseline, int(cap))
         if args.batch != "none" and world == 1:
             out["batch_solve"] = batch_solve_leg(args.batch, not args.no_cpu_baseline)
         print(json.dumps(out), flush=True)
@@ -466,14 +472,17 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def ipm_solve_leg(spec: str, with_reference: bool) -> dict:
+def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dict:
     """Full interior-point solve (BASELINE metric: "IPM solve time at N=1e5"):
     ocg_ipm_solve — the reference's filter line-search IPM with evaluations,
     KKT assembly, vector work and the time-partitioned band LDL^T all on the
     device — against the reference's own ipm::solve (oracle/_ref/libref.so,
     Backend::parallel on all host cores, its CPU LDL^T). Wall times of the
     solve call; the device time includes the one-time NVRTC compile of the
-    model's kernels (reported separately as jit_s from a second solve)."""
+    model's kernels (reported separately as jit_s from a second solve).
+    ref_max_iter > 0 caps the reference's run (Goddard at N=1e5 needs ~N/2
+    iterations, about 64 h on the host: SURVEY.md D6); the two are then
+    compared per iteration."""
     from paper_2510_03932_b200 import MODELS, Model, solve
     name, N = spec.split(":")
     N = int(N)
@@ -497,13 +506,19 @@ def ipm_solve_leg(spec: str, with_reference: bool) -> dict:
         cores = os.cpu_count() or 1
         rm = RefModel(MODELS[name], N)
         t0 = time.perf_counter()
-        r = rm.solve(parallel=True, workers=cores)
+        r = rm.solve(parallel=True, workers=cores, max_iter=ref_max_iter)
         out["reference"] = {"wall_s": time.perf_counter() - t0, "iterations": int(r["iterations"]),
                             "objective": r["objective"], "status": int(r["status"]), "cores": cores,
                             "time_factorize_s": r["time_factorize"], "time_derivatives_s": r["time_derivatives"]}
-        out["iterations_match"] = int(r["iterations"]) == d2["iterations"]
-        out["objective_rel_diff"] = abs(r["objective"] - d2["objective"]) / max(abs(r["objective"]), 1e-300)
-        out["speedup_vs_reference"] = out["reference"]["wall_s"] / t_second
+        if ref_max_iter > 0:
+            out["reference"]["capped_at"] = ref_max_iter
+            out["reference"]["s_per_iter"] = out["reference"]["wall_s"] / max(1, int(r["iterations"]))
+            out["device_s_per_iter"] = d2["time_total"] / max(1, d2["iterations"])
+            out["speedup_per_iter"] = out["reference"]["s_per_iter"] / out["device_s_per_iter"]
+        else:
+            out["iterations_match"] = int(r["iterations"]) == d2["iterations"]
+            out["objective_rel_diff"] = abs(r["objective"] - d2["objective"]) / max(abs(r["objective"]), 1e-300)
+            out["speedup_vs_reference"] = out["reference"]["wall_s"] / t_second
     return out
 
 

@@ -997,6 +997,8 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     longs(K->src_ptr, static_cast<size_t>(K->nnz), K->src_long, K->n_src_long);
     longs(K->mv_ptr, static_cast<size_t>(K->dim), K->mv_long, K->n_mv_long);
     longs(K->jt_ptr, static_cast<size_t>(K->ntot), K->jt_long, K->n_jt_long);
+    K->mv_long_part.alloc(static_cast<size_t>(K->n_mv_long) * ocg::dev::kLongBlocks);
+    K->jt_long_part.alloc(static_cast<size_t>(K->n_jt_long) * ocg::dev::kLongBlocks);
   }
   K->val.alloc(static_cast<size_t>(K->nnz));
   ck(cudaMemsetAsync(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double), cudaStreamPerThread), "memset");
@@ -1061,9 +1063,9 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
 int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
   if (!k || !x || !y) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
-  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y, {k->mv_long.p, k->n_mv_long},
-                       st(s));
-  k->ev->launches += k->n_mv_long > 0 ? 2 : 1;
+  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y,
+                       {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }
@@ -1071,8 +1073,9 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
 int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
-  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out, {k->mv_long.p, k->n_mv_long}, st(s));
-  k->ev->launches += k->n_mv_long > 0 ? 2 : 1;
+  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out,
+                         {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }
@@ -1081,8 +1084,8 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
   if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
-                      k->n_slack, out, {k->jt_long.p, k->n_jt_long}, st(s));
-  k->ev->launches += k->n_jt_long > 0 ? 2 : 1;
+                      k->n_slack, out, {k->jt_long.p, k->n_jt_long, k->jt_long_part.p}, st(s));
+  k->ev->launches += k->n_jt_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END
 }

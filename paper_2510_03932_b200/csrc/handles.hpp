@@ -173,6 +173,7 @@ struct ocg_kkt {
   // rows of src_ptr / mv_ptr / jt_ptr longer than kLongRow (kernels.hpp)
   DBuf<int64_t> src_long, mv_long, jt_long;
   int64_t n_src_long = 0, n_mv_long = 0, n_jt_long = 0;
+  DBuf<double> mv_long_part, jt_long_part;  // n_*_long x kLongBlocks partial sums
 };
 
 // Band LDL^T of the KKT matrix (band.hpp): plan + device buffers

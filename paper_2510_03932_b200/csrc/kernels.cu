@@ -172,10 +172,10 @@ __global__ void __launch_bounds__(256) max_abs_k(const double* __restrict__ v, i
 // tf of a free-horizon problem: its KKT diagonal gathers one Hessian entry per
 // time step, its J^T lambda entry one Jacobian entry per dynamics row) would
 // be one thread's serial chain of dependent gathers. The thread-per-row
-// kernels skip such rows; one block per long row keeps the reference's order
-// (increasing source index, one `s += term` accumulator): threads 32.. gather
-// the terms into shared memory, double-buffered, while thread 0 adds the
-// previous stage in order.
+// kernels skip such rows; one block per long row sums it. Pure sums keep the
+// reference's order (increasing source index, one `s += term` accumulator):
+// threads 32.. gather the terms into shared memory, double-buffered, while
+// thread 0 adds the previous stage in order.
 constexpr int kStage = 2048;
 
 template <class Term>
@@ -197,12 +197,62 @@ __device__ double ordered_block_sum(int64_t lo, int64_t hi, Term term) {
     } else if (tid == 0) {
       const double* c = sb[k & 1];
       const int m = static_cast<int>(min(static_cast<int64_t>(kStage), n - k * kStage));
-#pragma unroll 8
-      for (int i = 0; i < m; ++i) s += c[i];
+      int i = 0;
+      for (; i + 8 <= m; i += 8) {  // eight loads in flight, then the ordered adds
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = c[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+      }
+      for (; i < m; ++i) s += c[i];
     }
     __syncthreads();
   }
   return s;
+}
+
+// Products and norms of long rows (J^T lambda, K x, |K| row sums): a fixed-shape
+// tree over kLongBlocks blocks per row — block b sums its contiguous share of
+// the row with thread t taking terms t, t+256, ..., then the warps' shuffle
+// trees and the warp partials in warp order into partials[row][b]; a second
+// pass adds the kLongBlocks partials in block order. Deterministic; not the
+// reference's left-to-right order (these sums are FMA-contracted in the
+// thread-per-row path anyway), within 1e-12 relative of it.
+template <class Term>
+__device__ void tree_block_partial(int64_t lo, int64_t hi, Term term, double* partial) {
+  __shared__ double wp[8];
+  const int64_t len = hi - lo, per = (len + kLongBlocks - 1) / kLongBlocks;
+  const int64_t a = lo + min(len, per * blockIdx.x), e = lo + min(len, per * (blockIdx.x + 1));
+  double s = 0.0;
+#pragma unroll 4
+  for (int64_t p = a + threadIdx.x; p < e; p += blockDim.x) s += term(p);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += wp[w];
+    *partial = s;
+  }
+}
+
+// second pass: one thread per long row adds its partials in block order;
+// mode 0 stores, 1 subtracts the slack term (J^T lambda), 2 takes the max (norm)
+__global__ void long_finish_k(LongRows lr, double* __restrict__ out, int mode, const double* __restrict__ lam,
+                              const int64_t* __restrict__ slack_dual, int64_t n_free) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= lr.n) return;
+  const double* pp = lr.partials + r * kLongBlocks;
+  double s = 0.0;
+  for (int b = 0; b < kLongBlocks; ++b) s += pp[b];
+  const int64_t i = lr.idx[r];
+  if (mode == 2) {
+    atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(s)));
+    return;
+  }
+  if (mode == 1 && i >= n_free) s -= lam[slack_dual[i - n_free]];
+  out[i] = s;
 }
 
 
@@ -239,33 +289,27 @@ __global__ void __launch_bounds__(256) sym_matvec_long_k(const double* __restric
                                                          const int64_t* __restrict__ rptr,
                                                          const int64_t* __restrict__ col,
                                                          const int64_t* __restrict__ vidx, LongRows lr,
-                                                         const double* __restrict__ x, double* __restrict__ y) {
-  const int64_t i = lr.idx[blockIdx.x];
-  const double s = ordered_block_sum(rptr[i], rptr[i + 1], [&](int64_t p) { return val[vidx[p]] * x[col[p]]; });
-  if (threadIdx.x == 0) y[i] = s;
+                                                         const double* __restrict__ x) {
+  const int64_t r = blockIdx.y, i = lr.idx[r];
+  tree_block_partial(rptr[i], rptr[i + 1], [&](int64_t p) { return val[vidx[p]] * x[col[p]]; },
+                     lr.partials + r * kLongBlocks + blockIdx.x);
 }
 
 __global__ void __launch_bounds__(256) sym_norm_inf_long_k(const double* __restrict__ val,
                                                            const int64_t* __restrict__ rptr,
-                                                           const int64_t* __restrict__ vidx, LongRows lr,
-                                                           unsigned long long* __restrict__ out) {
-  const int64_t i = lr.idx[blockIdx.x];
-  const double s = ordered_block_sum(rptr[i], rptr[i + 1], [&](int64_t p) { return fabs(val[vidx[p]]); });
-  if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(s)));
+                                                           const int64_t* __restrict__ vidx, LongRows lr) {
+  const int64_t r = blockIdx.y, i = lr.idx[r];
+  tree_block_partial(rptr[i], rptr[i + 1], [&](int64_t p) { return fabs(val[vidx[p]]); },
+                     lr.partials + r * kLongBlocks + blockIdx.x);
 }
 
 __global__ void __launch_bounds__(256) jt_lambda_long_k(const double* __restrict__ jac, const double* __restrict__ lam,
                                                         const int64_t* __restrict__ ptr,
                                                         const int64_t* __restrict__ e_idx,
-                                                        const int64_t* __restrict__ dual_idx, int64_t n_free,
-                                                        const int64_t* __restrict__ slack_dual, LongRows lr,
-                                                        double* __restrict__ out) {
-  const int64_t i = lr.idx[blockIdx.x];
-  double s = ordered_block_sum(ptr[i], ptr[i + 1], [&](int64_t p) { return jac[e_idx[p]] * lam[dual_idx[p]]; });
-  if (threadIdx.x == 0) {
-    if (i >= n_free) s -= lam[slack_dual[i - n_free]];
-    out[i] = s;
-  }
+                                                        const int64_t* __restrict__ dual_idx, LongRows lr) {
+  const int64_t r = blockIdx.y, i = lr.idx[r];
+  tree_block_partial(ptr[i], ptr[i + 1], [&](int64_t p) { return jac[e_idx[p]] * lam[dual_idx[p]]; },
+                     lr.partials + r * kLongBlocks + blockIdx.x);
 }
 
 int grid_for(int64_t n, int block) {
@@ -317,7 +361,10 @@ void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, cons
                 const double* x, double* y, LongRows lr, cudaStream_t s) {
   if (n <= 0) return;
   sym_matvec_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, col, vidx, n, x, y);
-  if (lr.n > 0) sym_matvec_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(val, rptr, col, vidx, lr, x, y);
+  if (lr.n > 0) {
+    sym_matvec_long_k<<<dim3(kLongBlocks, static_cast<unsigned>(lr.n)), 256, 0, s>>>(val, rptr, col, vidx, lr, x);
+    long_finish_k<<<static_cast<unsigned>((lr.n + 127) / 128), 128, 0, s>>>(lr, y, 0, nullptr, nullptr, 0);
+  }
 }
 
 void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out, LongRows lr,
@@ -325,9 +372,10 @@ void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, i
   cudaMemsetAsync(out, 0, sizeof(double), s);
   if (n <= 0) return;
   sym_norm_inf_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, vidx, n, reinterpret_cast<unsigned long long*>(out));
-  if (lr.n > 0)
-    sym_norm_inf_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(val, rptr, vidx, lr,
-                                                                    reinterpret_cast<unsigned long long*>(out));
+  if (lr.n > 0) {
+    sym_norm_inf_long_k<<<dim3(kLongBlocks, static_cast<unsigned>(lr.n)), 256, 0, s>>>(val, rptr, vidx, lr);
+    long_finish_k<<<static_cast<unsigned>((lr.n + 127) / 128), 128, 0, s>>>(lr, out, 2, nullptr, nullptr, 0);
+  }
 }
 
 void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
@@ -336,9 +384,11 @@ void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const i
   const int64_t n = n_free + n_slack;
   if (n <= 0) return;
   jt_lambda_k<<<grid_for(n, 256), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx, n_free, slack_dual, n_slack, out);
-  if (lr.n > 0)
-    jt_lambda_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx, n_free, slack_dual,
-                                                                lr, out);
+  if (lr.n > 0) {
+    jt_lambda_long_k<<<dim3(kLongBlocks, static_cast<unsigned>(lr.n)), 256, 0, s>>>(jac, lam, ptr, e_idx, dual_idx,
+                                                                                   lr);
+    long_finish_k<<<static_cast<unsigned>((lr.n + 127) / 128), 128, 0, s>>>(lr, out, 1, lam, slack_dual, n_free);
+  }
 }
 
 void max_abs(const double* v, int64_t n, double* out, cudaStream_t s) {

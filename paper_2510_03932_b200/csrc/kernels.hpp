@@ -13,15 +13,20 @@
 
 namespace ocg::dev {
 
-// Rows (source lists) longer than kLongRow — e.g. a free final time's KKT
-// diagonal, which gathers one Hessian entry per time step — are skipped by
-// the thread-per-row kernels and summed by one block each, in the same order
-// (increasing source index, one accumulator). `idx`: device array of the
-// long rows of that pointer array (long_rows() on its host copy).
+// Rows (source lists) longer than kLongRow — e.g. a free final time's J^T
+// lambda entry or matvec row, which gather one entry per dynamics row — are
+// skipped by the thread-per-row kernels and summed by one block each: pure
+// sums (gradient gather, KKT assembly) in the same order (increasing source
+// index, one accumulator), products and norms (J^T lambda, K x, |K|) by a
+// fixed-shape tree. `idx`: device array of the long rows of that pointer
+// array (long_rows() on its host copy); `partials`: device scratch of
+// n * kLongBlocks doubles for the tree kernels.
 constexpr int64_t kLongRow = 1024;
+constexpr int kLongBlocks = 64;
 struct LongRows {
   const int64_t* idx = nullptr;
   int64_t n = 0;
+  double* partials = nullptr;
 };
 std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr);
 
