@@ -18,7 +18,7 @@ CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp"]
-CUDA_SRCS = ["kernels.cu", "band.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu"]
+CUDA_SRCS = ["kernels.cu", "band.cu", "sepcr.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu"]
 HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp"]
 
 

@@ -1259,7 +1259,11 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
                                                                         BandBatch{});
     if (P.wg > 0) schur_global_k<<<1, 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf, BandBatch{});
     if (timing) cudaEventRecord(ev[2], s);
-    fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
+    if (D.cr)
+      cr_factor(P, P.segs.back(), buf, D.primal, delta_w, delta_c, D.cr, D.crparts, inertia_parts + 3 * P.nseg, s);
+    else
+      fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts,
+                                          BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
@@ -1304,7 +1308,11 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
                                                                         gparts, work + sep.pos, BandBatch{});
     if (P.wg > 0)
       rhs_global_k<<<1, 32, 0, s>>>(P.nseg, P.wmax, P.b, P.wg, sep.n, gparts, work + sep.pos, BandBatch{});
-    solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    if (D.cr)
+      cr_solve(P, sep, D.cr, work, s);
+    else
+      solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
+                                          BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
     solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
   }

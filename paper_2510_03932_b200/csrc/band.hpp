@@ -112,7 +112,16 @@ struct BandDev {  // device copies of the plan
   const int64_t* perm = nullptr;
   const double* primal = nullptr;
   const int64_t* border_pos = nullptr;
+  // separator system by block cyclic reduction (sepcr.cu); NULL: one band block
+  double* cr = nullptr;        // cr_length(nseg - 1, b, wg) doubles
+  long long* crparts = nullptr;  // 3 (nseg - 1) inertia counts
 };
+
+// block cyclic reduction of the separator system (sepcr.cu)
+long long cr_length(int ns, int b, int w);
+void cr_factor(const BandPlan& P, const BandSeg& sep, const double* buf, const double* primal, double dw, double dc,
+               double* cr, long long* crparts, long long* sep_inertia, cudaStream_t s);
+void cr_solve(const BandPlan& P, const BandSeg& sep, double* cr, double* work, cudaStream_t s);
 
 // buf = P K P^T scattered into the segment and separator blocks (zeroed first)
 void band_assemble(const BandPlan& P, const BandDev& D, const double* kval, double* buf, cudaStream_t s);

@@ -1158,6 +1158,13 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
   L->dev.perm = L->perm.p;
   L->dev.primal = L->primal.p;
   L->dev.border_pos = L->border_pos.p;
+  const char* sep_mode = std::getenv("OCG_SEP");  // "band": the separator system as one band block
+  if (P.nseg > 1 && !(sep_mode && std::string(sep_mode) == "band")) {
+    L->cr.alloc(static_cast<size_t>(ocg::dev::cr_length(P.nseg - 1, P.b, P.wg)));
+    L->crparts.alloc(static_cast<size_t>(3 * (P.nseg - 1)));
+    L->dev.cr = L->cr.p;
+    L->dev.crparts = L->crparts.p;
+  }
   *out = L.release();
   return OCG_OK;
   OCG_GUARD_END

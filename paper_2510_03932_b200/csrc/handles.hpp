@@ -184,6 +184,8 @@ struct ocg_ldl {
   DBuf<ocg::BandSeg> segs;
   DBuf<double> primal, buf, Dinv, work;
   DBuf<long long> inertia, inertia_parts;
+  DBuf<double> cr;            // separator system by block cyclic reduction
+  DBuf<long long> crparts;
   ocg::dev::BandDev dev;
   double delta_w = 0.0, delta_c = 0.0;
   int64_t factorizations = 0;

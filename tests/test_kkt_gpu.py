@@ -83,3 +83,35 @@ def test_band_ldl_inertia_and_solve(name, segments, monkeypatch):
             xs = ldl.solve(b).cpu().numpy()
             ref = np.linalg.solve(K, b)
             assert np.max(np.abs(xs - ref)) <= 1e-8 * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("name,N,segments", [("goddard", 1500, "64"), ("quadrotor", 400, "29"),
+                                             ("shuttle", 500, "40"), ("double_integrator", 3000, "100")])
+def test_separator_cyclic_reduction(name, N, segments, monkeypatch):
+    """Many separators: the separator system by block cyclic reduction
+    (sepcr.cu, several levels, a border for the free-horizon models) against
+    the dense inertia and solve, and against the separator system factored as
+    one band block (OCG_SEP=band)."""
+    monkeypatch.setenv("OCG_LDL_SEGMENTS", segments)
+    m, ec, k, _ = _setup(name, N)
+    sigma = np.random.default_rng(5).uniform(0.5, 2.0, k.ntot)
+    k.assemble(sigma)
+    val = k.values().cpu().numpy()
+    cr = BandLdl(k)
+    assert cr.info()["segments"] > 16
+    monkeypatch.setenv("OCG_SEP", "band")
+    band = BandLdl(k)
+    b = np.random.default_rng(6).standard_normal(k.dim)
+    for dw, dc in [(0.0, 0.0), (1e-2, 0.0), (10.0, 1e-8)]:
+        K = torch.tensor(_dense(k, val, dw, dc), device="cuda")
+        ev = torch.linalg.eigvalsh(K).cpu().numpy()
+        tol = 1e-9 * np.abs(ev).max()
+        expect = (int((ev > tol).sum()), int((ev < -tol).sum()), int((np.abs(ev) <= tol).sum()))
+        got, got_band = cr.factor(dw, dc), band.factor(dw, dc)
+        assert sum(got) == k.dim
+        if expect[2] == 0 and got[2] == 0:
+            assert got == expect == got_band, (dw, dc, got, got_band, expect)
+            ref = torch.linalg.solve(K, torch.tensor(b, device="cuda")).cpu().numpy()
+            xs = cr.solve(b).cpu().numpy()
+            assert np.max(np.abs(xs - ref)) <= 1e-8 * max(1.0, np.max(np.abs(ref)))
+            assert np.max(np.abs(xs - band.solve(b).cpu().numpy())) <= 1e-8 * max(1.0, np.max(np.abs(ref)))
