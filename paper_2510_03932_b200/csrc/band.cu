@@ -1081,15 +1081,28 @@ int grid_for(int64_t n) {
 }  // namespace
 
 namespace {
+// column of CSC entry q (one thread per entry: a dense column — a free final
+// time's — must not become one thread's serial loop)
+__device__ __forceinline__ int64_t col_of(const int64_t* __restrict__ colp, int64_t dim, int64_t q) {
+  int64_t lo = 0, hi = dim;  // colp[lo] <= q < colp[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (colp[mid] <= q)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
 __global__ void bandwidth_k(const int64_t* __restrict__ colp, const int64_t* __restrict__ rowi,
-                            const int64_t* __restrict__ fpos, int64_t n, int64_t dim, unsigned long long* out) {
+                            const int64_t* __restrict__ fpos, int64_t n, int64_t dim, int64_t nnz,
+                            unsigned long long* out) {
   unsigned long long m = 0;
-  GRID_LOOP(j, dim) {
-    const int64_t pj = fpos[j];
-    for (int64_t q = colp[j]; q < colp[j + 1]; ++q) {
-      const int64_t pi = fpos[rowi[q]];
-      if (pi < n && pj < n) m = max(m, static_cast<unsigned long long>(pi > pj ? pi - pj : pj - pi));
-    }
+  GRID_LOOP(q, nnz) {
+    const int64_t pj = fpos[col_of(colp, dim, q)];
+    const int64_t pi = fpos[rowi[q]];
+    if (pi < n && pj < n) m = max(m, static_cast<unsigned long long>(pi > pj ? pi - pj : pj - pi));
   }
   atomicMax(out, m);
 }
@@ -1098,9 +1111,9 @@ __global__ void band_dst_k(BandDstIn in, const int8_t* __restrict__ lk, const in
                            const int64_t* __restrict__ ll, const BandSeg* __restrict__ segs,
                            int64_t* __restrict__ dst, int* __restrict__ err) {
   const int64_t n = in.n, b = in.b, wg = in.wg, n2 = in.n2;
-  GRID_LOOP(j, in.dim) {
-    const int64_t fc = in.fpos[j];
-    for (int64_t q = in.colp[j]; q < in.colp[j + 1]; ++q) {
+  GRID_LOOP(q, in.nnz) {
+    const int64_t fc = in.fpos[col_of(in.colp, in.dim, q)];
+    {
       const int64_t fa = in.fpos[in.rowi[q]];
       int ak = lk[fa], ck_ = lk[fc];
       int64_t ai = li[fa], al = ll[fa], ci = li[fc], cl = ll[fc];
@@ -1190,7 +1203,10 @@ int64_t bandwidth(const int64_t* colp, const int64_t* rowi, const int64_t* fpos,
   unsigned long long* d = nullptr;
   cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), s);
   cudaMemsetAsync(d, 0, sizeof(unsigned long long), s);
-  bandwidth_k<<<grid_for(dim), 256, 0, s>>>(colp, rowi, fpos, n, dim, d);
+  int64_t nnz = 0;
+  cudaMemcpyAsync(&nnz, colp + dim, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  bandwidth_k<<<grid_for(nnz), 256, 0, s>>>(colp, rowi, fpos, n, dim, nnz, d);
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(d, s);
@@ -1213,7 +1229,9 @@ int64_t* band_dst(const BandDstIn& in, const std::vector<int8_t>& lk, const std:
   cudaMallocAsync(reinterpret_cast<void**>(&derr), sizeof(int), s);
   cudaMemsetAsync(derr, 0, sizeof(int), s);
   cudaMallocAsync(reinterpret_cast<void**>(&dst), std::max<int64_t>(1, nnz) * sizeof(int64_t), s);
-  band_dst_k<<<grid_for(in.dim), 256, 0, s>>>(in, dlk, dli, dll, dseg, dst, derr);
+  BandDstIn in2 = in;
+  in2.nnz = nnz;
+  band_dst_k<<<grid_for(nnz), 256, 0, s>>>(in2, dlk, dli, dll, dseg, dst, derr);
   int err = 0;
   cudaMemcpyAsync(&err, derr, sizeof(int), cudaMemcpyDeviceToHost, s);
   for (void* p : {static_cast<void*>(dlk), static_cast<void*>(dli), static_cast<void*>(dll), static_cast<void*>(dseg),

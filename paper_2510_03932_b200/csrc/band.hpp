@@ -99,6 +99,7 @@ struct BandDstIn {
   const int64_t* rowi = nullptr;
   const int64_t* fpos = nullptr;
   int64_t dim = 0, n = 0, b = 0, wg = 0, n2 = 0, nseg = 1;
+  int64_t nnz = 0;
 };
 int64_t* upload_i64(const std::vector<int64_t>& v, cudaStream_t s);
 int64_t bandwidth(const int64_t* colp, const int64_t* rowi, const int64_t* fpos, int64_t n, int64_t dim,

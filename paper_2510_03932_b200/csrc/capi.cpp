@@ -986,13 +986,8 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   {
     // long rows of the three gathers (a free final time's diagonal, J^T lambda entry, matvec row)
     auto longs = [&](const DBuf<int64_t>& ptr, size_t n, DBuf<int64_t>& out, int64_t& count) {
-      std::vector<int64_t> h(n + 1);
-      ck(cudaMemcpyAsync(h.data(), ptr.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, cudaStreamPerThread),
-         "D2H ptr");
-      ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
-      const auto lr = ocg::dev::long_rows(h);
-      out.upload(lr);
-      count = static_cast<int64_t>(lr.size());
+      out.alloc(n);
+      count = ocg::dev::long_rows_device(ptr.p, static_cast<int64_t>(n), out.p, cudaStreamPerThread);
     };
     longs(K->src_ptr, static_cast<size_t>(K->nnz), K->src_long, K->n_src_long);
     longs(K->mv_ptr, static_cast<size_t>(K->dim), K->mv_long, K->n_mv_long);
@@ -1105,6 +1100,14 @@ int ocg::hd::set_error(int code, const std::string& msg) { return fail(code, msg
 int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ocg_ldl_create] %-16s %8.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+    tprev = now;
+  };
   const ocg::Nlp& nlp = k->ev->model->nlp;
   // time node of every KKT index: slots by their slab, rows by the last node
   // their Jacobian touches; free variables (and rows touching only them) are
@@ -1127,6 +1130,7 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
     node[static_cast<size_t>(k->n_free + q)] = row_node[static_cast<size_t>(k->slack_of[static_cast<size_t>(q)])];
   for (Index d = 0; d < k->m; ++d)
     node[static_cast<size_t>(k->ntot + d)] = row_node[static_cast<size_t>(k->dual_row[static_cast<size_t>(d)])];
+  lap("node map");
   auto L = std::make_unique<ocg_ldl>();
   L->kkt = k;
   {
@@ -1143,6 +1147,7 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
     L->plan = ocg::make_band_plan(k->dim, node, k->colp, k->rowi, k->ntot, target, &csc, &ddst);
     L->dst.adopt(ddst, static_cast<size_t>(csc.nnz));
   }
+  lap("band plan");
   const ocg::BandPlan& P = L->plan;
   L->perm.upload(P.perm);
   L->primal.upload(P.primal);
@@ -1165,6 +1170,7 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
     L->dev.cr = L->cr.p;
     L->dev.crparts = L->crparts.p;
   }
+  lap("buffers");
   *out = L.release();
   return OCG_OK;
   OCG_GUARD_END

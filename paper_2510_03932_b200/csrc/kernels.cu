@@ -397,6 +397,27 @@ void max_abs(const double* v, int64_t n, double* out, cudaStream_t s) {
   max_abs_k<<<grid_for(n, 256), 256, 0, s>>>(v, n, reinterpret_cast<unsigned long long*>(out));
 }
 
+namespace {
+__global__ void long_rows_k(const int64_t* __restrict__ ptr, int64_t n, int64_t* __restrict__ out,
+                            unsigned long long* __restrict__ count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (is_long(ptr, i)) out[atomicAdd(count, 1ull)] = i;
+}
+}  // namespace
+
+int64_t long_rows_device(const int64_t* ptr, int64_t n, int64_t* out, cudaStream_t s) {
+  unsigned long long* d = nullptr;
+  cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), s);
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), s);
+  if (n > 0) long_rows_k<<<grid_for(n, 256), 256, 0, s>>>(ptr, n, out, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  cudaStreamSynchronize(s);
+  return static_cast<int64_t>(h);
+}
+
 std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr) {
   std::vector<int64_t> out;
   for (size_t i = 0; i + 1 < ptr.size(); ++i)

@@ -29,6 +29,9 @@ struct LongRows {
   double* partials = nullptr;
 };
 std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr);
+// the same on the device: long rows of ptr[0..n] into out (capacity n, any
+// order — each is summed on its own); returns their count
+int64_t long_rows_device(const int64_t* ptr, int64_t n, int64_t* out, cudaStream_t s);
 
 // Objective: per-instance values -> f (EvalContext::eval_objective + Backend::par_reduce,
 // eval.cpp:175-200, backend.cpp:119-133): chunks of 512 summed in index

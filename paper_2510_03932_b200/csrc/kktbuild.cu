@@ -98,31 +98,36 @@ __global__ void slots_k(const unsigned long long* __restrict__ key, const int64_
   }
 }
 
-// mirrored entries of the lower CSC for the full symmetric CSR
-__global__ void mirror_k(const int64_t* __restrict__ colp, const int64_t* __restrict__ rowi, int64_t dim,
-                         const int64_t* __restrict__ mirror_off, unsigned long long* __restrict__ key,
-                         int64_t* __restrict__ val) {
-  GRID_LOOP(j, dim) {
-    int64_t o = mirror_off[j];
-    for (int64_t p = colp[j]; p < colp[j + 1]; ++p) {
-      const int64_t i = rowi[p];
-      key[o] = (static_cast<unsigned long long>(i) << 32) | static_cast<unsigned long long>(j);
-      val[o++] = p;
-      if (i != j) {
-        key[o] = (static_cast<unsigned long long>(j) << 32) | static_cast<unsigned long long>(i);
-        val[o++] = p;
-      }
-    }
+// column of CSC entry q by binary search: the mirror is built one thread per
+// entry, so a dense column (a free final time's) is not one thread's loop
+__device__ __forceinline__ int64_t col_of(const int64_t* __restrict__ colp, int64_t dim, int64_t q) {
+  int64_t lo = 0, hi = dim;  // colp[lo] <= q < colp[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (colp[mid] <= q)
+      lo = mid;
+    else
+      hi = mid;
   }
+  return lo;
 }
 
-__global__ void mirror_count_k(const int64_t* __restrict__ colp, const int64_t* __restrict__ rowi, int64_t dim,
-                               int64_t* __restrict__ cnt) {
-  GRID_LOOP(j, dim) {
-    int64_t c = 0;
-    for (int64_t p = colp[j]; p < colp[j + 1]; ++p) c += rowi[p] != j ? 2 : 1;
-    cnt[j] = c;
+// mirrored entries of the lower CSC for the full symmetric CSR: entry p gives
+// keys (row, col) at 2p and, off the diagonal, (col, row) at 2p + 1 (kNone on
+// the diagonal: sorts last and is cut off)
+__global__ void mirror_k(const int64_t* __restrict__ colp, const int64_t* __restrict__ rowi, int64_t dim,
+                         int64_t nnz, unsigned long long* __restrict__ key, int64_t* __restrict__ val,
+                         unsigned long long* __restrict__ ndiag) {
+  unsigned long long nd = 0;
+  GRID_LOOP(p, nnz) {
+    const int64_t j = col_of(colp, dim, p), i = rowi[p];
+    key[2 * p] = (static_cast<unsigned long long>(i) << 32) | static_cast<unsigned long long>(j);
+    val[2 * p] = p;
+    key[2 * p + 1] = i != j ? (static_cast<unsigned long long>(j) << 32) | static_cast<unsigned long long>(i) : kNone;
+    val[2 * p + 1] = p;
+    nd += i == j ? 1 : 0;
   }
+  if (nd) atomicAdd(ndiag, nd);
 }
 
 __global__ void split_key_k(const unsigned long long* __restrict__ key, int64_t n, int64_t* __restrict__ col,
@@ -245,17 +250,16 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   out.ncode = nvalid;
 
   // 3. full symmetric CSR for matvec: mirrored entries keyed (row, col)
-  auto* mcnt = dalloc<int64_t>(static_cast<size_t>(dim), s);
-  auto* moff = dalloc<int64_t>(static_cast<size_t>(dim) + 1, s);
-  mirror_count_k<<<grid_for(dim), 256, 0, s>>>(colp, rowi, dim, mcnt);
-  exclusive_offsets(mcnt, dim, moff, s);
-  int64_t mv_nnz = 0;
-  ck(cudaMemcpyAsync(&mv_nnz, moff + dim, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "mv nnz");
+  auto* mkey = dalloc<unsigned long long>(2 * static_cast<size_t>(nnz), s);
+  auto* mval = dalloc<int64_t>(2 * static_cast<size_t>(nnz), s);
+  auto* ndiag = dalloc<unsigned long long>(1, s);
+  ck(cudaMemsetAsync(ndiag, 0, sizeof(unsigned long long), s), "memset");
+  mirror_k<<<grid_for(nnz), 256, 0, s>>>(colp, rowi, dim, nnz, mkey, mval, ndiag);
+  unsigned long long nd = 0;
+  ck(cudaMemcpyAsync(&nd, ndiag, sizeof(nd), cudaMemcpyDeviceToHost, s), "ndiag");
   ck(cudaStreamSynchronize(s), "sync");
-  auto* mkey = dalloc<unsigned long long>(static_cast<size_t>(mv_nnz), s);
-  auto* mval = dalloc<int64_t>(static_cast<size_t>(mv_nnz), s);
-  mirror_k<<<grid_for(dim), 256, 0, s>>>(colp, rowi, dim, moff, mkey, mval);
-  sort_pairs(mkey, mval, mv_nnz, 64, s);
+  const int64_t mv_nnz = 2 * nnz - static_cast<int64_t>(nd);
+  sort_pairs(mkey, mval, 2 * nnz, 64, s);
   auto* mv_col = dalloc<int64_t>(static_cast<size_t>(mv_nnz), s);
   int* rowcnt = dalloc<int>(static_cast<size_t>(dim), s);
   ck(cudaMemsetAsync(rowcnt, 0, static_cast<size_t>(dim) * sizeof(int), s), "memset");
@@ -303,7 +307,7 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   ck(cudaStreamSynchronize(s), "sync");
   for (void* p : {static_cast<void*>(key), static_cast<void*>(flag), static_cast<void*>(slot),
                   static_cast<void*>(colcnt), static_cast<void*>(colcnt64), static_cast<void*>(colp),
-                  static_cast<void*>(rowi), static_cast<void*>(mcnt), static_cast<void*>(moff),
+                  static_cast<void*>(rowi), static_cast<void*>(ndiag),
                   static_cast<void*>(mkey), static_cast<void*>(rowcnt), static_cast<void*>(rowcnt64),
                   static_cast<void*>(jkey), static_cast<void*>(jcnt), static_cast<void*>(jcnt64)})
     cudaFreeAsync(p, s);
