@@ -55,7 +55,7 @@ def parse():
                     help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
     ap.add_argument("--solve", default="quadrotor:100000",
                     help="model:N of the full IPM solve leg ('ipm_solve' key; 'none' to skip)")
-    ap.add_argument("--goddard-solve", default="100000:3",
+    ap.add_argument("--goddard-solve", default="100000:10",
                     help="N[:ref_iters] of the Goddard full device solve (BASELINE config 2, 'goddard_solve' key); the "
                          "reference runs ref_iters iterations for a per-iteration comparison; 'none' to skip")
     ap.add_argument("--batch", default="4096:500",
@@ -481,7 +481,7 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
     solve call; the device time includes the one-time NVRTC compile of the
     model's kernels (reported separately as jit_s from a second solve).
     ref_max_iter > 0 caps the reference's run (Goddard at N=1e5 needs ~N/2
-    iterations, about 64 h on the host: SURVEY.md D6); the two are then
+    iterations, hours on the host: SURVEY.md D6); the two are then
     compared per iteration."""
     from paper_2510_03932_b200 import MODELS, Model, solve
     name, N = spec.split(":")
