@@ -439,6 +439,32 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     S[q] = v;
   }
   long long npos = 0, nneg = 0, nzero = 0;
+  // compile-time shapes: each thread owns its rank-1-update pairs (j1, j2) and
+  // early border entries (t, j) in registers, so a column's update is a few
+  // shared-memory read-modify-writes with no index arithmetic or table loads
+  constexpr bool kOwned = BC > 0 && WEC >= 0;
+  constexpr int kPairs = BC > 0 ? (BC - 1) * BC / 2 : 0;
+  constexpr int kPPT = kOwned && kPairs > 0 ? (kPairs + TT - 1) / TT : 1;
+  constexpr int kWb = kOwned ? WEC * (BC - 1) : 0;
+  constexpr int kWPT = kOwned && kWb > 0 ? (kWb + TT - 1) / TT : 1;
+  int oj1[kPPT], oj2[kPPT], ot[kWPT], oj[kWPT];
+  if constexpr (kOwned) {
+#pragma unroll
+    for (int i = 0; i < kPPT; ++i) {
+      const int p = tid + i * TT;
+      oj1[i] = oj2[i] = 0;
+      if (p < kPairs) {
+        oj1[i] = pj1[p];
+        oj2[i] = pj2[p];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i) {
+      const int q = tid + i * TT;
+      ot[i] = q < kWb ? q / (BC - 1) : -1;
+      oj[i] = q < kWb ? q - (q / (BC - 1)) * (BC - 1) + 1 : 0;
+    }
+  }
   __syncthreads();
 
   int s = 0;  // slot of column k = k mod B1
@@ -474,31 +500,45 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
       border[static_cast<long long>(t) * n + k] = v * dinv;
     }
     __syncthreads();
+    if constexpr (kOwned) {
+#pragma unroll
+      for (int i = 0; i < kPPT; ++i) {
+        const int j1 = oj1[i], j2 = oj2[i];
+        if (j1 > 0 && (!late || k + j2 < n)) {
+          const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
+          const double upd = l[j2] * y[j1];
+          W[s1 * B1 + (j2 - j1)] -= upd;
+          if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
+        }
+      }
+    } else {
 #pragma unroll 4
-    for (int p = tid; p < P; p += T) {
-      const int j1 = pj1[p], j2 = pj2[p];
-      if (!late || k + j2 < n) {
-        const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
-        const double upd = l[j2] * y[j1];
-        W[s1 * B1 + (j2 - j1)] -= upd;
-        if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
+      for (int p = tid; p < P; p += T) {
+        const int j1 = pj1[p], j2 = pj2[p];
+        if (!late || k + j2 < n) {
+          const int s1 = s + j1 >= B1 ? s + j1 - B1 : s + j1;
+          const double upd = l[j2] * y[j1];
+          W[s1 * B1 + (j2 - j1)] -= upd;
+          if (j1 == j2) ps[s1] = fmax(ps[s1], fabs(upd));
+        }
       }
     }
     if (!late) {
+      if constexpr (kOwned) {
+#pragma unroll
+        for (int i = 0; i < kWPT; ++i) {
+          const int t = ot[i], j = oj[i];
+          if (t >= 0) Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
+        }
+      } else {
 #pragma unroll 4
-      for (int q = tid; q < we * b; q += T) {
-        const int t = q / b, j = q - t * b + 1;
-        Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
-      }
-#pragma unroll 4
-      for (int q = tid; q < we * we; q += T) {
-        const int t = q / we, u = q - t * we;
-        if (u <= t) {
-          const double upd = lb[t] * yb[u];
-          S[t * w + u] -= upd;
-          if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
+        for (int q = tid; q < we * b; q += T) {
+          const int t = q / b, j = q - t * b + 1;
+          Wb[t * B1 + (s + j >= B1 ? s + j - B1 : s + j)] -= lb[t] * y[j];
         }
       }
+      // the early rows' border block S is updated after the loop, from the
+      // stored border factor (one pass over the segment, not a per-column step)
     } else {
       for (int q = tid; q < w * b; q += T) {
         const int t = q / b, j = q - t * b + 1;
@@ -537,6 +577,43 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
   }
   cp_wait<0>();
   __syncthreads();
+  {
+    // deferred early updates of S: S[t][u] -= sum_k L[t][k] d_k L[u][k] over
+    // the columns k < n - b (rows t, u < we), staged through the ring's shared
+    // memory in chunks of columns
+    const long long n_early = n > b ? n - b : 0;
+    const int CH = min(32, (kPrefetch * RW) / max(1, 2 * we));
+    double* lc = ring;            // we x CH: L[t][k]
+    double* yc = ring + we * CH;  // we x CH: L[u][k] d_k
+    const int npair = we * (we + 1) / 2;
+    for (long long c0 = 0; c0 < n_early; c0 += CH) {
+      const int m = static_cast<int>(min(static_cast<long long>(CH), n_early - c0));
+      for (int e = tid; e < we * CH; e += T) {
+        const int t = e / CH, j = e - t * CH;
+        if (j < m) {
+          const double lv = border[static_cast<long long>(t) * n + c0 + j];
+          lc[e] = lv;
+          yc[e] = lv * band[(c0 + j) * B1];
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < npair; q += T) {
+        int t = static_cast<int>((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+        while ((t + 1) * (t + 2) / 2 <= q) ++t;
+        while (t * (t + 1) / 2 > q) --t;
+        const int u = q - t * (t + 1) / 2;
+        double acc = S[t * w + u], mx = 0.0;
+        for (int j = 0; j < m; ++j) {
+          const double upd = lc[t * CH + j] * yc[u * CH + j];
+          acc -= upd;
+          mx = fmax(mx, fabs(upd));
+        }
+        S[t * w + u] = acc;
+        if (t == u) Sps[t] = fmax(Sps[t], mx);
+      }
+      __syncthreads();
+    }
+  }
   if (g.finalize) {
     // dense border block: sequential LDL^T with the same pivot rule
     if (tid == 0) {
