@@ -479,7 +479,8 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
     device — against the reference's own ipm::solve (oracle/_ref/libref.so,
     Backend::parallel on all host cores, its CPU LDL^T). Wall times of the
     solve call; the device time includes the one-time NVRTC compile of the
-    model's kernels (reported separately as jit_s from a second solve).
+    model's kernels (reported separately as jit_s); device_s is the median
+    wall of three further solves, each building its plans anew.
     ref_max_iter > 0 caps the reference's run (Goddard at N=1e5 needs ~N/2
     iterations, hours on the host: SURVEY.md D6); the two are then
     compared per iteration."""
@@ -490,11 +491,15 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
     t0 = time.perf_counter()
     d = solve(m)
     t_first = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    d2 = solve(m)  # kernels now in the compile cache
-    t_second = time.perf_counter() - t0
+    walls, d2 = [], None
+    for _ in range(3):  # kernels now in the compile cache; median of three solves
+        t0 = time.perf_counter()
+        d2 = solve(m)
+        walls.append(time.perf_counter() - t0)
+    t_second = float(np.median(walls))
     out = {"model": name, "N": N, "status": d2["status_name"], "iterations": d2["iterations"],
-           "objective": d2["objective"], "device_s": t_second, "device_s_incl_jit": t_first,
+           "objective": d2["objective"], "device_s": t_second, "device_s_all": walls,
+           "device_s_incl_jit": t_first,
            "jit_s": max(0.0, t_first - t_second), "factorizations": d2["factorizations"],
            "time_factorize_s": d2["time_factorize"], "time_solve_s": d2["time_solve"],
            "time_derivatives_s": d2["time_derivatives"], "time_total_s": d2["time_total"],

@@ -144,6 +144,84 @@ void host_structure(const ocg::Nlp& nlp, std::vector<Index>* jr, std::vector<Ind
   }
 }
 
+// the same COO structure built on the device (kernels.hpp struct_fill): one
+// launch per group over its instances x pattern entries, from the groups'
+// patterns and input addresses (a few KB uploaded once). jr/jc and/or hr/hc.
+void device_structure(const ocg::Nlp& nlp, DBuf<int64_t>* jr, DBuf<int64_t>* jc, DBuf<int64_t>* hr,
+                      DBuf<int64_t>* hc, cudaStream_t s) {
+  Index nj = 0, nh = 0;
+  for (const auto& g : nlp.cons) {
+    nj += static_cast<Index>(g.pattern.jac.size()) * g.range.count();
+    nh += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  }
+  for (const auto& g : nlp.objs) nh += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  if (jr) {
+    jr->alloc(static_cast<size_t>(nj));
+    jc->alloc(static_cast<size_t>(nj));
+  }
+  if (hr) {
+    hr->alloc(static_cast<size_t>(nh));
+    hc->alloc(static_cast<size_t>(nh));
+  }
+  // flat pattern / address tables
+  std::vector<int> pat;
+  std::vector<int64_t> addr;
+  struct Pending {
+    ocg::dev::StructGroup g;
+    size_t pa, pb, ia, n_in;
+  };
+  std::vector<Pending> todo;
+  auto add = [&](const ocg::Group& g, int kind, const auto& pairs, Index off) {
+    if (pairs.empty() || g.range.count() == 0) return;
+    Pending t;
+    t.g.lo = g.range.lo;
+    t.g.hi = g.range.hi;
+    t.g.endpoints = g.range.endpoints ? 1 : 0;
+    t.g.kind = kind;
+    t.g.np = static_cast<int>(pairs.size());
+    t.g.out_dim = g.out_dim();
+    t.g.off = off;
+    t.g.row_base = g.row_base;
+    t.pa = pat.size();
+    for (const auto& pr : pairs) pat.push_back(static_cast<int>(pr.first));
+    t.pb = pat.size();
+    for (const auto& pr : pairs) pat.push_back(static_cast<int>(pr.second));
+    const auto& ins = g.kernel.graph.inputs();
+    t.ia = addr.size();
+    t.n_in = ins.size();
+    for (const auto& a : ins) addr.push_back(a.base);
+    for (const auto& a : ins) addr.push_back(a.stride);
+    todo.push_back(t);
+  };
+  Index joff = 0, hoff = 0;
+  for (const auto& g : nlp.cons) {
+    if (jr) add(g, 0, g.pattern.jac, joff);
+    if (hr) add(g, 1, g.pattern.hess, hoff);
+    joff += static_cast<Index>(g.pattern.jac.size()) * g.range.count();
+    hoff += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  }
+  for (const auto& g : nlp.objs) {
+    if (hr) add(g, 1, g.pattern.hess, hoff);
+    hoff += static_cast<Index>(g.pattern.hess.size()) * g.range.count();
+  }
+  if (todo.empty()) return;
+  DBuf<int> dpat;
+  DBuf<int64_t> daddr;
+  dpat.upload(pat);
+  daddr.upload(addr);
+  for (auto& t : todo) {
+    t.g.pa = dpat.p + t.pa;
+    t.g.pb = dpat.p + t.pb;
+    t.g.ibase = daddr.p + t.ia;
+    t.g.istride = daddr.p + t.ia + t.n_in;
+    if (t.g.kind == 0)
+      ocg::dev::struct_fill(t.g, jr->p, jc->p, s);
+    else
+      ocg::dev::struct_fill(t.g, hr->p, hc->p, s);
+  }
+  ck(cudaStreamSynchronize(s), "structure sync");
+}
+
 const char* const kKernelNames[] = {"ocg_c", "ocg_cjac", "ocg_hess", "ocg_cjh", "ocg_objv", "ocg_grad"};
 
 // per-kernel (registers, spill-store bytes) from the ptxas -v part of an NVRTC log
@@ -854,22 +932,26 @@ int ocg_eval_compute_scaling(ocg_eval* e, const double* x0, int enabled, ocg_str
   if (ocg_eval_status(e, s) != OCG_OK) return OCG_OK;  // keep unit scales
   ocg_eval_constraints_jacobian(e, x0, cd.p, s);
   if (ocg_eval_status(e, s) != OCG_OK) return OCG_OK;
-  std::vector<double> g(nv), jv(static_cast<size_t>(e->lay.jac_nnz));
-  ck(cudaMemcpy(g.data(), gd.p, nv * sizeof(double), cudaMemcpyDeviceToHost), "grad d2h");
-  if (!jv.empty()) ck(cudaMemcpy(jv.data(), e->jac.p, jv.size() * sizeof(double), cudaMemcpyDeviceToHost), "jac d2h");
+  // the max rules on the device: max|grad| and per-row max|J| (exact)
+  const cudaStream_t cs = st(s);
+  DBuf<double> gm;
+  gm.alloc(1);
+  ocg::dev::max_abs(gd.p, static_cast<int64_t>(nv), gm.p, cs);
   double gmax = 0.0;
-  for (double v : g) gmax = std::max(gmax, std::abs(v));
+  ck(cudaMemcpyAsync(&gmax, gm.p, sizeof(double), cudaMemcpyDeviceToHost, cs), "gmax d2h");
   double os = 1.0;
   if (gmax > 0.0) os = std::min(1.0, 100.0 / gmax);
-  std::vector<Index> jr, jc;
-  host_structure(nlp, &jr, &jc, nullptr, nullptr, nullptr);
-  std::vector<double> jmax(m, 0.0), rs(m, 1.0);
-  for (size_t q = 0; q < jv.size(); ++q) {
-    const auto r = static_cast<size_t>(jr[q]);
-    jmax[r] = std::max(jmax[r], std::abs(jv[q]));
-  }
-  for (size_t r = 0; r < m; ++r) rs[r] = jmax[r] > 0.0 ? std::min(1.0, 100.0 / jmax[r]) : 1.0;
-  return ocg_eval_set_scaling(e, os, rs.data());
+  DBuf<int64_t> djr, djc;
+  device_structure(nlp, &djr, &djc, nullptr, nullptr, cs);
+  DBuf<double> jmax;
+  jmax.alloc(m);
+  ck(cudaMemsetAsync(jmax.p, 0, std::max<size_t>(m, 1) * sizeof(double), cs), "memset");
+  ocg::dev::row_absmax(e->jac.p, djr.p, static_cast<int64_t>(djr.n), jmax.p, cs);
+  ocg::dev::row_scale_rule(jmax.p, static_cast<int64_t>(m), e->row_scale.p, cs);
+  ck(cudaStreamSynchronize(cs), "scaling sync");
+  e->obj_scale = os;
+  e->refresh_objw(nullptr);
+  return OCG_OK;
   OCG_GUARD_END
 }
 
@@ -937,10 +1019,10 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   K->dim = K->ntot + K->m;
 
   lap("maps");
-  std::vector<Index> jr, jc, hr, hc;
-  host_structure(nlp, &jr, &jc, &hr, &hc, nullptr);
-  K->H = static_cast<Index>(hr.size());
-  K->J = static_cast<Index>(jr.size());
+  DBuf<int64_t> dhr, dhc, djr, djc;
+  device_structure(nlp, &djr, &djc, &dhr, &dhc, cudaStreamPerThread);
+  K->H = static_cast<Index>(dhr.n);
+  K->J = static_cast<Index>(djr.n);
   lap("structure");
   // pattern, assembly sources, matvec CSR and J^T lambda gather: sorted on
   // the device (kktbuild.cu); sources keep the reference's accumulation order
@@ -948,11 +1030,7 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     std::vector<int64_t> sd(static_cast<size_t>(K->n_slack));
     for (Index k = 0; k < K->n_slack; ++k)
       sd[static_cast<size_t>(k)] = K->dual_index[static_cast<size_t>(K->slack_of[static_cast<size_t>(k)])];
-    DBuf<int64_t> dhr, dhc, djr, djc, dprim, ddual;
-    dhr.upload(hr);
-    dhc.upload(hc);
-    djr.upload(jr);
-    djc.upload(jc);
+    DBuf<int64_t> dprim, ddual;
     dprim.upload(K->prim_index);
     ddual.upload(K->dual_index);
     K->jt_slack_dual.upload(sd);
@@ -1116,13 +1194,19 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
   for (const auto& sl : nlp.slabs)
     if (sl.nodes > 1)
       for (Index q = 0; q < sl.dim * sl.nodes; ++q) slot_node[static_cast<size_t>(sl.base + q)] = q / sl.dim;
-  std::vector<Index> jr, jc;
-  host_structure(nlp, &jr, &jc, nullptr, nullptr, nullptr);
   std::vector<Index> row_node(static_cast<size_t>(nlp.m_con), -1);
-  for (size_t q = 0; q < jr.size(); ++q) {
-    const Index nd = slot_node[static_cast<size_t>(jc[q])];
-    auto& rn = row_node[static_cast<size_t>(jr[q])];
-    rn = std::max(rn, nd);
+  {
+    DBuf<int64_t> djr, djc, dsn, drn;
+    device_structure(nlp, &djr, &djc, nullptr, nullptr, cudaStreamPerThread);
+    dsn.upload(slot_node);
+    drn.alloc(row_node.size());
+    ocg::dev::row_max_node(djr.p, djc.p, static_cast<int64_t>(djr.n), dsn.p, static_cast<int64_t>(row_node.size()),
+                           drn.p, cudaStreamPerThread);
+    if (!row_node.empty())
+      ck(cudaMemcpyAsync(row_node.data(), drn.p, row_node.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                         cudaStreamPerThread),
+         "row_node d2h");
+    ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
   }
   std::vector<int64_t> node(static_cast<size_t>(k->dim), -1);
   for (Index i = 0; i < k->n_free; ++i) node[static_cast<size_t>(i)] = slot_node[static_cast<size_t>(k->free_slot[static_cast<size_t>(i)])];

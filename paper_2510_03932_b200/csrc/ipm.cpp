@@ -142,6 +142,7 @@ class DeviceSolver {
   double mu_ = 0.1, tau_ = 0.99, delta_last_ = 0.0, obj_scale_ = 1.0;
   // OCG_TIMING diagnostics: solves, refinement rounds, line-search trials
   long long n_solves_ = 0, n_refine_ = 0, n_trials_ = 0;
+  double t_err_ = 0, t_assemble_ = 0, t_pre_ = 0, t_search_ = 0, t_accept_ = 0;
   double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
   double theta_min_ = 0.0, theta_max_ = kInf;
   std::vector<std::pair<double, double>> filter_;
@@ -258,6 +259,13 @@ void DeviceSolver::alloc_state(size_t nv, size_t mc) {
 }
 
 void DeviceSolver::setup(std::vector<double>& row_scale) {
+  static const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  Clock lapc;
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    std::fprintf(stderr, "[ipm setup] %-18s %8.3f s\n", what, lapc.elapsed());
+    lapc = Clock();
+  };
   nvar_ = ocg_model_nvar(model_);
   mcon_ = ocg_model_mcon(model_);
   int64_t d[7];
@@ -310,6 +318,7 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
     if (dual[r] >= 0) dual_row[static_cast<size_t>(dual[r])] = static_cast<int64_t>(r);
   }
 
+  lap("arrays + maps");
   // EvalContext::compute_scaling at x_start (solver.cpp:318)
   DVec<double> xs(nv);
   xs.upload(x0, s_);
@@ -317,6 +326,7 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   row_scale.assign(mc, 1.0);
   cko(ocg_eval_get_scaling(ev_, &obj_scale_, row_scale.data()), "get_scaling");
 
+  lap("scaling");
   // Solver::setup_bounds (solver.cpp:125-170)
   std::vector<double> lcon_s(mc), ucon_s(mc);
   for (size_t r = 0; r < mc; ++r) {
@@ -371,11 +381,13 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
     x[sl] = push_into(x[sl], lb[static_cast<size_t>(i)], ub[static_cast<size_t>(i)]);
   }
 
+  lap("bounds + start");
   // device state (allocated on the first run, reused by later instances)
   if (!allocated_) {
     allocated_ = true;
     alloc_state(nv, mc);
   }
+  lap("alloc state");
   free_slot_.upload(free_slot, s_);
   dual_row_.upload(dual_row, s_);
   slack_index_.upload(slack, s_);
@@ -400,6 +412,7 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   P_.lcon_s = lcon_s_.p;
   x_->upload(x, s_);
 
+  lap("uploads");
   // slacks from the constraint values at the start point, multipliers
   std::vector<double> c;
   eval_c(x_->p, c_->p);
@@ -422,6 +435,7 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   zu_.upload(zu, s_);
   ckc(cudaMemsetAsync(lambda_.p, 0, std::max<size_t>(static_cast<size_t>(m_), 1) * sizeof(double), s_), "memset");
   ckc(cudaStreamSynchronize(s_), "sync");
+  lap("slacks + duals");
 }
 
 // Solver::kkt_error (solver.cpp:260-287)
@@ -596,6 +610,11 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
                    "refinement rounds), derivatives %.3f s, %lld line-search trials\n",
                    iter, r_.time_total, r_.time_factorize, r_.factorizations, r_.time_solve, n_solves_, n_refine_,
                    r_.time_derivatives, n_trials_);
+    if (std::getenv("OCG_TIMING"))
+      std::fprintf(stderr,
+                   "[ipm] phases: kkt error + mu %.3f s, H + assembly + rhs %.3f s, step stats %.3f s, line search "
+                   "%.3f s, accept %.3f s\n",
+                   t_err_, t_assemble_, t_pre_, t_search_, t_accept_);
   };
   if (!eval_cj(x_->p, c_->p) || !eval_grad(x_->p, grad_->p)) {
     done(3, 0);
@@ -610,6 +629,11 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
   int consecutive_restorations = 0;
   bool hold_mu = false;
   for (int iter = 0;; ++iter) {
+    Clock ph;
+    auto mark = [&](double& acc) {
+      acc += ph.elapsed();
+      ph = Clock();
+    };
     cko(ocg_kkt_jt_lambda(kkt_, lambda_.p, jtlam_.p, s_), "jt_lambda");
     double comp = 0.0, stat = 0.0;
     const double e0 = kkt_error(0.0, g_.p, comp, stat);
@@ -629,6 +653,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
         filter_.clear();
       }
     }
+    mark(t_err_);
     ocg::ipmdev::expand_lambda(P_, lambda_.p, lamfull_.p, s_);
     if (!eval_h(x_->p, lamfull_.p)) {
       done(3, iter);
@@ -637,11 +662,14 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     ocg::ipmdev::sigma(P_, x_->p, s_v_->p, zl_.p, zu_.p, sigma_.p, s_);
     cko(ocg_kkt_assemble(kkt_, sigma_.p, s_), "kkt_assemble");
     ocg::ipmdev::rhs(P_, x_->p, s_v_->p, grad_->p, jtlam_.p, g_.p, mu_, rhs_.p, s_);
+    const double wmax = max_abs_h();
+    mark(t_assemble_);
     bool numeric_failure = false;
-    if (!solve_kkt(max_abs_h(), numeric_failure)) {
+    if (!solve_kkt(wmax, numeric_failure)) {
       done(3, iter);
       return OCG_OK;
     }
+    ph = Clock();
     const double alpha_max = ocg::ipmdev::fraction_to_boundary(P_, x_->p, s_v_->p, step_.p, tau_, sc_, s_);
     const double dphi = ocg::ipmdev::dphi(P_, x_->p, s_v_->p, grad_->p, step_.p, mu_, sc_, s_);
     const double theta_k = theta_of(g_.p);
@@ -655,6 +683,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
       phi_k = f_k - mu_ * bar;
     }
 
+    mark(t_pre_);
     double alpha = alpha_max;
     bool accepted = false, armijo_path = false, saw_eval_error = false;
     double theta_t = 0.0, phi_t = 0.0;
@@ -759,6 +788,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
       ocg::ipmdev::residual(P_, c_->p, s_v_->p, g_.p, s_);
       continue;
     }
+    mark(t_search_);
     consecutive_restorations = 0;
     hold_mu = false;
     if (!armijo_path) add_to_filter(theta_k, phi_k);
@@ -779,6 +809,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
       std::printf("iter %4d  f %+.8e  theta %.3e  mu %.2e  alpha %.2e  alpha_z %.2e  delta_w %.1e\n", iter + 1,
                   f_raw / obj_scale_, theta_of(g_.p), mu_, alpha, alpha_z, delta_last_);
     }
+    mark(t_accept_);
   }
 }
 

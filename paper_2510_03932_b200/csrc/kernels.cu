@@ -426,3 +426,88 @@ std::vector<int64_t> long_rows(const std::vector<int64_t>& ptr) {
 }
 
 }  // namespace ocg::dev
+
+namespace ocg::dev {
+
+namespace {
+
+__global__ void struct_fill_k(StructGroup g, int64_t* __restrict__ a, int64_t* __restrict__ b) {
+  const int64_t cnt = g.endpoints ? (g.lo == g.hi ? 1 : 2) : g.hi - g.lo;
+  const int64_t total = cnt * g.np;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = e / g.np;
+    const int p = static_cast<int>(e - k * g.np);
+    const int64_t idx = g.endpoints ? (k == 0 ? g.lo : g.hi) : g.lo + k;
+    const int ib = g.pb[p];
+    const int64_t sb = g.ibase[ib] + g.istride[ib] * idx;
+    if (g.kind == 0) {
+      a[g.off + e] = g.row_base + k * g.out_dim + g.pa[p];
+      b[g.off + e] = sb;
+    } else if (g.kind == 1) {
+      const int ia = g.pa[p];
+      const int64_t sa = g.ibase[ia] + g.istride[ia] * idx;
+      a[g.off + e] = sa > sb ? sa : sb;
+      b[g.off + e] = sa > sb ? sb : sa;
+    } else {
+      a[g.off + e] = sb;
+    }
+  }
+}
+
+__global__ void row_absmax_k(const double* __restrict__ v, const int64_t* __restrict__ row, int64_t n,
+                             unsigned long long* __restrict__ out) {
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicMax(out + row[q], static_cast<unsigned long long>(__double_as_longlong(fabs(v[q]))));
+}
+
+__global__ void row_scale_rule_k(const double* __restrict__ jmax, int64_t m, double* __restrict__ rs) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    rs[r] = jmax[r] > 0.0 ? fmin(1.0, 100.0 / jmax[r]) : 1.0;
+}
+
+__global__ void row_max_node_k(const int64_t* __restrict__ row, const int64_t* __restrict__ col, int64_t n,
+                               const int64_t* __restrict__ col_node, unsigned long long* __restrict__ node1) {
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicMax(node1 + row[q], static_cast<unsigned long long>(col_node[col[q]] + 1));
+}
+
+__global__ void minus_one_k(unsigned long long* __restrict__ v, int64_t m) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    reinterpret_cast<int64_t*>(v)[r] = static_cast<int64_t>(v[r]) - 1;
+}
+
+int grid_n(int64_t n) {
+  const int64_t want = (n + 255) / 256, cap = 148LL * 16;
+  return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace
+
+void struct_fill(const StructGroup& g, int64_t* a, int64_t* b, cudaStream_t s) {
+  const int64_t cnt = g.endpoints ? (g.lo == g.hi ? 1 : 2) : g.hi - g.lo;
+  if (cnt * g.np <= 0) return;
+  struct_fill_k<<<grid_n(cnt * g.np), 256, 0, s>>>(g, a, b);
+}
+
+void row_absmax(const double* v, const int64_t* row, int64_t n, double* out, cudaStream_t s) {
+  if (n > 0) row_absmax_k<<<grid_n(n), 256, 0, s>>>(v, row, n, reinterpret_cast<unsigned long long*>(out));
+}
+
+void row_scale_rule(const double* jmax, int64_t m, double* rs, cudaStream_t s) {
+  if (m > 0) row_scale_rule_k<<<grid_n(m), 256, 0, s>>>(jmax, m, rs);
+}
+
+void row_max_node(const int64_t* row, const int64_t* col, int64_t n, const int64_t* col_node, int64_t m,
+                  int64_t* node, cudaStream_t s) {
+  cudaMemsetAsync(node, 0, static_cast<size_t>(m) * sizeof(int64_t), s);
+  if (n > 0)
+    row_max_node_k<<<grid_n(n), 256, 0, s>>>(row, col, n, col_node, reinterpret_cast<unsigned long long*>(node));
+  if (m > 0) minus_one_k<<<grid_n(m), 256, 0, s>>>(reinterpret_cast<unsigned long long*>(node), m);
+}
+
+}  // namespace ocg::dev

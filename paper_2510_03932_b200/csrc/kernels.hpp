@@ -80,3 +80,31 @@ void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const i
 void max_abs(const double* v, int64_t n, double* out, cudaStream_t s);
 
 }  // namespace ocg::dev
+
+namespace ocg::dev {
+
+// COO structure of one group on the device (EvalContext's materialisation,
+// eval.cpp:83-119): entry e = off + k * np + p for instance k of the group's
+// range and pattern entry p. kind 0 Jacobian: a = row + k*out_dim + pa[p],
+// b = slot(pb[p]); kind 1 Hessian: (a, b) = (max, min) of the two slots;
+// kind 2 gradient: a = slot(pb[p]) (b unused). slot(i) = ibase[i] + istride[i] * idx.
+struct StructGroup {
+  int64_t lo = 0, hi = 0;
+  int endpoints = 0, kind = 0, np = 0, out_dim = 0;
+  int64_t off = 0, row_base = 0;
+  const int* pa = nullptr;
+  const int* pb = nullptr;
+  const int64_t* ibase = nullptr;
+  const int64_t* istride = nullptr;
+};
+void struct_fill(const StructGroup& g, int64_t* a, int64_t* b, cudaStream_t s);
+
+// out[row[q]] = max(out[row[q]], |v[q]|) over q < n (out zeroed by the caller; exact)
+void row_absmax(const double* v, const int64_t* row, int64_t n, double* out, cudaStream_t s);
+// rs[r] = jmax[r] > 0 ? min(1, 100 / jmax[r]) : 1 (EvalContext::compute_scaling, eval.cpp:260-286)
+void row_scale_rule(const double* jmax, int64_t m, double* rs, cudaStream_t s);
+// node[r] = max over entries q of row r of col_node[col[q]] (-1 when none)
+void row_max_node(const int64_t* row, const int64_t* col, int64_t n, const int64_t* col_node, int64_t m,
+                  int64_t* node, cudaStream_t s);
+
+}  // namespace ocg::dev
