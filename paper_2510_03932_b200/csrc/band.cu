@@ -995,6 +995,98 @@ __global__ void scatter_back_k(const double* __restrict__ work, const int64_t* _
 // mode 0: full solve of a finalized block (forward, border block, D, backward)
 // mode 1: segment forward; border accumulations -> gparts[blk * wmax + t]
 // mode 2: segment backward with the separator system's solution as border values
+// Segment forward (mode 1) / backward (mode 2) substitution with the window
+// in registers, one entry per lane (bands with b + 1 <= 32 and at most 32
+// border rows): lane j holds entry c + j of the window, lane t < w a border
+// row; a column is a broadcast, one FMA and a shuffle (forward) or a warp sum
+// (backward) — no shared memory, no warp barriers. Column data is prefetched
+// PF columns ahead into registers. solve_k's arithmetic per entry.
+template <int PF>
+__global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict__ segs, int mode,
+                                                       const double* __restrict__ buf,
+                                                       const double* __restrict__ Dinv, double* __restrict__ work,
+                                                       double* __restrict__ gparts, int wmax,
+                                                       const int64_t* __restrict__ border_pos, long long sep_pos0) {
+  const int blk = blockIdx.x;
+  const BandSeg g = segs[blk];
+  const int lane = threadIdx.x;
+  const long long n = g.n;
+  const int B1 = g.b + 1, w = g.w;
+  const double* band = buf + g.band;
+  const double* border = buf + g.border;
+  double* v = work + g.pos;
+  const double* dinv = Dinv + g.pos;
+  const bool inb = lane < B1, inw = lane < w;
+  if (mode == 1) {
+    double Y = inb && lane < n ? v[lane] : 0.0;
+    double yb = 0.0;
+    // column c's data for this lane: L[c + lane][c], border[lane][c], v[c + B1] (lane b)
+    auto colb = [&](long long c) { return inb && lane > 0 && c < n && c + lane < n ? band[c * B1 + lane] : 0.0; };
+    auto colw = [&](long long c) { return inw && c < n ? border[static_cast<long long>(lane) * n + c] : 0.0; };
+    auto colv = [&](long long c) { return lane == B1 - 1 && c + B1 < n ? v[c + B1] : 0.0; };
+    double pb[PF], pw[PF], pv[PF];
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      pb[q] = colb(q);
+      pw[q] = colw(q);
+      pv[q] = colv(q);
+    }
+    for (long long c0 = 0; c0 < n; c0 += PF) {
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const long long c = c0 + q;
+        if (c >= n) break;
+        const double yc = __shfl_sync(0xffffffffu, Y, 0);
+        if (lane == 0) v[c] = yc;
+        Y -= pb[q] * yc;
+        yb -= pw[q] * yc;
+        double Yn = __shfl_down_sync(0xffffffffu, Y, 1);
+        if (lane == B1 - 1) Yn = pv[q];
+        Y = Yn;
+        pb[q] = colb(c + PF);
+        pw[q] = colw(c + PF);
+        pv[q] = colv(c + PF);
+      }
+    }
+    if (inw) gparts[static_cast<int64_t>(blk) * wmax + lane] = yb;
+    return;
+  }
+  // mode 2: backward with the separator system's solution as border values
+  double xb = 0.0;
+  if (inw) {
+    const int64_t q = border_pos[static_cast<int64_t>(blk) * wmax + lane];
+    xb = q >= 0 ? work[sep_pos0 + q] : 0.0;
+  }
+  double X = 0.0;  // lane j >= 1: x[c + j]
+  auto colb = [&](long long c) { return inb && lane > 0 && c >= 0 && c + lane < n ? band[c * B1 + lane] : 0.0; };
+  auto colw = [&](long long c) { return inw && c >= 0 ? border[static_cast<long long>(lane) * n + c] : 0.0; };
+  auto cold = [&](long long c) { return lane == 0 && c >= 0 ? v[c] * dinv[c] : 0.0; };
+  double pb[PF], pw[PF], pd[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    pb[q] = colb(n - 1 - q);
+    pw[q] = colw(n - 1 - q);
+    pd[q] = cold(n - 1 - q);
+  }
+  for (long long i0 = 0; i0 < n; i0 += PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const long long c = n - 1 - (i0 + q);
+      if (c < 0) break;
+      double part = pb[q] * X + pw[q] * xb;
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double xc = __shfl_sync(0xffffffffu, pd[q], 0) - part;
+      if (lane == 0) v[c] = xc;
+      double Xn = __shfl_up_sync(0xffffffffu, X, 1);
+      if (lane == 1) Xn = xc;
+      X = Xn;
+      pb[q] = colb(c - PF);
+      pw[q] = colw(c - PF);
+      pd[q] = cold(c - PF);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, int seg0, int mode,
                                               const double* __restrict__ buf, const double* __restrict__ Dinv,
                                               double* __restrict__ work, double* __restrict__ gparts, int wmax,
@@ -1396,7 +1488,12 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
   } else {
     const BandSeg& sep = P.segs.back();
     if (timing) cudaEventRecord(ev[1], s);
-    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    const bool regwin = P.b + 1 <= 32 && P.wmax <= 32;
+    if (regwin)
+      solve_seg_warp_k<16><<<P.nseg, 32, 0, s>>>(D.segs, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    else
+      solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
+                                               BandBatch{});
     if (timing) cudaEventRecord(ev[2], s);
     for (int par = 0; par < 2; ++par)
       rhs_add_k<<<grid_for(((P.nseg + 1) / 2) * P.wmax), 256, 0, s>>>(P.nseg, par, P.wmax, sep.n, D.border_pos,
@@ -1409,7 +1506,11 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
       solve_k<<<1, 32, P.smem_solve, s>>>(D.segs, P.nseg, 0, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
                                           BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
-    solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos, BandBatch{});
+    if (regwin)
+      solve_seg_warp_k<16><<<P.nseg, 32, 0, s>>>(D.segs, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+    else
+      solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
+                                               BandBatch{});
   }
   scatter_back_k<<<grid_for(dim), 256, 0, s>>>(work, D.perm, dim, x, BandBatch{});
   if (timing) {
