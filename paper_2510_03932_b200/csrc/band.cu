@@ -996,12 +996,13 @@ __global__ void scatter_back_k(const double* __restrict__ work, const int64_t* _
 // mode 1: segment forward; border accumulations -> gparts[blk * wmax + t]
 // mode 2: segment backward with the separator system's solution as border values
 // Segment forward (mode 1) / backward (mode 2) substitution with the window
-// in registers, one entry per lane (bands with b + 1 <= 32 and at most 32
-// border rows): lane j holds entry c + j of the window, lane t < w a border
-// row; a column is a broadcast, one FMA and a shuffle (forward) or a warp sum
+// in registers: lane j holds window entries j, j + 32, ... (NW per lane) and
+// border rows lane, lane + 32, ... (NBW per lane); a column is a broadcast,
+// one FMA per held entry and a shuffle shift (forward) or a warp sum
 // (backward) — no shared memory, no warp barriers. Column data is prefetched
-// PF columns ahead into registers. solve_k's arithmetic per entry.
-template <int PF>
+// PF columns ahead into registers. solve_k's arithmetic per entry (the
+// backward's warp sum groups the terms differently).
+template <int PF, int NW, int NBW>
 __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict__ segs, int mode,
                                                        const double* __restrict__ buf,
                                                        const double* __restrict__ Dinv, double* __restrict__ work,
@@ -1016,19 +1017,32 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
   const double* border = buf + g.border;
   double* v = work + g.pos;
   const double* dinv = Dinv + g.pos;
-  const bool inb = lane < B1, inw = lane < w;
+  const int last = B1 - 1;  // window entry that takes the incoming value
+  auto colb = [&](long long c, int r) {
+    const int e = lane + 32 * r;
+    return e > 0 && e < B1 && c >= 0 && c < n && c + e < n ? band[c * B1 + e] : 0.0;
+  };
+  auto colw = [&](long long c, int r) {
+    const int t = lane + 32 * r;
+    return t < w && c >= 0 && c < n ? border[static_cast<long long>(t) * n + c] : 0.0;
+  };
   if (mode == 1) {
-    double Y = inb && lane < n ? v[lane] : 0.0;
-    double yb = 0.0;
-    // column c's data for this lane: L[c + lane][c], border[lane][c], v[c + B1] (lane b)
-    auto colb = [&](long long c) { return inb && lane > 0 && c < n && c + lane < n ? band[c * B1 + lane] : 0.0; };
-    auto colw = [&](long long c) { return inw && c < n ? border[static_cast<long long>(lane) * n + c] : 0.0; };
-    auto colv = [&](long long c) { return lane == B1 - 1 && c + B1 < n ? v[c + B1] : 0.0; };
-    double pb[PF], pw[PF], pv[PF];
+    double Y[NW], yb[NBW];
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int e = lane + 32 * r;
+      Y[r] = e < B1 && e < n ? v[e] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < NBW; ++r) yb[r] = 0.0;
+    auto colv = [&](long long c) { return lane == last % 32 && c + B1 < n ? v[c + B1] : 0.0; };
+    double pb[PF][NW], pw[PF][NBW], pv[PF];
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      pb[q] = colb(q);
-      pw[q] = colw(q);
+#pragma unroll
+      for (int r = 0; r < NW; ++r) pb[q][r] = colb(q, r);
+#pragma unroll
+      for (int r = 0; r < NBW; ++r) pw[q][r] = colw(q, r);
       pv[q] = colv(q);
     }
     for (long long c0 = 0; c0 < n; c0 += PF) {
@@ -1036,36 +1050,56 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
       for (int q = 0; q < PF; ++q) {
         const long long c = c0 + q;
         if (c >= n) break;
-        const double yc = __shfl_sync(0xffffffffu, Y, 0);
+        const double yc = __shfl_sync(0xffffffffu, Y[0], 0);
         if (lane == 0) v[c] = yc;
-        Y -= pb[q] * yc;
-        yb -= pw[q] * yc;
-        double Yn = __shfl_down_sync(0xffffffffu, Y, 1);
-        if (lane == B1 - 1) Yn = pv[q];
-        Y = Yn;
-        pb[q] = colb(c + PF);
-        pw[q] = colw(c + PF);
+#pragma unroll
+        for (int r = 0; r < NW; ++r) Y[r] -= pb[q][r] * yc;
+#pragma unroll
+        for (int r = 0; r < NBW; ++r) yb[r] -= pw[q][r] * yc;
+        // shift: entry e takes entry e + 1; entry B1 - 1 takes v[c + B1]
+#pragma unroll
+        for (int r = 0; r < NW; ++r) {
+          double dn = __shfl_down_sync(0xffffffffu, Y[r], 1);
+          if (r + 1 < NW) {
+            const double nx = __shfl_sync(0xffffffffu, Y[r + 1 < NW ? r + 1 : r], 0);
+            if (lane == 31) dn = nx;
+          }
+          if (r == last / 32 && lane == last % 32) dn = pv[q];
+          Y[r] = dn;
+        }
+#pragma unroll
+        for (int r = 0; r < NW; ++r) pb[q][r] = colb(c + PF, r);
+#pragma unroll
+        for (int r = 0; r < NBW; ++r) pw[q][r] = colw(c + PF, r);
         pv[q] = colv(c + PF);
       }
     }
-    if (inw) gparts[static_cast<int64_t>(blk) * wmax + lane] = yb;
+#pragma unroll
+    for (int r = 0; r < NBW; ++r)
+      if (lane + 32 * r < w) gparts[static_cast<int64_t>(blk) * wmax + lane + 32 * r] = yb[r];
     return;
   }
   // mode 2: backward with the separator system's solution as border values
-  double xb = 0.0;
-  if (inw) {
-    const int64_t q = border_pos[static_cast<int64_t>(blk) * wmax + lane];
-    xb = q >= 0 ? work[sep_pos0 + q] : 0.0;
+  double xb[NBW], X[NW];
+#pragma unroll
+  for (int r = 0; r < NBW; ++r) {
+    const int t = lane + 32 * r;
+    xb[r] = 0.0;
+    if (t < w) {
+      const int64_t q = border_pos[static_cast<int64_t>(blk) * wmax + t];
+      xb[r] = q >= 0 ? work[sep_pos0 + q] : 0.0;
+    }
   }
-  double X = 0.0;  // lane j >= 1: x[c + j]
-  auto colb = [&](long long c) { return inb && lane > 0 && c >= 0 && c + lane < n ? band[c * B1 + lane] : 0.0; };
-  auto colw = [&](long long c) { return inw && c >= 0 ? border[static_cast<long long>(lane) * n + c] : 0.0; };
+#pragma unroll
+  for (int r = 0; r < NW; ++r) X[r] = 0.0;  // entry e >= 1: x[c + e]
   auto cold = [&](long long c) { return lane == 0 && c >= 0 ? v[c] * dinv[c] : 0.0; };
-  double pb[PF], pw[PF], pd[PF];
+  double pb[PF][NW], pw[PF][NBW], pd[PF];
 #pragma unroll
   for (int q = 0; q < PF; ++q) {
-    pb[q] = colb(n - 1 - q);
-    pw[q] = colw(n - 1 - q);
+#pragma unroll
+    for (int r = 0; r < NW; ++r) pb[q][r] = colb(n - 1 - q, r);
+#pragma unroll
+    for (int r = 0; r < NBW; ++r) pw[q][r] = colw(n - 1 - q, r);
     pd[q] = cold(n - 1 - q);
   }
   for (long long i0 = 0; i0 < n; i0 += PF) {
@@ -1073,18 +1107,42 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
     for (int q = 0; q < PF; ++q) {
       const long long c = n - 1 - (i0 + q);
       if (c < 0) break;
-      double part = pb[q] * X + pw[q] * xb;
+      double part = 0.0;
+#pragma unroll
+      for (int r = 0; r < NW; ++r) part += pb[q][r] * X[r];
+#pragma unroll
+      for (int r = 0; r < NBW; ++r) part += pw[q][r] * xb[r];
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       const double xc = __shfl_sync(0xffffffffu, pd[q], 0) - part;
       if (lane == 0) v[c] = xc;
-      double Xn = __shfl_up_sync(0xffffffffu, X, 1);
-      if (lane == 1) Xn = xc;
-      X = Xn;
-      pb[q] = colb(c - PF);
-      pw[q] = colw(c - PF);
+      // shift: entry e takes entry e - 1; entry 1 takes x_c
+#pragma unroll
+      for (int r = NW - 1; r >= 0; --r) {
+        double up = __shfl_up_sync(0xffffffffu, X[r], 1);
+        if (r > 0) {
+          const double pr = __shfl_sync(0xffffffffu, X[r > 0 ? r - 1 : 0], 31);
+          if (lane == 0) up = pr;
+        }
+        if (r == 0 && lane == 1) up = xc;
+        X[r] = up;
+      }
+#pragma unroll
+      for (int r = 0; r < NW; ++r) pb[q][r] = colb(c - PF, r);
+#pragma unroll
+      for (int r = 0; r < NBW; ++r) pw[q][r] = colw(c - PF, r);
       pd[q] = cold(c - PF);
     }
   }
+}
+
+using SolveSegKernel = void (*)(const BandSeg*, int, const double*, const double*, double*, double*, int,
+                                const int64_t*, long long);
+
+SolveSegKernel solve_seg_kernel_for(int B1, int w) {
+  if (B1 <= 32 && w <= 32) return solve_seg_warp_k<16, 1, 1>;
+  if (B1 <= 32 && w <= 64) return solve_seg_warp_k<8, 1, 2>;
+  if (B1 <= 64 && w <= 96) return solve_seg_warp_k<8, 2, 3>;
+  return nullptr;
 }
 
 __global__ void __launch_bounds__(32) solve_k(const BandSeg* __restrict__ segs, int seg0, int mode,
@@ -1488,9 +1546,9 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
   } else {
     const BandSeg& sep = P.segs.back();
     if (timing) cudaEventRecord(ev[1], s);
-    const bool regwin = P.b + 1 <= 32 && P.wmax <= 32;
+    const SolveSegKernel regwin = solve_seg_kernel_for(P.b + 1, P.wmax);
     if (regwin)
-      solve_seg_warp_k<16><<<P.nseg, 32, 0, s>>>(D.segs, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+      regwin<<<P.nseg, 32, 0, s>>>(D.segs, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
     else
       solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 1, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
                                                BandBatch{});
@@ -1507,7 +1565,7 @@ void band_solve(const BandPlan& P, const BandDev& D, const double* buf, const do
                                           BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
     if (regwin)
-      solve_seg_warp_k<16><<<P.nseg, 32, 0, s>>>(D.segs, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
+      regwin<<<P.nseg, 32, 0, s>>>(D.segs, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos);
     else
       solve_k<<<P.nseg, 32, P.smem_solve, s>>>(D.segs, 0, 2, buf, Dinv, work, gparts, P.wmax, D.border_pos, sep.pos,
                                                BandBatch{});
