@@ -658,9 +658,13 @@ using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, doubl
 // instantiations for the blocks of the shipped models (segment: b + 1,
 // 2b + wg, b + wg, many blocks of 256 threads; separator system: 2b, wg, wg,
 // one block of 1024 threads), else the generic kernels
-FactorKernel factor_kernel_for(int B1, int w, int we, bool single) {
+FactorKernel factor_kernel_for(int B1, int w, int we, bool single, int threads = 256) {
 #define OCG_FK(a, c, e, t) \
-  if (B1 == (a) && w == (c) && we == (e) && single == ((t) == 1024)) return factor_k<a, c, e, t>;
+  if (B1 == (a) && w == (c) && we == (e) && single == ((t) == 1024) && (single || threads == (t))) \
+    return factor_k<a, c, e, t>;
+  OCG_FK(9, 16, 8, 128)    // small bands: 128-thread segment blocks (fewer warps per barrier)
+  OCG_FK(13, 25, 13, 128)
+  OCG_FK(17, 32, 16, 128)
   OCG_FK(9, 16, 8, 256)    // double integrator (b 8, wg 0)
   OCG_FK(16, 0, 0, 1024)
   OCG_FK(13, 25, 13, 256)  // Goddard (b 12, wg 1)
@@ -1481,10 +1485,12 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   // many segments: 256-thread blocks, two per SM; a single sequential block
   // (the separator system, or an unpartitioned band): 1024 threads
   const BandSeg& s0 = P.segs[0];
-  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, P.nseg == 1);
+  static const int env_threads = std::getenv("OCG_SEG_THREADS") ? std::atoi(std::getenv("OCG_SEG_THREADS")) : 0;
+  const int seg_threads = env_threads > 0 ? env_threads : (s0.b <= 16 ? 128 : kFactorThreads);
+  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, P.nseg == 1, seg_threads);
   const FactorKernel fsep =
       P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true) : fseg;
-  const int tseg = P.nseg == 1 ? 1024 : kFactorThreads;
+  const int tseg = P.nseg == 1 ? 1024 : seg_threads;
   if (P.smem_factor > 48 * 1024)
     for (FactorKernel f : {fseg, fsep})
       cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
