@@ -25,9 +25,12 @@ def _setup(name, N, seed=20250808):
     return m, ec, KktAssembler(m, ec), RefKkt(re)
 
 
-@pytest.mark.parametrize("name", ["double_integrator", "goddard", "quadrotor", "hang_glider", "shuttle"])
-def test_kkt_pattern_and_assembly(name):
-    m, ec, k, kr = _setup(name, 150)
+@pytest.mark.parametrize("name,N", [("double_integrator", 150), ("goddard", 150), ("quadrotor", 150),
+                                    ("hang_glider", 150), ("shuttle", 150),
+                                    # the free final time's rows gather > 1024 terms: one-block long-row kernels
+                                    ("goddard", 1500), ("hang_glider", 1500)])
+def test_kkt_pattern_and_assembly(name, N):
+    m, ec, k, kr = _setup(name, N)
     assert (k.dim, k.nnz, k.n_free, k.n_slack, k.m) == (kr.dim, kr.nnz, kr.n_free, kr.n_slack, kr.m)
     pa, pr = k.pattern(), kr.pattern()
     assert np.array_equal(pa[0], pr[0]) and np.array_equal(pa[1], pr[1])
@@ -40,6 +43,16 @@ def test_kkt_pattern_and_assembly(name):
     assert_close(val, kr.assemble(sigma), "K.val")
     xv = np.random.default_rng(4).standard_normal(k.dim)
     assert_close(k.matvec(xv).cpu().numpy(), kr.matvec(val, xv), "K x")
+    # J^T lambda (Solver::compute_jt_lambda, solver.cpp:244-257) against numpy
+    st = ec.structure()
+    jr, jc, jv = st["jac_row"], st["jac_col"], ec.jac_val.cpu().numpy()
+    lam = np.random.default_rng(7).standard_normal(k.m)
+    ref = np.zeros(k.ntot)
+    use = (ma["prim_index"][jc] >= 0) & (ma["dual_index"][jr] >= 0)
+    np.add.at(ref, ma["prim_index"][jc[use]], jv[use] * lam[ma["dual_index"][jr[use]]])
+    srow = np.nonzero(ma["slack_index"] >= 0)[0]
+    ref[k.n_free + ma["slack_index"][srow]] -= lam[ma["dual_index"][srow]]
+    assert_close(k.jt_lambda(lam).cpu().numpy(), ref, "J^T lambda")
 
 
 def _dense(k, val, dw, dc):
