@@ -31,11 +31,13 @@ namespace ocg {
 
 namespace {
 
-size_t factor_smem(int b, int w) {
+// factor_k's shared memory for a block of bandwidth b and w border rows with
+// a kp-column prefetch ring; `owned`: compile-time shape (no pair table)
+size_t factor_smem(int b, int w, int kp = 32, bool owned = false) {
   const size_t B1 = static_cast<size_t>(b) + 1, W = static_cast<size_t>(w);
-  constexpr size_t kPre = 32;
-  const size_t pairs = static_cast<size_t>(b) * (b + 1) / 2;
-  return sizeof(double) * (B1 * B1 + B1 + W * B1 + W * W + W + 2 * B1 + 2 * W + kPre * (B1 + W + 2)) +
+  const size_t pairs = owned ? 0 : static_cast<size_t>(b) * (b + 1) / 2;
+  return sizeof(double) * (B1 * B1 + B1 + W * B1 + W * (W + 1) / 2 + W + 2 * B1 + 2 * W +
+                           static_cast<size_t>(kp) * (B1 + W + 2)) +
          sizeof(short) * 2 * pairs + 64;
 }
 size_t solve_smem(int b, int w) {
@@ -92,7 +94,10 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   P.b = static_cast<int>(b);
   P.wg = static_cast<int>(wg);
 
-  // partition: P segments of >= 8b interior columns separated by b-wide separators
+  // partition: P segments of >= 8b interior columns separated by b-wide
+  // separators. Default: two segment blocks per SM, three for the deep bands
+  // whose factor blocks are sized to fit three (b >= 32: 72 KB at quadrotor's)
+  if (target_segments <= 0) target_segments = b >= 32 ? 3 * 148 : 2 * 148;
   int64_t nseg = std::min<int64_t>(target_segments, n / std::max<int64_t>(1, 8 * b));
   if (nseg < 2) nseg = 1;
   P.nseg = static_cast<int>(nseg);
@@ -361,6 +366,11 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     }
   }
   constexpr int T = TT;
+  // compile-time shapes: deep windows prefetch 16 columns (shared memory for 3
+  // blocks per SM), and the update pairs live in registers, not a table
+  constexpr bool kOwned = BC > 0 && WEC >= 0;
+  constexpr int KP = (BC > 0 && WC >= 0 && BC + WC > 96) ? 16 : kPrefetch;
+  constexpr int KM = KP - 1;
   const int tid = threadIdx.x;
   const long long n = g.n;
   const int B1 = BC > 0 ? BC : g.b + 1;
@@ -370,15 +380,15 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
   double* W = sm;                 // B1 * B1 (slot-major)
   double* ps = W + B1 * B1;       // B1
   double* Wb = ps + B1;           // w * B1
-  double* S = Wb + w * B1;        // w * w
-  double* Sps = S + w * w;        // w
+  double* S = Wb + w * B1;        // w (w + 1) / 2: lower triangle, row-packed
+  double* Sps = S + w * (w + 1) / 2;  // w
   double* y = Sps + w;            // B1
   double* l = y + B1;             // B1
   double* yb = l + B1;            // w
   double* lb = yb + w;            // w
-  double* ring = lb + w;          // kPrefetch * RW
+  double* ring = lb + w;          // KP * RW
   const int RW = B1 + w + 2;      // ring row: band column, its border entries, regularization flag, pivot-scale seed
-  short* pj1 = reinterpret_cast<short*>(ring + kPrefetch * RW);
+  short* pj1 = reinterpret_cast<short*>(ring + KP * RW);  // pair table (generic shapes only)
   const int P = b * (b + 1) / 2;
   short* pj2 = pj1 + P;
   double* band = buf + g.band;
@@ -388,15 +398,17 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
   const double* flag = primal + g.pos;
   double* dinvp = Dinv + g.pos;
 
-  for (int p = tid; p < P; p += T) {  // pairs j1 <= j2 in 1..b
-    int j1 = 1, rem = p;
-    while (rem >= b - j1 + 1) {
-      rem -= b - j1 + 1;
-      ++j1;
+  auto sidx = [](int t, int u) { return t * (t + 1) / 2 + u; };  // packed lower S
+  if constexpr (!kOwned)
+    for (int p = tid; p < P; p += T) {  // pairs j1 <= j2 in 1..b
+      int j1 = 1, rem = p;
+      while (rem >= b - j1 + 1) {
+        rem -= b - j1 + 1;
+        ++j1;
+      }
+      pj1[p] = static_cast<short>(j1);
+      pj2[p] = static_cast<short>(j1 + rem);
     }
-    pj1[p] = static_cast<short>(j1);
-    pj2[p] = static_cast<short>(j1 + rem);
-  }
   auto delta_of = [&](double f) { return f != 0.0 ? dw : -dc; };
   auto fetch = [&](long long c, int r) {  // column c -> ring row r (async)
     double* dstp = ring + r * RW;
@@ -425,24 +437,24 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     }
     for (int t = tid; t < w; t += T) Wb[t * B1 + c] = border[static_cast<long long>(t) * n + c];
   }
-  for (int r = 0; r < kPrefetch; ++r) {
+  for (int r = 0; r < KP; ++r) {
     if (B1 + r < n) fetch(B1 + r, r);
     cp_commit();
   }
   for (int q = tid; q < w * w; q += T) {
     const int t = q / w, u = q % w;
+    if (u > t) continue;
     double v = Sg[q];
     if (t == u) {
       if (g.finalize) v += delta_of(primal[g.bpos + t]);
       Sps[t] = fmax(fabs(v), ps0[n + t]);
     }
-    S[q] = v;
+    S[sidx(t, u)] = v;
   }
   long long npos = 0, nneg = 0, nzero = 0;
   // compile-time shapes: each thread owns its rank-1-update pairs (j1, j2) and
   // early border entries (t, j) in registers, so a column's update is a few
   // shared-memory read-modify-writes with no index arithmetic or table loads
-  constexpr bool kOwned = BC > 0 && WEC >= 0;
   constexpr int kPairs = BC > 0 ? (BC - 1) * BC / 2 : 0;
   constexpr int kPPT = kOwned && kPairs > 0 ? (kPairs + TT - 1) / TT : 1;
   constexpr int kWb = kOwned ? WEC * (BC - 1) : 0;
@@ -454,8 +466,13 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
       const int p = tid + i * TT;
       oj1[i] = oj2[i] = 0;
       if (p < kPairs) {
-        oj1[i] = pj1[p];
-        oj2[i] = pj2[p];
+        int j1 = 1, rem = p;
+        while (rem >= (BC - 1) - j1 + 1) {
+          rem -= (BC - 1) - j1 + 1;
+          ++j1;
+        }
+        oj1[i] = j1;
+        oj2[i] = j1 + rem;
       }
     }
 #pragma unroll
@@ -548,17 +565,17 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
         const int t = q / w, u = q - t * w;
         if (u <= t) {
           const double upd = lb[t] * yb[u];
-          S[t * w + u] -= upd;
+          S[sidx(t, u)] -= upd;
           if (t == u) Sps[t] = fmax(Sps[t], fabs(upd));
         }
       }
     }
     // column k is final: its slot takes column k + B1 from the prefetch ring
-    cp_wait<kPrefetch - 1>();
+    cp_wait<KP - 1>();
     __syncthreads();
     const long long cin = k + B1;
     if (cin < n) {
-      const double* src = ring + static_cast<int>(k & kMask) * RW;
+      const double* src = ring + static_cast<int>(k & KM) * RW;
 #pragma unroll
       for (int j = tid; j < B1; j += T) {
         double v = src[j];
@@ -572,7 +589,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
       for (int t = tid; t < w; t += T) Wb[t * B1 + s] = src[B1 + t];
     }
     __syncthreads();
-    if (cin + kPrefetch < n) fetch(cin + kPrefetch, static_cast<int>(k & kMask));
+    if (cin + KP < n) fetch(cin + KP, static_cast<int>(k & KM));
     cp_commit();
   }
   cp_wait<0>();
@@ -582,7 +599,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     // the columns k < n - b (rows t, u < we), staged through the ring's shared
     // memory in chunks of columns
     const long long n_early = n > b ? n - b : 0;
-    const int CH = min(32, (kPrefetch * RW) / max(1, 2 * we));
+    const int CH = min(32, (KP * RW) / max(1, 2 * we));
     double* lc = ring;            // we x CH: L[t][k]
     double* yc = ring + we * CH;  // we x CH: L[u][k] d_k
     const int npair = we * (we + 1) / 2;
@@ -602,13 +619,13 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
         while ((t + 1) * (t + 2) / 2 <= q) ++t;
         while (t * (t + 1) / 2 > q) --t;
         const int u = q - t * (t + 1) / 2;
-        double acc = S[t * w + u], mx = 0.0;
+        double acc = S[sidx(t, u)], mx = 0.0;
         for (int j = 0; j < m; ++j) {
           const double upd = lc[t * CH + j] * yc[u * CH + j];
           acc -= upd;
           mx = fmax(mx, fabs(upd));
         }
-        S[t * w + u] = acc;
+        S[sidx(t, u)] = acc;
         if (t == u) Sps[t] = fmax(Sps[t], mx);
       }
       __syncthreads();
@@ -618,7 +635,7 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
     // dense border block: sequential LDL^T with the same pivot rule
     if (tid == 0) {
       for (int t = 0; t < w; ++t) {
-        const double d = S[t * w + t];
+        const double d = S[sidx(t, t)];
         const bool zero = zero_pivot(d, Sps[t]);
         const double dinv = zero ? 0.0 : 1.0 / d;
         Dinv[g.bpos + t] = dinv;
@@ -630,18 +647,21 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
         else
           ++nneg;
         for (int u = t + 1; u < w; ++u) {
-          const double lu = S[u * w + t] * dinv;
+          const double lu = S[sidx(u, t)] * dinv;
           for (int v = t + 1; v <= u; ++v) {
-            const double upd = lu * S[v * w + t];
-            S[u * w + v] -= upd;
+            const double upd = lu * S[sidx(v, t)];
+            S[sidx(u, v)] -= upd;
             if (u == v) Sps[u] = fmax(Sps[u], fabs(upd));
           }
         }
-        for (int u = t + 1; u < w; ++u) Sg[u * w + t] = S[u * w + t] * dinv;
+        for (int u = t + 1; u < w; ++u) Sg[u * w + t] = S[sidx(u, t)] * dinv;
       }
     }
   } else {
-    for (int q = tid; q < w * w; q += T) Sg[q] = S[q];  // Schur complement on the border rows
+    for (int q = tid; q < w * w; q += T) {  // Schur complement on the border rows (lower)
+      const int t = q / w, u = q % w;
+      if (u <= t) Sg[q] = S[sidx(t, u)];
+    }
     for (int t = tid; t < w; t += T) ps0[n + t] = Sps[t];   // and its diagonal's largest single update
   }
   if (tid == 0) {
@@ -658,10 +678,13 @@ using FactorKernel = void (*)(const BandSeg*, int, double*, const double*, doubl
 // instantiations for the blocks of the shipped models (segment: b + 1,
 // 2b + wg, b + wg, many blocks of 256 threads; separator system: 2b, wg, wg,
 // one block of 1024 threads), else the generic kernels
-FactorKernel factor_kernel_for(int B1, int w, int we, bool single, int threads = 256) {
-#define OCG_FK(a, c, e, t) \
-  if (B1 == (a) && w == (c) && we == (e) && single == ((t) == 1024) && (single || threads == (t))) \
-    return factor_k<a, c, e, t>;
+// *smem: the dynamic shared memory of the returned kernel
+FactorKernel factor_kernel_for(int B1, int w, int we, bool single, int threads, size_t* smem) {
+#define OCG_FK(a, c, e, t)                                                                          \
+  if (B1 == (a) && w == (c) && we == (e) && single == ((t) == 1024) && (single || threads == (t))) { \
+    *smem = factor_smem((a) - 1, (c), (a) + (c) > 96 ? 16 : kPrefetch, true);                       \
+    return factor_k<a, c, e, t>;                                                                     \
+  }
   OCG_FK(9, 16, 8, 128)    // small bands: 128-thread segment blocks (fewer warps per barrier)
   OCG_FK(13, 25, 13, 128)
   OCG_FK(17, 32, 16, 128)
@@ -678,6 +701,7 @@ FactorKernel factor_kernel_for(int B1, int w, int we, bool single, int threads =
   OCG_FK(38, 74, 37, 256)  // quadrotor (b 37, wg 0)
   OCG_FK(74, 0, 0, 1024)
 #undef OCG_FK
+  *smem = factor_smem(B1 - 1, w, kPrefetch, false);
   return single ? factor_k<0, -1, -1, 1024> : factor_k<0, -1, -1, 256>;
 }
 
@@ -896,9 +920,12 @@ bool warp_kernels_for(int B1, FactorWarpKernel& f, SolveWarpKernel& s) {
 
 // unpartitioned bands of many small systems (batched solves): 128 threads per
 // system, several systems per SM
-FactorKernel factor_kernel_batch(int B1, int w, int we) {
-#define OCG_FKB(a, c, e) \
-  if (B1 == (a) && w == (c) && we == (e)) return factor_k<a, c, e, 128>;
+FactorKernel factor_kernel_batch(int B1, int w, int we, size_t* smem) {
+#define OCG_FKB(a, c, e)                                                        \
+  if (B1 == (a) && w == (c) && we == (e)) {                                     \
+    *smem = factor_smem((a) - 1, (c), (a) + (c) > 96 ? 16 : kPrefetch, true);   \
+    return factor_k<a, c, e, 128>;                                              \
+  }
   OCG_FKB(9, 0, 0)    // double integrator
   OCG_FKB(13, 1, 1)   // Goddard
   OCG_FKB(17, 0, 0)   // cart-pendulum
@@ -906,6 +933,7 @@ FactorKernel factor_kernel_batch(int B1, int w, int we) {
   OCG_FKB(28, 1, 1)   // shuttle
   OCG_FKB(38, 0, 0)   // quadrotor
 #undef OCG_FKB
+  *smem = factor_smem(B1 - 1, w, kPrefetch, false);
   return factor_k<0, -1, -1, 128>;
 }
 
@@ -1487,20 +1515,24 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
   const BandSeg& s0 = P.segs[0];
   static const int env_threads = std::getenv("OCG_SEG_THREADS") ? std::atoi(std::getenv("OCG_SEG_THREADS")) : 0;
   const int seg_threads = env_threads > 0 ? env_threads : (s0.b <= 16 ? 128 : kFactorThreads);
-  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, P.nseg == 1, seg_threads);
+  size_t sm_seg = 0, sm_sep = 0;
+  const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, P.nseg == 1, seg_threads, &sm_seg);
   const FactorKernel fsep =
-      P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true) : fseg;
+      P.nseg > 1 ? factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true, 1024, &sm_sep)
+                 : fseg;
   const int tseg = P.nseg == 1 ? 1024 : seg_threads;
-  if (P.smem_factor > 48 * 1024)
-    for (FactorKernel f : {fseg, fsep})
-      cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(P.smem_factor));
+  if (sm_seg > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fseg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm_seg));
+  if (P.nseg > 1 && sm_sep > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fsep), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm_sep));
   static const bool timing = std::getenv("OCG_TIMING") != nullptr;
   cudaEvent_t ev[4];
   if (timing)
     for (auto& e : ev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(ev[0], s);
-  fseg<<<P.nseg, tseg, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
+  fseg<<<P.nseg, tseg, sm_seg, s>>>(D.segs, 0, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts, BandBatch{});
   if (timing) cudaEventRecord(ev[1], s);
   int blocks = P.nseg;
   if (P.nseg > 1) {
@@ -1513,8 +1545,8 @@ void band_factor(const BandPlan& P, const BandDev& D, double* buf, double delta_
     if (D.cr)
       cr_factor(P, P.segs.back(), buf, D.primal, delta_w, delta_c, D.cr, D.crparts, inertia_parts + 3 * P.nseg, s);
     else
-      fsep<<<1, 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts,
-                                          BandBatch{});
+      fsep<<<1, 1024, sm_sep, s>>>(D.segs, P.nseg, buf, D.primal, delta_w, delta_c, Dinv, inertia_parts,
+                                   BandBatch{});
     if (timing) cudaEventRecord(ev[3], s);
     blocks += 1;
   }
@@ -1608,21 +1640,23 @@ void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, 
     if (P.nnz > 0)
       scatter_k<<<dim3(std::max(1, std::min(grid_for(P.nnz), 16)), ny), 256, 0, s>>>(kval, D.dst, P.nnz, buf, bb);
     const BandSeg& s0 = P.segs[0];
-    const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, false);
-    const FactorKernel fsep = factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true);
-    if (P.smem_factor > 48 * 1024)
-      for (FactorKernel f : {fseg, fsep})
+    size_t sm_seg = 0, sm_sep = 0;
+    const FactorKernel fseg = factor_kernel_for(s0.b + 1, s0.w, s0.w_early, false, kFactorThreads, &sm_seg);
+    const FactorKernel fsep =
+        factor_kernel_for(P.segs.back().b + 1, P.segs.back().w, P.segs.back().w_early, true, 1024, &sm_sep);
+    for (auto [f, sm] : {std::pair<FactorKernel, size_t>{fseg, sm_seg}, {fsep, sm_sep}})
+      if (sm > 48 * 1024)
         cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(P.smem_factor));
+                             static_cast<int>(sm));
     BandBatch pb = bb;
     pb.sparts = 3 * (P.nseg + 1);
-    fseg<<<dim3(P.nseg, ny), kFactorThreads, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
+    fseg<<<dim3(P.nseg, ny), kFactorThreads, sm_seg, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
     const int64_t per = static_cast<int64_t>(P.wmax) * P.wmax;
     for (int par = 0; par < 2; ++par)
       schur_add_k<<<dim3(std::max(1, std::min(grid_for(((P.nseg + 1) / 2) * per), 8)), ny), 256, 0, s>>>(
           D.segs, P.nseg, par, P.wmax, D.border_pos, buf, pb);
     if (P.wg > 0) schur_global_k<<<dim3(1, ny), 256, 0, s>>>(D.segs, P.nseg, P.wmax, P.b, P.wg, buf, pb);
-    fsep<<<dim3(1, ny), 1024, P.smem_factor, s>>>(D.segs, P.nseg, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
+    fsep<<<dim3(1, ny), 1024, sm_sep, s>>>(D.segs, P.nseg, buf, D.primal, 0.0, 0.0, Dinv, parts, pb);
     inertia_sum_k<<<dim3(1, ny), 32, 0, s>>>(parts, P.nseg + 1, inertia, pb);
     return;
   }
@@ -1637,11 +1671,12 @@ void band_factor_batch(const BandPlan& P, const BandDev& D, const double* kval, 
     fw<<<(nb + 3) / 4, 128, 0, s>>>(D.segs, buf, D.primal, Dinv, inertia, bb, nb);
     return;
   }
-  const FactorKernel f = factor_kernel_batch(s0.b + 1, s0.w, s0.w_early);
-  if (P.smem_factor > 48 * 1024)
+  size_t sm_f = 0;
+  const FactorKernel f = factor_kernel_batch(s0.b + 1, s0.w, s0.w_early, &sm_f);
+  if (sm_f > 48 * 1024)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(P.smem_factor));
-  f<<<dim3(1, ny), 128, P.smem_factor, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, inertia, bb);
+                         static_cast<int>(sm_f));
+  f<<<dim3(1, ny), 128, sm_f, s>>>(D.segs, 0, buf, D.primal, 0.0, 0.0, Dinv, inertia, bb);
 }
 
 void band_solve_batch(const BandPlan& P, const BandDev& D, const double* buf, const double* Dinv, const double* rhs,

@@ -80,7 +80,7 @@ struct DeviceCsc {
 // CSC. With dcsc the entry offsets come back in *d_dst (device,
 // cudaMallocAsync'd, caller owns) and P.dst stays empty.
 BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std::vector<int64_t>& colp,
-                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments = 296,
+                        const std::vector<int64_t>& rowi, int64_t ntot, int target_segments = 0,
                         const DeviceCsc* dcsc = nullptr, int64_t** d_dst = nullptr);
 
 namespace dev {

@@ -1166,7 +1166,7 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
 // ---- band LDL^T (band.hpp) ---------------------------------------------------
 
 int ocg_ldl_create(ocg_kkt* k, ocg_ldl** out) {
-  int target = 2 * 148;
+  int target = 0;  // the band plan's default (band.cu make_band_plan)
   if (const char* e = std::getenv("OCG_LDL_SEGMENTS")) target = std::max(1, std::atoi(e));
   return ocg::hd::ldl_create(k, target, out);
 }
