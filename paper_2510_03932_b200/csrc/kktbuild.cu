@@ -11,7 +11,10 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -196,6 +199,15 @@ int bits_for(int64_t v) {
 }  // namespace
 
 void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
+  static const bool timing = std::getenv("OCG_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build_kkt] %-22s %8.3f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
+  };
   const int64_t H = in.H, J = in.J, S = in.n_slack, ntot = in.n_free + in.n_slack, m = in.m;
   const int64_t dim = ntot + m;
   if (dim >= (1ll << 31)) throw std::runtime_error("KKT dimension exceeds the device pattern builder's 2^31");
@@ -206,6 +218,7 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   keys_k<<<grid_for(C), 256, 0, s>>>(in.hr, in.hc, H, in.jr, in.jc, J, in.prim, in.dual, in.slack_dual, in.n_free,
                                      S, ntot, m, key, code);
   sort_pairs(key, code, C, 64, s);
+  lap("sources sorted");
   // 2. slots: runs of equal keys
   auto* flag = dalloc<int64_t>(static_cast<size_t>(C), s);
   auto* slot = dalloc<int64_t>(static_cast<size_t>(C) + 1, s);
@@ -249,6 +262,7 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   out.src_code = code;  // sorted codes (first nvalid are the slots' sources)
   out.ncode = nvalid;
 
+  lap("slots + host pattern");
   // 3. full symmetric CSR for matvec: mirrored entries keyed (row, col)
   auto* mkey = dalloc<unsigned long long>(2 * static_cast<size_t>(nnz), s);
   auto* mval = dalloc<int64_t>(2 * static_cast<size_t>(nnz), s);
@@ -272,6 +286,7 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   out.mv_col = mv_col;
   out.mv_vidx = mval;
 
+  lap("symmetric CSR");
   // 4. J^T lambda gather: per free column, Jacobian entries in increasing order
   auto* jkey = dalloc<unsigned long long>(static_cast<size_t>(J), s);
   auto* jval = dalloc<int64_t>(static_cast<size_t>(J), s);
@@ -304,6 +319,7 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   out.jt_e = jval;
   out.jt_dual = jt_dual;
 
+  lap("J^T gather");
   ck(cudaStreamSynchronize(s), "sync");
   for (void* p : {static_cast<void*>(key), static_cast<void*>(flag), static_cast<void*>(slot),
                   static_cast<void*>(colcnt), static_cast<void*>(colcnt64), static_cast<void*>(colp),
