@@ -20,6 +20,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -40,6 +41,20 @@ size_t factor_smem(int b, int w, int kp = 32, bool owned = false) {
                            static_cast<size_t>(kp) * (B1 + W + 2)) +
          sizeof(short) * 2 * pairs + 64;
 }
+// host loop [0, n) split over the host cores (iterations independent)
+template <class F>
+void par_range(int64_t n, F f) {
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 65536));
+  if (nt <= 1) {
+    f(int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t) th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
+
 size_t solve_smem(int b, int w) {
   constexpr size_t kPre = 32;
   return sizeof(double) * (static_cast<size_t>(b) + 1 + 2 * static_cast<size_t>(w) +
@@ -73,7 +88,9 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     for (int64_t i = 0; i < dim; ++i) flat[static_cast<size_t>(start[bucket(i)]++)] = i;
   }
   std::vector<int64_t> fpos(static_cast<size_t>(dim));
-  for (int64_t p = 0; p < dim; ++p) fpos[static_cast<size_t>(flat[static_cast<size_t>(p)])] = p;
+  par_range(dim, [&](int64_t p0, int64_t p1) {
+    for (int64_t p = p0; p < p1; ++p) fpos[static_cast<size_t>(flat[static_cast<size_t>(p)])] = p;
+  });
   int64_t wg = 0;
   for (int64_t i = 0; i < dim; ++i) wg += node[static_cast<size_t>(i)] < 0 ? 1 : 0;
   const int64_t n = dim - wg;
@@ -151,21 +168,25 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     return {1, i, off - seg_len[static_cast<size_t>(i)]};
   };
   std::vector<Loc> loc(static_cast<size_t>(dim));
-  for (int64_t f = 0; f < dim; ++f) loc[static_cast<size_t>(f)] = loc_of_flat(f);
   P.perm.assign(static_cast<size_t>(dim), -1);
-  for (int64_t f = 0; f < dim; ++f) {
-    const Loc L = loc[static_cast<size_t>(f)];
-    int64_t pos;
-    if (L.kind == 0)
-      pos = seg_pos[static_cast<size_t>(L.idx)] + L.local;
-    else if (L.kind == 1)
-      pos = sep_pos0 + L.idx * b + L.local;
-    else
-      pos = sep_pos0 + n2 + L.local;
-    P.perm[static_cast<size_t>(pos)] = flat[static_cast<size_t>(f)];
-  }
+  par_range(dim, [&](int64_t f0, int64_t f1) {
+    for (int64_t f = f0; f < f1; ++f) {
+      const Loc L = loc_of_flat(f);
+      loc[static_cast<size_t>(f)] = L;
+      int64_t pos;
+      if (L.kind == 0)
+        pos = seg_pos[static_cast<size_t>(L.idx)] + L.local;
+      else if (L.kind == 1)
+        pos = sep_pos0 + L.idx * b + L.local;
+      else
+        pos = sep_pos0 + n2 + L.local;
+      P.perm[static_cast<size_t>(pos)] = flat[static_cast<size_t>(f)];  // a permutation: disjoint writes
+    }
+  });
   P.primal.resize(static_cast<size_t>(dim));
-  for (int64_t p = 0; p < dim; ++p) P.primal[static_cast<size_t>(p)] = P.perm[static_cast<size_t>(p)] < ntot ? 1.0 : 0.0;
+  par_range(dim, [&](int64_t p0, int64_t p1) {
+    for (int64_t p = p0; p < p1; ++p) P.primal[static_cast<size_t>(p)] = P.perm[static_cast<size_t>(p)] < ntot ? 1.0 : 0.0;
+  });
 
   // blocks and their buffers
   int64_t off = 0;
@@ -226,11 +247,13 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
     // the same classification per entry, on the device (dev::band_dst)
     std::vector<int8_t> lk(static_cast<size_t>(dim));
     std::vector<int64_t> li(static_cast<size_t>(dim)), ll(static_cast<size_t>(dim));
-    for (int64_t f = 0; f < dim; ++f) {
-      lk[static_cast<size_t>(f)] = static_cast<int8_t>(loc[static_cast<size_t>(f)].kind);
-      li[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].idx;
-      ll[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].local;
-    }
+    par_range(dim, [&](int64_t f0, int64_t f1) {
+      for (int64_t f = f0; f < f1; ++f) {
+        lk[static_cast<size_t>(f)] = static_cast<int8_t>(loc[static_cast<size_t>(f)].kind);
+        li[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].idx;
+        ll[static_cast<size_t>(f)] = loc[static_cast<size_t>(f)].local;
+      }
+    });
     dev::BandDstIn in;
     in.colp = dcsc->colp;
     in.rowi = dcsc->rowi;
