@@ -8,12 +8,14 @@
 #include <algorithm>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../../include/octgpu.h"
 #include "band.hpp"
+#include "devmem.hpp"
 #include "jit.hpp"
 #include "model.hpp"
 #include "plan.hpp"
@@ -35,37 +37,44 @@ struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   bool owned = true;
+  size_t cap = 0;  // bytes of a block from device_alloc (0: adopted from cudaMallocAsync)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  // Stream-ordered pool allocations on the calling thread's default stream:
-  // unlike cudaMalloc/cudaFree they never synchronize the device, so plans
-  // created and destroyed by concurrent host threads (batched solves) do not
-  // serialize each other's streams.
-  ~DBuf() {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+  // Stream-ordered pool allocations (device_alloc) on the calling thread's
+  // default stream: unlike cudaMalloc/cudaFree they do not synchronize the
+  // device, so plans built by concurrent host threads do not serialize.
+  ~DBuf() { release(); }
+  void release() {
+    if (p && owned) {
+      if (cap)
+        ocg::mem::device_free(p, cap);
+      else
+        cudaFreeAsync(p, cudaStreamPerThread);
+    }
+    p = nullptr;
+    cap = 0;
   }
   // caller-owned device memory of the same size replaces the library buffer
   void bind(T* ext) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    release();
     p = ext;
     owned = false;
   }
   // take ownership of device memory from cudaMallocAsync
   void adopt(T* ptr, size_t count) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    release();
     p = ptr;
     n = count;
     owned = true;
   }
   void alloc(size_t count) {
-    if (p && owned) cudaFreeAsync(p, cudaStreamPerThread);
+    release();
     owned = true;
-    p = nullptr;
     n = count;
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
-       "cudaMallocAsync");
-    ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
+    void* q = nullptr;
+    ck(ocg::mem::device_alloc(std::max<size_t>(count, 1) * sizeof(T), &q, &cap), "cudaMallocAsync");
+    p = static_cast<T*>(q);
   }
   void upload(const std::vector<T>& v) {
     alloc(v.size());

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/octgpu.h"
+#include "devmem.hpp"
 #include "ipm_kernels.hpp"
 
 namespace {
@@ -69,14 +70,14 @@ struct DVec {
   explicit DVec(size_t count) { alloc(count); }
   DVec(const DVec&) = delete;
   DVec& operator=(const DVec&) = delete;
-  ~DVec() {
-    if (p) cudaFreeAsync(p, cudaStreamPerThread);  // stream-ordered: no device-wide sync
-  }
+  size_t cap = 0;
+  ~DVec() { ocg::mem::device_free(p, cap); }  // large blocks back to the cache (devmem.hpp)
   void alloc(size_t count) {
+    ocg::mem::device_free(p, cap);
     n = count;
-    ckc(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaStreamPerThread),
-        "cudaMallocAsync");
-    ckc(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
+    void* q = nullptr;
+    ckc(ocg::mem::device_alloc(std::max<size_t>(count, 1) * sizeof(T), &q, &cap), "cudaMallocAsync");
+    p = static_cast<T*>(q);
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     if (!v.empty()) ckc(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");

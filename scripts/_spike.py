@@ -1,0 +1,9 @@
+import sys, time
+sys.path.insert(0, '.')
+from paper_2510_03932_b200 import MODELS, Model, solve
+m = Model(MODELS["quadrotor"], 100000)
+solve(m, max_iter=1)
+for i in range(10):
+    print("=== solve", i, file=sys.stderr, flush=True)
+    t = time.perf_counter(); r = solve(m)
+    print("wall", round(time.perf_counter() - t, 3), round(r["time_total"], 3), round(r["time_plan_eval"], 3), round(r["time_plan_kkt"], 3), round(r["time_plan_ldl"], 3), round(r["time_setup"], 3), file=sys.stderr, flush=True)
