@@ -1,3 +1,5 @@
+"""Back-to-back device solves of quadrotor N=1e5 with per-phase timings (OCG_TIMING=1):
+the plan-time variance evidence in profiles/r1_v14_plan_spikes_*.txt."""
 import sys, time
 sys.path.insert(0, '.')
 from paper_2510_03932_b200 import MODELS, Model, solve
