@@ -569,8 +569,21 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->device = o.device;
     e->block = o.block > 0 ? o.block : 128;
     ck(cudaSetDevice(o.device), "cudaSetDevice");
+    // device properties once per device and process (the query itself takes
+    // from milliseconds to a tenth of a second)
+    static std::mutex prop_mu;
+    static std::map<int, cudaDeviceProp> props;
     cudaDeviceProp prop;
-    ck(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
+    {
+      std::lock_guard<std::mutex> lk(prop_mu);
+      auto it = props.find(o.device);
+      if (it == props.end()) {
+        ck(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
+        props.emplace(o.device, prop);
+      } else {
+        prop = it->second;
+      }
+    }
     if (prop.major != 10) return fail(OCG_ERR_CUDA, "octgpu kernels target sm_100a; device is sm_" +
                                                         std::to_string(prop.major) + std::to_string(prop.minor));
     {

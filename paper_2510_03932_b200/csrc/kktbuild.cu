@@ -13,11 +13,14 @@
 
 #include <chrono>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
 
+#include "devmem.hpp"
 #include "kktbuild.hpp"
 
 namespace ocg::dev {
@@ -39,11 +42,40 @@ int grid_for(int64_t n) {
   return static_cast<int>(want < 1 ? 1 : (want > 148 * 32 ? 148 * 32 : want));
 }
 
+// blocks through the device block cache (devmem.hpp); their sizes are kept
+// so temporaries go back to the cache, outputs are handed over (forget)
+std::mutex g_cap_mu;
+std::unordered_map<void*, size_t> g_caps;
+
 template <class T>
-T* dalloc(size_t n, cudaStream_t s) {
-  T* p = nullptr;
-  ck(cudaMallocAsync(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T), s), "cudaMallocAsync");
-  return p;
+T* dalloc(size_t n, cudaStream_t) {
+  void* p = nullptr;
+  size_t cap = 0;
+  ck(ocg::mem::device_alloc((n ? n : 1) * sizeof(T), &p, &cap), "cudaMallocAsync");
+  std::lock_guard<std::mutex> lk(g_cap_mu);
+  g_caps[p] = cap;
+  return static_cast<T*>(p);
+}
+void dfree(void* p) {
+  if (!p) return;
+  size_t cap = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_cap_mu);
+    auto it = g_caps.find(p);
+    if (it != g_caps.end()) {
+      cap = it->second;
+      g_caps.erase(it);
+    }
+  }
+  if (cap)
+    ocg::mem::device_free(p, cap);
+  else
+    cudaFreeAsync(p, cudaStreamPerThread);
+}
+// an output adopted by the caller (freed with cudaFreeAsync)
+void forget(void* p) {
+  std::lock_guard<std::mutex> lk(g_cap_mu);
+  g_caps.erase(p);
 }
 
 // sources -> (key, code); invalid (folded/fixed) sources get kNone
@@ -172,9 +204,9 @@ void sort_pairs(unsigned long long*& keys, int64_t*& vals, int64_t n, int end_bi
   ck(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, k2, vals, v2, n, 0, end_bit, s), "sort size");
   void* tmp = dalloc<char>(tmp_bytes, s);
   ck(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, k2, vals, v2, n, 0, end_bit, s), "sort");
-  cudaFreeAsync(tmp, s);
-  cudaFreeAsync(keys, s);
-  cudaFreeAsync(vals, s);
+  dfree(tmp);
+  dfree(keys);
+  dfree(vals);
   keys = k2;
   vals = v2;
 }
@@ -187,7 +219,7 @@ void exclusive_offsets(const int64_t* in, int64_t n, int64_t* out, cudaStream_t 
   ck(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, in, out + 1, n, s), "scan size");
   void* tmp = dalloc<char>(tmp_bytes, s);
   ck(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, in, out + 1, n, s), "scan");
-  cudaFreeAsync(tmp, s);
+  dfree(tmp);
 }
 
 int bits_for(int64_t v) {
@@ -326,7 +358,11 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
                   static_cast<void*>(rowi), static_cast<void*>(ndiag),
                   static_cast<void*>(mkey), static_cast<void*>(rowcnt), static_cast<void*>(rowcnt64),
                   static_cast<void*>(jkey), static_cast<void*>(jcnt), static_cast<void*>(jcnt64)})
-    cudaFreeAsync(p, s);
+    dfree(p);
+  for (void* p : {static_cast<void*>(out.src_ptr), static_cast<void*>(out.src_code), static_cast<void*>(out.mv_ptr),
+                  static_cast<void*>(out.mv_col), static_cast<void*>(out.mv_vidx), static_cast<void*>(out.jt_ptr),
+                  static_cast<void*>(out.jt_e), static_cast<void*>(out.jt_dual)})
+    forget(p);
   ck(cudaStreamSynchronize(s), "sync");
 }
 
