@@ -61,3 +61,16 @@ def test_reusable_context_matches_fresh_solves():
         assert got["iterations"] == fresh["iterations"] == ref["iterations"]
         assert got["objective"] == fresh["objective"]
         assert abs(got["objective"] - ref["objective"]) <= 1e-8 * abs(ref["objective"])
+
+
+def test_repeated_solves_bit_identical():
+    """Plans rebuilt on recycled device blocks (csrc/devmem.hpp's cache hands
+    back memory the previous solve left dirty) give bit-identical solves."""
+    for name, N in (("quadrotor", 2000), ("goddard", 300), ("cart_pendulum", 300)):
+        m = Model(MODELS[name], N)
+        runs = [solve(m) for _ in range(3)]
+        for r in runs[1:]:
+            assert r["status"] == runs[0]["status"]
+            assert r["iterations"] == runs[0]["iterations"]
+            assert r["objective"] == runs[0]["objective"]
+            assert r["factorizations"] == runs[0]["factorizations"]
