@@ -786,9 +786,19 @@ __global__ void __launch_bounds__(128) factor_warp_k(const BandSeg* __restrict__
     if (lane < B1) W[c * B1 + lane] = v;
     if (lane == 0) ps[c] = fabs(v);
   }
-  double pf[PF];
+  // prefetched raw column entries and (lane 0) regularization flags: the
+  // delta is applied when the column enters the window, so no arithmetic
+  // waits on a load at prefetch time
+  auto raw = [&](long long c) -> double {
+    return lane < B1 && c < n && c + lane < n ? band[c * B1 + lane] : 0.0;
+  };
+  auto rawflag = [&](long long c) -> double { return lane == 0 && c < n ? flag[c] : 0.0; };
+  double pf[PF], pff[PF];
 #pragma unroll
-  for (int q = 0; q < PF; ++q) pf[q] = column(B1 + q);
+  for (int q = 0; q < PF; ++q) {
+    pf[q] = raw(B1 + q);
+    pff[q] = rawflag(B1 + q);
+  }
   __syncwarp();
   long long npos = 0, nneg = 0, nzero = 0;
   int s = 0;
@@ -829,9 +839,12 @@ __global__ void __launch_bounds__(128) factor_warp_k(const BandSeg* __restrict__
       }
       __syncwarp();
       // column k is final: its slot takes column k + B1
-      if (lane < B1) W[s * B1 + lane] = pf[q];
-      if (lane == 0) ps[s] = fabs(pf[q]);
-      pf[q] = column(k + B1 + PF);
+      double vin = pf[q];
+      if (lane == 0 && k + B1 < n) vin += pff[q] != 0.0 ? dw : -dc;
+      if (lane < B1) W[s * B1 + lane] = vin;
+      if (lane == 0) ps[s] = fabs(vin);
+      pf[q] = raw(k + B1 + PF);
+      pff[q] = rawflag(k + B1 + PF);
       s = s + 1 == B1 ? 0 : s + 1;
       __syncwarp();
     }
@@ -1147,15 +1160,19 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
   }
 #pragma unroll
   for (int r = 0; r < NW; ++r) X[r] = 0.0;  // entry e >= 1: x[c + e]
-  auto cold = [&](long long c) { return lane == 0 && c >= 0 ? v[c] * dinv[c] : 0.0; };
-  double pb[PF][NW], pw[PF][NBW], pd[PF];
+  // raw v[c] and dinv[c] (lane 0), multiplied when used: no arithmetic waits
+  // on a load at prefetch time
+  auto colv = [&](long long c) { return lane == 0 && c >= 0 ? v[c] : 0.0; };
+  auto coli = [&](long long c) { return lane == 0 && c >= 0 ? dinv[c] : 0.0; };
+  double pb[PF][NW], pw[PF][NBW], pv[PF], pi[PF];
 #pragma unroll
   for (int q = 0; q < PF; ++q) {
 #pragma unroll
     for (int r = 0; r < NW; ++r) pb[q][r] = colb(n - 1 - q, r);
 #pragma unroll
     for (int r = 0; r < NBW; ++r) pw[q][r] = colw(n - 1 - q, r);
-    pd[q] = cold(n - 1 - q);
+    pv[q] = colv(n - 1 - q);
+    pi[q] = coli(n - 1 - q);
   }
   for (long long i0 = 0; i0 < n; i0 += PF) {
 #pragma unroll
@@ -1168,7 +1185,7 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
 #pragma unroll
       for (int r = 0; r < NBW; ++r) part += pw[q][r] * xb[r];
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      const double xc = __shfl_sync(0xffffffffu, pd[q], 0) - part;
+      const double xc = __shfl_sync(0xffffffffu, pv[q] * pi[q], 0) - part;
       if (lane == 0) v[c] = xc;
       // shift: entry e takes entry e - 1; entry 1 takes x_c
 #pragma unroll
@@ -1185,7 +1202,8 @@ __global__ void __launch_bounds__(32) solve_seg_warp_k(const BandSeg* __restrict
       for (int r = 0; r < NW; ++r) pb[q][r] = colb(c - PF, r);
 #pragma unroll
       for (int r = 0; r < NBW; ++r) pw[q][r] = colw(c - PF, r);
-      pd[q] = cold(c - PF);
+      pv[q] = colv(c - PF);
+      pi[q] = coli(c - PF);
     }
   }
 }
