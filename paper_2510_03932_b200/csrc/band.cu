@@ -112,9 +112,10 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   P.wg = static_cast<int>(wg);
 
   // partition: P segments of >= 8b interior columns separated by b-wide
-  // separators. Default: two segment blocks per SM, three for the deep bands
-  // whose factor blocks are sized to fit three (b >= 32: 72 KB at quadrotor's)
-  if (target_segments <= 0) target_segments = b >= 32 ? 3 * 148 : 2 * 148;
+  // separators. Default: three segment blocks per SM (Goddard's 21 KB and
+  // quadrotor's 72 KB factor blocks both fit three); two for the narrowest
+  // bands (b < 12), whose iteration counts at N=2e4 moved with more segments
+  if (target_segments <= 0) target_segments = b >= 12 ? 3 * 148 : 2 * 148;
   int64_t nseg = std::min<int64_t>(target_segments, n / std::max<int64_t>(1, 8 * b));
   if (nseg < 2) nseg = 1;
   P.nseg = static_cast<int>(nseg);
