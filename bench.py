@@ -49,10 +49,9 @@ def parse():
     ap.add_argument("--N", type=int, default=100_000, help="time nodes per GPU")
     ap.add_argument("--scheme", default="trapezoid")
     ap.add_argument("--block", type=int, default=128)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--secondary", action="store_true",
-                    help="also time the other eval configs (quadrotor 1e6, hang glider, shuttle) into 'extra'")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the other eval configs (quadrotor 1e6 and 1e5, hang glider, shuttle; 'extra' key)")
     ap.add_argument("--solve", default="quadrotor:100000",
                     help="model:N of the full IPM solve leg ('ipm_solve' key; 'none' to skip)")
     ap.add_argument("--goddard-solve", default="100000:10",
@@ -232,23 +231,92 @@ def _ref_modules():
     return RefEval, RefModel
 
 
-def cpu_reference_eval(src: str, N: int, scheme: str, budget_s: float, steps: int | None = None,
-                       warmup: int = 0) -> dict:
+def load_models():
+    """models.py (model TEXT only, no imports) loaded by path, so that the
+    reference arm never imports the package (which maps libocgpu.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_ocg_model_texts", ROOT / "paper_2510_03932_b200" / "models.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(args, world: int) -> dict:
+    """The workload both arms report: identical dict (the driver compares them)."""
+    N = args.N * world
+    return {"workload": f"{args.model} {args.scheme} N={N} ({args.N} nodes/GPU) J+H eval "
+                        "(EvalContext::eval_constraints_jacobian + eval_hessian)",
+            "model": args.model, "N": N, "nodes_per_gpu": args.N, "scheme": args.scheme,
+            "parallelism": f"node-range shards x{world}",
+            "l2": "device: flushed (512 MiB read) before every timed step",
+            "inputs": "acceptance recipe mt19937(20250808)"}
+
+
+def _median_steps(re, x, lam, reps: int, warmup: int = 1) -> list[float]:
+    for _ in range(max(warmup, 1)):
+        t1, ok = re.step_seconds(x, lam, 1)
+        assert ok, "reference evaluation failed on the synthetic point"
+    return [re.step_seconds(x, lam, 1)[0] for _ in range(reps)]
+
+
+def cpu_reference_eval(src: str, N: int, scheme: str, reps: int = 5, serial: bool = True,
+                       outputs: bool = False) -> dict:
+    """the reference EvalContext J+H step (eval_constraints_jacobian
+    + eval_hessian) with Backend::parallel on every host core and with
+    Backend::serial, median of `reps` after one warm-up each."""
     RefEval, RefModel = _ref_modules()
     cores = os.cpu_count() or 1
     rm = RefModel(src, N, 1 if scheme == "trapezoid" else 0)
     x, lam = rm.synth_acceptance(20250808)
     re = RefEval(rm, parallel=True, workers=cores)
-    for _ in range(max(warmup, 1)):
-        t1, ok = re.step_seconds(x, lam, 1)
-        assert ok, "reference evaluation failed on the synthetic point"
-    reps = steps if steps is not None else max(1, min(50, int(budget_s / max(t1, 1e-6))))
-    times = [re.step_seconds(x, lam, 1)[0] for _ in range(reps)]
-    return {"times": times, "cores": re_workers(re), "reps": reps}
+    par = _median_steps(re, x, lam, reps)
+    out = {"parallel": {"median_s": float(np.median(par)), "times_s": par, "workers": int(re.L.ref_eval_workers(re.h))},
+           "cpu_model": cpu_model(), "nproc": cores, "reps": reps}
+    if serial:
+        rs = RefEval(rm, parallel=False)
+        ser = _median_steps(rs, x, lam, reps)
+        out["serial"] = {"median_s": float(np.median(ser)), "times_s": ser, "workers": 1}
+        del rs
+    if outputs:
+        ok1, c_r, j_r = re.constraints_jacobian(x)
+        ok2, h_r = re.hessian(x, lam)
+        out["outputs"] = (ok1 and ok2, c_r, j_r, h_r)
+    return out
 
 
-def re_workers(re) -> int:
-    return int(re.L.ref_eval_workers(re.h))
+def parity_of(name: str, got: dict, ref: tuple) -> dict:
+    """max relative error of the device c / jac / hess against the reference
+    EvalContext on the same inputs (tests/parity.py rule with the model's floor)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from parity import floor_for, rel_errors  # noqa: E402
+    ok, c_r, j_r, h_r = ref
+    fl = floor_for(name)
+    res = {"reference_ok": bool(ok), "floor": fl, "tolerance": 1e-12}
+    worst, worst0, exact, n = 0.0, 0.0, 0, 0
+    for k, r in (("c", c_r), ("jac", j_r), ("hess", h_r)):
+        g = got[k]
+        e = rel_errors(g, r, fl)
+        e0 = rel_errors(g, r, 0.0)
+        res[f"max_rel_err_{k}"] = float(e.max()) if e.size else 0.0
+        worst = max(worst, res[f"max_rel_err_{k}"])
+        worst0 = max(worst0, float(e0.max()) if e0.size else 0.0)
+        exact += int(np.sum(g == r))
+        n += r.size
+    res["max_rel_err"] = worst
+    res["max_rel_err_nofloor"] = worst0
+    res["bit_exact_frac"] = exact / max(n, 1)
+    res["entries"] = n
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -259,21 +327,31 @@ def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2510_03932_b200.models import MODELS
-    src = MODELS[args.model]
-    N = args.N * args.gpus
-    r = cpu_reference_eval(src, N, args.scheme, 0.0, steps=args.steps, warmup=args.warmup)
-    t = float(np.mean(r["times"]))
+    src = load_models().MODELS[args.model]
+    world = args.gpus
+    N = args.N * world
+    RefEval, RefModel = _ref_modules()
+    cores = os.cpu_count() or 1
+    rm = RefModel(src, N, 1 if args.scheme == "trapezoid" else 0)
+    x, lam = rm.synth_acceptance(20250808)
+    re = RefEval(rm, parallel=True, workers=cores)
+    for _ in range(max(args.warmup, 1)):
+        re.step_seconds(x, lam, 1)
+    times = [re.step_seconds(x, lam, 1)[0] for _ in range(args.steps)]
+    workers = int(re.L.ref_eval_workers(re.h))
+    t = float(np.mean(times))
     val = t * 1e9 / N
     line = {
         "metric": "jac+hess eval ns/node", "value": val, "unit": "ns/node", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.model} {args.scheme} N={N} J+H eval (EvalContext::eval_constraints_jacobian"
-                               f" + eval_hessian)", "model": args.model, "N": N, "scheme": args.scheme},
-        "cpu_baseline": {"value": val, "unit": "ns/node", "cores": r["cores"], "kind": "reference",
+        "config": bench_config(args, world),
+        "cpu_baseline": {"value": val, "unit": "ns/node", "cores": workers, "kind": "reference",
+                         "cpu_model": cpu_model(), "nproc": cores,
+                         "median_ns_per_node": float(np.median(times)) * 1e9 / N,
                          "sample": f"full workload (N={N}), {args.steps} steps after {args.warmup} warm-up, "
-                                   f"Backend::parallel x{r['cores']} workers"},
+                                   f"reference EvalContext (oracle/_ref/libref.so) with Backend::parallel "
+                                   f"x{workers} workers"},
         "e2e": {"value": val, "unit": "ns/node", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -356,6 +434,7 @@ def run_ours(args) -> None:
     wall = time.perf_counter() - t_wall0
     t_local = float(np.mean(times))
     ok = ec.status(stream)
+    dev_out = {"c": c.cpu().numpy(), "jac": ec.jac_val.cpu().numpy(), "hess": ec.hess_val.cpu().numpy()}
 
     # end to end through the public API with host buffers: pinned x, lambda in;
     # c, jac_val, hess_val segments this rank owns back to pinned host memory
@@ -414,12 +493,8 @@ def run_ours(args) -> None:
             "metric": "jac+hess eval ns/node", "value": value, "unit": "ns/node", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.model} {args.scheme} N={N} ({args.N} nodes/GPU) fused J+H eval "
-                                   "(EvalContext::eval_constraints_jacobian + eval_hessian)",
-                       "model": args.model, "N": N, "nodes_per_gpu": args.N, "scheme": args.scheme,
-                       "parallelism": f"node-range shards x{world}", "block": ec_block(ec),
-                       "l2": "flushed (512 MiB read) before every timed step",
-                       "inputs": "acceptance recipe mt19937(20250808)"},
+            "config": bench_config(args, world),
+            "launch": {"block": ec_block(ec), "kernel": "ocg_cjh"},
             "ok": not bad,
             "nodes_per_s": N / t_max,
             "hbm_gbs": achieved,
@@ -448,17 +523,22 @@ def run_ours(args) -> None:
                 pass
         if world == 1 and not args.no_cpu_baseline:
             try:
-                r = cpu_reference_eval(src, N, args.scheme, args.cpu_seconds)
-                tc = float(np.mean(r["times"]))
-                out["cpu_baseline"] = {"value": tc * 1e9 / N, "unit": "ns/node", "cores": r["cores"],
-                                       "kind": "reference",
-                                       "sample": f"full workload (N={N}) x{r['reps']} J+H evaluations, reference "
-                                                 f"EvalContext with Backend::parallel ({r['cores']} workers)"}
+                r = cpu_reference_eval(src, N, args.scheme, reps=5, serial=True, outputs=True)
+                tp, ts = r["parallel"]["median_s"], r["serial"]["median_s"]
+                out["cpu_baseline"] = {
+                    "value": tp * 1e9 / N, "unit": "ns/node", "cores": r["parallel"]["workers"], "kind": "reference",
+                    "serial_value": ts * 1e9 / N, "cpu_model": r["cpu_model"], "nproc": r["nproc"],
+                    "sample": f"full workload (N={N}), median of {r['reps']} J+H evaluations after one warm-up, "
+                              f"reference EvalContext (oracle/_ref/libref.so): value = Backend::parallel "
+                              f"({r['parallel']['workers']} workers), serial_value = Backend::serial",
+                    "parallel_times_s": r["parallel"]["times_s"], "serial_times_s": r["serial"]["times_s"]}
+                out["parity"] = parity_of(args.model, dev_out, r["outputs"])
+                out["max_rel_err"] = out["parity"]["max_rel_err"]
             except Exception as ex:  # the checker library is missing on this box
                 out["cpu_baseline"] = {"value": None, "unit": "ns/node", "cores": 0, "kind": "reference",
                                        "sample": f"unavailable: {ex}"}
-        if args.secondary and world == 1:
-            out["extra"] = secondary(dev, stream, flush, sink, peak)
+        if not args.no_secondary and world == 1:
+            out["extra"] = secondary(dev, stream, flush, sink, peak, not args.no_cpu_baseline)
         if args.solve != "none" and world == 1:
             out["ipm_solve"] = ipm_solve_leg(args.solve, not args.no_cpu_baseline)
         if args.goddard_solve != "none" and world == 1:  # BASELINE config 2
@@ -582,8 +662,11 @@ def ec_block(ec) -> int:
     return getattr(ec, "block", 128)
 
 
-def secondary(dev, stream, flush, sink, peak) -> list[dict]:
-    """The other eval-only configs (BASELINE.json configs[2..3]) at N=1 GPU."""
+def secondary(dev, stream, flush, sink, peak, with_reference: bool) -> list[dict]:
+    """The other eval-only configs (BASELINE.json configs[2..3]) at N=1 GPU:
+    quadrotor N=1e6 (north_star's >= 60% of HBM roofline at N >= 1e6),
+    quadrotor N=1e5, hang glider and shuttle N=1e5; each timed like the
+    headline and checked against the reference EvalContext (max_rel_err)."""
     import torch
 
     from paper_2510_03932_b200 import MODELS, EvalContext, Model
@@ -597,12 +680,22 @@ def secondary(dev, stream, flush, sink, peak) -> list[dict]:
         xd, ld = torch.as_tensor(x, device=dev), torch.as_tensor(lam, device=dev)
         c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
         ok = ec.eval_jac_hess(xd, ld, c)
-        ts, _ = time_eval_config(ec, xd, ld, c, flush, sink, stream, 20, 3)
+        ts, launches = time_eval_config(ec, xd, ld, c, flush, sink, stream, 20, 3)
         t = float(np.mean(ts))
         nb = algorithmic_bytes(st, *main_space(st), True)
-        res.append({"model": name, "N": N, "ok": ok, "ns_per_node": t * 1e9 / N, "us_per_step": t * 1e6,
-                    "gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak, "bytes_per_node": nb / N})
-        del ec
+        row = {"model": name, "N": N, "ok": ok and ec.status(stream), "ns_per_node": t * 1e9 / N,
+               "us_per_step": t * 1e6, "gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak, "bytes_per_node": nb / N,
+               "steps": 20, "warmup": 3, "gpu_launches": launches}
+        if with_reference:
+            got = {"c": c.cpu().numpy(), "jac": ec.jac_val.cpu().numpy(), "hess": ec.hess_val.cpu().numpy()}
+            del ec
+            r = cpu_reference_eval(MODELS[name], N, "trapezoid", reps=1, serial=False, outputs=True)
+            row["parity"] = parity_of(name, got, r["outputs"])
+            row["max_rel_err"] = row["parity"]["max_rel_err"]
+            row["cpu_baseline_ns_per_node"] = r["parallel"]["median_s"] * 1e9 / N
+        else:
+            del ec
+        res.append(row)
     return res
 
 

@@ -47,6 +47,11 @@ typedef void* ocg_stream;           /* cudaStream_t */
 const char* ocg_last_error(void);
 void ocg_free(void* p);
 const char* ocg_version(void);
+/* Library-internal device memory: large plan blocks are kept in a bounded
+ * cache (OCG_CACHE_MAX_MB, default 8192 MiB per device) and a private
+ * stream-ordered pool per device; this returns both to the driver for
+ * `device` (< 0: every device). Call with no work of the library in flight. */
+int ocg_release_cached_memory(int device);
 
 /* ---- model: parse + transcribe (reference transcribe.hpp:56-59) ---------- */
 /* scheme: 0 = euler, 1 = trapezoid (transcribe::Scheme) */
@@ -275,7 +280,10 @@ void ocg_ipm_default_options(ocg_ipm_options* o);
  * factorization plan are built once per model structure; each solve then
  * takes an instance's bounds and start point (NULL = the model's), e.g. the
  * members of a batch that differ only in boundary values (BASELINE config 5).
- * The instance must fix the same slots (equal folded bounds) as the model. */
+ * The instance must fix the same slots (equal folded bounds) as the model,
+ * and keep every kept row's kind: a row that is an equality (lcon == ucon) in
+ * the model must stay one, a range row must stay a range (the slack map is
+ * the model's); otherwise the solve returns OCG_ERR_ARG. */
 typedef struct ocg_ipm_ctx ocg_ipm_ctx;
 int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out);
 void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c);

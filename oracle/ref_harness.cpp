@@ -350,6 +350,56 @@ void ref_kkt_matvec(void* h, const double* val, const double* x, double* y) {
   sparse::matvec_sym(A, std::span<const double>(x, n), std::span<double>(y, n));
 }
 
+
+// KktAssembler::symbolic() (proj/src/ipm/eval.cpp:442-471): the AMD order with
+// the pivot_after_ deferral, then sparse::analyze_ordered (ldl.cpp:78-133).
+// sizes: out[0] = dim, out[1] = nnz(L).
+void ref_kkt_symbolic_sizes(void* h, int64_t* out) {
+  const auto& S = static_cast<RefKkt*>(h)->kkt->symbolic();
+  out[0] = S.n;
+  out[1] = S.lnz;
+}
+void ref_kkt_symbolic(void* h, int64_t* perm, int64_t* parent, int64_t* Lp) {
+  const auto& S = static_cast<RefKkt*>(h)->kkt->symbolic();
+  std::memcpy(perm, S.perm.data(), S.perm.size() * sizeof(Index));
+  std::memcpy(parent, S.parent.data(), S.parent.size() * sizeof(Index));
+  std::memcpy(Lp, S.Lp.data(), S.Lp.size() * sizeof(Index));
+}
+
+// sparse::factorize (ldl.cpp:139-213) of the given K values with the
+// reference's split (ntot) and shifts; D, Li, Lx, Dinv out (permuted order),
+// inertia[3] = (pos, neg, zero).
+void ref_kkt_factorize(void* h, const double* val, double dw, double dc, double* D, int64_t* Li, double* Lx,
+                       int64_t* inertia) {
+  auto* r = static_cast<RefKkt*>(h);
+  const auto& S = r->kkt->symbolic();
+  sparse::SparseSym A = r->kkt->K;
+  std::memcpy(A.val.data(), val, A.val.size() * sizeof(double));
+  sparse::LdlFactor F;
+  sparse::factorize(A, S, dw, dc, r->kkt->ntot, F);
+  if (D) std::memcpy(D, F.D.data(), F.D.size() * sizeof(double));
+  if (Li) std::memcpy(Li, F.Li.data(), F.Li.size() * sizeof(Index));
+  if (Lx) std::memcpy(Lx, F.Lx.data(), F.Lx.size() * sizeof(double));
+  inertia[0] = F.inertia.positive;
+  inertia[1] = F.inertia.negative;
+  inertia[2] = F.inertia.zero;
+}
+
+// sparse::solve (ldl.cpp:222-247) against a fresh factorization; returns 0 if
+// the factorization had zero pivots (the reference throws there).
+int ref_kkt_factor_solve(void* h, const double* val, double dw, double dc, const double* b, double* x) {
+  auto* r = static_cast<RefKkt*>(h);
+  const auto& S = r->kkt->symbolic();
+  sparse::SparseSym A = r->kkt->K;
+  std::memcpy(A.val.data(), val, A.val.size() * sizeof(double));
+  sparse::LdlFactor F;
+  sparse::factorize(A, S, dw, dc, r->kkt->ntot, F);
+  if (F.inertia.zero > 0) return 0;
+  auto y = sparse::solve(F, std::span<const double>(b, static_cast<size_t>(S.n)));
+  std::memcpy(x, y.data(), y.size() * sizeof(double));
+  return 1;
+}
+
 // ---- full solve ---------------------------------------------------------------
 
 // out: [objective, iterations, time_total, time_derivatives, time_factorize,

@@ -16,7 +16,7 @@ OCG_BUF_JAC, OCG_BUF_HESS, OCG_BUF_GRAD, OCG_BUF_ROWSCALE, OCG_BUF_OBJV = range(
 
 # every symbol include/octgpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "ocg_last_error", "ocg_free", "ocg_version",
+    "ocg_last_error", "ocg_free", "ocg_version", "ocg_release_cached_memory",
     "ocg_model_create", "ocg_model_create_from_nlp", "ocg_model_destroy", "ocg_model_nvar", "ocg_model_mcon", "ocg_model_grid",
     "ocg_model_arrays", "ocg_model_structure_json", "ocg_model_synth_acceptance", "ocg_synth_uniform",
     "ocg_eval_default_options", "ocg_eval_create", "ocg_eval_destroy", "ocg_eval_sizes", "ocg_eval_structure",
@@ -71,6 +71,7 @@ def _load() -> C.CDLL:
         "ocg_last_error": (C.c_char_p, []),
         "ocg_free": (None, [vp]),
         "ocg_version": (C.c_char_p, []),
+        "ocg_release_cached_memory": (C.c_int, [C.c_int]),
         "ocg_model_create": (i32, [C.c_char_p, i32, i64, i32, C.POINTER(vp)]),
         "ocg_model_create_from_nlp": (i32, [vp, C.POINTER(vp)]),
         "ocg_model_destroy": (None, [vp]),

@@ -27,6 +27,7 @@
 #include <string>
 
 #include "band.hpp"
+#include "devmem.hpp"
 
 namespace ocg {
 
@@ -114,8 +115,13 @@ BandPlan make_band_plan(int64_t dim, const std::vector<int64_t>& node, const std
   // partition: P segments of >= 8b interior columns separated by b-wide
   // separators. Default: three segment blocks per SM (Goddard's 21 KB and
   // quadrotor's 72 KB factor blocks both fit three); two for the narrowest
-  // bands (b < 12), whose iteration counts at N=2e4 moved with more segments
-  if (target_segments <= 0) target_segments = b >= 12 ? 3 * 148 : 2 * 148;
+  // bands (b < 12), whose iteration counts at N=2e4 moved with more segments.
+  // The count follows the device's SMs (148 on B200: 444 / 296); the pinned
+  // iteration counts were measured with those values.
+  if (target_segments <= 0) {
+    const int sms = ocg::mem::sm_count();
+    target_segments = b >= 12 ? 3 * sms : 2 * sms;
+  }
   int64_t nseg = std::min<int64_t>(target_segments, n / std::max<int64_t>(1, 8 * b));
   if (nseg < 2) nseg = 1;
   P.nseg = static_cast<int>(nseg);

@@ -26,6 +26,7 @@
 #include <exception>
 #include <limits>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <type_traits>
@@ -35,6 +36,13 @@
 #include "../../include/octgpu.h"
 #include "batch_kernels.hpp"
 #include "handles.hpp"
+
+namespace {
+// an instance whose data do not fit the model's structure (OCG_ERR_ARG)
+struct InvalidInstance : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+}  // namespace
 
 namespace {
 
@@ -452,6 +460,17 @@ void Batch::setup(const double* lvar, const double* uvar, const double* x0, cons
   ocg_model_arrays(model_, mlv.data(), muv.data(), mx0.data(), nullptr, nullptr, mlc.data(), muc.data());
   std::vector<int64_t> prim(nv), slack(mc), dual(mc), rslot(mc);
   ocg_kkt_maps(kkt_, prim.data(), slack.data(), dual.data(), rslot.data(), nullptr, nullptr);
+  // the slack map is the model's (eval.cpp:330-336): every instance must keep
+  // each kept row's kind (equality stays equality, range stays range)
+  for (size_t b = 0; b < B; ++b)
+    for (size_t r = 0; r < mc; ++r) {
+      if (dual[r] < 0) continue;
+      const double lo = lcon ? lcon[b * mc + r] : mlc[r], hi = ucon ? ucon[b * mc + r] : muc[r];
+      if ((lo == hi) != (slack[r] < 0))
+        throw InvalidInstance("instance " + std::to_string(b) + " row " + std::to_string(r) +
+                              (slack[r] < 0 ? " loosens an equality of the model into a range"
+                                            : " turns a range row of the model into an equality"));
+    }
   {
     char* js = ocg_model_structure_json(model_);
     if (js) {
@@ -501,8 +520,8 @@ void Batch::setup(const double* lvar, const double* uvar, const double* x0, cons
   ck(cudaStreamSynchronize(s_), "fold sync");
   for (size_t b = 0; b < B; ++b)
     if (flags[B + b])
-      throw std::runtime_error("instance " + std::to_string(b) +
-                               ": its bounds change which slots are fixed (the KKT structure differs)");
+      throw InvalidInstance("instance " + std::to_string(b) +
+                            ": its bounds change which slots are fixed (the KKT structure differs)");
 
   insts_.resize(B);
   for (size_t b = 0; b < B; ++b) {
@@ -1100,9 +1119,12 @@ extern "C" int ocg_ipm_batch_solve(ocg_model* m, const ocg_ipm_options* opts, in
   ocg_ipm_default_options(&o);
   if (opts) o = *opts;
   try {
+    ocg::mem::DeviceScope ds(device);
     Batch b(m, o, device, nb);
     b.run(lvar, uvar, x_start, lcon, ucon, out, x_out);
     return OCG_OK;
+  } catch (const InvalidInstance& ex) {
+    return ocg::hd::set_error(OCG_ERR_ARG, std::string("ocg_ipm_batch_solve: ") + ex.what());
   } catch (const std::exception& ex) {
     return ocg::hd::set_error(OCG_ERR_CUDA, std::string("ocg_ipm_batch_solve: ") + ex.what());
   }

@@ -586,17 +586,6 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     }
     if (prop.major != 10) return fail(OCG_ERR_CUDA, "octgpu kernels target sm_100a; device is sm_" +
                                                         std::to_string(prop.major) + std::to_string(prop.minor));
-    {
-      // Plans allocate and free GBs through the stream-ordered pool; keep what
-      // is freed mapped (like a caching allocator) instead of returning it to
-      // the driver at every synchronization, so rebuilding a plan is not paid
-      // in page mappings.
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-    }
     const ocg::Nlp& nlp = m->nlp;
     e->lay = ocg::make_layout(nlp);
     const Index lo = std::max(e->lay.idx_lo, o.idx_lo);
@@ -698,7 +687,12 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
   }
 }
 
-void ocg_eval_destroy(ocg_eval* e) { delete e; }
+void ocg_eval_destroy(ocg_eval* e) {
+  if (!e) return;
+  ocg::mem::DeviceScope ds(e->device);
+  cudaDeviceSynchronize();  // no queued work may still use the buffers
+  delete e;
+}
 
 int ocg_eval_sizes(const ocg_eval* e, int64_t* jn, int64_t* hn, int64_t* gn) {
   if (!e) return fail(OCG_ERR_ARG, "null eval");
@@ -738,6 +732,7 @@ double* ocg_eval_buffer(ocg_eval* e, int which) {
 int ocg_eval_bind_buffer(ocg_eval* e, int which, double* dev_ptr) {
   if (!e || !dev_ptr) return fail(OCG_ERR_ARG, "null argument");
   try {
+    ocg::mem::DeviceScope ds_(e->device);
     switch (which) {
       case OCG_BUF_JAC: e->jac.bind(dev_ptr); break;
       case OCG_BUF_HESS: e->hess.bind(dev_ptr); break;
@@ -760,6 +755,7 @@ int ocg_eval_bind_buffer(ocg_eval* e, int which, double* dev_ptr) {
 int ocg_eval_set_scaling(ocg_eval* e, double obj_scale, const double* row_scale) {
   if (!e) return fail(OCG_ERR_ARG, "null eval");
   try {
+    ocg::mem::DeviceScope ds_(e->device);
     const size_t m = static_cast<size_t>(e->model->nlp.m_con);
     std::vector<double> rs(m, 1.0);
     if (row_scale) std::copy(row_scale, row_scale + m, rs.begin());
@@ -775,6 +771,7 @@ int ocg_eval_set_scaling(ocg_eval* e, double obj_scale, const double* row_scale)
 int ocg_eval_get_scaling(ocg_eval* e, double* obj_scale, double* row_scale) {
   if (!e) return fail(OCG_ERR_ARG, "null eval");
   try {
+    ocg::mem::DeviceScope ds_(e->device);
     if (obj_scale) *obj_scale = e->obj_scale;
     const size_t m = static_cast<size_t>(e->model->nlp.m_con);
     if (row_scale && m) ck(cudaMemcpy(row_scale, e->row_scale.p, m * sizeof(double), cudaMemcpyDeviceToHost), "rs");
@@ -794,6 +791,7 @@ int ocg_eval_get_scaling(ocg_eval* e, double* obj_scale, double* row_scale) {
 int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s) {
   if (!e || !x || !c) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const double* rs = e->row_scale.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_c");
@@ -806,6 +804,7 @@ int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s) 
 int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_stream s) {
   if (!e || !x || !c) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const double* rs = e->row_scale.p;
   double* jac = e->jac.p;
   int* fl = e->flag.p;
@@ -819,6 +818,7 @@ int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_s
 int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_stream s) {
   if (!e || !x || !lambda) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const double* rs = e->row_scale.p;
   const double* ow = e->objw.p;
   double* hess = e->hess.p;
@@ -833,6 +833,7 @@ int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_str
 int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double* c, ocg_stream s) {
   if (!e || !x || !lambda || !c) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const double* rs = e->row_scale.p;
   const double* ow = e->objw.p;
   double* jac = e->jac.p;
@@ -848,6 +849,7 @@ int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double
 int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
   if (!e || !x || !f) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
@@ -865,6 +867,7 @@ int64_t ocg_eval_objective_chunks(const ocg_eval* e) { return e ? e->n_chunks : 
 int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, ocg_stream s) {
   if (!e || !x || !partials) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
@@ -880,6 +883,7 @@ int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, 
 int ocg_eval_objective_combine(ocg_eval* e, const double* partials, double* f, ocg_stream s) {
   if (!e || !partials || !f) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   ocg::dev::objective_combine(partials, e->og_cbase.p, e->og_weight.p, static_cast<int>(e->obj_weight.size()),
                               e->obj_scale, f, e->flag.p, st(s));
   e->launches += 1;
@@ -890,6 +894,7 @@ int ocg_eval_objective_combine(ocg_eval* e, const double* partials, double* f, o
 int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stream s) {
   if (!e || !x || !grad_dense) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const double* ow = e->objw.p;
   double* g = e->grad.p;
   int* fl = e->flag.p;
@@ -906,6 +911,7 @@ int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stre
 int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s) {
   if (!e || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   ocg::dev::max_abs(e->hess.p, e->lay.hess_nnz, out, st(s));
   e->launches += 1;
   return OCG_OK;
@@ -915,6 +921,7 @@ int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s) {
 int ocg_eval_status(ocg_eval* e, ocg_stream s) {
   if (!e) return fail(OCG_ERR_ARG, "null eval");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   int h = 0;
   ck(cudaMemcpyAsync(&h, e->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st(s)), "flag d2h");
   ck(cudaStreamSynchronize(st(s)), "sync");
@@ -934,6 +941,7 @@ int64_t ocg_eval_launch_count(const ocg_eval* e) { return e ? e->launches : -1; 
 int ocg_eval_compute_scaling(ocg_eval* e, const double* x0, int enabled, ocg_stream s) {
   if (!e || !x0) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
   const auto& nlp = e->model->nlp;
   const size_t m = static_cast<size_t>(nlp.m_con), nv = static_cast<size_t>(nlp.nvar);
   int rc = ocg_eval_set_scaling(e, 1.0, nullptr);
@@ -1095,7 +1103,12 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   OCG_GUARD_END
 }
 
-void ocg_kkt_destroy(ocg_kkt* k) { delete k; }
+void ocg_kkt_destroy(ocg_kkt* k) {
+  if (!k) return;
+  ocg::mem::DeviceScope ds(k->ev->device);
+  cudaDeviceSynchronize();
+  delete k;
+}
 
 int ocg_kkt_dims(const ocg_kkt* k, int64_t* out) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
@@ -1139,6 +1152,7 @@ double* ocg_kkt_values(ocg_kkt* k) { return k ? k->val.p : nullptr; }
 int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
   if (!k || !sigma) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(k->ev->device);
   ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
                          k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s));
   k->ev->launches += k->n_src_long > 0 ? 2 : 1;
@@ -1149,6 +1163,7 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
 int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
   if (!k || !x || !y) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(k->ev->device);
   ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y,
                        {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
   k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
@@ -1159,6 +1174,7 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
 int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(k->ev->device);
   ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out,
                          {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
   k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
@@ -1169,6 +1185,7 @@ int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
 int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream s) {
   if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(k->ev->device);
   ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
                       k->n_slack, out, {k->jt_long.p, k->n_jt_long, k->jt_long_part.p}, st(s));
   k->ev->launches += k->n_jt_long > 0 ? 3 : 1;
@@ -1275,7 +1292,17 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
 
 extern "C" {
 
-void ocg_ldl_destroy(ocg_ldl* l) { delete l; }
+void ocg_ldl_destroy(ocg_ldl* l) {
+  if (!l) return;
+  ocg::mem::DeviceScope ds(l->kkt->ev->device);
+  cudaDeviceSynchronize();
+  delete l;
+}
+
+int ocg_release_cached_memory(int device) {
+  ocg::mem::trim(device);
+  return OCG_OK;
+}
 
 int ocg_ldl_info(const ocg_ldl* l, int64_t* out) {
   if (!l || !out) return fail(OCG_ERR_ARG, "null argument");
@@ -1290,6 +1317,7 @@ int ocg_ldl_info(const ocg_ldl* l, int64_t* out) {
 int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia, ocg_stream s) {
   if (!l) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(l->kkt->ev->device);
   const ocg::BandPlan& P = l->plan;
   ocg::dev::band_assemble(P, l->dev, l->kkt->val.p, l->buf.p, st(s));
   ocg::dev::band_factor(P, l->dev, l->buf.p, delta_w, delta_c, l->Dinv.p, l->inertia_parts.p, l->inertia.p, st(s));
@@ -1310,6 +1338,7 @@ int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia,
 int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
   if (!l || !rhs || !x) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(l->kkt->ev->device);
   const ocg::BandPlan& P = l->plan;
   ocg::dev::band_solve(P, l->dev, l->buf.p, l->Dinv.p, rhs, x, l->work.p, st(s));
   l->kkt->ev->launches += P.nseg > 1 ? 8 : 3;

@@ -30,6 +30,10 @@
 #include "devmem.hpp"
 #include "ipm_kernels.hpp"
 
+namespace ocg::hd {
+int set_error(int code, const std::string& msg);  // capi.cpp: ocg_last_error's message
+}
+
 namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
@@ -87,11 +91,22 @@ struct DVec {
     if (n) ckc(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
     ckc(cudaStreamSynchronize(s), "sync");
   }
+  // exchange whole blocks (pointer, length and the block size the cache files them under)
+  void swap(DVec& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(cap, o.cap);
+  }
+};
+
+// an instance whose data do not fit the model's structure (OCG_ERR_ARG)
+struct InvalidInstance : std::runtime_error {
+  using std::runtime_error::runtime_error;
 };
 
 class DeviceSolver {
  public:
-  DeviceSolver(ocg_model* model, const ocg_ipm_options& o, int device) : model_(model), o_(o) {
+  DeviceSolver(ocg_model* model, const ocg_ipm_options& o, int device) : model_(model), o_(o), device_(device) {
     Clock t;
     ckc(cudaSetDevice(device), "cudaSetDevice");
     ckc(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
@@ -108,6 +123,8 @@ class DeviceSolver {
     r_.time_plan_ldl = t3.elapsed();
   }
   ~DeviceSolver() {
+    ocg::mem::DeviceScope ds(device_);
+    if (s_) cudaStreamSynchronize(s_);
     if (ldl_) ocg_ldl_destroy(ldl_);
     if (kkt_) ocg_kkt_destroy(kkt_);
     if (ev_) ocg_eval_destroy(ev_);
@@ -115,6 +132,7 @@ class DeviceSolver {
   }
 
   int run(ocg_ipm_result* res, double* x_out);
+  int device() const { return device_; }
   // instance data for the next run (NULL = the model's own arrays)
   void set_instance(const ocg_ipm_options& o, const double* lvar, const double* uvar, const double* x0,
                     const double* lcon, const double* ucon) {
@@ -131,6 +149,7 @@ class DeviceSolver {
   bool allocated_ = false;
   ocg_model* model_;
   ocg_ipm_options o_;
+  int device_ = 0;
   cudaStream_t s_ = nullptr;
   ocg_eval* ev_ = nullptr;
   ocg_kkt* kkt_ = nullptr;
@@ -308,7 +327,14 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
     }
     for (size_t sl = 0; sl < nv; ++sl)
       if ((prim[sl] < 0) != (xlo[sl] == xhi[sl]))
-        throw std::runtime_error("instance bounds change which slots are fixed: the KKT structure differs");
+        throw InvalidInstance("instance bounds change which slots are fixed: the KKT structure differs");
+    // the slack map is the model's (eval.cpp:330-336): a kept equality row
+    // must stay an equality and a kept range row a range
+    for (size_t r = 0; r < mc; ++r)
+      if (dual[r] >= 0 && (lcon[r] == ucon[r]) != (slack[r] < 0))
+        throw InvalidInstance("instance row " + std::to_string(r) +
+                              (slack[r] < 0 ? " loosens an equality of the model into a range"
+                                            : " turns a range row of the model into an equality"));
   }
   std::vector<int64_t> free_slot(static_cast<size_t>(nfree_)), slack_of(static_cast<size_t>(nslack_)),
       dual_row(static_cast<size_t>(m_));
@@ -738,7 +764,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
           if (!eval_trial()) break;
           if (acceptable(alpha_soc)) {
             accepted = true;
-            std::swap(step_.p, step2_.p);
+            step_.swap(step2_);
             dir = step_.p;
             alpha = alpha_soc;
             break;
@@ -842,8 +868,9 @@ struct ocg_ipm_ctx {
 };
 
 int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out) {
-  if (!m || !out) return OCG_ERR_ARG;
+  if (!m || !out) return ocg::hd::set_error(OCG_ERR_ARG, "ocg_ipm_ctx_create: null argument");
   try {
+    ocg::mem::DeviceScope ds(device);
     ocg_ipm_options o;
     ocg_ipm_default_options(&o);
     auto c = std::make_unique<ocg_ipm_ctx>();
@@ -851,40 +878,41 @@ int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out) {
     *out = c.release();
     return OCG_OK;
   } catch (const std::exception& ex) {
-    std::fprintf(stderr, "ocg_ipm_ctx_create: %s\n", ex.what());
-    return OCG_ERR_CUDA;
+    return ocg::hd::set_error(OCG_ERR_CUDA, std::string("ocg_ipm_ctx_create: ") + ex.what());
   }
 }
 
-void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c) { delete c; }
+void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c) { delete c; }  // ~DeviceSolver makes its device current
 
 int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double* lvar, const double* uvar,
                       const double* x_start, const double* lcon, const double* ucon, ocg_ipm_result* out,
                       double* x_out) {
-  if (!c || !out) return OCG_ERR_ARG;
+  if (!c || !out) return ocg::hd::set_error(OCG_ERR_ARG, "ocg_ipm_ctx_solve: null argument");
   ocg_ipm_options o;
   ocg_ipm_default_options(&o);
   if (opts) o = *opts;
   try {
+    ocg::mem::DeviceScope ds(c->solver->device());
     c->solver->set_instance(o, lvar, uvar, x_start, lcon, ucon);
     return c->solver->run(out, x_out);
+  } catch (const InvalidInstance& ex) {
+    return ocg::hd::set_error(OCG_ERR_ARG, std::string("ocg_ipm_ctx_solve: ") + ex.what());
   } catch (const std::exception& ex) {
-    std::fprintf(stderr, "ocg_ipm_ctx_solve: %s\n", ex.what());
-    return OCG_ERR_CUDA;
+    return ocg::hd::set_error(OCG_ERR_CUDA, std::string("ocg_ipm_ctx_solve: ") + ex.what());
   }
 }
 
 int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out) {
-  if (!m || !out) return -1;
+  if (!m || !out) return ocg::hd::set_error(OCG_ERR_ARG, "ocg_ipm_solve: null argument");
   ocg_ipm_options o;
   ocg_ipm_default_options(&o);
   if (opts) o = *opts;
   try {
+    ocg::mem::DeviceScope ds(device);
     DeviceSolver solver(m, o, device);
     return solver.run(out, x_out);
   } catch (const std::exception& ex) {
-    std::fprintf(stderr, "ocg_ipm_solve: %s\n", ex.what());
-    return OCG_ERR_CUDA;
+    return ocg::hd::set_error(OCG_ERR_CUDA, std::string("ocg_ipm_solve: ") + ex.what());
   }
 }
 

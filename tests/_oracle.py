@@ -61,6 +61,10 @@ def ref_lib(which: str = "ref") -> C.CDLL:
             "ref_kkt_maps": (None, [vp] + [dp] * 6),
             "ref_kkt_assemble": (None, [vp, dp, dp]),
             "ref_kkt_matvec": (None, [vp, dp, dp, dp]),
+            "ref_kkt_symbolic_sizes": (None, [vp, dp]),
+            "ref_kkt_symbolic": (None, [vp, dp, dp, dp]),
+            "ref_kkt_factorize": (None, [vp, dp, C.c_double, C.c_double, dp, dp, dp, dp]),
+            "ref_kkt_factor_solve": (i32, [vp, dp, C.c_double, C.c_double, dp, dp]),
             "ref_solve": (i32, [vp, i32, i32, i32, C.c_double, dp]),
             "ref_synth_acceptance": (None, [vp, C.c_uint32, dp, dp]),
             "ref_synth_uniform": (None, [C.c_uint32, C.c_double, C.c_double, i64, dp]),
@@ -239,6 +243,35 @@ class RefKkt:
         y = np.empty(self.dim)
         self.L.ref_kkt_matvec(self.h, _p(val), _p(x), _p(y))
         return y
+
+    def symbolic(self) -> dict:
+        """KktAssembler::symbolic() (eval.cpp:442-471): perm, etree parent, Lp."""
+        sz = np.zeros(2, dtype=np.int64)
+        self.L.ref_kkt_symbolic_sizes(self.h, _p(sz))
+        n, lnz = (int(v) for v in sz)
+        out = dict(perm=np.empty(n, dtype=np.int64), parent=np.empty(n, dtype=np.int64),
+                   Lp=np.empty(n + 1, dtype=np.int64))
+        self.L.ref_kkt_symbolic(self.h, _p(out["perm"]), _p(out["parent"]), _p(out["Lp"]))
+        out["lnz"] = lnz
+        return out
+
+    def factorize(self, val, delta_w: float = 0.0, delta_c: float = 0.0) -> dict:
+        """sparse::factorize (ldl.cpp:139-213): D, Li, Lx in pivot order, inertia."""
+        lnz = self.symbolic()["lnz"]
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        D, Li, Lx = np.empty(self.dim), np.empty(lnz, dtype=np.int64), np.empty(lnz)
+        inertia = np.zeros(3, dtype=np.int64)
+        self.L.ref_kkt_factorize(self.h, _p(val), float(delta_w), float(delta_c), _p(D), _p(Li), _p(Lx),
+                                 _p(inertia))
+        return dict(D=D, Li=Li, Lx=Lx, inertia=tuple(int(v) for v in inertia))
+
+    def factor_solve(self, val, b, delta_w: float = 0.0, delta_c: float = 0.0):
+        """sparse::factorize + sparse::solve (ldl.cpp:222-247); None on zero pivots."""
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.dim)
+        ok = self.L.ref_kkt_factor_solve(self.h, _p(val), float(delta_w), float(delta_c), _p(b), _p(x))
+        return x if ok else None
 
 
 # ---- the C restatement (oracle/port, liboracle.so) ---------------------------

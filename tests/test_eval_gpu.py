@@ -50,36 +50,36 @@ def test_values_acceptance_recipe(name, N):
     ok_r, c_r = re.constraints(x)
     assert ec.eval_constraints(x, c) == ok_r
     if ok_r:
-        assert_close(c.cpu().numpy(), c_r, f"{name} c")
+        assert_close(c.cpu().numpy(), c_r, f"{name} c", model=name)
 
     ok_r, c_r, j_r = re.constraints_jacobian(x)
     assert ec.eval_constraints_jacobian(x, c) == ok_r
     if ok_r:
-        assert_close(c.cpu().numpy(), c_r, f"{name} c(cjac)")
-        assert_close(ec.jac_val.cpu().numpy(), j_r, f"{name} jac")
+        assert_close(c.cpu().numpy(), c_r, f"{name} c(cjac)", model=name)
+        assert_close(ec.jac_val.cpu().numpy(), j_r, f"{name} jac", model=name)
 
     ok_r, f_r = re.objective(x)
     ok, f = ec.eval_objective(x)
     assert ok == ok_r
     if ok_r:
-        assert_close(np.array([f]), np.array([f_r]), f"{name} f")
+        assert_close(np.array([f]), np.array([f_r]), f"{name} f", model=name)
 
     ok_r, g_r, gc_r = re.gradient(x)
     g = torch.empty(m.nvar, dtype=torch.float64, device=dev)
     assert ec.eval_gradient(x, g) == ok_r
     if ok_r:
-        assert_close(ec.grad_val.cpu().numpy(), gc_r, f"{name} grad coo")
-        assert_close(g.cpu().numpy(), g_r, f"{name} grad dense")
+        assert_close(ec.grad_val.cpu().numpy(), gc_r, f"{name} grad coo", model=name)
+        assert_close(g.cpu().numpy(), g_r, f"{name} grad dense", model=name)
 
     ok_r, h_r = re.hessian(x, lam)
     assert ec.eval_hessian(x, lam) == ok_r
     if ok_r:
-        assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} hess")
+        assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} hess", model=name)
         # max|H| is exact over our own values and within tolerance of the
         # reference's (the entries themselves agree to 1e-12, not bitwise)
         mh = ec.max_abs_hessian()
         assert mh == float(np.max(np.abs(ec.hess_val.cpu().numpy()))) if ec.hess_nnz else mh == 0.0
-        assert_close(np.array([mh]), np.array([re.max_abs_hessian()]), f"{name} max|H|")
+        assert_close(np.array([mh]), np.array([re.max_abs_hessian()]), f"{name} max|H|", model=name)
 
 
 @pytest.mark.parametrize("N", [1000])
@@ -92,14 +92,14 @@ def test_quadrotor_eval_recipe(N):
     c = torch.empty(m.m_con, dtype=torch.float64, device=ec.device)
     ok_r, c_r, j_r = re.constraints_jacobian(x)
     assert ok_r and ec.eval_constraints_jacobian(x, c)
-    st_j = assert_close(ec.jac_val.cpu().numpy(), j_r, "jac")
+    st_j = assert_close(ec.jac_val.cpu().numpy(), j_r, "jac", model="quadrotor")
     ok_r, h_r = re.hessian(x, lam)
     assert ok_r and ec.eval_hessian(x, lam)
-    st_h = assert_close(ec.hess_val.cpu().numpy(), h_r, "hess")
+    st_h = assert_close(ec.hess_val.cpu().numpy(), h_r, "hess", model="quadrotor")
     ok_r, f_r = re.objective(x)
     ok, f = ec.eval_objective(x)
     assert ok and ok_r
-    assert_close(np.array([f]), np.array([f_r]), "f")
+    assert_close(np.array([f]), np.array([f_r]), "f", model="quadrotor")
     print("quadrotor bit-exact fractions: jac", st_j["bit_exact"], "hess", st_h["bit_exact"])
 
 
@@ -133,14 +133,14 @@ def test_scaling_matches_reference(name):
     c = torch.empty(m.m_con, dtype=torch.float64, device=ec.device)
     ok_r, c_r, j_r = re.constraints_jacobian(x)
     assert ec.eval_constraints_jacobian(x, c) == ok_r
-    assert_close(ec.jac_val.cpu().numpy(), j_r, "scaled jac")
+    assert_close(ec.jac_val.cpu().numpy(), j_r, "scaled jac", model=name)
     ok_r, h_r = re.hessian(x, lam)
     assert ec.eval_hessian(x, lam) == ok_r
-    assert_close(ec.hess_val.cpu().numpy(), h_r, "scaled hess")
+    assert_close(ec.hess_val.cpu().numpy(), h_r, "scaled hess", model=name)
     ok_r, f_r = re.objective(x)
     ok, f = ec.eval_objective(x)
     assert ok == ok_r
-    assert_close(np.array([f]), np.array([f_r]), "scaled f")
+    assert_close(np.array([f]), np.array([f_r]), "scaled f", model=name)
 
 
 def test_domain_errors_flagged():
@@ -172,10 +172,10 @@ def test_euler_scheme():
         c = torch.empty(m.m_con, dtype=torch.float64, device=ec.device)
         ok_r, c_r, j_r = re.constraints_jacobian(x)
         assert ec.eval_constraints_jacobian(x, c) == ok_r
-        assert_close(ec.jac_val.cpu().numpy(), j_r, f"{name} euler jac")
+        assert_close(ec.jac_val.cpu().numpy(), j_r, f"{name} euler jac", model=name)
         ok_r, h_r = re.hessian(x, lam)
         assert ec.eval_hessian(x, lam) == ok_r
-        assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} euler hess")
+        assert_close(ec.hess_val.cpu().numpy(), h_r, f"{name} euler hess", model=name)
 
 
 @pytest.mark.parametrize("name", ["goddard", "quadrotor", "shuttle", "cart_pendulum"])
@@ -192,6 +192,6 @@ def test_values_against_c_restatement(name):
     ok, c_p, j_p = pe.constraints_jacobian(x)
     ok2, h_p = pe.hessian(x, lam)
     assert ok and ok2
-    assert_close(c.cpu().numpy(), c_p, f"{name} c")
-    assert_close(ec.jac_val.cpu().numpy(), j_p, f"{name} jac")
-    assert_close(ec.hess_val.cpu().numpy(), h_p, f"{name} hess")
+    assert_close(c.cpu().numpy(), c_p, f"{name} c", model=name)
+    assert_close(ec.jac_val.cpu().numpy(), j_p, f"{name} jac", model=name)
+    assert_close(ec.hess_val.cpu().numpy(), h_p, f"{name} hess", model=name)
