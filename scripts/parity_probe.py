@@ -28,7 +28,10 @@ def worst(got, ref, k=6):
     den = np.where(ref == 0, 1.0, np.abs(ref))
     err = np.abs(got - ref) / den
     idx = np.argsort(err)[::-1][:k]
-    return {"max_rel_nofloor": float(err.max()) if err.size else 0.0,
+    # smallest floor f with |got - ref| <= 1e-12 * max(|ref|, f * max|ref|) everywhere
+    bad = np.abs(got - ref) > 1e-12 * np.abs(ref)
+    need = float(np.max(np.abs(got - ref)[bad]) / (1e-12 * scale)) if bad.any() and scale > 0 else 0.0
+    return {"max_rel_nofloor": float(err.max()) if err.size else 0.0, "floor_needed": need,
             "n_over_1e-12": int((err > 1e-12).sum()), "n": int(ref.size), "bit_exact_frac": float(np.mean(got == ref)),
             "worst": [{"i": int(i), "ref": float(ref[i]), "got": float(got[i]), "rel": float(err[i]),
                        "ref_over_max": float(abs(ref[i]) / scale)} for i in idx]}
