@@ -244,6 +244,34 @@ int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia,
 /* x = (K + deltas)^{-1} rhs with the last factorization (device vectors) */
 int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s);
 
+/* Elimination orders of ocg_ldl_create_ex:
+ * OCG_LDL_BAND       the node-major band above (ocg_ldl_create; fast, parallel
+ *                    in time; its 1x1 pivots are not the reference's);
+ * OCG_LDL_REFERENCE  the reference's order: KktAssembler::symbolic's AMD
+ *                    ordering with the pivot_after_ deferral (eval.cpp:442-471,
+ *                    ldl.cpp:54-137), the same 1x1 pivots and zero-pivot rule
+ *                    as sparse::factorize (ldl.cpp:139-213), so inertia
+ *                    corrections follow the reference's. The sequential part
+ *                    (the elimination tree's chain) runs on one warp. */
+#define OCG_LDL_BAND 0
+#define OCG_LDL_REFERENCE 1
+int ocg_ldl_create_ex(ocg_kkt* k, int order, ocg_ldl** out);
+int ocg_ldl_order(const ocg_ldl* l);
+/* OCG_LDL_REFERENCE: nnz of L (sparse::SymbolicLdl::lnz); 0 for the band */
+int64_t ocg_ldl_factor_nnz(const ocg_ldl* l);
+/* OCG_LDL_REFERENCE: host copies of the last factorization in the reference's
+ * layout (LdlFactor: perm[dim], Lp[dim+1], Li[lnz], D[dim] by pivot position,
+ * Lx[lnz]); any pointer may be NULL. Synchronizes the device. */
+int ocg_ldl_factors(const ocg_ldl* l, int64_t* perm, int64_t* Lp, int64_t* Li, double* D, double* Lx);
+/* Host only (no device needed): the reference-order symbolic analysis of a
+ * lower-CSC KKT pattern colp[dim+1]/rowi (indices [0, n_free) free primal,
+ * [n_free, ntot) slacks, [ntot, dim) duals) -- KktAssembler::symbolic +
+ * sparse::analyze_ordered: perm[dim] (position -> index), etree parent[dim],
+ * Lp[dim+1], Li[*lnz] (pass Li = NULL to get *lnz first). Any output may be
+ * NULL. */
+int ocg_ldl_ref_symbolic(int64_t dim, const int64_t* colp, const int64_t* rowi, int64_t n_free, int64_t ntot,
+                         int64_t* perm, int64_t* parent, int64_t* Lp, int64_t* Li, int64_t* lnz);
+
 /* ---- device-resident interior-point solve -----------------------------------
  * ipm::solve (proj/src/ipm/solver.cpp:304-702, options solver.hpp:31-56): the
  * reference's filter line-search IPM with every vector on the device —
@@ -259,6 +287,7 @@ typedef struct {
   int refine_rounds;
   double refine_trigger;
   int verbose;
+  int kkt_order; /* OCG_LDL_BAND (default) or OCG_LDL_REFERENCE (ocg_ldl_create_ex) */
 } ocg_ipm_options;
 
 typedef struct {

@@ -13,6 +13,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libocgpu.so"
 OCG_OK = 0
 OCG_EVAL_DOMAIN = 1
 OCG_BUF_JAC, OCG_BUF_HESS, OCG_BUF_GRAD, OCG_BUF_ROWSCALE, OCG_BUF_OBJV = range(5)
+OCG_LDL_BAND, OCG_LDL_REFERENCE = 0, 1
 
 # every symbol include/octgpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -29,6 +30,7 @@ EXPORTS = [
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
+    "ocg_ldl_create_ex", "ocg_ldl_order", "ocg_ldl_factor_nnz", "ocg_ldl_factors", "ocg_ldl_ref_symbolic",
     "ocg_kkt_norm_inf", "ocg_ipm_default_options", "ocg_ipm_solve",
     "ocg_ipm_ctx_create", "ocg_ipm_ctx_destroy", "ocg_ipm_ctx_solve", "ocg_ipm_batch_solve",
 ]
@@ -45,7 +47,7 @@ class IpmOptions(C.Structure):
                 ("reg_initial_scale", C.c_double), ("reg_grow", C.c_double), ("reg_shrink", C.c_double),
                 ("reg_dual_scale", C.c_double), ("reg_dual_power", C.c_double), ("reg_max_delta", C.c_double),
                 ("scale", C.c_int), ("bound_relax_factor", C.c_double), ("refine_rounds", C.c_int),
-                ("refine_trigger", C.c_double), ("verbose", C.c_int)]
+                ("refine_trigger", C.c_double), ("verbose", C.c_int), ("kkt_order", C.c_int)]
 
 
 class IpmResult(C.Structure):
@@ -129,6 +131,11 @@ def _load() -> C.CDLL:
         "ocg_ldl_info": (i32, [vp, dp]),
         "ocg_ldl_factor": (i32, [vp, C.c_double, C.c_double, dp, vp]),
         "ocg_ldl_solve": (i32, [vp, dp, dp, vp]),
+        "ocg_ldl_create_ex": (i32, [vp, i32, C.POINTER(vp)]),
+        "ocg_ldl_order": (i32, [vp]),
+        "ocg_ldl_factor_nnz": (i64, [vp]),
+        "ocg_ldl_factors": (i32, [vp, dp, dp, dp, dp, dp]),
+        "ocg_ldl_ref_symbolic": (i32, [i64, dp, dp, i64, i64, dp, dp, dp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -17,9 +17,9 @@ LIB = PKG / "libocgpu.so"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
-HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp"]
-CUDA_SRCS = ["kernels.cu", "band.cu", "sepcr.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu"]
-HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp", "devmem.hpp"]
+HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp", "refldl.cpp"]
+CUDA_SRCS = ["kernels.cu", "band.cu", "sepcr.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu", "refldl.cu"]
+HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp", "devmem.hpp", "refldl.hpp"]
 
 
 def _run(cmd: list[str]) -> None:

@@ -1290,7 +1290,149 @@ int ocg::hd::ldl_create(ocg_kkt* k, int target, ocg_ldl** out) {
   OCG_GUARD_END
 }
 
+namespace {
+
+// the reference-order factorization's plan (refldl.hpp) on the device
+std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
+  auto R = std::make_unique<ocg_ldl::Ref>();
+  R->S = ocg::rl::analyze(k->dim, k->colp.data(), k->rowi.data(), k->n_free, k->ntot);
+  const ocg::rl::HostPlan H = ocg::rl::build_plan(R->S, k->colp.data(), k->rowi.data());
+  R->nleaf = static_cast<int64_t>(H.lf_pos.size());
+  R->nnl = static_cast<int64_t>(H.nl_pos.size());
+  auto up64 = [](DBuf<int64_t>& b, const std::vector<int64_t>& v) { b.upload(v.empty() ? std::vector<int64_t>{0} : v); };
+  auto up32 = [](DBuf<int32_t>& b, const std::vector<int32_t>& v) { b.upload(v.empty() ? std::vector<int32_t>{0} : v); };
+  up64(R->nl_pos, H.nl_pos);
+  up64(R->nl_foff, H.nl_foff);
+  up64(R->nl_soff, H.nl_soff);
+  up64(R->nl_voff, H.nl_voff);
+  up64(R->sc_ptr, H.sc_ptr);
+  up64(R->lf_pos, H.lf_pos);
+  up64(R->lf_aoff, H.lf_aoff);
+  up64(R->pa_ptr, H.pa_ptr);
+  up64(R->fl_ptr, H.fl_ptr);
+  up64(R->fl_lx, H.fl_lx);
+  up64(R->fl_col, H.fl_col);
+  up64(R->Lp, R->S.Lp);
+  up64(R->Li, R->S.Li);
+  up64(R->sc_dst, H.sc_dst);
+  up64(R->sc_dpos, H.sc_dpos);
+  up64(R->sc_ms, H.sc_ms);
+  up64(R->perm, R->S.perm);
+  up32(R->nl_f, H.nl_f);
+  up32(R->sc_child, H.sc_child);
+  up32(R->lf_f, H.lf_f);
+  up32(R->pa_j, H.pa_j);
+  up32(R->pa_leaf, H.pa_leaf);
+  up32(R->fl_j, H.fl_j);
+  up32(R->rel, H.rel);
+  R->primal.upload(H.primal.empty() ? std::vector<int8_t>{0} : H.primal);
+  const size_t dim = static_cast<size_t>(std::max<int64_t>(1, k->dim));
+  R->W.alloc(static_cast<size_t>(H.w_len));
+  R->stash.alloc(static_cast<size_t>(H.stash_len));
+  R->D.alloc(dim);
+  R->Dinv.alloc(dim);
+  R->Lx.alloc(static_cast<size_t>(std::max<int64_t>(1, H.lnz)));
+  R->y.alloc(dim);
+  R->xp.alloc(dim);
+  R->V.alloc(static_cast<size_t>(H.v_len));
+  R->Vs.alloc(static_cast<size_t>(H.stash_len));
+  R->inertia.alloc(3);
+  ocg::rl::Dev& d = R->dev;
+  d.dim = H.dim;
+  d.nnz = H.nnz;
+  d.lnz = H.lnz;
+  d.nleaf = R->nleaf;
+  d.nnl = R->nnl;
+  d.npa = static_cast<int64_t>(H.pa_j.size());
+  d.nfl = static_cast<int64_t>(H.fl_j.size());
+  d.fmax = H.fmax;
+  d.nl_pos = R->nl_pos.p;
+  d.nl_f = R->nl_f.p;
+  d.nl_foff = R->nl_foff.p;
+  d.nl_soff = R->nl_soff.p;
+  d.nl_voff = R->nl_voff.p;
+  d.sc_ptr = R->sc_ptr.p;
+  d.sc_child = R->sc_child.p;
+  d.lf_pos = R->lf_pos.p;
+  d.lf_f = R->lf_f.p;
+  d.lf_aoff = R->lf_aoff.p;
+  d.pa_j = R->pa_j.p;
+  d.pa_ptr = R->pa_ptr.p;
+  d.pa_leaf = R->pa_leaf.p;
+  d.fl_j = R->fl_j.p;
+  d.fl_ptr = R->fl_ptr.p;
+  d.fl_lx = R->fl_lx.p;
+  d.fl_col = R->fl_col.p;
+  d.Lp = R->Lp.p;
+  d.Li = R->Li.p;
+  d.rel = R->rel.p;
+  d.sc_dst = R->sc_dst.p;
+  d.sc_dpos = R->sc_dpos.p;
+  d.sc_ms = R->sc_ms.p;
+  d.perm = R->perm.p;
+  d.primal = R->primal.p;
+  d.w_len = H.w_len;
+  d.stash_len = H.stash_len;
+  d.v_len = H.v_len;
+  return R;
+}
+
+}  // namespace
+
 extern "C" {
+
+int ocg_ldl_create_ex(ocg_kkt* k, int order, ocg_ldl** out) {
+  if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
+  if (order == OCG_LDL_BAND) return ocg_ldl_create(k, out);
+  if (order != OCG_LDL_REFERENCE) return fail(OCG_ERR_ARG, "ocg_ldl_create_ex: unknown order");
+  OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(k->ev->device);
+  auto L = std::make_unique<ocg_ldl>();
+  L->kkt = k;
+  L->plan.dim = k->dim;
+  L->ref = make_ref_ldl(k);
+  *out = L.release();
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_ldl_order(const ocg_ldl* l) { return l && l->ref ? OCG_LDL_REFERENCE : OCG_LDL_BAND; }
+
+int64_t ocg_ldl_factor_nnz(const ocg_ldl* l) { return l && l->ref ? static_cast<int64_t>(l->ref->S.Li.size()) : 0; }
+
+int ocg_ldl_factors(const ocg_ldl* l, int64_t* perm, int64_t* Lp, int64_t* Li, double* D, double* Lx) {
+  if (!l) return fail(OCG_ERR_ARG, "null argument");
+  if (!l->ref) return fail(OCG_ERR_STATE, "ocg_ldl_factors: not a reference-order factorization");
+  OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(l->kkt->ev->device);
+  const auto& R = *l->ref;
+  const size_t n = R.S.perm.size(), lnz = R.S.Li.size();
+  if (perm) std::copy(R.S.perm.begin(), R.S.perm.end(), perm);
+  if (Lp) std::copy(R.S.Lp.begin(), R.S.Lp.end(), Lp);
+  if (Li) std::copy(R.S.Li.begin(), R.S.Li.end(), Li);
+  ck(cudaDeviceSynchronize(), "sync");
+  if (D && n) ck(cudaMemcpy(D, R.D.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D d2h");
+  if (Lx && lnz) ck(cudaMemcpy(Lx, R.Lx.p, lnz * sizeof(double), cudaMemcpyDeviceToHost), "Lx d2h");
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_ldl_ref_symbolic(int64_t dim, const int64_t* colp, const int64_t* rowi, int64_t n_free, int64_t ntot,
+                         int64_t* perm, int64_t* parent, int64_t* Lp, int64_t* Li, int64_t* lnz) {
+  if (dim < 0 || (dim > 0 && (!colp || !rowi)) || n_free < 0 || ntot < n_free || ntot > dim)
+    return fail(OCG_ERR_ARG, "ocg_ldl_ref_symbolic: bad arguments");
+  try {
+    const ocg::rl::Symbolic S = ocg::rl::analyze(dim, colp, rowi, n_free, ntot);
+    if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+    if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+    if (Lp) std::copy(S.Lp.begin(), S.Lp.end(), Lp);
+    if (Li) std::copy(S.Li.begin(), S.Li.end(), Li);
+    if (lnz) *lnz = static_cast<int64_t>(S.Li.size());
+    return OCG_OK;
+  } catch (const std::exception& ex) {
+    return fail(OCG_ERR_ARG, std::string("ocg_ldl_ref_symbolic: ") + ex.what());
+  }
+}
 
 void ocg_ldl_destroy(ocg_ldl* l) {
   if (!l) return;
@@ -1306,6 +1448,14 @@ int ocg_release_cached_memory(int device) {
 
 int ocg_ldl_info(const ocg_ldl* l, int64_t* out) {
   if (!l || !out) return fail(OCG_ERR_ARG, "null argument");
+  if (l->ref) {  // reference order: no segments; "bandwidth" = the largest column count of L
+    out[0] = l->ref->S.dim;
+    out[1] = 0;
+    out[2] = l->ref->dev.fmax - 1;
+    out[3] = 0;
+    out[4] = l->factorizations;
+    return OCG_OK;
+  }
   out[0] = l->plan.dim;
   out[1] = l->plan.nseg;
   out[2] = l->plan.b;
@@ -1318,6 +1468,22 @@ int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia,
   if (!l) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(l->kkt->ev->device);
+  if (l->ref) {
+    auto& R = *l->ref;
+    ocg::rl::factor(R.dev, l->kkt->val.p, delta_w, delta_c, R.W.p, R.stash.p, R.D.p, R.Dinv.p, R.Lx.p, R.inertia.p,
+                    st(s));
+    l->kkt->ev->launches += 2 + (R.nleaf > 0) + (R.dev.npa > 0) + (R.nnl > 0);
+    l->delta_w = delta_w;
+    l->delta_c = delta_c;
+    ++l->factorizations;
+    if (inertia) {
+      unsigned long long h[3];
+      ck(cudaMemcpyAsync(h, R.inertia.p, sizeof h, cudaMemcpyDeviceToHost, st(s)), "inertia d2h");
+      ck(cudaStreamSynchronize(st(s)), "sync");
+      for (int i = 0; i < 3; ++i) inertia[i] = static_cast<int64_t>(h[i]);
+    }
+    return OCG_OK;
+  }
   const ocg::BandPlan& P = l->plan;
   ocg::dev::band_assemble(P, l->dev, l->kkt->val.p, l->buf.p, st(s));
   ocg::dev::band_factor(P, l->dev, l->buf.p, delta_w, delta_c, l->Dinv.p, l->inertia_parts.p, l->inertia.p, st(s));
@@ -1339,6 +1505,12 @@ int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
   if (!l || !rhs || !x) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(l->kkt->ev->device);
+  if (l->ref) {
+    auto& R = *l->ref;
+    ocg::rl::solve(R.dev, R.Dinv.p, R.Lx.p, rhs, x, R.y.p, R.xp.p, R.V.p, R.Vs.p, st(s));
+    l->kkt->ev->launches += 2 + (R.dev.nfl > 0) + (R.nnl > 0 ? 3 : 0) + (R.nleaf > 0);
+    return OCG_OK;
+  }
   const ocg::BandPlan& P = l->plan;
   ocg::dev::band_solve(P, l->dev, l->buf.p, l->Dinv.p, rhs, x, l->work.p, st(s));
   l->kkt->ev->launches += P.nseg > 1 ? 8 : 3;

@@ -19,6 +19,7 @@
 #include "jit.hpp"
 #include "model.hpp"
 #include "plan.hpp"
+#include "refldl.hpp"
 
 namespace ocg::hd {
 
@@ -198,6 +199,19 @@ struct ocg_ldl {
   ocg::dev::BandDev dev;
   double delta_w = 0.0, delta_c = 0.0;
   int64_t factorizations = 0;
+  // OCG_LDL_REFERENCE: the reference's elimination order (refldl.hpp) instead of the band
+  struct Ref {
+    ocg::rl::Symbolic S;
+    int64_t nleaf = 0, nnl = 0;
+    DBuf<int64_t> nl_pos, nl_foff, nl_soff, nl_voff, sc_ptr, lf_pos, lf_aoff, pa_ptr, fl_ptr, fl_lx, fl_col, Lp, Li,
+        sc_dst, sc_dpos, sc_ms, perm;
+    DBuf<int32_t> nl_f, sc_child, lf_f, pa_j, pa_leaf, fl_j, rel;
+    DBuf<int8_t> primal;
+    DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs;
+    DBuf<unsigned long long> inertia;
+    ocg::rl::Dev dev;
+  };
+  std::unique_ptr<Ref> ref;
 };
 
 

@@ -118,14 +118,12 @@ class DeviceSolver {
     Clock t2;
     cko(ocg_kkt_create(model, ev_, &kkt_), "kkt_create");
     r_.time_plan_kkt = t2.elapsed();
-    Clock t3;
-    cko(ocg_ldl_create(kkt_, &ldl_), "ldl_create");
-    r_.time_plan_ldl = t3.elapsed();
   }
   ~DeviceSolver() {
     ocg::mem::DeviceScope ds(device_);
     if (s_) cudaStreamSynchronize(s_);
-    if (ldl_) ocg_ldl_destroy(ldl_);
+    for (ocg_ldl* l : ldls_)
+      if (l) ocg_ldl_destroy(l);
     if (kkt_) ocg_kkt_destroy(kkt_);
     if (ev_) ocg_eval_destroy(ev_);
     if (s_) cudaStreamDestroy(s_);
@@ -153,7 +151,20 @@ class DeviceSolver {
   cudaStream_t s_ = nullptr;
   ocg_eval* ev_ = nullptr;
   ocg_kkt* kkt_ = nullptr;
-  ocg_ldl* ldl_ = nullptr;
+  ocg_ldl* ldl_ = nullptr;      // the factorization of this run: ldls_[o_.kkt_order]
+  ocg_ldl* ldls_[2] = {nullptr, nullptr};
+  // the factorization plan of the requested elimination order, built on first use
+  void select_ldl() {
+    const int order = o_.kkt_order == OCG_LDL_REFERENCE ? OCG_LDL_REFERENCE : OCG_LDL_BAND;
+    if (!ldls_[order]) {
+      Clock t;
+      cko(ocg_ldl_create_ex(kkt_, order, &ldls_[order]), "ldl_create");
+      plan_ldl_s_[order] = t.elapsed();
+    }
+    ldl_ = ldls_[order];
+    r_.time_plan_ldl = plan_ldl_s_[order];
+  }
+  double plan_ldl_s_[2] = {0.0, 0.0};
   ocg::ipmdev::Iter P_;
   ocg::ipmdev::Scratch sc_;
 
@@ -611,6 +622,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     theta_min_ = 0.0;
     theta_max_ = kInf;
   }
+  select_ldl();
   std::vector<double> row_scale;
   mu_ = o_.mu_init;
   tau_ = std::max(o_.tau_min, 1.0 - mu_);
@@ -861,6 +873,7 @@ void ocg_ipm_default_options(ocg_ipm_options* o) {
   o->refine_rounds = 5;
   o->refine_trigger = 1e-8;
   o->verbose = 0;
+  o->kkt_order = OCG_LDL_BAND;
 }
 
 struct ocg_ipm_ctx {

@@ -355,12 +355,26 @@ def _cuda_memcpy_d2d(dst: int, src: int, nbytes: int) -> None:
 
 class BandLdl:
     """Device LDL^T of the KKT matrix (include/octgpu.h ocg_ldl_*): the
-    stand-in for sparse::factorize/solve and for cuDSS."""
+    stand-in for sparse::factorize/solve and for cuDSS. order="band" (default)
+    is the time-partitioned band; order="reference" keeps the reference's
+    elimination order and 1x1 pivots (ocg_ldl_create_ex, OCG_LDL_REFERENCE)."""
 
-    def __init__(self, kkt: KktAssembler):
+    def __init__(self, kkt: KktAssembler, order: str = "band"):
         h = C.c_void_p()
-        check(LIB.ocg_ldl_create(kkt._h, C.byref(h)), "ocg_ldl_create")
-        self._h, self.kkt = h, kkt
+        code = {"band": _lib.OCG_LDL_BAND, "reference": _lib.OCG_LDL_REFERENCE}[order]
+        check(LIB.ocg_ldl_create_ex(kkt._h, code, C.byref(h)), "ocg_ldl_create_ex")
+        self._h, self.kkt, self.order = h, kkt, order
+
+    def factors(self) -> dict:
+        """order="reference": the last factorization in the reference's LdlFactor
+        layout: perm, Lp, Li, D (by pivot position), Lx."""
+        dim, lnz = self.kkt.dim, int(LIB.ocg_ldl_factor_nnz(self._h))
+        out = dict(perm=np.empty(dim, dtype=np.int64), Lp=np.empty(dim + 1, dtype=np.int64),
+                   Li=np.empty(max(lnz, 1), dtype=np.int64), D=np.empty(dim), Lx=np.empty(max(lnz, 1)))
+        check(LIB.ocg_ldl_factors(self._h, *(out[k].ctypes.data for k in ("perm", "Lp", "Li", "D", "Lx"))),
+              "ocg_ldl_factors")
+        out["Li"], out["Lx"] = out["Li"][:lnz], out["Lx"][:lnz]
+        return out
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -388,6 +402,35 @@ class BandLdl:
 STATUS = {0: "optimal", 1: "max_iter", 2: "infeasible_detected", 3: "eval_error"}
 
 
+def ref_symbolic(colp, rowi, n_free: int, ntot: int) -> dict:
+    """Host-only reference-order symbolic analysis (ocg_ldl_ref_symbolic):
+    KktAssembler::symbolic + sparse::analyze_ordered on a lower-CSC KKT
+    pattern -> perm, parent (etree), Lp, Li. No device needed."""
+    colp = np.ascontiguousarray(colp, dtype=np.int64)
+    rowi = np.ascontiguousarray(rowi, dtype=np.int64)
+    dim = len(colp) - 1
+    lnz = np.zeros(1, dtype=np.int64)
+    out = dict(perm=np.empty(dim, dtype=np.int64), parent=np.empty(dim, dtype=np.int64),
+               Lp=np.empty(dim + 1, dtype=np.int64))
+    check(LIB.ocg_ldl_ref_symbolic(dim, colp.ctypes.data, rowi.ctypes.data, int(n_free), int(ntot),
+                                   out["perm"].ctypes.data, out["parent"].ctypes.data, out["Lp"].ctypes.data, None,
+                                   lnz.ctypes.data), "ocg_ldl_ref_symbolic")
+    Li = np.empty(max(int(lnz[0]), 1), dtype=np.int64)
+    check(LIB.ocg_ldl_ref_symbolic(dim, colp.ctypes.data, rowi.ctypes.data, int(n_free), int(ntot), None, None, None,
+                                   Li.ctypes.data, lnz.ctypes.data), "ocg_ldl_ref_symbolic")
+    out["Li"] = Li[:int(lnz[0])]
+    return out
+
+
+def _kkt_order(options: dict) -> dict:
+    """kkt_order may be given as "band" / "reference" (IpmOptions.kkt_order)."""
+    v = options.get("kkt_order")
+    if isinstance(v, str):
+        options = dict(options)
+        options["kkt_order"] = {"band": _lib.OCG_LDL_BAND, "reference": _lib.OCG_LDL_REFERENCE}[v]
+    return options
+
+
 def solve(model: Model, device: int = 0, return_x: bool = False, **options) -> dict:
     """ipm::solve on the device (include/octgpu.h ocg_ipm_solve): the
     reference's filter line-search IPM (proj/src/ipm/solver.cpp) with every
@@ -397,7 +440,7 @@ def solve(model: Model, device: int = 0, return_x: bool = False, **options) -> d
         raise RuntimeError("octgpu solve needs a CUDA device (no CPU fallback)")
     o = _lib.IpmOptions()
     LIB.ocg_ipm_default_options(C.byref(o))
-    for k, v in options.items():
+    for k, v in _kkt_order(options).items():
         if not hasattr(o, k):
             raise TypeError(f"unknown IPM option {k!r}")
         setattr(o, k, type(getattr(o, k))(v))
@@ -426,7 +469,7 @@ def solve_batch(model: Model, instances: list[Model] | None = None, n: int | Non
         raise RuntimeError("octgpu solve_batch needs a CUDA device (no CPU fallback)")
     o = _lib.IpmOptions()
     LIB.ocg_ipm_default_options(C.byref(o))
-    for k, v in options.items():
+    for k, v in _kkt_order(options).items():
         if not hasattr(o, k):
             raise TypeError(f"unknown IPM option {k!r}")
         setattr(o, k, type(getattr(o, k))(v))
@@ -488,7 +531,7 @@ class Solver:
     def solve(self, instance: Model | None = None, return_x: bool = False, **options) -> dict:
         o = _lib.IpmOptions()
         LIB.ocg_ipm_default_options(C.byref(o))
-        for k, v in options.items():
+        for k, v in _kkt_order(options).items():
             if not hasattr(o, k):
                 raise TypeError(f"unknown IPM option {k!r}")
             setattr(o, k, type(getattr(o, k))(v))
