@@ -1302,6 +1302,7 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   auto up64 = [](DBuf<int64_t>& b, const std::vector<int64_t>& v) { b.upload(v.empty() ? std::vector<int64_t>{0} : v); };
   auto up32 = [](DBuf<int32_t>& b, const std::vector<int32_t>& v) { b.upload(v.empty() ? std::vector<int32_t>{0} : v); };
   up64(R->nl_pos, H.nl_pos);
+  up64(R->nl_lp, H.nl_lp);
   up64(R->nl_foff, H.nl_foff);
   up64(R->nl_soff, H.nl_soff);
   up64(R->nl_voff, H.nl_voff);
@@ -1326,6 +1327,7 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   up32(R->fl_j, H.fl_j);
   up32(R->rel, H.rel);
   R->primal.upload(H.primal.empty() ? std::vector<int8_t>{0} : H.primal);
+  R->rec.upload(H.rec.empty() ? std::vector<ocg::rl::ColRec>(1) : H.rec);
   const size_t dim = static_cast<size_t>(std::max<int64_t>(1, k->dim));
   R->W.alloc(static_cast<size_t>(H.w_len));
   R->stash.alloc(static_cast<size_t>(H.stash_len));
@@ -1346,7 +1348,9 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   d.npa = static_cast<int64_t>(H.pa_j.size());
   d.nfl = static_cast<int64_t>(H.fl_j.size());
   d.fmax = H.fmax;
+  d.rec = R->rec.p;
   d.nl_pos = R->nl_pos.p;
+  d.nl_lp = R->nl_lp.p;
   d.nl_f = R->nl_f.p;
   d.nl_foff = R->nl_foff.p;
   d.nl_soff = R->nl_soff.p;

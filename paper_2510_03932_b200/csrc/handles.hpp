@@ -203,10 +203,11 @@ struct ocg_ldl {
   struct Ref {
     ocg::rl::Symbolic S;
     int64_t nleaf = 0, nnl = 0;
-    DBuf<int64_t> nl_pos, nl_foff, nl_soff, nl_voff, sc_ptr, lf_pos, lf_aoff, pa_ptr, fl_ptr, fl_lx, fl_col, Lp, Li,
+    DBuf<int64_t> nl_pos, nl_lp, nl_foff, nl_soff, nl_voff, sc_ptr, lf_pos, lf_aoff, pa_ptr, fl_ptr, fl_lx, fl_col, Lp, Li,
         sc_dst, sc_dpos, sc_ms, perm;
     DBuf<int32_t> nl_f, sc_child, lf_f, pa_j, pa_leaf, fl_j, rel;
     DBuf<int8_t> primal;
+    DBuf<ocg::rl::ColRec> rec;
     DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs;
     DBuf<unsigned long long> inertia;
     ocg::rl::Dev dev;

@@ -199,6 +199,7 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
     if (has_child[static_cast<size_t>(k)]) {
       jidx[static_cast<size_t>(k)] = static_cast<int64_t>(H.nl_pos.size());
       H.nl_pos.push_back(k);
+      H.nl_lp.push_back(S.Lp[static_cast<size_t>(k)]);
       H.nl_f.push_back(static_cast<int32_t>(f));
     } else {
       lidx[static_cast<size_t>(k)] = static_cast<int64_t>(H.lf_pos.size());
@@ -330,6 +331,20 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
         H.sc_dst[static_cast<size_t>(p)] = H.lf_aoff[static_cast<size_t>(lidx[static_cast<size_t>(lo)])] + r;
       }
     }
+  // packed per-column records of the warp walks (32-bit fields)
+  if (H.lnz >= (int64_t{1} << 31) || dim >= (int64_t{1} << 31) || H.stash_len >= (int64_t{1} << 31))
+    throw std::runtime_error("reference-order LDL: factor too large for the 32-bit column records");
+  H.rec.resize(static_cast<size_t>(nnl));
+  for (int64_t j = 0; j < nnl; ++j) {
+    ColRec& r = H.rec[static_cast<size_t>(j)];
+    r.foff = H.nl_foff[static_cast<size_t>(j)];
+    r.lp = static_cast<int>(H.nl_lp[static_cast<size_t>(j)]);
+    r.pos = static_cast<int>(H.nl_pos[static_cast<size_t>(j)]);
+    r.f = H.nl_f[static_cast<size_t>(j)];
+    r.soff = static_cast<int>(H.nl_soff[static_cast<size_t>(j)]);
+    r.sc0 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j)]);
+    r.sc1 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j) + 1]);
+  }
   H.primal.resize(n);
   for (size_t k = 0; k < n; ++k) H.primal[k] = S.perm[k] < S.ntot ? 1 : 0;
   return H;

@@ -127,82 +127,424 @@ __device__ void build_tables(unsigned char* ta, unsigned char* tb) {
     }
 }
 
-__global__ void __launch_bounds__(32) chain_factor_k(Dev P, double* __restrict__ W, double* __restrict__ stash,
-                                                     double* __restrict__ D, double* __restrict__ Dinv,
-                                                     double* __restrict__ Lx, unsigned long long* __restrict__ inertia) {
-  __shared__ unsigned char ta[kTab], tb[kTab];
-  build_tables(ta, tb);
+// ---- the chain: one warp, columns streamed through a ring of shared-memory
+// slots by cp.async (LDGSTS) NS-1 columns ahead ----------------------------------
+
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_n() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// wait until at most n groups are pending (n <= 14)
+__device__ __forceinline__ void cp_wait(int n) {
+  switch (n) {
+    case 0: cp_wait_n<0>(); break;
+    case 1: cp_wait_n<1>(); break;
+    case 2: cp_wait_n<2>(); break;
+    case 3: cp_wait_n<3>(); break;
+    case 4: cp_wait_n<4>(); break;
+    case 5: cp_wait_n<5>(); break;
+    case 6: cp_wait_n<6>(); break;
+    case 7: cp_wait_n<7>(); break;
+    case 8: cp_wait_n<8>(); break;
+    case 9: cp_wait_n<9>(); break;
+    case 10: cp_wait_n<10>(); break;
+    case 11: cp_wait_n<11>(); break;
+    case 12: cp_wait_n<12>(); break;
+    case 13: cp_wait_n<13>(); break;
+    default: cp_wait_n<14>(); break;
+  }
+}
+
+// Per chain column metadata (Dev::rec): streamed into a shared-memory ring of
+// kMetaRing records two 32-column blocks ahead of the walk.
+constexpr int kMetaRing = 128;
+
+// copy the records of walk steps [blk*32, blk*32+32) (columns in walking
+// direction) into the meta ring
+__device__ __forceinline__ void issue_meta(const Dev& P, int dir, long long blk, ColRec* ring) {
+  const long long k = blk * 32 + threadIdx.x;
+  if (k < P.nnl) {
+    const long long c = dir > 0 ? k : P.nnl - 1 - k;
+    ColRec* dst = ring + (k & (kMetaRing - 1));
+    const ColRec* src = P.rec + c;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst)) + 16u),
+                 "l"(reinterpret_cast<const char*>(src) + 16)
+                 : "memory");
+  }
+}
+// meta blocks 0 and 1 before the walk starts
+__device__ __forceinline__ void meta_prologue(const Dev& P, int dir, ColRec* ring) {
+  issue_meta(P, dir, 0, ring);
+  issue_meta(P, dir, 1, ring);
+  cp_commit();
+  cp_wait(0);
   __syncwarp();
+}
+
+__device__ __forceinline__ int tri32(int a) { return a * (a + 1) / 2; }
+__device__ __forceinline__ int next_slot(int s, int ns) { return s + 1 == ns ? 0 : s + 1; }
+
+// factor slot: [front: tri(f) packed lower + f diagonal maxima][rel: f-1 int32]
+__device__ __forceinline__ void issue_factor_slot(const Dev& P, const double* W, const ColRec& m, double* slot) {
+  const int f = m.f;
+  const int nf = tri32(f) + f;
+  const double* src = W + m.foff;
+  for (int i = threadIdx.x; i < nf; i += 32) cp8(slot + i, src + i);
+  int* rel = reinterpret_cast<int*>(slot + nf);
+  for (int i = threadIdx.x; i < f - 1; i += 32) cp4(rel + i, P.rel + m.lp + i);
+}
+
+__global__ void __launch_bounds__(32) chain_factor_k(Dev P, int ns, int slotd, const double* __restrict__ W,
+                                                     double* __restrict__ stash, double* __restrict__ D,
+                                                     double* __restrict__ Dinv, double* __restrict__ Lx,
+                                                     unsigned long long* __restrict__ inertia) {
+  __shared__ unsigned char ta[kTab], tb[kTab];
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  extern __shared__ double slots[];
+  build_tables(ta, tb);
   const int lane = threadIdx.x;
+  const long long n = P.nnl;
+  const int L = ns - 1;  // slot lookahead
+  meta_prologue(P, 1, ring);
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue_factor_slot(P, W, ring[q], slots + q * slotd);
+    cp_commit();
+  }
+  // the lane's first update-matrix entry (a, b): fixed for the whole walk
+  const int ua = ta[lane], ub = tb[lane];
   unsigned long long c[3] = {0, 0, 0};
-  for (int64_t j = 0; j < P.nnl; ++j) {
-    const int64_t pos = P.nl_pos[j];
-    const int f = P.nl_f[j];
-    double* F = W + P.nl_foff[j];
-    double* ms = F + tri(f);
-    const int64_t lp = P.Lp[pos];
-    const int32_t* r = P.rel + lp;
-    // update matrices of children that were not the previous column
-    for (int64_t q = P.sc_ptr[j]; q < P.sc_ptr[j + 1]; ++q) {
-      const int cj = P.sc_child[q];
-      const int fc = P.nl_f[cj];
-      const double* Us = stash + P.nl_soff[cj];
-      const int32_t* rc = P.rel + P.Lp[P.nl_pos[cj]];
-      const int tu = (fc - 1) * fc / 2;
+  int sj = 0, sa = L % ns;  // slots of step j and of step j + L
+  for (long long j = 0; j < n; ++j) {
+    if ((j & 31) == 0) issue_meta(P, 1, (j >> 5) + 2, ring);
+    if (j + L < n) issue_factor_slot(P, W, ring[(j + L) & (kMetaRing - 1)], slots + sa * slotd);
+    cp_commit();
+    cp_wait(L - 1);  // steps j and j+1 have landed
+    __syncwarp();
+    const ColRec m = ring[j & (kMetaRing - 1)];
+    const int f = m.f;
+    double* F = slots + sj * slotd;
+    const int tf = tri32(f);
+    double* ms = F + tf;
+    const int* r = reinterpret_cast<const int*>(ms + f);
+    // update matrices of children that were not the previous column (global stash)
+    for (int q = m.sc0; q < m.sc1; ++q) {
+      const ColRec mc = P.rec[P.sc_child[q]];
+      const int32_t* rc = P.rel + mc.lp;
+      const double* Us = stash + mc.soff;
+      const int tu = (mc.f - 1) * mc.f / 2;
       for (int u = lane; u < tu; u += 32) {
-        const int64_t e = tri(rc[ta[u] - 1]) + rc[tb[u] - 1];
+        const int e = tri32(rc[ta[u] - 1]) + rc[tb[u] - 1];
         F[e] = __dadd_rn(F[e], Us[u]);
       }
-      for (int a = lane; a < fc - 1; a += 32) ms[rc[a]] = fmax(ms[rc[a]], Us[tu + a]);
+      for (int a = lane; a < mc.f - 1; a += 32) ms[rc[a]] = fmax(ms[rc[a]], Us[tu + a]);
       __syncwarp();
     }
     const double d = F[0];
     const bool zero = zero_pivot(d, ms[0]);
     const double dinv = zero ? 0.0 : __drcp_rn(d);
     if (lane == 0) {
-      D[pos] = d;
-      Dinv[pos] = dinv;
+      D[m.pos] = d;
+      Dinv[m.pos] = dinv;
       count_pivot(d, zero, c);
     }
-    for (int t = lane + 1; t < f; t += 32) Lx[lp + t - 1] = __dmul_rn(F[tri(t)], dinv);
-    const int64_t so = P.nl_soff[j];
-    if (so != kRoot) {
-      double* Fn = nullptr;
-      double* msn = nullptr;
-      double* Us = nullptr;
-      if (so == kChain) {
-        const int fn = P.nl_f[j + 1];
-        Fn = W + P.nl_foff[j + 1];
-        msn = Fn + tri(fn);
-      } else {
-        Us = stash + so;
-      }
-      const int tu = (f - 1) * f / 2;
+    const int sn = next_slot(sj, ns);
+    double* Fn = nullptr;
+    double* msn = nullptr;
+    double* Us = nullptr;
+    if (m.soff == kChain) {
+      Fn = slots + sn * slotd;
+      msn = Fn + tri32(ring[(j + 1) & (kMetaRing - 1)].f);
+    } else if (m.soff >= 0) {
+      Us = stash + m.soff;
+    }
+    // L's column and the diagonal maxima of the update matrix: rows 1..f-1
+    for (int a = lane + 1; a < f; a += 32) {
+      const double Fa0 = F[tri32(a)];
+      const double l = __dmul_rn(Fa0, dinv);
+      Lx[m.lp + a - 1] = l;
+      const double mx = fmax(ms[a], fabs(__dmul_rn(l, Fa0)));
+      if (Fn)
+        msn[r[a - 1]] = fmax(msn[r[a - 1]], mx);
+      else if (Us)
+        Us[tf - f + a - 1] = mx;  // after the (f-1)f/2 entries
+    }
+    if (Fn || Us) {
+      const int tu = tf - f;  // (f-1) f / 2
       for (int u = lane; u < tu; u += 32) {
-        const int a = ta[u], b = tb[u];
-        const double Lb = __dmul_rn(F[tri(b)], dinv);
-        const double U = __dsub_rn(F[tri(a) + b], __dmul_rn(Lb, F[tri(a)]));
+        const int a = u == lane ? ua : ta[u], b = u == lane ? ub : tb[u];
+        const double Lb = __dmul_rn(F[tri32(b)], dinv);
+        const double U = __dsub_rn(F[tri32(a) + b], __dmul_rn(Lb, F[tri32(a)]));
         if (Fn) {
-          const int64_t e = tri(r[a - 1]) + r[b - 1];
+          const int e = tri32(r[a - 1]) + r[b - 1];
           Fn[e] = __dadd_rn(Fn[e], U);
         } else {
           Us[u] = U;
         }
       }
-      for (int a = lane + 1; a < f; a += 32) {
-        const double Fa0 = F[tri(a)];
-        const double m = fmax(ms[a], fabs(__dmul_rn(__dmul_rn(Fa0, dinv), Fa0)));
-        if (Fn)
-          msn[r[a - 1]] = fmax(msn[r[a - 1]], m);
-        else
-          Us[tu + a - 1] = m;
-      }
     }
     __syncwarp();
+    sj = sn;
+    sa = next_slot(sa, ns);
   }
+  cp_wait(0);
   if (lane == 0)
     for (int q = 0; q < 3; ++q)
       if (c[q]) atomicAdd(inertia + q, c[q]);
+}
+
+// ---- small fronts (f <= FM, FM <= 16): fixed slot layout, every lane owns
+// fixed update-matrix entries and rows; no loops over the front ------------------
+
+template <int FM>
+struct Small {
+  static constexpr int TF = FM * (FM + 1) / 2;     // packed front
+  static constexpr int TU = (FM - 1) * FM / 2;     // packed update matrix
+  static constexpr int UPL = (TU + 31) / 32;       // update entries per lane
+  static constexpr int FSLOT = TF + FM + FM / 2 + 1;  // [front TF][maxima FM][rel FM-1 ints]
+  static constexpr int VSLOT = 3 * FM + 2;            // solves
+};
+constexpr int kSmallSlots = 8;
+
+template <int FM>
+__global__ void __launch_bounds__(32) chain_factor_small_k(Dev P, const double* __restrict__ W,
+                                                           double* __restrict__ stash, double* __restrict__ D,
+                                                           double* __restrict__ Dinv, double* __restrict__ Lx,
+                                                           unsigned long long* __restrict__ inertia) {
+  using S = Small<FM>;
+  constexpr int NS = kSmallSlots, L = NS - 1;
+  __shared__ unsigned char ta[kTab], tb[kTab];
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  __shared__ __align__(16) double slots[NS * S::FSLOT];
+  build_tables(ta, tb);
+  const int lane = threadIdx.x;
+  const long long n = P.nnl;
+  meta_prologue(P, 1, ring);
+  auto issue = [&](const ColRec& m, double* slot) {
+    const int tf = tri32(m.f);
+    const double* src = W + m.foff;
+#pragma unroll
+    for (int k = 0; k < (S::TF + FM + 31) / 32; ++k) {
+      const int i = lane + 32 * k;
+      if (i < tf)
+        cp8(slot + i, src + i);
+      else if (i < tf + m.f)
+        cp8(slot + S::TF + (i - tf), src + i);
+    }
+    if (lane < m.f - 1) cp4(reinterpret_cast<int*>(slot + S::TF + FM) + lane, P.rel + m.lp + lane);
+  };
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue(ring[q], slots + q * S::FSLOT);
+    cp_commit();
+  }
+  int ua[S::UPL], ub[S::UPL];
+#pragma unroll
+  for (int k = 0; k < S::UPL; ++k) {
+    const int u = lane + 32 * k;
+    ua[k] = u < S::TU ? ta[u] : 0;
+    ub[k] = u < S::TU ? tb[u] : 0;
+  }
+  unsigned long long c[3] = {0, 0, 0};
+  int sj = 0, sa = L;
+  for (long long j = 0; j < n; ++j) {
+    if ((j & 31) == 0) issue_meta(P, 1, (j >> 5) + 2, ring);
+    if (j + L < n) issue(ring[(j + L) & (kMetaRing - 1)], slots + sa * S::FSLOT);
+    cp_commit();
+    cp_wait_n<L - 1>();
+    __syncwarp();
+    const ColRec m = ring[j & (kMetaRing - 1)];
+    const int f = m.f;
+    double* F = slots + sj * S::FSLOT;
+    double* ms = F + S::TF;
+    const int* r = reinterpret_cast<const int*>(F + S::TF + FM);
+    for (int q = m.sc0; q < m.sc1; ++q) {  // stashed children (rare)
+      const ColRec mc = P.rec[P.sc_child[q]];
+      const int32_t* rc = P.rel + mc.lp;
+      const double* Us = stash + mc.soff;
+      const int tu = (mc.f - 1) * mc.f / 2;
+      for (int u = lane; u < tu; u += 32) {
+        const int e = tri32(rc[ta[u] - 1]) + rc[tb[u] - 1];
+        F[e] = __dadd_rn(F[e], Us[u]);
+      }
+      for (int a = lane; a < mc.f - 1; a += 32) ms[rc[a]] = fmax(ms[rc[a]], Us[tu + a]);
+      __syncwarp();
+    }
+    const double d = F[0];
+    const bool zero = zero_pivot(d, ms[0]);
+    const double dinv = zero ? 0.0 : __drcp_rn(d);
+    if (lane == 0) {
+      D[m.pos] = d;
+      Dinv[m.pos] = dinv;
+      count_pivot(d, zero, c);
+    }
+    const int sn = sj + 1 == NS ? 0 : sj + 1;
+    double* Fn = m.soff == kChain ? slots + sn * S::FSLOT : nullptr;
+    double* Us = m.soff >= 0 ? stash + m.soff : nullptr;
+    const int tu = (f - 1) * f / 2;
+    if (lane >= 1 && lane < f) {  // row `lane`: L's entry and the diagonal maximum
+      const double Fa0 = F[tri32(lane)];
+      const double l = __dmul_rn(Fa0, dinv);
+      Lx[m.lp + lane - 1] = l;
+      const double mx = fmax(ms[lane], fabs(__dmul_rn(l, Fa0)));
+      if (Fn)
+        Fn[S::TF + r[lane - 1]] = fmax(Fn[S::TF + r[lane - 1]], mx);
+      else if (Us)
+        Us[tu + lane - 1] = mx;
+    }
+#pragma unroll
+    for (int k = 0; k < S::UPL; ++k) {
+      const int u = lane + 32 * k;
+      if (u < tu && (Fn || Us)) {
+        const int a = ua[k], b = ub[k];
+        const double U = __dsub_rn(F[tri32(a) + b], __dmul_rn(__dmul_rn(F[tri32(b)], dinv), F[tri32(a)]));
+        if (Fn) {
+          const int e = tri32(r[a - 1]) + r[b - 1];
+          Fn[e] = __dadd_rn(Fn[e], U);
+        } else {
+          Us[u] = U;
+        }
+      }
+    }
+    __syncwarp();
+    sj = sn;
+    sa = sa + 1 == NS ? 0 : sa + 1;
+  }
+  cp_wait_n<0>();
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q)
+      if (c[q]) atomicAdd(inertia + q, c[q]);
+}
+
+template <int FM>
+__global__ void __launch_bounds__(32) fwd_chain_small_k(Dev P, const double* __restrict__ Lx, double* __restrict__ y,
+                                                        double* __restrict__ Vs) {
+  using S = Small<FM>;
+  constexpr int NS = kSmallSlots, L = NS - 1;
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  __shared__ __align__(16) double slots[NS * S::VSLOT];  // [v FM][Lx FM][rel FM ints]
+  const int lane = threadIdx.x;
+  const long long n = P.nnl;
+  meta_prologue(P, 1, ring);
+  auto issue = [&](const ColRec& m, double* slot) {
+    if (lane == 0) cp8(slot, y + m.pos);
+    if (lane >= 1 && lane < FM) slot[lane] = 0.0;
+    if (lane < m.f - 1) {
+      cp8(slot + FM + lane, Lx + m.lp + lane);
+      cp4(reinterpret_cast<int*>(slot + 2 * FM) + lane, P.rel + m.lp + lane);
+    }
+  };
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue(ring[q], slots + q * S::VSLOT);
+    cp_commit();
+  }
+  int sj = 0, sa = L;
+  for (long long j = 0; j < n; ++j) {
+    if ((j & 31) == 0) issue_meta(P, 1, (j >> 5) + 2, ring);
+    if (j + L < n) issue(ring[(j + L) & (kMetaRing - 1)], slots + sa * S::VSLOT);
+    cp_commit();
+    cp_wait_n<L - 1>();
+    __syncwarp();
+    const ColRec m = ring[j & (kMetaRing - 1)];
+    double* v = slots + sj * S::VSLOT;
+    const int* r = reinterpret_cast<const int*>(v + 2 * FM);
+    for (int q = m.sc0; q < m.sc1; ++q) {
+      const ColRec mc = P.rec[P.sc_child[q]];
+      const int32_t* rc = P.rel + mc.lp;
+      const double* us = Vs + mc.soff;
+      for (int a = lane; a < mc.f - 1; a += 32) v[rc[a]] = __dadd_rn(v[rc[a]], us[a]);
+      __syncwarp();
+    }
+    const double yk = v[0];
+    if (lane == 0) y[m.pos] = yk;
+    const int sn = sj + 1 == NS ? 0 : sj + 1;
+    if (lane >= 1 && lane < m.f && m.soff != kRoot) {
+      const double u = __dsub_rn(v[lane], __dmul_rn(v[FM + lane - 1], yk));
+      if (m.soff == kChain) {
+        double* vn = slots + sn * S::VSLOT;
+        vn[r[lane - 1]] = __dadd_rn(vn[r[lane - 1]], u);
+      } else {
+        Vs[m.soff + lane - 1] = u;
+      }
+    }
+    __syncwarp();
+    sj = sn;
+    sa = sa + 1 == NS ? 0 : sa + 1;
+  }
+  cp_wait_n<0>();
+}
+
+template <int FM>
+__global__ void __launch_bounds__(32) bwd_chain_small_k(Dev P, const double* __restrict__ Lx,
+                                                        const double* __restrict__ Dinv, const double* __restrict__ y,
+                                                        double* __restrict__ xp) {
+  using S = Small<FM>;
+  constexpr int NS = kSmallSlots, L = NS - 2;
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  __shared__ __align__(16) double slots[NS * S::VSLOT];  // [X FM][Lx FM][y, Dinv][rel FM ints]
+  const int lane = threadIdx.x;
+  const long long n = P.nnl;
+  meta_prologue(P, -1, ring);
+  auto issue = [&](const ColRec& m, double* slot) {
+    if (lane < m.f - 1) {
+      cp8(slot + FM + lane, Lx + m.lp + lane);
+      cp4(reinterpret_cast<int*>(slot + 2 * FM + 2) + lane, P.rel + m.lp + lane);
+    }
+    if (lane == 30) cp8(slot + 2 * FM, y + m.pos);
+    if (lane == 31) cp8(slot + 2 * FM + 1, Dinv + m.pos);
+  };
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue(ring[q], slots + q * S::VSLOT);
+    cp_commit();
+  }
+  int sk = 0, sp = NS - 1, sa = L;
+  for (long long k = 0; k < n; ++k) {
+    if ((k & 31) == 0) issue_meta(P, -1, (k >> 5) + 2, ring);
+    if (k + L < n) issue(ring[(k + L) & (kMetaRing - 1)], slots + sa * S::VSLOT);
+    cp_commit();
+    cp_wait_n<L>();
+    __syncwarp();
+    const ColRec m = ring[k & (kMetaRing - 1)];
+    const int f = m.f;
+    double* X = slots + sk * S::VSLOT;
+    const int* r = reinterpret_cast<const int*>(X + 2 * FM + 2);
+    const bool chain = m.soff == kChain;
+    const double* Xn = slots + sp * S::VSLOT;
+    // X[a] = x of row a; the terms L(a) * X[a] summed in row order by lane 0
+    double xa = 0.0;
+    if (lane >= 1 && lane < f) {
+      xa = chain ? Xn[r[lane - 1]] : xp[P.Li[m.lp + lane - 1]];
+      X[lane] = xa;
+    }
+    const double term = lane >= 1 && lane < f ? __dmul_rn(X[FM + lane - 1], xa) : 0.0;
+    double s = __dmul_rn(X[2 * FM], X[2 * FM + 1]);
+#pragma unroll
+    for (int a = 1; a < FM; ++a) {
+      const double t = __shfl_sync(0xffffffffu, term, a);
+      if (a < f) s = __dsub_rn(s, t);
+    }
+    if (lane == 0) {
+      X[0] = s;
+      xp[m.pos] = s;
+    }
+    __syncwarp();
+    sp = sk;
+    sk = sk + 1 == NS ? 0 : sk + 1;
+    sa = sa + 1 == NS ? 0 : sa + 1;
+  }
+  cp_wait_n<0>();
 }
 
 // ---- solves ------------------------------------------------------------------
@@ -232,72 +574,121 @@ __global__ void fwd_leaf_k(Dev P, const double* __restrict__ Lx, double* __restr
   }
 }
 
-// vector fronts: V_j = [y_pos, 0, ...]
-__global__ void vinit_k(Dev P, const double* __restrict__ y, double* __restrict__ V) {
-  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P.nnl;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double* v = V + P.nl_voff[j];
-    v[0] = y[P.nl_pos[j]];
-    for (int a = 1; a < P.nl_f[j]; ++a) v[a] = 0.0;
-  }
+// forward slot: [v: f][Lx: f-1][rel: f-1 int32]; v = [y_pos, 0, ...]
+__device__ __forceinline__ void issue_fwd_slot(const Dev& P, const double* Lx, const double* y, const ColRec& m,
+                                               double* slot) {
+  const int f = m.f;
+  if (threadIdx.x == 0) cp8(slot, y + m.pos);
+  for (int i = 1 + threadIdx.x; i < f; i += 32) slot[i] = 0.0;
+  for (int i = threadIdx.x; i < f - 1; i += 32) cp8(slot + f + i, Lx + m.lp + i);
+  int* rel = reinterpret_cast<int*>(slot + 2 * f - 1);
+  for (int i = threadIdx.x; i < f - 1; i += 32) cp4(rel + i, P.rel + m.lp + i);
 }
 
-__global__ void __launch_bounds__(32) fwd_chain_k(Dev P, const double* __restrict__ Lx, double* __restrict__ y,
-                                                  double* __restrict__ V, double* __restrict__ Vs) {
+__global__ void __launch_bounds__(32) fwd_chain_k(Dev P, int ns, int slotd, const double* __restrict__ Lx,
+                                                  double* __restrict__ y, double* __restrict__ Vs) {
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  extern __shared__ double slots[];
   const int lane = threadIdx.x;
-  for (int64_t j = 0; j < P.nnl; ++j) {
-    const int f = P.nl_f[j];
-    double* v = V + P.nl_voff[j];
-    for (int64_t q = P.sc_ptr[j]; q < P.sc_ptr[j + 1]; ++q) {
-      const int cj = P.sc_child[q];
-      const int32_t* rc = P.rel + P.Lp[P.nl_pos[cj]];
-      const double* us = Vs + P.nl_soff[cj];
-      for (int a = lane; a < P.nl_f[cj] - 1; a += 32) v[rc[a]] = __dadd_rn(v[rc[a]], us[a]);
+  const long long n = P.nnl;
+  const int L = ns - 1;
+  meta_prologue(P, 1, ring);
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue_fwd_slot(P, Lx, y, ring[q], slots + q * slotd);
+    cp_commit();
+  }
+  int sj = 0, sa = L % ns;
+  for (long long j = 0; j < n; ++j) {
+    if ((j & 31) == 0) issue_meta(P, 1, (j >> 5) + 2, ring);
+    if (j + L < n) issue_fwd_slot(P, Lx, y, ring[(j + L) & (kMetaRing - 1)], slots + sa * slotd);
+    cp_commit();
+    cp_wait(L - 1);
+    __syncwarp();
+    const ColRec m = ring[j & (kMetaRing - 1)];
+    const int f = m.f;
+    double* v = slots + sj * slotd;
+    const double* lx = v + f;
+    const int* r = reinterpret_cast<const int*>(v + 2 * f - 1);
+    for (int q = m.sc0; q < m.sc1; ++q) {
+      const ColRec mc = P.rec[P.sc_child[q]];
+      const int32_t* rc = P.rel + mc.lp;
+      const double* us = Vs + mc.soff;
+      for (int a = lane; a < mc.f - 1; a += 32) v[rc[a]] = __dadd_rn(v[rc[a]], us[a]);
       __syncwarp();
     }
-    const int64_t pos = P.nl_pos[j];
     const double yk = v[0];
-    if (lane == 0) y[pos] = yk;
-    const int64_t so = P.nl_soff[j];
-    if (so != kRoot) {
-      const int64_t lp = P.Lp[pos];
-      const int32_t* r = P.rel + lp;
-      double* vn = so == kChain ? V + P.nl_voff[j + 1] : nullptr;
+    if (lane == 0) y[m.pos] = yk;
+    const int sn = next_slot(sj, ns);
+    if (m.soff != kRoot) {
+      double* vn = m.soff == kChain ? slots + sn * slotd : nullptr;
       for (int a = lane + 1; a < f; a += 32) {
-        const double u = __dsub_rn(v[a], __dmul_rn(Lx[lp + a - 1], yk));
+        const double u = __dsub_rn(v[a], __dmul_rn(lx[a - 1], yk));
         if (vn)
           vn[r[a - 1]] = __dadd_rn(vn[r[a - 1]], u);
         else
-          Vs[so + a - 1] = u;
+          Vs[m.soff + a - 1] = u;
       }
     }
     __syncwarp();
+    sj = sn;
+    sa = next_slot(sa, ns);
   }
+  cp_wait(0);
 }
 
-// backward: x-fronts X_j = [x_pos, x of the rows of column j]
-__global__ void __launch_bounds__(32) bwd_chain_k(Dev P, const double* __restrict__ Lx, const double* __restrict__ Dinv,
-                                                  const double* __restrict__ y, double* __restrict__ xp,
-                                                  double* __restrict__ V) {
+// backward slot: [X: f][Lx: f-1][y_pos, Dinv_pos][rel: f-1 int32]; X = [x_pos, x of the rows]
+__device__ __forceinline__ void issue_bwd_slot(const Dev& P, const double* Lx, const double* Dinv, const double* y,
+                                               const ColRec& m, double* slot) {
+  const int f = m.f;
+  for (int i = threadIdx.x; i < f - 1; i += 32) cp8(slot + f + i, Lx + m.lp + i);
+  if (threadIdx.x == 0) cp8(slot + 2 * f - 1, y + m.pos);
+  if (threadIdx.x == 1) cp8(slot + 2 * f, Dinv + m.pos);
+  int* rel = reinterpret_cast<int*>(slot + 2 * f + 1);
+  for (int i = threadIdx.x; i < f - 1; i += 32) cp4(rel + i, P.rel + m.lp + i);
+}
+
+__global__ void __launch_bounds__(32) bwd_chain_k(Dev P, int ns, int slotd, const double* __restrict__ Lx,
+                                                  const double* __restrict__ Dinv, const double* __restrict__ y,
+                                                  double* __restrict__ xp) {
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  extern __shared__ double slots[];
   const int lane = threadIdx.x;
-  for (int64_t j = P.nnl - 1; j >= 0; --j) {
-    const int64_t pos = P.nl_pos[j];
-    const int f = P.nl_f[j];
-    double* X = V + P.nl_voff[j];
-    const int64_t lp = P.Lp[pos];
-    const int32_t* r = P.rel + lp;
-    const bool chain = P.nl_soff[j] == kChain;
-    const double* Xn = chain ? V + P.nl_voff[j + 1] : nullptr;
-    for (int a = lane + 1; a < f; a += 32) X[a] = chain ? Xn[r[a - 1]] : xp[P.Li[lp + a - 1]];
+  const long long n = P.nnl;
+  // step k walks column n-1-k; it reads step k-1's slot, so the prefetch runs
+  // L = ns-2 steps ahead and never lands in either
+  const int L = ns - 2;
+  meta_prologue(P, -1, ring);
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue_bwd_slot(P, Lx, Dinv, y, ring[q], slots + q * slotd);
+    cp_commit();
+  }
+  int sk = 0, sp = ns - 1, sa = L % ns;  // slots of steps k, k-1, k+L
+  for (long long k = 0; k < n; ++k) {
+    if ((k & 31) == 0) issue_meta(P, -1, (k >> 5) + 2, ring);
+    if (k + L < n) issue_bwd_slot(P, Lx, Dinv, y, ring[(k + L) & (kMetaRing - 1)], slots + sa * slotd);
+    cp_commit();
+    cp_wait(L);
     __syncwarp();
+    const ColRec m = ring[k & (kMetaRing - 1)];
+    const int f = m.f;
+    double* X = slots + sk * slotd;
+    const double* lx = X + f;
+    const int* r = reinterpret_cast<const int*>(X + 2 * f + 1);
+    const bool chain = m.soff == kChain;
+    const double* Xn = slots + sp * slotd;  // column j+1, the previous step
+    for (int a = lane + 1; a < f; a += 32) X[a] = chain ? Xn[r[a - 1]] : xp[P.Li[m.lp + a - 1]];
     if (lane == 0) {
-      double s = __dmul_rn(y[pos], Dinv[pos]);
-      for (int a = 1; a < f; ++a) s = __dsub_rn(s, __dmul_rn(Lx[lp + a - 1], X[a]));
+      double s = __dmul_rn(X[2 * f - 1], X[2 * f]);
+      for (int a = 1; a < f; ++a) s = __dsub_rn(s, __dmul_rn(lx[a - 1], chain ? Xn[r[a - 1]] : xp[P.Li[m.lp + a - 1]]));
       X[0] = s;
-      xp[pos] = s;
+      xp[m.pos] = s;
     }
     __syncwarp();
+    sp = sk;
+    sk = next_slot(sk, ns);
+    sa = next_slot(sa, ns);
   }
+  cp_wait(0);
 }
 
 __global__ void bwd_leaf_k(Dev P, const double* __restrict__ Lx, const double* __restrict__ Dinv,
@@ -312,6 +703,12 @@ __global__ void bwd_leaf_k(Dev P, const double* __restrict__ Lx, const double* _
   }
 }
 
+// ring depth: up to 16 slots, within 160 KB of dynamic shared memory
+int ring_slots(int slotd) {
+  const int by_smem = static_cast<int>((160 * 1024) / (static_cast<size_t>(slotd) * sizeof(double)));
+  return std::max(2, std::min(15, by_smem));
+}
+
 }  // namespace
 
 void factor(const Dev& P, const double* kval, double delta_w, double delta_c, double* W, double* stash, double* D,
@@ -322,18 +719,39 @@ void factor(const Dev& P, const double* kval, double delta_w, double delta_c, do
                                                 delta_c, W);
   if (P.nleaf) leaf_k<<<grid_for(P.nleaf), kThreads, 0, s>>>(P, W, D, Dinv, Lx, inertia);
   if (P.npa) preassemble_k<<<grid_for(P.npa), kThreads, 0, s>>>(P, W, Lx);
-  if (P.nnl) chain_factor_k<<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
+  if (P.nnl && P.fmax <= 8) {
+    chain_factor_small_k<8><<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
+  } else if (P.nnl && P.fmax <= 16) {
+    chain_factor_small_k<16><<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
+  } else if (P.nnl) {
+    const int slotd = static_cast<int>(P.fmax * (P.fmax + 1) / 2 + P.fmax + P.fmax / 2 + 1);
+    const int ns = ring_slots(slotd);
+    ck(cudaFuncSetAttribute(chain_factor_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024), "smem attr");
+    chain_factor_k<<<1, 32, static_cast<size_t>(ns) * slotd * sizeof(double), s>>>(P, ns, slotd, W, stash, D, Dinv,
+                                                                                   Lx, inertia);
+  }
   ck(cudaGetLastError(), "factor launch");
 }
 
 void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs, double* x, double* y, double* xp,
            double* V, double* Vs, cudaStream_t s) {
+  (void)V;
   gather_k<<<grid_for(P.dim), kThreads, 0, s>>>(P.perm, rhs, y, P.dim);
   if (P.nfl) fwd_leaf_k<<<grid_for(P.nfl), kThreads, 0, s>>>(P, Lx, y);
-  if (P.nnl) {
-    vinit_k<<<grid_for(P.nnl), kThreads, 0, s>>>(P, y, V);
-    fwd_chain_k<<<1, 32, 0, s>>>(P, Lx, y, V, Vs);
-    bwd_chain_k<<<1, 32, 0, s>>>(P, Lx, Dinv, y, xp, V);
+  if (P.nnl && P.fmax <= 8) {
+    fwd_chain_small_k<8><<<1, 32, 0, s>>>(P, Lx, y, Vs);
+    bwd_chain_small_k<8><<<1, 32, 0, s>>>(P, Lx, Dinv, y, xp);
+  } else if (P.nnl && P.fmax <= 16) {
+    fwd_chain_small_k<16><<<1, 32, 0, s>>>(P, Lx, y, Vs);
+    bwd_chain_small_k<16><<<1, 32, 0, s>>>(P, Lx, Dinv, y, xp);
+  } else if (P.nnl) {
+    const int slotd = static_cast<int>(3 * P.fmax + 2);
+    const int ns = ring_slots(slotd);
+    const size_t smem = static_cast<size_t>(ns) * slotd * sizeof(double);
+    ck(cudaFuncSetAttribute(fwd_chain_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024), "smem attr");
+    ck(cudaFuncSetAttribute(bwd_chain_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024), "smem attr");
+    fwd_chain_k<<<1, 32, smem, s>>>(P, ns, slotd, Lx, y, Vs);
+    bwd_chain_k<<<1, 32, smem, s>>>(P, ns, slotd, Lx, Dinv, y, xp);
   }
   if (P.nleaf) bwd_leaf_k<<<grid_for(P.nleaf), kThreads, 0, s>>>(P, Lx, Dinv, y, xp);
   scatter_out_k<<<grid_for(P.dim), kThreads, 0, s>>>(P.perm, xp, x, P.dim);

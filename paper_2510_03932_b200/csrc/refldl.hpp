@@ -55,14 +55,26 @@ struct Symbolic {
 };
 Symbolic analyze(int64_t dim, const int64_t* colp, const int64_t* rowi, int64_t n_free, int64_t ntot);
 
+constexpr int64_t kChain = -1, kRoot = -2;  // ColRec::soff / Dev::nl_soff markers
+
 // Largest front (1 + column count of L) the warp kernels take.
 constexpr int kMaxFront = 128;
+
+// One chain column's metadata for the warp walks (32 bytes).
+struct alignas(16) ColRec {
+  long long foff;  // front in W
+  int lp;          // first entry of the column in Li / Lx / rel
+  int pos;         // position
+  int f;           // front size
+  int soff;        // stash offset, or kChain / kRoot
+  int sc0, sc1;    // stashed children: sc_child[sc0, sc1)
+};
 
 // Host side of the device plan (below), built once per KKT pattern.
 struct HostPlan {
   int64_t dim = 0, nnz = 0, lnz = 0;
   int fmax = 0;
-  std::vector<int64_t> nl_pos, nl_foff, nl_soff, nl_voff, sc_ptr;
+  std::vector<int64_t> nl_pos, nl_lp, nl_foff, nl_soff, nl_voff, sc_ptr;
   std::vector<int32_t> nl_f, sc_child;
   std::vector<int64_t> lf_pos, lf_aoff;
   std::vector<int32_t> lf_f;
@@ -73,6 +85,7 @@ struct HostPlan {
   std::vector<int32_t> rel;
   std::vector<int64_t> sc_dst, sc_dpos, sc_ms;
   std::vector<int8_t> primal;
+  std::vector<ColRec> rec;
   int64_t w_len = 0, stash_len = 0, v_len = 0;
 };
 HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi);
@@ -83,7 +96,9 @@ struct Dev {
   int64_t dim = 0, nnz = 0, lnz = 0, nleaf = 0, nnl = 0, npa = 0, nfl = 0;
   int fmax = 0;
   // chain columns, j = 0..nnl-1
+  const ColRec* rec = nullptr;       // [nnl] the same, packed for the walks
   const int64_t* nl_pos = nullptr;   // position
+  const int64_t* nl_lp = nullptr;    // Lp[position]
   const int32_t* nl_f = nullptr;     // front size (1 + column count)
   const int64_t* nl_foff = nullptr;  // front (packed lower, row-major, then f diagonal maxima) in W
   // stash of the update matrix / vector when the parent is not column j+1:
@@ -117,7 +132,6 @@ struct Dev {
   const int8_t* primal = nullptr;    // position: 1 = +delta_w, 0 = -delta_c
   int64_t w_len = 0, stash_len = 0, v_len = 0;
 };
-constexpr int64_t kChain = -1, kRoot = -2;
 
 // numeric factorization: W (w_len) and stash (stash_len) scratch; D, Dinv by
 // position; Lx in the layout of Lp/Li; inertia (device, 3 counts) =
