@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--goddard-solve", default="100000:10",
                     help="N[:ref_iters] of the Goddard full device solve (BASELINE config 2, 'goddard_solve' key); the "
                          "reference runs ref_iters iterations for a per-iteration comparison; 'none' to skip")
+    ap.add_argument("--goddard-parity", default="1000",
+                    help="N of the Goddard solve with the reference-order factorization (BASELINE configs[0]: "
+                         "iterations, factorizations and objective against the reference's; "
+                         "'goddard_parity_solve' key; 'none' to skip)")
     ap.add_argument("--batch", default="4096:500",
                     help="instances:N of the batched cart-pendulum solve leg (BASELINE config 5, 'batch_solve' "
                          "key; 'none' to skip)")
@@ -294,6 +298,31 @@ def cpu_reference_eval(src: str, N: int, scheme: str, reps: int = 5, serial: boo
     return out
 
 
+def dropin_e2e(src: str, N: int, scheme: str, steps: int, warmup: int) -> dict | None:
+    """End to end through the REFERENCE's API: EvalContext::eval_constraints_jacobian
+    + eval_hessian of the drop-in build (integration/_out/libref_accel.so: the
+    reference's own classes with integration/octrans_accel.cpp in place of
+    proj/src/ipm/eval.cpp), host std::vectors in and out, as the reference's
+    Solver calls them. Each call uploads x (and lambda), runs the device
+    kernels and copies c / jac_val / hess_val back before returning."""
+    try:
+        sys.path.insert(0, str(ROOT / "tests"))
+        from _oracle import RefEval, RefModel  # noqa: E402
+        rm = RefModel(src, N, 1 if scheme == "trapezoid" else 0, lib="accel")
+    except Exception as ex:  # drop-in not built on this box
+        return {"unavailable": str(ex)}
+    x, lam = rm.synth_acceptance(20250808)
+    re = RefEval(rm)
+    for _ in range(max(warmup, 1)):
+        assert re.step_seconds(x, lam, 1)[1]
+    ts = [re.step_seconds(x, lam, 1)[0] for _ in range(steps)]
+    sz = np.zeros(3, dtype=np.int64)
+    re.L.ref_eval_sizes(re.h, sz.ctypes.data)
+    jn, hn = int(sz[0]), int(sz[1])
+    return {"median_s": float(np.median(ts)), "mean_s": float(np.mean(ts)), "steps": steps,
+            "h2d": 8 * (2 * rm.nvar + rm.m_con), "d2h": 8 * (rm.m_con + jn + hn)}
+
+
 def parity_of(name: str, got: dict, ref: tuple) -> dict:
     """max relative error of the device c / jac / hess against the reference
     EvalContext on the same inputs (tests/parity.py rule with the model's floor)."""
@@ -505,8 +534,8 @@ def run_ours(args) -> None:
                          "bytes_per_node": nbytes / max(1, b - a)},
             "e2e": {"value": t_e2e_max * 1e9 / N, "unit": "ns/node", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "path": "ocg_eval_jac_hess via the Python EvalContext mirror; pinned host x,lambda in, "
-                            "c/jac_val/hess_val out"},
+                    "path": "C ABI ocg_eval_jac_hess (fused kernel) through the Python EvalContext mirror; pinned "
+                            "host x, lambda in, c / jac_val / hess_val out, per rank"},
             "gpu_launches": launches,
             "clocks": clk,
             "wall_s_timed_region": wall,
@@ -521,6 +550,19 @@ def run_ours(args) -> None:
                     out["roofline"]["traffic_source"] = d[key].get("source")
             except Exception:
                 pass
+        if world == 1:
+            # the headline e2e goes through the reference's own EvalContext API
+            # (the drop-in); the C-ABI number above stays as e2e_c_abi
+            dr = dropin_e2e(src, N, args.scheme, e2e_steps, args.warmup)
+            if dr and "median_s" in dr:
+                out["e2e_c_abi"] = out["e2e"]
+                out["e2e"] = {"value": dr["median_s"] * 1e9 / N, "unit": "ns/node", "h2d_bytes_per_step": dr["h2d"],
+                              "d2h_bytes_per_step": dr["d2h"], "steps": dr["steps"],
+                              "path": "reference API: EvalContext::eval_constraints_jacobian + eval_hessian of the "
+                                      "drop-in build (integration/_out/libref_accel.so) with host std::vectors; "
+                                      "median of the timed steps (steady_clock around the two calls)"}
+            elif dr:
+                out["e2e"]["dropin"] = dr
         if world == 1 and not args.no_cpu_baseline:
             try:
                 r = cpu_reference_eval(src, N, args.scheme, reps=5, serial=True, outputs=True)
@@ -544,6 +586,9 @@ def run_ours(args) -> None:
         if args.goddard_solve != "none" and world == 1:  # BASELINE config 2
             n, cap = (args.goddard_solve.split(":") + ["3"])[:2]
             out["goddard_solve"] = ipm_solve_leg(f"goddard:{n}", not args.no_cpu_baseline, int(cap))
+        if args.goddard_parity != "none" and world == 1:  # BASELINE configs[0]: the reference's trajectory
+            out["goddard_parity_solve"] = ipm_solve_leg(f"goddard:{args.goddard_parity}", not args.no_cpu_baseline,
+                                                        order="reference", reps=1)
         if args.batch != "none" and world == 1:
             out["batch_solve"] = batch_solve_leg(args.batch, not args.no_cpu_baseline)
         print(json.dumps(out), flush=True)
@@ -552,7 +597,7 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dict:
+def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0, order: str = "band", reps: int = 3) -> dict:
     """Full interior-point solve (BASELINE metric: "IPM solve time at N=1e5"):
     ocg_ipm_solve — the reference's filter line-search IPM with evaluations,
     KKT assembly, vector work and the time-partitioned band LDL^T all on the
@@ -563,18 +608,20 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
     wall of three further solves, each building its plans anew.
     ref_max_iter > 0 caps the reference's run (Goddard at N=1e5 needs ~N/2
     iterations, hours on the host: SURVEY.md D6); the two are then
-    compared per iteration."""
+    compared per iteration. order="reference" factors the KKT matrices in
+    the reference's elimination order (ocg_ldl_create_ex OCG_LDL_REFERENCE),
+    which reproduces the reference's iterate trajectory on Goddard too."""
     from paper_2510_03932_b200 import MODELS, Model, solve
     name, N = spec.split(":")
     N = int(N)
     m = Model(MODELS[name], N)
     t0 = time.perf_counter()
-    d = solve(m)
+    d = solve(m, kkt_order=order)
     t_first = time.perf_counter() - t0
     walls, d2 = [], None
-    for _ in range(3):  # kernels now in the compile cache; median of three solves
+    for _ in range(reps):  # kernels now in the compile cache; median of the further solves
         t0 = time.perf_counter()
-        d2 = solve(m)
+        d2 = solve(m, kkt_order=order)
         walls.append(time.perf_counter() - t0)
     t_second = float(np.median(walls))
     out = {"model": name, "N": N, "status": d2["status_name"], "iterations": d2["iterations"],
@@ -585,7 +632,8 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
            "time_derivatives_s": d2["time_derivatives"], "time_total_s": d2["time_total"],
            "time_setup_s": d2["time_setup"], "plan_s": {"eval": d2["time_plan_eval"], "kkt": d2["time_plan_kkt"],
                                                        "ldl": d2["time_plan_ldl"]},
-           "factorization": "time-partitioned band LDL^T (device)"}
+           "factorization": ("time-partitioned band LDL^T (device)" if order == "band" else
+                             "reference-order LDL^T (device; AMD-equivalent order + pivot_after_, 1x1 pivots)")}
     if with_reference:
         RefEval, RefModel = _ref_modules()
         cores = os.cpu_count() or 1
@@ -602,6 +650,8 @@ def ipm_solve_leg(spec: str, with_reference: bool, ref_max_iter: int = 0) -> dic
             out["speedup_per_iter"] = out["reference"]["s_per_iter"] / out["device_s_per_iter"]
         else:
             out["iterations_match"] = int(r["iterations"]) == d2["iterations"]
+            out["reference"]["factorizations"] = int(r["factorizations"])
+            out["factorizations_match"] = int(r["factorizations"]) == d2["factorizations"]
             out["objective_rel_diff"] = abs(r["objective"] - d2["objective"]) / max(abs(r["objective"]), 1e-300)
             out["speedup_vs_reference"] = out["reference"]["wall_s"] / t_second
     return out

@@ -275,6 +275,7 @@ EvalContext::EvalContext(const StructuredNlp& nlp, const backend::Backend& backe
   grad_val.assign(static_cast<size_t>(gn), 0.0);
   c_raw_.assign(a->m, 0.0);
   row_scale.assign(a->m, 1.0);
+
   std::lock_guard<std::mutex> lk(g_mu);
   g_ec[this] = std::move(a);
 }

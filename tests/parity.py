@@ -20,15 +20,18 @@ import numpy as np
 #   goddard       max 2.0e-15 per entry                       -> no floor
 #   hang_glider   max 3.3e-13 per entry                       -> no floor
 #   double_integr. linear/quadratic, exact                    -> no floor
-#   quadrotor     J/H entries ~1e-11..1e-14 of max cancel: worst |err| = 7.9e-23
-#                 with max|ref| ~1 (N=1e6)  -> needs floor >= 7.9e-11 -> 1e-9
+#   quadrotor     J/H/grad entries down to ~1e-9 of max cancel (sin/cos
+#                 products of the attitude); with a floor of 1e-6 the worst
+#                 entry still has 1.1e-11 relative error, i.e. |err| / max =
+#                 1.1e-17 (hess, N=1e6, r2_v3 GPU run)  -> needs floor >= 1.1e-5
+#                                                                    -> 1e-4
 #   shuttle       H entries down to 1e-24 of max; the entry with the largest
 #                 ABSOLUTE error has |err| / max = 8.7e-17 (N=1e5, r2_v1
 #                 GPU run) -> needs floor >= 8.7e-5                    -> 1e-4
 #   cart_pendulum H entries ~1e-6 of max: worst |err| / max = 3.3e-17
 #                 -> needs floor >= 3.3e-5                             -> 1e-4
 REL_TOL = 1e-12
-CANCELLING = {"quadrotor": 1e-9, "shuttle": 1e-4, "cart_pendulum": 1e-4}
+CANCELLING = {"quadrotor": 1e-4, "shuttle": 1e-4, "cart_pendulum": 1e-4}
 # default for callers that do not name a model (scaled / synthetic cases)
 FLOOR = 1e-4
 
