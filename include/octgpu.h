@@ -194,6 +194,11 @@ int ocg_eval_objective_combine(ocg_eval* e, const double* partials, double* f, o
 /* Synchronise s; OCG_OK if every evaluation since the last call was finite,
  * else OCG_EVAL_DOMAIN. Clears the flag. */
 int ocg_eval_status(ocg_eval* e, ocg_stream s);
+/* Asynchronous form: enqueue on s the copy of the finiteness flag into
+ * *host_flag (page-locked host memory) and its reset; once s has been
+ * synchronized, *host_flag != 0 means some evaluation since the last status
+ * call was not finite (ocg_eval_status's OCG_EVAL_DOMAIN). */
+int ocg_eval_status_async(ocg_eval* e, int* host_flag, ocg_stream s);
 /* number of kernels this context has launched (all entry points) */
 int64_t ocg_eval_launch_count(const ocg_eval* e);
 

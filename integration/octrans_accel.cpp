@@ -26,16 +26,19 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ipm/ipm_internal.hpp"
 #include "octgpu.h"
+#include "xfer.hpp"
 
 namespace octrans::ipm::detail {
 
@@ -48,6 +51,24 @@ void ck(int rc, const char* what) {
 void ckc(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("cuda ") + what + ": " + cudaGetErrorString(e));
 }
+
+// OCTRANS_ACCEL_TIMING=1: per-phase wall times of the eval calls on stderr
+class Lap {
+ public:
+  explicit Lap(const char* what) : what_(what), on_(std::getenv("OCTRANS_ACCEL_TIMING") != nullptr) {}
+  void operator()(const char* phase) {
+    if (!on_) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[octrans_accel] %s %-16s %8.3f ms\n", what_, phase,
+                 std::chrono::duration<double, std::milli>(now - t_).count());
+    t_ = now;
+  }
+
+ private:
+  const char* what_;
+  bool on_;
+  std::chrono::steady_clock::time_point t_ = std::chrono::steady_clock::now();
+};
 
 class Timer {
  public:
@@ -189,12 +210,20 @@ struct Accel {
   size_t nvar = 0, m = 0;
   Dev<double> x, lam, c, grad, f, scratch;
   ~Accel() {
+    xfer.reset();  // synchronises the stream destroyed below
+    if (flag) cudaFreeHost(flag);
     if (ev) ocg_eval_destroy(ev);
     if (model) ocg_model_destroy(model);
     if (stream) cudaStreamDestroy(stream);
   }
+  // large arrays move through the pipelined page-locked staging of xfer.hpp
+  static constexpr size_t kStaged = size_t{1} << 16;
+  std::unique_ptr<octrans_accel::Xfer> xfer;
   void upload(const double* src, Dev<double>& dst, size_t n) {
-    if (n) ckc(cudaMemcpyAsync(dst.p, src, n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+    if (n >= kStaged)
+      xfer->h2d(dst.p, src, n);
+    else if (n)
+      ckc(cudaMemcpyAsync(dst.p, src, n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
   }
   void download(const Dev<double>& src, double* dst, size_t n) {
     if (n) ckc(cudaMemcpyAsync(dst, src.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
@@ -204,6 +233,22 @@ struct Accel {
       ckc(cudaMemcpyAsync(dst, ocg_eval_buffer(ev, which), n * sizeof(double), cudaMemcpyDeviceToHost, stream),
           "D2H");
   }
+  // several device arrays to host, synchronous on return
+  void download_all(const std::vector<octrans_accel::Xfer::Part>& parts) {
+    std::vector<octrans_accel::Xfer::Part> big;
+    for (const auto& p : parts)
+      if (p.n >= kStaged)
+        big.push_back(p);
+      else if (p.n)
+        ckc(cudaMemcpyAsync(p.dst, p.dsrc, p.n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
+    if (!big.empty()) xfer->d2h(big);
+    ckc(cudaStreamSynchronize(stream), "sync");
+  }
+  // the reference's bool without a synchronisation of its own: the flag is
+  // copied behind the outputs and read once the downloads are done
+  int* flag = nullptr;  // page-locked
+  void status_async() { ck(ocg_eval_status_async(ev, flag, stream), "eval_status_async"); }
+  bool flag_ok() const { return *flag == 0; }
   // the reference's bool: synchronises, reports and clears the device flag
   bool status() {
     const int rc = ocg_eval_status(ev, stream);
@@ -252,6 +297,18 @@ EvalContext::EvalContext(const StructuredNlp& nlp, const backend::Backend& backe
   ckc(cudaSetDevice(o.device), "cudaSetDevice");
   ck(ocg_eval_create(a->model, &o, &a->ev), "eval_create");
   ckc(cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking), "stream");
+  ckc(cudaMallocHost(&a->flag, sizeof(int)), "cudaMallocHost");
+  *a->flag = 0;
+  {
+    // staging: 6 slots of 2^18 doubles (2 MiB), half the host threads (at most
+    // 8) copying -- the best of a sweep on the B200 box (Goddard N=1e5 J+H
+    // step 1.47 ms; 4 MiB x 4: 2.4 ms, 1 MiB x 8: 1.75 ms, profiles/
+    // r2_dropin_xfer_sweep.txt); OCTRANS_ACCEL_XFER="chunk_doubles,slots,threads"
+    size_t chunk = size_t{1} << 18;
+    int slots = 6, threads = static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 1u, 8u));
+    if (const char* e = std::getenv("OCTRANS_ACCEL_XFER")) std::sscanf(e, "%zu,%d,%d", &chunk, &slots, &threads);
+    a->xfer = std::make_unique<octrans_accel::Xfer>(a->stream, std::max(1, threads), std::max<size_t>(chunk, 1024), slots);
+  }
   a->nvar = static_cast<size_t>(nlp.nvar());
   a->m = static_cast<size_t>(nlp.m_con);
   a->x.alloc(a->nvar);
@@ -294,22 +351,26 @@ bool EvalContext::eval_constraints(std::span<const double> x, std::vector<double
   ck(ocg_eval_constraints(a.ev, a.x.p, a.c.p, a.stream), "eval_constraints");
   if (!a.status()) return false;
   c_scaled.resize(a.m);
-  a.download(a.c, c_scaled.data(), a.m);
-  ckc(cudaStreamSynchronize(a.stream), "sync");
+  a.download_all({{c_scaled.data(), a.c.p, a.m}});
   return true;
 }
 
 bool EvalContext::eval_constraints_jacobian(std::span<const double> x, std::vector<double>& c_scaled) {
   Timer t(time_derivatives);
   Accel& a = accel(this);
+  Lap lap("eval_constraints_jacobian");
   a.upload(x.data(), a.x, a.nvar);
+  lap("h2d x");
   ck(ocg_eval_constraints_jacobian(a.ev, a.x.p, a.c.p, a.stream), "eval_constraints_jacobian");
-  if (!a.status()) return false;
+  a.status_async();
+  lap("kernel enqueued");
+  // c and jac_val come back unconditionally (on a domain error the reference
+  // also leaves partial values behind); the bool is read after the copies
   c_scaled.resize(a.m);
-  a.download(a.c, c_scaled.data(), a.m);
-  a.download_buf(OCG_BUF_JAC, jac_val.data(), jac_val.size());
-  ckc(cudaStreamSynchronize(a.stream), "sync");
-  return true;
+  a.download_all({{c_scaled.data(), a.c.p, a.m},
+                  {jac_val.data(), static_cast<const double*>(ocg_eval_buffer(a.ev, OCG_BUF_JAC)), jac_val.size()}});
+  lap("d2h c, jac_val");
+  return a.flag_ok();
 }
 
 bool EvalContext::eval_objective(std::span<const double> x, double& f_scaled) {
@@ -330,24 +391,26 @@ bool EvalContext::eval_gradient(std::span<const double> x, std::vector<double>& 
   ck(ocg_eval_gradient(a.ev, a.x.p, a.grad.p, a.stream), "eval_gradient");
   if (!a.status()) return false;
   grad_dense.resize(a.nvar);
-  a.download(a.grad, grad_dense.data(), a.nvar);
-  a.download_buf(OCG_BUF_GRAD, grad_val.data(), grad_val.size());
-  ckc(cudaStreamSynchronize(a.stream), "sync");
+  a.download_all({{grad_dense.data(), a.grad.p, a.nvar},
+                  {grad_val.data(), static_cast<const double*>(ocg_eval_buffer(a.ev, OCG_BUF_GRAD)), grad_val.size()}});
   return true;
 }
 
 bool EvalContext::eval_hessian(std::span<const double> x, std::span<const double> lambda_scaled) {
   Timer t(time_derivatives);
   Accel& a = accel(this);
+  Lap lap("eval_hessian");
   a.upload(x.data(), a.x, a.nvar);
   a.upload(lambda_scaled.data(), a.lam, a.m);
+  lap("h2d x, lambda");
   ck(ocg_eval_hessian(a.ev, a.x.p, a.lam.p, a.stream), "eval_hessian");
-  const bool ok = a.status();
+  a.status_async();
+  lap("kernel enqueued");
   // hess_val is public: keep the host mirror current (the reference leaves
   // partial values behind on failure too)
-  a.download_buf(OCG_BUF_HESS, hess_val.data(), hess_val.size());
-  ckc(cudaStreamSynchronize(a.stream), "sync");
-  return ok;
+  a.download_all({{hess_val.data(), static_cast<const double*>(ocg_eval_buffer(a.ev, OCG_BUF_HESS)), hess_val.size()}});
+  lap("d2h hess_val");
+  return a.flag_ok();
 }
 
 double EvalContext::max_abs_hessian() const {

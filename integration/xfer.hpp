@@ -1,0 +1,181 @@
+// Host <-> device copies of the reference's pageable std::vectors at PCIe rate
+// (drop-in only: the reference's EvalContext hands the library plain
+// std::vector<double> buffers, and a pageable cudaMemcpy runs at a fraction
+// of the link's bandwidth).
+//
+// Each transfer is cut into chunks staged through a ring of page-locked
+// buffers: while the DMA engine moves chunk i+1.., a small fork-join pool of
+// host threads copies chunk i between the staging slot and the caller's
+// memory. Registering the caller's vectors instead (cudaHostRegister) is not
+// an option: EvalContext has no destructor the drop-in could hook, so the
+// registration would outlive the memory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstddef>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace octrans_accel {
+
+// fork-join memcpy over T threads (the caller is one of them)
+class CopyPool {
+ public:
+  explicit CopyPool(int threads) {
+    for (int t = 1; t < threads; ++t) workers_.emplace_back([this, t] { run(t); });
+    nthreads_ = threads;
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t{1} << 18) || nthreads_ == 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      pending_ = nthreads_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void part(int t) {
+    const size_t per = (bytes_ / nthreads_ + 63) & ~size_t{63};
+    const size_t lo = std::min(bytes_, per * static_cast<size_t>(t)), hi = std::min(bytes_, lo + per);
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void run(int t) {
+    size_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      part(t);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  int nthreads_ = 1;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  size_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+class Xfer {
+ public:
+  static constexpr int kMaxSlots = 8;
+
+  // chunk: doubles per staging slot; slots <= kMaxSlots
+  Xfer(cudaStream_t s, int threads, size_t chunk, int slots)
+      : kChunk(chunk), kSlots(std::clamp(slots, 2, kMaxSlots)), stream_(s), pool_(threads) {
+    for (int i = 0; i < kSlots; ++i) {
+      ck(cudaMallocHost(&stage_[i], kChunk * sizeof(double)), "cudaMallocHost");
+      ck(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
+    }
+  }
+  ~Xfer() {
+    cudaStreamSynchronize(stream_);
+    for (int i = 0; i < kSlots; ++i) {
+      cudaFreeHost(stage_[i]);
+      cudaEventDestroy(ev_[i]);
+    }
+  }
+  Xfer(const Xfer&) = delete;
+  Xfer& operator=(const Xfer&) = delete;
+
+  // enqueue host -> device; returns once the host source has been consumed
+  void h2d(double* ddst, const double* src, size_t n) {
+    for (size_t off = 0; off < n; off += kChunk) {
+      const size_t len = std::min(kChunk, n - off);
+      const int s = next_slot();
+      ck(cudaEventSynchronize(ev_[s]), "slot sync");  // the slot's previous DMA is done
+      pool_.copy(stage_[s], src + off, len * sizeof(double));
+      ck(cudaMemcpyAsync(ddst + off, stage_[s], len * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D");
+      ck(cudaEventRecord(ev_[s], stream_), "record");
+    }
+  }
+
+  struct Part {
+    double* dst;
+    const double* dsrc;
+    size_t n;
+  };
+  // device -> host for several arrays in one pipeline; synchronous
+  void d2h(const std::vector<Part>& parts) {
+    struct Chunk {
+      double* dst;
+      const double* dsrc;
+      size_t len;
+    };
+    std::vector<Chunk> ch;
+    for (const Part& p : parts)
+      for (size_t off = 0; off < p.n; off += kChunk) ch.push_back({p.dst + off, p.dsrc + off, std::min(kChunk, p.n - off)});
+    std::vector<int> slot(ch.size());
+    auto issue = [&](size_t i) {
+      const int s = next_slot();
+      slot[i] = s;
+      ck(cudaMemcpyAsync(stage_[s], ch[i].dsrc, ch[i].len * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H");
+      ck(cudaEventRecord(ev_[s], stream_), "record");
+    };
+    const size_t ahead = std::min<size_t>(kSlots, ch.size());
+    for (size_t i = 0; i < ahead; ++i) issue(i);
+    for (size_t i = 0; i < ch.size(); ++i) {
+      ck(cudaEventSynchronize(ev_[slot[i]]), "D2H sync");
+      pool_.copy(ch[i].dst, stage_[slot[i]], ch[i].len * sizeof(double));
+      if (i + kSlots < ch.size()) issue(i + kSlots);
+    }
+  }
+
+ private:
+  static void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("octrans_accel xfer ") + what + ": " + cudaGetErrorString(e));
+  }
+  int next_slot() {
+    const int s = slot_;
+    slot_ = (slot_ + 1) % kSlots;
+    return s;
+  }
+  const size_t kChunk;
+  const int kSlots;
+  cudaStream_t stream_;
+  CopyPool pool_;
+  double* stage_[kMaxSlots] = {};
+  cudaEvent_t ev_[kMaxSlots] = {};
+  int slot_ = 0;
+};
+
+}  // namespace octrans_accel

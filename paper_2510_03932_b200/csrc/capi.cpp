@@ -934,6 +934,16 @@ int ocg_eval_status(ocg_eval* e, ocg_stream s) {
   OCG_GUARD_END
 }
 
+int ocg_eval_status_async(ocg_eval* e, int* host_flag, ocg_stream s) {
+  if (!e || !host_flag) return fail(OCG_ERR_ARG, "null argument");
+  OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
+  ck(cudaMemcpyAsync(host_flag, e->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st(s)), "flag d2h");
+  ck(cudaMemsetAsync(e->flag.p, 0, sizeof(int), st(s)), "flag reset");
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
 int64_t ocg_eval_launch_count(const ocg_eval* e) { return e ? e->launches : -1; }
 
 // EvalContext::compute_scaling (eval.cpp:266-286): gradient and Jacobian at x0
