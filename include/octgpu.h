@@ -213,6 +213,55 @@ int ocg_debug_compile(const ocg_model* m, int fma, int block);
  * context with these options would load; NULL on failure (ocg_free it). */
 char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_options* opts);
 
+/* ---- node-range shards over several GPUs -------------------
+ * A communicator between the ranks of one evaluation: NCCL (the library
+ * loads libnccl.so.2 at run time; rank 0 makes the unique id and the caller
+ * broadcasts it), or host callbacks (e.g. torch.distributed over gloo), whose
+ * buffers are host memory. Callbacks return 0 on success; a zero count means
+ * "nothing to send / receive" and must not communicate. */
+typedef struct ocg_comm ocg_comm;
+typedef struct {
+  void* ctx;
+  /* in place over all ranks: element-wise sum of n doubles / max of n int32 */
+  int (*allreduce_sum_f64)(void* ctx, double* buf, int64_t n);
+  int (*allreduce_max_i32)(void* ctx, int32_t* buf, int64_t n);
+  /* send n_send doubles to rank `to` and receive n_recv doubles from rank `from` */
+  int (*sendrecv_f64)(void* ctx, const double* send, int64_t n_send, int to, double* recv, int64_t n_recv, int from);
+} ocg_comm_host_fns;
+int ocg_comm_nccl_unique_id(unsigned char id[128]);
+int ocg_comm_create_nccl(const unsigned char id[128], int rank, int world, int device, ocg_comm** out);
+int ocg_comm_create_host(const ocg_comm_host_fns* fns, int rank, int world, int device, ocg_comm** out);
+void ocg_comm_destroy(ocg_comm* c);
+/* The shard of `comm`'s rank: main grid indices [lo, hi) with boundaries on
+ * multiples of 512 (no objective chunk straddles two ranks), the endpoint
+ * instances on rank 0. opts->idx_lo / idx_hi / specials are ignored. The
+ * context keeps `comm` (which must outlive it). */
+int ocg_eval_create_sharded(const ocg_model* m, const ocg_eval_options* opts, ocg_comm* comm, ocg_eval** out);
+/* out[6] = idx_lo, idx_hi, specials, rank, world, halo doubles per exchange */
+int ocg_eval_shard(const ocg_eval* e, int64_t* out);
+/* x_dev (device, nvar): the slots this rank owns copied from x_host (host,
+ * nvar), then the halo nodes from their owners (ocg_eval_halo_exchange).
+ * Returns the host->device bytes in *h2d_bytes (may be NULL). */
+int ocg_eval_scatter_x(ocg_eval* e, const double* x_host, double* x_dev, int64_t* h2d_bytes, ocg_stream s);
+/* the nodes this rank reads but does not own, from their owners, into x_dev */
+int ocg_eval_halo_exchange(ocg_eval* e, double* x_dev, ocg_stream s);
+/* lambda_dev (device, m_con): the rows this rank's instances read, from lambda_host */
+int ocg_eval_scatter_rows(ocg_eval* e, const double* lambda_host, double* lambda_dev, int64_t* h2d_bytes,
+                          ocg_stream s);
+/* ocg_eval_status over all ranks (the ok flags max-reduced): OCG_OK or OCG_EVAL_DOMAIN on every rank */
+int ocg_eval_status_all(ocg_eval* e, ocg_stream s);
+/* the scaled objective over all ranks into *f (host): each rank's chunk
+ * partials, the chunks it does not own zeroed, summed over the ranks (one
+ * nonzero term per chunk) and combined in the reference's order; equal bit
+ * for bit to ocg_eval_objective on one device. OCG_EVAL_DOMAIN if any rank
+ * saw a non-finite value. */
+int ocg_eval_objective_all(ocg_eval* e, const double* x_dev, double* f, ocg_stream s);
+
+/* Host only: rank's shard plan as JSON (ocg_free it): {"lo", "hi", "specials",
+ * "x_own": [[off, len]...], "send_to"/"recv_from": [[[off, len]...] per peer],
+ * "rows": [[off, len]...], "chunk_owned": [0/1...], "halo_doubles"}. */
+char* ocg_shard_plan_json(const ocg_model* m, int rank, int world);
+
 /* ---- Reduction + KktAssembler (eval.cpp:290-440) -------------------------- */
 int ocg_kkt_create(const ocg_model* m, ocg_eval* e, ocg_kkt** out);
 void ocg_kkt_destroy(ocg_kkt* k);

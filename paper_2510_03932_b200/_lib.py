@@ -31,6 +31,9 @@ EXPORTS = [
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
     "ocg_ldl_create_ex", "ocg_ldl_order", "ocg_ldl_factor_nnz", "ocg_ldl_factors", "ocg_ldl_ref_symbolic",
+    "ocg_comm_nccl_unique_id", "ocg_comm_create_nccl", "ocg_comm_create_host", "ocg_comm_destroy",
+    "ocg_eval_create_sharded", "ocg_eval_shard", "ocg_eval_scatter_x", "ocg_eval_halo_exchange",
+    "ocg_eval_scatter_rows", "ocg_eval_status_all", "ocg_eval_objective_all", "ocg_shard_plan_json",
     "ocg_kkt_norm_inf", "ocg_ipm_default_options", "ocg_ipm_solve",
     "ocg_ipm_ctx_create", "ocg_ipm_ctx_destroy", "ocg_ipm_ctx_solve", "ocg_ipm_batch_solve",
 ]
@@ -48,6 +51,18 @@ class IpmOptions(C.Structure):
                 ("reg_dual_scale", C.c_double), ("reg_dual_power", C.c_double), ("reg_max_delta", C.c_double),
                 ("scale", C.c_int), ("bound_relax_factor", C.c_double), ("refine_rounds", C.c_int),
                 ("refine_trigger", C.c_double), ("verbose", C.c_int), ("kkt_order", C.c_int)]
+
+
+# ocg_comm_host_fns callbacks
+ALLREDUCE_F64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+ALLREDUCE_I32 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.c_int64)
+SENDRECV_F64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_int, C.POINTER(C.c_double),
+                           C.c_int64, C.c_int)
+
+
+class CommHostFns(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allreduce_sum_f64", ALLREDUCE_F64), ("allreduce_max_i32", ALLREDUCE_I32),
+                ("sendrecv_f64", SENDRECV_F64)]
 
 
 class IpmResult(C.Structure):
@@ -137,6 +152,18 @@ def _load() -> C.CDLL:
         "ocg_ldl_factor_nnz": (i64, [vp]),
         "ocg_ldl_factors": (i32, [vp, dp, dp, dp, dp, dp]),
         "ocg_ldl_ref_symbolic": (i32, [i64, dp, dp, i64, i64, dp, dp, dp, dp, dp]),
+        "ocg_comm_nccl_unique_id": (i32, [dp]),
+        "ocg_comm_create_nccl": (i32, [dp, i32, i32, i32, C.POINTER(vp)]),
+        "ocg_comm_create_host": (i32, [C.POINTER(CommHostFns), i32, i32, i32, C.POINTER(vp)]),
+        "ocg_comm_destroy": (None, [vp]),
+        "ocg_eval_create_sharded": (i32, [vp, C.POINTER(EvalOptions), vp, C.POINTER(vp)]),
+        "ocg_eval_shard": (i32, [vp, dp]),
+        "ocg_eval_scatter_x": (i32, [vp, dp, dp, dp, vp]),
+        "ocg_eval_halo_exchange": (i32, [vp, dp, vp]),
+        "ocg_eval_scatter_rows": (i32, [vp, dp, dp, dp, vp]),
+        "ocg_eval_status_all": (i32, [vp, vp]),
+        "ocg_eval_objective_all": (i32, [vp, dp, dp, vp]),
+        "ocg_shard_plan_json": (vp, [vp, i32, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

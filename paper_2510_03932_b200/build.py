@@ -17,9 +17,9 @@ LIB = PKG / "libocgpu.so"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
-HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp", "refldl.cpp"]
+HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp", "refldl.cpp", "shard.cpp"]
 CUDA_SRCS = ["kernels.cu", "band.cu", "sepcr.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu", "refldl.cu"]
-HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp", "devmem.hpp", "refldl.hpp"]
+HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp", "devmem.hpp", "refldl.hpp", "shard.hpp"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -61,7 +61,7 @@ def build(verbose: bool = False) -> Path:
         objs.append(obj)
     if _stale(LIB, objs):
         cmd = [cxx, "-shared", "-pthread", "-Wl,--exclude-libs,ALL", "-o", str(LIB)] + [str(o) for o in objs] + [
-            f"-L{CUDA / 'lib64'}", "-lcudart", "-lnvrtc", f"-Wl,-rpath,{CUDA / 'lib64'}"]
+            f"-L{CUDA / 'lib64'}", "-lcudart", "-lnvrtc", "-ldl", f"-Wl,-rpath,{CUDA / 'lib64'}"]
         if verbose:
             print(" ".join(cmd))
         _run(cmd)

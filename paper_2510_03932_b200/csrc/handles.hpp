@@ -105,9 +105,16 @@ struct ocg_model {
   ocg::Nlp nlp;
 };
 
+namespace ocg {
+struct ShardPlan;  // shard.hpp
+}
+
 struct ocg_eval {
   const ocg_model* model = nullptr;
   int device = 0;
+  // ocg_eval_create_sharded: the communicator (not owned) and this rank's plan
+  ocg_comm* comm = nullptr;
+  std::shared_ptr<ocg::ShardPlan> shard;
   ocg::Layout lay;
   std::map<std::string, std::shared_ptr<ocg::JitModule>> mods;  // one module per kernel (process-wide cache)
   cudaKernel_t k_c = nullptr, k_cjac = nullptr, k_hess = nullptr, k_cjh = nullptr, k_objv = nullptr,

@@ -76,6 +76,99 @@ def synth_uniform(seed: int, lo: float, hi: float, n: int) -> np.ndarray:
     return out
 
 
+def host_comm_callbacks(group=None):
+    """The three ocg_comm_host_fns callbacks over torch.distributed (host
+    buffers as ctypes pointers; return 0 on success). A zero count does not
+    communicate (both sides of an exchange know the sizes)."""
+    import torch.distributed as dist
+
+    def to_global(r):
+        return r if group is None else dist.get_global_rank(group, r)
+
+    def allreduce_sum(ctx, buf, n):
+        try:
+            if n > 0:
+                dist.all_reduce(torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,))), op=dist.ReduceOp.SUM,
+                                group=group)
+            return 0
+        except Exception:  # noqa: BLE001 (reported to the library as a failed call)
+            return 1
+
+    def allreduce_max(ctx, buf, n):
+        try:
+            if n > 0:
+                dist.all_reduce(torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,))), op=dist.ReduceOp.MAX,
+                                group=group)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def sendrecv(ctx, sbuf, ns, to, rbuf, nr, frm):
+        try:
+            ops = []
+            if ns > 0:
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ctypeslib.as_array(sbuf, shape=(ns,)).copy()),
+                                      to_global(to), group))
+            if nr > 0:
+                ops.append(dist.P2POp(dist.irecv, torch.from_numpy(np.ctypeslib.as_array(rbuf, shape=(nr,))),
+                                      to_global(frm), group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    return allreduce_sum, allreduce_max, sendrecv
+
+
+class Comm:
+    """Communicator between the ranks of one sharded evaluation (ocg_comm):
+    Comm.nccl(...) — NCCL inside the library (ncclSend/Recv halos, ncclAllReduce),
+    or Comm.host(...) — the library's collectives through torch.distributed
+    (any backend, e.g. gloo) on host buffers."""
+
+    def __init__(self, h, rank: int, world: int, keep=None):
+        self._h, self.rank, self.world, self._keep = h, rank, world, keep
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        check(LIB.ocg_comm_nccl_unique_id(buf), "ocg_comm_nccl_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, device: int, unique_id: bytes) -> "Comm":
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(LIB.ocg_comm_create_nccl(buf, rank, world, device, C.byref(h)), "ocg_comm_create_nccl")
+        return cls(h, rank, world)
+
+    @classmethod
+    def host(cls, device: int, group=None) -> "Comm":
+        """Collectives over torch.distributed (the default group unless given)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        ar_f, ar_i, sr = host_comm_callbacks(group)
+        fns = _lib.CommHostFns(None, _lib.ALLREDUCE_F64(ar_f), _lib.ALLREDUCE_I32(ar_i), _lib.SENDRECV_F64(sr))
+        h = C.c_void_p()
+        check(LIB.ocg_comm_create_host(C.byref(fns), rank, world, device, C.byref(h)), "ocg_comm_create_host")
+        return cls(h, rank, world, keep=fns)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.ocg_comm_destroy(self._h)
+            self._h = None
+
+
+def shard_plan(model: "Model", rank: int, world: int) -> dict:
+    """Host-only: the node-range shard plan of `rank` (ocg_shard_plan_json)."""
+    p = LIB.ocg_shard_plan_json(model._h, rank, world)
+    if not p:
+        raise _lib.OcgError(LIB.ocg_last_error().decode())
+    return json.loads(_lib.take_string(p))
+
+
 class EvalContext:
     """Device EvalContext: COO structure bit-identical to the reference's; values
     in `jac_val`, `hess_val`, `grad_val` (CUDA tensors); `obj_scale`/`row_scale`
@@ -83,7 +176,10 @@ class EvalContext:
 
     def __init__(self, model: Model, device: int = 0, fma: bool = False, block: int = 128,
                  idx_lo: int = 0, idx_hi: int = -1, specials: bool = True, min_blocks: int = 0,
-                 split_kinds: int = -1):
+                 split_kinds: int = -1, comm: Comm | None = None):
+        """comm: a sharded context (ocg_eval_create_sharded) — this rank's
+        node range, endpoint instances on rank 0; idx_lo/idx_hi/specials are
+        then derived from the rank."""
         if not torch.cuda.is_available():
             raise RuntimeError("octgpu EvalContext needs a CUDA device (no CPU fallback)")
         self.model = model
@@ -92,7 +188,12 @@ class EvalContext:
         opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials), int(min_blocks),
                                 int(split_kinds))
         h = C.c_void_p()
-        check(LIB.ocg_eval_create(model._h, C.byref(opts), C.byref(h)), "ocg_eval_create")
+        self.comm = comm
+        if comm is None:
+            check(LIB.ocg_eval_create(model._h, C.byref(opts), C.byref(h)), "ocg_eval_create")
+        else:
+            check(LIB.ocg_eval_create_sharded(model._h, C.byref(opts), comm._h, C.byref(h)),
+                  "ocg_eval_create_sharded")
         self._h = h
         j, hh, g = C.c_int64(), C.c_int64(), C.c_int64()
         check(LIB.ocg_eval_sizes(h, C.byref(j), C.byref(hh), C.byref(g)))
@@ -116,6 +217,40 @@ class EvalContext:
         if getattr(self, "_h", None):
             LIB.ocg_eval_destroy(self._h)
             self._h = None
+
+    # ---- node-range shards (comm=...) ----
+    def shard(self) -> dict:
+        o = np.zeros(6, dtype=np.int64)
+        check(LIB.ocg_eval_shard(self._h, o.ctypes.data))
+        return dict(zip(["idx_lo", "idx_hi", "specials", "rank", "world", "halo_doubles"], (int(v) for v in o)))
+
+    def scatter_x(self, x_host: np.ndarray, x_dev: torch.Tensor, stream=None) -> int:
+        """x_dev <- the slots this rank owns of x_host, then the halo from the
+        owners; returns the host->device bytes."""
+        x_host = np.ascontiguousarray(x_host, dtype=np.float64)
+        nb = C.c_int64()
+        check(LIB.ocg_eval_scatter_x(self._h, x_host.ctypes.data, _ptr(x_dev), C.byref(nb), _stream(stream)),
+              "ocg_eval_scatter_x")
+        return nb.value
+
+    def scatter_rows(self, lam_host: np.ndarray, lam_dev: torch.Tensor, stream=None) -> int:
+        lam_host = np.ascontiguousarray(lam_host, dtype=np.float64)
+        nb = C.c_int64()
+        check(LIB.ocg_eval_scatter_rows(self._h, lam_host.ctypes.data, _ptr(lam_dev), C.byref(nb), _stream(stream)),
+              "ocg_eval_scatter_rows")
+        return nb.value
+
+    def halo_exchange(self, x_dev: torch.Tensor, stream=None) -> None:
+        check(LIB.ocg_eval_halo_exchange(self._h, _ptr(x_dev), _stream(stream)), "ocg_eval_halo_exchange")
+
+    def status_all(self, stream=None) -> bool:
+        return check(LIB.ocg_eval_status_all(self._h, _stream(stream)), "ocg_eval_status_all") == _lib.OCG_OK
+
+    def objective_all(self, x_dev: torch.Tensor, stream=None) -> tuple[bool, float]:
+        f = C.c_double()
+        rc = check(LIB.ocg_eval_objective_all(self._h, _ptr(x_dev), C.byref(f), _stream(stream)),
+                   "ocg_eval_objective_all")
+        return rc == _lib.OCG_OK, f.value
 
     # ---- structure queries (host int64, EvalContext's public members) ----
     def structure(self) -> dict:
