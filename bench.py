@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--scheme", default="trapezoid")
     ap.add_argument("--block", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lib-shard", action="store_true",
+                    help="use the library's sharded context (NCCL communicator) even on one rank")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the other eval configs (quadrotor 1e6 and 1e5, hang glider, shuttle; 'extra' key)")
     ap.add_argument("--solve", default="quadrotor:100000",
@@ -390,18 +392,24 @@ def run_reference(args) -> None:
 # our arm
 # ---------------------------------------------------------------------------
 
-def time_eval_config(ec, xd, ld, c, flush, sink, stream, steps: int, warmup: int):
-    """Per-step CUDA events around exactly one fused J+H launch; the L2 flush
-    (a 512 MiB read) runs before each step outside the events."""
+def time_eval_config(ec, xd, ld, c, flush, sink, stream, steps: int, warmup: int, halo: bool = False):
+    """Per-step CUDA events around exactly one fused J+H launch — preceded, on
+    a sharded context, by the halo exchange over the communicator (ncclSend /
+    ncclRecv on the same stream); the L2 flush (a 512 MiB read) runs before
+    each step outside the events."""
     import torch
     for _ in range(warmup):
         torch.sum(flush, dim=0, out=sink)
+        if halo:
+            ec.halo_exchange(xd, stream)
         ec.launch_jac_hess(xd, ld, c, stream)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     n0 = ec.launch_count
     for s, e in ev:
         torch.sum(flush, dim=0, out=sink)
         s.record(stream)
+        if halo:
+            ec.halo_exchange(xd, stream)
         ec.launch_jac_hess(xd, ld, c, stream)
         e.record(stream)
     stream.synchronize()
@@ -437,15 +445,37 @@ def run_ours(args) -> None:
     N = args.N * world
     m = Model(src, N, args.scheme)
     st = m.structure()
-    a, b = shard_of(st, rank, world, args.N)
-    specials = rank == 0
-    ec = EvalContext(m, device=local, block=args.block, idx_lo=a, idx_hi=b if rank < world - 1 else -1,
-                     specials=specials)
     x, lam = m.synth_acceptance(20250808)
-    xd = torch.as_tensor(x, device=dev)
-    ld = torch.as_tensor(lam, device=dev)
+    sharded = world > 1 or args.lib_shard
+    comm = None
+    if sharded:
+        # node-range shards inside the library (ocg_eval_create_sharded): NCCL
+        # when every rank has its own GPU, else torch.distributed callbacks
+        from paper_2510_03932_b200 import Comm
+        if world == 1 or dist.get_backend() == "nccl":
+            uid = [Comm.nccl_unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(uid, src=0)
+            comm = Comm.nccl(rank, world, local, uid[0])
+        else:
+            comm = Comm.host(local)
+        ec = EvalContext(m, device=local, block=args.block, comm=comm)
+        sh = ec.shard()
+        a, b, specials = sh["idx_lo"], sh["idx_hi"], bool(sh["specials"])
+        xd = torch.full((m.nvar,), float("nan"), dtype=torch.float64, device=dev)
+        ld = torch.full((m.m_con,), float("nan"), dtype=torch.float64, device=dev)
+        ec.scatter_x(x, xd, stream)  # owned slots + halo over the communicator
+        ec.scatter_rows(lam, ld, stream)
+    else:
+        a, b = shard_of(st, 0, 1, args.N)
+        specials = True
+        ec = EvalContext(m, device=local, block=args.block)
+        xd = torch.as_tensor(x, device=dev)
+        ld = torch.as_tensor(lam, device=dev)
     c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
     assert ec.eval_jac_hess(xd, ld, c), "evaluation flagged a domain error on the synthetic point"
+    if sharded:
+        assert ec.status_all(stream)
     flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
     sink = torch.zeros((), dtype=torch.float64, device=dev)
 
@@ -456,13 +486,14 @@ def run_ours(args) -> None:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t_wall0 = time.perf_counter()
-    times, launches = time_eval_config(ec, xd, ld, c, flush, sink, stream, args.steps, args.warmup)
+    times, launches = time_eval_config(ec, xd, ld, c, flush, sink, stream, args.steps, args.warmup,
+                                       halo=sharded)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - t_wall0
     t_local = float(np.mean(times))
-    ok = ec.status(stream)
+    ok = ec.status_all(stream) if sharded else ec.status(stream)
     dev_out = {"c": c.cpu().numpy(), "jac": ec.jac_val.cpu().numpy(), "hess": ec.hess_val.cpu().numpy()}
 
     # end to end through the public API with host buffers: pinned x, lambda in;
@@ -477,10 +508,15 @@ def run_ours(args) -> None:
     h2d = 8 * (m.nvar + m.m_con)
     d2h = 8 * sum(n for _, _, n in segs)
     e2e_steps = max(3, min(args.steps, 20))
+    xh_np, lh_np = xh.numpy(), lh.numpy()
 
     def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        ld.copy_(lh, non_blocking=True)
+        nonlocal h2d
+        if sharded:  # this rank's slots and rows only, the halo over the communicator
+            h2d = ec.scatter_x(xh_np, xd, stream) + ec.scatter_rows(lh_np, ld, stream)
+        else:
+            xd.copy_(xh, non_blocking=True)
+            ld.copy_(lh, non_blocking=True)
         ec.launch_jac_hess(xd, ld, c, stream)
         for buf, s0, n in segs:
             host[buf][s0:s0 + n].copy_(devbuf[buf][s0:s0 + n], non_blocking=True)
@@ -498,7 +534,7 @@ def run_ours(args) -> None:
         e.record(stream)
         e.synchronize()
         e2e_t.append(s.elapsed_time(e) * 1e-3)
-    ok = ok and ec.status(stream)
+    ok = ok and (ec.status_all(stream) if sharded else ec.status(stream))
     clk = clocks.stop()
     # a result read back must match the device copy
     for buf, s0, n in segs[:3]:
