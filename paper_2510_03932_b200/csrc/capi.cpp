@@ -1104,6 +1104,12 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
     K->mv_long_part.alloc(static_cast<size_t>(K->n_mv_long) * ocg::dev::kLongBlocks);
     K->jt_long_part.alloc(static_cast<size_t>(K->n_jt_long) * ocg::dev::kLongBlocks);
   }
+  // compact single-source codes for the assembly (kernels.hpp kkt_code32);
+  // slots in slot order (see kkt_assemble_fast_k for the source-order A/B)
+  K->src_code32.alloc(static_cast<size_t>(std::max<Index>(1, K->nnz)));
+  if (!ocg::dev::kkt_code32(K->src_ptr.p, K->src_code.p, K->nnz, K->H, K->J, K->n_slack, K->ntot, K->src_code32.p,
+                            cudaStreamPerThread))
+    K->src_code32.release();
   K->val.alloc(static_cast<size_t>(K->nnz));
   ck(cudaMemsetAsync(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double), cudaStreamPerThread), "memset");
   ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
@@ -1164,7 +1170,8 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(k->ev->device);
   ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
-                         k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s));
+                         k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s), k->src_code32.p,
+                         k->src_order.p);
   k->ev->launches += k->n_src_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END

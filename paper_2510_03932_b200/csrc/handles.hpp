@@ -182,6 +182,8 @@ struct ocg_kkt {
   std::vector<Index> colp, rowi;
   DBuf<double> val;
   DBuf<int64_t> src_ptr, src_code;
+  DBuf<uint32_t> src_code32;  // per slot in source order: (tag << 29) | index (kernels.hpp kkt_code32)
+  DBuf<int32_t> src_order;    // slots in order of their first source (kktbuild.hpp source_order)
   Index H = 0, J = 0;
   // matvec (full symmetric CSR in increasing column order)
   DBuf<int64_t> mv_ptr, mv_col, mv_vidx;

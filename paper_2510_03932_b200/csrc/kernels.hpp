@@ -57,9 +57,15 @@ void gather_sum(const double* src, const int64_t* ptr, const int32_t* idx, int64
 // K.val[p] = sum of its sources in code order (KktAssembler::assemble,
 // eval.cpp:429-440): code < H: hess[code]; < H+J: jac[code-H]; < H+J+S: -1.0;
 // < H+J+S+ntot: sigma[code-H-J-S]; else 0 (the dual diagonal's structural slot).
+// code32 / order (kkt_code32 + kktbuild.hpp source_order, may be NULL): the
+// slots walked in source order, single-source slots through one 32-bit word.
 void kkt_assemble(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
                   const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
-                  LongRows lr, cudaStream_t s);
+                  LongRows lr, cudaStream_t s, const uint32_t* code32 = nullptr, const int32_t* order = nullptr);
+// per slot: (array tag << 29) | index for a single source, a "several" tag
+// otherwise; false (nothing written) when an index does not fit 29 bits
+bool kkt_code32(const int64_t* ptr, const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot,
+                uint32_t* out, cudaStream_t s);
 
 // y[i] = sum over the full symmetric row i (increasing column) of K_ij x_j —
 // the accumulation order of sparse::matvec_sym (sparse.cpp:51-61).

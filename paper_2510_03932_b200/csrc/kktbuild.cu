@@ -366,4 +366,34 @@ void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out) {
   ck(cudaStreamSynchronize(s), "sync");
 }
 
+// Slots ordered by their first source code (kktbuild.hpp source_order).
+__global__ void first_code_k(const int64_t* __restrict__ ptr, const int64_t* __restrict__ code, int64_t nnz,
+                             int64_t max_code, unsigned long long* __restrict__ key, int64_t* __restrict__ slot) {
+  GRID_LOOP(p, nnz) {
+    key[p] = static_cast<unsigned long long>(ptr[p + 1] > ptr[p] ? code[ptr[p]] : max_code);
+    slot[p] = p;
+  }
+}
+__global__ void permute_codes_k(const int64_t* __restrict__ slot, const uint32_t* __restrict__ code32, int64_t nnz,
+                                int32_t* __restrict__ order, uint32_t* __restrict__ code32_sorted) {
+  GRID_LOOP(t, nnz) {
+    const int64_t p = slot[t];
+    order[t] = static_cast<int32_t>(p);
+    code32_sorted[t] = code32[p];
+  }
+}
+
+void source_order(const int64_t* ptr, const int64_t* code, const uint32_t* code32, int64_t nnz, int64_t max_code,
+                  int32_t* order, uint32_t* code32_sorted, cudaStream_t s) {
+  if (nnz <= 0) return;
+  auto* key = dalloc<unsigned long long>(static_cast<size_t>(nnz), s);
+  auto* slot = dalloc<int64_t>(static_cast<size_t>(nnz), s);
+  first_code_k<<<grid_for(nnz), 256, 0, s>>>(ptr, code, nnz, max_code, key, slot);
+  sort_pairs(key, slot, nnz, bits_for(max_code + 1), s);
+  permute_codes_k<<<grid_for(nnz), 256, 0, s>>>(slot, code32, nnz, order, code32_sorted);
+  ck(cudaStreamSynchronize(s), "sync");
+  dfree(key);
+  dfree(slot);
+}
+
 }  // namespace ocg::dev

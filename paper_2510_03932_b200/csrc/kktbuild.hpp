@@ -32,4 +32,12 @@ struct KktBuildOut {
 
 void build_kkt(const KktBuildIn& in, cudaStream_t s, KktBuildOut& out);
 
+// The assembly's slots ordered by their first source code: order[t] = slot,
+// code32_sorted[t] = code32[slot]. Walking slots in this order the assembly
+// reads hess / jac / sigma nearly sequentially (coalesced) and scatters the
+// writes, instead of gathering the sources slot by slot (kernels.cu
+// kkt_assemble_fast_k).
+void source_order(const int64_t* ptr, const int64_t* code, const uint32_t* code32, int64_t nnz, int64_t max_code,
+                  int32_t* order, uint32_t* code32_sorted, cudaStream_t s);
+
 }  // namespace ocg::dev
