@@ -50,7 +50,8 @@ const char* ocg_version(void);
 /* Library-internal device memory: large plan blocks are kept in a bounded
  * cache (OCG_CACHE_MAX_MB, default 8192 MiB per device) and a private
  * stream-ordered pool per device; this returns both to the driver for
- * `device` (< 0: every device). Call with no work of the library in flight. */
+ * `device` (< 0: every device), after dropping ocg_ipm_solve's cached plans.
+ * Call with no work of the library in flight. */
 int ocg_release_cached_memory(int device);
 
 /* ---- model: parse + transcribe (reference transcribe.hpp:56-59) ---------- */
@@ -373,7 +374,10 @@ void ocg_ipm_ctx_destroy(ocg_ipm_ctx* c);
 int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double* lvar, const double* uvar,
                       const double* x_start, const double* lcon, const double* ucon, ocg_ipm_result* out,
                       double* x_out);
-/* x_out[nvar] (host, may be NULL): final iterate */
+/* x_out[nvar] (host, may be NULL): final iterate. The plans (evaluation,
+ * KKT pattern, factorization) are kept per (model, device) and reused by the
+ * next ocg_ipm_solve of the same model, as an ocg_ipm_ctx would; they go with
+ * ocg_model_destroy or ocg_release_cached_memory (OCG_IPM_PLAN_CACHE=0: off). */
 int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm_result* out, double* x_out);
 
 /* nb independent instances of the model's structure solved together

@@ -471,7 +471,11 @@ int ocg_model_create_from_nlp(const ocg_nlp_desc* d, ocg_model** out) {
   }
 }
 
-void ocg_model_destroy(ocg_model* m) { delete m; }
+void ocg_model_destroy(ocg_model* m) {
+  if (!m) return;
+  ocg::hd::drop_ipm_plans(m);  // ocg_ipm_solve's cached plans of this model
+  delete m;
+}
 int64_t ocg_model_nvar(const ocg_model* m) { return m ? m->nlp.nvar : -1; }
 int64_t ocg_model_mcon(const ocg_model* m) { return m ? m->nlp.m_con : -1; }
 int64_t ocg_model_grid(const ocg_model* m) { return m ? m->nlp.N : -1; }
@@ -1463,6 +1467,7 @@ void ocg_ldl_destroy(ocg_ldl* l) {
 }
 
 int ocg_release_cached_memory(int device) {
+  ocg::hd::drop_ipm_plans(nullptr);
   ocg::mem::trim(device);
   return OCG_OK;
 }

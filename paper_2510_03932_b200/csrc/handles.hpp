@@ -230,4 +230,6 @@ namespace ocg::hd {
 int ldl_create(ocg_kkt* k, int target, ocg_ldl** out);
 // ocg_last_error's message for this thread; returns code
 int set_error(int code, const std::string& msg);
+// ipm.cpp: drop ocg_ipm_solve's cached plans of a model (NULL: all)
+void drop_ipm_plans(const ocg_model* m);
 }  // namespace ocg::hd

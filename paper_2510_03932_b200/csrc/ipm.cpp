@@ -20,7 +20,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -854,6 +856,60 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
 
 }  // namespace
 
+struct ocg_ipm_ctx {
+  std::unique_ptr<DeviceSolver> solver;
+};
+
+namespace {
+
+// Process-wide plans of ocg_ipm_solve, per (model, device): the evaluation
+// plan, the KKT pattern and the factorization plans are built by the first
+// solve and reused by the next ones, as an ocg_ipm_ctx would. Dropped when
+// the model is destroyed (ocg_model_destroy) or by ocg_release_cached_memory;
+// OCG_IPM_PLAN_CACHE=0 turns the cache off.
+struct PlanCacheEntry {
+  std::mutex mu;  // held while a solve uses the plans
+  std::unique_ptr<DeviceSolver> solver;
+};
+std::mutex g_plan_mu;
+std::map<std::pair<const ocg_model*, int>, std::shared_ptr<PlanCacheEntry>>& plan_cache() {
+  static auto* c = new std::map<std::pair<const ocg_model*, int>, std::shared_ptr<PlanCacheEntry>>;
+  return *c;
+}
+std::shared_ptr<PlanCacheEntry> plan_cache_entry(const ocg_model* m, int device) {
+  if (const char* e = std::getenv("OCG_IPM_PLAN_CACHE"); e && std::atoi(e) == 0) return nullptr;
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto& c = plan_cache();
+  auto& slot = c[{m, device}];
+  if (!slot) slot = std::make_shared<PlanCacheEntry>();
+  return slot;
+}
+
+}  // namespace
+
+namespace ocg::hd {
+// drop the cached solve plans of model m (every device; all models when m is NULL)
+void drop_ipm_plans(const ocg_model* m) {
+  std::vector<std::shared_ptr<PlanCacheEntry>> gone;
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto& c = plan_cache();
+    for (auto it = c.begin(); it != c.end();) {
+      if (!m || it->first.first == m) {
+        gone.push_back(it->second);
+        it = c.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  for (auto& e : gone) {
+    std::lock_guard<std::mutex> lk(e->mu);  // wait for a solve in flight
+    e->solver.reset();
+  }
+}
+}  // namespace ocg::hd
+
 extern "C" {
 
 void ocg_ipm_default_options(ocg_ipm_options* o) {
@@ -876,9 +932,7 @@ void ocg_ipm_default_options(ocg_ipm_options* o) {
   o->kkt_order = OCG_LDL_BAND;
 }
 
-struct ocg_ipm_ctx {
-  std::unique_ptr<DeviceSolver> solver;
-};
+
 
 int ocg_ipm_ctx_create(ocg_model* m, int device, ocg_ipm_ctx** out) {
   if (!m || !out) return ocg::hd::set_error(OCG_ERR_ARG, "ocg_ipm_ctx_create: null argument");
@@ -922,6 +976,16 @@ int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm
   if (opts) o = *opts;
   try {
     ocg::mem::DeviceScope ds(device);
+    // plans of this model and device from a previous solve, unless another
+    // thread is solving with them right now (then this solve builds its own)
+    std::shared_ptr<PlanCacheEntry> e = plan_cache_entry(m, device);
+    std::unique_lock<std::mutex> lk;
+    if (e) lk = std::unique_lock<std::mutex>(e->mu, std::try_to_lock);
+    if (e && lk.owns_lock()) {
+      if (!e->solver) e->solver = std::make_unique<DeviceSolver>(m, o, device);
+      e->solver->set_instance(o, nullptr, nullptr, nullptr, nullptr, nullptr);
+      return e->solver->run(out, x_out);
+    }
     DeviceSolver solver(m, o, device);
     return solver.run(out, x_out);
   } catch (const std::exception& ex) {
