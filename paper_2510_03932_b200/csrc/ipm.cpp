@@ -242,6 +242,10 @@ class DeviceSolver {
 
   void setup(std::vector<double>& row_scale);
   void alloc_state(size_t nv, size_t mc);
+  // OCG_IPM_DUMP=<dir> OCG_IPM_DUMP_ITERS=i,j,...: the iterate and the vector
+  // kernels' results at those iterations, for tests against the reference's
+  // Solver math (tests/test_ipm_kernels_gpu.py)
+  void dump_iterate(int iter, double alpha_max, double dphi);
   double theta_of(const double* g) { return ocg::ipmdev::l1(g, m_, sc_, s_); }
   double kkt_error(double mu, const double* g, double& comp_out, double& stat_out);
   void add_to_filter(double theta, double phi);
@@ -476,6 +480,90 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   ckc(cudaMemsetAsync(lambda_.p, 0, std::max<size_t>(static_cast<size_t>(m_), 1) * sizeof(double), s_), "memset");
   ckc(cudaStreamSynchronize(s_), "sync");
   lap("slacks + duals");
+}
+
+void DeviceSolver::dump_iterate(int iter, double alpha_max, double dphi) {
+  const char* dir = std::getenv("OCG_IPM_DUMP");
+  const char* which = std::getenv("OCG_IPM_DUMP_ITERS");
+  if (!dir || !which) return;
+  bool hit = false;
+  for (const char* p = which; *p;) {
+    if (std::atoi(p) == iter) hit = true;
+    while (*p && *p != ',') ++p;
+    if (*p == ',') ++p;
+  }
+  if (!hit) return;
+  const std::string base = std::string(dir) + "/it" + std::to_string(iter) + "_";
+  auto put = [&](const char* name, const void* dev, size_t bytes) {
+    std::vector<char> h(bytes);
+    if (bytes) ckc(cudaMemcpyAsync(h.data(), dev, bytes, cudaMemcpyDeviceToHost, s_), "dump d2h");
+    ckc(cudaStreamSynchronize(s_), "sync");
+    if (FILE* f = std::fopen((base + name).c_str(), "wb")) {
+      if (bytes) std::fwrite(h.data(), 1, bytes, f);
+      std::fclose(f);
+    }
+  };
+  const size_t D = sizeof(double);
+  put("x.f64", x_->p, static_cast<size_t>(nvar_) * D);
+  put("s.f64", s_v_->p, static_cast<size_t>(nslack_) * D);
+  put("zl.f64", zl_.p, static_cast<size_t>(ntot_) * D);
+  put("zu.f64", zu_.p, static_cast<size_t>(ntot_) * D);
+  put("lambda.f64", lambda_.p, static_cast<size_t>(m_) * D);
+  put("grad.f64", grad_->p, static_cast<size_t>(nvar_) * D);
+  put("jtlam.f64", jtlam_.p, static_cast<size_t>(ntot_) * D);
+  put("g.f64", g_.p, static_cast<size_t>(m_) * D);
+  put("c.f64", c_->p, static_cast<size_t>(mcon_) * D);
+  put("step.f64", step_.p, static_cast<size_t>(dim_) * D);
+  put("sigma.f64", sigma_.p, static_cast<size_t>(ntot_) * D);
+  put("rhs.f64", rhs_.p, static_cast<size_t>(dim_) * D);
+  put("free_slot.i64", free_slot_.p, static_cast<size_t>(nfree_) * sizeof(int64_t));
+  put("dual_row.i64", dual_row_.p, static_cast<size_t>(m_) * sizeof(int64_t));
+  put("slack_index.i64", slack_index_.p, static_cast<size_t>(mcon_) * sizeof(int64_t));
+  put("lb.f64", lb_.p, static_cast<size_t>(ntot_) * D);
+  put("ub.f64", ub_.p, static_cast<size_t>(ntot_) * D);
+  put("has_lb.i8", has_lb_.p, static_cast<size_t>(ntot_));
+  put("has_ub.i8", has_ub_.p, static_cast<size_t>(ntot_));
+  put("lcon_s.f64", lcon_s_.p, static_cast<size_t>(mcon_) * D);
+  // the remaining kernels on scratch copies (the solver's state is untouched)
+  double p5[5] = {0, 0, 0, 0, 0};
+  ocg::ipmdev::kkt_error_parts(P_, x_->p, s_v_->p, zl_.p, zu_.p, lambda_.p, grad_->p, jtlam_.p, g_.p, mu_, p5, sc_, s_);
+  double bar = 0.0;
+  const bool bar_ok = ocg::ipmdev::barrier(P_, x_->p, s_v_->p, bar, sc_, s_);
+  const double theta = theta_of(g_.p);
+  DVec<double> dzl(static_cast<size_t>(std::max<int64_t>(1, ntot_))), dzu(static_cast<size_t>(std::max<int64_t>(1, ntot_)));
+  const double alpha_z = ocg::ipmdev::dual_direction(P_, x_->p, s_v_->p, zl_.p, zu_.p, step_.p, mu_, tau_, dzl.p, dzu.p,
+                                                     sc_, s_);
+  put("dzl.f64", dzl.p, static_cast<size_t>(ntot_) * D);
+  put("dzu.f64", dzu.p, static_cast<size_t>(ntot_) * D);
+  // a trial point at alpha_max and the accepted multipliers there
+  DVec<double> xn(static_cast<size_t>(std::max<int64_t>(1, nvar_))), sn(static_cast<size_t>(std::max<int64_t>(1, nslack_)));
+  DVec<double> lam2(static_cast<size_t>(std::max<int64_t>(1, m_))), zl2(static_cast<size_t>(std::max<int64_t>(1, ntot_))),
+      zu2(static_cast<size_t>(std::max<int64_t>(1, ntot_)));
+  ckc(cudaMemcpyAsync(xn.p, x_->p, static_cast<size_t>(nvar_) * D, cudaMemcpyDeviceToDevice, s_), "copy");
+  ckc(cudaMemcpyAsync(lam2.p, lambda_.p, static_cast<size_t>(m_) * D, cudaMemcpyDeviceToDevice, s_), "copy");
+  ckc(cudaMemcpyAsync(zl2.p, zl_.p, static_cast<size_t>(ntot_) * D, cudaMemcpyDeviceToDevice, s_), "copy");
+  ckc(cudaMemcpyAsync(zu2.p, zu_.p, static_cast<size_t>(ntot_) * D, cudaMemcpyDeviceToDevice, s_), "copy");
+  ocg::ipmdev::trial(P_, x_->p, s_v_->p, step_.p, alpha_max, xn.p, sn.p, s_);
+  const double az = std::min(alpha_z, std::max(alpha_max, 1e-2));
+  ocg::ipmdev::accept(P_, step_.p, dzl.p, dzu.p, alpha_max, az, mu_, kKappaSigma, xn.p, sn.p, lam2.p, zl2.p, zu2.p, s_);
+  put("x_trial.f64", xn.p, static_cast<size_t>(nvar_) * D);
+  put("s_trial.f64", sn.p, static_cast<size_t>(nslack_) * D);
+  put("lambda_acc.f64", lam2.p, static_cast<size_t>(m_) * D);
+  put("zl_acc.f64", zl2.p, static_cast<size_t>(ntot_) * D);
+  put("zu_acc.f64", zu2.p, static_cast<size_t>(ntot_) * D);
+  if (FILE* f = std::fopen((base + "meta.json").c_str(), "w")) {
+    std::fprintf(f,
+                 "{\"iter\": %d, \"nvar\": %lld, \"m_con\": %lld, \"n_free\": %lld, \"n_slack\": %lld, "
+                 "\"ntot\": %lld, \"m\": %lld, \"dim\": %lld, \"mu\": %.17g, \"tau\": %.17g, "
+                 "\"alpha_max\": %.17g, \"dphi\": %.17g, \"kkt_parts\": [%.17g, %.17g, %.17g, %.17g, %.17g], "
+                 "\"barrier\": %.17g, \"barrier_ok\": %s, \"theta\": %.17g, \"alpha_z\": %.17g, "
+                 "\"alpha_z_used\": %.17g, \"kappa_sigma\": %.17g}\n",
+                 iter, static_cast<long long>(nvar_), static_cast<long long>(mcon_), static_cast<long long>(nfree_),
+                 static_cast<long long>(nslack_), static_cast<long long>(ntot_), static_cast<long long>(m_),
+                 static_cast<long long>(dim_), mu_, tau_, alpha_max, dphi, p5[0], p5[1], p5[2], p5[3], p5[4], bar,
+                 bar_ok ? "true" : "false", theta, alpha_z, az, kKappaSigma);
+    std::fclose(f);
+  }
 }
 
 // Solver::kkt_error (solver.cpp:260-287)
@@ -713,6 +801,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     ph = Clock();
     const double alpha_max = ocg::ipmdev::fraction_to_boundary(P_, x_->p, s_v_->p, step_.p, tau_, sc_, s_);
     const double dphi = ocg::ipmdev::dphi(P_, x_->p, s_v_->p, grad_->p, step_.p, mu_, sc_, s_);
+    if (std::getenv("OCG_IPM_DUMP")) dump_iterate(iter, alpha_max, dphi);
     const double theta_k = theta_of(g_.p);
     double phi_k = 0.0;
     {
