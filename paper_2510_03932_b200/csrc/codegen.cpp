@@ -972,6 +972,38 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         forward(E, g, "idx", false, parts(m, mb.objective, g).partials, 0, none, &inv);
       }
     }
+    // Distinct regions: the tile's outputs of every group leave together after
+    // the last group, one bulk copy per lane; each lane's copy (destination
+    // base, row length, shared-memory offset, range slice) is set up once here
+    const bool batched = opt_.distinct_regions && !opt_.split_kinds;
+    struct Copy {
+      std::string dst;
+      Index S, soff;
+      int R;
+    };
+    std::vector<Copy> copies;
+    if (batched) {
+      std::map<std::string, int> rid;
+      for (size_t q = 0; q < members.size(); ++q) {
+        const Inst& mb = members[q];
+        const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+        const std::string key = range_param(g.range, true) + "," + range_param(g.range, false);
+        if (!rid.count(key)) {
+          const int r = static_cast<int>(rid.size());
+          rid[key] = r;
+        }
+        for (const Out& o : outs[q]) copies.push_back({o.dst, o.per_k, o.soff, rid.at(key)});
+      }
+      for (size_t c0 = 0; c0 < copies.size(); c0 += 32) {
+        const std::string C = std::to_string(c0 / 32);
+        E.line("double* cd" + C + "_dst = nullptr; long long cd" + C + "_S = 0, cd" + C + "_soff = 0; int cd" + C +
+               "_R = -1;");
+        for (size_t j = c0; j < std::min(copies.size(), c0 + 32); ++j)
+          E.line("if (lane == " + std::to_string(j - c0) + ") { cd" + C + "_dst = " + copies[j].dst + "; cd" + C +
+                 "_S = " + i64(copies[j].S) + "; cd" + C + "_soff = " + i64(copies[j].soff) + "; cd" + C +
+                 "_R = " + std::to_string(copies[j].R) + "; }");
+      }
+    }
     E.open("for (long long tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb)");
     E.line("const long long ib = i0 + tile * 32;");
     E.line("const long long idx = ib + lane;");
@@ -1118,7 +1150,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       store_to_ = nullptr;
       row_from_ = nullptr;
       store_hook_ = nullptr;
-      if (outs[q].empty()) continue;
+      if (outs[q].empty() || batched) continue;
       // rows are unpadded (pitch == per_k): the tile's segment of each output
       // is contiguous in shared memory and in the COO array -> one bulk copy
       if (opt_.split_kinds) {
@@ -1143,6 +1175,30 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         E.line("const double* const bs = " + ssel + ";");
         E.line("const int bn = " + nsel + ";");
         E.line("if (lane < " + std::to_string(outs[q].size()) + " && bn > 0) { ocg_bulk_store(bd, bs, bn); ocg_bulk_commit(); }");
+        E.close();
+      }
+    }
+    if (batched && !copies.empty()) {
+      // every output of the tile, one bulk copy per lane (chunks of 32)
+      E.line("ocg_fence_async(); __syncwarp();");
+      const int nslice = static_cast<int>(slices_.size());
+      auto sel = [&](const std::string& C, const char* what) {
+        std::string e = what + std::to_string(nslice - 1);
+        for (int r = nslice - 2; r >= 0; --r)
+          e = "(cd" + C + "_R == " + std::to_string(r) + " ? " + what + std::to_string(r) + " : " + e + ")";
+        return e;
+      };
+      for (size_t c0 = 0; c0 < copies.size(); c0 += 32) {
+        const std::string C = std::to_string(c0 / 32);
+        E.open("if (cd" + C + "_R >= 0)");
+        E.line("const long long k0s = " + sel(C, "k0") + ";");
+        E.line("const int r0s = " + sel(C, "r0") + ", nks = " + sel(C, "nk") + ";");
+        E.open("if (nks > 0)");
+        E.line("double* const g = cd" + C + "_dst + k0s * cd" + C + "_S;");
+        E.line("const double* const sb = smem + cd" + C + "_soff + r0s * cd" + C + "_S;");
+        E.line("ocg_bulk_store(g, sb + ocg_shift(g, sb), nks * (int)cd" + C + "_S);");
+        E.line("ocg_bulk_commit();");
+        E.close();
         E.close();
       }
     }
