@@ -1360,6 +1360,12 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   R->V.alloc(static_cast<size_t>(H.v_len));
   R->Vs.alloc(static_cast<size_t>(H.stash_len));
   R->inertia.alloc(3);
+  const size_t nnl = static_cast<size_t>(std::max<int64_t>(1, R->nnl));
+  R->sr.alloc(nnl * 8);
+  R->ypre.alloc(nnl + 2);  // + the double a rounded-up bulk copy reads past the end
+  R->ych.alloc(nnl + 2);
+  R->chunk_foff.upload(H.chunk_foff);
+  up64(R->fl_all_ptr, H.fl_all_ptr);
   ocg::rl::Dev& d = R->dev;
   d.dim = H.dim;
   d.nnz = H.nnz;
@@ -1397,6 +1403,12 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   d.perm = R->perm.p;
   d.primal = R->primal.p;
   d.w_len = H.w_len;
+  d.fronts_len = H.fronts_len;
+  d.chunk_foff = H.fmax <= 8 ? R->chunk_foff.p : nullptr;
+  d.fl_all_ptr = R->fl_all_ptr.p;
+  d.sr = R->sr.p;
+  d.ypre = R->ypre.p;
+  d.ych = R->ych.p;
   d.stash_len = H.stash_len;
   d.v_len = H.v_len;
   return R;

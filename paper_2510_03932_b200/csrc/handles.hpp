@@ -217,7 +217,9 @@ struct ocg_ldl {
     DBuf<int32_t> nl_f, sc_child, lf_f, pa_j, pa_leaf, fl_j, rel;
     DBuf<int8_t> primal;
     DBuf<ocg::rl::ColRec> rec;
-    DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs;
+    DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs, sr, ypre, ych;
+    DBuf<int64_t> fl_all_ptr;
+    DBuf<long long> chunk_foff;
     DBuf<unsigned long long> inertia;
     ocg::rl::Dev dev;
   };

@@ -236,7 +236,8 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
   for (int64_t j = 0; j < nnl; ++j) {
     const int64_t f = H.nl_f[static_cast<size_t>(j)];
     H.nl_foff[static_cast<size_t>(j)] = w;
-    w += f * (f + 1) / 2 + f;
+    const int64_t sz = f * (f + 1) / 2 + f;
+    w += sz + (sz & 1);  // fronts start on 16 bytes: chunks of them stream by bulk copies
     H.nl_voff[static_cast<size_t>(j)] = v;
     v += f;
     const int64_t p = S.parent[static_cast<size_t>(H.nl_pos[static_cast<size_t>(j)])];
@@ -249,6 +250,7 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
       st += (f - 1) * f / 2 + (f - 1);
     }
   }
+  H.fronts_len = w;
   H.lf_aoff.resize(H.lf_pos.size());
   for (size_t i = 0; i < H.lf_pos.size(); ++i) {
     H.lf_aoff[i] = w;
@@ -295,7 +297,10 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
         terms[static_cast<size_t>(jidx[static_cast<size_t>(S.Li[static_cast<size_t>(t)])])].emplace_back(t, c);
     }
     H.fl_ptr.push_back(0);
+    H.fl_all_ptr.assign(static_cast<size_t>(nnl) + 1, 0);
     for (int64_t j = 0; j < nnl; ++j) {
+      H.fl_all_ptr[static_cast<size_t>(j) + 1] =
+          H.fl_all_ptr[static_cast<size_t>(j)] + static_cast<int64_t>(terms[static_cast<size_t>(j)].size());
       if (terms[static_cast<size_t>(j)].empty()) continue;
       H.fl_j.push_back(static_cast<int32_t>(j));
       for (const auto& [t, c] : terms[static_cast<size_t>(j)]) {
@@ -344,7 +349,19 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
     r.soff = static_cast<int>(H.nl_soff[static_cast<size_t>(j)]);
     r.sc0 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j)]);
     r.sc1 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j) + 1]);
+    r.inv8 = 0;
+    r.rel8 = 0;
+    if (r.f <= 8)
+      for (int a = 1; a < r.f; ++a)
+        r.rel8 |= static_cast<unsigned long long>(H.rel[static_cast<size_t>(r.lp + a - 1)]) << (8 * (a - 1));
+    if (r.soff == kChain && r.f <= 8 && H.nl_f[static_cast<size_t>(j) + 1] <= 8)
+      for (int a = 1; a < r.f; ++a) {
+        const int dst = H.rel[static_cast<size_t>(r.lp + a - 1)];
+        r.inv8 |= static_cast<unsigned long long>(a) << (8 * dst);
+      }
   }
+  for (int64_t j = 0; j < nnl; j += 16) H.chunk_foff.push_back(H.nl_foff[static_cast<size_t>(j)]);
+  H.chunk_foff.push_back(H.fronts_len);
   H.primal.resize(n);
   for (size_t k = 0; k < n; ++k) H.primal[k] = S.perm[k] < S.ntot ? 1 : 0;
   return H;

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -183,6 +184,9 @@ __device__ __forceinline__ void issue_meta(const Dev& P, int dir, long long blk,
                  : "memory");
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst)) + 16u),
                  "l"(reinterpret_cast<const char*>(src) + 16)
+                 : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst)) + 32u),
+                 "l"(reinterpret_cast<const char*>(src) + 32)
                  : "memory");
   }
 }
@@ -428,6 +432,154 @@ __global__ void __launch_bounds__(32) chain_factor_small_k(Dev P, const double* 
       if (c[q]) atomicAdd(inertia + q, c[q]);
 }
 
+// Fronts of at most 8 rows, register-resident: lane u owns update-matrix
+// entry (a, b), u = tri(a-1) + b-1 (28 lanes), and holds F(a,b), F(a,0),
+// F(b,0), the pivot F(0,0) and the diagonal maxima in registers. Along the
+// chain (the next column is the parent and has no stashed children) the
+// update matrix moves to the next front's owners by shuffles (ColRec::inv8),
+// added to the pre-assembled values prefetched into the ring; the pivot's
+// dependency chain per column is then shuffle -> add -> reciprocal -> three
+// products. Other transitions go through the shared-memory front as in
+// chain_factor_small_k.
+__global__ void __launch_bounds__(32) chain_factor_reg_k(Dev P, const double* __restrict__ W,
+                                                        double* __restrict__ stash, double* __restrict__ D,
+                                                        double* __restrict__ Dinv, double* __restrict__ Lx,
+                                                        unsigned long long* __restrict__ inertia) {
+  constexpr int FM = 8;
+  using S = Small<FM>;
+  constexpr int NS = kSmallSlots, L = NS - 1;
+  __shared__ unsigned char ta[kTab], tb[kTab];
+  __shared__ __align__(16) ColRec ring[kMetaRing];
+  __shared__ __align__(16) double slots[NS * S::FSLOT];
+  build_tables(ta, tb);
+  const int lane = threadIdx.x;
+  const long long n = P.nnl;
+  meta_prologue(P, 1, ring);
+  auto issue = [&](const ColRec& m, double* slot) {
+    const int tf = tri32(m.f);
+    const double* src = W + m.foff;
+#pragma unroll
+    for (int k = 0; k < (S::TF + FM + 31) / 32; ++k) {
+      const int i = lane + 32 * k;
+      if (i < tf)
+        cp8(slot + i, src + i);
+      else if (i < tf + m.f)
+        cp8(slot + S::TF + (i - tf), src + i);
+    }
+    if (lane < m.f - 1) cp4(reinterpret_cast<int*>(slot + S::TF + FM) + lane, P.rel + m.lp + lane);
+  };
+  for (int q = 0; q < L; ++q) {
+    if (q < n) issue(ring[q], slots + q * S::FSLOT);
+    cp_commit();
+  }
+  // this lane's entry (la, lb); lanes 28..31 own none (la = 0)
+  int la = 0, lb = 0;
+#pragma unroll
+  for (int a = 1; a < FM; ++a)
+    if (lane >= tri32(a - 1) && lane < tri32(a)) {
+      la = a;
+      lb = lane - tri32(a - 1) + 1;
+    }
+  const bool diag = la > 0 && la == lb;
+  double X = 0.0, Y = 0.0, Z = 0.0, Pv = 0.0, M0 = 0.0, Ma = 0.0;
+  bool need_load = true;
+  unsigned long long c[3] = {0, 0, 0};
+  int sj = 0, sa = L;
+  for (long long j = 0; j < n; ++j) {
+    if ((j & 31) == 0) issue_meta(P, 1, (j >> 5) + 2, ring);
+    if (j + L < n) issue(ring[(j + L) & (kMetaRing - 1)], slots + sa * S::FSLOT);
+    cp_commit();
+    cp_wait_n<L - 1>();
+    __syncwarp();
+    const ColRec m = ring[j & (kMetaRing - 1)];
+    const int f = m.f;
+    double* F = slots + sj * S::FSLOT;
+    const int* r = reinterpret_cast<const int*>(F + S::TF + FM);
+    if (need_load) {
+      double* ms = F + S::TF;
+      for (int q = m.sc0; q < m.sc1; ++q) {  // stashed children (rare)
+        const ColRec mc = P.rec[P.sc_child[q]];
+        const int32_t* rc = P.rel + mc.lp;
+        const double* Us = stash + mc.soff;
+        const int tu = (mc.f - 1) * mc.f / 2;
+        for (int u = lane; u < tu; u += 32) {
+          const int e = tri32(rc[ta[u] - 1]) + rc[tb[u] - 1];
+          F[e] = __dadd_rn(F[e], Us[u]);
+        }
+        for (int a = lane; a < mc.f - 1; a += 32) ms[rc[a]] = fmax(ms[rc[a]], Us[tu + a]);
+        __syncwarp();
+      }
+      X = F[tri32(la) + lb];
+      Y = F[tri32(la)];
+      Z = F[tri32(lb)];
+      Pv = F[0];
+      M0 = ms[0];
+      Ma = ms[la];
+    }
+    const bool zero = zero_pivot(Pv, M0);
+    const double dinv = zero ? 0.0 : __drcp_rn(Pv);
+    if (lane == 0) {
+      D[m.pos] = Pv;
+      Dinv[m.pos] = dinv;
+      count_pivot(Pv, zero, c);
+    }
+    const bool act = la > 0 && la < f;
+    const double Lv = __dmul_rn(Y, dinv);  // L(la) on lanes with lb == 1
+    if (act && lb == 1) Lx[m.lp + la - 1] = Lv;
+    const double U = __dsub_rn(X, __dmul_rn(__dmul_rn(Z, dinv), Y));
+    const double MU = diag ? fmax(Ma, fabs(__dmul_rn(Lv, Y))) : 0.0;
+    const int sn = sj + 1 == NS ? 0 : sj + 1;
+    need_load = true;
+    if (m.soff != kRoot) {
+      const ColRec mn = ring[(j + 1) & (kMetaRing - 1)];
+      if (m.soff == kChain && mn.sc0 == mn.sc1 && m.inv8 != 0) {
+        // register path: this lane's entry of the next front = pre-assembled + U of the row pair mapping here
+        const double* Fn = slots + sn * S::FSLOT;
+        const int ia = static_cast<int>((m.inv8 >> (8 * la)) & 0xff);
+        const int ib = static_cast<int>((m.inv8 >> (8 * lb)) & 0xff);
+        const int sx = ia && ib ? tri32(ia - 1) + ib - 1 : 0;
+        const int sy = ia ? tri32(ia - 1) : 0;
+        const int sz = ib ? tri32(ib - 1) : 0;
+        const int sm = ia ? tri32(ia - 1) + ia - 1 : 0;
+        const double vx = __shfl_sync(0xffffffffu, U, sx);
+        const double vy = __shfl_sync(0xffffffffu, U, sy);
+        const double vz = __shfl_sync(0xffffffffu, U, sz);
+        const double vp = __shfl_sync(0xffffffffu, U, 0);
+        const double m0 = __shfl_sync(0xffffffffu, MU, 0);
+        const double ma = __shfl_sync(0xffffffffu, MU, sm);
+        X = ia && ib ? __dadd_rn(Fn[tri32(la) + lb], vx) : Fn[tri32(la) + lb];
+        Y = ia ? __dadd_rn(Fn[tri32(la)], vy) : Fn[tri32(la)];
+        Z = ib ? __dadd_rn(Fn[tri32(lb)], vz) : Fn[tri32(lb)];
+        Pv = __dadd_rn(Fn[0], vp);
+        M0 = fmax(Fn[S::TF], m0);
+        Ma = ia ? fmax(Fn[S::TF + la], ma) : Fn[S::TF + la];
+        need_load = false;
+      } else if (m.soff == kChain) {
+        double* Fn = slots + sn * S::FSLOT;
+        if (act) {
+          const int e = tri32(r[la - 1]) + r[lb - 1];
+          Fn[e] = __dadd_rn(Fn[e], U);
+          if (diag) Fn[S::TF + r[la - 1]] = fmax(Fn[S::TF + r[la - 1]], MU);
+        }
+      } else {
+        double* Us = stash + m.soff;
+        const int tu = (f - 1) * f / 2;
+        if (act) {
+          Us[lane] = U;
+          if (diag) Us[tu + la - 1] = MU;
+        }
+      }
+    }
+    __syncwarp();
+    sj = sn;
+    sa = sa + 1 == NS ? 0 : sa + 1;
+  }
+  cp_wait_n<0>();
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q)
+      if (c[q]) atomicAdd(inertia + q, c[q]);
+}
+
 template <int FM>
 __global__ void __launch_bounds__(32) fwd_chain_small_k(Dev P, const double* __restrict__ Lx, double* __restrict__ y,
                                                         double* __restrict__ Vs) {
@@ -545,6 +697,329 @@ __global__ void __launch_bounds__(32) bwd_chain_small_k(Dev P, const double* __r
     sa = sa + 1 == NS ? 0 : sa + 1;
   }
   cp_wait_n<0>();
+}
+
+// ---- streamed walks (fronts <= 8 rows) ------------------------------------------
+// The chain's per-column data are contiguous in walk order (column records,
+// pre-assembled fronts, L entries + Dinv, right-hand sides), so they stream
+// into shared memory in chunks of kChunk columns by 1D bulk copies (TMA,
+// cp.async.bulk) completing on an mbarrier: one wait per chunk instead of
+// per-column asynchronous copies, and the per-column loop only reads shared
+// memory and shuffles registers.
+
+constexpr int kChunk = 16, kStages = 4;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct FStage {
+  ColRec rec[kChunk];
+  double fr[kChunk * 44];  // fronts of <= 8 rows: 36 + 8 doubles each
+};
+
+// chain factorization, fronts <= 8 rows, register-resident (see
+// chain_factor_reg_k) with the chunked bulk-copy stream. chunk_foff[c] = the
+// W offset of chunk c's first front (c = 0..nchunks, the last = fronts_len).
+__global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long long* __restrict__ chunk_foff,
+                                                           const double* __restrict__ W, double* __restrict__ stash,
+                                                           double* __restrict__ D, double* __restrict__ Dinv,
+                                                           double* __restrict__ Lx,
+                                                           unsigned long long* __restrict__ inertia) {
+  constexpr int FM = 8, TFM = FM * (FM + 1) / 2;
+  __shared__ __align__(16) FStage stg[kStages];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ unsigned char ta[kTab], tb[kTab];
+  build_tables(ta, tb);
+  const int lane = threadIdx.x;
+  const long long n = P.nnl, nch = (n + kChunk - 1) / kChunk;
+  if (lane == 0) {
+    for (int q = 0; q < kStages; ++q) mbar_init(&bar[q]);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](long long c) {  // lane 0
+    if (c >= nch) return;
+    const int st = static_cast<int>(c % kStages);
+    const long long j0 = c * kChunk;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    const long long fa = chunk_foff[c], fb = chunk_foff[c + 1];
+    const unsigned rb = static_cast<unsigned>(cnt * sizeof(ColRec)), fbytes = static_cast<unsigned>((fb - fa) * 8);
+    mbar_expect(&bar[st], rb + fbytes);
+    bulk_load(stg[st].rec, P.rec + j0, rb, &bar[st]);
+    if (fbytes) bulk_load(stg[st].fr, W + fa, fbytes, &bar[st]);
+  };
+  if (lane == 0)
+    for (long long c = 0; c < kStages - 1; ++c) issue(c);
+  int la = 0, lb = 0;
+#pragma unroll
+  for (int a = 1; a < FM; ++a)
+    if (lane >= tri32(a - 1) && lane < tri32(a)) {
+      la = a;
+      lb = lane - tri32(a - 1) + 1;
+    }
+  const bool diag = la > 0 && la == lb;
+  double X = 0.0, Y = 0.0, Z = 0.0, Pv = 0.0, M0 = 0.0, Ma = 0.0;
+  bool need_load = true;
+  unsigned long long cnts[3] = {0, 0, 0};
+  for (long long c = 0; c < nch; ++c) {
+    if (lane == 0) issue(c + kStages - 1);
+    const int st = static_cast<int>(c % kStages);
+    mbar_wait(&bar[st], static_cast<unsigned>((c / kStages) & 1));
+    const bool more = c + 1 < nch;
+    const int st1 = static_cast<int>((c + 1) % kStages);
+    if (more) mbar_wait(&bar[st1], static_cast<unsigned>(((c + 1) / kStages) & 1));
+    const long long fa = __ldg(chunk_foff + c), fa1 = more ? __ldg(chunk_foff + c + 1) : 0;
+    const long long j0 = c * kChunk;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    for (int jj = 0; jj < cnt; ++jj) {
+      const long long j = j0 + jj;
+      const ColRec m = stg[st].rec[jj];
+      const int f = m.f;
+      double* F = stg[st].fr + (m.foff - fa);
+      double* ms = F + tri32(f);
+      if (need_load) {
+        for (int q = m.sc0; q < m.sc1; ++q) {  // stashed children (rare)
+          const ColRec mc = P.rec[P.sc_child[q]];
+          const int32_t* rc = P.rel + mc.lp;
+          const double* Us = stash + mc.soff;
+          const int tu = (mc.f - 1) * mc.f / 2;
+          for (int u = lane; u < tu; u += 32) {
+            const int e = tri32(rc[ta[u] - 1]) + rc[tb[u] - 1];
+            F[e] = __dadd_rn(F[e], Us[u]);
+          }
+          for (int a = lane; a < mc.f - 1; a += 32) ms[rc[a]] = fmax(ms[rc[a]], Us[tu + a]);
+          __syncwarp();
+        }
+        const bool in = la < f;
+        X = in ? F[tri32(la) + lb] : 0.0;
+        Y = in ? F[tri32(la)] : 0.0;
+        Z = in ? F[tri32(lb)] : 0.0;
+        Pv = F[0];
+        M0 = ms[0];
+        Ma = in ? ms[la] : 0.0;
+      }
+      const bool zero = zero_pivot(Pv, M0);
+      const double dinv = zero ? 0.0 : __drcp_rn(Pv);
+      const bool act = la > 0 && la < f;
+      const double Lv = __dmul_rn(Y, dinv);
+      const double U = __dsub_rn(X, __dmul_rn(__dmul_rn(Z, dinv), Y));
+      const double MU = diag ? fmax(Ma, fabs(__dmul_rn(Lv, Y))) : 0.0;
+      if (lane == 0) {
+        D[m.pos] = Pv;
+        Dinv[m.pos] = dinv;
+        P.sr[j * 8 + 7] = dinv;
+        count_pivot(Pv, zero, cnts);
+      }
+      if (act && lb == 1) {
+        Lx[m.lp + la - 1] = Lv;
+        P.sr[j * 8 + la - 1] = Lv;
+      }
+      need_load = true;
+      if (m.soff != kRoot && j + 1 < n) {
+        const bool same = jj + 1 < cnt;
+        const ColRec& mn = same ? stg[st].rec[jj + 1] : stg[st1].rec[0];
+        double* Fn = same ? stg[st].fr + (mn.foff - fa) : stg[st1].fr + (mn.foff - fa1);
+        const int fnn = mn.f;
+        if (m.soff == kChain && mn.sc0 == mn.sc1 && m.inv8 != 0) {
+          const int ia = static_cast<int>((m.inv8 >> (8 * la)) & 0xff);
+          const int ib = static_cast<int>((m.inv8 >> (8 * lb)) & 0xff);
+          const double vx = __shfl_sync(0xffffffffu, U, ia && ib ? tri32(ia - 1) + ib - 1 : 0);
+          const double vy = __shfl_sync(0xffffffffu, U, ia ? tri32(ia - 1) : 0);
+          const double vz = __shfl_sync(0xffffffffu, U, ib ? tri32(ib - 1) : 0);
+          const double vp = __shfl_sync(0xffffffffu, U, 0);
+          const double m0 = __shfl_sync(0xffffffffu, MU, 0);
+          const double ma = __shfl_sync(0xffffffffu, MU, ia ? tri32(ia - 1) + ia - 1 : 0);
+          const bool in = la < fnn;
+          const double* msn = Fn + tri32(fnn);
+          const double px = in ? Fn[tri32(la) + lb] : 0.0, py = in ? Fn[tri32(la)] : 0.0;
+          const double pz = in ? Fn[tri32(lb)] : 0.0, pm = in ? msn[la] : 0.0;
+          X = ia && ib ? __dadd_rn(px, vx) : px;
+          Y = ia ? __dadd_rn(py, vy) : py;
+          Z = ib ? __dadd_rn(pz, vz) : pz;
+          Pv = __dadd_rn(Fn[0], vp);
+          M0 = fmax(msn[0], m0);
+          Ma = ia ? fmax(pm, ma) : pm;
+          need_load = false;
+        } else if (m.soff == kChain) {
+          if (act) {
+            const int ra = static_cast<int>((m.rel8 >> (8 * (la - 1))) & 0xff);
+            const int rb = static_cast<int>((m.rel8 >> (8 * (lb - 1))) & 0xff);
+            const int e = tri32(ra) + rb;
+            Fn[e] = __dadd_rn(Fn[e], U);
+            if (diag) Fn[tri32(fnn) + ra] = fmax(Fn[tri32(fnn) + ra], MU);
+          }
+        } else if (m.soff >= 0) {
+          double* Us = stash + m.soff;
+          const int tu = (f - 1) * f / 2;
+          if (act) {
+            Us[lane] = U;
+            if (diag) Us[tu + la - 1] = MU;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  (void)TFM;
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q)
+      if (cnts[q]) atomicAdd(inertia + q, cnts[q]);
+}
+
+// chain rows of the right-hand side minus their leaf terms, in walk order
+__global__ void fwd_pre_k(Dev P, const double* __restrict__ Lx, const double* __restrict__ y) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P.nnl;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = y[P.nl_pos[j]];
+    for (int64_t t = P.fl_all_ptr[j]; t < P.fl_all_ptr[j + 1]; ++t)
+      s = __dsub_rn(s, __dmul_rn(Lx[P.fl_lx[t]], y[P.fl_col[t]]));
+    P.ypre[j] = s;
+  }
+}
+
+struct VStage {
+  ColRec rec[kChunk];
+  double sr[kChunk * 8];
+  double y[kChunk + 2];
+};
+
+// chunk c into stage (seq % kStages): seq is the chunk's place in the walk
+// (c for the forward walk, nch-1-c for the backward one), which also sets
+// the mbarrier phase of its wait, (seq / kStages) & 1
+__device__ __forceinline__ void issue_vstage(const Dev& P, const double* yv, long long c, long long seq, long long nch,
+                                             VStage* stg, uint64_t* bar) {
+  if (c < 0 || c >= nch) return;
+  const long long n = P.nnl;
+  const int st = static_cast<int>(seq % kStages);
+  const long long j0 = c * kChunk;
+  const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+  const unsigned rb = static_cast<unsigned>(cnt * sizeof(ColRec)), sb = static_cast<unsigned>(cnt * 64),
+                 yb = static_cast<unsigned>(((cnt + 1) & ~1) * 8);
+  mbar_expect(&bar[st], rb + sb + yb);
+  bulk_load(stg[st].rec, P.rec + j0, rb, &bar[st]);
+  bulk_load(stg[st].sr, P.sr + j0 * 8, sb, &bar[st]);
+  bulk_load(stg[st].y, yv + j0, yb, &bar[st]);
+}
+
+// forward substitution along the chain: lane a holds v(a) of the current
+// front (v(0): the pivot row); v'(a') = pre + u(inv(a')) by shuffles
+__global__ void __launch_bounds__(32) fwd_chain_stream_k(Dev P, double* __restrict__ Vs) {
+  __shared__ __align__(16) VStage stg[kStages];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ double vbuf[32];
+  const int lane = threadIdx.x;
+  const long long n = P.nnl, nch = (n + kChunk - 1) / kChunk;
+  if (lane == 0) {
+    for (int q = 0; q < kStages; ++q) mbar_init(&bar[q]);
+    mbar_fence_init();
+    for (long long c = 0; c < kStages - 1; ++c) issue_vstage(P, P.ypre, c, c, nch, stg, bar);
+  }
+  __syncwarp();
+  double v = 0.0;
+  bool need_load = true;
+  for (long long c = 0; c < nch; ++c) {
+    if (lane == 0) issue_vstage(P, P.ypre, c + kStages - 1, c + kStages - 1, nch, stg, bar);
+    const int st = static_cast<int>(c % kStages);
+    mbar_wait(&bar[st], static_cast<unsigned>((c / kStages) & 1));
+    const bool more = c + 1 < nch;
+    const int st1 = static_cast<int>((c + 1) % kStages);
+    if (more) mbar_wait(&bar[st1], static_cast<unsigned>(((c + 1) / kStages) & 1));
+    const long long j0 = c * kChunk;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    for (int jj = 0; jj < cnt; ++jj) {
+      const long long j = j0 + jj;
+      const ColRec m = stg[st].rec[jj];
+      if (need_load) v = lane == 0 ? stg[st].y[jj] : 0.0;
+      if (m.sc0 < m.sc1) {  // stashed children (rare): through shared memory
+        vbuf[lane] = v;
+        __syncwarp();
+        for (int q = m.sc0; q < m.sc1; ++q) {
+          const ColRec mc = P.rec[P.sc_child[q]];
+          const int32_t* rc = P.rel + mc.lp;
+          const double* us = Vs + mc.soff;
+          for (int a = lane; a < mc.f - 1; a += 32) vbuf[rc[a]] = __dadd_rn(vbuf[rc[a]], us[a]);
+          __syncwarp();
+        }
+        v = vbuf[lane];
+        __syncwarp();
+      }
+      const double yk = __shfl_sync(0xffffffffu, v, 0);
+      if (lane == 0) P.ych[j] = yk;
+      const int f = m.f;
+      const double u = lane >= 1 && lane < f ? __dsub_rn(v, __dmul_rn(stg[st].sr[jj * 8 + lane - 1], yk)) : 0.0;
+      need_load = true;
+      if (m.soff == kChain && m.inv8 != 0 && j + 1 < n) {
+        const bool same = jj + 1 < cnt;
+        const double pre = same ? stg[st].y[jj + 1] : stg[st1].y[0];
+        const int src = lane < 8 ? static_cast<int>((m.inv8 >> (8 * lane)) & 0xff) : 0;
+        const double w = __shfl_sync(0xffffffffu, u, src);
+        v = lane == 0 ? __dadd_rn(pre, w) : (src ? w : 0.0);
+        need_load = false;
+      } else if (m.soff >= 0 && lane >= 1 && lane < f) {
+        Vs[m.soff + lane - 1] = u;
+      }
+    }
+  }
+}
+
+// backward substitution along the chain, last column first: lane a holds
+// X(a), the solution at row a of the current front (X(0) its pivot row),
+// gathered from the parent's front by shuffles (rel8)
+__global__ void __launch_bounds__(32) bwd_chain_stream_k(Dev P, double* __restrict__ xp) {
+  __shared__ __align__(16) VStage stg[kStages];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  const int lane = threadIdx.x;
+  const long long n = P.nnl, nch = (n + kChunk - 1) / kChunk;
+  if (lane == 0) {
+    for (int q = 0; q < kStages; ++q) mbar_init(&bar[q]);
+    mbar_fence_init();
+    for (long long k = 0; k < kStages - 1; ++k) issue_vstage(P, P.ych, nch - 1 - k, k, nch, stg, bar);
+  }
+  __syncwarp();
+  double Xp = 0.0;  // X of the previous (higher) column
+  for (long long k = 0; k < nch; ++k) {
+    const long long c = nch - 1 - k;
+    if (lane == 0) issue_vstage(P, P.ych, c - (kStages - 1), k + kStages - 1, nch, stg, bar);
+    const int st = static_cast<int>(k % kStages);
+    mbar_wait(&bar[st], static_cast<unsigned>((k / kStages) & 1));
+    const long long j0 = c * kChunk;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    for (int jj = cnt - 1; jj >= 0; --jj) {
+      const ColRec m = stg[st].rec[jj];
+      const int f = m.f;
+      const int ra = lane >= 1 && lane < f ? static_cast<int>((m.rel8 >> (8 * (lane - 1))) & 0xff) : 0;
+      double xa = __shfl_sync(0xffffffffu, Xp, ra);
+      if (m.soff != kChain && lane >= 1 && lane < f) xa = xp[P.Li[m.lp + lane - 1]];  // parent not the previous column
+      double t = lane >= 1 && lane < f ? __dmul_rn(stg[st].sr[jj * 8 + lane - 1], xa) : 0.0;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+      const double s = __dsub_rn(__dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]), t);
+      Xp = lane == 0 ? s : xa;
+      if (lane == 0) xp[m.pos] = s;
+      __syncwarp();
+    }
+  }
 }
 
 // ---- solves ------------------------------------------------------------------
@@ -719,7 +1194,12 @@ void factor(const Dev& P, const double* kval, double delta_w, double delta_c, do
                                                 delta_c, W);
   if (P.nleaf) leaf_k<<<grid_for(P.nleaf), kThreads, 0, s>>>(P, W, D, Dinv, Lx, inertia);
   if (P.npa) preassemble_k<<<grid_for(P.npa), kThreads, 0, s>>>(P, W, Lx);
-  if (P.nnl && P.fmax <= 8) {
+  static const int variant = std::getenv("OCG_REFLDL_KERNEL") ? std::atoi(std::getenv("OCG_REFLDL_KERNEL")) : 0;
+  if (P.nnl && P.fmax <= 8 && variant == 0 && P.chunk_foff) {
+    chain_factor_stream_k<<<1, 32, 0, s>>>(P, P.chunk_foff, W, stash, D, Dinv, Lx, inertia);
+  } else if (P.nnl && P.fmax <= 8 && variant == 1) {
+    chain_factor_reg_k<<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
+  } else if (P.nnl && P.fmax <= 8) {
     chain_factor_small_k<8><<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
   } else if (P.nnl && P.fmax <= 16) {
     chain_factor_small_k<16><<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
@@ -737,8 +1217,14 @@ void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs
            double* V, double* Vs, cudaStream_t s) {
   (void)V;
   gather_k<<<grid_for(P.dim), kThreads, 0, s>>>(P.perm, rhs, y, P.dim);
-  if (P.nfl) fwd_leaf_k<<<grid_for(P.nfl), kThreads, 0, s>>>(P, Lx, y);
-  if (P.nnl && P.fmax <= 8) {
+  static const int variant = std::getenv("OCG_REFLDL_KERNEL") ? std::atoi(std::getenv("OCG_REFLDL_KERNEL")) : 0;
+  const bool streamed = P.nnl && P.fmax <= 8 && variant == 0 && P.chunk_foff;
+  if (P.nfl && !streamed) fwd_leaf_k<<<grid_for(P.nfl), kThreads, 0, s>>>(P, Lx, y);
+  if (streamed) {
+    fwd_pre_k<<<grid_for(P.nnl), kThreads, 0, s>>>(P, Lx, y);
+    fwd_chain_stream_k<<<1, 32, 0, s>>>(P, Vs);
+    bwd_chain_stream_k<<<1, 32, 0, s>>>(P, xp);
+  } else if (P.nnl && P.fmax <= 8) {
     fwd_chain_small_k<8><<<1, 32, 0, s>>>(P, Lx, y, Vs);
     bwd_chain_small_k<8><<<1, 32, 0, s>>>(P, Lx, Dinv, y, xp);
   } else if (P.nnl && P.fmax <= 16) {

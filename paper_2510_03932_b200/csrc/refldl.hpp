@@ -60,7 +60,7 @@ constexpr int64_t kChain = -1, kRoot = -2;  // ColRec::soff / Dev::nl_soff marke
 // Largest front (1 + column count of L) the warp kernels take.
 constexpr int kMaxFront = 128;
 
-// One chain column's metadata for the warp walks (32 bytes).
+// One chain column's metadata for the warp walks (48 bytes).
 struct alignas(16) ColRec {
   long long foff;  // front in W
   int lp;          // first entry of the column in Li / Lx / rel
@@ -68,6 +68,11 @@ struct alignas(16) ColRec {
   int f;           // front size
   int soff;        // stash offset, or kChain / kRoot
   int sc0, sc1;    // stashed children: sc_child[sc0, sc1)
+  // kChain with both fronts <= 8 rows: byte r of the parent's front is the
+  // row of this front that lands there (0 = none) — the inverse of rel
+  unsigned long long inv8;
+  // fronts <= 8 rows: byte a-1 = rel of row a (where it lands in the parent's front)
+  unsigned long long rel8;
 };
 
 // Host side of the device plan (below), built once per KKT pattern.
@@ -82,11 +87,13 @@ struct HostPlan {
   std::vector<int64_t> pa_ptr;
   std::vector<int32_t> fl_j;
   std::vector<int64_t> fl_ptr, fl_lx, fl_col;
+  std::vector<int64_t> fl_all_ptr;  // [nnl+1]: the same terms indexed by every chain column
   std::vector<int32_t> rel;
   std::vector<int64_t> sc_dst, sc_dpos, sc_ms;
   std::vector<int8_t> primal;
   std::vector<ColRec> rec;
-  int64_t w_len = 0, stash_len = 0, v_len = 0;
+  int64_t w_len = 0, stash_len = 0, v_len = 0, fronts_len = 0;
+  std::vector<long long> chunk_foff;  // per 16 chain columns, then fronts_len
 };
 HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi);
 
@@ -120,6 +127,15 @@ struct Dev {
   const int64_t* fl_ptr = nullptr;   // [nfl+1]
   const int64_t* fl_lx = nullptr;    // L entry index
   const int64_t* fl_col = nullptr;   // leaf position
+  const int64_t* fl_all_ptr = nullptr;  // [nnl+1] leaf terms of every chain column
+  // streamed walks (fronts <= 8): per chain column, its L entries and Dinv
+  // (8 doubles, written by the factorization), the right-hand side after the
+  // leaf terms and the forward result, all in walk order
+  double* sr = nullptr;     // [nnl * 8]
+  double* ypre = nullptr;   // [nnl]
+  double* ych = nullptr;    // [nnl]
+  int64_t fronts_len = 0;   // doubles of W holding the chain fronts
+  const long long* chunk_foff = nullptr;  // [nchunks+1] W offset of every kChunk(16)-column chunk's fronts
   // L pattern
   const int64_t* Lp = nullptr;       // [dim+1] by position
   const int64_t* Li = nullptr;       // [lnz]
