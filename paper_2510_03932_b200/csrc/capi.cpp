@@ -1447,6 +1447,7 @@ int ocg_ldl_factors(const ocg_ldl* l, int64_t* perm, int64_t* Lp, int64_t* Li, d
   if (perm) std::copy(R.S.perm.begin(), R.S.perm.end(), perm);
   if (Lp) std::copy(R.S.Lp.begin(), R.S.Lp.end(), Lp);
   if (Li) std::copy(R.S.Li.begin(), R.S.Li.end(), Li);
+  ocg::rl::fill_lx(R.dev, R.Lx.p, cudaStreamPerThread);
   ck(cudaDeviceSynchronize(), "sync");
   if (D && n) ck(cudaMemcpy(D, R.D.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D d2h");
   if (Lx && lnz) ck(cudaMemcpy(Lx, R.Lx.p, lnz * sizeof(double), cudaMemcpyDeviceToHost), "Lx d2h");

@@ -345,7 +345,8 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
     r.foff = H.nl_foff[static_cast<size_t>(j)];
     r.lp = static_cast<int>(H.nl_lp[static_cast<size_t>(j)]);
     r.pos = static_cast<int>(H.nl_pos[static_cast<size_t>(j)]);
-    r.f = H.nl_f[static_cast<size_t>(j)];
+    r.f = static_cast<short>(H.nl_f[static_cast<size_t>(j)]);
+    r.flags = 0;
     r.soff = static_cast<int>(H.nl_soff[static_cast<size_t>(j)]);
     r.sc0 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j)]);
     r.sc1 = static_cast<int>(H.sc_ptr[static_cast<size_t>(j) + 1]);
@@ -359,6 +360,8 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
         const int dst = H.rel[static_cast<size_t>(r.lp + a - 1)];
         r.inv8 |= static_cast<unsigned long long>(a) << (8 * dst);
       }
+    if (r.soff == kChain && r.inv8 != 0 && H.sc_ptr[static_cast<size_t>(j) + 1] == H.sc_ptr[static_cast<size_t>(j) + 2])
+      r.flags |= 1;
   }
   for (int64_t j = 0; j < nnl; j += 16) H.chunk_foff.push_back(H.nl_foff[static_cast<size_t>(j)]);
   H.chunk_foff.push_back(H.fronts_len);

@@ -741,12 +741,15 @@ struct FStage {
 // chain factorization, fronts <= 8 rows, register-resident (see
 // chain_factor_reg_k) with the chunked bulk-copy stream. chunk_foff[c] = the
 // W offset of chunk c's first front (c = 0..nchunks, the last = fronts_len).
+// Chunks whose every column hands its update matrix to the next column by
+// shuffles (ColRec::flags bit 0) run a branch-free loop; L's chain columns
+// go to the walk-order records (P.sr), Lx is filled from them on demand
+// (fill_lx).
 __global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long long* __restrict__ chunk_foff,
                                                            const double* __restrict__ W, double* __restrict__ stash,
                                                            double* __restrict__ D, double* __restrict__ Dinv,
-                                                           double* __restrict__ Lx,
                                                            unsigned long long* __restrict__ inertia) {
-  constexpr int FM = 8, TFM = FM * (FM + 1) / 2;
+  constexpr int FM = 8;
   __shared__ __align__(16) FStage stg[kStages];
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ unsigned char ta[kTab], tb[kTab];
@@ -758,19 +761,24 @@ __global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long lo
     mbar_fence_init();
   }
   __syncwarp();
-  auto issue = [&](long long c) {  // lane 0
+  auto issue = [&](long long c, long long fa, long long fb) {  // lane 0
     if (c >= nch) return;
     const int st = static_cast<int>(c % kStages);
     const long long j0 = c * kChunk;
     const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
-    const long long fa = chunk_foff[c], fb = chunk_foff[c + 1];
     const unsigned rb = static_cast<unsigned>(cnt * sizeof(ColRec)), fbytes = static_cast<unsigned>((fb - fa) * 8);
     mbar_expect(&bar[st], rb + fbytes);
     bulk_load(stg[st].rec, P.rec + j0, rb, &bar[st]);
     if (fbytes) bulk_load(stg[st].fr, W + fa, fbytes, &bar[st]);
   };
   if (lane == 0)
-    for (long long c = 0; c < kStages - 1; ++c) issue(c);
+    for (long long c = 0; c < kStages - 1 && c < nch; ++c) issue(c, chunk_foff[c], chunk_foff[c + 1]);
+  // bounds of the chunk issued next, loaded one chunk ahead of their use
+  long long pf0 = 0, pf1 = 0;
+  if (kStages - 1 < nch) {
+    pf0 = chunk_foff[kStages - 1];
+    pf1 = chunk_foff[kStages];
+  }
   int la = 0, lb = 0;
 #pragma unroll
   for (int a = 1; a < FM; ++a)
@@ -781,17 +789,68 @@ __global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long lo
   const bool diag = la > 0 && la == lb;
   double X = 0.0, Y = 0.0, Z = 0.0, Pv = 0.0, M0 = 0.0, Ma = 0.0;
   bool need_load = true;
-  unsigned long long cnts[3] = {0, 0, 0};
+  unsigned long long np = 0, nn = 0, nz = 0;
   for (long long c = 0; c < nch; ++c) {
-    if (lane == 0) issue(c + kStages - 1);
+    if (lane == 0 && c + kStages - 1 < nch) issue(c + kStages - 1, pf0, pf1);
+    if (c + kStages < nch) {
+      pf0 = __ldg(chunk_foff + c + kStages);
+      pf1 = __ldg(chunk_foff + c + kStages + 1);
+    }
     const int st = static_cast<int>(c % kStages);
     mbar_wait(&bar[st], static_cast<unsigned>((c / kStages) & 1));
     const bool more = c + 1 < nch;
     const int st1 = static_cast<int>((c + 1) % kStages);
     if (more) mbar_wait(&bar[st1], static_cast<unsigned>(((c + 1) / kStages) & 1));
-    const long long fa = __ldg(chunk_foff + c), fa1 = more ? __ldg(chunk_foff + c + 1) : 0;
     const long long j0 = c * kChunk;
     const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    const long long fa = stg[st].rec[0].foff, fa1 = more ? stg[st1].rec[0].foff : 0;
+    const bool fast = !need_load && more && __all_sync(0xffffffffu, lane >= cnt || (stg[st].rec[lane & (kChunk - 1)].flags & 1));
+    if (fast) {
+      // every column: pivot, L, update matrix, shuffled into the next front's owners
+#pragma unroll 2
+      for (int jj = 0; jj < cnt; ++jj) {
+        const long long j = j0 + jj;
+        const ColRec m = stg[st].rec[jj];
+        const bool zero = zero_pivot(Pv, M0);
+        const double dinv = zero ? 0.0 : __drcp_rn(Pv);
+        const double Lv = __dmul_rn(Y, dinv);
+        const double U = __dsub_rn(X, __dmul_rn(__dmul_rn(Z, dinv), Y));
+        const double MU = diag ? fmax(Ma, fabs(__dmul_rn(Lv, Y))) : 0.0;
+        if (lane == 0) {
+          D[m.pos] = Pv;
+          Dinv[m.pos] = dinv;
+          P.sr[j * 8 + 7] = dinv;
+          np += !zero && Pv > 0;
+          nn += !zero && !(Pv > 0);
+          nz += zero;
+        }
+        if (la > 0 && la < m.f && lb == 1) P.sr[j * 8 + la - 1] = Lv;
+        const bool same = jj + 1 < cnt;
+        const ColRec& mn = same ? stg[st].rec[jj + 1] : stg[st1].rec[0];
+        const double* Fn = same ? stg[st].fr + (mn.foff - fa) : stg[st1].fr + (mn.foff - fa1);
+        const int fnn = mn.f;
+        const int ia = static_cast<int>((m.inv8 >> (8 * la)) & 0xff);
+        const int ib = static_cast<int>((m.inv8 >> (8 * lb)) & 0xff);
+        const double vx = __shfl_sync(0xffffffffu, U, ia && ib ? tri32(ia - 1) + ib - 1 : 0);
+        const double vy = __shfl_sync(0xffffffffu, U, ia ? tri32(ia - 1) : 0);
+        const double vz = __shfl_sync(0xffffffffu, U, ib ? tri32(ib - 1) : 0);
+        const double vp = __shfl_sync(0xffffffffu, U, 0);
+        const double m0 = __shfl_sync(0xffffffffu, MU, 0);
+        const double ma = __shfl_sync(0xffffffffu, MU, ia ? tri32(ia - 1) + ia - 1 : 0);
+        const bool in = la < fnn;
+        const double* msn = Fn + tri32(fnn);
+        const double px = in ? Fn[tri32(la) + lb] : 0.0, py = in ? Fn[tri32(la)] : 0.0;
+        const double pz = in ? Fn[tri32(lb)] : 0.0, pm = in ? msn[la] : 0.0;
+        X = ia && ib ? __dadd_rn(px, vx) : px;
+        Y = ia ? __dadd_rn(py, vy) : py;
+        Z = ib ? __dadd_rn(pz, vz) : pz;
+        Pv = __dadd_rn(Fn[0], vp);
+        M0 = fmax(msn[0], m0);
+        Ma = ia ? fmax(pm, ma) : pm;
+      }
+      __syncwarp();
+      continue;
+    }
     for (int jj = 0; jj < cnt; ++jj) {
       const long long j = j0 + jj;
       const ColRec m = stg[st].rec[jj];
@@ -829,19 +888,18 @@ __global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long lo
         D[m.pos] = Pv;
         Dinv[m.pos] = dinv;
         P.sr[j * 8 + 7] = dinv;
-        count_pivot(Pv, zero, cnts);
+        np += !zero && Pv > 0;
+        nn += !zero && !(Pv > 0);
+        nz += zero;
       }
-      if (act && lb == 1) {
-        Lx[m.lp + la - 1] = Lv;
-        P.sr[j * 8 + la - 1] = Lv;
-      }
+      if (act && lb == 1) P.sr[j * 8 + la - 1] = Lv;
       need_load = true;
       if (m.soff != kRoot && j + 1 < n) {
         const bool same = jj + 1 < cnt;
         const ColRec& mn = same ? stg[st].rec[jj + 1] : stg[st1].rec[0];
         double* Fn = same ? stg[st].fr + (mn.foff - fa) : stg[st1].fr + (mn.foff - fa1);
         const int fnn = mn.f;
-        if (m.soff == kChain && mn.sc0 == mn.sc1 && m.inv8 != 0) {
+        if (m.flags & 1) {
           const int ia = static_cast<int>((m.inv8 >> (8 * la)) & 0xff);
           const int ib = static_cast<int>((m.inv8 >> (8 * lb)) & 0xff);
           const double vx = __shfl_sync(0xffffffffu, U, ia && ib ? tri32(ia - 1) + ib - 1 : 0);
@@ -881,10 +939,22 @@ __global__ void __launch_bounds__(32) chain_factor_stream_k(Dev P, const long lo
       __syncwarp();
     }
   }
-  (void)TFM;
-  if (lane == 0)
-    for (int q = 0; q < 3; ++q)
-      if (cnts[q]) atomicAdd(inertia + q, cnts[q]);
+  if (lane == 0) {
+    if (np) atomicAdd(inertia + 0, np);
+    if (nn) atomicAdd(inertia + 1, nn);
+    if (nz) atomicAdd(inertia + 2, nz);
+  }
+}
+
+// Lx of the chain columns from the walk-order records (the streamed
+// factorization writes only those): one thread per chain column
+__global__ void fill_lx_k(Dev P, double* __restrict__ Lx) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P.nnl;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = P.nl_f[j];
+    const int64_t lp = P.nl_lp[j];
+    for (int a = 1; a < f; ++a) Lx[lp + a - 1] = P.sr[j * 8 + a - 1];
+  }
 }
 
 // chain rows of the right-hand side minus their leaf terms, in walk order
@@ -947,6 +1017,21 @@ __global__ void __launch_bounds__(32) fwd_chain_stream_k(Dev P, double* __restri
     if (more) mbar_wait(&bar[st1], static_cast<unsigned>(((c + 1) / kStages) & 1));
     const long long j0 = c * kChunk;
     const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    if (!need_load && more && __all_sync(0xffffffffu, lane >= cnt || (stg[st].rec[lane & (kChunk - 1)].flags & 1))) {
+      // every column hands its update vector to the next one by a shuffle
+#pragma unroll 2
+      for (int jj = 0; jj < cnt; ++jj) {
+        const ColRec m = stg[st].rec[jj];
+        const double yk = __shfl_sync(0xffffffffu, v, 0);
+        if (lane == 0) P.ych[j0 + jj] = yk;
+        const double u = lane >= 1 && lane < m.f ? __dsub_rn(v, __dmul_rn(stg[st].sr[jj * 8 + lane - 1], yk)) : 0.0;
+        const double pre = jj + 1 < cnt ? stg[st].y[jj + 1] : stg[st1].y[0];
+        const int src = lane < 8 ? static_cast<int>((m.inv8 >> (8 * lane)) & 0xff) : 0;
+        const double w = __shfl_sync(0xffffffffu, u, src);
+        v = lane == 0 ? __dadd_rn(pre, w) : (src ? w : 0.0);
+      }
+      continue;
+    }
     for (int jj = 0; jj < cnt; ++jj) {
       const long long j = j0 + jj;
       const ColRec m = stg[st].rec[jj];
@@ -1005,6 +1090,23 @@ __global__ void __launch_bounds__(32) bwd_chain_stream_k(Dev P, double* __restri
     mbar_wait(&bar[st], static_cast<unsigned>((k / kStages) & 1));
     const long long j0 = c * kChunk;
     const int cnt = static_cast<int>(min(static_cast<long long>(kChunk), n - j0));
+    if (__all_sync(0xffffffffu, lane >= cnt || stg[st].rec[lane & (kChunk - 1)].soff == kChain)) {
+      // every column's parent is the column walked just before: X by shuffles
+#pragma unroll 2
+      for (int jj = cnt - 1; jj >= 0; --jj) {
+        const ColRec m = stg[st].rec[jj];
+        const bool row = lane >= 1 && lane < m.f;
+        const int ra = row ? static_cast<int>((m.rel8 >> (8 * (lane - 1))) & 0xff) : 0;
+        const double xa = __shfl_sync(0xffffffffu, Xp, ra);
+        double t = row ? __dmul_rn(stg[st].sr[jj * 8 + lane - 1], xa) : 0.0;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+        const double s = __dsub_rn(__dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]), t);
+        Xp = lane == 0 ? s : xa;
+        if (lane == 0) xp[m.pos] = s;
+      }
+      continue;
+    }
     for (int jj = cnt - 1; jj >= 0; --jj) {
       const ColRec m = stg[st].rec[jj];
       const int f = m.f;
@@ -1196,7 +1298,7 @@ void factor(const Dev& P, const double* kval, double delta_w, double delta_c, do
   if (P.npa) preassemble_k<<<grid_for(P.npa), kThreads, 0, s>>>(P, W, Lx);
   static const int variant = std::getenv("OCG_REFLDL_KERNEL") ? std::atoi(std::getenv("OCG_REFLDL_KERNEL")) : 0;
   if (P.nnl && P.fmax <= 8 && variant == 0 && P.chunk_foff) {
-    chain_factor_stream_k<<<1, 32, 0, s>>>(P, P.chunk_foff, W, stash, D, Dinv, Lx, inertia);
+    chain_factor_stream_k<<<1, 32, 0, s>>>(P, P.chunk_foff, W, stash, D, Dinv, inertia);
   } else if (P.nnl && P.fmax <= 8 && variant == 1) {
     chain_factor_reg_k<<<1, 32, 0, s>>>(P, W, stash, D, Dinv, Lx, inertia);
   } else if (P.nnl && P.fmax <= 8) {
@@ -1211,6 +1313,15 @@ void factor(const Dev& P, const double* kval, double delta_w, double delta_c, do
                                                                                    Lx, inertia);
   }
   ck(cudaGetLastError(), "factor launch");
+}
+
+bool streamed_factor(const Dev& P) {
+  static const int variant = std::getenv("OCG_REFLDL_KERNEL") ? std::atoi(std::getenv("OCG_REFLDL_KERNEL")) : 0;
+  return P.nnl && P.fmax <= 8 && variant == 0 && P.chunk_foff;
+}
+
+void fill_lx(const Dev& P, double* Lx, cudaStream_t s) {
+  if (streamed_factor(P)) fill_lx_k<<<grid_for(P.nnl), kThreads, 0, s>>>(P, Lx);
 }
 
 void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs, double* x, double* y, double* xp,

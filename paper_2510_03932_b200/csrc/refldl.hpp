@@ -65,7 +65,8 @@ struct alignas(16) ColRec {
   long long foff;  // front in W
   int lp;          // first entry of the column in Li / Lx / rel
   int pos;         // position
-  int f;           // front size
+  short f;         // front size
+  short flags;     // bit 0: the next column is the parent, has no stashed children and both fronts <= 8 rows
   int soff;        // stash offset, or kChain / kRoot
   int sc0, sc1;    // stashed children: sc_child[sc0, sc1)
   // kChain with both fronts <= 8 rows: byte r of the parent's front is the
@@ -154,6 +155,9 @@ struct Dev {
 // (positive, negative, zero)
 void factor(const Dev& P, const double* kval, double delta_w, double delta_c, double* W, double* stash, double* D,
             double* Dinv, double* Lx, unsigned long long* inertia, cudaStream_t s);
+// the streamed factorization (fronts <= 8) leaves the chain columns of L in
+// P.sr only; this writes them into Lx (the LdlFactor layout) on demand
+void fill_lx(const Dev& P, double* Lx, cudaStream_t s);
 // x = (K + deltas)^{-1} rhs in KKT index order; y, xp (dim), V (v_len), Vs
 // (stash_len) scratch
 void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs, double* x, double* y, double* xp,
