@@ -19,6 +19,9 @@ ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 HOST_SRCS = ["graph.cpp", "dsl.cpp", "transcribe.cpp", "codegen.cpp", "jit.cpp", "capi.cpp", "ipm.cpp", "batch.cpp", "refldl.cpp", "shard.cpp"]
 CUDA_SRCS = ["kernels.cu", "band.cu", "sepcr.cu", "ipm_kernels.cu", "kktbuild.cu", "batch_kernels.cu", "refldl.cu"]
+# the interior-point vector kernels round every product and sum separately,
+# as the reference's loops do on x86-64 (no FMA contraction there)
+NO_FMA = {"ipm_kernels.cu", "batch_kernels.cu"}
 HEADERS = ["model.hpp", "plan.hpp", "jit.hpp", "kernels.hpp", "band.hpp", "ipm_kernels.hpp", "kktbuild.hpp", "batch_kernels.hpp", "handles.hpp", "devmem.hpp", "refldl.hpp", "shard.hpp"]
 
 
@@ -55,6 +58,8 @@ def build(verbose: bool = False) -> Path:
         if _stale(obj, [src] + hdrs):
             cmd = [str(CUDA / "bin" / "nvcc"), ARCH, "-O3", "-lineinfo", "-std=c++17",
                    "-Xptxas", "-v", "-Xcompiler", "-fPIC", "-c", str(src), "-o", str(obj)]
+            if s in NO_FMA:
+                cmd.insert(3, "-fmad=false")
             if verbose:
                 print(" ".join(cmd))
             _run(cmd)
