@@ -143,6 +143,12 @@ typedef struct {
   int split_kinds;  /* shared-memory staging of the outputs: 0 = one region reused group
                        after group, 1 = one region per output kind in turn, 2 = a region
                        per group (one wait per tile); -1 = auto */
+  int input_staging; /* how a tile's inputs (node slabs, row_scale and lambda rows) reach
+                       shared memory: 0 = per-lane LDGSTS, waited for before the tile computes;
+                       1 = per-lane LDGSTS double-buffered (the next tile's copies in flight
+                       while this one computes); 2 = TMA bulk copies on mbarriers,
+                       double-buffered, one-warp blocks (forces block = 32); -1 = auto (1
+                       when the second buffer costs no resident blocks, else 0) */
 } ocg_eval_options;
 
 void ocg_eval_default_options(ocg_eval_options* o);
@@ -209,6 +215,8 @@ int64_t ocg_eval_launch_count(const ocg_eval* e);
  * sm_100a without loading (works without a GPU).
  */
 char* ocg_debug_generated_source(const ocg_model* m, int fma, int block);
+/* the same for an input_staging mode (0, 1, 2 as in ocg_eval_options) */
+char* ocg_debug_generated_source_ex(const ocg_model* m, int fma, int block, int input_staging);
 int ocg_debug_compile(const ocg_model* m, int fma, int block);
 /* NVRTC/ptxas log (registers, spills per kernel) of the module an eval
  * context with these options would load; NULL on failure (ocg_free it). */

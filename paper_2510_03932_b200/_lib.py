@@ -26,7 +26,7 @@ EXPORTS = [
     "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_max_abs_hessian", "ocg_eval_status", "ocg_eval_status_async",
     "ocg_eval_objective_chunks", "ocg_eval_objective_partials", "ocg_eval_objective_combine",
     "ocg_eval_launch_count",
-    "ocg_debug_generated_source", "ocg_debug_compile", "ocg_debug_compile_log",
+    "ocg_debug_generated_source", "ocg_debug_generated_source_ex", "ocg_debug_compile", "ocg_debug_compile_log",
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
@@ -42,7 +42,7 @@ EXPORTS = [
 class EvalOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("fma", C.c_int), ("block", C.c_int), ("idx_lo", C.c_int64),
                 ("idx_hi", C.c_int64), ("specials", C.c_int), ("min_blocks", C.c_int),
-                ("split_kinds", C.c_int)]
+                ("split_kinds", C.c_int), ("input_staging", C.c_int)]
 
 
 class IpmOptions(C.Structure):
@@ -123,6 +123,7 @@ def _load() -> C.CDLL:
         "ocg_eval_objective_combine": (i32, [vp, dp, dp, vp]),
         "ocg_eval_launch_count": (i64, [vp]),
         "ocg_debug_generated_source": (vp, [vp, i32, i32]),
+        "ocg_debug_generated_source_ex": (vp, [vp, i32, i32, i32]),
         "ocg_debug_compile": (i32, [vp, i32, i32]),
         "ocg_debug_compile_log": (vp, [vp, C.POINTER(EvalOptions)]),
         "ocg_kkt_create": (i32, [vp, vp, C.POINTER(vp)]),

@@ -436,7 +436,7 @@ void Batch::gen(cudaKernel_t k, const char* name, std::vector<void*> ptr_args, c
   gb.s[9] = 1;
   Index ns = ev_->n_spec(name);
   std::vector<void*> args;
-  args.push_back(ev_->prm.data());
+  args.push_back(ev_->prm_arg());
   for (void* p : ptr_args) args.push_back(p);
   args.push_back(&ev_->i0);
   args.push_back(&ev_->n_main);

@@ -263,7 +263,7 @@ std::map<std::string, std::pair<int, int>> ptxas_stats(const std::string& log) {
 // compiled for `target` resident blocks per SM (capped by what its shared
 // memory allows), stepping the budget down for kernels whose code would spill.
 ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, ocg::GenOptions go, int target,
-                                 int split, int smem_per_sm, int smem_per_block_max, std::string* log_out,
+                                 int split, int staging, int smem_per_sm, int smem_per_block_max, std::string* log_out,
                                  std::map<std::string, std::string>* cubins_out = nullptr) {
   auto max_smem = [](const ocg::Generated& g) {
     int mx = 0;
@@ -285,6 +285,12 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
     go.split_kinds = split == 1;
     go.distinct_regions = split == 2;
   }
+  if (const char* e = std::getenv("OCG_STAGING")) staging = std::atoi(e);
+  go.idx32 = ocg::fits_idx32(nlp, lay);
+  if (const char* e = std::getenv("OCG_IDX64")) go.idx32 = go.idx32 && std::atoi(e) == 0;
+  go.tma = staging == 2;
+  if (go.tma) go.block = 32;
+  go.prefetch = staging == 1;
   ocg::Generated gen = ocg::generate(nlp, lay, go);
   // shared memory per block scales with warps per block: halve the block
   // until every kernel fits the per-block limit
@@ -292,13 +298,30 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
     go.block /= 2;
     gen = ocg::generate(nlp, lay, go);
   }
+  // auto staging: double-buffer the inputs when the second buffer costs no
+  // resident blocks of the fused kernel (its budget is rarely above 3-4
+  // blocks per SM), else stage once per tile
+  if (staging < 0 && go.distinct_regions && !go.split_kinds) {
+    auto blocks = [&](const ocg::Generated& g) {
+      return std::min(std::max(1, smem_per_sm / (g.smem.at("ocg_cjh") + 1024)), 4 * std::max(1, 128 / go.block));
+    };
+    go.prefetch = true;
+    ocg::Generated g2 = ocg::generate(nlp, lay, go);
+    if (max_smem(g2) <= smem_per_block_max && blocks(g2) >= blocks(gen))
+      gen = std::move(g2);
+    else
+      go.prefetch = false;
+  }
   if (max_smem(gen) > smem_per_block_max)
     throw std::runtime_error("model needs more shared memory per warp than one block provides");
+  // the target counts 128-thread blocks; one-warp blocks (TMA tiles) scale it
+  // to the same warps per SM, within the 32 resident blocks an SM holds
+  const int per128 = std::max(1, 128 / go.block);
   for (const char* k : kKernelNames) {
     const int sm = gen.smem.at(k) + 1024;  // + per-block reservation
     const int by_smem = std::max(1, smem_per_sm / std::max(sm, 1));
-    const int by_threads = std::max(1, 2048 / go.block);
-    go.min_blocks[k] = std::max(1, std::min({target, by_smem, by_threads}));
+    const int by_threads = std::min(32, std::max(1, 2048 / go.block));
+    go.min_blocks[k] = std::max(1, std::min({target * per128, by_smem, by_threads}));
   }
   // every kernel is its own compilation unit, compiled concurrently; each
   // steps its register budget down while ptxas reports spills
@@ -322,7 +345,7 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
           // a few spilled registers (served from L1) cost less than a lost
           // block of occupancy: step the budget down only past spill_ok bytes
           if (f == st.end() || f->second.second <= spill_ok || mbs[i] <= 1) break;
-          mbs[i] -= 1;
+          mbs[i] = std::max(1, mbs[i] - (mbs[i] > per128 ? per128 : 1));
         }
       } catch (const std::exception& ex) {
         errs[i] = ex.what();
@@ -340,6 +363,9 @@ ocg::Generated generate_budgeted(const ocg::Nlp& nlp, const ocg::Layout& lay, oc
   gen.block = go.block;
   gen.split_kinds = go.split_kinds;
   gen.distinct_regions = go.distinct_regions;
+  gen.prefetch = go.prefetch;
+  gen.tma = go.tma;
+  gen.idx32 = go.idx32;
   return gen;
 }
 
@@ -552,6 +578,7 @@ void ocg_eval_default_options(ocg_eval_options* o) {
   o->specials = 1;
   o->min_blocks = 0;
   o->split_kinds = -1;
+  o->input_staging = -1;
 }
 
 int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval** out) {
@@ -604,7 +631,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     lap("device props");
     std::map<std::string, std::string> cubins;
     ocg::Generated gen =
-        generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), o.split_kinds,
+        generate_budgeted(nlp, e->lay, go, auto_min_blocks(o), o.split_kinds, o.input_staging,
                           static_cast<int>(prop.sharedMemPerMultiprocessor),
                           static_cast<int>(prop.sharedMemPerBlockOptin), nullptr, &cubins);
     go.block = gen.block;
@@ -614,6 +641,7 @@ int ocg_eval_create(const ocg_model* m, const ocg_eval_options* opts, ocg_eval**
     e->tail = gen.tail;
     e->smem = gen.smem;
     e->prm = gen.params;
+    e->set_idx32(gen.idx32);
     lap("generate+compile");
     for (const char* k : kKernelNames) e->mods[k] = loaded_module(cubins.at(k));
     lap("load modules");
@@ -799,7 +827,7 @@ int ocg_eval_constraints(ocg_eval* e, const double* x, double* c, ocg_stream s) 
   const double* rs = e->row_scale.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_c");
-  void* args[] = {e->prm.data(), &x, &rs, &c, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &rs, &c, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_c, "ocg_c", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -813,7 +841,7 @@ int ocg_eval_constraints_jacobian(ocg_eval* e, const double* x, double* c, ocg_s
   double* jac = e->jac.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_cjac");
-  void* args[] = {e->prm.data(), &x, &rs, &c, &jac, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &rs, &c, &jac, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_cjac, "ocg_cjac", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -828,7 +856,7 @@ int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_str
   double* hess = e->hess.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_hess");
-  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &lambda, &rs, &ow, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_hess, "ocg_hess", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -844,7 +872,7 @@ int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double
   double* hess = e->hess.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_cjh");
-  void* args[] = {e->prm.data(), &x, &lambda, &rs, &ow, &c, &jac, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &lambda, &rs, &ow, &c, &jac, &hess, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_cjh, "ocg_cjh", args, st(s));
   return OCG_OK;
   OCG_GUARD_END
@@ -857,7 +885,7 @@ int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
-  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_objv, "ocg_objv", args, st(s));
   ocg::dev::objective_reduce(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks, e->og_weight.p,
                              static_cast<int>(e->obj_weight.size()), e->obj_scale, e->partials.p, f, e->flag.p, st(s));
@@ -875,7 +903,7 @@ int ocg_eval_objective_partials(ocg_eval* e, const double* x, double* partials, 
   double* ov = e->objv.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_objv");
-  void* args[] = {e->prm.data(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &ov, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_objv, "ocg_objv", args, st(s));
   ocg::dev::objective_chunk_sums(e->objv.p, e->og_off.p, e->og_count.p, e->og_cbase.p, e->n_chunks,
                                  static_cast<int>(e->obj_weight.size()), partials, st(s));
@@ -903,7 +931,7 @@ int ocg_eval_gradient(ocg_eval* e, const double* x, double* grad_dense, ocg_stre
   double* g = e->grad.p;
   int* fl = e->flag.p;
   Index ns = e->n_spec("ocg_grad");
-  void* args[] = {e->prm.data(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
+  void* args[] = {e->prm_arg(), &x, &ow, &g, &fl, &e->i0, &e->n_main, &ns, &kNoBatch};
   e->launch(e->k_grad, "ocg_grad", args, st(s));
   ocg::dev::gather_sum(e->grad.p, e->gg_ptr.p, e->gg_idx.p, e->model->nlp.nvar, grad_dense,
                        {e->gg_long.p, e->n_gg_long}, st(s));
@@ -1560,10 +1588,18 @@ int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
 }  // extern "C"
 
 extern "C" char* ocg_debug_generated_source(const ocg_model* m, int fma, int block) {
+  return ocg_debug_generated_source_ex(m, fma, block, 0);
+}
+
+extern "C" char* ocg_debug_generated_source_ex(const ocg_model* m, int fma, int block, int input_staging) {
   if (!m) return nullptr;
   ocg::GenOptions go;
   go.fma = fma != 0;
   go.block = block > 0 ? block : 128;
+  go.prefetch = input_staging == 1;
+  go.tma = input_staging == 2;
+  go.idx32 = ocg::fits_idx32(m->nlp, ocg::make_layout(m->nlp));
+  if (go.tma && go.block != 32) return nullptr;
   if (const char* e = std::getenv("OCG_SPLIT")) {
     go.split_kinds = std::atoi(e) == 1;
     go.distinct_regions = std::atoi(e) == 2;
@@ -1599,12 +1635,14 @@ extern "C" char* ocg_debug_compile_log(const ocg_model* m, const ocg_eval_option
     std::string log;
     // B200: 228 KB shared memory per SM, 227 KB per block (opt-in)
     const ocg::Generated gen =
-        generate_budgeted(m->nlp, ocg::make_layout(m->nlp), go, auto_min_blocks(o), o.split_kinds, 233472, 232448,
+        generate_budgeted(m->nlp, ocg::make_layout(m->nlp), go, auto_min_blocks(o), o.split_kinds, o.input_staging,
+                          233472, 232448,
                           &log);
     std::string s = log + "\n// min_blocks:";
     for (const auto& [k, v] : gen.min_blocks) s += " " + k + "=" + std::to_string(v);
     s += " block=" + std::to_string(gen.block) + " staging=" +
-         std::to_string(gen.split_kinds ? 1 : (gen.distinct_regions ? 2 : 0)) + "\n";
+         std::to_string(gen.split_kinds ? 1 : (gen.distinct_regions ? 2 : 0)) +
+         " input_staging=" + std::to_string(gen.tma ? 2 : (gen.prefetch ? 1 : 0)) + "\n";
     char* out = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(out, s.c_str(), s.size() + 1);
     return out;

@@ -291,7 +291,9 @@ class Generator {
     os << "#define OCG_BLOCK " << opt_.block << "\n";
     os << "// grid-size-dependent integers (offsets, ranges, slab bases) arrive by value:\n";
     for (size_t i = 0; i < pkeys_.size(); ++i) os << "//   prm.v[" << i << "] = " << pkeys_[i] << "\n";
-    os << "struct OcgParams { long long v[" << std::max<size_t>(1, pkeys_.size()) << "]; };\n";
+    // index arithmetic in 32 bits when every array index of the model fits
+    os << "typedef " << (opt_.idx32 ? "int" : "long long") << " OIX;\n";
+    os << "struct OcgParams { OIX v[" << std::max<size_t>(1, pkeys_.size()) << "]; };\n";
     // batched launches over independent instances of one structure: block z
     // evaluates instance ids[z]; every array argument advances by its
     // per-instance stride (roles: x, lam, rs, objw, c, jac, hess, objv, grad,
@@ -309,6 +311,8 @@ class Generator {
     os << "__device__ __forceinline__ void ocg_cp8(double* s, const double* g) {\n"
           "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" :: \"r\"((unsigned)__cvta_generic_to_shared(s)), \"l\"(g) : \"memory\");\n}\n";
     os << "__device__ __forceinline__ void ocg_cp_wait() { asm volatile(\"cp.async.wait_all;\\n\" ::: \"memory\"); }\n";
+    os << "__device__ __forceinline__ void ocg_cp_commit() { asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
+    os << "__device__ __forceinline__ void ocg_cp_wait1() { asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\"); }\n";
     // TMA bulk copy-out (cp.async.bulk shared::cta -> global, SASS UBLKCP):
     // an 8-byte head/tail goes by plain stores so the bulk part is 16-byte
     // aligned and a multiple of 16 bytes
@@ -327,6 +331,36 @@ __device__ __forceinline__ void ocg_bulk_store(double* g, const double* s, int n
 __device__ __forceinline__ void ocg_bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void ocg_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// TMA bulk copy-in (cp.async.bulk global -> shared, SASS UBLKCP) completing
+// on an mbarrier: one lane posts the byte count of every copy (expect_tx),
+// issues the copies and arrives; the warp waits on the phase parity
+__device__ __forceinline__ unsigned ocg_su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ocg_mbar_init(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(ocg_su32(b)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void ocg_mbar_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" :: "r"(ocg_su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ocg_mbar_arrive(unsigned long long* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" :: "r"(ocg_su32(b)) : "memory");
+}
+__device__ __forceinline__ void ocg_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n OCG_W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra OCG_W_%=;\n}\n"
+               :: "r"(ocg_su32(b)), "r"(parity) : "memory");
+}
+// n > 0 doubles from g to shared memory at p, where p and g agree modulo 16
+// bytes: the 16-byte chunks holding g[0..n) move whole (every chunk holds a
+// valid element, so no page beyond the array is touched)
+__device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long long n, unsigned long long* b) {
+  const unsigned long long ga = ((unsigned long long)g) & ~15ull;
+  const unsigned long long ge = (((unsigned long long)(g + n)) + 15ull) & ~15ull;
+  const unsigned nb = (unsigned)(ge - ga);
+  ocg_mbar_tx(b, nb);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               :: "r"(ocg_su32(p - ((((unsigned long long)g) & 15ull) >> 3))), "l"(ga), "r"(nb), "r"(ocg_su32(b))
+               : "memory");
+}
 )";
     os << "#endif\n\n";
     out.prelude = os.str();
@@ -352,6 +386,9 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
   // entry); empty string = global memory
   std::function<std::string(const Addr&)> load_from_;
   std::function<std::string(int, Index)> store_to_;
+  // predicate of a direct global store inside a tile (lanes outside the
+  // group's range must not write); empty = unpredicated
+  std::string store_pred_;
   // staged row inputs of the current group: what 0 = row_scale, 1 = lambda;
   // empty string = global memory
   std::function<std::string(int, int)> row_from_;
@@ -739,7 +776,9 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     if (!v.is_c) E.line(acc_ + " = __fma_rn(" + E.s(v) + ", 0.0, " + acc_ + ");");
   }
 
-  static std::string i64(Index v) { return std::to_string(v) + "LL"; }
+  // integer literal of the kernel's index type (OIX: int when every array
+  // index fits 32 bits, else long long)
+  std::string i64(Index v) const { return std::to_string(v) + (opt_.idx32 ? "" : "LL"); }
 
   // AD + stores for one group instance; k is the range ordinal expression.
   void group_body(Emitter& E, Mode m, bool objective, int gi, const Fwd& f, const std::string& k) {
@@ -762,6 +801,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     auto lv = [&](int kind, Index e, const std::string& global) {
       const std::string s = store_to_ ? store_to_(kind, e) : std::string();
       if (!s.empty() && store_hook_) store_hook_(kind);
+      if (s.empty() && !store_pred_.empty()) return "if (" + store_pred_ + ") " + global;
       return s.empty() ? global : s;
     };
     if (p.values) {
@@ -853,6 +893,20 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     scan(false, nlp_.cons);
     scan(true, nlp_.objs);
     constexpr Index W = 32;  // grid indices per warp tile
+    // One-warp blocks (block == 32): every tile-level quantity derives from
+    // blockIdx and the parameters, so it is warp-uniform by construction; the
+    // tile's inputs then come in by TMA bulk copies on an mbarrier, double-
+    // buffered (tile t+1's copies are in flight while tile t computes), and
+    // one lane issues the tile's bulk copies out from uniform registers.
+    if (opt_.tma && opt_.block != 32) throw std::runtime_error("TMA tiles need one-warp blocks (block = 32)");
+    const bool tma = opt_.tma;
+    const bool distinct = tma || opt_.distinct_regions;
+    const bool split = !tma && opt_.split_kinds;
+    const bool pf = !tma && opt_.prefetch && distinct && !split;
+    // one-warp blocks: tile-level values are uniform, lane 0 issues the
+    // tile's bulk copies out straight-line from uniform registers
+    const bool uni = opt_.block == 32;
+    const Index slack = tma ? 4 : 0;  // per staged input region: alignment lead, shift, tail
 
     // node slabs read by any member group: nodes [ib, ib + W + max_off)
     struct Use {
@@ -871,7 +925,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     Index cur = 0;
     for (auto& [s, u] : uses) {
       u.soff = cur;
-      cur += (W + u.max_off) * nlp_.slabs[s].dim;
+      cur += (W + u.max_off) * nlp_.slabs[s].dim + slack;
     }
     // row inputs of the member groups (row_scale, lambda): the warp's 32
     // instances read one contiguous segment of rows per group, staged with the
@@ -888,13 +942,18 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       const Index od = g.out_dim();
       if (p.values || p.jac || p.hess) {
         rows[q].rs = cur;
-        cur += W * od;
+        cur += W * od + slack;
       }
       if (p.hess) {
         rows[q].lam = cur;
-        cur += W * od;
+        cur += W * od + slack;
       }
     }
+    // TMA tiles: two input buffers of IN doubles after the two mbarriers, the
+    // output regions after them
+    const Index IN = cur + (cur & 1);
+    if (tma) cur = 0;
+    if (pf) cur = 2 * IN;  // prefetch: two input buffers, then the outputs
     // output rows: one region reused by every group (warp-synchronous)
     struct Out {
       int kind;
@@ -909,14 +968,17 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
       const Parts p = parts(m, mb.objective, g);
       const size_t gi = static_cast<size_t>(mb.gi);
-      Index off = opt_.distinct_regions ? running : cur;
+      Index off = distinct ? running : cur;
       auto add_out = [&](int kind, Index per_k, const std::string& dst) {
-        if (per_k <= 0) return;
+        // one value per instance: the lanes' stores to global memory are
+        // already coalesced (8 bytes per lane, consecutive), so they go there
+        // directly instead of through a staged region and a bulk copy
+        if (per_k <= 1) return;
         const Index pitch = per_k;  // unpadded: the copy-out is one linear bulk copy
         outs[q].push_back({kind, per_k, pitch, off, dst});
         // + slack for the 16-byte alignment shift; split mode: every output
         // kind reuses one region, flushed before the next kind is staged
-        if (opt_.split_kinds)
+        if (split)
           region = std::max(region, W * pitch + 2);
         else
           off += W * pitch + 2;
@@ -936,6 +998,8 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     }
     Index per_warp = cur + region;  // doubles of shared memory per warp
     per_warp += per_warp & 1;       // keep every warp's base 16-byte aligned (bulk copies)
+    const Index out_base = tma ? 2 + 2 * IN : 0;
+    if (tma) per_warp += out_base;
 
     Emitter E;
     E.depth = 0;
@@ -943,7 +1007,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     // compilation (each kernel is compiled as its own module)
     E.line("extern \"C\" __global__ void __launch_bounds__(OCG_BLOCK, OCG_MINB_" + std::string(name) + ") " +
            std::string(name) +
-           "(const OcgParams prm, " + params + ", long long i0, long long n_main, long long n_spec, const OcgBatch bt) {");
+           "(const OcgParams prm, " + params + ", long long i0_, long long n_main_, long long n_spec, const OcgBatch bt) {");
     E.depth = 1;
     {
       static const char* const roles[] = {"x", "lam", "rs", "objw", "cout", "jac", "hess", "objv", "gout", "flag"};
@@ -955,27 +1019,38 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         if (names.count(roles[r])) adv += std::string(" ") + roles[r] + " += bz * bt.s[" + std::to_string(r) + "];";
       E.line("if (bt.ids) { const long long bz = bt.ids[blockIdx.z];" + adv + " }");
     }
+    E.line("const OIX i0 = (OIX)i0_, n_main = (OIX)n_main_;");
     E.line("extern __shared__ __align__(16) double smem_all[];");
     E.line("const int lane = threadIdx.x & 31;");
-    E.line("double* __restrict__ smem = smem_all + (threadIdx.x >> 5) * " + i64(per_warp) + ";");
+    if (tma) {
+      E.line("unsigned long long* const ocg_bar = reinterpret_cast<unsigned long long*>(smem_all);");
+      E.line("double* const sin0 = smem_all + 2;");
+      E.line("double* __restrict__ smem = smem_all + " + i64(out_base) + ";");
+      E.line("if (lane == 0) { ocg_mbar_init(ocg_bar); ocg_mbar_init(ocg_bar + 1); }");
+      E.line("__syncwarp();");
+    } else {
+      E.line(uni ? std::string("double* __restrict__ smem = smem_all;")
+                 : "double* __restrict__ smem = smem_all + (threadIdx.x >> 5) * " + i64(per_warp) + ";");
+    }
     E.line("double okacc = 0.0;  // fma(v, 0, acc) turns NaN iff some checked v is not finite");
     E.line("bool ok = true;");
-    E.line("const long long ntiles = (n_main + 31) / 32;");
-    E.line("const long long wpb = OCG_BLOCK / 32;");
+    E.line("const OIX ntiles = (n_main + 31) / 32;");
+    E.line("const OIX wpb = OCG_BLOCK / 32;");
     // loop invariants (free variables such as tf and everything computed from
-    // them alone) once per thread, before the tile loop
-    {
+    // them alone) once per thread, before the tile loop; emitted after the
+    // first tile's copies are issued so that both loads are in flight together
+    auto emit_invariants = [&]() {
       std::vector<Check> none;
       for (const Inst& mb : members) {
         const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
         const std::vector<char> inv = invariant_nodes(g.kernel.graph);
         forward(E, g, "idx", false, parts(m, mb.objective, g).partials, 0, none, &inv);
       }
-    }
+    };
     // Distinct regions: the tile's outputs of every group leave together after
     // the last group, one bulk copy per lane; each lane's copy (destination
     // base, row length, shared-memory offset, range slice) is set up once here
-    const bool batched = opt_.distinct_regions && !opt_.split_kinds;
+    const bool batched = distinct && !split;
     struct Copy {
       std::string dst;
       Index S, soff;
@@ -984,6 +1059,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
     std::vector<Copy> copies;
     if (batched) {
       std::map<std::string, int> rid;
+      // (TMA tiles: lane 0 issues every copy; no per-lane descriptors)
       for (size_t q = 0; q < members.size(); ++q) {
         const Inst& mb = members[q];
         const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
@@ -994,9 +1070,9 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         }
         for (const Out& o : outs[q]) copies.push_back({o.dst, o.per_k, o.soff, rid.at(key)});
       }
-      for (size_t c0 = 0; c0 < copies.size(); c0 += 32) {
+      for (size_t c0 = 0; c0 < copies.size() && !uni; c0 += 32) {
         const std::string C = std::to_string(c0 / 32);
-        E.line("double* cd" + C + "_dst = nullptr; long long cd" + C + "_S = 0, cd" + C + "_soff = 0; int cd" + C +
+        E.line("double* cd" + C + "_dst = nullptr; OIX cd" + C + "_S = 0, cd" + C + "_soff = 0; int cd" + C +
                "_R = -1;");
         for (size_t j = c0; j < std::min(copies.size(), c0 + 32); ++j)
           E.line("if (lane == " + std::to_string(j - c0) + ") { cd" + C + "_dst = " + copies[j].dst + "; cd" + C +
@@ -1004,67 +1080,182 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
                  "_R = " + std::to_string(copies[j].R) + "; }");
       }
     }
-    E.open("for (long long tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb)");
-    E.line("const long long ib = i0 + tile * 32;");
-    E.line("const long long idx = ib + lane;");
-    E.line("const bool in = idx < i0 + n_main;");
-    // the tile's slice of every distinct group range
-    slices_.clear();
-    for (const Inst& mb : members) {
-      const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
-      const std::string key = range_param(g.range, true) + "," + range_param(g.range, false);
-      if (slices_.count(key)) continue;
-      const std::string R = std::to_string(slices_.size());
-      slices_[key] = R;
-      const std::string lo = range_param(g.range, true), hi = range_param(g.range, false);
-      E.line("const long long kb" + R + " = ib - " + lo + ";");
-      E.line("const long long k0" + R + " = kb" + R + " > 0 ? kb" + R + " : 0;");
-      E.line("long long k1" + R + " = kb" + R + " + 32; if (k1" + R + " > " + hi + " - " + lo + ") k1" + R + " = " + hi +
-             " - " + lo + "; if (k1" + R + " > i0 + n_main - " + lo + ") k1" + R + " = i0 + n_main - " + lo + ";");
-      E.line("const int nk" + R + " = k1" + R + " > k0" + R + " ? (int)(k1" + R + " - k0" + R + ") : 0, r0" + R +
-             " = (int)(k0" + R + " - kb" + R + ");");
-    }
-    first_store_of_tile_ = true;
-    // stage every global input of the tile with asynchronous copies, then wait once
-    for (auto& [s, u] : uses) {
-      const Slab& sl = nlp_.slabs[s];
-      const Index n = (W + u.max_off) * sl.dim;
-      const std::string sb = P("slab" + std::to_string(s) + ".base", sl.base);
-      const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
-      // the copy count is bounded at generation time: straight-line
-      // predicated copies, no loop control
-      E.line("{ const long long gb = " + sb + " + ib * " + i64(sl.dim) + "; long long nv = " + se +
-             " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) + "; const int nvi = (int)nv;");
-      for (Index j0 = 0; j0 < n; j0 += 32)
-        E.line("  if (lane + " + std::to_string(j0) + " < nvi) ocg_cp8(smem + " + i64(u.soff + j0) + " + lane, x + gb + " +
-               std::to_string(j0) + " + lane);");
-      E.line("}");
-    }
-    bool staged_any = !uses.empty();
-    for (size_t q = 0; q < members.size(); ++q) {
-      if (rows[q].rs < 0 && rows[q].lam < 0) continue;
-      const Inst& mb = members[q];
-      const Group& g = nlp_.cons[static_cast<size_t>(mb.gi)];
-      const std::string rb = G(false, mb.gi, "row_base", g.row_base);
-      const std::string od = i64(g.out_dim());
-      const std::string R = slice_of(g.range);
-      E.open("");
-      E.line("const int nr = nk" + R + " * (int)" + od + ", so = r0" + R + " * (int)" + od + ";");
-      E.line("const long long g0 = " + rb + " + k0" + R + " * " + od + ";");
-      const Index nmax = W * g.out_dim();
-      for (Index j0 = 0; j0 < nmax; j0 += 32) {
-        const std::string j = std::to_string(j0) + " + lane";
-        if (rows[q].rs >= 0)
-          E.line("if (" + j + " < nr) ocg_cp8(smem + " + i64(rows[q].rs) + " + so + " + j + ", rs + g0 + " + j + ");");
-        if (rows[q].lam >= 0)
-          E.line("if (" + j + " < nr) ocg_cp8(smem + " + i64(rows[q].lam) + " + so + " + j + ", lam + g0 + " + j + ");");
+    // the tile's slice of every distinct group range (tile base `ib` in scope)
+    auto emit_slices = [&]() {
+      slices_.clear();
+      for (const Inst& mb : members) {
+        const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+        const std::string key = range_param(g.range, true) + "," + range_param(g.range, false);
+        if (slices_.count(key)) continue;
+        const std::string R = std::to_string(slices_.size());
+        slices_[key] = R;
+        const std::string lo = range_param(g.range, true), hi = range_param(g.range, false);
+        E.line("const OIX kb" + R + " = ib - " + lo + ";");
+        E.line("const OIX k0" + R + " = kb" + R + " > 0 ? kb" + R + " : 0;");
+        E.line("OIX k1" + R + " = kb" + R + " + 32; if (k1" + R + " > " + hi + " - " + lo + ") k1" + R + " = " +
+               hi + " - " + lo + "; if (k1" + R + " > i0 + n_main - " + lo + ") k1" + R + " = i0 + n_main - " + lo + ";");
+        E.line("const int nk" + R + " = k1" + R + " > k0" + R + " ? (int)(k1" + R + " - k0" + R + ") : 0, r0" + R +
+               " = (int)(k0" + R + " - kb" + R + ");");
       }
-      E.close();
-      staged_any = true;
+    };
+    // global source and shared-memory region start of a staged row segment
+    auto row_src = [&](size_t q, int what) {
+      const Group& g = nlp_.cons[static_cast<size_t>(members[q].gi)];
+      const std::string R = slice_of(g.range), od = i64(g.out_dim());
+      return std::string(what == 0 ? "rs" : "lam") + " + " + G(false, members[q].gi, "row_base", g.row_base) + " + k0" + R +
+             " * " + od;
+    };
+    auto row_pos = [&](size_t q, int what, const std::string& buf) {
+      const Group& g = nlp_.cons[static_cast<size_t>(members[q].gi)];
+      const std::string R = slice_of(g.range), od = i64(g.out_dim());
+      return buf + " + " + i64((what == 0 ? rows[q].rs : rows[q].lam) + 1) + " + r0" + R + " * " + od;
+    };
+    auto slab_src = [&](size_t s) {
+      const Slab& sl = nlp_.slabs[s];
+      return "x + " + P("slab" + std::to_string(s) + ".base", sl.base) + " + ib * " + i64(sl.dim);
+    };
+    // LDGSTS staging of a tile's inputs into buffer `buf` (tile base `ib` and
+    // its slices in scope); returns whether anything is staged
+    auto emit_ldgsts = [&](const std::string& buf) {
+      bool any = false;
+      for (auto& [s, u] : uses) {
+        const Slab& sl = nlp_.slabs[s];
+        const Index n = (W + u.max_off) * sl.dim;
+        const std::string sb = P("slab" + std::to_string(s) + ".base", sl.base);
+        const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
+        // the copy count is bounded at generation time: straight-line
+        // predicated copies, no loop control
+        E.line("{ const OIX gb = " + sb + " + ib * " + i64(sl.dim) + "; OIX nv = " + se +
+               " - gb; if (nv > " + i64(n) + ") nv = " + i64(n) + "; const int nvi = (int)nv;");
+        for (Index j0 = 0; j0 < n; j0 += 32)
+          E.line("  if (lane + " + std::to_string(j0) + " < nvi) ocg_cp8(" + buf + " + " + i64(u.soff + j0) +
+                 " + lane, x + gb + " + std::to_string(j0) + " + lane);");
+        E.line("}");
+        any = true;
+      }
+      for (size_t q = 0; q < members.size(); ++q) {
+        if (rows[q].rs < 0 && rows[q].lam < 0) continue;
+        const Inst& mb = members[q];
+        const Group& g = nlp_.cons[static_cast<size_t>(mb.gi)];
+        const std::string rb = G(false, mb.gi, "row_base", g.row_base);
+        const std::string od = i64(g.out_dim());
+        const std::string R = slice_of(g.range);
+        E.open("");
+        E.line("const int nr = nk" + R + " * (int)" + od + ", so = r0" + R + " * (int)" + od + ";");
+        E.line("const OIX g0 = " + rb + " + k0" + R + " * " + od + ";");
+        const Index nmax = W * g.out_dim();
+        for (Index j0 = 0; j0 < nmax; j0 += 32) {
+          const std::string j = std::to_string(j0) + " + lane";
+          if (rows[q].rs >= 0)
+            E.line("if (" + j + " < nr) ocg_cp8(" + buf + " + " + i64(rows[q].rs) + " + so + " + j + ", rs + g0 + " + j +
+                   ");");
+          if (rows[q].lam >= 0)
+            E.line("if (" + j + " < nr) ocg_cp8(" + buf + " + " + i64(rows[q].lam) + " + so + " + j + ", lam + g0 + " + j +
+                   ");");
+        }
+        E.close();
+        any = true;
+      }
+      return any;
+    };
+    if (pf) {
+      // double-buffered LDGSTS staging: tile t+1's copies are issued before
+      // tile t computes (one cp.async group per tile, wait_group 1)
+      E.open("auto ocg_stage = [&](const OIX t, double* const sb)");
+      E.line("const OIX ib = i0 + t * 32;");
+      emit_slices();
+      emit_ldgsts("sb");
+      E.close(";");
+      E.line("if (blockIdx.x * wpb + (threadIdx.x >> 5) < ntiles) ocg_stage(blockIdx.x * wpb + (threadIdx.x >> 5), smem);");
+      E.line("ocg_cp_commit();");
+      E.line("OIX it = 0;");
     }
-    if (staged_any) {
-      E.line("ocg_cp_wait();");
+    if (tma) {
+      // tile t's inputs into buffer buf: one bulk copy per node slab and per
+      // row segment, each landing where shared memory agrees with global
+      // memory modulo 16 bytes (a shift of 0 or 1 double inside its region)
+      E.open("auto ocg_stage = [&](const OIX t, const int buf)");
+      E.line("double* const sb = sin0 + buf * " + i64(IN) + ";");
+      E.line("unsigned long long* const bar = ocg_bar + buf;");
+      E.line("const OIX ib = i0 + t * 32;");
+      emit_slices();
+      for (auto& [s, u] : uses) {
+        const Slab& sl = nlp_.slabs[s];
+        const Index n = (W + u.max_off) * sl.dim;
+        const std::string se = P("slab" + std::to_string(s) + ".end", sl.base + sl.nodes * sl.dim);
+        E.line("{ const double* const g = " + slab_src(s) + "; OIX nv = (OIX)((x + " + se + ") - g); if (nv > " + i64(n) +
+               ") nv = " + i64(n) + "; double* const r = sb + " + i64(u.soff + 1) +
+               "; if (nv > 0) ocg_bulk_load(r + ocg_shift(g, r), g, nv, bar); }");
+      }
+      for (size_t q = 0; q < members.size(); ++q) {
+        if (rows[q].rs < 0 && rows[q].lam < 0) continue;
+        const Group& g = nlp_.cons[static_cast<size_t>(members[q].gi)];
+        const std::string R = slice_of(g.range), od = i64(g.out_dim());
+        E.open("if (nk" + R + " > 0)");
+        for (int what = 0; what < 2; ++what) {
+          if ((what == 0 ? rows[q].rs : rows[q].lam) < 0) continue;
+          E.line("{ const double* const g = " + row_src(q, what) + "; double* const r = " + row_pos(q, what, "sb") +
+                 "; ocg_bulk_load(r + ocg_shift(g, r), g, (OIX)nk" + R + " * " + od + ", bar); }");
+        }
+        E.close();
+      }
+      E.line("ocg_mbar_arrive(bar);");
+      E.close(";");
+      E.line("if (lane == 0 && (OIX)blockIdx.x < ntiles) ocg_stage(blockIdx.x, 0);");
+      E.line("OIX it = 0;");
+      emit_invariants();
+      E.open("for (OIX tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it)");
+      E.line("const int buf = (int)(it & 1);");
+      E.line("if (lane == 0 && tile + gridDim.x < ntiles) { ocg_fence_async(); ocg_stage(tile + gridDim.x, buf ^ 1); }");
+    } else {
+      emit_invariants();
+      E.open(std::string(uni ? "for (OIX tile = blockIdx.x; tile < ntiles; tile += gridDim.x"
+                             : "for (OIX tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb") +
+             std::string(pf ? ", ++it)" : ")"));
+    }
+    E.line("const OIX ib = i0 + tile * 32;");
+    E.line("const OIX idx = ib + lane;");
+    E.line("const bool in = idx < i0 + n_main;");
+    emit_slices();
+    first_store_of_tile_ = true;
+    if (tma) {
+      // wait for this tile's copies; per-region pointers with this tile's shifts
+      E.line("ocg_mbar_wait(ocg_bar + buf, (unsigned)((it >> 1) & 1));");
       E.line("__syncwarp();");
+      E.line("double* const sin = sin0 + buf * " + i64(IN) + ";");
+      for (auto& [s, u] : uses) {
+        const std::string S = std::to_string(s);
+        E.line("const double* const xs" + S + " = sin + " + i64(u.soff + 1) + " + ocg_shift(" + slab_src(s) + ", sin + " +
+               i64(u.soff + 1) + ");");
+      }
+      for (size_t q = 0; q < members.size(); ++q) {
+        for (int what = 0; what < 2; ++what) {
+          if ((what == 0 ? rows[q].rs : rows[q].lam) < 0) continue;
+          E.line("const double* const rq" + std::to_string(q) + "_" + std::to_string(what) + " = sin + " +
+                 i64((what == 0 ? rows[q].rs : rows[q].lam) + 1) + " + ocg_shift(" + row_src(q, what) + ", " +
+                 row_pos(q, what, "sin") + ");");
+        }
+      }
+    }
+    if (!tma && !pf) {
+      // stage every global input of the tile with asynchronous copies, then wait once
+      if (emit_ldgsts("smem")) {
+        E.line("ocg_cp_wait();");
+        E.line("__syncwarp();");
+      }
+    } else if (pf) {
+      // this tile's copies (the only group in flight) and the previous tile's
+      // bulk copy-out reads are complete before the next tile's copies go
+      // out: ptxas tracks LDGSTS and the bulk copies on one scoreboard, so a
+      // read wait later in the tile would also wait for the prefetch
+      E.line("double* const sin = smem + (it & 1) * " + i64(IN) + ";");
+      E.line("ocg_cp_wait();");
+      E.line("ocg_bulk_wait_read();");
+      E.line("__syncwarp();");
+      E.line("if (tile + gridDim.x * wpb < ntiles) ocg_stage(tile + gridDim.x * wpb, smem + ((it + 1) & 1) * " + i64(IN) +
+             ");");
+      E.line("ocg_cp_commit();");
+      first_store_of_tile_ = false;
     }
     load_from_ = [&](const Addr& a) -> std::string {
       if (a.stride == 0) return "";
@@ -1072,7 +1263,8 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       const long s = slab_of(a, node, comp);
       if (s < 0) return "";
       const Index dim = nlp_.slabs[static_cast<size_t>(s)].dim;
-      return "smem[" + i64(uses.at(static_cast<size_t>(s)).soff + node * dim + comp) + " + lane * " + i64(dim) + "]";
+      if (tma) return "xs" + std::to_string(s) + "[" + i64(node * dim + comp) + " + lane * " + i64(dim) + "]";
+      return std::string(pf ? "sin[" : "smem[") + i64(uses.at(static_cast<size_t>(s)).soff + node * dim + comp) + " + lane * " + i64(dim) + "]";
     };
     for (size_t q = 0; q < members.size(); ++q) {
       const Inst& mb = members[q];
@@ -1106,13 +1298,13 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       int cur_kind = -2;  // -2: nothing stored yet in this group
       store_hook_ = [&](int kind) {
         if (kind == cur_kind) return;
-        if (opt_.split_kinds && cur_kind >= 0) {
+        if (split && cur_kind >= 0) {
           for (size_t oi = 0; oi < outs[q].size(); ++oi)
             if (outs[q][oi].kind == cur_kind) flush(oi);
         }
         // region free again? (distinct regions: only the tile's first store
         // waits, for the previous tile's copy-out)
-        if ((cur_kind == -2 && (!opt_.distinct_regions || first_store_of_tile_)) || opt_.split_kinds)
+        if ((cur_kind == -2 && (!distinct || first_store_of_tile_)) || split)
           E.line("ocg_bulk_wait_read(); __syncwarp();");
         first_store_of_tile_ = false;
         cur_kind = kind;
@@ -1129,7 +1321,10 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       row_from_ = [&](int what, int r) -> std::string {
         const Index off = what == 0 ? rows[q].rs : rows[q].lam;
         if (off < 0) return "";
-        return "smem[" + i64(off + r) + " + lane * " + i64(g.out_dim()) + "]";
+        if (tma)
+          return "rq" + std::to_string(q) + "_" + std::to_string(what) + "[" + i64(r) + " + lane * " + i64(g.out_dim()) +
+                 "]";
+        return std::string(pf ? "sin[" : "smem[") + i64(off + r) + " + lane * " + i64(g.out_dim()) + "]";
       };
       // Every lane evaluates every member group in one scope (so common
       // subexpressions are shared across groups) and stores its rows to
@@ -1139,6 +1334,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       E.line("// ---- " + std::string(mb.objective ? "objective" : "constraint") + " group " +
              std::to_string(mb.gi) + ": " + g.label);
       E.line("const bool p" + qs + " = in && idx >= " + lo + " && idx < " + hi + ";");
+      store_pred_ = "p" + qs;
       E.line("double okg" + qs + " = 0.0;");
       acc_ = "okg" + qs;
       std::vector<Check> sc;
@@ -1148,12 +1344,13 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       E.line("if (p" + qs + ") okacc += okg" + qs + ";");
       acc_ = "okacc";
       store_to_ = nullptr;
+      store_pred_.clear();
       row_from_ = nullptr;
       store_hook_ = nullptr;
       if (outs[q].empty() || batched) continue;
       // rows are unpadded (pitch == per_k): the tile's segment of each output
       // is contiguous in shared memory and in the COO array -> one bulk copy
-      if (opt_.split_kinds) {
+      if (split) {
         for (size_t oi = 0; oi < outs[q].size(); ++oi)
           if (outs[q][oi].kind == cur_kind) flush(oi);
       } else {
@@ -1178,7 +1375,27 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         E.close();
       }
     }
-    if (batched && !copies.empty()) {
+    if (uni && batched && !copies.empty()) {
+      // every output of the tile: lane 0 issues the copies (uniform operands)
+      E.line("ocg_fence_async(); __syncwarp();");
+      E.open("if (lane == 0)");
+      for (size_t q = 0; q < members.size(); ++q) {
+        const Inst& mb = members[q];
+        const Group& g = mb.objective ? nlp_.objs[static_cast<size_t>(mb.gi)] : nlp_.cons[static_cast<size_t>(mb.gi)];
+        const std::string R = slice_of(g.range);
+        for (const Out& o : outs[q]) {
+          const std::string S = i64(o.per_k);
+          E.line("if (nk" + R + " > 0) { double* const g = " + o.dst + " + k0" + R + " * " + S +
+                 "; const double* const sb = smem + " + i64(o.soff) + " + r0" + R + " * " + S +
+                 "; ocg_bulk_store(g, sb + ocg_shift(g, sb), nk" + R + " * (int)" + S + "); }");
+        }
+      }
+      E.line("ocg_bulk_commit();");
+      E.close();
+    } else if (tma) {
+      E.line("__syncwarp();");
+    }
+    if (batched && !copies.empty() && !uni) {
       // every output of the tile, one bulk copy per lane (chunks of 32)
       E.line("ocg_fence_async(); __syncwarp();");
       const int nslice = static_cast<int>(slices_.size());
@@ -1191,7 +1408,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       for (size_t c0 = 0; c0 < copies.size(); c0 += 32) {
         const std::string C = std::to_string(c0 / 32);
         E.open("if (cd" + C + "_R >= 0)");
-        E.line("const long long k0s = " + sel(C, "k0") + ";");
+        E.line("const OIX k0s = " + sel(C, "k0") + ";");
         E.line("const int r0s = " + sel(C, "r0") + ", nks = " + sel(C, "nk") + ";");
         E.open("if (nks > 0)");
         E.line("double* const g = cd" + C + "_dst + k0s * cd" + C + "_S;");
@@ -1203,6 +1420,10 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
       }
     }
     load_from_ = nullptr;
+    // every lane is done reading this tile's staged inputs before any lane
+    // stages the next tile's (a kernel whose outputs all go straight to
+    // global memory has no copy-out barrier)
+    E.line("__syncwarp();");
     E.close();  // tile loop
     E.line("ocg_bulk_wait_all();  // bulk copies done before the block exits");
 
@@ -1217,7 +1438,7 @@ __device__ __forceinline__ void ocg_bulk_wait_all() { asm volatile("cp.async.bul
         E.open("case " + std::to_string(s) + ":");
         const std::string idx = in.k == 0 ? G(in.objective, in.gi, "lo", g.range.lo)
                                           : G(in.objective, in.gi, "hi", g.range.hi);
-        E.line("const long long sidx = " + idx + ";");
+        E.line("const OIX sidx = " + idx + ";");
         std::vector<Check> sc;
         Fwd f = forward(E, g, "sidx", false, p.partials, 0, sc);
         for (const auto& c : sc) check_inline(E, c.v);

@@ -123,6 +123,13 @@ struct ocg_eval {
   bool specials = true;
   std::map<std::string, int> slices, tail, smem;
   std::vector<long long> prm;  // by-value parameter block of the generated kernels
+  std::vector<int> prm32;      // the same as 32-bit integers (modules with 32-bit indexing)
+  bool idx32 = false;
+  void set_idx32(bool on) {
+    idx32 = on;
+    prm32.assign(prm.begin(), prm.end());
+  }
+  void* prm_arg() { return idx32 ? static_cast<void*>(prm32.data()) : static_cast<void*>(prm.data()); }
   std::map<std::string, int> resident;  // resident blocks per SM per kernel
   int sm_count = 148;
   Index i0 = 0, n_main = 0;

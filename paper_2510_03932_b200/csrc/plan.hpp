@@ -1,6 +1,7 @@
 // Device evaluation plan: COO offsets, thread mapping and generated kernels.
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
@@ -28,6 +29,13 @@ struct Layout {
 
 Layout make_layout(const Nlp& nlp);
 
+// every index the generated kernels form (array slots, COO offsets, tile
+// bases) fits 32-bit arithmetic, with room for a tile's overshoot
+inline bool fits_idx32(const Nlp& nlp, const Layout& lay) {
+  Index mx = std::max({lay.jac_nnz, lay.hess_nnz, lay.grad_nnz, lay.objv_n, nlp.nvar, nlp.m_con, lay.idx_hi});
+  return mx < (Index{1} << 30);
+}
+
 struct GenOptions {
   bool fma = false;  // false: no FMA contraction (bit-compatible with the x86 reference)
   int block = 128;
@@ -40,6 +48,13 @@ struct GenOptions {
   // every group's outputs in their own shared region: one wait per tile
   // instead of one per group (more shared memory per warp)
   bool distinct_regions = false;
+  // double-buffered input staging: the next tile's LDGSTS copies are in
+  // flight while this tile computes (two input buffers per warp)
+  bool prefetch = false;
+  // TMA tiles (block 32 only): bulk copy-in on mbarriers, double-buffered
+  bool tma = false;
+  // 32-bit index arithmetic (every array index of the model < 2^31)
+  bool idx32 = false;
 };
 
 struct Generated {
@@ -60,6 +75,9 @@ struct Generated {
   int block = 128;
   bool split_kinds = false;
   bool distinct_regions = false;
+  bool prefetch = false;
+  bool tma = false;
+  bool idx32 = false;
 };
 
 // Kernel entry points in the generated module (all extern "C"):

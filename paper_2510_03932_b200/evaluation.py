@@ -66,8 +66,8 @@ class Model:
         check(LIB.ocg_model_synth_acceptance(self._h, seed, x.ctypes.data, lam.ctypes.data))
         return x, lam
 
-    def generated_source(self, fma: bool = False, block: int = 128) -> str:
-        return _lib.take_string(LIB.ocg_debug_generated_source(self._h, int(fma), block))
+    def generated_source(self, fma: bool = False, block: int = 128, input_staging: int = 0) -> str:
+        return _lib.take_string(LIB.ocg_debug_generated_source_ex(self._h, int(fma), block, int(input_staging)))
 
 
 def synth_uniform(seed: int, lo: float, hi: float, n: int) -> np.ndarray:
@@ -176,7 +176,7 @@ class EvalContext:
 
     def __init__(self, model: Model, device: int = 0, fma: bool = False, block: int = 128,
                  idx_lo: int = 0, idx_hi: int = -1, specials: bool = True, min_blocks: int = 0,
-                 split_kinds: int = -1, comm: Comm | None = None):
+                 split_kinds: int = -1, comm: Comm | None = None, input_staging: int = -1):
         """comm: a sharded context (ocg_eval_create_sharded) — this rank's
         node range, endpoint instances on rank 0; idx_lo/idx_hi/specials are
         then derived from the rank."""
@@ -186,7 +186,7 @@ class EvalContext:
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials), int(min_blocks),
-                                int(split_kinds))
+                                int(split_kinds), int(input_staging))
         h = C.c_void_p()
         self.comm = comm
         if comm is None:

@@ -20,6 +20,7 @@ ap.add_argument("cases", nargs="*", default=["goddard:100000", "quadrotor:100000
 ap.add_argument("--minb", default="0")
 ap.add_argument("--split", default="-1")
 ap.add_argument("--block", type=int, default=128)
+ap.add_argument("--staging", default="-1", help="input_staging values, comma separated")
 ap.add_argument("--steps", type=int, default=30)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
@@ -36,8 +37,9 @@ for case in a.cases:
     xd, ld = torch.as_tensor(x, device=dev), torch.as_tensor(lam, device=dev)
     c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
     nb = bench.algorithmic_bytes(st, *bench.main_space(st), True)
-    for mb, sp in [(int(v), int(w)) for v in a.minb.split(",") for w in a.split.split(",")]:
-        ec = EvalContext(m, block=a.block, min_blocks=mb, split_kinds=sp)
+    for mb, sp, stg in [(int(v), int(w), int(z)) for v in a.minb.split(",") for w in a.split.split(",")
+                        for z in a.staging.split(",")]:
+        ec = EvalContext(m, block=a.block, min_blocks=mb, split_kinds=sp, input_staging=stg)
         ok = ec.eval_jac_hess(xd, ld, c)
         ts, _ = bench.time_eval_config(ec, xd, ld, c, flush, sink, stream, a.steps, 3)
         t = float(np.median(ts))
@@ -53,7 +55,7 @@ for case in a.cases:
             e.synchronize()
             sep.append(s.elapsed_time(e) * 1e-3)
         ts2 = float(np.median(sep))
-        print(json.dumps({"model": name, "N": N, "minb": mb, "split": sp, "ok": ok, "us_fused": t * 1e6, "us_sep": ts2 * 1e6,
+        print(json.dumps({"model": name, "N": N, "minb": mb, "split": sp, "staging": stg, "block": a.block, "ok": ok, "us_fused": t * 1e6, "us_sep": ts2 * 1e6,
                           "ns_per_node": t * 1e9 / N, "frac_fused": nb / t / 1e9 / peak,
                           "frac_sep": nb / ts2 / 1e9 / peak}), flush=True)
         del ec

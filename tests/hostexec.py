@@ -44,12 +44,18 @@ template <class T> static inline T __ldg(const T* p) { return *p; }
 // asynchronous copies complete immediately on the host
 static inline void ocg_cp8(double* s, const double* g) { *s = *g; }
 static inline void ocg_cp_wait() {}
+static inline void ocg_cp_commit() {}
+static inline void ocg_cp_wait1() {}
 static inline int ocg_shift(const double* g, const double* s) { return (int)((((unsigned long long)g) ^ ((unsigned long long)s)) >> 3) & 1; }
 static inline void ocg_fence_async() {}
 static inline void ocg_bulk_store(double* g, const double* s, int n) { for (int i = 0; i < n; ++i) g[i] = s[i]; }
 static inline void ocg_bulk_commit() {}
 static inline void ocg_bulk_wait_read() {}
 static inline void ocg_bulk_wait_all() {}
+static inline void ocg_mbar_init(unsigned long long*) {}
+static inline void ocg_mbar_arrive(unsigned long long*) {}
+static inline void ocg_mbar_wait(unsigned long long*, unsigned) {}
+static inline void ocg_bulk_load(double* p, const double* g, long long n, unsigned long long*) { for (long long i = 0; i < n; ++i) p[i] = g[i]; }
 static inline double __longlong_as_double(long long v) { double d; std::memcpy(&d, &v, 8); return d; }
 // the reference evaluates sin and cos separately with glibc
 static inline void ocg_sincos(double a, double* s, double* c) { *s = std::sin(a); *c = std::cos(a); }
@@ -82,7 +88,7 @@ def _driver(name: str, params: str) -> str:
     args = ", ".join(p.split()[-1].lstrip("*") for p in params.split(","))
     return (f'extern "C" void run_{name}(const long long* pv, {params}, long long i0, long long n_main,'
             f" long long n_spec, long long total, int ys) {{\n"
-            f"  OcgParams prm; std::memcpy(prm.v, pv, sizeof prm.v);\n"
+            f"  OcgParams prm; for (size_t i = 0; i < sizeof prm.v / sizeof prm.v[0]; ++i) prm.v[i] = (OIX)pv[i];\n"
             f"  (void)total; (void)ys;\n"
             f"  // persistent warp-synchronous kernel: one block of one warp walks every\n"
             f"  // tile; lanes are real threads meeting at __syncwarp\n"
@@ -110,10 +116,10 @@ def compile_generated(source: str) -> C.CDLL:
 class HostKernels:
     """Runs the generated kernels for a Model on the CPU (layout from the model)."""
 
-    def __init__(self, model, layout: dict):
+    def __init__(self, model, layout: dict, input_staging: int = 1):
 
         # satisfied by sequential execution
-        src = model.generated_source(fma=False, block=32)
+        src = model.generated_source(fma=False, block=32, input_staging=input_staging)
         meta = src[src.rindex("// ocg-meta ") + len("// ocg-meta "):]
         import json
         self.meta = json.loads(meta)
@@ -163,13 +169,14 @@ def layout_from_structure(st: dict) -> dict:
     return {"idx_lo": lo, "n_main": hi - lo, "n_spec": n_spec, "jac_nnz": jac, "hess_nnz": hess}
 
 
-def run_all(model, x, lam, obj_scale: float = 1.0, row_scale=None):
+def run_all(model, x, lam, obj_scale: float = 1.0, row_scale=None, input_staging: int = 1):
     """Host execution of every generated kernel: c, c+jac, hess, objective
     instance values and gradient COO, with the reference's unit (or given)
-    scaling."""
+    scaling. input_staging: 0 LDGSTS once per tile, 1 double-buffered LDGSTS
+    (the default on the device), 2 TMA bulk copies on mbarriers."""
     st = model.structure()
     lay = layout_from_structure(st)
-    hk = HostKernels(model, lay)
+    hk = HostKernels(model, lay, input_staging)
     rs = np.ones(model.m_con) if row_scale is None else np.ascontiguousarray(row_scale, dtype=np.float64)
     objw = np.array([obj_scale * g["weight"] for g in st["obj_groups"]] or [0.0])
     out = {}

@@ -25,14 +25,19 @@ def _ref_all(r, x, lam):
     return out
 
 
+# input staging modes (ocg_eval_options.input_staging): 1 is the device
+# default; N = 100 walks four tiles, so the double buffers alternate
+STAGINGS = [(1, 2), (1, 25), (1, 100), (0, 100), (2, 25), (2, 100)]
+
+
 @pytest.mark.parametrize("name", list(MODELS))
-@pytest.mark.parametrize("N", [2, 25])
+@pytest.mark.parametrize("staging,N", STAGINGS)
 @pytest.mark.parametrize("scheme", ["trapezoid", "euler"])
-def test_generated_code_bit_exact(name, N, scheme):
+def test_generated_code_bit_exact(name, N, scheme, staging):
     m = Model(MODELS[name], N, scheme)
     r = RefModel(MODELS[name], N, 1 if scheme == "trapezoid" else 0)
     x, lam = r.synth_acceptance(20250808)
-    got, ref = run_all(m, x, lam), _ref_all(r, x, lam)
+    got, ref = run_all(m, x, lam, input_staging=staging), _ref_all(r, x, lam)
     for key in ("c_ok", "cjac_ok", "hess_ok", "grad_ok"):
         assert got[key] == ref[key], key
     flag_of = {"c": "c_ok", "c_cjac": "cjac_ok", "jac": "cjac_ok", "hess": "hess_ok", "grad": "grad_ok"}

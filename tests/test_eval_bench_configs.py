@@ -1,5 +1,5 @@
 """GPU parity at the BENCHMARKED configurations, launched exactly as bench.py
-launches them (block 128, default options: the persistent grid where blocks
+launches them (block 32 and 128, default options: the persistent grid where blocks
 loop over several tiles, shared-memory staging reused across tiles behind the
 bulk-copy read waits, alignment shifts of the bulk copy-out), against the
 reference EvalContext (oracle/_ref/libref.so, Backend::parallel) on:
@@ -55,35 +55,43 @@ def _check_all(name, m, ec, re, x, lam):
     return out
 
 
+# 32: one-warp blocks, TMA bulk copy-in double-buffered on mbarriers (the
+# default); 128: four warps per block with LDGSTS staging
+BLOCKS = [32, 128]
+
+
+@pytest.mark.parametrize("block", BLOCKS)
 @pytest.mark.parametrize("name,N", CONFIGS)
-def test_bench_config_acceptance_recipe(name, N):
+def test_bench_config_acceptance_recipe(name, N, block):
     src = MODELS[name]
     m, r = Model(src, N), RefModel(src, N)
     x, lam = r.synth_acceptance(20250808)
-    ec = EvalContext(m, device=0, block=128)  # bench.py's options
+    ec = EvalContext(m, device=0, block=block)
     re = RefEval(r, parallel=True, workers=os.cpu_count() or 1)
     st = _check_all(name, m, ec, re, x, lam)
     print(name, N, {k: (v["max_rel"], v["bit_exact"]) for k, v in st.items()})
 
 
+@pytest.mark.parametrize("block", BLOCKS)
 @pytest.mark.parametrize("N", [100_000, 1_000_000])
-def test_bench_config_quadrotor_recipe(N):
+def test_bench_config_quadrotor_recipe(N, block):
     src = MODELS["quadrotor"]
     m, r = Model(src, N), RefModel(src, N)
     x = synth_uniform(11, -0.5, 0.5, m.nvar)
     lam = np.full(m.m_con, 0.25)
-    ec = EvalContext(m, device=0, block=128)
+    ec = EvalContext(m, device=0, block=block)
     re = RefEval(r, parallel=True, workers=os.cpu_count() or 1)
     _check_all("quadrotor", m, ec, re, x, lam)
 
 
+@pytest.mark.parametrize("block", BLOCKS)
 @pytest.mark.parametrize("name,N", [("goddard", 100_000), ("quadrotor", 100_000)])
-def test_bench_config_objective_gradient(name, N):
+def test_bench_config_objective_gradient(name, N, block):
     """f (reference 512-chunk order) and the dense gradient at bench sizes."""
     src = MODELS[name]
     m, r = Model(src, N), RefModel(src, N)
     x, _ = r.synth_acceptance(20250808)
-    ec = EvalContext(m, device=0, block=128)
+    ec = EvalContext(m, device=0, block=block)
     re = RefEval(r, parallel=True, workers=os.cpu_count() or 1)
     ok_r, f_r = re.objective(x)
     ok, f = ec.eval_objective(x)
