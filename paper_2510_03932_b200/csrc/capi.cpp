@@ -1142,6 +1142,51 @@ int ocg_kkt_create(const ocg_model* mdl, ocg_eval* e, ocg_kkt** out) {
   if (!ocg::dev::kkt_code32(K->src_ptr.p, K->src_code.p, K->nnz, K->H, K->J, K->n_slack, K->ntot, K->src_code32.p,
                             cudaStreamPerThread))
     K->src_code32.release();
+  // 32-bit copies of the matvec / J^T lambda indices (values < nnz_K, dim, nnz_J, m)
+  if (K->nnz < (Index{1} << 31) && K->dim < (Index{1} << 31) && K->J < (Index{1} << 31) &&
+      !(std::getenv("OCG_IDX64") && std::atoi(std::getenv("OCG_IDX64")) != 0)) {
+    int64_t nmv = 0, njt = 0;
+    ck(cudaMemcpyAsync(&nmv, K->mv_ptr.p + K->dim, sizeof(int64_t), cudaMemcpyDeviceToHost, cudaStreamPerThread), "mv n");
+    ck(cudaMemcpyAsync(&njt, K->jt_ptr.p + K->ntot, sizeof(int64_t), cudaMemcpyDeviceToHost, cudaStreamPerThread), "jt n");
+    ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
+    K->mv_col32.alloc(static_cast<size_t>(std::max<int64_t>(1, nmv)));
+    K->mv_vidx32.alloc(static_cast<size_t>(std::max<int64_t>(1, nmv)));
+    K->jt_e32.alloc(static_cast<size_t>(std::max<int64_t>(1, njt)));
+    K->jt_dual32.alloc(static_cast<size_t>(std::max<int64_t>(1, njt)));
+    ocg::dev::narrow_i32(K->mv_col.p, nmv, K->mv_col32.p, cudaStreamPerThread);
+    ocg::dev::narrow_i32(K->mv_vidx.p, nmv, K->mv_vidx32.p, cudaStreamPerThread);
+    ocg::dev::narrow_i32(K->jt_e.p, njt, K->jt_e32.p, cudaStreamPerThread);
+    ocg::dev::narrow_i32(K->jt_dual.p, njt, K->jt_dual32.p, cudaStreamPerThread);
+  }
+  // tiled assembly: one source stream per COO group of hess and jac, and sigma
+  if (K->src_code32.p && !(std::getenv("OCG_KKT_TILED") && std::atoi(std::getenv("OCG_KKT_TILED")) == 0)) {
+    const ocg::Layout& lay = e->lay;
+    std::vector<int64_t> sb;
+    for (Index o : lay.hess_off_con) sb.push_back(o);
+    for (Index o : lay.hess_off_obj) sb.push_back(o);
+    for (Index o : lay.jac_off) sb.push_back(K->H + o);
+    sb.push_back(K->H + K->J + K->n_slack);
+    sb.push_back(K->H + K->J + K->n_slack + K->ntot);
+    bool sorted = std::is_sorted(sb.begin(), sb.end()) && !sb.empty() && sb.front() == 0;
+    if (sorted) {
+      K->t_sb.alloc(sb.size());
+      ck(cudaMemcpyAsync(K->t_sb.p, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, cudaStreamPerThread),
+         "stream bounds");
+      ocg::dev::KktTiles t;
+      const Index ncode = static_cast<Index>(K->src_code.n);
+      if (ocg::dev::kkt_tile_plan(K->src_code32.p, K->src_ptr.p, K->src_code.p, K->nnz, ncode, K->t_sb.p,
+                                  static_cast<int>(sb.size()) - 1, K->H, K->J, K->n_slack, K->ntot, t,
+                                  cudaStreamPerThread)) {
+        const size_t nw = static_cast<size_t>(t.ntile) * static_cast<size_t>(t.ns);
+        K->t_wlo.adopt(t.wlo, nw);
+        K->t_wlen.adopt(t.wlen, nw);
+        K->t_woff.adopt(t.woff, nw);
+        K->t_code32.adopt(t.code32, static_cast<size_t>(K->nnz));
+        K->t_mcode.adopt(t.mcode, static_cast<size_t>(std::max<Index>(1, ncode)));
+        K->tiles = t;
+      }
+    }
+  }
   K->val.alloc(static_cast<size_t>(K->nnz));
   ck(cudaMemsetAsync(K->val.p, 0, static_cast<size_t>(K->nnz) * sizeof(double), cudaStreamPerThread), "memset");
   ck(cudaStreamSynchronize(cudaStreamPerThread), "sync");
@@ -1201,9 +1246,13 @@ int ocg_kkt_assemble(ocg_kkt* k, const double* sigma, ocg_stream s) {
   if (!k || !sigma) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(k->ev->device);
-  ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
-                         k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s), k->src_code32.p,
-                         k->src_order.p);
+  if (k->tiles.ntile > 0)
+    ocg::dev::kkt_assemble_tiled(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
+                                 k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, k->tiles, st(s));
+  else
+    ocg::dev::kkt_assemble(k->ev->hess.p, k->ev->jac.p, sigma, k->src_ptr.p, k->src_code.p, k->nnz, k->H, k->J,
+                           k->n_slack, k->ntot, k->val.p, {k->src_long.p, k->n_src_long}, st(s), k->src_code32.p,
+                           k->src_order.p);
   k->ev->launches += k->n_src_long > 0 ? 2 : 1;
   return OCG_OK;
   OCG_GUARD_END
@@ -1213,8 +1262,12 @@ int ocg_kkt_matvec(ocg_kkt* k, const double* x, double* y, ocg_stream s) {
   if (!k || !x || !y) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(k->ev->device);
-  ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y,
-                       {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  if (k->mv_col32.p)
+    ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col32.p, k->mv_vidx32.p, k->dim, x, y,
+                         {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  else
+    ocg::dev::sym_matvec(k->val.p, k->mv_ptr.p, k->mv_col.p, k->mv_vidx.p, k->dim, x, y,
+                         {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
   k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END
@@ -1224,8 +1277,12 @@ int ocg_kkt_norm_inf(ocg_kkt* k, double* out, ocg_stream s) {
   if (!k || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(k->ev->device);
-  ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out,
-                         {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  if (k->mv_vidx32.p)
+    ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx32.p, k->dim, out,
+                           {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
+  else
+    ocg::dev::sym_norm_inf(k->val.p, k->mv_ptr.p, k->mv_vidx.p, k->dim, out,
+                           {k->mv_long.p, k->n_mv_long, k->mv_long_part.p}, st(s));
   k->ev->launches += k->n_mv_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END
@@ -1235,8 +1292,12 @@ int ocg_kkt_jt_lambda(ocg_kkt* k, const double* lambda, double* out, ocg_stream 
   if (!k || !lambda || !out) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN
   ocg::mem::DeviceScope ds_(k->ev->device);
-  ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
-                      k->n_slack, out, {k->jt_long.p, k->n_jt_long, k->jt_long_part.p}, st(s));
+  if (k->jt_e32.p)
+    ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e32.p, k->jt_dual32.p, k->n_free, k->jt_slack_dual.p,
+                        k->n_slack, out, {k->jt_long.p, k->n_jt_long, k->jt_long_part.p}, st(s));
+  else
+    ocg::dev::jt_lambda(k->ev->jac.p, lambda, k->jt_ptr.p, k->jt_e.p, k->jt_dual.p, k->n_free, k->jt_slack_dual.p,
+                        k->n_slack, out, {k->jt_long.p, k->n_jt_long, k->jt_long_part.p}, st(s));
   k->ev->launches += k->n_jt_long > 0 ? 3 : 1;
   return OCG_OK;
   OCG_GUARD_END

@@ -17,6 +17,7 @@
 #include "band.hpp"
 #include "devmem.hpp"
 #include "jit.hpp"
+#include "kernels.hpp"
 #include "model.hpp"
 #include "plan.hpp"
 #include "refldl.hpp"
@@ -191,11 +192,18 @@ struct ocg_kkt {
   DBuf<int64_t> src_ptr, src_code;
   DBuf<uint32_t> src_code32;  // per slot in source order: (tag << 29) | index (kernels.hpp kkt_code32)
   DBuf<int32_t> src_order;    // slots in order of their first source (kktbuild.hpp source_order)
+  // tiled assembly (kernels.hpp KktTiles): per-tile source windows, rewritten codes
+  ocg::dev::KktTiles tiles;
+  DBuf<int64_t> t_sb, t_wlo;
+  DBuf<int32_t> t_wlen, t_woff;
+  DBuf<uint32_t> t_code32, t_mcode;
   Index H = 0, J = 0;
   // matvec (full symmetric CSR in increasing column order)
   DBuf<int64_t> mv_ptr, mv_col, mv_vidx;
   // J^T lambda
   DBuf<int64_t> jt_ptr, jt_e, jt_dual, jt_slack_dual;
+  // 32-bit copies of the matvec and J^T lambda index arrays (when their values fit)
+  DBuf<int32_t> mv_col32, mv_vidx32, jt_e32, jt_dual32;
   // rows of src_ptr / mv_ptr / jt_ptr longer than kLongRow (kernels.hpp)
   DBuf<int64_t> src_long, mv_long, jt_long;
   int64_t n_src_long = 0, n_mv_long = 0, n_jt_long = 0;

@@ -3,6 +3,8 @@
 // mirrors. All of them are HBM-bound streaming/gather kernels; grids are
 // sized in multiples of the 148 SMs x resident blocks.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.hpp"
@@ -188,9 +190,247 @@ __global__ void __launch_bounds__(256) kkt_assemble_fast_k(const double* __restr
   }
 }
 
+// ---- tiled assembly (kkt_tile_*): a block owns kTileSlots consecutive slots;
+// the sources its slots read from each source stream (one per COO group of
+// hess / jac, and sigma) form one window [lo, lo + len) that the block copies
+// into shared memory with coalesced loads, so every source byte leaves DRAM
+// about once; slot codes then address shared memory (tag kTagSmem). Windows
+// too sparse or too large for the block's budget stay in global memory.
+constexpr uint32_t kTagSmem = 5;
+// a slot with 2..kMultiMax sources whose codes sit in the tile's staged copy
+// of mcode: (count << kMultiShift) | offset from the tile's first code
+constexpr uint32_t kTagMultiLocal = 6;
+constexpr uint32_t kMultiShift = 24, kMultiMax = 31;
+
+__device__ __forceinline__ int stream_of(const int64_t* __restrict__ sb, int ns, int64_t c) {
+  int lo = 0, hi = ns;  // sb[0..ns]: stream s covers [sb[s], sb[s+1])
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(sb + mid) <= c) lo = mid; else hi = mid;
+  }
+  return (c >= __ldg(sb) && c < __ldg(sb + ns)) ? lo : -1;
+}
+
+// unified code of a compact single-source word (-1: no data: constants, multi)
+__device__ __forceinline__ int64_t unified_of(uint32_t w, int64_t H, int64_t HJS) {
+  const uint32_t tag = w >> kTagShift, i = w & kIdxMask;
+  if (tag == kTagHess) return i;
+  if (tag == kTagJac) return H + i;
+  if (tag == kTagSigma) return HJS + i;
+  return -1;
+}
+__device__ __forceinline__ uint32_t word_of(int64_t c, int64_t H, int64_t J, int64_t S, int64_t ntot) {
+  const int64_t HJ = H + J, HJS = HJ + S;
+  if (c < H) return (kTagHess << kTagShift) | static_cast<uint32_t>(c);
+  if (c < HJ) return (kTagJac << kTagShift) | static_cast<uint32_t>(c - H);
+  if (c < HJS) return kTagMinus1 << kTagShift;
+  if (c < HJS + ntot) return (kTagSigma << kTagShift) | static_cast<uint32_t>(c - HJS);
+  return kTagZero << kTagShift;
+}
+
+__global__ void __launch_bounds__(256) kkt_tile_minmax_k(const uint32_t* __restrict__ code32,
+                                                         const int64_t* __restrict__ ptr,
+                                                         const int64_t* __restrict__ code, int64_t nnz,
+                                                         const int64_t* __restrict__ sb, int ns, int64_t H,
+                                                         int64_t J, int64_t S, unsigned long long* __restrict__ mn,
+                                                         unsigned long long* __restrict__ mx,
+                                                         unsigned int* __restrict__ cnt) {
+  const int64_t HJS = H + J + S;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = p / kTileSlots;
+    const uint32_t w = code32[p];
+    auto note = [&](int64_t c) {
+      const int st = c >= 0 ? stream_of(sb, ns, c) : -1;
+      if (st < 0) return;
+      atomicMin(mn + t * ns + st, static_cast<unsigned long long>(c));
+      atomicMax(mx + t * ns + st, static_cast<unsigned long long>(c));
+      atomicAdd(cnt + t * ns + st, 1u);
+    };
+    if ((w >> kTagShift) == kTagMulti) {
+      if (is_long(ptr, p)) continue;
+      for (int64_t q = ptr[p]; q < ptr[p + 1]; ++q) {
+        const int64_t c = code[q];
+        if (c < H + J || (c >= HJS)) note(c);
+      }
+    } else {
+      note(unified_of(w, H, HJS));
+    }
+  }
+}
+
+// one thread per tile: window lengths and shared-memory offsets; a window is
+// staged when it is dense (len <= kTileSparse * the sources read from it +
+// 32) and fits the block's budget
+__global__ void kkt_tile_plan_k(const unsigned long long* __restrict__ mn, const unsigned long long* __restrict__ mx,
+                                const unsigned int* __restrict__ cnt,
+                                int64_t ntile, int ns, int64_t nnz, int64_t* __restrict__ wlo,
+                                int32_t* __restrict__ wlen, int32_t* __restrict__ woff) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ntile) return;
+  int32_t off = kTileConsts;  // win[0] = -1.0, win[1] = 0.0
+  for (int st = 0; st < ns; ++st) {
+    const unsigned long long a = mn[t * ns + st], b = mx[t * ns + st];
+    int32_t len = 0;
+    if (b >= a && b != ~0ull) {
+      const int64_t l = static_cast<int64_t>(b - a) + 1;
+      if (l <= static_cast<int64_t>(kTileSparse) * cnt[t * ns + st] + 32 && off + l + 2 <= kTileWindow)
+        len = static_cast<int32_t>(l);
+    }
+    wlo[t * ns + st] = static_cast<int64_t>(a);
+    wlen[t * ns + st] = len;
+    woff[t * ns + st] = off;
+    off += len + (len & 1);
+  }
+}
+
+// rewrite the codes of staged sources to shared-memory offsets
+__global__ void __launch_bounds__(256) kkt_tile_codes_k(uint32_t* __restrict__ code32, const int64_t* __restrict__ ptr,
+                                                        const int64_t* __restrict__ code, uint32_t* __restrict__ mcode,
+                                                        int64_t nnz, const int64_t* __restrict__ sb, int ns,
+                                                        const int64_t* __restrict__ wlo, const int32_t* __restrict__ wlen,
+                                                        const int32_t* __restrict__ woff, int64_t H, int64_t J,
+                                                        int64_t S, int64_t ntot) {
+  const int64_t HJS = H + J + S;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = p / kTileSlots;
+    auto staged = [&](int64_t c, uint32_t& w) {
+      const int st = c >= 0 ? stream_of(sb, ns, c) : -1;
+      if (st < 0) return;
+      const int64_t k = t * ns + st;
+      if (wlen[k] > 0) w = (kTagSmem << kTagShift) | static_cast<uint32_t>(woff[k] + (c - wlo[k]));
+    };
+    auto consts = [](uint32_t& w) {
+      if ((w >> kTagShift) == kTagMinus1) w = (kTagSmem << kTagShift) | 0u;
+      if ((w >> kTagShift) == kTagZero) w = (kTagSmem << kTagShift) | 1u;
+    };
+    uint32_t w = code32[p];
+    if ((w >> kTagShift) == kTagMulti) {
+      if (is_long(ptr, p)) continue;
+      for (int64_t q = ptr[p]; q < ptr[p + 1]; ++q) {
+        const int64_t c = code[q];
+        uint32_t mw = word_of(c, H, J, S, ntot);
+        if (c < H + J || c >= HJS) staged(c, mw);
+        consts(mw);
+        mcode[q] = mw;
+      }
+      const int64_t n = ptr[p + 1] - ptr[p], off = ptr[p] - ptr[t * kTileSlots];
+      if (n <= kMultiMax && off < (int64_t{1} << kMultiShift))
+        code32[p] = (kTagMultiLocal << kTagShift) | (static_cast<uint32_t>(n) << kMultiShift) | static_cast<uint32_t>(off);
+    } else {
+      staged(unified_of(w, H, HJS), w);
+      consts(w);
+      code32[p] = w;
+    }
+  }
+}
+
+__device__ __forceinline__ double tile_fetch(uint32_t w, const double* __restrict__ win, const double* __restrict__ hess,
+                                             const double* __restrict__ jac, const double* __restrict__ sigma) {
+  const uint32_t tag = w >> kTagShift, i = w & kIdxMask;
+  switch (tag) {
+    case kTagSmem: return win[i];
+    case kTagHess: return __ldg(hess + i);
+    case kTagJac: return __ldg(jac + i);
+    case kTagSigma: return __ldg(sigma + i);
+    case kTagMinus1: return -1.0;
+    default: return 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) kkt_assemble_tiled_k(const double* __restrict__ hess,
+                                                            const double* __restrict__ jac,
+                                                            const double* __restrict__ sigma,
+                                                            const uint32_t* __restrict__ code32,
+                                                            const int64_t* __restrict__ ptr,
+                                                            const uint32_t* __restrict__ mcode, int64_t nnz,
+                                                            int ns, const int64_t* __restrict__ wlo,
+                                                            const int32_t* __restrict__ wlen,
+                                                            const int32_t* __restrict__ woff, int64_t H, int64_t J,
+                                                            int64_t S, double* __restrict__ val) {
+  extern __shared__ __align__(16) double win[];
+  constexpr int kPer = static_cast<int>(kTileSlots / 256);  // slots per thread (blockDim.x == 256)
+  const int64_t t = blockIdx.x;
+  const int64_t HJS = H + J + S;
+  const int64_t p0 = t * kTileSlots;
+  // the tile's codes first (one DRAM round trip for all of them) ...
+  uint32_t w[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int64_t p = p0 + j * 256 + threadIdx.x;
+    w[j] = p < nnz ? __ldg(code32 + p) : (kTagZero << kTagShift);
+  }
+  // ... while the tile's window table comes in (one load per stream, all in
+  // flight together) ...
+  __shared__ int64_t s_lo[kTileMaxStreams];
+  __shared__ int32_t s_len[kTileMaxStreams], s_off[kTileMaxStreams];
+  for (int st = threadIdx.x; st < ns; st += blockDim.x) {
+    s_lo[st] = wlo[t * ns + st];
+    s_len[st] = wlen[t * ns + st];
+    s_off[st] = woff[t * ns + st];
+  }
+  __syncthreads();
+  // ... and then the windows: warp w copies windows w, w + 8, ... (LDGSTS,
+  // coalesced; every copy of the tile in flight together, one wait)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int st = warp; st < ns; st += 8) {
+    const int32_t len = s_len[st];
+    if (len == 0) continue;
+    const int64_t lo = s_lo[st];
+    const double* src = lo < H ? hess + lo : (lo < H + J ? jac + (lo - H) : sigma + (lo - HJS));
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + s_off[st]));
+    for (int32_t i = lane; i < len; i += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * static_cast<unsigned>(i)), "l"(src + i)
+                   : "memory");
+  }
+  // the codes of the tile's multi-source slots (one contiguous range of mcode)
+  const int64_t q0 = __ldg(ptr + p0), q1 = __ldg(ptr + min(nnz, p0 + kTileSlots));
+  const int nq = static_cast<int>(q1 - q0 < kTileMcode ? q1 - q0 : kTileMcode);
+  uint32_t* const mloc = reinterpret_cast<uint32_t*>(win + kTileWindow);
+  for (int i = threadIdx.x; i < nq; i += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(mloc + i))),
+                 "l"(mcode + q0 + i)
+                 : "memory");
+  if (threadIdx.x == 0) {
+    win[0] = -1.0;
+    win[1] = 0.0;
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int64_t p = p0 + j * 256 + threadIdx.x;
+    if (p >= nnz) break;
+    const uint32_t tag = w[j] >> kTagShift;
+    double s;
+    if (tag == kTagSmem) {
+      s = win[w[j] & kIdxMask];
+    } else if (tag == kTagMultiLocal) {
+      const uint32_t off = w[j] & ((1u << kMultiShift) - 1);
+      const int n = static_cast<int>((w[j] >> kMultiShift) & kMultiMax);
+      // codes staged (or, past the staged range, from global memory)
+      const uint32_t* c = static_cast<int>(off) + n <= nq ? mloc + off : mcode + q0 + off;
+      s = 0.0;  // the reference's order
+      for (int i = 0; i < n; ++i) {
+        const uint32_t cw = c[i];
+        s += (cw >> kTagShift) == kTagSmem ? win[cw & kIdxMask] : tile_fetch(cw, win, hess, jac, sigma);
+      }
+    } else if (tag != kTagMulti) {
+      s = tile_fetch(w[j], win, hess, jac, sigma);
+    } else {  // more than kMultiMax sources (long rows: kkt_assemble_long_k)
+      if (is_long(ptr, p)) continue;
+      s = 0.0;
+      for (int64_t q = ptr[p]; q < ptr[p + 1]; ++q) s += tile_fetch(__ldg(mcode + q), win, hess, jac, sigma);
+    }
+    val[p] = s;
+  }
+}
+
+template <class I>
 __global__ void __launch_bounds__(256) sym_matvec_k(const double* __restrict__ val, const int64_t* __restrict__ rptr,
-                                                    const int64_t* __restrict__ col,
-                                                    const int64_t* __restrict__ vidx, int64_t n,
+                                                    const I* __restrict__ col,
+                                                    const I* __restrict__ vidx, int64_t n,
                                                     const double* __restrict__ x, double* __restrict__ y) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -202,8 +442,9 @@ __global__ void __launch_bounds__(256) sym_matvec_k(const double* __restrict__ v
 }
 
 // max over rows of sum_j |K_ij| with the symmetric mirror (sparse::norm_inf_sym)
+template <class I>
 __global__ void __launch_bounds__(256) sym_norm_inf_k(const double* __restrict__ val, const int64_t* __restrict__ rptr,
-                                                      const int64_t* __restrict__ vidx, int64_t n,
+                                                      const I* __restrict__ vidx, int64_t n,
                                                       unsigned long long* __restrict__ out) {
   double m = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -223,9 +464,10 @@ __global__ void __launch_bounds__(256) sym_norm_inf_k(const double* __restrict__
   }
 }
 
+template <class I>
 __global__ void __launch_bounds__(256) jt_lambda_k(const double* __restrict__ jac, const double* __restrict__ lam,
-                                                   const int64_t* __restrict__ ptr, const int64_t* __restrict__ e_idx,
-                                                   const int64_t* __restrict__ dual_idx, int64_t n_free,
+                                                   const int64_t* __restrict__ ptr, const I* __restrict__ e_idx,
+                                                   const I* __restrict__ dual_idx, int64_t n_free,
                                                    const int64_t* __restrict__ slack_dual, int64_t n_slack,
                                                    double* __restrict__ out) {
   const int64_t ntot = n_free + n_slack;
@@ -373,28 +615,31 @@ __global__ void __launch_bounds__(256) kkt_assemble_long_k(const double* __restr
   if (threadIdx.x == 0) val[p] = s;
 }
 
+template <class I>
 __global__ void __launch_bounds__(256) sym_matvec_long_k(const double* __restrict__ val,
                                                          const int64_t* __restrict__ rptr,
-                                                         const int64_t* __restrict__ col,
-                                                         const int64_t* __restrict__ vidx, LongRows lr,
+                                                         const I* __restrict__ col,
+                                                         const I* __restrict__ vidx, LongRows lr,
                                                          const double* __restrict__ x) {
   const int64_t r = blockIdx.y, i = lr.idx[r];
   tree_block_partial(rptr[i], rptr[i + 1], [&](int64_t p) { return val[vidx[p]] * x[col[p]]; },
                      lr.partials + r * kLongBlocks + blockIdx.x);
 }
 
+template <class I>
 __global__ void __launch_bounds__(256) sym_norm_inf_long_k(const double* __restrict__ val,
                                                            const int64_t* __restrict__ rptr,
-                                                           const int64_t* __restrict__ vidx, LongRows lr) {
+                                                           const I* __restrict__ vidx, LongRows lr) {
   const int64_t r = blockIdx.y, i = lr.idx[r];
   tree_block_partial(rptr[i], rptr[i + 1], [&](int64_t p) { return fabs(val[vidx[p]]); },
                      lr.partials + r * kLongBlocks + blockIdx.x);
 }
 
+template <class I>
 __global__ void __launch_bounds__(256) jt_lambda_long_k(const double* __restrict__ jac, const double* __restrict__ lam,
                                                         const int64_t* __restrict__ ptr,
-                                                        const int64_t* __restrict__ e_idx,
-                                                        const int64_t* __restrict__ dual_idx, LongRows lr) {
+                                                        const I* __restrict__ e_idx,
+                                                        const I* __restrict__ dual_idx, LongRows lr) {
   const int64_t r = blockIdx.y, i = lr.idx[r];
   tree_block_partial(ptr[i], ptr[i + 1], [&](int64_t p) { return jac[e_idx[p]] * lam[dual_idx[p]]; },
                      lr.partials + r * kLongBlocks + blockIdx.x);
@@ -456,7 +701,74 @@ void kkt_assemble(const double* hess, const double* jac, const double* sigma, co
                                                                    val);
 }
 
-void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
+bool kkt_tile_plan(const uint32_t* code32_in, const int64_t* ptr, const int64_t* code, int64_t nnz, int64_t ncode,
+                   const int64_t* stream_bounds_dev, int ns, int64_t H, int64_t J, int64_t S, int64_t ntot,
+                   KktTiles& out, cudaStream_t s) {
+  if (!code32_in || nnz <= 0 || ns <= 0 || ns > kTileMaxStreams) return false;
+  const int64_t ntile = (nnz + kTileSlots - 1) / kTileSlots;
+  const size_t nw = static_cast<size_t>(ntile) * static_cast<size_t>(ns);
+  unsigned long long *mn = nullptr, *mx = nullptr;
+  unsigned int* cnt = nullptr;
+  if (cudaMallocAsync(&mn, nw * 8, s) != cudaSuccess || cudaMallocAsync(&mx, nw * 8, s) != cudaSuccess ||
+      cudaMallocAsync(&cnt, nw * 4, s) != cudaSuccess)
+    return false;
+  cudaMemsetAsync(mn, 0xff, nw * 8, s);
+  cudaMemsetAsync(mx, 0, nw * 8, s);
+  cudaMemsetAsync(cnt, 0, nw * 4, s);
+  // "max" starts at 0 and "min" at ~0: an untouched window has mx < mn
+  kkt_tile_minmax_k<<<grid_for(nnz, 256), 256, 0, s>>>(code32_in, ptr, code, nnz, stream_bounds_dev, ns, H, J, S, mn,
+                                                       mx, cnt);
+  cudaMallocAsync(&out.wlo, nw * sizeof(int64_t), s);
+  cudaMallocAsync(&out.wlen, nw * sizeof(int32_t), s);
+  cudaMallocAsync(&out.woff, nw * sizeof(int32_t), s);
+  cudaMallocAsync(&out.code32, static_cast<size_t>(nnz) * sizeof(uint32_t), s);
+  cudaMallocAsync(&out.mcode, static_cast<size_t>(std::max<int64_t>(1, ncode)) * sizeof(uint32_t), s);
+  kkt_tile_plan_k<<<static_cast<unsigned>((ntile + 127) / 128), 128, 0, s>>>(mn, mx, cnt, ntile, ns, nnz, out.wlo, out.wlen,
+                                                                             out.woff);
+  cudaMemcpyAsync(out.code32, code32_in, static_cast<size_t>(nnz) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+  kkt_tile_codes_k<<<grid_for(nnz, 256), 256, 0, s>>>(out.code32, ptr, code, out.mcode, nnz, stream_bounds_dev, ns,
+                                                      out.wlo, out.wlen, out.woff, H, J, S, ntot);
+  if (std::getenv("OCG_KKT_TILE_STATS")) {  // diagnostic: where the slots' sources come from
+    std::vector<uint32_t> c(static_cast<size_t>(nnz));
+    std::vector<int32_t> len(nw);
+    cudaMemcpyAsync(c.data(), out.code32, c.size() * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(len.data(), out.wlen, len.size() * 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    int64_t tags[8] = {0};
+    for (uint32_t w : c) ++tags[w >> kTagShift];
+    int64_t staged = 0, windows = 0;
+    for (int32_t l : len) { staged += l; windows += l > 0; }
+    std::fprintf(stderr, "[kkt_tile] nnz %lld tiles %lld streams %d: smem %lld hess %lld jac %lld sigma %lld -1 %lld 0 %lld multi %lld; staged %lld doubles in %lld windows (%.2f per slot)\n",
+                 (long long)nnz, (long long)ntile, ns, (long long)tags[kTagSmem], (long long)tags[kTagHess],
+                 (long long)tags[kTagJac], (long long)tags[kTagSigma], (long long)tags[kTagMinus1], (long long)tags[kTagZero],
+                 (long long)tags[kTagMulti], (long long)staged, (long long)windows, double(staged) / double(nnz));
+  }
+  cudaFreeAsync(mn, s);
+  cudaFreeAsync(mx, s);
+  cudaFreeAsync(cnt, s);
+  out.ntile = ntile;
+  out.ns = ns;
+  return cudaGetLastError() == cudaSuccess;
+}
+
+void kkt_assemble_tiled(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
+                        const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
+                        LongRows lr, const KktTiles& t, cudaStream_t s) {
+  if (nnz <= 0) return;
+  static bool attr = [] {
+    return cudaFuncSetAttribute(kkt_assemble_tiled_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kTileWindow * static_cast<int>(sizeof(double)) + kTileMcode * 4) == cudaSuccess;
+  }();
+  (void)attr;
+  kkt_assemble_tiled_k<<<static_cast<unsigned>(t.ntile), 256, kTileWindow * sizeof(double) + kTileMcode * 4, s>>>(
+      hess, jac, sigma, t.code32, ptr, t.mcode, nnz, t.ns, t.wlo, t.wlen, t.woff, H, J, S, val);
+  if (lr.n > 0)
+    kkt_assemble_long_k<<<static_cast<unsigned>(lr.n), 256, 0, s>>>(hess, jac, sigma, ptr, code, lr, H, J, S, ntot,
+                                                                   val);
+}
+
+template <class I>
+void sym_matvec(const double* val, const int64_t* rptr, const I* col, const I* vidx, int64_t n,
                 const double* x, double* y, LongRows lr, cudaStream_t s) {
   if (n <= 0) return;
   sym_matvec_k<<<grid_for(n, 256), 256, 0, s>>>(val, rptr, col, vidx, n, x, y);
@@ -466,7 +778,8 @@ void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, cons
   }
 }
 
-void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out, LongRows lr,
+template <class I>
+void sym_norm_inf(const double* val, const int64_t* rptr, const I* vidx, int64_t n, double* out, LongRows lr,
                   cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(double), s);
   if (n <= 0) return;
@@ -477,8 +790,9 @@ void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, i
   }
 }
 
-void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
-               const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
+template <class I>
+void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const I* e_idx,
+               const I* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
                LongRows lr, cudaStream_t s) {
   const int64_t n = n_free + n_slack;
   if (n <= 0) return;
@@ -607,6 +921,31 @@ void row_max_node(const int64_t* row, const int64_t* col, int64_t n, const int64
   if (n > 0)
     row_max_node_k<<<grid_n(n), 256, 0, s>>>(row, col, n, col_node, reinterpret_cast<unsigned long long*>(node));
   if (m > 0) minus_one_k<<<grid_n(m), 256, 0, s>>>(reinterpret_cast<unsigned long long*>(node), m);
+}
+
+template void sym_matvec<int64_t>(const double*, const int64_t*, const int64_t*, const int64_t*, int64_t, const double*,
+                                   double*, LongRows, cudaStream_t);
+template void sym_matvec<int32_t>(const double*, const int64_t*, const int32_t*, const int32_t*, int64_t, const double*,
+                                   double*, LongRows, cudaStream_t);
+template void sym_norm_inf<int64_t>(const double*, const int64_t*, const int64_t*, int64_t, double*, LongRows,
+                                     cudaStream_t);
+template void sym_norm_inf<int32_t>(const double*, const int64_t*, const int32_t*, int64_t, double*, LongRows,
+                                     cudaStream_t);
+template void jt_lambda<int64_t>(const double*, const double*, const int64_t*, const int64_t*, const int64_t*, int64_t,
+                                  const int64_t*, int64_t, double*, LongRows, cudaStream_t);
+template void jt_lambda<int32_t>(const double*, const double*, const int64_t*, const int32_t*, const int32_t*, int64_t,
+                                  const int64_t*, int64_t, double*, LongRows, cudaStream_t);
+
+namespace {
+__global__ void narrow_k(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(in[i]);
+}
+}  // namespace
+
+void narrow_i32(const int64_t* in, int64_t n, int32_t* out, cudaStream_t s) {
+  if (n > 0) narrow_k<<<grid_for(n, 256), 256, 0, s>>>(in, n, out);
 }
 
 }  // namespace ocg::dev

@@ -22,7 +22,7 @@ namespace ocg::dev {
 // array (long_rows() on its host copy); `partials`: device scratch of
 // n * kLongBlocks doubles for the tree kernels.
 constexpr int64_t kLongRow = 1024;
-constexpr int kLongBlocks = 64;
+constexpr int kLongBlocks = 296;  // two blocks per SM for each long row
 struct LongRows {
   const int64_t* idx = nullptr;
   int64_t n = 0;
@@ -64,23 +64,54 @@ void kkt_assemble(const double* hess, const double* jac, const double* sigma, co
                   LongRows lr, cudaStream_t s, const uint32_t* code32 = nullptr, const int32_t* order = nullptr);
 // per slot: (array tag << 29) | index for a single source, a "several" tag
 // otherwise; false (nothing written) when an index does not fit 29 bits
+// Tiled assembly: a block owns kTileSlots consecutive K slots and stages the
+// sources they read from each source stream (the COO segment of one hess /
+// jac group, or sigma) into shared memory as one window with coalesced
+// loads; slot codes address the window. kkt_tile_plan builds the windows and
+// the rewritten codes on the device (stream_bounds: ns+1 ascending unified
+// codes, hess [0,H), jac [H,H+J), sigma [H+J+S, ...)); same sums, same order.
+constexpr int64_t kTileSlots = 1024;
+constexpr int kTileWindow = 2560;  // doubles of shared memory per block (20 KB)
+constexpr int kTileMaxStreams = 256;
+constexpr int kTileConsts = 2;  // win[0] = -1.0 (slack entries), win[1] = 0.0 (structural zeros)  // source streams (COO groups + sigma) the tiled path takes
+constexpr int kTileMcode = 2048;   // codes of the tile's multi-source slots staged (uint32)
+constexpr int kTileSparse = 5;     // a window is staged when len <= kTileSparse * (sources read from it) + 32
+struct KktTiles {
+  int64_t ntile = 0;
+  int ns = 0;
+  int64_t* wlo = nullptr;
+  int32_t *wlen = nullptr, *woff = nullptr;
+  uint32_t *code32 = nullptr, *mcode = nullptr;
+};
+bool kkt_tile_plan(const uint32_t* code32, const int64_t* ptr, const int64_t* code, int64_t nnz, int64_t ncode,
+                   const int64_t* stream_bounds_dev, int ns, int64_t H, int64_t J, int64_t S, int64_t ntot,
+                   KktTiles& out, cudaStream_t s);
+void kkt_assemble_tiled(const double* hess, const double* jac, const double* sigma, const int64_t* ptr,
+                        const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot, double* val,
+                        LongRows lr, const KktTiles& t, cudaStream_t s);
 bool kkt_code32(const int64_t* ptr, const int64_t* code, int64_t nnz, int64_t H, int64_t J, int64_t S, int64_t ntot,
                 uint32_t* out, cudaStream_t s);
 
 // y[i] = sum over the full symmetric row i (increasing column) of K_ij x_j —
 // the accumulation order of sparse::matvec_sym (sparse.cpp:51-61).
-void sym_matvec(const double* val, const int64_t* rptr, const int64_t* col, const int64_t* vidx, int64_t n,
+// (I = int64_t, or int32_t for the narrowed index copies)
+template <class I>
+void sym_matvec(const double* val, const int64_t* rptr, const I* col, const I* vidx, int64_t n,
                 const double* x, double* y, LongRows lr, cudaStream_t s);
 
 // *out = max_i sum_j |K_ij| over the full symmetric rows (sparse::norm_inf_sym)
-void sym_norm_inf(const double* val, const int64_t* rptr, const int64_t* vidx, int64_t n, double* out, LongRows lr,
+template <class I>
+void sym_norm_inf(const double* val, const int64_t* rptr, const I* vidx, int64_t n, double* out, LongRows lr,
                   cudaStream_t s);
 
 // out[i] = sum_p jac[e_p] * lam[dual_p] (p in increasing e), then for slack
 // rows out[i] -= lam[dual] (Solver::compute_jt_lambda, solver.cpp:244-257).
-void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const int64_t* e_idx,
-               const int64_t* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
+template <class I>
+void jt_lambda(const double* jac, const double* lam, const int64_t* ptr, const I* e_idx,
+               const I* dual_idx, int64_t n_free, const int64_t* slack_dual, int64_t n_slack, double* out,
                LongRows lr, cudaStream_t s);
+// out[i] = (int32) in[i] (index arrays whose values fit 32 bits)
+void narrow_i32(const int64_t* in, int64_t n, int32_t* out, cudaStream_t s);
 
 // max |v| over n entries into *out (device scalar); exact.
 void max_abs(const double* v, int64_t n, double* out, cudaStream_t s);
