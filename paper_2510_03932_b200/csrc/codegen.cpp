@@ -1425,7 +1425,10 @@ __device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long l
     // global memory has no copy-out barrier)
     E.line("__syncwarp();");
     E.close();  // tile loop
-    E.line("ocg_bulk_wait_all();  // bulk copies done before the block exits");
+    // the block's shared memory must outlive the bulk copies' reads; their
+    // global writes complete with the grid (as a TMA-store epilogue's
+    // wait_group.read 0 before exit)
+    E.line("ocg_bulk_wait_read();");
 
     if (!tails.empty()) {
       E.open("if (blockIdx.x == gridDim.x - 1)");
