@@ -395,6 +395,15 @@ __device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long l
   Index smem_out_ = 0;  // dynamic shared memory (bytes) of the last kernel
   // finiteness accumulator the checks of the code being emitted go to
   std::string acc_ = "okacc";
+  // a group's checks rotate over kAccChains independent accumulators
+  // (acc_ + "_0" ...), so the finiteness DFMAs form short chains instead of
+  // one serial chain through the whole group
+  static constexpr int kAccChains = 4;
+  int acc_chains_ = 1, acc_rr_ = 0;
+  std::string acc_next() {
+    if (acc_chains_ <= 1) return acc_;
+    return acc_ + "_" + std::to_string(acc_rr_++ % acc_chains_);
+  }
   // called before every shared-memory store of the current group with the
   // output kind: emits the waits/flushes of the staged copy-out
   std::function<void(int)> store_hook_;
@@ -748,9 +757,11 @@ __device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long l
           case Op::pow: {
             const V s = E.mul(K(nd.c * (nd.c - 1.0)), E.powc(f.v[ia], nd.c - 2.0));
             p1d = E.mul(s, dv[ia]);
-            if (!ak.zero() && !s.is_c)
-              E.line(acc_ + " = (fin(" + E.s(s) + ") | (" + E.s(ak) + " == 0.0)) ? " + acc_ +
+            if (!ak.zero() && !s.is_c) {
+              const std::string acc = acc_next();
+              E.line(acc + " = (fin(" + E.s(s) + ") | (" + E.s(ak) + " == 0.0)) ? " + acc +
                      " : __longlong_as_double(0x7ff8000000000000LL);");
+            }
             break;
           }
           default: break;
@@ -773,7 +784,10 @@ __device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long l
 
   // finiteness: one DFMA per checked value (v*0 is NaN iff v is not finite)
   void check_inline(Emitter& E, V v) {
-    if (!v.is_c) E.line(acc_ + " = __fma_rn(" + E.s(v) + ", 0.0, " + acc_ + ");");
+    if (!v.is_c) {
+      const std::string a = acc_next();
+      E.line(a + " = __fma_rn(" + E.s(v) + ", 0.0, " + a + ");");
+    }
   }
 
   // integer literal of the kernel's index type (OIX: int when every array
@@ -1335,14 +1349,25 @@ __device__ __forceinline__ void ocg_bulk_load(double* p, const double* g, long l
              std::to_string(mb.gi) + ": " + g.label);
       E.line("const bool p" + qs + " = in && idx >= " + lo + " && idx < " + hi + ";");
       store_pred_ = "p" + qs;
-      E.line("double okg" + qs + " = 0.0;");
+      {
+        std::string decl = "double okg" + qs + "_0 = 0.0";
+        for (int a = 1; a < kAccChains; ++a) decl += ", okg" + qs + "_" + std::to_string(a) + " = 0.0";
+        E.line(decl + ";");
+      }
       acc_ = "okg" + qs;
+      acc_chains_ = kAccChains;
+      acc_rr_ = 0;
       std::vector<Check> sc;
       Fwd f = forward(E, g, "idx", false, p.partials, 0, sc);
       for (const auto& c : sc) check_inline(E, c.v);
       group_body(E, m, mb.objective, mb.gi, f, "(idx - " + lo + ")");
-      E.line("if (p" + qs + ") okacc += okg" + qs + ";");
+      {
+        std::string sum = "okg" + qs + "_0";
+        for (int a = 1; a < kAccChains; ++a) sum = "(" + sum + " + okg" + qs + "_" + std::to_string(a) + ")";
+        E.line("if (p" + qs + ") okacc += " + sum + ";");
+      }
       acc_ = "okacc";
+      acc_chains_ = 1;
       store_to_ = nullptr;
       store_pred_.clear();
       row_from_ = nullptr;
