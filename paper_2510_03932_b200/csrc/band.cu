@@ -600,9 +600,12 @@ __global__ void __launch_bounds__(TT) factor_k(const BandSeg* __restrict__ segs,
         }
       }
     }
-    // column k is final: its slot takes column k + B1 from the prefetch ring
+    // column k is final: its slot takes column k + B1 from the prefetch ring.
+    // No barrier before the refill: every thread reads back exactly the ring
+    // entries its own cp.async copied (same j / t mapping as fetch), slot s
+    // was last read before the barrier above (the multipliers), and this
+    // column's updates above write only slots s+1 .. s+b and ps of those.
     cp_wait<KP - 1>();
-    __syncthreads();
     const long long cin = k + B1;
     if (cin < n) {
       const double* src = ring + static_cast<int>(k & KM) * RW;
