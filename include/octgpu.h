@@ -319,6 +319,16 @@ int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s);
 #define OCG_LDL_BAND 0
 #define OCG_LDL_REFERENCE 1
 int ocg_ldl_create_ex(ocg_kkt* k, int order, ocg_ldl** out);
+/* Speculative inertia correction (reference order): factor n candidate
+ * regularizations (delta_w[i], delta_c[i]) concurrently — independent numeric
+ * buffers, one stream each, the same arithmetic as n calls of
+ * ocg_ldl_factor — and return their inertias in inertia[3 i .. 3 i + 2].
+ * Candidate 0's factors are then current; ocg_ldl_select(l, i) makes
+ * candidate i's current for ocg_ldl_solve / ocg_ldl_factors. The band order
+ * takes n = 1 only (its factorization already fills the device). */
+int ocg_ldl_factor_many(ocg_ldl* l, int n, const double* delta_w, const double* delta_c, int64_t* inertia,
+                        ocg_stream s);
+int ocg_ldl_select(ocg_ldl* l, int i);
 int ocg_ldl_order(const ocg_ldl* l);
 /* OCG_LDL_REFERENCE: nnz of L (sparse::SymbolicLdl::lnz); 0 for the band */
 int64_t ocg_ldl_factor_nnz(const ocg_ldl* l);

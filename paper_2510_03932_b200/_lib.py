@@ -30,7 +30,7 @@ EXPORTS = [
     "ocg_kkt_create", "ocg_kkt_destroy", "ocg_kkt_dims", "ocg_kkt_pattern", "ocg_kkt_maps", "ocg_kkt_values",
     "ocg_kkt_assemble", "ocg_kkt_matvec", "ocg_kkt_jt_lambda",
     "ocg_ldl_create", "ocg_ldl_destroy", "ocg_ldl_info", "ocg_ldl_factor", "ocg_ldl_solve",
-    "ocg_ldl_create_ex", "ocg_ldl_order", "ocg_ldl_factor_nnz", "ocg_ldl_factors", "ocg_ldl_ref_symbolic",
+    "ocg_ldl_create_ex", "ocg_ldl_factor_many", "ocg_ldl_select", "ocg_ldl_order", "ocg_ldl_factor_nnz", "ocg_ldl_factors", "ocg_ldl_ref_symbolic",
     "ocg_comm_nccl_unique_id", "ocg_comm_create_nccl", "ocg_comm_create_host", "ocg_comm_destroy",
     "ocg_eval_create_sharded", "ocg_eval_shard", "ocg_eval_scatter_x", "ocg_eval_halo_exchange",
     "ocg_eval_scatter_rows", "ocg_eval_status_all", "ocg_eval_objective_all", "ocg_shard_plan_json",
@@ -149,6 +149,8 @@ def _load() -> C.CDLL:
         "ocg_ldl_factor": (i32, [vp, C.c_double, C.c_double, dp, vp]),
         "ocg_ldl_solve": (i32, [vp, dp, dp, vp]),
         "ocg_ldl_create_ex": (i32, [vp, i32, C.POINTER(vp)]),
+        "ocg_ldl_factor_many": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), vp]),
+        "ocg_ldl_select": (i32, [vp, i32]),
         "ocg_ldl_order": (i32, [vp]),
         "ocg_ldl_factor_nnz": (i64, [vp]),
         "ocg_ldl_factors": (i32, [vp, dp, dp, dp, dp, dp]),

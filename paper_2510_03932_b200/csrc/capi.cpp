@@ -1629,6 +1629,89 @@ int ocg_ldl_factor(ocg_ldl* l, double delta_w, double delta_c, int64_t* inertia,
   OCG_GUARD_END
 }
 
+int ocg_ldl_factor_many(ocg_ldl* l, int n, const double* delta_w, const double* delta_c, int64_t* inertia,
+                        ocg_stream s) {
+  if (!l || n < 1 || !delta_w || !delta_c || !inertia) return fail(OCG_ERR_ARG, "null argument");
+  if (!l->ref) {
+    if (n != 1) return fail(OCG_ERR_ARG, "ocg_ldl_factor_many: the band order takes one candidate");
+    return ocg_ldl_factor(l, delta_w[0], delta_c[0], inertia, s);
+  }
+  OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(l->kkt->ev->device);
+  auto& R = *l->ref;
+  const cudaStream_t s0 = st(s);
+  const ocg::rl::Dev& d0 = R.dev;
+  while (static_cast<int>(R.cand.size()) < n - 1) {
+    auto c = std::make_unique<ocg_ldl::Ref::Cand>();
+    c->W.alloc(static_cast<size_t>(std::max<int64_t>(1, d0.w_len)));
+    c->stash.alloc(static_cast<size_t>(std::max<int64_t>(1, d0.stash_len)));
+    c->D.alloc(static_cast<size_t>(d0.dim));
+    c->Dinv.alloc(static_cast<size_t>(d0.dim));
+    c->Lx.alloc(static_cast<size_t>(std::max<int64_t>(1, d0.lnz)));
+    c->sr.alloc(static_cast<size_t>(std::max<int64_t>(1, R.nnl * 8)));
+    c->inertia.alloc(3);
+    ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "candidate stream");
+    ck(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming), "candidate event");
+    R.cand.push_back(std::move(c));
+  }
+  if (!R.ev0) ck(cudaEventCreateWithFlags(&R.ev0, cudaEventDisableTiming), "event");
+  const double* kval = l->kkt->val.p;
+  ck(cudaEventRecord(R.ev0, s0), "record");
+  for (int i = 1; i < n; ++i) {  // candidates 1.. on their streams, after the caller's work so far
+    auto& c = *R.cand[static_cast<size_t>(i - 1)];
+    ck(cudaStreamWaitEvent(c.st, R.ev0, 0), "wait");
+    ocg::rl::Dev d = d0;
+    d.sr = c.sr.p;
+    ocg::rl::factor(d, kval, delta_w[i], delta_c[i], c.W.p, c.stash.p, c.D.p, c.Dinv.p, c.Lx.p, c.inertia.p, c.st);
+    c.dw = delta_w[i];
+    c.dc = delta_c[i];
+    ck(cudaEventRecord(c.ev, c.st), "record");
+  }
+  ocg::rl::factor(d0, kval, delta_w[0], delta_c[0], R.W.p, R.stash.p, R.D.p, R.Dinv.p, R.Lx.p, R.inertia.p, s0);
+  std::vector<unsigned long long> h(static_cast<size_t>(3 * n));
+  ck(cudaMemcpyAsync(h.data(), R.inertia.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0), "inertia");
+  for (int i = 1; i < n; ++i) {
+    auto& c = *R.cand[static_cast<size_t>(i - 1)];
+    ck(cudaStreamWaitEvent(s0, c.ev, 0), "wait");
+    ck(cudaMemcpyAsync(h.data() + 3 * i, c.inertia.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0),
+       "inertia");
+  }
+  ck(cudaStreamSynchronize(s0), "sync");
+  for (int i = 0; i < 3 * n; ++i) inertia[i] = static_cast<int64_t>(h[static_cast<size_t>(i)]);
+  l->kkt->ev->launches += static_cast<int64_t>(n) * (2 + (R.nleaf > 0) + (R.dev.npa > 0) + (R.nnl > 0));
+  l->delta_w = delta_w[0];
+  l->delta_c = delta_c[0];
+  l->factorizations += n;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
+int ocg_ldl_select(ocg_ldl* l, int i) {
+  if (!l) return fail(OCG_ERR_ARG, "null argument");
+  if (i == 0) return OCG_OK;
+  if (!l->ref || i < 0 || i > static_cast<int>(l->ref->cand.size()))
+    return fail(OCG_ERR_ARG, "ocg_ldl_select: no such candidate");
+  auto& R = *l->ref;
+  auto& c = *R.cand[static_cast<size_t>(i - 1)];
+  auto sw = [](auto& a, auto& b) {
+    std::swap(a.p, b.p);
+    std::swap(a.n, b.n);
+    std::swap(a.cap, b.cap);
+    std::swap(a.owned, b.owned);
+  };
+  sw(R.W, c.W);
+  sw(R.stash, c.stash);
+  sw(R.D, c.D);
+  sw(R.Dinv, c.Dinv);
+  sw(R.Lx, c.Lx);
+  sw(R.sr, c.sr);
+  sw(R.inertia, c.inertia);
+  R.dev.sr = R.sr.p;
+  std::swap(l->delta_w, c.dw);
+  std::swap(l->delta_c, c.dc);
+  return OCG_OK;
+}
+
 int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
   if (!l || !rhs || !x) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN

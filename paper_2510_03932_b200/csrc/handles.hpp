@@ -237,6 +237,24 @@ struct ocg_ldl {
     DBuf<long long> chunk_foff;
     DBuf<unsigned long long> inertia;
     ocg::rl::Dev dev;
+    // speculative candidates (ocg_ldl_factor_many): numeric buffers and a
+    // stream each; candidate 0 is the set above
+    struct Cand {
+      DBuf<double> W, stash, D, Dinv, Lx, sr;
+      DBuf<unsigned long long> inertia;
+      cudaStream_t st = nullptr;
+      cudaEvent_t ev = nullptr;
+      double dw = 0.0, dc = 0.0;
+      ~Cand() {
+        if (ev) cudaEventDestroy(ev);
+        if (st) cudaStreamDestroy(st);
+      }
+    };
+    std::vector<std::unique_ptr<Cand>> cand;
+    cudaEvent_t ev0 = nullptr;
+    ~Ref() {
+      if (ev0) cudaEventDestroy(ev0);
+    }
   };
   std::unique_ptr<Ref> ref;
 };

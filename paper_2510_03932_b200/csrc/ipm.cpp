@@ -165,6 +165,8 @@ class DeviceSolver {
     }
     ldl_ = ldls_[order];
     r_.time_plan_ldl = plan_ldl_s_[order];
+    const char* e = std::getenv("OCG_IPM_SPECULATE");
+    speculate_ = order == OCG_LDL_REFERENCE && !(e && std::atoi(e) == 0);
   }
   double plan_ldl_s_[2] = {0.0, 0.0};
   ocg::ipmdev::Iter P_;
@@ -177,6 +179,9 @@ class DeviceSolver {
   long long n_solves_ = 0, n_refine_ = 0, n_trials_ = 0;
   double t_err_ = 0, t_assemble_ = 0, t_pre_ = 0, t_search_ = 0, t_accept_ = 0;
   double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
+  // speculative inertia correction (reference order only, OCG_IPM_SPECULATE=0 off)
+  bool speculate_ = false;
+  long long r_speculative_ = 0;
   double theta_min_ = 0.0, theta_max_ = kInf;
   std::vector<std::pair<double, double>> filter_;
   ocg_ipm_result r_{};
@@ -622,11 +627,8 @@ bool DeviceSolver::solve_kkt(double wmax, bool& numeric_failure) {
   Clock tf;
   double dw = 0.0, dc = 0.0;
   bool first_bump = true;
-  for (;;) {
-    int64_t in[3];
-    cko(ocg_ldl_factor(ldl_, dw, dc, in, s_), "ldl_factor");
-    ++r_.factorizations;
-    if (in[0] == ntot_ && in[1] == m_ && in[2] == 0) break;
+  // the reference's next regularization after a rejected inertia `in`
+  auto next_delta = [&](const int64_t* in) {
     if (first_bump) {
       dw = delta_last_ > 0.0 ? std::max(1e-20, delta_last_ / o_.reg_shrink)
                              : o_.reg_initial_scale * std::max(1.0, wmax);
@@ -636,6 +638,55 @@ bool DeviceSolver::solve_kkt(double wmax, bool& numeric_failure) {
     } else {
       dw *= o_.reg_grow;
     }
+  };
+  auto accepted = [&](const int64_t* in) { return in[0] == ntot_ && in[1] == m_ && in[2] == 0; };
+  bool done = false;
+  if (speculate_) {
+    // Reference order: the factorization is one sequential chain on one SM,
+    // so the first four attempts of the reference's decision tree run
+    // concurrently — (0, 0); (dw1, 0); then (dw1, dc1) if that one found zero
+    // pivots, else (dw1 grow, 0) — and the walk below takes exactly the
+    // sequential loop's decisions over their inertias; factorizations counts
+    // the attempts the sequential loop would have made.
+    const double dw1 = delta_last_ > 0.0 ? std::max(1e-20, delta_last_ / o_.reg_shrink)
+                                         : o_.reg_initial_scale * std::max(1.0, wmax);
+    const double dc1 = o_.reg_dual_scale * std::pow(mu_, o_.reg_dual_power);
+    const double cdw[4] = {0.0, dw1, dw1, dw1 * o_.reg_grow}, cdc[4] = {0.0, 0.0, dc1, 0.0};
+    int nc = 4;
+    while (nc > 1 && cdw[nc - 1] > o_.reg_max_delta) --nc;
+    int64_t in[4][3];
+    cko(ocg_ldl_factor_many(ldl_, nc, cdw, cdc, &in[0][0], s_), "ldl_factor_many");
+    r_speculative_ += nc;
+    int cur = 0;
+    for (;;) {
+      ++r_.factorizations;
+      if (accepted(in[cur])) {
+        cko(ocg_ldl_select(ldl_, cur), "ldl_select");
+        done = true;
+        break;
+      }
+      next_delta(in[cur]);
+      if (dw > o_.reg_max_delta) {
+        numeric_failure = true;
+        r_.time_factorize += tf.elapsed();
+        return false;
+      }
+      int nxt = -1;
+      for (int i = cur + 1; i < nc; ++i)
+        if (cdw[i] == dw && cdc[i] == dc && (cur > 0 || i == 1) && (cur != 1 || i >= 2)) {
+          nxt = i;
+          break;
+        }
+      if (nxt < 0) break;  // past the speculated attempts: on sequentially from (dw, dc)
+      cur = nxt;
+    }
+  }
+  while (!done) {
+    int64_t in[3];
+    cko(ocg_ldl_factor(ldl_, dw, dc, in, s_), "ldl_factor");
+    ++r_.factorizations;
+    if (accepted(in)) break;
+    next_delta(in);
     if (dw > o_.reg_max_delta) {
       numeric_failure = true;
       r_.time_factorize += tf.elapsed();
@@ -707,6 +758,7 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     r_.time_plan_kkt = pk;
     r_.time_plan_ldl = pl;
     filter_.clear();
+    r_speculative_ = 0;
     delta_last_ = 0.0;
     dw_ = dc_ = 0.0;
     theta_min_ = 0.0;
@@ -735,10 +787,10 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     *res = r_;
     if (std::getenv("OCG_TIMING"))
       std::fprintf(stderr,
-                   "[ipm] %d iterations: total %.3f s, factorize %.3f s (%d), solve %.3f s (%lld solves + %lld "
-                   "refinement rounds), derivatives %.3f s, %lld line-search trials\n",
-                   iter, r_.time_total, r_.time_factorize, r_.factorizations, r_.time_solve, n_solves_, n_refine_,
-                   r_.time_derivatives, n_trials_);
+                   "[ipm] %d iterations: total %.3f s, factorize %.3f s (%d; %lld speculative), solve %.3f s (%lld "
+                   "solves + %lld refinement rounds), derivatives %.3f s, %lld line-search trials\n",
+                   iter, r_.time_total, r_.time_factorize, r_.factorizations, r_speculative_, r_.time_solve, n_solves_,
+                   n_refine_, r_.time_derivatives, n_trials_);
     if (std::getenv("OCG_TIMING"))
       std::fprintf(stderr,
                    "[ipm] phases: kkt error + mu %.3f s, H + assembly + rhs %.3f s, step stats %.3f s, line search "

@@ -527,6 +527,22 @@ class BandLdl:
         check(LIB.ocg_ldl_factor(self._h, float(delta_w), float(delta_c), inertia.ctypes.data, _stream()))
         return tuple(int(v) for v in inertia)
 
+    def factor_many(self, deltas) -> list[tuple[int, int, int]]:
+        """order="reference": factor the candidate regularizations [(delta_w,
+        delta_c), ...] concurrently (ocg_ldl_factor_many); candidate 0 is then
+        current. Returns every candidate's inertia."""
+        n = len(deltas)
+        dw = (C.c_double * n)(*[float(d[0]) for d in deltas])
+        dc = (C.c_double * n)(*[float(d[1]) for d in deltas])
+        inertia = np.zeros(3 * n, dtype=np.int64)
+        check(LIB.ocg_ldl_factor_many(self._h, n, dw, dc, inertia.ctypes.data_as(C.POINTER(C.c_int64)), _stream()),
+              "ocg_ldl_factor_many")
+        return [tuple(int(v) for v in inertia[3 * i:3 * i + 3]) for i in range(n)]
+
+    def select(self, i: int) -> None:
+        """Make candidate i of the last factor_many current."""
+        check(LIB.ocg_ldl_select(self._h, int(i)), "ocg_ldl_select")
+
     def solve(self, rhs) -> torch.Tensor:
         r = self.kkt.ec._dev(rhs)
         x = torch.empty_like(r)

@@ -118,3 +118,25 @@ def test_goddard_2500_reference_trajectory():
     assert got["factorizations"] == ref["factorizations"]
     assert abs(got["objective"] - ref["objective"]) <= 1e-8 * abs(ref["objective"])
     assert abs(got["objective"] - 1.0125663) <= 1e-7  # the published J(2500), 8 digits
+
+
+@pytest.mark.parametrize("name,N", [("goddard", 1000), ("cart_pendulum", 100), ("quadrotor", 60)])
+def test_speculative_candidates_equal_sequential_factorizations(name, N):
+    """ocg_ldl_factor_many: every candidate's inertia, factors and solve are
+    bit-identical to a sequential ocg_ldl_factor with the same deltas (the IPM
+    walks the reference's decision tree over them, ipm.cpp solve_kkt)."""
+    m, ec, k, kr = _setup(name, N)
+    sigma = np.random.default_rng(7).uniform(0.5, 2.0, k.ntot)
+    k.assemble(sigma)
+    cands = [(0.0, 0.0), (1e-4, 0.0), (1e-4, 1e-8), (8e-4, 0.0)]
+    spec = BandLdl(k, order="reference")
+    seq = BandLdl(k, order="reference")
+    rhs = torch.tensor(np.random.default_rng(8).standard_normal(k.dim), device=ec.device)
+    inertias = spec.factor_many(cands)
+    for i, (dw, dc) in enumerate(cands):
+        assert seq.factor(dw, dc) == inertias[i], f"candidate {i}"
+        spec.select(i)
+        a, b = spec.factors(), seq.factors()
+        assert np.array_equal(a["D"], b["D"]) and np.array_equal(a["Lx"], b["Lx"]), f"candidate {i} factors"
+        assert torch.equal(spec.solve(rhs), seq.solve(rhs)), f"candidate {i} solve"
+        spec.select(i)  # swap back: candidate 0's set is current again
