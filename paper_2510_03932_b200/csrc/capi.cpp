@@ -1455,6 +1455,7 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   R->ych.alloc(nnl + 2);
   R->chunk_foff.upload(H.chunk_foff);
   up64(R->fl_all_ptr, H.fl_all_ptr);
+  up32(R->pre_long, H.pre_long);
   ocg::rl::Dev& d = R->dev;
   d.dim = H.dim;
   d.nnz = H.nnz;
@@ -1495,6 +1496,8 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   d.fronts_len = H.fronts_len;
   d.chunk_foff = H.fmax <= 8 ? R->chunk_foff.p : nullptr;
   d.fl_all_ptr = R->fl_all_ptr.p;
+  d.pre_long = R->pre_long.p;
+  d.npre_long = static_cast<int64_t>(H.pre_long.size());
   d.sr = R->sr.p;
   d.ypre = R->ypre.p;
   d.ych = R->ych.p;

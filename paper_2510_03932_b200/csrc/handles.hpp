@@ -234,6 +234,7 @@ struct ocg_ldl {
     DBuf<ocg::rl::ColRec> rec;
     DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs, sr, ypre, ych;
     DBuf<int64_t> fl_all_ptr;
+    DBuf<int32_t> pre_long;
     DBuf<long long> chunk_foff;
     DBuf<unsigned long long> inertia;
     ocg::rl::Dev dev;

@@ -301,6 +301,7 @@ HostPlan build_plan(const Symbolic& S, const int64_t* colp, const int64_t* rowi)
     for (int64_t j = 0; j < nnl; ++j) {
       H.fl_all_ptr[static_cast<size_t>(j) + 1] =
           H.fl_all_ptr[static_cast<size_t>(j)] + static_cast<int64_t>(terms[static_cast<size_t>(j)].size());
+      if (static_cast<int64_t>(terms[static_cast<size_t>(j)].size()) > kPreLong) H.pre_long.push_back(static_cast<int32_t>(j));
       if (terms[static_cast<size_t>(j)].empty()) continue;
       H.fl_j.push_back(static_cast<int32_t>(j));
       for (const auto& [t, c] : terms[static_cast<size_t>(j)]) {

@@ -961,6 +961,7 @@ __global__ void fill_lx_k(Dev P, double* __restrict__ Lx) {
 __global__ void fwd_pre_k(Dev P, const double* __restrict__ Lx, const double* __restrict__ y) {
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P.nnl;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (P.fl_all_ptr[j + 1] - P.fl_all_ptr[j] > kPreLong) continue;  // fwd_pre_long_k
     double s = y[P.nl_pos[j]];
     for (int64_t t = P.fl_all_ptr[j]; t < P.fl_all_ptr[j + 1]; ++t)
       s = __dsub_rn(s, __dmul_rn(Lx[P.fl_lx[t]], y[P.fl_col[t]]));
@@ -994,6 +995,45 @@ __device__ __forceinline__ void issue_vstage(const Dev& P, const double* yv, lon
 
 // forward substitution along the chain: lane a holds v(a) of the current
 // front (v(0): the pivot row); v'(a') = pre + u(inv(a')) by shuffles
+// one block per long chain column: the products L * y (each exact on its
+// own) are staged into shared memory by threads 32.., double-buffered, while
+// thread 0 subtracts the previous stage from the right-hand side in term
+// order — the same sequence of roundings as fwd_pre_k's one thread
+__global__ void __launch_bounds__(256) fwd_pre_long_k(Dev P, const double* __restrict__ Lx, const double* __restrict__ y) {
+  constexpr int kStage = 2048;
+  __shared__ double sb[2][kStage];
+  const int64_t j = P.pre_long[blockIdx.x];
+  const int64_t lo = P.fl_all_ptr[j], n = P.fl_all_ptr[j + 1] - lo;
+  const int tid = threadIdx.x, nl = static_cast<int>(blockDim.x) - 32;
+  auto stage = [&](int64_t k, double* dst) {
+    const int64_t b = k * kStage, e = min(n, b + kStage);
+    for (int64_t t = b + (tid - 32); t < e; t += nl) dst[t - b] = __dmul_rn(Lx[P.fl_lx[lo + t]], y[P.fl_col[lo + t]]);
+  };
+  double s = tid == 0 ? y[P.nl_pos[j]] : 0.0;
+  const int64_t nst = (n + kStage - 1) / kStage;
+  if (tid >= 32 && nst > 0) stage(0, sb[0]);
+  __syncthreads();
+  for (int64_t k = 0; k < nst; ++k) {
+    if (tid >= 32) {
+      if (k + 1 < nst) stage(k + 1, sb[(k + 1) & 1]);
+    } else if (tid == 0) {
+      const double* c = sb[k & 1];
+      const int m = static_cast<int>(min(static_cast<int64_t>(kStage), n - k * kStage));
+      int i = 0;
+      for (; i + 8 <= m; i += 8) {  // eight loads in flight, then the ordered subtractions
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = c[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dsub_rn(s, v[q]);
+      }
+      for (; i < m; ++i) s = __dsub_rn(s, c[i]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) P.ypre[j] = s;
+}
+
 __global__ void __launch_bounds__(32) fwd_chain_stream_k(Dev P, double* __restrict__ Vs) {
   __shared__ __align__(16) VStage stg[kStages];
   __shared__ __align__(8) uint64_t bar[kStages];
@@ -1333,6 +1373,7 @@ void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs
   if (P.nfl && !streamed) fwd_leaf_k<<<grid_for(P.nfl), kThreads, 0, s>>>(P, Lx, y);
   if (streamed) {
     fwd_pre_k<<<grid_for(P.nnl), kThreads, 0, s>>>(P, Lx, y);
+    if (P.npre_long) fwd_pre_long_k<<<static_cast<unsigned>(P.npre_long), 256, 0, s>>>(P, Lx, y);
     fwd_chain_stream_k<<<1, 32, 0, s>>>(P, Vs);
     bwd_chain_stream_k<<<1, 32, 0, s>>>(P, xp);
   } else if (P.nnl && P.fmax <= 8) {

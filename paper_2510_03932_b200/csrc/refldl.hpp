@@ -77,6 +77,8 @@ struct alignas(16) ColRec {
 };
 
 // Host side of the device plan (below), built once per KKT pattern.
+constexpr int64_t kPreLong = 256;
+
 struct HostPlan {
   int64_t dim = 0, nnz = 0, lnz = 0;
   int fmax = 0;
@@ -89,6 +91,7 @@ struct HostPlan {
   std::vector<int32_t> fl_j;
   std::vector<int64_t> fl_ptr, fl_lx, fl_col;
   std::vector<int64_t> fl_all_ptr;  // [nnl+1]: the same terms indexed by every chain column
+  std::vector<int32_t> pre_long;    // chain columns with more than kPreLong leaf terms
   std::vector<int32_t> rel;
   std::vector<int64_t> sc_dst, sc_dpos, sc_ms;
   std::vector<int8_t> primal;
@@ -129,6 +132,10 @@ struct Dev {
   const int64_t* fl_lx = nullptr;    // L entry index
   const int64_t* fl_col = nullptr;   // leaf position
   const int64_t* fl_all_ptr = nullptr;  // [nnl+1] leaf terms of every chain column
+  // chain columns with more than kPreLong leaf terms (a free final time's
+  // row): summed by one block each, in order, instead of one thread
+  const int32_t* pre_long = nullptr;
+  int64_t npre_long = 0;
   // streamed walks (fronts <= 8): per chain column, its L entries and Dinv
   // (8 doubles, written by the factorization), the right-hand side after the
   // leaf terms and the forward result, all in walk order
