@@ -179,6 +179,12 @@ class DeviceSolver {
   long long n_solves_ = 0, n_refine_ = 0, n_trials_ = 0;
   double t_err_ = 0, t_assemble_ = 0, t_pre_ = 0, t_search_ = 0, t_accept_ = 0;
   double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
+  // setup's host arrays, reused across solves of this context
+  struct HostScratch {
+    std::vector<double> lvar, uvar, x0, lcon, ucon, xlo, xhi, lcon_s, ucon_s, lb, ub, x, c, s, zl, zu;
+    std::vector<int64_t> prim, slack, dual, rslot, free_slot, slack_of, dual_row;
+    std::vector<int8_t> hl, hu;
+  } hs_;
   // speculative inertia correction (reference order only, OCG_IPM_SPECULATE=0 off)
   bool speculate_ = false;
   long long r_speculative_ = 0;
@@ -321,10 +327,18 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
   r_.kkt_dim = dim_;
   r_.kkt_nnz = d[5];
   const auto nv = static_cast<size_t>(nvar_), mc = static_cast<size_t>(mcon_);
-  std::vector<double> lvar(nv), uvar(nv), x0(nv), lcon(mc), ucon(mc), xlo(nv), xhi(nv);
+  // host arrays live in hs_ and keep their memory across solves of this
+  // context (cached with the plans): no fresh pages to fault in per solve
+  auto& lvar = hs_.lvar; auto& uvar = hs_.uvar; auto& x0 = hs_.x0; auto& lcon = hs_.lcon; auto& ucon = hs_.ucon;
+  auto& xlo = hs_.xlo; auto& xhi = hs_.xhi;
+  for (auto* v : {&lvar, &uvar, &x0, &xlo, &xhi}) v->resize(nv);
+  lcon.resize(mc);
+  ucon.resize(mc);
   cko(ocg_model_arrays(model_, lvar.data(), uvar.data(), x0.data(), nullptr, nullptr, lcon.data(), ucon.data()),
       "model_arrays");
-  std::vector<int64_t> prim(nv), slack(mc), dual(mc), rslot(mc);
+  auto& prim = hs_.prim; auto& slack = hs_.slack; auto& dual = hs_.dual; auto& rslot = hs_.rslot;
+  prim.resize(nv);
+  for (auto* v : {&slack, &dual, &rslot}) v->resize(mc);
   cko(ocg_kkt_maps(kkt_, prim.data(), slack.data(), dual.data(), rslot.data(), xlo.data(), xhi.data()), "kkt_maps");
   if (inst_[0] || inst_[1] || inst_[2] || inst_[3] || inst_[4]) {
     // another instance of the same structure: its bounds and start point, and
@@ -358,8 +372,10 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
                               (slack[r] < 0 ? " loosens an equality of the model into a range"
                                             : " turns a range row of the model into an equality"));
   }
-  std::vector<int64_t> free_slot(static_cast<size_t>(nfree_)), slack_of(static_cast<size_t>(nslack_)),
-      dual_row(static_cast<size_t>(m_));
+  auto& free_slot = hs_.free_slot; auto& slack_of = hs_.slack_of; auto& dual_row = hs_.dual_row;
+  free_slot.resize(static_cast<size_t>(nfree_));
+  slack_of.resize(static_cast<size_t>(nslack_));
+  dual_row.resize(static_cast<size_t>(m_));
   for (size_t sl = 0; sl < nv; ++sl)
     if (prim[sl] >= 0) free_slot[static_cast<size_t>(prim[sl])] = static_cast<int64_t>(sl);
   for (size_t r = 0; r < mc; ++r) {
@@ -377,14 +393,19 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
 
   lap("scaling");
   // Solver::setup_bounds (solver.cpp:125-170)
-  std::vector<double> lcon_s(mc), ucon_s(mc);
+  auto& lcon_s = hs_.lcon_s; auto& ucon_s = hs_.ucon_s;
+  lcon_s.resize(mc);
+  ucon_s.resize(mc);
   for (size_t r = 0; r < mc; ++r) {
     lcon_s[r] = row_scale[r] * lcon[r];
     ucon_s[r] = row_scale[r] * ucon[r];
   }
   const auto nt = static_cast<size_t>(ntot_);
-  std::vector<double> lb(nt, -kInf), ub(nt, kInf);
-  std::vector<int8_t> hl(nt, 0), hu(nt, 0);
+  auto& lb = hs_.lb; auto& ub = hs_.ub; auto& hl = hs_.hl; auto& hu = hs_.hu;
+  lb.assign(nt, -kInf);
+  ub.assign(nt, kInf);
+  hl.assign(nt, 0);
+  hu.assign(nt, 0);
   for (int64_t i = 0; i < nfree_; ++i) {
     const auto sl = static_cast<size_t>(free_slot[static_cast<size_t>(i)]);
     if (std::isfinite(xlo[sl])) {
@@ -416,7 +437,8 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
     }
 
   // Solver::initialize_iterate (solver.cpp:172-206)
-  std::vector<double> x = x0;
+  auto& x = hs_.x;
+  x = x0;
   for (size_t sl = 0; sl < nv; ++sl)
     if (xlo[sl] == xhi[sl]) x[sl] = xlo[sl];
   auto push_into = [](double v, double l, double u) {
@@ -463,17 +485,20 @@ void DeviceSolver::setup(std::vector<double>& row_scale) {
 
   lap("uploads");
   // slacks from the constraint values at the start point, multipliers
-  std::vector<double> c;
+  auto& c = hs_.c;
   eval_c(x_->p, c_->p);
   c_->download(c, s_);
-  std::vector<double> s(static_cast<size_t>(nslack_));
+  auto& s = hs_.s;
+  s.resize(static_cast<size_t>(nslack_));
   for (int64_t k = 0; k < nslack_; ++k) {
     const auto r = static_cast<size_t>(slack_of[static_cast<size_t>(k)]);
     const auto i = static_cast<size_t>(nfree_ + k);
     s[static_cast<size_t>(k)] = push_into(c[r], lb[i], ub[i]);
   }
   s_v_->upload(s, s_);
-  std::vector<double> zl(nt, 0.0), zu(nt, 0.0);
+  auto& zl = hs_.zl; auto& zu = hs_.zu;
+  zl.assign(nt, 0.0);
+  zu.assign(nt, 0.0);
   for (size_t i = 0; i < nt; ++i) {
     const double v = static_cast<int64_t>(i) < nfree_ ? x[static_cast<size_t>(free_slot[i])]
                                                       : s[i - static_cast<size_t>(nfree_)];
@@ -759,6 +784,8 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     r_.time_plan_ldl = pl;
     filter_.clear();
     r_speculative_ = 0;
+    n_solves_ = n_refine_ = n_trials_ = 0;
+    t_err_ = t_assemble_ = t_pre_ = t_search_ = t_accept_ = 0.0;
     delta_last_ = 0.0;
     dw_ = dc_ = 0.0;
     theta_min_ = 0.0;
