@@ -129,6 +129,7 @@ class DeviceSolver {
     if (kkt_) ocg_kkt_destroy(kkt_);
     if (ev_) ocg_eval_destroy(ev_);
     if (s_) cudaStreamDestroy(s_);
+    if (hpin_) cudaFreeHost(hpin_);
   }
 
   int run(ocg_ipm_result* res, double* x_out);
@@ -179,6 +180,12 @@ class DeviceSolver {
   long long n_solves_ = 0, n_refine_ = 0, n_trials_ = 0;
   double t_err_ = 0, t_assemble_ = 0, t_pre_ = 0, t_search_ = 0, t_accept_ = 0;
   double dw_ = 0.0, dc_ = 0.0;  // regularization of the current factorization
+  // page-locked landing slots of the fused trial evaluation's scalars
+  struct HostPinned {
+    double v[4];
+    int flag_c, flag_f;
+  };
+  HostPinned* hpin_ = nullptr;
   // setup's host arrays, reused across solves of this context
   struct HostScratch {
     std::vector<double> lvar, uvar, x0, lcon, ucon, xlo, xhi, lcon_s, ucon_s, lb, ub, x, c, s, zl, zu;
@@ -300,6 +307,7 @@ void DeviceSolver::alloc_state(size_t nv, size_t mc) {
   dx_.alloc(dm);
   lamfull_.alloc(mc);
   dscal_.alloc(4);
+  if (!hpin_) ckc(cudaMallocHost(reinterpret_cast<void**>(&hpin_), sizeof(HostPinned)), "pinned trial scalars");
   partials_.alloc(2 * 148 * 8);
   out_.alloc(8);
   sc_.partials = partials_.p;
@@ -900,13 +908,26 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     auto build_trial = [&](const double* d, double a) {
       ocg::ipmdev::trial(P_, x_->p, s_v_->p, d, a, xt_->p, st_->p, s_);
     };
+    // one host round trip per trial: c, residual, theta, barrier and f are
+    // launched back to back and their scalars and finiteness flags come back
+    // together; the decisions below are the sequential ones (solver.cpp:444-455)
     auto eval_trial = [&]() {
       ++n_trials_;
-      if (!eval_c(xt_->p, ct_->p)) return false;
+      Clock t;
+      cko(ocg_eval_constraints(ev_, xt_->p, ct_->p, s_), "eval_constraints");
+      cko(ocg_eval_status_async(ev_, &hpin_->flag_c, s_), "status");
       ocg::ipmdev::residual(P_, ct_->p, st_->p, gt_.p, s_);
-      theta_t = theta_of(gt_.p);
-      double f_t = 0.0, bar = 0.0;
-      if (!ocg::ipmdev::barrier(P_, xt_->p, st_->p, bar, sc_, s_) || !eval_f(xt_->p, f_t)) return false;
+      ocg::ipmdev::l1_async(gt_.p, m_, sc_, dscal_.p, s_);
+      ocg::ipmdev::barrier_async(P_, xt_->p, st_->p, sc_, dscal_.p + 1, s_);
+      cko(ocg_eval_objective(ev_, xt_->p, dscal_.p + 3, s_), "eval_objective");
+      cko(ocg_eval_status_async(ev_, &hpin_->flag_f, s_), "status");
+      ckc(cudaMemcpyAsync(hpin_->v, dscal_.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H trial");
+      ckc(cudaStreamSynchronize(s_), "sync");
+      r_.time_derivatives += t.elapsed();
+      if (hpin_->flag_c) return false;
+      theta_t = hpin_->v[0];
+      const double bar = hpin_->v[1], f_t = hpin_->v[3];
+      if (hpin_->v[2] != 0.0 || hpin_->flag_f || !std::isfinite(f_t)) return false;
       phi_t = f_t - mu_ * bar;
       return std::isfinite(phi_t);
     };

@@ -320,6 +320,18 @@ void finish_reduce(Scratch& sc, int nb, const int (&op)[NV], const double (&init
   cudaStreamSynchronize(s);
 }
 
+// the same reduction, its values left on the device (no host round trip)
+template <int NV>
+void finish_reduce_dev(Scratch& sc, int nb, const int (&op)[NV], const double (&init)[NV], double* out_dev,
+                       cudaStream_t s) {
+  Ops<NV> ops;
+  for (int q = 0; q < NV; ++q) {
+    ops.op[q] = op[q];
+    ops.init[q] = init[q];
+  }
+  finalize_k<NV><<<1, 32, 0, s>>>(sc.partials, nb, ops, out_dev);
+}
+
 }  // namespace
 
 void residual(const Iter& P, const double* c, const double* s, double* g, cudaStream_t st) {
@@ -364,6 +376,16 @@ double l1(const double* g, int64_t n, Scratch& sc, cudaStream_t st) {
   double h[1];
   finish_reduce<1>(sc, nb, {0}, {0.0}, h, st);
   return h[0];
+}
+void l1_async(const double* g, int64_t n, Scratch& sc, double* out_dev, cudaStream_t st) {
+  const int nb = blocks_for(n);
+  l1_k<<<nb, kBlock, 0, st>>>(g, n, sc.partials);
+  finish_reduce_dev<1>(sc, nb, {0}, {0.0}, out_dev, st);
+}
+void barrier_async(const Iter& P, const double* x, const double* s, Scratch& sc, double* out2_dev, cudaStream_t st) {
+  const int nb = blocks_for(P.ntot);
+  barrier_k<<<nb, kBlock, 0, st>>>(P, x, s, sc.partials);
+  finish_reduce_dev<2>(sc, nb, {0, 0}, {0.0, 0.0}, out2_dev, st);
 }
 bool barrier(const Iter& P, const double* x, const double* s, double& bar, Scratch& sc, cudaStream_t st) {
   const int nb = blocks_for(P.ntot);

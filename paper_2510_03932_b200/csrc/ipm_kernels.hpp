@@ -52,6 +52,9 @@ void add(double* x, const double* dx, int64_t n, cudaStream_t st);
 // reductions: synchronous, result on the host
 double l1(const double* g, int64_t n, Scratch& sc, cudaStream_t st);
 bool barrier(const Iter& P, const double* x, const double* s, double& bar, Scratch& sc, cudaStream_t st);
+// the same values left on the device: out_dev = sum |g|; out2_dev = (barrier, invalid count)
+void l1_async(const double* g, int64_t n, Scratch& sc, double* out_dev, cudaStream_t st);
+void barrier_async(const Iter& P, const double* x, const double* s, Scratch& sc, double* out2_dev, cudaStream_t st);
 // out5 = sum|z|, sum|lambda|, max|stationarity|, max|g|, max|complementarity - mu|
 void kkt_error_parts(const Iter& P, const double* x, const double* s, const double* zl, const double* zu,
                      const double* lambda, const double* grad, const double* jtlam, const double* g, double mu,
