@@ -325,6 +325,19 @@ def dropin_e2e(src: str, N: int, scheme: str, steps: int, warmup: int) -> dict |
             "h2d": 8 * (2 * rm.nvar + rm.m_con), "d2h": 8 * (rm.m_con + jn + hn)}
 
 
+def dropin_e2e_isolated(name: str, N: int, scheme: str, steps: int, warmup: int) -> dict | None:
+    """dropin_e2e in a fresh process: in the bench process the drop-in's host
+    copy threads competed with the (spinning) thread pools left by the
+    measurements before it — 14.5 ns/node alone, 17.7-24.2 in-process on the
+    same box. The measurement itself is unchanged."""
+    try:
+        r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--dropin-e2e-child",
+                            f"{name}:{N}:{scheme}:{steps}:{warmup}"], capture_output=True, text=True, timeout=600)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as ex:
+        return {"unavailable": f"drop-in child process: {ex}"}
+
+
 def parity_of(name: str, got: dict, ref: tuple) -> dict:
     """max relative error of the device c / jac / hess against the reference
     EvalContext on the same inputs (tests/parity.py rule with the model's floor)."""
@@ -589,7 +602,7 @@ def run_ours(args) -> None:
         if world == 1:
             # the headline e2e goes through the reference's own EvalContext API
             # (the drop-in); the C-ABI number above stays as e2e_c_abi
-            dr = dropin_e2e(src, N, args.scheme, e2e_steps, args.warmup)
+            dr = dropin_e2e_isolated(args.model, N, args.scheme, e2e_steps, args.warmup)
             if dr and "median_s" in dr:
                 out["e2e_c_abi"] = out["e2e"]
                 out["e2e"] = {"value": dr["median_s"] * 1e9 / N, "unit": "ns/node", "h2d_bytes_per_step": dr["h2d"],
@@ -804,6 +817,11 @@ def secondary(dev, stream, flush, sink, peak, with_reference: bool) -> list[dict
 
 
 def main():
+    if len(sys.argv) > 2 and sys.argv[1] == "--dropin-e2e-child":
+        # the drop-in measurement in a process of its own (see dropin_e2e_isolated)
+        src_name, N, scheme, steps, warmup = sys.argv[2].split(":")
+        print(json.dumps(dropin_e2e(load_models().MODELS[src_name], int(N), scheme, int(steps), int(warmup))))
+        return
     args = parse()
     if args.impl == "reference":
         run_reference(args)
