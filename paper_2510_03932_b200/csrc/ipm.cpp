@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <array>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -129,6 +130,7 @@ class DeviceSolver {
     if (kkt_) ocg_kkt_destroy(kkt_);
     if (ev_) ocg_eval_destroy(ev_);
     if (s_) cudaStreamDestroy(s_);
+    drop_graphs();
     if (hpin_) cudaFreeHost(hpin_);
   }
 
@@ -168,6 +170,11 @@ class DeviceSolver {
     r_.time_plan_ldl = plan_ldl_s_[order];
     const char* e = std::getenv("OCG_IPM_SPECULATE");
     speculate_ = order == OCG_LDL_REFERENCE && !(e && std::atoi(e) == 0);
+    const char* g = std::getenv("OCG_IPM_GRAPHS");
+    graphs_ = !(g && std::atoi(g) == 0);
+    // captured graphs hold this solve's scalars (e.g. the objective scale) by
+    // value: every solve captures its own
+    drop_graphs();
   }
   double plan_ldl_s_[2] = {0.0, 0.0};
   ocg::ipmdev::Iter P_;
@@ -183,8 +190,19 @@ class DeviceSolver {
   // page-locked landing slots of the fused trial evaluation's scalars
   struct HostPinned {
     double v[4];
+    double alpha;
     int flag_c, flag_f;
   };
+  // graph-captured line-search trials (OCG_IPM_GRAPHS=0 off), one executable
+  // graph per pointer set of the iterate, trial and direction buffers
+  bool graphs_ = true;
+  using TrialKey = std::array<const void*, 6>;
+  std::map<TrialKey, cudaGraphExec_t> trial_graphs_;
+  void drop_graphs() {
+    for (auto& [k, g] : trial_graphs_)
+      if (g) cudaGraphExecDestroy(g);
+    trial_graphs_.clear();
+  }
   HostPinned* hpin_ = nullptr;
   // setup's host arrays, reused across solves of this context
   struct HostScratch {
@@ -306,7 +324,7 @@ void DeviceSolver::alloc_state(size_t nv, size_t mc) {
   r_v_.alloc(dm);
   dx_.alloc(dm);
   lamfull_.alloc(mc);
-  dscal_.alloc(4);
+  dscal_.alloc(8);
   if (!hpin_) ckc(cudaMallocHost(reinterpret_cast<void**>(&hpin_), sizeof(HostPinned)), "pinned trial scalars");
   partials_.alloc(2 * 148 * 8);
   out_.alloc(8);
@@ -905,15 +923,20 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
     bool accepted = false, armijo_path = false, saw_eval_error = false;
     double theta_t = 0.0, phi_t = 0.0;
     const double* dir = step_.p;
+    // the trial point and its evaluation replay as one CUDA graph per
+    // (iterate, trial buffer, direction) pointer set; the step length goes
+    // in through a page-locked slot the graph copies to the device first
+    const double* trial_dir = step_.p;
+    double trial_alpha = 0.0;
     auto build_trial = [&](const double* d, double a) {
-      ocg::ipmdev::trial(P_, x_->p, s_v_->p, d, a, xt_->p, st_->p, s_);
+      trial_dir = d;
+      trial_alpha = a;
+      if (!graphs_) ocg::ipmdev::trial(P_, x_->p, s_v_->p, d, a, xt_->p, st_->p, s_);
     };
     // one host round trip per trial: c, residual, theta, barrier and f are
     // launched back to back and their scalars and finiteness flags come back
     // together; the decisions below are the sequential ones (solver.cpp:444-455)
-    auto eval_trial = [&]() {
-      ++n_trials_;
-      Clock t;
+    auto enqueue_eval = [&]() {
       cko(ocg_eval_constraints(ev_, xt_->p, ct_->p, s_), "eval_constraints");
       cko(ocg_eval_status_async(ev_, &hpin_->flag_c, s_), "status");
       ocg::ipmdev::residual(P_, ct_->p, st_->p, gt_.p, s_);
@@ -922,6 +945,28 @@ int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
       cko(ocg_eval_objective(ev_, xt_->p, dscal_.p + 3, s_), "eval_objective");
       cko(ocg_eval_status_async(ev_, &hpin_->flag_f, s_), "status");
       ckc(cudaMemcpyAsync(hpin_->v, dscal_.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H trial");
+    };
+    auto eval_trial = [&]() {
+      ++n_trials_;
+      Clock t;
+      if (graphs_) {
+        hpin_->alpha = trial_alpha;
+        const TrialKey key{x_->p, xt_->p, s_v_->p, st_->p, trial_dir, ct_->p};
+        cudaGraphExec_t& ge = trial_graphs_[key];
+        if (!ge) {
+          cudaGraph_t g = nullptr;
+          ckc(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal), "capture");
+          ckc(cudaMemcpyAsync(dscal_.p + 4, &hpin_->alpha, sizeof(double), cudaMemcpyHostToDevice, s_), "alpha");
+          ocg::ipmdev::trial_dev(P_, x_->p, s_v_->p, trial_dir, dscal_.p + 4, xt_->p, st_->p, s_);
+          enqueue_eval();
+          ckc(cudaStreamEndCapture(s_, &g), "end capture");
+          ckc(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+          cudaGraphDestroy(g);
+        }
+        ckc(cudaGraphLaunch(ge, s_), "graph launch");
+      } else {
+        enqueue_eval();
+      }
       ckc(cudaStreamSynchronize(s_), "sync");
       r_.time_derivatives += t.elapsed();
       if (hpin_->flag_c) return false;

@@ -123,6 +123,21 @@ __global__ void trial_scatter_k(Iter P, const double* __restrict__ x, const doub
   }
 }
 
+// the same with the step length read from device memory (graph-captured trials)
+__global__ void trial_scatter_dev_k(Iter P, const double* __restrict__ x, const double* __restrict__ s,
+                                    const double* __restrict__ dir, const double* __restrict__ ap,
+                                    double* __restrict__ xt, double* __restrict__ st) {
+  const double a = *ap;
+  GRID_LOOP(i, P.ntot) {
+    if (i < P.n_free) {
+      const int64_t slot = P.free_slot[i];
+      xt[slot] = x[slot] + a * dir[i];
+    } else {
+      st[i - P.n_free] = s[i - P.n_free] + a * dir[i];
+    }
+  }
+}
+
 // solver.cpp:641-646 expand_lambda (zeros elsewhere)
 __global__ void zero_k(double* __restrict__ v, int64_t n) {
   GRID_LOOP(i, n) v[i] = 0.0;
@@ -349,6 +364,11 @@ void trial(const Iter& P, const double* x, const double* s, const double* dir, d
            cudaStream_t st) {
   cudaMemcpyAsync(xt, x, P.nvar * sizeof(double), cudaMemcpyDeviceToDevice, st);
   if (P.ntot > 0) trial_scatter_k<<<blocks_for(P.ntot), kBlock, 0, st>>>(P, x, s, dir, a, xt, stv);
+}
+void trial_dev(const Iter& P, const double* x, const double* s, const double* dir, const double* a_dev, double* xt,
+               double* stv, cudaStream_t st) {
+  cudaMemcpyAsync(xt, x, P.nvar * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (P.ntot > 0) trial_scatter_dev_k<<<blocks_for(P.ntot), kBlock, 0, st>>>(P, x, s, dir, a_dev, xt, stv);
 }
 void expand_lambda(const Iter& P, const double* lambda, double* full, cudaStream_t st) {
   zero_k<<<blocks_for(P.m_con), kBlock, 0, st>>>(full, P.m_con);

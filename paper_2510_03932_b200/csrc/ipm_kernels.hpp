@@ -41,6 +41,9 @@ void rhs(const Iter& P, const double* x, const double* s, const double* grad, co
          double mu, double* out, cudaStream_t st);
 void trial(const Iter& P, const double* x, const double* s, const double* dir, double a, double* xt, double* stv,
            cudaStream_t st);
+// the same with the step length at a_dev (device), for graph capture
+void trial_dev(const Iter& P, const double* x, const double* s, const double* dir, const double* a_dev, double* xt,
+               double* stv, cudaStream_t st);
 void expand_lambda(const Iter& P, const double* lambda, double* full, cudaStream_t st);
 void axpy(double a, const double* x, const double* y, double* out, int64_t n, cudaStream_t st);
 void rhs_soc(const Iter& P, const double* rhs, const double* gsoc, double* out, cudaStream_t st);
