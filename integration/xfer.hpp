@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstddef>
 #include <cstring>
@@ -26,18 +28,22 @@
 
 namespace octrans_accel {
 
-// fork-join memcpy over T threads (the caller is one of them)
+// fork-join memcpy over T threads (the caller is one of them). A transfer
+// hands the pool one chunk after another every few tens of microseconds, so
+// the workers spin on the generation counter for a while after each chunk
+// (a futex wake-up per chunk cost as much as the chunk's memcpy) and park on
+// the condition variable only when the pool has been idle for kSpin.
 class CopyPool {
  public:
   explicit CopyPool(int threads) {
-    for (int t = 1; t < threads; ++t) workers_.emplace_back([this, t] { run(t); });
     nthreads_ = threads;
+    for (int t = 1; t < threads; ++t) workers_.emplace_back([this, t] { run(t); });
   }
   ~CopyPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
+      stop_.store(true, std::memory_order_relaxed);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto& w : workers_) w.join();
@@ -47,21 +53,26 @@ class CopyPool {
       std::memcpy(dst, src, bytes);
       return;
     }
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    bytes_ = bytes;
+    pending_.store(nthreads_ - 1, std::memory_order_relaxed);
     {
-      std::lock_guard<std::mutex> lk(mu_);
-      dst_ = static_cast<char*>(dst);
-      src_ = static_cast<const char*>(src);
-      bytes_ = bytes;
-      pending_ = nthreads_ - 1;
-      ++gen_;
+      std::lock_guard<std::mutex> lk(mu_);  // orders the publication against a worker about to park
+      gen_.fetch_add(1, std::memory_order_release);
     }
-    cv_.notify_all();
+    if (parked_.load(std::memory_order_acquire) > 0) cv_.notify_all();
     part(0);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [this] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) != 0) pause();
   }
 
  private:
+  static constexpr auto kSpin = std::chrono::microseconds(300);
+  static void pause() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
   void part(int t) {
     const size_t per = (bytes_ / nthreads_ + 63) & ~size_t{63};
     const size_t lo = std::min(bytes_, per * static_cast<size_t>(t)), hi = std::min(bytes_, lo + per);
@@ -70,26 +81,34 @@ class CopyPool {
   void run(int t) {
     size_t seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
-        if (stop_) return;
+      auto t0 = std::chrono::steady_clock::now();
+      int spins = 0;
+      while (gen_.load(std::memory_order_acquire) == seen) {
+        pause();
+        if (++spins == 1024) {
+          spins = 0;
+          if (std::chrono::steady_clock::now() - t0 > kSpin) {
+            std::unique_lock<std::mutex> lk(mu_);
+            parked_.fetch_add(1, std::memory_order_acq_rel);
+            cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+            parked_.fetch_sub(1, std::memory_order_acq_rel);
+            t0 = std::chrono::steady_clock::now();
+          }
+        }
       }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load(std::memory_order_relaxed)) return;
       part(t);
-      {
-        std::lock_guard<std::mutex> lk(mu_);
-        if (--pending_ == 0) done_.notify_one();
-      }
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   std::vector<std::thread> workers_;
   int nthreads_ = 1;
   std::mutex mu_;
-  std::condition_variable cv_, done_;
-  size_t gen_ = 0;
-  int pending_ = 0;
-  bool stop_ = false;
+  std::condition_variable cv_;
+  std::atomic<size_t> gen_{0};
+  std::atomic<int> pending_{0}, parked_{0};
+  std::atomic<bool> stop_{false};
   char* dst_ = nullptr;
   const char* src_ = nullptr;
   size_t bytes_ = 0;
