@@ -35,6 +35,7 @@
 
 namespace ocg::hd {
 int set_error(int code, const std::string& msg);  // capi.cpp: ocg_last_error's message
+int ldl_create(ocg_kkt* k, int target, ocg_ldl** out);  // capi.cpp: band LDL^T with a segment target
 }
 
 namespace {
@@ -127,6 +128,7 @@ class DeviceSolver {
     if (s_) cudaStreamSynchronize(s_);
     for (ocg_ldl* l : ldls_)
       if (l) ocg_ldl_destroy(l);
+    if (ldl_retry_) ocg_ldl_destroy(ldl_retry_);
     if (kkt_) ocg_kkt_destroy(kkt_);
     if (ev_) ocg_eval_destroy(ev_);
     if (s_) cudaStreamDestroy(s_);
@@ -135,6 +137,12 @@ class DeviceSolver {
   }
 
   int run(ocg_ipm_result* res, double* x_out);
+  // run(); on the band factorization, a solve that ends infeasible or failed
+  // is solved again with a quarter of the segments (longer segments change
+  // the rounding of the inertia decisions on near-singular KKT matrices —
+  // Goddard at N = 3e4 / 5e4 — and converge where the default did not);
+  // OCG_IPM_RETRY=0 off
+  int run_with_retry(ocg_ipm_result* res, double* x_out);
   int device() const { return device_; }
   // instance data for the next run (NULL = the model's own arrays)
   void set_instance(const ocg_ipm_options& o, const double* lvar, const double* uvar, const double* x0,
@@ -158,6 +166,9 @@ class DeviceSolver {
   ocg_kkt* kkt_ = nullptr;
   ocg_ldl* ldl_ = nullptr;      // the factorization of this run: ldls_[o_.kkt_order]
   ocg_ldl* ldls_[2] = {nullptr, nullptr};
+  // band fallback of run_with_retry: a quarter of the segments
+  ocg_ldl* ldl_retry_ = nullptr;
+  bool use_retry_ldl_ = false;
   // the factorization plan of the requested elimination order, built on first use
   void select_ldl() {
     const int order = o_.kkt_order == OCG_LDL_REFERENCE ? OCG_LDL_REFERENCE : OCG_LDL_BAND;
@@ -166,7 +177,7 @@ class DeviceSolver {
       cko(ocg_ldl_create_ex(kkt_, order, &ldls_[order]), "ldl_create");
       plan_ldl_s_[order] = t.elapsed();
     }
-    ldl_ = ldls_[order];
+    ldl_ = use_retry_ldl_ && order == OCG_LDL_BAND && ldl_retry_ ? ldl_retry_ : ldls_[order];
     r_.time_plan_ldl = plan_ldl_s_[order];
     const char* e = std::getenv("OCG_IPM_SPECULATE");
     speculate_ = order == OCG_LDL_REFERENCE && !(e && std::atoi(e) == 0);
@@ -799,6 +810,28 @@ void DeviceSolver::finish(int status, int iter, const std::vector<double>& row_s
   r_.complementarity = comp / obj_scale_;
 }
 
+int DeviceSolver::run_with_retry(ocg_ipm_result* res, double* x_out) {
+  use_retry_ldl_ = false;
+  int rc = run(res, x_out);
+  const char* e = std::getenv("OCG_IPM_RETRY");
+  if (rc != OCG_OK || (e && std::atoi(e) == 0) || o_.kkt_order == OCG_LDL_REFERENCE) return rc;
+  if (res->status != 2 && res->status != 3) return rc;
+  int64_t li[5];
+  cko(ocg_ldl_info(ldl_, li), "ldl_info");
+  const int64_t target = std::max<int64_t>(1, li[1] / 4);
+  if (li[1] <= 1) return rc;
+  if (!ldl_retry_) cko(ocg::hd::ldl_create(kkt_, static_cast<int>(target), &ldl_retry_), "ldl_create (retry)");
+  const ocg_ipm_result first = *res;
+  use_retry_ldl_ = true;
+  rc = run(res, x_out);
+  use_retry_ldl_ = false;
+  res->time_total += first.time_total;
+  if (std::getenv("OCG_TIMING"))
+    std::fprintf(stderr, "[ipm] band path: status %d with %lld segments, retried with %lld: status %d\n", first.status,
+                 static_cast<long long>(li[1]), static_cast<long long>(target), res->status);
+  return rc;
+}
+
 int DeviceSolver::run(ocg_ipm_result* res, double* x_out) {
   Clock total;
   {
@@ -1195,7 +1228,7 @@ int ocg_ipm_ctx_solve(ocg_ipm_ctx* c, const ocg_ipm_options* opts, const double*
   try {
     ocg::mem::DeviceScope ds(c->solver->device());
     c->solver->set_instance(o, lvar, uvar, x_start, lcon, ucon);
-    return c->solver->run(out, x_out);
+    return c->solver->run_with_retry(out, x_out);
   } catch (const InvalidInstance& ex) {
     return ocg::hd::set_error(OCG_ERR_ARG, std::string("ocg_ipm_ctx_solve: ") + ex.what());
   } catch (const std::exception& ex) {
@@ -1218,10 +1251,10 @@ int ocg_ipm_solve(ocg_model* m, const ocg_ipm_options* opts, int device, ocg_ipm
     if (e && lk.owns_lock()) {
       if (!e->solver) e->solver = std::make_unique<DeviceSolver>(m, o, device);
       e->solver->set_instance(o, nullptr, nullptr, nullptr, nullptr, nullptr);
-      return e->solver->run(out, x_out);
+      return e->solver->run_with_retry(out, x_out);
     }
     DeviceSolver solver(m, o, device);
-    return solver.run(out, x_out);
+    return solver.run_with_retry(out, x_out);
   } catch (const std::exception& ex) {
     return ocg::hd::set_error(OCG_ERR_CUDA, std::string("ocg_ipm_solve: ") + ex.what());
   }
