@@ -306,8 +306,10 @@ EvalContext::EvalContext(const StructuredNlp& nlp, const backend::Backend& backe
     // r2_dropin_xfer_sweep.txt); OCTRANS_ACCEL_XFER="chunk_doubles,slots,threads"
     size_t chunk = size_t{1} << 18;
     int slots = 6, threads = static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 1u, 8u));
-    if (const char* e = std::getenv("OCTRANS_ACCEL_XFER")) std::sscanf(e, "%zu,%d,%d", &chunk, &slots, &threads);
-    a->xfer = std::make_unique<octrans_accel::Xfer>(a->stream, std::max(1, threads), std::max<size_t>(chunk, 1024), slots);
+    int nt = 0;
+    if (const char* e = std::getenv("OCTRANS_ACCEL_XFER")) std::sscanf(e, "%zu,%d,%d,%d", &chunk, &slots, &threads, &nt);
+    a->xfer =
+        std::make_unique<octrans_accel::Xfer>(a->stream, std::max(1, threads), std::max<size_t>(chunk, 1024), slots, nt);
   }
   a->nvar = static_cast<size_t>(nlp.nvar());
   a->m = static_cast<size_t>(nlp.m_con);

@@ -12,12 +12,16 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstddef>
+#include <cstdint>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -27,6 +31,50 @@
 #include <vector>
 
 namespace octrans_accel {
+
+// Copy whose destination lines are written with non-temporal (streaming)
+// stores: the destination is not read for ownership first and does not
+// displace the staging ring from the last-level cache. Used for the
+// staging -> caller copies of device-to-host transfers, whose destinations
+// (the reference's COO vectors, tens of MB) are not read again by this
+// process before the next evaluation overwrites them.
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) inline void copy_nt_avx2(char* dst, const char* src, size_t bytes) {
+  size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+  if (head > bytes) head = bytes;
+  if (head) std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  bytes -= head;
+  size_t i = 0;
+  for (; i + 128 <= bytes; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+  }
+  if (i < bytes) std::memcpy(dst + i, src + i, bytes - i);
+  _mm_sfence();  // the streamed lines are visible before the caller's completion signal
+}
+inline bool have_avx2() {
+  static const bool yes = __builtin_cpu_supports("avx2");
+  return yes;
+}
+#endif
+inline void copy_bytes(void* dst, const void* src, size_t bytes, bool nt) {
+#if defined(__x86_64__)
+  if (nt && have_avx2()) {
+    copy_nt_avx2(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+    return;
+  }
+#endif
+  (void)nt;
+  std::memcpy(dst, src, bytes);
+}
 
 // fork-join memcpy over T threads (the caller is one of them). A transfer
 // hands the pool one chunk after another every few tens of microseconds, so
@@ -48,11 +96,12 @@ class CopyPool {
     cv_.notify_all();
     for (auto& w : workers_) w.join();
   }
-  void copy(void* dst, const void* src, size_t bytes) {
+  void copy(void* dst, const void* src, size_t bytes, bool nt = false) {
     if (bytes < (size_t{1} << 18) || nthreads_ == 1) {
-      std::memcpy(dst, src, bytes);
+      copy_bytes(dst, src, bytes, nt);
       return;
     }
+    nt_ = nt;
     dst_ = static_cast<char*>(dst);
     src_ = static_cast<const char*>(src);
     bytes_ = bytes;
@@ -76,7 +125,7 @@ class CopyPool {
   void part(int t) {
     const size_t per = (bytes_ / nthreads_ + 63) & ~size_t{63};
     const size_t lo = std::min(bytes_, per * static_cast<size_t>(t)), hi = std::min(bytes_, lo + per);
-    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    if (hi > lo) copy_bytes(dst_ + lo, src_ + lo, hi - lo, nt_);
   }
   void run(int t) {
     size_t seen = 0;
@@ -111,6 +160,7 @@ class CopyPool {
   std::atomic<bool> stop_{false};
   char* dst_ = nullptr;
   const char* src_ = nullptr;
+  bool nt_ = false;
   size_t bytes_ = 0;
 };
 
@@ -119,8 +169,11 @@ class Xfer {
   static constexpr int kMaxSlots = 8;
 
   // chunk: doubles per staging slot; slots <= kMaxSlots
-  Xfer(cudaStream_t s, int threads, size_t chunk, int slots)
-      : kChunk(chunk), kSlots(std::clamp(slots, 2, kMaxSlots)), stream_(s), pool_(threads) {
+  // nt: bit 0 = streaming stores into the caller's memory on device-to-host
+  // transfers, bit 1 = streaming stores into the staging slots on host-to-
+  // device transfers
+  Xfer(cudaStream_t s, int threads, size_t chunk, int slots, int nt = 1)
+      : kChunk(chunk), kSlots(std::clamp(slots, 2, kMaxSlots)), nt_d2h_(nt & 1), nt_h2d_(nt & 2), stream_(s), pool_(threads) {
     for (int i = 0; i < kSlots; ++i) {
       ck(cudaMallocHost(&stage_[i], kChunk * sizeof(double)), "cudaMallocHost");
       ck(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
@@ -142,7 +195,7 @@ class Xfer {
       const size_t len = std::min(kChunk, n - off);
       const int s = next_slot();
       ck(cudaEventSynchronize(ev_[s]), "slot sync");  // the slot's previous DMA is done
-      pool_.copy(stage_[s], src + off, len * sizeof(double));
+      pool_.copy(stage_[s], src + off, len * sizeof(double), nt_h2d_);
       ck(cudaMemcpyAsync(ddst + off, stage_[s], len * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D");
       ck(cudaEventRecord(ev_[s], stream_), "record");
     }
@@ -174,7 +227,7 @@ class Xfer {
     for (size_t i = 0; i < ahead; ++i) issue(i);
     for (size_t i = 0; i < ch.size(); ++i) {
       ck(cudaEventSynchronize(ev_[slot[i]]), "D2H sync");
-      pool_.copy(ch[i].dst, stage_[slot[i]], ch[i].len * sizeof(double));
+      pool_.copy(ch[i].dst, stage_[slot[i]], ch[i].len * sizeof(double), nt_d2h_);
       if (i + kSlots < ch.size()) issue(i + kSlots);
     }
   }
@@ -190,6 +243,7 @@ class Xfer {
   }
   const size_t kChunk;
   const int kSlots;
+  const bool nt_d2h_, nt_h2d_;
   cudaStream_t stream_;
   CopyPool pool_;
   double* stage_[kMaxSlots] = {};

@@ -6,6 +6,7 @@ O=gpurun_out
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/${T}_env.txt
 timeout 1500 python -m pytest tests -m gpu -q -x > $O/${T}_gputests.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.txt 2>&1
 timeout 900 python bench.py > $O/${T}_bench.json 2> $O/${T}_bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/${T}_bench_ref.json 2>> $O/${T}_bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_launches.csv \
