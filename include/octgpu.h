@@ -187,6 +187,22 @@ int ocg_eval_hessian(ocg_eval* e, const double* x, const double* lambda, ocg_str
 /* fused eval_constraints_jacobian + eval_hessian at one x (one forward pass) */
 int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double* c, ocg_stream s);
 int ocg_eval_max_abs_hessian(ocg_eval* e, double* out, ocg_stream s); /* out: device scalar */
+/* The fused J+H evaluation from host buffers to host buffers, pipelined over
+ * `chunks` node ranges of the main grid (boundaries on the 32-node tile grid,
+ * the endpoint instances with the last): x goes up whole, then per chunk its
+ * multiplier rows go up and its kernel runs on `s` while the previous chunk's
+ * c / jac_val / hess_val segments come back on a second stream, so the two
+ * copy directions overlap (host buffers page-locked for that). Reference
+ * counterpart: EvalContext::eval_constraints_jacobian + eval_hessian at one x
+ * with host vectors (proj/src/ipm/eval.cpp:148-173, 225-258). Stream-ordered:
+ * the host outputs are complete when `s` is; *bytes (may be NULL) = bytes
+ * copied in both directions. Not for sharded contexts. Measured on the B200
+ * box: host<->device traffic in both directions together saturates at about
+ * 55 GB/s, so overlapping the directions gains nothing there and each extra
+ * chunk adds per-copy overhead (profiles/r2_host_pipeline_sweep.jsonl):
+ * chunks = 1 (no pipelining) is the fastest setting on that host. */
+int ocg_eval_jac_hess_host(ocg_eval* e, const double* x_host, const double* lambda_host, double* c_host,
+                           double* jac_host, double* hess_host, int chunks, int64_t* bytes, ocg_stream s);
 /* Node-range shards: the objective's 512-instance chunk
  * partials (Backend::par_reduce, backend.cpp:119-133) of this context's
  * instances — device array of ocg_eval_objective_chunks() doubles, chunks of

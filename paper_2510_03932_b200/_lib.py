@@ -23,7 +23,7 @@ EXPORTS = [
     "ocg_eval_default_options", "ocg_eval_create", "ocg_eval_destroy", "ocg_eval_sizes", "ocg_eval_structure",
     "ocg_eval_buffer", "ocg_eval_bind_buffer", "ocg_eval_set_scaling", "ocg_eval_get_scaling", "ocg_eval_compute_scaling",
     "ocg_eval_constraints", "ocg_eval_constraints_jacobian", "ocg_eval_objective", "ocg_eval_gradient",
-    "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_max_abs_hessian", "ocg_eval_status", "ocg_eval_status_async",
+    "ocg_eval_hessian", "ocg_eval_jac_hess", "ocg_eval_jac_hess_host", "ocg_eval_max_abs_hessian", "ocg_eval_status", "ocg_eval_status_async",
     "ocg_eval_objective_chunks", "ocg_eval_objective_partials", "ocg_eval_objective_combine",
     "ocg_eval_launch_count",
     "ocg_debug_generated_source", "ocg_debug_generated_source_ex", "ocg_debug_compile", "ocg_debug_compile_log",
@@ -115,6 +115,7 @@ def _load() -> C.CDLL:
         "ocg_eval_gradient": (i32, [vp, dp, dp, vp]),
         "ocg_eval_hessian": (i32, [vp, dp, dp, vp]),
         "ocg_eval_jac_hess": (i32, [vp, dp, dp, dp, vp]),
+        "ocg_eval_jac_hess_host": (i32, [vp, dp, dp, dp, dp, dp, i32, ip, vp]),
         "ocg_eval_max_abs_hessian": (i32, [vp, dp, vp]),
         "ocg_eval_status": (i32, [vp, vp]),
         "ocg_eval_status_async": (i32, [vp, dp, vp]),

@@ -878,6 +878,140 @@ int ocg_eval_jac_hess(ocg_eval* e, const double* x, const double* lambda, double
   OCG_GUARD_END
 }
 
+namespace {
+
+// One COO / c segment a node range writes: (buffer 0 = c, 1 = jac, 2 = hess,
+// offset, count). Groups are laid out group-major, instance-major inside a
+// group (eval.cpp:44-119), so a range's outputs are one segment per group
+// and output kind; tail groups (endpoint pairs, boundary kind) go with the
+// chunk that runs the specials.
+struct OutSeg {
+  int buf;
+  Index off, n;
+};
+
+std::vector<OutSeg> range_segments(const ocg::Nlp& nlp, const ocg::Layout& L, Index a, Index b, bool specials) {
+  std::vector<OutSeg> v;
+  auto span = [&](const ocg::Group& g, Index& k0, Index& k1) {
+    const bool tail = g.range.endpoints || g.kind == ocg::Group::Kind::boundary;
+    if (tail) {
+      k0 = 0;
+      k1 = specials ? g.range.count() : 0;
+    } else {
+      k0 = std::max<Index>(0, std::max(g.range.lo, a) - g.range.lo);
+      k1 = std::max<Index>(0, std::min(g.range.hi, b) - g.range.lo);
+    }
+  };
+  for (size_t gi = 0; gi < nlp.cons.size(); ++gi) {
+    const ocg::Group& g = nlp.cons[gi];
+    Index k0 = 0, k1 = 0;
+    span(g, k0, k1);
+    if (k1 <= k0) continue;
+    const Index od = g.out_dim(), nj = static_cast<Index>(g.pattern.jac.size()),
+                nh = static_cast<Index>(g.pattern.hess.size());
+    v.push_back({0, g.row_base + k0 * od, (k1 - k0) * od});
+    if (nj) v.push_back({1, L.jac_off[gi] + k0 * nj, (k1 - k0) * nj});
+    if (nh) v.push_back({2, L.hess_off_con[gi] + k0 * nh, (k1 - k0) * nh});
+  }
+  for (size_t gi = 0; gi < nlp.objs.size(); ++gi) {
+    const ocg::Group& g = nlp.objs[gi];
+    Index k0 = 0, k1 = 0;
+    span(g, k0, k1);
+    const Index nh = static_cast<Index>(g.pattern.hess.size());
+    if (k1 > k0 && nh) v.push_back({2, L.hess_off_obj[gi] + k0 * nh, (k1 - k0) * nh});
+  }
+  // adjacent segments of one buffer merged (fewer, larger copies)
+  std::sort(v.begin(), v.end(), [](const OutSeg& p, const OutSeg& q) { return p.buf != q.buf ? p.buf < q.buf : p.off < q.off; });
+  std::vector<OutSeg> m;
+  for (const OutSeg& sg : v) {
+    if (!m.empty() && m.back().buf == sg.buf && m.back().off + m.back().n == sg.off)
+      m.back().n += sg.n;
+    else
+      m.push_back(sg);
+  }
+  return m;
+}
+
+}  // namespace
+
+int ocg_eval_jac_hess_host(ocg_eval* e, const double* x, const double* lambda, double* c, double* jac, double* hess,
+                           int chunks, int64_t* bytes, ocg_stream s) {
+  if (!e || !x || !lambda || !c || !jac || !hess) return fail(OCG_ERR_ARG, "null argument");
+  if (e->shard) return fail(OCG_ERR_ARG, "ocg_eval_jac_hess_host: a sharded context uploads its shard (ocg_eval_scatter_x)");
+  OCG_GUARD_BEGIN
+  ocg::mem::DeviceScope ds_(e->device);
+  const ocg::Nlp& nlp = e->model->nlp;
+  const size_t nv = static_cast<size_t>(nlp.nvar), mc = static_cast<size_t>(nlp.m_con);
+  if (!e->host_x.p) {
+    e->host_x.alloc(nv);
+    e->host_lam.alloc(std::max<size_t>(mc, 1));
+    e->host_c.alloc(std::max<size_t>(mc, 1));
+    ck(cudaStreamCreateWithFlags(&e->out_stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming), "event");
+  }
+  const cudaStream_t cs = st(s);
+  // chunk boundaries on the 32-node tile grid; the specials with the last
+  // chunk (every x node is on the device by then)
+  const Index lo = e->i0, hi = e->i0 + e->n_main;
+  const Index nch = std::max<Index>(1, std::min<Index>(chunks > 0 ? chunks : 1, (hi - lo + 31) / 32));
+  while (static_cast<Index>(e->chunk_ev.size()) < nch) {
+    cudaEvent_t ev = nullptr;
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    e->chunk_ev.push_back(ev);
+  }
+  double* const dx = e->host_x.p;
+  double* const dl = e->host_lam.p;
+  double* const dc = e->host_c.p;
+  int64_t moved = 0;
+  // x whole first: a chunk's kernels read its right halo and the free
+  // variables (tf), and x is the smallest array
+  ck(cudaMemcpyAsync(dx, x, nv * sizeof(double), cudaMemcpyHostToDevice, cs), "x h2d");
+  moved += static_cast<int64_t>(nv * sizeof(double));
+  const double* rs = e->row_scale.p;
+  const double* ow = e->objw.p;
+  double* dj = e->jac.p;
+  double* dh = e->hess.p;
+  int* fl = e->flag.p;
+  double* const hbuf[3] = {c, jac, hess};
+  const double* const dbuf[3] = {dc, dj, dh};
+  for (Index q = 0; q < nch; ++q) {
+    // [a, b): boundaries on the tile grid
+    const Index a = q == 0 ? lo : std::min(hi, lo + ((hi - lo) * q / nch + 31) / 32 * 32);
+    const Index b = q + 1 == nch ? hi : std::min(hi, lo + ((hi - lo) * (q + 1) / nch + 31) / 32 * 32);
+    const bool last = q + 1 == nch;
+    const std::vector<OutSeg> segs = range_segments(nlp, e->lay, a, b, last && e->specials);
+    // this chunk's multiplier rows are exactly its c rows
+    for (const OutSeg& sg : segs)
+      if (sg.buf == 0) {
+        ck(cudaMemcpyAsync(dl + sg.off, lambda + sg.off, static_cast<size_t>(sg.n) * sizeof(double),
+                            cudaMemcpyHostToDevice, cs),
+            "lambda h2d");
+        moved += sg.n * static_cast<int64_t>(sizeof(double));
+      }
+    Index i0 = a, nm = b - a;
+    Index ns = last ? e->n_spec("ocg_cjh") : 0;
+    const double* xin = dx;
+    const double* lin = dl;
+    double* cout = dc;
+    void* args[] = {e->prm_arg(), &xin, &lin, &rs, &ow, &cout, &dj, &dh, &fl, &i0, &nm, &ns, &kNoBatch};
+    e->launch_range(e->k_cjh, "ocg_cjh", args, cs, nm, ns);
+    ck(cudaEventRecord(e->chunk_ev[static_cast<size_t>(q)], cs), "record");
+    ck(cudaStreamWaitEvent(e->out_stream, e->chunk_ev[static_cast<size_t>(q)], 0), "wait");
+    for (const OutSeg& sg : segs) {
+      ck(cudaMemcpyAsync(hbuf[sg.buf] + sg.off, dbuf[sg.buf] + sg.off, static_cast<size_t>(sg.n) * sizeof(double),
+                          cudaMemcpyDeviceToHost, e->out_stream),
+          "d2h");
+      moved += sg.n * static_cast<int64_t>(sizeof(double));
+    }
+  }
+  // the caller's stream is done when the last copy out is
+  ck(cudaEventRecord(e->join_ev, e->out_stream), "record");
+  ck(cudaStreamWaitEvent(cs, e->join_ev, 0), "wait");
+  if (bytes) *bytes = moved;
+  return OCG_OK;
+  OCG_GUARD_END
+}
+
 int ocg_eval_objective(ocg_eval* e, const double* x, double* f, ocg_stream s) {
   if (!e || !x || !f) return fail(OCG_ERR_ARG, "null argument");
   OCG_GUARD_BEGIN

@@ -154,6 +154,18 @@ struct ocg_eval {
   int64_t launches = 0;
   std::map<std::string, int> min_blocks;  // register budget the kernels were compiled for
 
+  // ocg_eval_jac_hess_host: device x / lambda / c, and the stream and events
+  // that carry each node-range chunk's outputs back while the next computes
+  DBuf<double> host_x, host_lam, host_c;
+  cudaStream_t out_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t join_ev = nullptr;
+  ~ocg_eval() {
+    for (cudaEvent_t ev : chunk_ev) cudaEventDestroy(ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (out_stream) cudaStreamDestroy(out_stream);
+  }
+
   // tail instances this shard runs for kernel `name`
   Index n_spec(const char* name) const { return specials ? tail.at(name) : 0; }
 
@@ -169,6 +181,19 @@ struct ocg_eval {
     ocg::hd::ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid, 1, nz), dim3(static_cast<unsigned>(block)), args,
                         static_cast<size_t>(smem.at(name)), s),
        "launch generated kernel");
+    ++launches;
+  }
+
+  // one node range [i0, i0 + nm) of the main grid (+ ns tail instances):
+  // the same persistent grid rule over the range's tiles
+  void launch_range(cudaKernel_t k, const char* name, void** args, cudaStream_t s, Index nm, Index ns) {
+    const Index tiles = (nm + block - 1) / block;
+    if (tiles <= 0 && ns <= 0) return;
+    const Index cap = static_cast<Index>(sm_count) * std::max(1, resident.at(name));
+    const unsigned grid = static_cast<unsigned>(std::max<Index>(1, std::min(tiles, cap)));
+    ocg::hd::ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid, 1, 1), dim3(static_cast<unsigned>(block)), args,
+                                 static_cast<size_t>(smem.at(name)), s),
+                "launch generated kernel");
     ++launches;
   }
 

@@ -349,6 +349,19 @@ class EvalContext:
     def launch_jac_hess(self, x: torch.Tensor, lam: torch.Tensor, c: torch.Tensor, stream=None) -> None:
         check(LIB.ocg_eval_jac_hess(self._h, _ptr(x), _ptr(lam), _ptr(c), _stream(stream)))
 
+    def launch_jac_hess_host(self, x_host: torch.Tensor, lam_host: torch.Tensor, c_host: torch.Tensor,
+                             jac_host: torch.Tensor, hess_host: torch.Tensor, chunks: int = 1, stream=None) -> int:
+        """ocg_eval_jac_hess_host: host (page-locked) buffers in and out,
+        pipelined over `chunks` node ranges; returns the bytes copied. The
+        host outputs are complete once `stream` is."""
+        for t in (x_host, lam_host, c_host, jac_host, hess_host):
+            assert t.device.type == "cpu" and t.dtype == torch.float64 and t.is_contiguous()
+        assert jac_host.numel() >= self.jac_nnz and hess_host.numel() >= self.hess_nnz
+        nb = C.c_int64(0)
+        check(LIB.ocg_eval_jac_hess_host(self._h, _ptr(x_host), _ptr(lam_host), _ptr(c_host), _ptr(jac_host),
+                                         _ptr(hess_host), int(chunks), C.byref(nb), _stream(stream)))
+        return int(nb.value)
+
     def launch_constraints(self, x: torch.Tensor, c: torch.Tensor, stream=None) -> None:
         check(LIB.ocg_eval_constraints(self._h, _ptr(x), _ptr(c), _stream(stream)))
 
