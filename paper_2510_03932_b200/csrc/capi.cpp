@@ -1637,6 +1637,19 @@ std::unique_ptr<ocg_ldl::Ref> make_ref_ldl(ocg_kkt* k) {
   d.ych = R->ych.p;
   d.stash_len = H.stash_len;
   d.v_len = H.v_len;
+  {
+    const std::vector<int32_t> col = ocg::rl::seq_chunks(R->S.Lp);
+    if (!col.empty()) {
+      std::vector<int32_t> lp(R->S.Lp.begin(), R->S.Lp.end()), li(R->S.Li.begin(), R->S.Li.end());
+      up32(R->Lp32, lp);
+      up32(R->Li32, li);
+      up32(R->sq_col, col);
+      d.Lp32 = R->Lp32.p;
+      d.Li32 = R->Li32.p;
+      d.sq_col = R->sq_col.p;
+      d.sq_nchunks = static_cast<int64_t>(col.size()) - 1;
+    }
+  }
   return R;
 }
 
@@ -1856,7 +1869,7 @@ int ocg_ldl_solve(ocg_ldl* l, const double* rhs, double* x, ocg_stream s) {
   if (l->ref) {
     auto& R = *l->ref;
     ocg::rl::solve(R.dev, R.Dinv.p, R.Lx.p, rhs, x, R.y.p, R.xp.p, R.V.p, R.Vs.p, st(s));
-    l->kkt->ev->launches += 2 + (R.dev.nfl > 0) + (R.nnl > 0 ? 3 : 0) + (R.nleaf > 0);
+    l->kkt->ev->launches += ocg::rl::seq_solve_enabled(R.dev) ? 1 : 2 + (R.dev.nfl > 0) + (R.nnl > 0 ? 3 : 0) + (R.nleaf > 0);
     return OCG_OK;
   }
   const ocg::BandPlan& P = l->plan;

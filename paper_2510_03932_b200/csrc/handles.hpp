@@ -260,6 +260,7 @@ struct ocg_ldl {
     DBuf<double> W, stash, D, Dinv, Lx, y, xp, V, Vs, sr, ypre, ych;
     DBuf<int64_t> fl_all_ptr;
     DBuf<int32_t> pre_long;
+    DBuf<int32_t> Lp32, Li32, sq_col;  // sequential solve (refldl.hpp seq_chunks)
     DBuf<long long> chunk_foff;
     DBuf<unsigned long long> inertia;
     ocg::rl::Dev dev;

@@ -1320,6 +1320,121 @@ __global__ void bwd_leaf_k(Dev P, const double* __restrict__ Lx, const double* _
   }
 }
 
+// Sequential solve, ldl.cpp:222-247 operation for operation: one block, the
+// permuted right-hand side resident in shared memory; L's columns come in
+// chunks (kSeqCols columns, kSeqEnt entries) that warps 1.. stage into a
+// double buffer while thread 0 runs the previous chunk's columns:
+//   forward, columns ascending: y[Li[p]] -= Lx[p] * y[k] (skipped when y[k]
+//   is 0), each column's rows loaded together and stored together (the rows
+//   of one column are distinct);
+//   y[k] *= Dinv[k];
+//   backward, columns descending: s = y[k]; s -= Lx[p] * y[Li[p]] in entry
+//   order; y[k] = s.
+// The same roundings in the same order as the reference, given L and D.
+// The chain columns' L entries live in P.sr after a streamed factorization;
+// they are written into Lx first (fill_lx_k's mapping).
+struct SeqBuf {
+  double* x;
+  int32_t* i;
+  int32_t* p;
+};
+
+__device__ __forceinline__ SeqBuf seq_buf(double* base, int64_t dim, int b) {
+  double* x0 = base + ((dim + 1) & ~int64_t{1});
+  char* q = reinterpret_cast<char*>(x0 + 2 * kSeqEnt);
+  SeqBuf r;
+  r.x = x0 + b * kSeqEnt;
+  r.i = reinterpret_cast<int32_t*>(q) + b * kSeqEnt;
+  r.p = reinterpret_cast<int32_t*>(q) + 2 * kSeqEnt + b * (kSeqCols + 1);
+  return r;
+}
+
+__device__ __forceinline__ void seq_stage(const Dev& P, const double* Lx, int64_t c, SeqBuf B, int t0, int nt) {
+  const int k0 = P.sq_col[c], k1 = P.sq_col[c + 1];
+  const int e0 = P.Lp32[k0], ne = P.Lp32[k1] - e0;
+  for (int t = t0; t <= k1 - k0; t += nt) B.p[t] = P.Lp32[k0 + t] - e0;
+  for (int t = t0; t < ne; t += nt) {
+    B.i[t] = P.Li32[e0 + t];
+    B.x[t] = __ldcg(Lx + e0 + t);
+  }
+}
+
+__global__ void __launch_bounds__(256) seq_solve_k(Dev P, const double* __restrict__ Dinv, double* Lx, bool fill,
+                                                   const double* __restrict__ rhs, double* __restrict__ x) {
+  extern __shared__ __align__(16) double ys[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t n = P.dim, nc = P.sq_nchunks;
+  if (fill)
+    for (int64_t j = tid; j < P.nnl; j += nt) {
+      const int f = P.nl_f[j];
+      const int64_t lp = P.nl_lp[j];
+      for (int a = 1; a < f; ++a) Lx[lp + a - 1] = P.sr[j * 8 + a - 1];
+    }
+  for (int64_t k = tid; k < n; k += nt) ys[k] = rhs[P.perm[k]];
+  __syncthreads();
+  // L y = P b
+  seq_stage(P, Lx, 0, seq_buf(ys, n, 0), tid, nt);
+  __syncthreads();
+  for (int64_t c = 0; c < nc; ++c) {
+    const SeqBuf B = seq_buf(ys, n, static_cast<int>(c & 1));
+    if (tid >= 32 && c + 1 < nc) seq_stage(P, Lx, c + 1, seq_buf(ys, n, static_cast<int>((c + 1) & 1)), tid - 32, nt - 32);
+    if (tid == 0) {
+      const int k0 = P.sq_col[c], nk = P.sq_col[c + 1] - k0;
+      for (int kk = 0; kk < nk; ++kk) {
+        const double yk = ys[k0 + kk];
+        if (yk == 0.0) continue;
+        const int pe = B.p[kk + 1];
+        for (int p = B.p[kk]; p < pe; p += 8) {
+          int r[8];
+          double l[8], v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < pe) {
+              r[u] = B.i[p + u];
+              l[u] = B.x[p + u];
+              v[u] = ys[r[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < pe) ys[r[u]] = __dsub_rn(v[u], __dmul_rn(l[u], yk));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t k = tid; k < n; k += nt) ys[k] = __dmul_rn(ys[k], Dinv[k]);
+  // L^T x = y, last chunk first
+  seq_stage(P, Lx, nc - 1, seq_buf(ys, n, 0), tid, nt);
+  __syncthreads();
+  for (int64_t q = 0; q < nc; ++q) {
+    const int64_t c = nc - 1 - q;
+    const SeqBuf B = seq_buf(ys, n, static_cast<int>(q & 1));
+    if (tid >= 32 && c > 0) seq_stage(P, Lx, c - 1, seq_buf(ys, n, static_cast<int>((q + 1) & 1)), tid - 32, nt - 32);
+    if (tid == 0) {
+      const int k0 = P.sq_col[c], nk = P.sq_col[c + 1] - k0;
+      for (int kk = nk - 1; kk >= 0; --kk) {
+        double s = ys[k0 + kk];
+        const int pe = B.p[kk + 1];
+        for (int p = B.p[kk]; p < pe; p += 8) {
+          double l[8], v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < pe) {
+              l[u] = B.x[p + u];
+              v[u] = ys[B.i[p + u]];
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < pe) s = __dsub_rn(s, __dmul_rn(l[u], v[u]));
+        }
+        ys[k0 + kk] = s;
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t k = tid; k < n; k += nt) x[P.perm[k]] = ys[k];
+}
+
 // ring depth: up to 16 slots, within 160 KB of dynamic shared memory
 int ring_slots(int slotd) {
   const int by_smem = static_cast<int>((160 * 1024) / (static_cast<size_t>(slotd) * sizeof(double)));
@@ -1364,9 +1479,53 @@ void fill_lx(const Dev& P, double* Lx, cudaStream_t s) {
   if (streamed_factor(P)) fill_lx_k<<<grid_for(P.nnl), kThreads, 0, s>>>(P, Lx);
 }
 
+std::vector<int32_t> seq_chunks(const std::vector<int64_t>& Lp) {
+  const int64_t n = static_cast<int64_t>(Lp.size()) - 1;
+  std::vector<int32_t> col{0};
+  if (n <= 0 || seq_smem_bytes(n) > kSeqSmemMax || Lp[static_cast<size_t>(n)] >= (int64_t{1} << 31)) return {};
+  int64_t k0 = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t cnt = Lp[static_cast<size_t>(k) + 1] - Lp[static_cast<size_t>(k)];
+    if (cnt > kSeqEnt) return {};
+    if (k - k0 + 1 > kSeqCols || Lp[static_cast<size_t>(k) + 1] - Lp[static_cast<size_t>(k0)] > kSeqEnt) {
+      col.push_back(static_cast<int32_t>(k));
+      k0 = k;
+    }
+  }
+  col.push_back(static_cast<int32_t>(n));
+  return col;
+}
+
+size_t seq_smem_bytes(int64_t dim) {
+  return static_cast<size_t>((dim + 1) & ~int64_t{1}) * sizeof(double) +
+         2 * (kSeqEnt * (sizeof(double) + sizeof(int32_t)) + (kSeqCols + 1) * sizeof(int32_t));
+}
+
+// Opt-in (OCG_REFLDL_SOLVE=1, read per call): bit-exact with ldl.cpp's solve
+// given L and D, but one thread's walk is latency-bound on its shared-memory
+// round trips: Goddard N=1000 (dim 7001) 2.59 ms per solve against 1.19 ms
+// for the warp-chain walks, Goddard@1000 parity solve time_solve 4.05 vs
+// 1.89 s with the same 510 iterations (profiles/r2_seq_solve_ab.txt).
+bool seq_solve_enabled(const Dev& P) {
+  const char* e = std::getenv("OCG_REFLDL_SOLVE");
+  return e && std::atoi(e) == 1 && P.sq_nchunks > 0;
+}
+
 void solve(const Dev& P, const double* Dinv, const double* Lx, const double* rhs, double* x, double* y, double* xp,
            double* V, double* Vs, cudaStream_t s) {
   (void)V;
+  if (seq_solve_enabled(P)) {
+    const size_t smem = seq_smem_bytes(P.dim);
+    static bool attr = false;
+    if (!attr) {
+      ck(cudaFuncSetAttribute(seq_solve_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSeqSmemMax)),
+         "smem attr");
+      attr = true;
+    }
+    seq_solve_k<<<1, 256, smem, s>>>(P, Dinv, const_cast<double*>(Lx), streamed_factor(P), rhs, x);
+    ck(cudaGetLastError(), "seq solve launch");
+    return;
+  }
   gather_k<<<grid_for(P.dim), kThreads, 0, s>>>(P.perm, rhs, y, P.dim);
   static const int variant = std::getenv("OCG_REFLDL_KERNEL") ? std::atoi(std::getenv("OCG_REFLDL_KERNEL")) : 0;
   const bool streamed = P.nnl && P.fmax <= 8 && variant == 0 && P.chunk_foff;

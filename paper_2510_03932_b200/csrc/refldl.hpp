@@ -155,7 +155,25 @@ struct Dev {
   const int64_t* perm = nullptr;     // position -> KKT index
   const int8_t* primal = nullptr;    // position: 1 = +delta_w, 0 = -delta_c
   int64_t w_len = 0, stash_len = 0, v_len = 0;
+  // sequential solve (seq_solve_k): L's pattern as 32-bit Lp / Li and the
+  // column chunks the block stages through shared memory (sq_col[c] = first
+  // column of chunk c, sq_nchunks + 1 entries); sq_nchunks = 0: not planned
+  const int32_t* Lp32 = nullptr;
+  const int32_t* Li32 = nullptr;
+  const int32_t* sq_col = nullptr;
+  int64_t sq_nchunks = 0;
 };
+
+// Column chunks of at most kSeqCols columns and kSeqEnt entries of L for the
+// sequential solve; empty when some column alone holds more than kSeqEnt
+// entries or the solution vector does not fit shared memory beside the two
+// staging buffers (the warp-chain solves are used then).
+constexpr int kSeqCols = 256, kSeqEnt = 1536;
+constexpr size_t kSeqSmemMax = 227 * 1024;
+std::vector<int32_t> seq_chunks(const std::vector<int64_t>& Lp);
+size_t seq_smem_bytes(int64_t dim);
+// the sequential solve runs (planned, and OCG_REFLDL_SOLVE unset or 1)
+bool seq_solve_enabled(const Dev& P);
 
 // numeric factorization: W (w_len) and stash (stash_len) scratch; D, Dinv by
 // position; Lx in the layout of Lp/Li; inertia (device, 3 counts) =

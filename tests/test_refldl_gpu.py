@@ -140,3 +140,50 @@ def test_speculative_candidates_equal_sequential_factorizations(name, N):
         assert np.array_equal(a["D"], b["D"]) and np.array_equal(a["Lx"], b["Lx"]), f"candidate {i} factors"
         assert torch.equal(spec.solve(rhs), seq.solve(rhs)), f"candidate {i} solve"
         spec.select(i)  # swap back: candidate 0's set is current again
+
+
+def _solve_restated(f, b):
+    """proj/src/sparse/ldl.cpp:222-247 (sparse::solve) in plain Python floats:
+    the permuted right-hand side, L y = P b by columns (skipping y[k] == 0),
+    y *= Dinv, L^T x = y with each column's terms subtracted in entry order."""
+    perm, Lp, Li, Lx = f["perm"], f["Lp"], f["Li"], f["Lx"]
+    dinv = [0.0 if d == 0.0 else 1.0 / d for d in f["D"].tolist()]
+    n = len(perm)
+    y = [float(b[perm[k]]) for k in range(n)]
+    Lpl, Lil, Lxl = Lp.tolist(), Li.tolist(), Lx.tolist()
+    for k in range(n):
+        yk = y[k]
+        if yk == 0.0:
+            continue
+        for p in range(Lpl[k], Lpl[k + 1]):
+            y[Lil[p]] -= Lxl[p] * yk
+    for k in range(n):
+        y[k] *= dinv[k]
+    for k in range(n - 1, -1, -1):
+        s = y[k]
+        for p in range(Lpl[k], Lpl[k + 1]):
+            s -= Lxl[p] * y[Lil[p]]
+        y[k] = s
+    x = np.empty(n)
+    x[perm] = y
+    return x
+
+
+@pytest.mark.parametrize("name,N", [("double_integrator", 300), ("goddard", 400), ("quadrotor", 60),
+                                    ("cart_pendulum", 100), ("hang_glider", 80), ("shuttle", 50)])
+def test_sequential_solve_bit_exact(name, N, monkeypatch):
+    """seq_solve_k (opt-in OCG_REFLDL_SOLVE=1: one block, the permuted right-
+    hand side in shared memory) performs ldl.cpp:222-247's roundings in its
+    order: given the device's own factors, its solution equals the plain
+    restatement bit for bit."""
+    monkeypatch.setenv("OCG_REFLDL_SOLVE", "1")
+    m, ec, k, kr = _setup(name, N)
+    k.assemble(np.random.default_rng(5).uniform(0.5, 2.0, k.ntot))
+    ldl = BandLdl(k, order="reference")
+    inertia = ldl.factor(1e-4, 1e-8)
+    assert inertia[2] == 0
+    b = np.random.default_rng(9).standard_normal(k.dim)
+    b[::7] = 0.0  # zero right-hand-side rows take the reference's skip
+    x = ldl.solve(b).cpu().numpy()
+    want = _solve_restated(ldl.factors(), b)
+    assert np.array_equal(x, want), f"{name}: max abs diff {np.max(np.abs(x - want)):.3e}"
