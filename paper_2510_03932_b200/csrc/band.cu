@@ -1037,18 +1037,26 @@ __global__ void schur_global_k(const BandSeg* __restrict__ segs, int nseg, int w
 
 __global__ void inertia_sum_k(const long long* __restrict__ parts, int nblocks, long long* __restrict__ out,
                               BandBatch bb) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // integer counts: one warp, lane-strided sums and a shuffle tree (exact in
+  // any order)
+  if (blockIdx.x != 0) return;
   if (bb.ids) {
     const long long bi = bb.ids[blockIdx.y];
     parts += bi * bb.sparts;
     out += bi * 3;
   }
   long long a = 0, c = 0, z = 0;
-  for (int i = 0; i < nblocks; ++i) {
+  for (int i = threadIdx.x; i < nblocks; i += 32) {
     a += parts[3 * i];
     c += parts[3 * i + 1];
     z += parts[3 * i + 2];
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    z += __shfl_xor_sync(0xffffffffu, z, o);
+  }
+  if (threadIdx.x != 0) return;
   out[0] = a;
   out[1] = c;
   out[2] = z;

@@ -49,12 +49,36 @@ __global__ void __launch_bounds__(256) chunk_sums(const double* __restrict__ obj
 __global__ void combine_chunks(const double* __restrict__ partials, const int64_t* __restrict__ cbase,
                                const double* __restrict__ weights, int n_groups, double obj_scale,
                                double* __restrict__ f, int* __restrict__ flag) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double total = 0.0;
-  for (int g = 0; g < n_groups; ++g) {
-    double part = 0.0;
-    for (int64_t c = cbase[g]; c < cbase[g + 1]; ++c) part += partials[c];
+  // one warp: the lanes stage the chunk partials into shared memory a tile
+  // at a time, lane 0 adds them in chunk order and closes each group in
+  // group order (the same roundings as one thread reading global memory,
+  // without a global-load round trip per chunk)
+  if (blockIdx.x != 0) return;
+  constexpr int kTile = 1024;
+  __shared__ double buf[kTile];
+  const int lane = threadIdx.x;
+  double total = 0.0, part = 0.0;
+  int g = 0;
+  const int64_t c0 = n_groups > 0 ? cbase[0] : 0, c1 = n_groups > 0 ? cbase[n_groups] : 0;
+  for (int64_t t0 = c0; t0 < c1; t0 += kTile) {
+    const int n = static_cast<int>(c1 - t0 < kTile ? c1 - t0 : kTile);
+    for (int i = lane; i < n; i += 32) buf[i] = partials[t0 + i];
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < n; ++i) {
+        while (t0 + i >= cbase[g + 1]) {  // groups ending before this chunk, empty ones included
+          total += weights[g] * part;
+          part = 0.0;
+          ++g;
+        }
+        part += buf[i];
+      }
+    __syncwarp();
+  }
+  if (lane != 0) return;
+  for (; g < n_groups; ++g) {
     total += weights[g] * part;
+    part = 0.0;
   }
   const double fs = obj_scale * total;
   *f = fs;
