@@ -57,15 +57,25 @@ __global__ void __launch_bounds__(kBlock) finalize_k(const double* __restrict__ 
   __shared__ double sp[kMaxBlocks * NV];
   for (int i = threadIdx.x; i < nblocks * NV; i += blockDim.x) sp[i] = partials[i];
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  for (int q = 0; q < NV; ++q) {
-    double a = ops.init[q];
-    for (int b = 0; b < nblocks; ++b) {
-      const double v = sp[b * NV + q];
-      a = ops.op[q] == 0 ? a + v : (ops.op[q] == 1 ? fmax(a, v) : fmin(a, v));
-    }
-    out[q] = a;
+  // thread q combines slot q (slots are independent), eight partials loaded
+  // ahead of their in-order combine
+  const int q = threadIdx.x;
+  if (q >= NV) return;
+  const int op = ops.op[q];
+  double a = ops.init[q];
+  int b = 0;
+  for (; b + 8 <= nblocks; b += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = sp[(b + u) * NV + q];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a = op == 0 ? a + v[u] : (op == 1 ? fmax(a, v[u]) : fmin(a, v[u]));
   }
+  for (; b < nblocks; ++b) {
+    const double v = sp[b * NV + q];
+    a = op == 0 ? a + v : (op == 1 ? fmax(a, v) : fmin(a, v));
+  }
+  out[q] = a;
 }
 
 int blocks_for(int64_t n) {
