@@ -1138,10 +1138,15 @@ __global__ void __launch_bounds__(32) bwd_chain_stream_k(Dev P, double* __restri
         const bool row = lane >= 1 && lane < m.f;
         const int ra = row ? static_cast<int>((m.rel8 >> (8 * (lane - 1))) & 0xff) : 0;
         const double xa = __shfl_sync(0xffffffffu, Xp, ra);
-        double t = row ? __dmul_rn(stg[st].sr[jj * 8 + lane - 1], xa) : 0.0;
+        // every lane gathers the front's X values by broadcast shuffles and
+        // subtracts the terms in entry order: ldl.cpp:240-243's roundings
+        double xs[7];
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-        const double s = __dsub_rn(__dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]), t);
+        for (int a = 1; a < 8; ++a) xs[a - 1] = __shfl_sync(0xffffffffu, Xp, static_cast<int>((m.rel8 >> (8 * (a - 1))) & 0xff));
+        double s = __dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]);
+#pragma unroll
+        for (int a = 1; a < 8; ++a)
+          if (a < m.f) s = __dsub_rn(s, __dmul_rn(stg[st].sr[jj * 8 + a - 1], xs[a - 1]));
         Xp = lane == 0 ? s : xa;
         if (lane == 0) xp[m.pos] = s;
       }
@@ -1153,10 +1158,14 @@ __global__ void __launch_bounds__(32) bwd_chain_stream_k(Dev P, double* __restri
       const int ra = lane >= 1 && lane < f ? static_cast<int>((m.rel8 >> (8 * (lane - 1))) & 0xff) : 0;
       double xa = __shfl_sync(0xffffffffu, Xp, ra);
       if (m.soff != kChain && lane >= 1 && lane < f) xa = xp[P.Li[m.lp + lane - 1]];  // parent not the previous column
-      double t = lane >= 1 && lane < f ? __dmul_rn(stg[st].sr[jj * 8 + lane - 1], xa) : 0.0;
+      // X of row a on every lane (lane a's value broadcast), the terms
+      // subtracted in entry order (ldl.cpp:240-243)
+      double s = __dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]);
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-      const double s = __dsub_rn(__dmul_rn(stg[st].y[jj], stg[st].sr[jj * 8 + 7]), t);
+      for (int a = 1; a < 8; ++a) {
+        const double x_a = __shfl_sync(0xffffffffu, xa, a);
+        if (a < f) s = __dsub_rn(s, __dmul_rn(stg[st].sr[jj * 8 + a - 1], x_a));
+      }
       Xp = lane == 0 ? s : xa;
       if (lane == 0) xp[m.pos] = s;
       __syncwarp();
