@@ -338,6 +338,20 @@ def dropin_e2e_isolated(name: str, N: int, scheme: str, steps: int, warmup: int)
         return {"unavailable": f"drop-in child process: {ex}"}
 
 
+def batch_solve_isolated(spec: str, with_reference: bool) -> dict:
+    """batch_solve_leg in a fresh process: the batched solver's host thread
+    issues ~1800 launch groups per batch, and in the bench process it competed
+    with the spinning thread pools the reference measurements leave behind
+    (whole-batch walls 1.1-2.2 s against a steady 0.86 s alone on the same
+    box, device time unchanged). The measurement itself is unchanged."""
+    try:
+        r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--batch-child",
+                            f"{spec}:{int(with_reference)}"], capture_output=True, text=True, timeout=1200)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as ex:
+        return {"unavailable": f"batch child process: {ex}"}
+
+
 def parity_of(name: str, got: dict, ref: tuple) -> dict:
     """max relative error of the device c / jac / hess against the reference
     EvalContext on the same inputs (tests/parity.py rule with the model's floor)."""
@@ -454,6 +468,13 @@ def run_ours(args) -> None:
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 
+    # the batched-solve leg first, in a child process, before this process has
+    # started any reference thread pools (they keep spinning afterwards and
+    # the batch's host launch loop competed with them even from a child:
+    # whole-batch walls 1.1-2.5 s against a steady 0.86 s otherwise)
+    batch_early = None
+    if args.batch != "none" and world == 1:
+        batch_early = batch_solve_isolated(args.batch, not args.no_cpu_baseline)
     src = MODELS[args.model]
     N = args.N * world
     m = Model(src, N, args.scheme)
@@ -639,7 +660,7 @@ def run_ours(args) -> None:
             out["goddard_parity_solve"] = ipm_solve_leg(f"goddard:{args.goddard_parity}", not args.no_cpu_baseline,
                                                         order="reference", reps=1)
         if args.batch != "none" and world == 1:
-            out["batch_solve"] = batch_solve_leg(args.batch, not args.no_cpu_baseline)
+            out["batch_solve"] = batch_early
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -735,10 +756,11 @@ def batch_solve_leg(spec: str, with_reference: bool, ref_sample: int = 64) -> di
     lcon = np.ascontiguousarray(np.stack([r["lcon"] for r in arrs]))
     ucon = np.ascontiguousarray(np.stack([r["ucon"] for r in arrs]))
     solve_batch(base, insts[:2])  # kernels into the compile cache
-    # three whole-batch solves, the median wall reported (single walls vary
-    # 0.8-2.0 s on a fresh box with the device time unchanged)
+    # five whole-batch solves, the median wall reported (single walls vary
+    # 0.85-2.5 s on some boxes with the solver's own time_total unchanged at
+    # 0.82-0.84 s: host-side noise outside the solve, profiles/r2_batch_wall.txt)
     walls = []
-    for _ in range(3):
+    for _ in range(5):
         t0 = time.perf_counter()
         res = solve_batch(base, lcon=lcon, ucon=ucon)
         walls.append(time.perf_counter() - t0)
@@ -821,6 +843,11 @@ def main():
         # the drop-in measurement in a process of its own (see dropin_e2e_isolated)
         src_name, N, scheme, steps, warmup = sys.argv[2].split(":")
         print(json.dumps(dropin_e2e(load_models().MODELS[src_name], int(N), scheme, int(steps), int(warmup))))
+        return
+    if len(sys.argv) > 2 and sys.argv[1] == "--batch-child":
+        # the batched-solve leg in a process of its own (see batch_solve_isolated)
+        B, N, ref = sys.argv[2].split(":")
+        print(json.dumps(batch_solve_leg(f"{B}:{N}", ref == "1")))
         return
     args = parse()
     if args.impl == "reference":

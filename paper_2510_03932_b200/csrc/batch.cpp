@@ -1120,8 +1120,21 @@ extern "C" int ocg_ipm_batch_solve(ocg_model* m, const ocg_ipm_options* opts, in
   if (opts) o = *opts;
   try {
     ocg::mem::DeviceScope ds(device);
-    Batch b(m, o, device, nb);
-    b.run(lvar, uvar, x_start, lcon, ucon, out, x_out);
+    const bool timing = std::getenv("OCG_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::chrono::steady_clock::time_point t1, t2;
+    {
+      Batch b(m, o, device, nb);
+      t1 = std::chrono::steady_clock::now();
+      b.run(lvar, uvar, x_start, lcon, ucon, out, x_out);
+      t2 = std::chrono::steady_clock::now();
+    }
+    if (timing) {
+      const auto t3 = std::chrono::steady_clock::now();
+      auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+      std::fprintf(stderr, "[ocg_ipm_batch_solve] plans %.3f s, run %.3f s, release %.3f s\n", sec(t0, t1), sec(t1, t2),
+                   sec(t2, t3));
+    }
     return OCG_OK;
   } catch (const InvalidInstance& ex) {
     return ocg::hd::set_error(OCG_ERR_ARG, std::string("ocg_ipm_batch_solve: ") + ex.what());
