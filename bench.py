@@ -48,7 +48,10 @@ def parse():
     ap.add_argument("--model", default="goddard")
     ap.add_argument("--N", type=int, default=100_000, help="time nodes per GPU")
     ap.add_argument("--scheme", default="trapezoid")
-    ap.add_argument("--block", type=int, default=128)
+    # one-warp blocks: 16.5-16.6 us per Goddard N=1e5 step against 17.2-17.3
+    # with four-warp blocks, alternated on one box (profiles/r2_block_ab.jsonl);
+    # both are parity-tested at every bench config (test_eval_bench_configs.py)
+    ap.add_argument("--block", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lib-shard", action="store_true",
                     help="use the library's sharded context (NCCL communicator) even on one rank")

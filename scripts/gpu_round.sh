@@ -10,8 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.t
 timeout 900 python bench.py > $O/${T}_bench.json 2> $O/${T}_bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/${T}_bench_ref.json 2>> $O/${T}_bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_launches.csv \
-  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --solve none --goddard-solve none --batch none > /dev/null 2>> $O/${T}_ncu.err
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --solve none --goddard-solve none --goddard-parity none --batch none > /dev/null 2>> $O/${T}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ocg_cjh -s 1 -c 1 -o $O/${T}_prof_goddard -f \
-  python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary --solve none --goddard-solve none --batch none > /dev/null 2>> $O/${T}_ncu.err
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary --solve none --goddard-solve none --goddard-parity none --batch none > /dev/null 2>> $O/${T}_ncu.err
 timeout 900 bash scripts/ipm_vec_ncu.sh $O/${T}_ipm_vec_ncu.csv
 echo done
