@@ -184,6 +184,7 @@ class EvalContext:
             raise RuntimeError("octgpu EvalContext needs a CUDA device (no CPU fallback)")
         self.model = model
         self.device = torch.device("cuda", device)
+        self.block = block
         torch.cuda.set_device(self.device)
         opts = _lib.EvalOptions(device, int(fma), block, idx_lo, idx_hi, int(specials), int(min_blocks),
                                 int(split_kinds), int(input_staging))
