@@ -83,7 +83,11 @@ int blocks_for(int64_t n) {
   return static_cast<int>(want < 1 ? 1 : (want > kMaxBlocks ? kMaxBlocks : want));
 }
 
+// unrolled by four so that the loads of later elements are issued before the
+// earlier ones are consumed (each thread's elements stay in the same order:
+// the reductions' roundings are unchanged)
 #define GRID_LOOP(i, n)                                                                  \
+  _Pragma("unroll 4")                                                                    \
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
