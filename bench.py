@@ -806,15 +806,16 @@ def ec_block(ec) -> int:
 
 def secondary(dev, stream, flush, sink, peak, with_reference: bool) -> list[dict]:
     """The other eval-only configs (BASELINE.json configs[2..3]) at N=1 GPU:
-    quadrotor N=1e6 (north_star's >= 60% of HBM roofline at N >= 1e6),
+    Goddard and quadrotor N=1e6 (north_star's >= 60% of HBM roofline at
+    N >= 1e6),
     quadrotor N=1e5, hang glider and shuttle N=1e5; each timed like the
     headline and checked against the reference EvalContext (max_rel_err)."""
     import torch
 
     from paper_2510_03932_b200 import MODELS, EvalContext, Model
     res = []
-    for name, N in (("quadrotor", 1_000_000), ("quadrotor", 100_000), ("hang_glider", 100_000),
-                    ("shuttle", 100_000)):
+    for name, N in (("goddard", 1_000_000), ("quadrotor", 1_000_000), ("quadrotor", 100_000),
+                    ("hang_glider", 100_000), ("shuttle", 100_000)):
         m = Model(MODELS[name], N)
         st = m.structure()
         ec = EvalContext(m, device=dev.index)
