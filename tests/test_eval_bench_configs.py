@@ -25,7 +25,7 @@ from paper_2510_03932_b200 import MODELS, EvalContext, Model
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 CONFIGS = [("goddard", 100_000), ("hang_glider", 100_000), ("shuttle", 100_000), ("quadrotor", 100_000),
-           ("quadrotor", 1_000_000)]
+           ("quadrotor", 1_000_000), ("goddard", 1_000_000)]
 
 
 def _check_all(name, m, ec, re, x, lam):
