@@ -814,11 +814,17 @@ def secondary(dev, stream, flush, sink, peak, with_reference: bool) -> list[dict
 
     from paper_2510_03932_b200 import MODELS, EvalContext, Model
     res = []
+    # launch block per model: the faster of one- and four-warp blocks,
+    # alternated twice on one box (profiles/r2_sec_block_ab.jsonl): one-warp
+    # blocks for Goddard N=1e6 (96.4 vs 101.3 us), hang glider (36.9 vs 38.8)
+    # and shuttle (65.4 vs 67.6); four-warp blocks for the quadrotor (35.9 vs
+    # 36.8 us at N=1e5, 283.6 vs 304.8 at N=1e6)
+    block_of = {"quadrotor": 128}
     for name, N in (("goddard", 1_000_000), ("quadrotor", 1_000_000), ("quadrotor", 100_000),
                     ("hang_glider", 100_000), ("shuttle", 100_000)):
         m = Model(MODELS[name], N)
         st = m.structure()
-        ec = EvalContext(m, device=dev.index)
+        ec = EvalContext(m, device=dev.index, block=block_of.get(name, 32))
         x, lam = m.synth_acceptance(20250808)
         xd, ld = torch.as_tensor(x, device=dev), torch.as_tensor(lam, device=dev)
         c = torch.zeros(m.m_con, dtype=torch.float64, device=dev)
@@ -828,7 +834,7 @@ def secondary(dev, stream, flush, sink, peak, with_reference: bool) -> list[dict
         nb = algorithmic_bytes(st, *main_space(st), True)
         row = {"model": name, "N": N, "ok": ok and ec.status(stream), "ns_per_node": t * 1e9 / N,
                "us_per_step": t * 1e6, "gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak, "bytes_per_node": nb / N,
-               "steps": 20, "warmup": 3, "gpu_launches": launches}
+               "steps": 20, "warmup": 3, "gpu_launches": launches, "block": ec.block}
         if with_reference:
             got = {"c": c.cpu().numpy(), "jac": ec.jac_val.cpu().numpy(), "hess": ec.hess_val.cpu().numpy()}
             del ec
